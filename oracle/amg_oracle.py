@@ -1,0 +1,739 @@
+"""CPU oracle for the AMG-PCG hot path — TEST INFRASTRUCTURE ONLY.
+
+This module restates, in numpy/scipy, the reference algorithm of
+arXiv 2602.23613's ``hcurl_amg`` package for the path named by
+BASELINE.json's north star: ``build_hierarchy`` ("alg" and "ref" routes),
+``vcycle``, ``pcg``, ``amg_solve`` and ``operator_complexity``.  It is the
+checker the GPU product is compared against; only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline / reference arm
+may import it.  The product path (``paper_2602_23613_b200``) never calls it.
+
+The floating-point parts use the very same scipy/numpy/LAPACK primitives as
+the reference (the reference's arithmetic lives in scipy 1.18.1 sparsetools,
+scipy.sparse.csgraph and numpy 2.3.5 / scipy-openblas 0.3.30), so on the same
+inputs this restatement is bit-identical to the reference; the combinatorial
+parts (strong adjacency, greedy C/F, matching) are reorganised (vectorised
+masks, a lazy max-heap instead of an O(N) argmax per pick) but keep the
+reference's exact tie-break semantics.  Pinning: ``tests/test_oracle_golden.py``
+checks every function against fixtures produced by the reference itself
+(``tests/golden/make_golden.py``, run in the build container where
+``/root/reference`` is importable).
+
+Citations are ``file:line`` in ``/root/reference/pkg/src/hcurl_amg``.
+Known deliberate divergence: the reference factors components / coarsest
+matrices above 4096 DoFs with a pure-Python up-looking sparse Cholesky
+(sparse.py:212-273); this oracle always uses the dense LAPACK path (the same
+factorization, different roundoff) — the survey's "raised cutoff" run.
+"""
+
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.linalg
+import scipy.sparse as sp
+from scipy.sparse.csgraph import connected_components, reverse_cuthill_mckee
+
+PIVOT_RTOL = 1e-13                  # sparse.py:30
+INV_SQRT2 = 1.0 / np.sqrt(2.0)      # splitting.py:47 (0x3FE6A09E667F3BCC)
+
+
+class NotPositiveDefiniteError(RuntimeError):
+    """Cholesky breakdown with the failing pivot (sparse.py:50-55)."""
+
+    def __init__(self, pivot, message=None):
+        self.pivot = int(pivot)
+        super().__init__(message or f"matrix is not positive definite (pivot {pivot})")
+
+
+# ----------------------------------------------------------------------------- sparse core
+
+def canon(a, shape=None):
+    """Canonical CSR: sorted, duplicates summed, exact zeros dropped (sparse.py:58-65)."""
+    m = sp.csr_matrix(a, shape=shape, dtype=np.float64)
+    m.sum_duplicates()
+    m.sort_indices()
+    m.eliminate_zeros()
+    return m
+
+
+def max_abs(M):
+    return float(np.abs(M.data).max()) if M.nnz else 0.0
+
+
+def symmetric_part(M):
+    """canon(0.5 (M + M^T)) — used by nodal_dual and galerkin (splitting.py:133, sparse.py:122)."""
+    return canon(0.5 * (M + M.T))
+
+
+def galerkin(P, A):
+    """P^T A P symmetrised (sparse.py:113-122)."""
+    if A.shape[0] != A.shape[1] or A.shape[0] != P.shape[0]:
+        raise ValueError(f"dimension mismatch: P {P.shape}, A {A.shape}")
+    return symmetric_part(P.T @ (A @ P))
+
+
+def _pivot_loop(Ad, floor):
+    """Column Cholesky naming the first failing pivot (sparse.py:172-185)."""
+    n = Ad.shape[0]
+    L = np.zeros_like(Ad)
+    for j in range(n):
+        d = Ad[j, j] - L[j, :j] @ L[j, :j]
+        if not np.isfinite(d) or d <= floor:
+            raise NotPositiveDefiniteError(j)
+        L[j, j] = np.sqrt(d)
+        if j + 1 < n:
+            L[j + 1:, j] = (Ad[j + 1:, j] - L[j + 1:, :j] @ L[j, :j]) / L[j, j]
+    return L
+
+
+def dense_chol(Ad):
+    """LAPACK lower Cholesky + relative pivot floor (sparse.py:188-209)."""
+    if Ad.shape[0] == 0:
+        return np.zeros((0, 0))
+    dg = np.diag(Ad)
+    scale = float(np.abs(dg).max()) if len(dg) else 0.0
+    try:
+        L = np.linalg.cholesky(Ad)
+    except np.linalg.LinAlgError:
+        _pivot_loop(Ad, PIVOT_RTOL * scale)
+        raise
+    piv = np.diag(L) ** 2
+    if piv.min() <= PIVOT_RTOL * scale:
+        raise NotPositiveDefiniteError(int(np.argmin(piv)),
+                                       f"pivot {piv.min():.3e} below the breakdown floor "
+                                       "(near-singular block)")
+    return L
+
+
+@dataclass
+class Factor:
+    """Permuted dense Cholesky of the coarsest operator (sparse.py:146-165, 276-301)."""
+
+    perm: np.ndarray
+    L: np.ndarray
+
+    @property
+    def n(self):
+        return self.L.shape[0]
+
+
+def factor_coarsest(A):
+    if A.shape[0] != A.shape[1]:
+        raise ValueError("matrix must be square")
+    asym, scale = max_abs(canon(A - A.T)), max_abs(A)
+    if scale > 0 and asym > 1e-12 * scale:
+        raise ValueError(f"matrix not symmetric: asymmetry {asym:.3e}")
+    n = A.shape[0]
+    if n == 0:
+        return Factor(np.zeros(0, dtype=np.int64), np.zeros((0, 0)))
+    perm = np.asarray(reverse_cuthill_mckee(A, symmetric_mode=True), dtype=np.int64)
+    L = dense_chol(A[perm][:, perm].tocsr().toarray())
+    # the reference stores csr(L) and densifies it again: same values
+    return Factor(perm, canon(L).toarray())
+
+
+def solve_coarsest(f, b):
+    """sparse.py:304-321 (dense path)."""
+    b = np.asarray(b, dtype=np.float64)
+    if b.shape[0] != f.n:
+        raise ValueError(f"dimension mismatch: factor {f.n}, rhs {b.shape}")
+    if f.n == 0:
+        return b.copy()
+    y = scipy.linalg.solve_triangular(f.L, b[f.perm], lower=True)
+    xp = scipy.linalg.solve_triangular(f.L.T, y, lower=False)
+    x = np.empty_like(xp)
+    x[f.perm] = xp
+    return x
+
+
+# ----------------------------------------------------------------------------- splitting
+
+@dataclass(frozen=True)
+class Pair:
+    """ExteriorPair (splitting.py:50-57)."""
+
+    dof1: int
+    dof2: int
+    sign1: int
+    sign2: int
+    tail: int
+    mid: int
+    head: int
+
+
+@dataclass
+class Split:
+    """Splitting (splitting.py:60-85)."""
+
+    pairs: list
+    interior_dofs: np.ndarray
+    n: int
+    dof_edges: np.ndarray = None
+    pair_mesh_edges: np.ndarray = None
+    coarse_nodes: np.ndarray = None
+
+    @property
+    def n_pairs(self):
+        return len(self.pairs)
+
+
+def augment(G):
+    """augment_gradient (splitting.py:100-125) -> (Gtilde, boundary column ids)."""
+    G = canon(G)
+    per_row = np.diff(G.indptr)
+    if np.any(per_row > 2):
+        raise ValueError(f"row {int(np.argmax(per_row > 2))} has more than 2 nonzeros")
+    if G.nnz and np.any(np.abs(G.data) != 1.0):
+        raise ValueError("gradient entries must be +-1")
+    lone = np.flatnonzero(per_row == 1)
+    m = G.shape[1]
+    if lone.size == 0:
+        return G, np.zeros(0, dtype=np.int64)
+    extra = canon((-G.data[G.indptr[lone]], (lone, np.arange(lone.size))),
+                  shape=(G.shape[0], lone.size))
+    return canon(sp.hstack([G, extra])), (m + np.arange(lone.size)).astype(np.int64)
+
+
+def nodal_dual(A, Gt):
+    """G~^T (A G~), symmetrised (splitting.py:128-133)."""
+    if A.shape[1] != Gt.shape[0]:
+        raise ValueError(f"dimension mismatch: A {A.shape}, Gtilde {Gt.shape}")
+    return symmetric_part(Gt.T @ (A @ Gt))
+
+
+def _rows_of(M):
+    return np.repeat(np.arange(M.shape[0]), np.diff(M.indptr))
+
+
+def strong_lists(An, theta):
+    """Strong mask per stored entry (splitting.py:136-155), vectorised.
+
+    Entry (i, j), j != i, is strong iff |a_ij| >= theta * max_{k != i} |a_ik|.
+    Returns (strong CSR pattern, its transpose = strong_to lists).
+    """
+    rows = _rows_of(An)
+    off = An.indices != rows
+    mag = np.where(off, np.abs(An.data), -np.inf)
+    rmax = np.full(An.shape[0], -np.inf)
+    np.maximum.at(rmax, rows, mag)
+    mask = off & (np.abs(An.data) >= theta * rmax[rows])
+    S = sp.csr_matrix((np.ones(int(mask.sum())), (rows[mask], An.indices[mask])),
+                      shape=An.shape)
+    S.sort_indices()
+    ST = S.T.tocsr()
+    ST.sort_indices()
+    return S, ST
+
+
+def neighbours(An):
+    """Stored off-diagonal pattern per row (splitting.py:158-165)."""
+    rows = _rows_of(An)
+    keep = An.indices != rows
+    cnt = np.bincount(rows[keep], minlength=An.shape[0])
+    ptr = np.concatenate([[0], np.cumsum(cnt)])
+    return ptr, An.indices[keep].astype(np.int64)
+
+
+UNASSIGNED, COARSE, FINE = 0, 1, 2
+
+
+def greedy_cf(An, c_init=(), f_init=(), theta=0.25):
+    """classical_cf (splitting.py:171-211) with a lazy max-heap.
+
+    The reference picks argmax(measure over unassigned), lowest index on ties;
+    a heap keyed (-measure, index) with stale-entry skipping yields the same
+    sequence of picks because measures only ever grow.
+    """
+    n = An.shape[0]
+    c_init = np.asarray(list(c_init), dtype=np.int64)
+    f_init = np.asarray(list(f_init), dtype=np.int64)
+    if len(np.intersect1d(c_init, f_init)) > 0:
+        raise ValueError("initial coarse and fine sets overlap")
+    state = np.zeros(n, dtype=np.int8)
+    state[c_init] = COARSE
+    state[f_init] = FINE
+    S, ST = strong_lists(An, theta)
+    nptr, nidx = neighbours(An)
+    # measure[i] = number of strong neighbours of i already fine
+    measure = np.asarray(S @ (state == FINE).astype(np.float64)).astype(np.int64)
+    heap = [(-int(measure[i]), int(i)) for i in np.flatnonzero(state == UNASSIGNED)]
+    heapq.heapify(heap)
+    st_ptr, st_idx = ST.indptr, ST.indices
+    while heap:
+        negm, i = heapq.heappop(heap)
+        if state[i] != UNASSIGNED or -negm != measure[i]:
+            continue
+        state[i] = COARSE
+        for j in nidx[nptr[i]:nptr[i + 1]]:
+            if state[j] != UNASSIGNED:
+                continue
+            state[j] = FINE
+            for k in st_idx[st_ptr[j]:st_ptr[j + 1]]:
+                measure[k] += 1
+                if state[k] == UNASSIGNED:
+                    heapq.heappush(heap, (-int(measure[k]), int(k)))
+    return np.flatnonzero(state == COARSE), np.flatnonzero(state == FINE)
+
+
+def nodal_split(A, Gt, bcols, theta=0.25):
+    """nodal_cf (splitting.py:214-229) -> (c_G, F, A_nodal)."""
+    An = nodal_dual(A, Gt)
+    bcols = np.asarray(bcols, dtype=np.int64)
+    nptr, nidx = neighbours(An)
+    touched = np.concatenate([nidx[nptr[b]:nptr[b + 1]] for b in bcols]) if len(bcols) else np.zeros(0, np.int64)
+    f_init = np.setdiff1d(np.unique(touched), bcols)
+    C, F = greedy_cf(An, c_init=bcols, f_init=f_init, theta=theta)
+    return np.setdiff1d(C, bcols), F, An
+
+
+def edge_table(Gt):
+    """(min node, max node) -> (row, value at min, value at max) over two-entry
+    rows, later rows winning (splitting.py:232-243)."""
+    table = {}
+    two = np.flatnonzero(np.diff(Gt.indptr) == 2)
+    lo = Gt.indptr[two]
+    for r, a, b, va, vb in zip(two.tolist(), Gt.indices[lo].tolist(), Gt.indices[lo + 1].tolist(),
+                               Gt.data[lo].tolist(), Gt.data[lo + 1].tolist()):
+        table[(a, b)] = (r, va, vb)
+    return table
+
+
+def algebraic_split(A, G, theta=0.25, dof_edges=None):
+    """build_algebraic_splitting (splitting.py:246-298)."""
+    Gt, bcols = augment(G)
+    c_G, _, An = nodal_split(A, Gt, bcols, theta)
+    coarse = np.union1d(c_G, bcols)
+    in_b = np.zeros(An.shape[0], dtype=bool)
+    in_b[bcols] = True
+    is_c = np.zeros(An.shape[0], dtype=bool)
+    is_c[coarse] = True
+    nptr, nidx = neighbours(An)
+    nsets = [set(nidx[nptr[v]:nptr[v + 1]].tolist()) for v in range(An.shape[0])]
+    table = edge_table(Gt)
+    free = np.ones(A.shape[0], dtype=bool)
+    used_mid = np.zeros(An.shape[0], dtype=bool)
+    pairs = []
+    for i in coarse.tolist():
+        reach = set()
+        for k in nidx[nptr[i]:nptr[i + 1]].tolist():
+            reach |= nsets[k]
+        for j in sorted(v for v in reach if v > i and is_c[v]):
+            if in_b[i] and in_b[j]:
+                continue
+            for k in sorted(nsets[i] & nsets[j]):
+                if used_mid[k]:
+                    continue
+                e1 = table.get((i, k) if i < k else (k, i))
+                e2 = table.get((k, j) if k < j else (j, k))
+                if e1 is None or e2 is None or e1[0] == e2[0]:
+                    continue
+                if not (free[e1[0]] and free[e2[0]]):
+                    continue
+                g1 = e1[1] if k < i else e1[2]      # Gtilde[dof1, k]
+                g2 = e2[1] if k < j else e2[2]      # Gtilde[dof2, k]
+                pairs.append(Pair(e1[0], e2[0], int(np.sign(g1)), int(-np.sign(g2)), i, k, j))
+                free[e1[0]] = free[e2[0]] = False
+                used_mid[k] = True
+                break
+    return Split(pairs, np.flatnonzero(free), A.shape[0], dof_edges=dof_edges, coarse_nodes=c_G)
+
+
+def refinement_split(coarse_mesh, fine_mesh, rmap, edge_to_dof, n):
+    """build_refinement_splitting (splitting.py:301-330)."""
+    free = np.ones(n, dtype=bool)
+    dof_edges = np.full(n, -1, dtype=np.int64)
+    live = np.flatnonzero(edge_to_dof >= 0)
+    dof_edges[edge_to_dof[live]] = live
+    pairs, owners = [], []
+    fe = np.asarray(fine_mesh.edges)
+    for E in range(coarse_mesh.ne):
+        c1, c2 = (int(c) for c in rmap.coarse_edge_children[E])
+        d1, d2 = int(edge_to_dof[c1]), int(edge_to_dof[c2])
+        if d1 < 0 or d2 < 0:
+            continue
+        t, h = (int(v) for v in coarse_mesh.edges[E])
+        mid = int(np.intersect1d(fe[c1], fe[c2])[0])
+        pairs.append(Pair(d1, d2, 1 if fe[c1][1] == mid else -1, 1 if fe[c2][0] == mid else -1,
+                          t, mid, h))
+        owners.append(E)
+        free[d1] = free[d2] = False
+    return Split(pairs, np.flatnonzero(free), n, dof_edges=dof_edges,
+                 pair_mesh_edges=np.array(owners, dtype=np.int64))
+
+
+def restriction(split):
+    """R of realize_RS (splitting.py:333-347, 363-372)."""
+    npair = split.n_pairs
+    rows = np.repeat(np.arange(npair), 2)
+    cols = np.array([d for p in split.pairs for d in (p.dof1, p.dof2)], dtype=np.int64)
+    vals = np.array([s * INV_SQRT2 for p in split.pairs for s in (p.sign1, p.sign2)])
+    return canon((vals, (rows, cols)), shape=(npair, split.n))
+
+
+def dump(split):
+    """dump_splitting text (splitting.py:375-380): parity-fixture format."""
+    out = [f"n {split.n}"]
+    out += [f"{p.tail} {p.mid} {p.head} {p.dof1} {p.sign1} {p.dof2} {p.sign2}" for p in split.pairs]
+    return "\n".join(out) + "\n"
+
+
+# ----------------------------------------------------------------------------- transfer
+
+def components(A_II):
+    """Connected components as sorted index arrays (transfer.py:49-52)."""
+    ncomp, lab = connected_components(A_II, directed=False)
+    order = np.argsort(lab, kind="stable")
+    cuts = np.searchsorted(lab[order], np.arange(ncomp + 1))
+    return [order[cuts[c]:cuts[c + 1]] for c in range(ncomp)]
+
+
+def coarse_grad(R, G, mode, coarse_nodes=None):
+    """coarse_gradient (transfer.py:55-74) -> (Gc, kept columns)."""
+    RG = canon(R @ G)
+    cnt = np.diff(RG.tocsc().indptr)
+    if mode == "refinement":
+        cols = np.flatnonzero(cnt > 0)
+    elif mode == "algebraic":
+        if coarse_nodes is None:
+            raise ValueError("algebraic mode needs the coarse nodal set")
+        cols = np.asarray(sorted(coarse_nodes), dtype=np.int64)
+        cols = cols[cnt[cols] > 0]
+    else:
+        raise ValueError(f"unknown mode {mode!r}")
+    Gc = canon(RG[:, cols]) if len(cols) else sp.csr_matrix((RG.shape[0], 0))
+    return Gc, cols
+
+
+@dataclass
+class Transfer:
+    P: sp.csr_matrix
+    R: sp.csr_matrix
+    Gc: sp.csr_matrix
+    cols: np.ndarray
+    Z_blocks: list = field(default_factory=list)   # (interior rows, keep cols, Z) per component
+
+
+def harmonic_interp(A, split, mode="refinement", G=None):
+    """sparse_ideal_interp (transfer.py:77-122): P = R^T - S_I A_II^{-1} S_I^T A R^T."""
+    R = restriction(split)
+    Rt = canon(R.T)
+    inner = split.interior_dofs
+    blocks = []
+    if len(inner) == 0 or split.n_pairs == 0:
+        P = Rt
+    else:
+        Ai = A[inner, :]
+        W = canon(Ai @ Rt)
+        A_II = canon(Ai[:, inner])
+        ri, ci, vi = [], [], []
+        for comp in components(A_II):
+            Wc = W[comp, :].tocsc()
+            keep = np.flatnonzero(np.diff(Wc.indptr) > 0)
+            if keep.size == 0:
+                continue
+            L = dense_chol(A_II[comp][:, comp].toarray())
+            Z = scipy.linalg.cho_solve((L, True), np.asarray(Wc[:, keep].todense()))
+            blocks.append((inner[comp], keep, Z))
+            nzr, nzc = np.nonzero(Z)
+            ri.append(inner[comp[nzr]])
+            ci.append(keep[nzc])
+            vi.append(-Z[nzr, nzc])
+        if ri:
+            corr = canon((np.concatenate(vi), (np.concatenate(ri), np.concatenate(ci))),
+                         shape=(split.n, split.n_pairs))
+        else:
+            corr = sp.csr_matrix((split.n, split.n_pairs))
+        P = canon(Rt + corr)
+    if G is not None:
+        Gc, cols = coarse_grad(R, G, mode, split.coarse_nodes)
+    else:
+        Gc, cols = sp.csr_matrix((split.n_pairs, 0)), np.zeros(0, dtype=np.int64)
+    return Transfer(P, R, Gc, cols, blocks)
+
+
+# ----------------------------------------------------------------------------- smoother
+
+@dataclass
+class Patches:
+    """PatchSet (smoothers.py:26-40)."""
+
+    patches: list
+    factors: list
+    update_rows: list
+    update_blocks: list
+
+
+def vertex_patches(A, Gl):
+    """build_patches (smoothers.py:60-95)."""
+    n = A.shape[0]
+    Gc = Gl.tocsc()
+    pl = []
+    seen = np.zeros(n, dtype=bool)
+    for v in range(Gc.shape[1]):
+        r = Gc.indices[Gc.indptr[v]:Gc.indptr[v + 1]]
+        if r.size:
+            p = np.unique(r)
+            pl.append(p)
+            seen[p] = True
+    pl += [np.array([d]) for d in np.flatnonzero(~seen)]
+    Ac = A.tocsc()
+    facs, rows_l, blocks = [], [], []
+    for pid, p in enumerate(pl):
+        cols = Ac[:, p]
+        rows = np.unique(cols.indices)
+        blk = np.asarray(cols[rows, :].todense())
+        try:
+            facs.append(dense_chol(blk[np.searchsorted(rows, p), :]))
+        except NotPositiveDefiniteError as err:
+            raise NotPositiveDefiniteError(err.pivot, f"singular patch block {pid}") from err
+        rows_l.append(rows)
+        blocks.append(blk)
+    return Patches(pl, facs, rows_l, blocks)
+
+
+def l1_diag(A):
+    """build_l1_jacobi (smoothers.py:50-52)."""
+    return np.asarray(abs(A).sum(axis=1)).ravel()
+
+
+def _sweep(ps, x, r, order):
+    for p in order:
+        idx = ps.patches[p]
+        d = scipy.linalg.cho_solve((ps.factors[p], True), r[idx])
+        x[idx] += d
+        r[ps.update_rows[p]] -= ps.update_blocks[p] @ d
+
+
+def _jacobi(A, l1, x, r):
+    d = r / l1
+    x += d
+    r -= A @ d
+
+
+def smooth(A, ps, l1, x, b, direction="forward"):
+    """OSS-l1 (smoothers.py:112-137)."""
+    if A.shape[0] != len(b) or len(x) != len(b):
+        raise ValueError("shape mismatch")
+    x = np.array(x, dtype=np.float64)
+    r = b - A @ x
+    m = len(ps.patches)
+    if direction == "forward":
+        _sweep(ps, x, r, range(m))
+        _jacobi(A, l1, x, r)
+    elif direction == "backward":
+        _jacobi(A, l1, x, r)
+        _sweep(ps, x, r, range(m - 1, -1, -1))
+    elif direction == "symmetric":
+        _sweep(ps, x, r, range(m))
+        _jacobi(A, l1, x, r)
+        _jacobi(A, l1, x, r)
+        _sweep(ps, x, r, range(m - 1, -1, -1))
+    else:
+        raise ValueError(f"unknown direction {direction!r}")
+    return x
+
+
+# ----------------------------------------------------------------------------- multilevel
+
+@dataclass
+class OLevel:
+    A: sp.csr_matrix
+    G: sp.csr_matrix
+    P: sp.csr_matrix = None
+    patches: Patches = None
+    l1: np.ndarray = None
+    coarse_factor: Factor = None
+    splitting: Split = None
+    transfer: Transfer = None
+
+    @property
+    def n(self):
+        return self.A.shape[0]
+
+
+@dataclass
+class OHierarchy:
+    levels: list
+    method: str
+    stalled: bool = False
+    notes: list = field(default_factory=list)
+
+    @property
+    def depth(self):
+        return len(self.levels)
+
+
+@dataclass
+class OReport:
+    iterations: int
+    residual_history: np.ndarray
+    converged: bool
+    operator_complexity: float
+    note: str = ""
+
+
+def sign_gradient(Gc):
+    """_normalized_gradient (multilevel.py:71-75)."""
+    G = canon(Gc)
+    G.data = np.sign(G.data)
+    return canon(G)
+
+
+def hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse=32,
+              theta=0.25, smoother=True):
+    """build_hierarchy (multilevel.py:78-164) for the "alg" and "ref" routes.
+
+    ``smoother=False`` skips the patch factorisation (used when only the
+    setup integers/operators are compared at sizes where it is slow).
+    """
+    if method in ("geo", "ref") and (meshes is None or rmaps is None):
+        raise ValueError(f"method {method!r} requires the nested mesh chain")
+    if method not in ("ref", "alg"):
+        raise ValueError(f"unknown method {method!r}")
+    A, G = system.A, system.G
+    levels, notes, stalled = [], [], False
+    pos = len(meshes) - 1 if meshes is not None else 0
+    e2d = system.free_edges
+    dof_edges = None
+    if e2d is not None:
+        dof_edges = np.full(system.n, -1, dtype=np.int64)
+        live = np.flatnonzero(e2d >= 0)
+        dof_edges[e2d[live]] = live
+    while True:
+        n = A.shape[0]
+        if n <= min_coarse or len(levels) + 1 >= max_levels:
+            break
+        if method == "ref":
+            if pos == 0:
+                stalled = True
+                notes.append(f"mesh chain exhausted at {n} DoFs")
+                break
+            split = refinement_split(meshes[pos - 1], meshes[pos], rmaps[pos - 1], e2d, n)
+            if split.n_pairs == 0:
+                stalled = True
+                notes.append("refinement splitting produced no pairs")
+                break
+            tr = harmonic_interp(A, split, "refinement", G)
+            nxt = np.full(meshes[pos - 1].ne, -1, dtype=np.int64)
+            nxt[split.pair_mesh_edges] = np.arange(split.n_pairs)
+        else:
+            split = algebraic_split(A, G, theta, dof_edges if not levels else None)
+            if split.n_pairs == 0 or split.n_pairs >= n:
+                if split.n_pairs == 0:
+                    stalled = True
+                    notes.append("algebraic coarsening found no pairs")
+                break
+            tr = harmonic_interp(A, split, "algebraic", G)
+            nxt = None
+        P = tr.P
+        if P.shape[1] == 0 or P.shape[1] >= n:
+            stalled = True
+            notes.append(f"no size reduction ({n} -> {P.shape[1]})")
+            break
+        levels.append(OLevel(A, G, P, vertex_patches(A, G) if smoother else None, l1_diag(A),
+                             splitting=split, transfer=tr))
+        A = galerkin(P, A)
+        G = sign_gradient(tr.Gc)
+        e2d = nxt
+        pos -= 1
+    levels.append(OLevel(A, G, coarse_factor=factor_coarsest(A)))
+    return OHierarchy(levels, method, stalled, notes)
+
+
+def _cycle(levels, ell, b):
+    """multilevel.py:177-184."""
+    lv = levels[ell]
+    if lv.P is None:
+        return solve_coarsest(lv.coarse_factor, b)
+    x = smooth(lv.A, lv.patches, lv.l1, np.zeros_like(b), b, "forward")
+    r = b - lv.A @ x
+    x = x + lv.P @ _cycle(levels, ell + 1, lv.P.T @ r)
+    return smooth(lv.A, lv.patches, lv.l1, x, b, "backward")
+
+
+def vcycle(h, b, x=None):
+    """multilevel.py:187-196."""
+    b = np.asarray(b, dtype=np.float64)
+    if b.shape[0] != h.levels[0].n:
+        raise ValueError("rhs does not match the finest level")
+    if x is None:
+        return _cycle(h.levels, 0, b)
+    x = np.asarray(x, dtype=np.float64)
+    return x + _cycle(h.levels, 0, b - h.levels[0].A @ x)
+
+
+def operator_complexity(h):
+    """multilevel.py:199-201."""
+    return float(sum(lv.A.nnz for lv in h.levels)) / float(h.levels[0].A.nnz)
+
+
+def amg_solve(h, b, x0=None, tol=1e-8, maxit=500):
+    """multilevel.py:204-235."""
+    if tol <= 0:
+        raise ValueError("tolerance must be positive")
+    A = h.levels[0].A
+    b = np.asarray(b, dtype=np.float64)
+    x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64)
+    bn = np.linalg.norm(b)
+    if bn == 0.0:
+        return np.zeros_like(b), OReport(0, np.zeros(0), True, operator_complexity(h))
+    hist = []
+    rel = np.linalg.norm(b - A @ x) / bn
+    done = rel <= tol
+    note, growth, it = "", 0, 0
+    while not done and it < maxit:
+        x = vcycle(h, b, x)
+        prev, rel = rel, np.linalg.norm(b - A @ x) / bn
+        hist.append(rel)
+        it += 1
+        if rel <= tol:
+            done = True
+            break
+        growth = growth + 1 if rel > prev else 0
+        if growth >= 5:
+            note = "diverged: residual grew over 5 consecutive iterations"
+            break
+    return x, OReport(it, np.array(hist), done, operator_complexity(h), note)
+
+
+def pcg(A, b, precond, x0=None, tol=1e-8, maxit=500, oc=1.0):
+    """multilevel.py:238-281."""
+    if tol <= 0:
+        raise ValueError("tolerance must be positive")
+    b = np.asarray(b, dtype=np.float64)
+    x = np.zeros_like(b) if x0 is None else np.array(x0, dtype=np.float64)
+    bn = np.linalg.norm(b)
+    if bn == 0.0:
+        return np.zeros_like(b), OReport(0, np.zeros(0), True, oc)
+    r = b - A @ x
+    rel = np.linalg.norm(r) / bn
+    if rel <= tol:
+        return x, OReport(0, np.zeros(0), True, oc)
+    z = precond(r)
+    p = z.copy()
+    rz = r @ z
+    hist, it, done = [], 0, False
+    while it < maxit:
+        Ap = A @ p
+        pAp = p @ Ap
+        if pAp <= 0.0:
+            raise RuntimeError(f"PCG breakdown: p^T A p = {pAp:.3e} (non-SPD operator)")
+        alpha = rz / pAp
+        x += alpha * p
+        r -= alpha * Ap
+        it += 1
+        rel = np.linalg.norm(r) / bn
+        hist.append(rel)
+        if rel <= tol:
+            done = True
+            break
+        z = precond(r)
+        rz_new = r @ z
+        if rz_new <= 0.0:
+            raise RuntimeError("PCG breakdown: preconditioner is not SPD")
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    return x, OReport(it, np.array(hist), done, oc)

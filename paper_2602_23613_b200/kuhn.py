@@ -1,0 +1,255 @@
+"""Seeded 3D Kuhn-cube curl-curl systems (input generation, not the hot path).
+
+The reference package only meshes 2D domains (``mesh.py``/``fem.py``); every
+BASELINE configuration is a unit cube split into n^3 hexahedra x 6 Kuhn
+tetrahedra.  This module produces those systems with the reference's own
+conventions so the oracle and the GPU path see identical
+arrays:
+
+* vertices of the (n+1)^3 grid, lexicographic numbering v = (k(n+1)+j)(n+1)+i;
+* six tets per hex, cube-major / permutation-minor, vertex order
+  v0 -> v0+e_a -> v0+e_a+e_b -> v0+e_x+e_y+e_z;
+* edges stored tail < head, numbered by lexicographic (tail, head) sort
+  (as ``mesh_from_cells``, reference mesh.py:128-141);
+* Whitney element matrices with unit tangential-integral DoFs, the 3D
+  analogue of ``tri_element_matrices`` (reference fem.py:53-84);
+* tangential Dirichlet elimination and the discrete gradient exactly as
+  ``build_gradient``/``assemble`` (reference fem.py:111-195): edge rows and
+  vertex columns on the boundary are removed, G[e, head] = +1,
+  G[e, tail] = -1, and A = csr(0.5 (A + A^T)) with A = As + beta Am.
+
+The stiffness weight is mu^{-1} per tet (BASELINE states mu^{-1} directly;
+the reference multiplies the element stiffness by 1/mu, fem.py:173).
+"""
+
+from __future__ import annotations
+
+import itertools
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+__all__ = ["KuhnSystem", "kuhn_mesh", "assemble_kuhn", "config_system", "CONFIGS", "rhs"]
+
+
+def _canon(a, shape=None):
+    """Canonical CSR (sorted, duplicates summed, exact zeros dropped) — the same
+    normal form as the reference's ``csr()`` (sparse.py:58-65)."""
+    m = sp.csr_matrix(a, shape=shape, dtype=np.float64)
+    m.sum_duplicates()
+    m.sort_indices()
+    m.eliminate_zeros()
+    return m
+
+
+@dataclass
+class KuhnMesh:
+    n: int
+    vertices: np.ndarray        # (nv, 3)
+    tets: np.ndarray            # (nt, 4)
+    edges: np.ndarray           # (ne, 2) tail < head
+    tet_edges: np.ndarray       # (nt, 6)
+    tet_edge_signs: np.ndarray  # (nt, 6)
+    boundary_edge: np.ndarray
+    boundary_vertex: np.ndarray
+
+    @property
+    def nv(self):
+        return len(self.vertices)
+
+    @property
+    def ne(self):
+        return len(self.edges)
+
+    @property
+    def nc(self):
+        return len(self.tets)
+
+    def tet_centroids(self):
+        return self.vertices[self.tets].mean(axis=1)
+
+
+@dataclass
+class KuhnSystem:
+    """Same fields as the reference's ``CurlCurlSystem`` (fem.py:30-50)."""
+
+    A: sp.csr_matrix
+    As: sp.csr_matrix
+    Am: sp.csr_matrix
+    G: sp.csr_matrix
+    beta: float
+    free_edges: np.ndarray
+    free_nodes: np.ndarray
+    mesh: KuhnMesh = None
+
+    @property
+    def n(self):
+        return self.A.shape[0]
+
+
+_LOCAL_EDGES = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))
+
+
+def kuhn_mesh(n):
+    """Unit cube, n^3 hexes, 6 Kuhn tets each (conforming, nested under 2x)."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    N = n + 1
+    idx = np.arange(N ** 3, dtype=np.int64)
+    gi, gj, gk = idx % N, (idx // N) % N, idx // (N * N)
+    vertices = np.stack([gi, gj, gk], axis=1).astype(np.float64) / n
+    step = np.array([1, N, N * N], dtype=np.int64)
+    ck, cj, ci = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    v0 = ((ck * N + cj) * N + ci).ravel()
+    far = v0 + step.sum()
+    tets = []
+    for a, b, _ in itertools.permutations(range(3)):
+        tets.append(np.stack([v0, v0 + step[a], v0 + step[a] + step[b], far], axis=1))
+    # cube-major / permutation-minor order
+    tets = np.stack(tets, axis=1).reshape(-1, 4)
+
+    loc = np.array(_LOCAL_EDGES)
+    ends = tets[:, loc]                      # (nt, 6, 2)
+    lo, hi = ends.min(axis=2), ends.max(axis=2)
+    keys = lo * (N ** 3) + hi
+    uniq, inv = np.unique(keys.ravel(), return_inverse=True)
+    edges = np.stack([uniq // (N ** 3), uniq % (N ** 3)], axis=1)
+    tet_edges = inv.reshape(-1, 6)
+    tet_edge_signs = np.where(ends[:, :, 0] < ends[:, :, 1], 1, -1)
+
+    g = np.stack([gi, gj, gk], axis=1)
+    on_face = (g == 0) | (g == n)                         # (nv, 3)
+    boundary_vertex = on_face.any(axis=1)
+    t, h = edges[:, 0], edges[:, 1]
+    same_low = (g[t] == g[h]) & (g[t] == 0)
+    same_high = (g[t] == g[h]) & (g[t] == n)
+    boundary_edge = (same_low | same_high).any(axis=1)
+    return KuhnMesh(n, vertices, tets, edges, tet_edges, tet_edge_signs,
+                    boundary_edge, boundary_vertex)
+
+
+def _tet_element(coords):
+    """Whitney stiffness/mass (6x6) of one tet; local edge (i,j) basis
+    W_ij = l_i grad l_j - l_j grad l_i with unit tangential integral i->j."""
+    M4 = np.column_stack([np.ones(4), coords])
+    inv = np.linalg.inv(M4)                  # columns: lambda coefficients
+    grads = inv[1:, :].T                      # (4, 3) grad lambda_i
+    vol = abs(np.linalg.det(M4)) / 6.0
+    curls = np.array([2.0 * np.cross(grads[i], grads[j]) for i, j in _LOCAL_EDGES])
+    S = vol * curls @ curls.T
+    gram = grads @ grads.T
+    I2 = vol / 20.0 * (np.ones((4, 4)) + np.eye(4))
+    M = np.empty((6, 6))
+    for a, (i, j) in enumerate(_LOCAL_EDGES):
+        for b, (k, l) in enumerate(_LOCAL_EDGES):
+            M[a, b] = (gram[j, l] * I2[i, k] - gram[j, k] * I2[i, l]
+                       - gram[i, l] * I2[j, k] + gram[i, k] * I2[j, l])
+    return S, M
+
+
+def assemble_kuhn(mesh, muinv, beta):
+    """Assemble A = As(mu^{-1}) + beta Am on the free edges (fem.py:143-195 in 3D)."""
+    muinv = np.asarray(muinv, dtype=np.float64)
+    if muinv.shape != (mesh.nc,):
+        raise ValueError("coefficient field does not match the mesh")
+    if np.any(muinv <= 0):
+        raise ValueError("coefficient values must be positive")
+    if beta < 0:
+        raise ValueError("shift must be nonnegative")
+    nper = 6
+    # all tets of one permutation type are translates: 6 element matrix pairs
+    S6, M6 = [], []
+    for p in range(nper):
+        S, M = _tet_element(mesh.vertices[mesh.tets[p]])
+        S6.append(S)
+        M6.append(M)
+    S6, M6 = np.array(S6), np.array(M6)
+    ptype = np.arange(mesh.nc) % nper
+    signs = mesh.tet_edge_signs.astype(np.float64)
+    D = signs[:, :, None] * signs[:, None, :]
+    Se = S6[ptype] * D * muinv[:, None, None]
+    Me = M6[ptype] * D
+    ge = mesh.tet_edges
+    rows = np.repeat(ge, 6, axis=1).ravel()
+    cols = np.tile(ge, (1, 6)).ravel()
+    shape = (mesh.ne, mesh.ne)
+    As_full = _canon((Se.ravel(), (rows, cols)), shape=shape)
+    Am_full = _canon((Me.ravel(), (rows, cols)), shape=shape)
+
+    free_e = ~mesh.boundary_edge
+    free_v = ~mesh.boundary_vertex
+    free_edges = np.full(mesh.ne, -1, dtype=np.int64)
+    free_edges[free_e] = np.arange(int(free_e.sum()))
+    free_nodes = np.full(mesh.nv, -1, dtype=np.int64)
+    free_nodes[free_v] = np.arange(int(free_v.sum()))
+    fe = np.flatnonzero(free_e)
+    t, h = mesh.edges[fe, 0], mesh.edges[fe, 1]
+    r = free_edges[fe]
+    hv, tv = free_nodes[h], free_nodes[t]
+    gr = np.concatenate([r[hv >= 0], r[tv >= 0]])
+    gc = np.concatenate([hv[hv >= 0], tv[tv >= 0]])
+    gv = np.concatenate([np.ones(int((hv >= 0).sum())), -np.ones(int((tv >= 0).sum()))])
+    G = _canon((gv, (gr, gc)), shape=(int(free_e.sum()), int(free_v.sum())))
+
+    keep = fe
+    As = _canon(As_full[keep][:, keep])
+    Am = _canon(Am_full[keep][:, keep])
+    As = _canon(0.5 * (As + As.T))
+    Am = _canon(0.5 * (Am + Am.T))
+    A = _canon(As + beta * Am) if beta > 0 else As.copy()
+    A = _canon(0.5 * (A + A.T))
+    return KuhnSystem(A, As, Am, G, float(beta), free_edges, free_nodes, mesh)
+
+
+# --------------------------------------------------------------- coefficient fields
+
+def _checkerboard(mesh, k, lo, hi):
+    """k^3 checkerboard of sub-cubes; (I+J+K) even -> lo, odd -> hi (per tet centroid)."""
+    c = mesh.tet_centroids()
+    cell = np.clip((c * k).astype(np.int64), 0, k - 1)
+    par = cell.sum(axis=1) % 2
+    return np.where(par == 0, lo, hi)
+
+
+def _block_loguniform(mesh, block, seed, lo_exp=-3.0, hi_exp=3.0):
+    """mu^{-1} constant on block^3-hex blocks, 10^U(lo,hi), block-lexicographic draw."""
+    nb = mesh.n // block
+    rng = np.random.default_rng(seed)
+    vals = 10.0 ** rng.uniform(lo_exp, hi_exp, nb ** 3)
+    c = mesh.tet_centroids()
+    cell = np.clip((c * nb).astype(np.int64), 0, nb - 1)
+    return vals[(cell[:, 2] * nb + cell[:, 1]) * nb + cell[:, 0]]
+
+
+def _inclusions(mesh, count, seed, rmin=0.03, rmax=0.08, inside=1e-6, background=1.0):
+    rng = np.random.default_rng(seed)
+    radii = rng.uniform(rmin, rmax, count)
+    centres = rng.uniform(0.0, 1.0, (count, 3))
+    c = mesh.tet_centroids()
+    out = np.full(mesh.nc, background)
+    for r, x in zip(radii, centres):
+        out[np.sum((c - x) ** 2, axis=1) <= r * r] = inside
+    return out
+
+
+# name -> (n, beta, coefficient builder, route); BASELINE.json configs[0..4]
+CONFIGS = {
+    "c1": dict(n=8, beta=1e-2, field=lambda m: np.ones(m.nc), route="alg"),
+    "c2": dict(n=32, beta=1e-3, field=lambda m: _checkerboard(m, 4, 1.0, 1e6), route="alg"),
+    "c3": dict(n=64, beta=1e-3, field=lambda m: _block_loguniform(m, 8, seed=0), route="ref"),
+    "c4": dict(n=128, beta=1e-4, field=lambda m: _inclusions(m, 64, seed=0), route="alg"),
+    "c5": dict(n=256, beta=1e-3, field=lambda m: _checkerboard(m, 8, 1.0, 1e6), route="alg"),
+}
+
+
+def config_system(name, n=None):
+    """Build the system of a BASELINE config (optionally at another size n)."""
+    cfg = CONFIGS[name]
+    mesh = kuhn_mesh(cfg["n"] if n is None else n)
+    return assemble_kuhn(mesh, cfg["field"](mesh), cfg["beta"])
+
+
+def rhs(n, seed=0):
+    """Seeded uniform[-1,1] right-hand side (seed recorded as 0 by default)."""
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, n)
