@@ -1,0 +1,153 @@
+/*
+ * libhcamg — C-ABI of the B200-native AMG-PCG hot path for lowest-order
+ * Nédélec H(curl) systems (arXiv 2602.23613).
+ *
+ * The reference package exposes this path as Python functions in
+ * hcurl_amg/multilevel.py; every entry point below replaces one of them and
+ * is what a ctypes / cffi binding of that module binds (INTEGRATION.md shows
+ * the binding).  Plain pointers and sizes only: matrices are canonical CSR
+ * (int64 row pointers, int32 column indices, fp64 values, sorted, no stored
+ * zeros — the normal form of hcurl_amg/sparse.py:58-65); vectors are fp64.
+ *
+ * Return codes: 0 on success, a negative HCAMG_E* code otherwise; the
+ * message is available from hcamg_last_error() and, for HCAMG_ENOTSPD, the
+ * failing pivot from hcamg_error_index().  Calls on one handle are not
+ * thread-safe; distinct handles are independent.  One handle = one device
+ * and one CUDA stream; every matrix of the hierarchy stays resident in HBM
+ * between calls.
+ */
+#ifndef HCAMG_H_
+#define HCAMG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HCAMG_OK 0
+#define HCAMG_EINVAL (-1)      /* ValueError (shapes, method, malformed G)      */
+#define HCAMG_ENOTSPD (-2)     /* NotPositiveDefiniteError(pivot)  sparse.py:50 */
+#define HCAMG_EBREAKDOWN (-3)  /* RuntimeError("PCG breakdown…") multilevel.py:265,278 */
+#define HCAMG_ENOMEM (-4)
+#define HCAMG_ECUDA (-5)
+#define HCAMG_ENOTSYM (-6)     /* ValueError("matrix not symmetric…") sparse.py:294 */
+#define HCAMG_EUNSUPPORTED (-7)
+
+typedef struct hcamg_handle hcamg_handle;
+
+/* Host CSR view (read-only). */
+typedef struct {
+  int64_t nrows, ncols;
+  const int64_t* indptr;   /* nrows + 1 */
+  const int32_t* indices;  /* indptr[nrows] */
+  const double* data;      /* indptr[nrows] */
+} hcamg_csr;
+
+/* Solve report (multilevel.py:62-68 SolveReport, minus the history array,
+ * which is written to a caller buffer). */
+typedef struct {
+  int64_t iterations;
+  int32_t converged;
+  int32_t zero_rhs;        /* b == 0: x = 0, 0 iterations */
+  int32_t diverged;        /* amg_solve divergence guard fired (multilevel.py:230-233) */
+  int32_t pad;
+  double final_relres;
+} hcamg_report;
+
+/* Hierarchy summary (multilevel.py:50-59 Hierarchy). */
+typedef struct {
+  int32_t depth;
+  int32_t stalled;
+  int32_t method;          /* 0 = "ref", 1 = "alg", 2 = user-assembled */
+  int32_t pad;
+  double operator_complexity;   /* multilevel.py:199-201 */
+  double setup_seconds;         /* device-synchronised wall time of the setup */
+} hcamg_info;
+
+/* Per-level sizes for exports. */
+typedef struct {
+  int64_t n, nnz_A, ncols_G, nnz_G, nnz_P, n_pairs, n_interior, n_coarse_nodes;
+  int64_t n_patches, n_patch_entries, n_waves, n_gc_cols, coarsest, n_components, max_component, pad;
+} hcamg_level_info;
+
+/* ---- lifetime ---------------------------------------------------------- */
+int hcamg_create(hcamg_handle** out, int device, void* cuda_stream /* NULL: own stream */);
+void hcamg_destroy(hcamg_handle* h);
+const char* hcamg_last_error(const hcamg_handle* h);
+int64_t hcamg_error_index(const hcamg_handle* h);
+int hcamg_version(void);
+
+/* ---- setup: build_hierarchy (multilevel.py:78-164) ---------------------- */
+/* method "alg": splitting.py:246-298 + transfer.py:77-122 per level. */
+int hcamg_setup_alg(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* G, int32_t max_levels,
+                    int64_t min_coarse, double theta, hcamg_info* info);
+/* method "ref": the nested mesh chain, coarsest first (multilevel.py:118-131,
+ * splitting.py:301-330).  edges[i]: ne[i] x 2 (tail < head) of mesh i;
+ * children[i]: ne[i] x 2 fine-edge ids of coarse edge E of mesh i in mesh i+1
+ * (RefinementMap.coarse_edge_children); free_edges: finest mesh edge -> DoF
+ * (-1 eliminated). */
+int hcamg_setup_ref(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* G, int32_t n_meshes,
+                    const int64_t* ne, const int64_t* const* edges, const int64_t* const* children,
+                    const int64_t* free_edges, int32_t max_levels, int64_t min_coarse, hcamg_info* info);
+/* user-assembled hierarchy (Hierarchy(levels=[Level(A, G, P)...]) built by
+ * hand, as tests/test_multilevel.py:125-134 does): push levels finest first;
+ * a level with P == NULL is the coarsest and is factored directly
+ * (sparse.py:276-301). */
+int hcamg_hier_begin(hcamg_handle* h);
+int hcamg_hier_push(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* G /* may be NULL */,
+                    const hcamg_csr* P /* NULL: coarsest */);
+int hcamg_hier_end(hcamg_handle* h, hcamg_info* info);
+/* as hcamg_hier_end, but the coarsest solve applies coarse_matrix^{-1}: the
+ * matrix whose Cholesky factor the user attached as Level.coarse_factor. */
+int hcamg_hier_end_with(hcamg_handle* h, const hcamg_csr* coarse_matrix, hcamg_info* info);
+
+/* ---- queries / exports (lazily materialised Level fields) -------------- */
+int hcamg_info_get(hcamg_handle* h, hcamg_info* info);
+int hcamg_notes(hcamg_handle* h, char* buf, int64_t cap);   /* '\n'-separated Hierarchy.notes */
+int hcamg_level(hcamg_handle* h, int32_t level, hcamg_level_info* out);
+/* which: 0 = A, 1 = P, 2 = G.  Buffers sized from hcamg_level. */
+int hcamg_export_csr(hcamg_handle* h, int32_t level, int32_t which, int64_t* indptr, int32_t* indices,
+                     double* data);
+/* pairs: n_pairs x 7 (dof1, dof2, sign1, sign2, tail, mid, head); interior:
+ * n_interior; coarse_nodes: n_coarse_nodes (algebraic c_G) or mesh edges
+ * of the pairs (refinement route); any pointer may be NULL. */
+int hcamg_export_splitting(hcamg_handle* h, int32_t level, int64_t* pairs, int64_t* interior,
+                           int64_t* coarse_nodes);
+int hcamg_export_l1(hcamg_handle* h, int32_t level, double* d);
+/* patches in reference order: ptr (n_patches + 1), dofs (n_patch_entries), wave of each patch */
+int hcamg_export_patches(hcamg_handle* h, int32_t level, int64_t* ptr, int64_t* dofs, int64_t* wave);
+int hcamg_export_coarse_cols(hcamg_handle* h, int32_t level, int64_t* cols);
+
+/* ---- solve ------------------------------------------------------------- */
+/* vcycle(h, b, x=None) (multilevel.py:187-196): out = x + V(b - A x), or V(b). */
+int hcamg_vcycle(hcamg_handle* h, const double* b, const double* x_or_null, double* out);
+/* pcg(A, b, precond=lambda r: vcycle(h, r), x0, tol, maxit) (multilevel.py:238-281)
+ * with A = the finest operator; history: maxit doubles (may be NULL). */
+int hcamg_pcg(hcamg_handle* h, const double* b, const double* x0_or_null, double tol, int64_t maxit,
+              double* x, double* history, hcamg_report* report);
+/* amg_solve(h, b, x0, tol, maxit) (multilevel.py:204-235). */
+int hcamg_amg_solve(hcamg_handle* h, const double* b, const double* x0_or_null, double tol, int64_t maxit,
+                    double* x, double* history, hcamg_report* report);
+/* Device-resident variant of hcamg_pcg: b, x0, x are device pointers on the
+ * handle's device; no host synchronisation when report == NULL. */
+int hcamg_pcg_device(hcamg_handle* h, const double* d_b, const double* d_x0_or_null, double tol,
+                     int64_t maxit, double* d_x, hcamg_report* report);
+/* Kernel launches recorded in the last PCG / V-cycle graph (gpu_launches). */
+int64_t hcamg_graph_launches(hcamg_handle* h, int32_t which /* 0 vcycle, 1 pcg init, 2 pcg body */);
+/* Device stream of the handle (cudaStream_t) for event timing. */
+void* hcamg_stream(hcamg_handle* h);
+
+/* ---- generic PCG with a host preconditioner (any `precond` callable) ---- */
+typedef int (*hcamg_precond_fn)(const double* r, double* z, int64_t n, void* ctx);
+/* A: any square operator (uploaded); precond called with host vectors. */
+int hcamg_pcg_generic(hcamg_handle* h, const hcamg_csr* A, const double* b, const double* x0_or_null,
+                      double tol, int64_t maxit, hcamg_precond_fn precond, void* ctx, double* x,
+                      double* history, hcamg_report* report);
+/* y = A x on the device (A uploaded per call; used by the drop-in for A @ x). */
+int hcamg_spmv(hcamg_handle* h, const hcamg_csr* A, const double* x, double* y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HCAMG_H_ */

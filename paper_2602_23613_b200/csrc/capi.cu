@@ -1,0 +1,818 @@
+// C-ABI of libhcamg (include/hcamg.h): handle lifetime, the build_hierarchy
+// driver (hcurl_amg/multilevel.py:78-164) and the solve entry points
+// (multilevel.py:187-281) with their CUDA-graph executables.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/hcamg.h"
+#include "dense.cuh"
+#include "interp.cuh"
+#include "smoother.cuh"
+#include "solve.cuh"
+
+using namespace hcamg;
+
+namespace {
+
+struct Graph {
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphExec_t pre = nullptr, body = nullptr;  // host-driven fallback
+  bool conditional = false;
+  int64_t launches_pre = 0, launches_body = 0;
+  void reset() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (pre) cudaGraphExecDestroy(pre);
+    if (body) cudaGraphExecDestroy(body);
+    exec = pre = body = nullptr;
+    launches_pre = launches_body = 0;
+  }
+};
+
+}  // namespace
+
+struct hcamg_handle {
+  int device = 0;
+  cudaStream_t stream = nullptr, aux = nullptr;
+  bool own_stream = false;
+  cublasHandle_t cublas = nullptr;
+  std::vector<std::unique_ptr<DevLevel>> levels;
+  std::vector<DevLevel*> lv;
+  bool stalled = false;
+  int method = 1;
+  std::vector<std::string> notes;
+  double setup_seconds = 0.0;
+  Workspace ws;
+  Graph g_vc, g_pcg, g_amg;
+  DBuf<double> vc_b, vc_x;
+  int64_t graph_maxit = -1;
+  std::string err;
+  int64_t err_index = -1;
+  // user-assembled hierarchy under construction
+  std::vector<std::unique_ptr<DevLevel>> pending;
+};
+
+namespace {
+
+void upload_csr(const hcamg_csr* M, DCsr& out, cudaStream_t s) {
+  require(M != nullptr, "missing matrix");
+  require(M->nrows >= 0 && M->ncols >= 0, "negative matrix shape");
+  csr_upload(M->indptr, M->indices, M->data, M->nrows, M->ncols, out, s);
+}
+
+void invalidate(hcamg_handle* h) {
+  h->g_vc.reset();
+  h->g_pcg.reset();
+  h->g_amg.reset();
+  h->graph_maxit = -1;
+}
+
+void refresh_views(hcamg_handle* h) {
+  h->lv.clear();
+  for (auto& l : h->levels) h->lv.push_back(l.get());
+}
+
+void alloc_level_vectors(DevLevel& L, cudaStream_t s) {
+  const int64_t n = std::max<int64_t>(L.n, 1);
+  for (DBuf<double>* v : {&L.b, &L.x, &L.r, &L.d0, &L.d1, &L.dj}) {
+    v->alloc(n, s);
+    v->zero();
+  }
+}
+
+// ---- Galerkin product P^T (A P), symmetrised (sparse.py:113-122)
+void galerkin(const DCsr& P, const DCsr& Pt, const DCsr& A, DCsr& out, cudaStream_t s) {
+  DCsr AP, M;
+  spgemm(A, P, AP, s);
+  spgemm(Pt, AP, M, s);
+  AP = DCsr();
+  symmetrize(M, out, s);
+}
+
+__global__ void k_asym(const int64_t* __restrict__ p, const int32_t* __restrict__ ix, const double* __restrict__ v,
+                       int64_t n, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t e = p[r]; e < p[r + 1]; ++e) {
+      const int32_t c = ix[e];
+      int64_t lo = p[c], hi = p[c + 1];
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (ix[mid] < r) lo = mid + 1; else hi = mid;
+      }
+      const double t = (lo < p[c + 1] && ix[lo] == r) ? v[lo] : 0.0;
+      m = fmax(m, fabs(v[e] - t));
+    }
+  }
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+__global__ void k_densify(const int64_t* __restrict__ p, const int32_t* __restrict__ ix, const double* __restrict__ v,
+                          int64_t n, double* __restrict__ D) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = p[r]; e < p[r + 1]; ++e) D[r + (int64_t)ix[e] * n] = v[e];  // column-major
+}
+
+__global__ void k_eye(double* D, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * n; i += (int64_t)gridDim.x * blockDim.x)
+    D[i] = (i % (n + 1) == 0) ? 1.0 : 0.0;
+}
+
+// Coarsest level: cholesky(A) (sparse.py:276-301) -> explicit inverse.
+void factor_coarsest(hcamg_handle* h, DevLevel& L, const DCsr& M) {
+  cudaStream_t s = h->stream;
+  const int64_t n = M.nrows;
+  require(M.nrows == M.ncols, "matrix must be square");
+  {
+    DBuf<unsigned long long> a(1, s);
+    a.zero();
+    if (n) k_asym<<<grid_for(n, 128), 128, 0, s>>>(M.ptr.p, M.idx.p, M.val.p, n, a.p);
+    HC_CHECK_LAUNCH();
+    unsigned long long ha = read_scalar(a.p, s);
+    double asym;
+    memcpy(&asym, &ha, 8);
+    const double scale = max_abs(M, s);
+    if (scale > 0 && asym > 1e-12 * scale) {
+      char buf[128];
+      snprintf(buf, sizeof buf, "matrix not symmetric: asymmetry %.3e", asym);
+      throw Error(ENOTSYM_, buf);
+    }
+  }
+  L.coarsest = true;
+  if (n == 0) return;
+  DBuf<double> D(n * n, s);
+  D.zero();
+  k_densify<<<grid_for(n, 128), 128, 0, s>>>(M.ptr.p, M.idx.p, M.val.p, n, D.p);
+  HC_CHECK_LAUNCH();
+  int64_t bad = dense_cholesky(h->cublas, D.p, n, n, s);
+  if (bad >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(bad) + ")", bad);
+  L.Ainv.alloc(n * n, s);
+  k_eye<<<grid_for(n * n, 256), 256, 0, s>>>(L.Ainv.p, n);
+  HC_CHECK_LAUNCH();
+  dense_cholesky_solve(h->cublas, D.p, n, n, L.Ainv.p, n, n, s);
+}
+
+void finish_level(hcamg_handle* h, DevLevel& L) {
+  cudaStream_t s = h->stream;
+  L.n = L.A.nrows;
+  alloc_level_vectors(L, s);
+  if (L.has_P) {
+    build_l1(L.A, L.l1, s);
+    build_smoother(L.A, L.G, L.sm, s);
+  }
+}
+
+struct RefChain {
+  int32_t nm = 0;
+  const int64_t* ne = nullptr;
+  const int64_t* const* edges = nullptr;
+  const int64_t* const* children = nullptr;
+  const int64_t* free_edges = nullptr;
+};
+
+void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, int method, int32_t max_levels,
+                     int64_t min_coarse, double theta, const RefChain* chain) {
+  cudaStream_t s = h->stream;
+  invalidate(h);
+  h->levels.clear();
+  h->lv.clear();
+  h->notes.clear();
+  h->stalled = false;
+  h->method = method;
+  require(Ah->nrows == Ah->ncols, "A must be square");
+  require(Gh->nrows == Ah->nrows, "G rows must match A");
+  HC_CUDA(cudaStreamSynchronize(s));
+  auto t0 = std::chrono::steady_clock::now();
+  auto cur = std::make_unique<DevLevel>();
+  upload_csr(Ah, cur->A, s);
+  upload_csr(Gh, cur->G, s);
+  int32_t pos = method == 0 ? chain->nm - 1 : 0;
+  std::vector<int64_t> e2d;
+  if (method == 0) e2d.assign(chain->free_edges, chain->free_edges + chain->ne[chain->nm - 1]);
+  while (true) {
+    const int64_t n = cur->A.nrows;
+    if (n <= min_coarse || (int64_t)h->levels.size() + 1 >= max_levels) break;
+    SplitResult sp;
+    int mode;
+    if (method == 0) {
+      if (pos == 0) {
+        if (n > min_coarse) {
+          h->stalled = true;
+          h->notes.push_back("mesh chain exhausted at " + std::to_string(n) + " DoFs");
+        }
+        break;
+      }
+      refinement_splitting(chain->edges[pos - 1], chain->ne[pos - 1], chain->edges[pos], chain->ne[pos],
+                           chain->children[pos - 1], e2d.data(), n, sp, s);
+      if (sp.n_pairs() == 0) {
+        h->stalled = true;
+        h->notes.push_back("refinement splitting produced no pairs");
+        break;
+      }
+      mode = 0;
+    } else {
+      algebraic_splitting(cur->A, cur->G, theta, sp, s);
+      if (sp.n_pairs() == 0 || sp.n_pairs() >= n) {
+        if (sp.n_pairs() == 0) {
+          h->stalled = true;
+          h->notes.push_back("algebraic coarsening found no pairs");
+        }
+        break;
+      }
+      mode = 1;
+    }
+    InterpResult ip;
+    build_interp(cur->A, cur->G, sp, mode, h->cublas, ip, s);
+    if (ip.P.ncols == 0 || ip.P.ncols >= n) {
+      h->stalled = true;
+      h->notes.push_back("no size reduction (" + std::to_string(n) + " -> " + std::to_string(ip.P.ncols) + ")");
+      break;
+    }
+    auto next = std::make_unique<DevLevel>();
+    galerkin(ip.P, ip.Pt, cur->A, next->A, s);
+    next->G = std::move(ip.Gc);
+    cur->has_P = true;
+    cur->P = std::move(ip.P);
+    cur->Pt = std::move(ip.Pt);
+    cur->gc_cols = ip.gc_cols;
+    if (method == 0) {
+      std::vector<int64_t> nx((size_t)chain->ne[pos - 1], -1);
+      for (size_t t = 0; t < sp.pair_mesh_edges.size(); ++t) nx[(size_t)sp.pair_mesh_edges[t]] = (int64_t)t;
+      e2d.swap(nx);
+      --pos;
+    }
+    cur->split = std::move(sp);
+    finish_level(h, *cur);
+    h->levels.push_back(std::move(cur));
+    cur = std::move(next);
+  }
+  factor_coarsest(h, *cur, cur->A);
+  finish_level(h, *cur);
+  h->levels.push_back(std::move(cur));
+  refresh_views(h);
+  HC_CUDA(cudaStreamSynchronize(s));
+  h->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+void fill_info(hcamg_handle* h, hcamg_info* info) {
+  if (!info) return;
+  info->depth = (int32_t)h->levels.size();
+  info->stalled = h->stalled;
+  info->method = h->method;
+  double tot = 0;
+  for (auto& l : h->levels) tot += (double)l->A.nnz;
+  info->operator_complexity = h->levels.empty() || h->levels[0]->A.nnz == 0 ? 0.0 : tot / (double)h->levels[0]->A.nnz;
+  info->setup_seconds = h->setup_seconds;
+}
+
+// ---- graphs
+
+void ensure_ws(hcamg_handle* h, int64_t maxit) {
+  const int64_t n = h->levels.empty() ? 0 : h->levels[0]->n;
+  const void* old[] = {h->ws.x.p, h->ws.hist.p, h->ws.ctl.p};
+  h->ws.ensure(n, std::max<int64_t>(maxit, 1), h->stream);
+  const void* now[] = {h->ws.x.p, h->ws.hist.p, h->ws.ctl.p};
+  if (memcmp(old, now, sizeof old) != 0) invalidate(h);
+}
+
+void build_loop_graph(hcamg_handle* h, Graph& G, bool pcg) {
+  cudaStream_t s = h->stream, s2 = h->aux;
+  Workspace& w = h->ws;
+  const double* b = w.b.p;
+  G.reset();
+  // try a single graph with a device-side WHILE loop
+  cudaGraph_t g = nullptr;
+  HC_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle cond;
+  cudaError_t ce = cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault);
+  if (ce == cudaSuccess) {
+    HC_CUDA(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    int64_t lp = pcg ? record_pcg_init(*h->lv[0], w, b, nullptr, s, 0) + record_pcg_first(h->lv, w, s)
+                     : record_amg_init(*h->lv[0], w, b, nullptr, s, 0);
+    cudaStreamCaptureStatus st;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    cudaGraph_t cg = nullptr;
+    HC_CUDA(cudaStreamGetCaptureInfo(s, &st, nullptr, &cg, &deps, &nd));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cn;
+    HC_CUDA(cudaGraphAddNode(&cn, cg, deps, nd, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    HC_CUDA(cudaStreamUpdateCaptureDependencies(s, &cn, 1, cudaStreamSetCaptureDependencies));
+    HC_CUDA(cudaStreamBeginCaptureToGraph(s2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    const unsigned long long hc = (unsigned long long)cond;
+    int64_t lb = pcg ? record_pcg_body(h->lv, w, s2, hc) : record_amg_body(h->lv, w, s2, hc);
+    HC_CUDA(cudaStreamEndCapture(s2, &body));
+    cudaGraph_t gout = nullptr;
+    HC_CUDA(cudaStreamEndCapture(s, &gout));
+    ce = cudaGraphInstantiate(&G.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ce == cudaSuccess) {
+      G.conditional = true;
+      G.launches_pre = lp;
+      G.launches_body = lb;
+      return;
+    }
+    cudaGetLastError();
+    G.exec = nullptr;
+  } else {
+    cudaGetLastError();
+    cudaGraphDestroy(g);
+  }
+  // fallback: host-driven loop over a body graph
+  cudaGraph_t gp = nullptr, gb = nullptr;
+  HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  G.launches_pre = pcg ? record_pcg_init(*h->lv[0], w, b, nullptr, s, 0) + record_pcg_first(h->lv, w, s)
+                       : record_amg_init(*h->lv[0], w, b, nullptr, s, 0);
+  HC_CUDA(cudaStreamEndCapture(s, &gp));
+  HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  G.launches_body = pcg ? record_pcg_body(h->lv, w, s, 0) : record_amg_body(h->lv, w, s, 0);
+  HC_CUDA(cudaStreamEndCapture(s, &gb));
+  HC_CUDA(cudaGraphInstantiate(&G.pre, gp, 0));
+  HC_CUDA(cudaGraphInstantiate(&G.body, gb, 0));
+  cudaGraphDestroy(gp);
+  cudaGraphDestroy(gb);
+  G.conditional = false;
+}
+
+void run_loop_graph(hcamg_handle* h, Graph& G) {
+  cudaStream_t s = h->stream;
+  if (G.conditional) {
+    HC_CUDA(cudaGraphLaunch(G.exec, s));
+    return;
+  }
+  HC_CUDA(cudaGraphLaunch(G.pre, s));
+  while (true) {
+    int stop = read_scalar(&h->ws.ctl.p->stop, s);
+    if (stop) break;
+    HC_CUDA(cudaGraphLaunch(G.body, s));
+  }
+}
+
+void set_ctl(hcamg_handle* h, double tol, int64_t maxit) {
+  Ctl c{};
+  c.tol = tol;
+  c.maxit = maxit;
+  HC_CUDA(cudaMemcpyAsync(h->ws.ctl.p, &c, sizeof(Ctl), cudaMemcpyHostToDevice, h->stream));
+}
+
+void require_hierarchy(hcamg_handle* h) {
+  require(!h->levels.empty(), "no hierarchy: call hcamg_setup_* first");
+}
+
+void prepare_loop(hcamg_handle* h, Graph& G, bool pcg, int64_t maxit) {
+  ensure_ws(h, maxit);
+  if (!(G.exec || G.pre)) build_loop_graph(h, G, pcg);
+}
+
+void read_report(hcamg_handle* h, hcamg_report* rep, int* error) {
+  Ctl c = read_scalar(h->ws.ctl.p, h->stream);
+  if (rep) {
+    rep->iterations = c.it;
+    rep->converged = c.converged;
+    rep->zero_rhs = c.zero_b;
+    rep->diverged = c.error == 3;
+    rep->final_relres = c.rel;
+  }
+  *error = c.error;
+}
+
+template <class F>
+int guarded(hcamg_handle* h, F&& f) {
+  if (!h) return HCAMG_EINVAL;
+  h->err.clear();
+  h->err_index = -1;
+  try {
+    HC_CUDA(cudaSetDevice(h->device));
+    f();
+    return HCAMG_OK;
+  } catch (const Error& e) {
+    h->err = e.what();
+    h->err_index = e.index;
+    cudaGetLastError();
+    return e.code;
+  } catch (const std::exception& e) {
+    h->err = e.what();
+    return HCAMG_ECUDA;
+  }
+}
+
+int pcg_breakdown(hcamg_handle* h, int error) {
+  if (error == kErrPAp) {
+    Ctl c = read_scalar(h->ws.ctl.p, h->stream);
+    char buf[160];
+    snprintf(buf, sizeof buf, "PCG breakdown: p^T A p = %.3e (non-SPD operator)", c.pAp);
+    throw Error(EBREAKDOWN_, buf);
+  }
+  if (error == kErrRz) throw Error(EBREAKDOWN_, "PCG breakdown: preconditioner is not SPD");
+  return 0;
+}
+
+}  // namespace
+
+// ============================================================================ C-ABI
+
+extern "C" {
+
+int hcamg_version(void) { return 1; }
+
+int hcamg_create(hcamg_handle** out, int device, void* cuda_stream) {
+  if (!out) return HCAMG_EINVAL;
+  auto* h = new hcamg_handle();
+  h->device = device;
+  try {
+    HC_CUDA(cudaSetDevice(device));
+    if (cuda_stream) {
+      h->stream = (cudaStream_t)cuda_stream;
+    } else {
+      HC_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      h->own_stream = true;
+    }
+    HC_CUDA(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
+    if (cublasCreate(&h->cublas) != CUBLAS_STATUS_SUCCESS) throw Error(ECUDA_, "cublasCreate failed");
+  } catch (const Error& e) {
+    fprintf(stderr, "hcamg_create: %s\n", e.what());
+    delete h;
+    *out = nullptr;
+    return e.code;
+  }
+  *out = h;
+  return HCAMG_OK;
+}
+
+void hcamg_destroy(hcamg_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  invalidate(h);
+  h->levels.clear();
+  h->pending.clear();
+  h->ws = Workspace();
+  h->vc_b.release();
+  h->vc_x.release();
+  cudaStreamSynchronize(h->stream);
+  if (h->cublas) cublasDestroy(h->cublas);
+  if (h->aux) cudaStreamDestroy(h->aux);
+  if (h->own_stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+const char* hcamg_last_error(const hcamg_handle* h) { return h ? h->err.c_str() : "null handle"; }
+int64_t hcamg_error_index(const hcamg_handle* h) { return h ? h->err_index : -1; }
+void* hcamg_stream(hcamg_handle* h) { return h ? (void*)h->stream : nullptr; }
+
+int hcamg_setup_alg(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* G, int32_t max_levels, int64_t min_coarse,
+                    double theta, hcamg_info* info) {
+  return guarded(h, [&] {
+    require(A && G, "A and G are required");
+    build_hierarchy(h, A, G, 1, max_levels, min_coarse, theta, nullptr);
+    fill_info(h, info);
+  });
+}
+
+int hcamg_setup_ref(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* G, int32_t n_meshes, const int64_t* ne,
+                    const int64_t* const* edges, const int64_t* const* children, const int64_t* free_edges,
+                    int32_t max_levels, int64_t min_coarse, hcamg_info* info) {
+  return guarded(h, [&] {
+    require(A && G, "A and G are required");
+    require(n_meshes >= 1 && ne && edges && free_edges && (n_meshes == 1 || children),
+            "method 'ref' requires the nested mesh chain");
+    RefChain c{n_meshes, ne, edges, children, free_edges};
+    build_hierarchy(h, A, G, 0, max_levels, min_coarse, 0.25, &c);
+    fill_info(h, info);
+  });
+}
+
+int hcamg_hier_begin(hcamg_handle* h) {
+  return guarded(h, [&] { h->pending.clear(); });
+}
+
+int hcamg_hier_push(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* G, const hcamg_csr* P) {
+  return guarded(h, [&] {
+    cudaStream_t s = h->stream;
+    auto L = std::make_unique<DevLevel>();
+    upload_csr(A, L->A, s);
+    require(L->A.nrows == L->A.ncols, "A must be square");
+    if (G) upload_csr(G, L->G, s);
+    else { L->G.alloc(L->A.nrows, 0, 0, s); L->G.ptr.zero(); }
+    if (P) {
+      require(P->nrows == A->nrows, "P rows must match A");
+      upload_csr(P, L->P, s);
+      csr_transpose(L->P, L->Pt, s);
+      L->has_P = true;
+    }
+    h->pending.push_back(std::move(L));
+  });
+}
+
+// Coarsest level of a user-assembled hierarchy: coarse_matrix (if given) is
+// the matrix whose Cholesky factor the user attached (Level.coarse_factor).
+int hcamg_hier_end_with(hcamg_handle* h, const hcamg_csr* coarse_matrix, hcamg_info* info) {
+  return guarded(h, [&] {
+    require(!h->pending.empty(), "empty hierarchy");
+    invalidate(h);
+    h->levels = std::move(h->pending);
+    h->pending.clear();
+    h->notes.clear();
+    h->stalled = false;
+    h->method = 2;
+    for (size_t i = 0; i + 1 < h->levels.size(); ++i)
+      require(h->levels[i]->has_P, "only the last level may lack P");
+    DevLevel& last = *h->levels.back();
+    last.has_P = false;
+    if (coarse_matrix) {
+      DCsr M;
+      upload_csr(coarse_matrix, M, h->stream);
+      factor_coarsest(h, last, M);
+    } else {
+      factor_coarsest(h, last, last.A);
+    }
+    for (auto& l : h->levels) finish_level(h, *l);
+    refresh_views(h);
+    HC_CUDA(cudaStreamSynchronize(h->stream));
+    fill_info(h, info);
+  });
+}
+
+int hcamg_hier_end(hcamg_handle* h, hcamg_info* info) { return hcamg_hier_end_with(h, nullptr, info); }
+
+int hcamg_info_get(hcamg_handle* h, hcamg_info* info) {
+  return guarded(h, [&] { fill_info(h, info); });
+}
+
+int hcamg_notes(hcamg_handle* h, char* buf, int64_t cap) {
+  return guarded(h, [&] {
+    std::string all;
+    for (size_t i = 0; i < h->notes.size(); ++i) all += (i ? "\n" : "") + h->notes[i];
+    if (buf && cap > 0) {
+      int64_t n = std::min<int64_t>(cap - 1, (int64_t)all.size());
+      memcpy(buf, all.data(), (size_t)n);
+      buf[n] = 0;
+    }
+  });
+}
+
+int hcamg_level(hcamg_handle* h, int32_t level, hcamg_level_info* o) {
+  return guarded(h, [&] {
+    require(level >= 0 && level < (int32_t)h->levels.size() && o, "level out of range");
+    DevLevel& L = *h->levels[(size_t)level];
+    memset(o, 0, sizeof *o);
+    o->n = L.n;
+    o->nnz_A = L.A.nnz;
+    o->ncols_G = L.G.ncols;
+    o->nnz_G = L.G.nnz;
+    o->nnz_P = L.has_P ? L.P.nnz : 0;
+    o->n_pairs = L.split.n_pairs();
+    o->n_interior = (int64_t)L.split.interior.size();
+    o->n_coarse_nodes = (int64_t)(h->method == 0 ? L.split.pair_mesh_edges.size() : L.split.coarse_nodes.size());
+    o->n_patches = L.sm.npatch;
+    o->n_patch_entries = L.sm.h_patch_dofs.size();
+    o->n_waves = L.sm.nwave;
+    o->n_gc_cols = (int64_t)L.gc_cols.size();
+    o->coarsest = L.coarsest;
+  });
+}
+
+int hcamg_export_csr(hcamg_handle* h, int32_t level, int32_t which, int64_t* indptr, int32_t* indices, double* data) {
+  return guarded(h, [&] {
+    require(level >= 0 && level < (int32_t)h->levels.size(), "level out of range");
+    DevLevel& L = *h->levels[(size_t)level];
+    const DCsr* M = which == 0 ? &L.A : which == 1 ? (L.has_P ? &L.P : nullptr) : &L.G;
+    require(M != nullptr, "level has no P");
+    cudaStream_t s = h->stream;
+    if (indptr) HC_CUDA(cudaMemcpyAsync(indptr, M->ptr.p, 8 * (M->nrows + 1), cudaMemcpyDeviceToHost, s));
+    if (M->nnz && indices) HC_CUDA(cudaMemcpyAsync(indices, M->idx.p, 4 * M->nnz, cudaMemcpyDeviceToHost, s));
+    if (M->nnz && data) HC_CUDA(cudaMemcpyAsync(data, M->val.p, 8 * M->nnz, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int hcamg_export_splitting(hcamg_handle* h, int32_t level, int64_t* pairs, int64_t* interior, int64_t* coarse_nodes) {
+  return guarded(h, [&] {
+    require(level >= 0 && level < (int32_t)h->levels.size(), "level out of range");
+    const SplitResult& sp = h->levels[(size_t)level]->split;
+    if (pairs && !sp.pairs.empty()) memcpy(pairs, sp.pairs.data(), 8 * sp.pairs.size());
+    if (interior && !sp.interior.empty()) memcpy(interior, sp.interior.data(), 8 * sp.interior.size());
+    const std::vector<int64_t>& cn = h->method == 0 ? sp.pair_mesh_edges : sp.coarse_nodes;
+    if (coarse_nodes && !cn.empty()) memcpy(coarse_nodes, cn.data(), 8 * cn.size());
+  });
+}
+
+int hcamg_export_l1(hcamg_handle* h, int32_t level, double* d) {
+  return guarded(h, [&] {
+    require(level >= 0 && level < (int32_t)h->levels.size(), "level out of range");
+    DevLevel& L = *h->levels[(size_t)level];
+    require(L.has_P, "coarsest level has no smoother");
+    HC_CUDA(cudaMemcpyAsync(d, L.l1.p, 8 * L.n, cudaMemcpyDeviceToHost, h->stream));
+    HC_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+int hcamg_export_patches(hcamg_handle* h, int32_t level, int64_t* ptr, int64_t* dofs, int64_t* wave) {
+  return guarded(h, [&] {
+    require(level >= 0 && level < (int32_t)h->levels.size(), "level out of range");
+    const Smoother& sm = h->levels[(size_t)level]->sm;
+    if (ptr) memcpy(ptr, sm.h_patch_ptr.data(), 8 * sm.h_patch_ptr.size());
+    if (dofs && !sm.h_patch_dofs.empty()) memcpy(dofs, sm.h_patch_dofs.data(), 8 * sm.h_patch_dofs.size());
+    if (wave) {
+      for (int64_t w = 0; w < sm.nwave; ++w)
+        for (int64_t t = sm.wave_ptr[(size_t)w]; t < sm.wave_ptr[(size_t)w + 1]; ++t) wave[sm.orig_of[(size_t)t]] = w;
+    }
+  });
+}
+
+int hcamg_export_coarse_cols(hcamg_handle* h, int32_t level, int64_t* cols) {
+  return guarded(h, [&] {
+    require(level >= 0 && level < (int32_t)h->levels.size(), "level out of range");
+    const auto& c = h->levels[(size_t)level]->gc_cols;
+    if (cols && !c.empty()) memcpy(cols, c.data(), 8 * c.size());
+  });
+}
+
+int hcamg_vcycle(hcamg_handle* h, const double* b, const double* x_or_null, double* out) {
+  return guarded(h, [&] {
+    require_hierarchy(h);
+    cudaStream_t s = h->stream;
+    const int64_t n = h->levels[0]->n;
+    ensure_ws(h, 1);
+    if (!h->g_vc.exec) {
+      cudaGraph_t g;
+      HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      h->g_vc.launches_pre = record_vcycle(h->lv, h->ws.r.p, h->ws.z.p, h->ws.zero_flag.p, s);
+      HC_CUDA(cudaStreamEndCapture(s, &g));
+      HC_CUDA(cudaGraphInstantiate(&h->g_vc.exec, g, 0));
+      cudaGraphDestroy(g);
+    }
+    HC_CUDA(cudaMemcpyAsync(h->ws.b.p, b, 8 * n, cudaMemcpyHostToDevice, s));
+    if (x_or_null) {
+      // out = x + V(b - A x)  (multilevel.py:196)
+      HC_CUDA(cudaMemcpyAsync(h->ws.x.p, x_or_null, 8 * n, cudaMemcpyHostToDevice, s));
+      set_ctl(h, 1.0, 1);
+      generic_init(h->levels[0]->A, h->ws, s);  // ws.r = b - A x
+    } else {
+      HC_CUDA(cudaMemcpyAsync(h->ws.r.p, h->ws.b.p, 8 * n, cudaMemcpyDeviceToDevice, s));
+    }
+    HC_CUDA(cudaGraphLaunch(h->g_vc.exec, s));
+    if (x_or_null) vec_add(n, h->ws.x.p, h->ws.z.p, h->ws.z.p, s);
+    HC_CUDA(cudaMemcpyAsync(out, h->ws.z.p, 8 * n, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+static int pcg_impl(hcamg_handle* h, const double* b, bool b_dev, const double* x0, bool x0_dev, double tol,
+                    int64_t maxit, double* x, bool x_dev, double* history, hcamg_report* report, bool sync) {
+  return guarded(h, [&] {
+    require_hierarchy(h);
+    require(tol > 0, "tolerance must be positive");
+    cudaStream_t s = h->stream;
+    const int64_t n = h->levels[0]->n;
+    prepare_loop(h, h->g_pcg, true, maxit);
+    HC_CUDA(cudaMemcpyAsync(h->ws.b.p, b, 8 * n, b_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    if (x0) HC_CUDA(cudaMemcpyAsync(h->ws.x.p, x0, 8 * n, x0_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    else h->ws.x.zero();
+    set_ctl(h, tol, maxit);
+    run_loop_graph(h, h->g_pcg);
+    HC_CUDA(cudaMemcpyAsync(x, h->ws.x.p, 8 * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    if (!sync && !report && !history) return;
+    int error = 0;
+    hcamg_report rep{};
+    read_report(h, &rep, &error);
+    pcg_breakdown(h, error);
+    if (rep.zero_rhs) {
+      if (x_dev) HC_CUDA(cudaMemsetAsync(x, 0, 8 * n, s));
+      else memset(x, 0, 8 * n);
+    }
+    if (history && rep.iterations)
+      HC_CUDA(cudaMemcpyAsync(history, h->ws.hist.p, 8 * rep.iterations, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+    if (report) *report = rep;
+  });
+}
+
+int hcamg_pcg(hcamg_handle* h, const double* b, const double* x0, double tol, int64_t maxit, double* x,
+              double* history, hcamg_report* report) {
+  return pcg_impl(h, b, false, x0, false, tol, maxit, x, false, history, report, true);
+}
+
+int hcamg_pcg_device(hcamg_handle* h, const double* d_b, const double* d_x0, double tol, int64_t maxit, double* d_x,
+                     hcamg_report* report) {
+  return pcg_impl(h, d_b, true, d_x0, true, tol, maxit, d_x, true, nullptr, report, report != nullptr);
+}
+
+int hcamg_amg_solve(hcamg_handle* h, const double* b, const double* x0, double tol, int64_t maxit, double* x,
+                    double* history, hcamg_report* report) {
+  return guarded(h, [&] {
+    require_hierarchy(h);
+    require(tol > 0, "tolerance must be positive");
+    cudaStream_t s = h->stream;
+    const int64_t n = h->levels[0]->n;
+    prepare_loop(h, h->g_amg, false, maxit);
+    HC_CUDA(cudaMemcpyAsync(h->ws.b.p, b, 8 * n, cudaMemcpyHostToDevice, s));
+    if (x0) HC_CUDA(cudaMemcpyAsync(h->ws.x.p, x0, 8 * n, cudaMemcpyHostToDevice, s));
+    else h->ws.x.zero();
+    set_ctl(h, tol, maxit);
+    run_loop_graph(h, h->g_amg);
+    HC_CUDA(cudaMemcpyAsync(x, h->ws.x.p, 8 * n, cudaMemcpyDeviceToHost, s));
+    int error = 0;
+    hcamg_report rep{};
+    read_report(h, &rep, &error);
+    if (rep.zero_rhs) memset(x, 0, 8 * n);
+    if (history && rep.iterations)
+      HC_CUDA(cudaMemcpyAsync(history, h->ws.hist.p, 8 * rep.iterations, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+    if (report) *report = rep;
+  });
+}
+
+int64_t hcamg_graph_launches(hcamg_handle* h, int32_t which) {
+  if (!h) return -1;
+  if (which == 0) return h->g_vc.launches_pre;
+  if (which == 1) return h->g_pcg.launches_pre;
+  if (which == 2) return h->g_pcg.launches_body;
+  if (which == 3) return h->g_amg.launches_pre;
+  if (which == 4) return h->g_amg.launches_body;
+  return -1;
+}
+
+int hcamg_spmv(hcamg_handle* h, const hcamg_csr* A, const double* x, double* y) {
+  return guarded(h, [&] {
+    cudaStream_t s = h->stream;
+    DCsr M;
+    upload_csr(A, M, s);
+    DBuf<double> dx(std::max<int64_t>(M.ncols, 1), s), dy(std::max<int64_t>(M.nrows, 1), s);
+    if (M.ncols) HC_CUDA(cudaMemcpyAsync(dx.p, x, 8 * M.ncols, cudaMemcpyHostToDevice, s));
+    dy.zero();
+    if (M.nrows) apply_operator(M, dx.p, dy.p, s);
+    if (M.nrows) HC_CUDA(cudaMemcpyAsync(y, dy.p, 8 * M.nrows, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int hcamg_pcg_generic(hcamg_handle* h, const hcamg_csr* A, const double* b, const double* x0, double tol,
+                      int64_t maxit, hcamg_precond_fn precond, void* ctx, double* x, double* history,
+                      hcamg_report* report) {
+  return guarded(h, [&] {
+    require(tol > 0, "tolerance must be positive");
+    require(A && A->nrows == A->ncols, "A must be square");
+    cudaStream_t s = h->stream;
+    DCsr M;
+    upload_csr(A, M, s);
+    const int64_t n = M.nrows;
+    Workspace& w = h->ws;
+    invalidate(h);
+    w.ensure(n, std::max<int64_t>(maxit, 1), s);
+    HC_CUDA(cudaMemcpyAsync(w.b.p, b, 8 * n, cudaMemcpyHostToDevice, s));
+    if (x0) HC_CUDA(cudaMemcpyAsync(w.x.p, x0, 8 * n, cudaMemcpyHostToDevice, s));
+    else w.x.zero();
+    set_ctl(h, tol, maxit);
+    generic_init(M, w, s);
+    Ctl c = read_scalar(w.ctl.p, s);
+    hcamg_report rep{};
+    std::vector<double> hr((size_t)n), hz((size_t)n);
+    auto call_precond = [&]() {
+      HC_CUDA(cudaMemcpyAsync(hr.data(), w.r.p, 8 * n, cudaMemcpyDeviceToHost, s));
+      HC_CUDA(cudaStreamSynchronize(s));
+      if (precond(hr.data(), hz.data(), n, ctx) != 0) throw Error(EINVAL_, "preconditioner callback failed");
+      HC_CUDA(cudaMemcpyAsync(w.z.p, hz.data(), 8 * n, cudaMemcpyHostToDevice, s));
+    };
+    if (!c.stop) {
+      call_precond();
+      generic_rz(w, true, s);
+      for (;;) {
+        generic_pap(M, w, s);
+        c = read_scalar(w.ctl.p, s);
+        if (c.error) break;
+        generic_update(w, s);
+        c = read_scalar(w.ctl.p, s);
+        if (c.stop) break;
+        call_precond();
+        generic_rz(w, false, s);
+        c = read_scalar(w.ctl.p, s);
+        if (c.error) break;
+        generic_p(w, s);
+      }
+    }
+    rep.iterations = c.it;
+    rep.converged = c.converged;
+    rep.zero_rhs = c.zero_b;
+    rep.final_relres = c.rel;
+    pcg_breakdown(h, c.error);
+    HC_CUDA(cudaMemcpyAsync(x, w.x.p, 8 * n, cudaMemcpyDeviceToHost, s));
+    if (history && c.it) HC_CUDA(cudaMemcpyAsync(history, w.hist.p, 8 * c.it, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+    if (rep.zero_rhs) memset(x, 0, 8 * n);
+    if (report) *report = rep;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// Shared device infrastructure for libhcamg: error plumbing, stream-ordered
+// device buffers, device CSR, and small launch helpers.  sm_100a only.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+namespace hcamg {
+
+// Status codes mirrored in include/hcamg.h.
+enum Status : int {
+  OK = 0,
+  EINVAL_ = -1,      // bad argument / shape -> ValueError
+  ENOTSPD_ = -2,     // Cholesky breakdown -> NotPositiveDefiniteError(pivot)
+  EBREAKDOWN_ = -3,  // PCG breakdown -> RuntimeError
+  ENOMEM_ = -4,
+  ECUDA_ = -5,
+  ENOTSYM_ = -6,     // coarsest symmetry check -> ValueError
+  EUNSUPPORTED_ = -7,
+};
+
+struct Error : std::runtime_error {
+  int code;
+  int64_t index;
+  Error(int c, const std::string& m, int64_t idx = -1) : std::runtime_error(m), code(c), index(idx) {}
+};
+
+#define HC_CUDA(x)                                                                          \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::hcamg::Error(e_ == cudaErrorMemoryAllocation ? ::hcamg::ENOMEM_ : ::hcamg::ECUDA_, \
+                           std::string(#x) + ": " + cudaGetErrorString(e_) + " @" __FILE__ ":" + \
+                               std::to_string(__LINE__));                                   \
+  } while (0)
+
+#define HC_CHECK_LAUNCH() HC_CUDA(cudaGetLastError())
+
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) throw Error(EINVAL_, msg);
+}
+
+// Stream-ordered device buffer (cudaMallocAsync pool).
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  int64_t n = 0;
+  cudaStream_t s = 0;
+  DBuf() = default;
+  DBuf(int64_t count, cudaStream_t st) { alloc(count, st); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(int64_t count, cudaStream_t st) {
+    release();
+    s = st;
+    n = count;
+    if (count > 0) HC_CUDA(cudaMallocAsync((void**)&p, sizeof(T) * (size_t)count, st));
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  void zero() { if (n) HC_CUDA(cudaMemsetAsync(p, 0, sizeof(T) * (size_t)n, s)); }
+  void fill_bytes(int v) { if (n) HC_CUDA(cudaMemsetAsync(p, v, sizeof(T) * (size_t)n, s)); }
+  void upload(const T* host, int64_t count) {
+    alloc(count, s);
+    if (count) HC_CUDA(cudaMemcpyAsync(p, host, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice, s));
+  }
+  void upload(const T* host, int64_t count, cudaStream_t st) { s = st; upload(host, count); }
+  std::vector<T> download() const {
+    std::vector<T> h((size_t)n);
+    if (n) {
+      HC_CUDA(cudaMemcpyAsync(h.data(), p, sizeof(T) * (size_t)n, cudaMemcpyDeviceToHost, s));
+      HC_CUDA(cudaStreamSynchronize(s));
+    }
+    return h;
+  }
+  T* get() const { return p; }
+};
+
+template <class T>
+inline T read_scalar(const T* dev, cudaStream_t s) {
+  T h;
+  HC_CUDA(cudaMemcpyAsync(&h, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
+  HC_CUDA(cudaStreamSynchronize(s));
+  return h;
+}
+
+// Device CSR: int64 row pointers, int32 column indices, fp64 values.
+struct DCsr {
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  DBuf<int64_t> ptr;
+  DBuf<int32_t> idx;
+  DBuf<double> val;
+  void alloc(int64_t r, int64_t c, int64_t z, cudaStream_t s) {
+    nrows = r; ncols = c; nnz = z;
+    ptr.alloc(r + 1, s);
+    idx.alloc(z, s);
+    val.alloc(z, s);
+  }
+};
+
+inline unsigned grid_for(int64_t work, int threads, int64_t cap = 148 * 32) {
+  int64_t g = (work + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+constexpr int kSMs = 148;
+
+}  // namespace hcamg

@@ -1,0 +1,215 @@
+// Dense SPD kernels (see dense.cuh).
+#include <cmath>
+#include <vector>
+
+#include "dense.cuh"
+
+namespace hcamg {
+
+namespace {
+
+constexpr int kSmallWarps = 4;
+
+// Reference breakdown rule given the pivots computed so far (j0 = index of the
+// first non-positive / non-finite pivot, or k if none).
+__device__ int64_t breakdown_index(const double* piv, int k, int j0, double floor_) {
+  if (j0 < k) {
+    for (int j = 0; j <= j0; ++j)
+      if (!(piv[j] > floor_) || !isfinite(piv[j])) return j;
+    return j0;
+  }
+  int am = -1;
+  double mn = INFINITY;
+  for (int j = 0; j < k; ++j)
+    if (piv[j] < mn) { mn = piv[j]; am = j; }
+  if (am >= 0 && mn <= floor_) return am;
+  return -1;
+}
+
+template <bool kInverse>
+__global__ void __launch_bounds__(32 * kSmallWarps) k_small_spd(const DenseJob* __restrict__ jobs, int64_t njobs,
+                                                                const double* __restrict__ A, double* __restrict__ B,
+                                                                double* __restrict__ piv, int64_t* __restrict__ status) {
+  __shared__ double T[kSmallWarps][32][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double(*t)[33] = T[w];
+  for (int64_t jb = (int64_t)blockIdx.x * kSmallWarps + w; jb < njobs; jb += (int64_t)gridDim.x * kSmallWarps) {
+    const DenseJob jobv = jobs[jb];
+    const int k = jobv.k;
+    const double* a = A + jobv.a_off;
+    double* pv = piv + jobv.piv_off;
+    for (int c = 0; c < k; ++c)
+      if (lane < k) t[lane][c] = a[lane + (int64_t)c * k];
+    __syncwarp();
+    double sc = lane < k ? fabs(t[lane][lane]) : 0.0;
+    for (int o = 16; o; o >>= 1) sc = fmax(sc, __shfl_xor_sync(0xffffffffu, sc, o));
+    const double floor_ = kPivotRtol * sc;
+    int j0 = k;
+    for (int j = 0; j < k; ++j) {
+      double d = t[j][j];
+      if (lane == 0) pv[j] = d;
+      if (!(d > 0.0) || !isfinite(d)) { j0 = j; break; }
+      double ljj = sqrt(d);
+      __syncwarp();
+      if (lane > j && lane < k) t[lane][j] = t[lane][j] / ljj;
+      if (lane == j) t[j][j] = ljj;
+      __syncwarp();
+      for (int l = j + 1; l < k; ++l)
+        if (lane >= l && lane < k) t[lane][l] = t[lane][l] - t[lane][j] * t[l][j];
+      __syncwarp();
+    }
+    __syncwarp();
+    int64_t bad = -1;
+    if (lane == 0) bad = breakdown_index(pv, k, j0, floor_);
+    bad = __shfl_sync(0xffffffffu, bad, 0);
+    if (lane == 0) status[jb] = bad;
+    if (bad >= 0) continue;
+    double* b = B + jobv.b_off;
+    const int nrhs = kInverse ? k : jobv.nrhs;
+    for (int c = lane; c < nrhs; c += 32) {
+      double y[32];
+      for (int i = 0; i < k; ++i) {
+        double v = kInverse ? (i == c ? 1.0 : 0.0) : b[i + (int64_t)c * k];
+        for (int p = 0; p < i; ++p) v -= t[i][p] * y[p];
+        y[i] = v / t[i][i];
+      }
+      for (int i = k - 1; i >= 0; --i) {
+        double v = y[i];
+        for (int p = i + 1; p < k; ++p) v -= t[p][i] * y[p];
+        y[i] = v / t[i][i];
+      }
+      for (int i = 0; i < k; ++i) b[i + (int64_t)c * k] = y[i];
+    }
+    __syncwarp();
+  }
+}
+
+constexpr int kTile = 96;
+constexpr int kTileThreads = 256;
+
+// Unblocked Cholesky of one nb x nb diagonal tile in shared memory.
+__global__ void __launch_bounds__(kTileThreads) k_potrf_tile(double* __restrict__ A, int64_t ld, int nb,
+                                                             double* __restrict__ piv, int* __restrict__ bad) {
+  extern __shared__ double T[];  // nb x (nb+1), row-major T[i*(nb+1)+j]
+  const int ldt = nb + 1;
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int i = e % nb, j = e / nb;
+    if (i >= j) T[i * ldt + j] = A[i + (int64_t)j * ld];
+  }
+  __syncthreads();
+  __shared__ int stop;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    double d = T[j * ldt + j];
+    if (threadIdx.x == 0) {
+      piv[j] = d;
+      if (!(d > 0.0) || !isfinite(d)) { stop = 1; *bad = j; }
+    }
+    __syncthreads();
+    if (stop) return;
+    double ljj = sqrt(d);
+    for (int i = j + 1 + threadIdx.x; i < nb; i += blockDim.x) T[i * ldt + j] /= ljj;
+    __syncthreads();
+    if (threadIdx.x == 0) T[j * ldt + j] = ljj;
+    for (int i = j + 1 + threadIdx.x; i < nb; i += blockDim.x) {
+      const double lij = T[i * ldt + j];
+      for (int l = j + 1; l <= i; ++l) T[i * ldt + l] -= lij * T[l * ldt + j];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int i = e % nb, j = e / nb;
+    if (i >= j) A[i + (int64_t)j * ld] = T[i * ldt + j];
+  }
+}
+
+__global__ void k_diag_absmax(const double* __restrict__ A, int64_t k, int64_t ld, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(A[i + i * ld]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+void cublas_check(cublasStatus_t st, const char* what) {
+  if (st != CUBLAS_STATUS_SUCCESS) throw Error(ECUDA_, std::string("cuBLAS failure in ") + what);
+}
+
+}  // namespace
+
+void batched_small_spd_solve(const DenseJob* d_jobs, int64_t njobs, double* A, double* B, double* piv,
+                             int64_t* status, cudaStream_t s) {
+  if (!njobs) return;
+  unsigned g = (unsigned)std::min<int64_t>((njobs + kSmallWarps - 1) / kSmallWarps, kSMs * 16);
+  k_small_spd<false><<<g, 32 * kSmallWarps, 0, s>>>(d_jobs, njobs, A, B, piv, status);
+  HC_CHECK_LAUNCH();
+}
+
+void batched_small_spd_inverse(const DenseJob* d_jobs, int64_t njobs, double* A, double* B, double* piv,
+                               int64_t* status, cudaStream_t s) {
+  if (!njobs) return;
+  unsigned g = (unsigned)std::min<int64_t>((njobs + kSmallWarps - 1) / kSmallWarps, kSMs * 16);
+  k_small_spd<true><<<g, 32 * kSmallWarps, 0, s>>>(d_jobs, njobs, A, B, piv, status);
+  HC_CHECK_LAUNCH();
+}
+
+int64_t dense_cholesky(cublasHandle_t h, double* A, int64_t k, int64_t ld, cudaStream_t s) {
+  if (k == 0) return -1;
+  cublas_check(cublasSetStream(h, s), "setStream");
+  DBuf<unsigned long long> mx(1, s);
+  mx.zero();
+  k_diag_absmax<<<grid_for(k, 256), 256, 0, s>>>(A, k, ld, mx.p);
+  HC_CHECK_LAUNCH();
+  DBuf<double> piv(k, s);
+  DBuf<int> bad(1, s);
+  bad.fill_bytes(0xff);
+  const size_t smem = sizeof(double) * kTile * (kTile + 1);
+  HC_CUDA(cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const double one = 1.0, mone = -1.0;
+  int64_t j0 = k;
+  for (int64_t kb = 0; kb < k; kb += kTile) {
+    const int nb = (int)std::min<int64_t>(kTile, k - kb);
+    double* Akk = A + kb + kb * ld;
+    k_potrf_tile<<<1, kTileThreads, smem, s>>>(Akk, ld, nb, piv.p + kb, bad.p);
+    HC_CHECK_LAUNCH();
+    int b = read_scalar(bad.p, s);
+    if (b >= 0) { j0 = kb + b; break; }
+    const int64_t rest = k - kb - nb;
+    if (rest > 0) {
+      double* A21 = Akk + nb;
+      double* A22 = A21 + nb * ld;
+      cublas_check(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
+                               (int)rest, nb, &one, Akk, (int)ld, A21, (int)ld), "dtrsm");
+      cublas_check(cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, (int)rest, nb, &mone, A21, (int)ld, &one,
+                               A22, (int)ld), "dsyrk");
+    }
+  }
+  unsigned long long hm = read_scalar(mx.p, s);
+  double scale;
+  memcpy(&scale, &hm, 8);
+  const double floor_ = kPivotRtol * scale;
+  std::vector<double> hp = piv.download();
+  if (j0 < k) {
+    for (int64_t j = 0; j <= j0; ++j)
+      if (!(hp[(size_t)j] > floor_) || !std::isfinite(hp[(size_t)j])) return j;
+    return j0;
+  }
+  int64_t am = 0;
+  for (int64_t j = 1; j < k; ++j)
+    if (hp[(size_t)j] < hp[(size_t)am]) am = j;
+  return hp[(size_t)am] <= floor_ ? am : -1;
+}
+
+void dense_cholesky_solve(cublasHandle_t h, const double* L, int64_t k, int64_t ld, double* B, int64_t nrhs,
+                          int64_t ldb, cudaStream_t s) {
+  if (k == 0 || nrhs == 0) return;
+  cublas_check(cublasSetStream(h, s), "setStream");
+  const double one = 1.0;
+  cublas_check(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)k,
+                           (int)nrhs, &one, L, (int)ld, B, (int)ldb), "dtrsm L");
+  cublas_check(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)k,
+                           (int)nrhs, &one, L, (int)ld, B, (int)ldb), "dtrsm L^T");
+}
+
+}  // namespace hcamg

@@ -1,0 +1,57 @@
+// Device-resident hierarchy: one DevLevel per AMG level, laid out for the
+// solve kernels.
+#pragma once
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "split.cuh"
+
+namespace hcamg {
+
+// OSS-l1 smoother data in wavefront order (smoothers.py:60-137).
+//
+// Patches are renumbered wave-major: wave w holds patches [wave_ptr[w],
+// wave_ptr[w+1]) of the reordered list; within a wave they are pairwise
+// non-conflicting (no DoF of one is A-coupled to a DoF of another), so a wave
+// is one parallel step of the multiplicative sweep.  The residual update of a
+// wave is applied lazily by the NEXT step as a gather ("pull"): a gather row
+// (w, u) lists A[u, j] for the DoFs j of wave w; rows inside a patch of the
+// next wave are pulled by that patch's warp, the others by generic threads.
+struct Smoother {
+  int64_t npatch = 0, nwave = 0, kmax = 0;
+  std::vector<int64_t> wave_ptr;        // host copy (launch geometry)
+  DBuf<int64_t> patch_ptr;              // reordered patches -> entries
+  DBuf<int32_t> patch_dofs;             // entry -> DoF
+  DBuf<int64_t> binv_off;               // reordered patch -> offset of its k x k inverse
+  DBuf<double> binv;                    // column-major inverses
+  std::vector<int64_t> orig_of;         // reordered patch -> reference patch id
+  // gather rows
+  DBuf<int64_t> grow_ptr;
+  DBuf<int32_t> grow_u, gcol;
+  DBuf<double> gval;
+  DBuf<int32_t> own_fw, own_bw;         // per entry: gather row pulled before the patch solve (-1: none)
+  DBuf<int32_t> gen_fw, gen_bw;         // generic gather rows, grouped by source wave
+  std::vector<int64_t> gen_fw_ptr, gen_bw_ptr;  // per source wave offsets (host)
+  DBuf<int32_t> last_row;               // per DoF: gather row of the last wave (-1: none)
+  DBuf<uint8_t> in_first;               // per DoF: member of a wave-0 patch
+  // host copies for export (reference PatchSet layout, original patch order)
+  std::vector<int64_t> h_patch_ptr, h_patch_dofs;
+};
+
+struct DevLevel {
+  int64_t n = 0;
+  DCsr A, G;
+  bool has_P = false;
+  DCsr P, Pt;
+  DBuf<double> l1;
+  Smoother sm;
+  SplitResult split;     // diagnostics (pairs / interior / c_G)
+  std::vector<int64_t> gc_cols;
+  bool coarsest = false;
+  DBuf<double> Ainv;     // coarsest: dense inverse (row-major n x n)
+  // work vectors
+  DBuf<double> b, x, r, d0, d1, dj;
+};
+
+}  // namespace hcamg

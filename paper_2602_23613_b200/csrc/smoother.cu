@@ -1,0 +1,427 @@
+// OSS-l1 smoother setup on the GPU (hcurl_amg/smoothers.py:50-95):
+//   * vertex patches read off the level gradient (column v of G), singletons
+//     for uncovered DoFs (smoothers.py:60-76);
+//   * explicit inverses of the patch blocks A[patch, patch] (smoothers.py:78-89;
+//     breakdown -> NotPositiveDefiniteError(pivot, "singular patch block id"));
+//   * the wavefront schedule that reproduces the multiplicative sweep order
+//     exactly: patch q waits for every earlier patch p with
+//     patch_q ∩ upd_p ≠ ∅ or upd_q ∩ patch_p ≠ ∅ (smoothers.py:98-103);
+//   * gather ("pull") lists for the lazily applied residual updates;
+//   * the l1 diagonal d_i = sum_j |a_ij| (smoothers.py:50-52).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "dense.cuh"
+#include "smoother.cuh"
+
+namespace hcamg {
+
+namespace {
+
+__global__ void k_nonempty(const int64_t* __restrict__ p, int64_t n, int64_t* __restrict__ f, int want_empty) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool ne = p[i + 1] > p[i];
+    f[i] = want_empty ? !ne : ne;
+  }
+}
+
+__global__ void k_patch_sizes(const int64_t* __restrict__ gtp, const int64_t* __restrict__ vcols, int64_t nv,
+                              int64_t m, int64_t* __restrict__ sz) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+    sz[t] = t < nv ? gtp[vcols[t] + 1] - gtp[vcols[t]] : 1;
+}
+
+__global__ void k_patch_fill(const int64_t* __restrict__ gtp, const int32_t* __restrict__ gti,
+                             const int64_t* __restrict__ vcols, int64_t nv, const int64_t* __restrict__ singles,
+                             int64_t m, const int64_t* __restrict__ pp, int32_t* __restrict__ dofs) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t o = pp[t];
+    if (t < nv) {
+      int64_t c = vcols[t];
+      for (int64_t e = gtp[c]; e < gtp[c + 1]; ++e) dofs[o++] = gti[e];
+    } else {
+      dofs[o] = (int32_t)singles[t - nv];
+    }
+  }
+}
+
+__global__ void k_patch_blocks(const int64_t* __restrict__ ap, const int32_t* __restrict__ ai,
+                               const double* __restrict__ av, const int64_t* __restrict__ pp,
+                               const int32_t* __restrict__ dofs, int64_t m, const int64_t* __restrict__ boff,
+                               double* __restrict__ blk) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p0 = pp[t], k = pp[t + 1] - p0;
+    double* B = blk + boff[t];
+    for (int64_t a = 0; a < k; ++a) {
+      const int32_t i = dofs[p0 + a];
+      int64_t b = 0;
+      for (int64_t e = ap[i]; e < ap[i + 1]; ++e) {
+        const int32_t j = ai[e];
+        while (b < k && dofs[p0 + b] < j) ++b;
+        if (b == k) break;
+        if (dofs[p0 + b] == j) B[a + b * k] = av[e];
+      }
+    }
+  }
+}
+
+__global__ void k_jobs(const int64_t* __restrict__ pp, const int64_t* __restrict__ boff, int64_t m,
+                       DenseJob* __restrict__ jobs) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+    int32_t k = (int32_t)(pp[t + 1] - pp[t]);
+    jobs[t] = DenseJob{boff[t], boff[t], pp[t], k, k};
+  }
+}
+
+__global__ void k_sq(const int64_t* __restrict__ pp, int64_t m, int64_t* __restrict__ o) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t k = pp[t + 1] - pp[t];
+    o[t] = k * k;
+  }
+}
+
+// Sequential wavefront levels (one warp walks the patches in reference order).
+__global__ void k_wave_levels(const int64_t* __restrict__ pp, const int32_t* __restrict__ dofs, int64_t m,
+                              const int64_t* __restrict__ atp, const int32_t* __restrict__ ati, int* lastU,
+                              int* lastP, int32_t* __restrict__ level) {
+  const int lane = threadIdx.x;
+  for (int64_t q = 0; q < m; ++q) {
+    const int64_t p0 = pp[q], p1 = pp[q + 1];
+    int lv = 0;
+    for (int64_t e = p0; e < p1; ++e) {
+      const int32_t i = dofs[e];
+      if (lane == 0) lv = max(lv, lastU[i] + 1);
+      for (int64_t f = atp[i] + lane; f < atp[i + 1]; f += 32) lv = max(lv, lastP[ati[f]] + 1);
+    }
+    for (int o = 16; o; o >>= 1) lv = max(lv, __shfl_xor_sync(0xffffffffu, lv, o));
+    __syncwarp();
+    for (int64_t e = p0; e < p1; ++e) {
+      const int32_t i = dofs[e];
+      if (lane == 0) atomicMax(&lastP[i], lv);
+      for (int64_t f = atp[i] + lane; f < atp[i + 1]; f += 32) atomicMax(&lastU[ati[f]], lv);
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) level[q] = lv;
+  }
+}
+
+__global__ void k_fill_int(int* v, int64_t n, int x) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] = x;
+}
+
+__global__ void k_iota_i32(int32_t* v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] = (int32_t)i;
+}
+
+__global__ void k_reorder_sizes(const int32_t* __restrict__ order, const int64_t* __restrict__ pp, int64_t m,
+                                int64_t* __restrict__ sz, int64_t* __restrict__ sq) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t k = pp[order[t] + 1] - pp[order[t]];
+    sz[t] = k;
+    sq[t] = k * k;
+  }
+}
+
+__global__ void k_reorder_fill(const int32_t* __restrict__ order, const int64_t* __restrict__ pp,
+                               const int32_t* __restrict__ dofs, const int64_t* __restrict__ boff,
+                               const double* __restrict__ binv, int64_t m, const int64_t* __restrict__ npp,
+                               const int64_t* __restrict__ nboff, int32_t* __restrict__ ndofs,
+                               double* __restrict__ nbinv, const int32_t* __restrict__ level,
+                               unsigned long long* __restrict__ mkeys, int32_t* __restrict__ mvals) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t q = order[t];
+    const int64_t k = pp[q + 1] - pp[q];
+    const unsigned long long w = (unsigned long long)(uint32_t)level[q];
+    for (int64_t a = 0; a < k; ++a) {
+      const int32_t dof = dofs[pp[q] + a];
+      ndofs[npp[t] + a] = dof;
+      mkeys[npp[t] + a] = (w << 32) | (uint32_t)dof;
+      mvals[npp[t] + a] = (int32_t)(npp[t] + a);
+    }
+    for (int64_t e = 0; e < k * k; ++e) nbinv[nboff[t] + e] = binv[boff[q] + e];
+  }
+}
+
+__global__ void k_entry_wave(const int64_t* __restrict__ npp, const int32_t* __restrict__ order,
+                             const int32_t* __restrict__ level, int64_t m, int32_t* __restrict__ ewave) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m; t += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = npp[t]; e < npp[t + 1]; ++e) ewave[e] = level[order[t]];
+}
+
+__global__ void k_trip_count(const int32_t* __restrict__ ndofs, int64_t ne, const int64_t* __restrict__ atp,
+                             int64_t* __restrict__ cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t j = ndofs[e];
+    cnt[e] = atp[j + 1] - atp[j];
+  }
+}
+
+__global__ void k_trip_fill(const int32_t* __restrict__ ndofs, const int32_t* __restrict__ ewave, int64_t ne,
+                            const int64_t* __restrict__ atp, const int32_t* __restrict__ ati,
+                            const double* __restrict__ atv, const int64_t* __restrict__ toff,
+                            unsigned long long* __restrict__ tkeys, int32_t* __restrict__ tcol,
+                            double* __restrict__ tval, int32_t* __restrict__ tid) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = ndofs[e];
+    const unsigned long long w = (unsigned long long)(uint32_t)ewave[e];
+    int64_t o = toff[e];
+    for (int64_t f = atp[j]; f < atp[j + 1]; ++f, ++o) {
+      tkeys[o] = (w << 32) | (uint32_t)ati[f];  // row u = ati[f], value A[u, j] = atv[f]
+      tcol[o] = j;
+      tval[o] = atv[f];
+      tid[o] = (int32_t)o;
+    }
+  }
+}
+
+__global__ void k_trip_gather(const int32_t* __restrict__ perm, const int32_t* __restrict__ tcol,
+                              const double* __restrict__ tval, int64_t nt, int32_t* __restrict__ gcol,
+                              double* __restrict__ gval) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nt; t += (int64_t)gridDim.x * blockDim.x) {
+    gcol[t] = tcol[perm[t]];
+    gval[t] = tval[perm[t]];
+  }
+}
+
+__device__ __forceinline__ int64_t find_key(const unsigned long long* __restrict__ keys, int64_t n,
+                                            unsigned long long k) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (keys[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  return (lo < n && keys[lo] == k) ? lo : -1;
+}
+
+// Classify gather rows (w, u) for both sweep directions.
+__global__ void k_classify(const unsigned long long* __restrict__ gkeys, int64_t ng,
+                           const unsigned long long* __restrict__ mkeys, const int32_t* __restrict__ mvals,
+                           int64_t nm, int64_t nwave, int32_t* __restrict__ own_fw, int32_t* __restrict__ own_bw,
+                           int64_t* __restrict__ gen_fw_flag, int64_t* __restrict__ gen_bw_flag,
+                           int32_t* __restrict__ last_row, int32_t* __restrict__ grow_u) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < ng; r += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long key = gkeys[r];
+    const int64_t w = (int64_t)(key >> 32);
+    const uint32_t u = (uint32_t)(key & 0xffffffffull);
+    grow_u[r] = (int32_t)u;
+    gen_fw_flag[r] = 0;
+    gen_bw_flag[r] = 0;
+    if (w + 1 < nwave) {
+      int64_t at = find_key(mkeys, nm, ((unsigned long long)(w + 1) << 32) | u);
+      if (at >= 0) own_fw[mvals[at]] = (int32_t)r; else gen_fw_flag[r] = 1;
+    } else {
+      last_row[u] = (int32_t)r;
+    }
+    if (w >= 1) {
+      int64_t at = find_key(mkeys, nm, ((unsigned long long)(w - 1) << 32) | u);
+      if (at >= 0) own_bw[mvals[at]] = (int32_t)r; else gen_bw_flag[r] = 1;
+    }
+  }
+}
+
+__global__ void k_to_i32(const int64_t* __restrict__ a, int64_t n, int32_t* __restrict__ o) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = (int32_t)a[i];
+}
+
+__global__ void k_wave_hist(const unsigned long long* __restrict__ gkeys, const int64_t* __restrict__ list,
+                            int64_t n, int64_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd((unsigned long long*)&cnt[gkeys[list[i]] >> 32], 1ull);
+}
+
+__global__ void k_in_first(const unsigned long long* __restrict__ mkeys, int64_t nm, uint8_t* __restrict__ f) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nm; i += (int64_t)gridDim.x * blockDim.x)
+    if ((mkeys[i] >> 32) == 0) f[mkeys[i] & 0xffffffffull] = 1;
+}
+
+__global__ void k_l1(const int64_t* __restrict__ ap, const double* __restrict__ av, int64_t n, double* __restrict__ d) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t e = ap[r]; e < ap[r + 1]; ++e) s = __dadd_rn(s, fabs(av[e]));
+    d[r] = s;
+  }
+}
+
+}  // namespace
+
+void build_l1(const DCsr& A, DBuf<double>& l1, cudaStream_t s) {
+  l1.alloc(A.nrows, s);
+  if (A.nrows) k_l1<<<grid_for(A.nrows, 256), 256, 0, s>>>(A.ptr.p, A.val.p, A.nrows, l1.p);
+  HC_CHECK_LAUNCH();
+}
+
+void build_smoother(const DCsr& A, const DCsr& G, Smoother& sm, cudaStream_t s) {
+  const int64_t n = A.nrows;
+  require(G.nrows == n, "smoother: gradient rows do not match the operator");
+  DCsr GT, AT;
+  csr_transpose(G, GT, s);
+  csr_transpose(A, AT, s);
+  // ---- patches in reference order
+  DBuf<int64_t> fcol(std::max<int64_t>(G.ncols, 1), s), frow(std::max<int64_t>(n, 1), s);
+  if (G.ncols) k_nonempty<<<grid_for(G.ncols, 256), 256, 0, s>>>(GT.ptr.p, G.ncols, fcol.p, 0);
+  if (n) k_nonempty<<<grid_for(n, 256), 256, 0, s>>>(G.ptr.p, n, frow.p, 1);
+  HC_CHECK_LAUNCH();
+  DBuf<int64_t> vcols, singles;
+  const int64_t nv = compact_flags(fcol.p, G.ncols, vcols, s);
+  const int64_t nsg = compact_flags(frow.p, n, singles, s);
+  const int64_t m = nv + nsg;
+  sm.npatch = m;
+  DBuf<int64_t> sz(std::max<int64_t>(m, 1), s), pp(m + 1, s);
+  if (m) k_patch_sizes<<<grid_for(m, 256), 256, 0, s>>>(GT.ptr.p, vcols.p, nv, m, sz.p);
+  HC_CHECK_LAUNCH();
+  const int64_t ne = exclusive_scan(sz.p, pp.p, m, s);
+  DBuf<int32_t> dofs(std::max<int64_t>(ne, 1), s);
+  if (m) k_patch_fill<<<grid_for(m, 256), 256, 0, s>>>(GT.ptr.p, GT.idx.p, vcols.p, nv, singles.p, m, pp.p, dofs.p);
+  HC_CHECK_LAUNCH();
+  sm.h_patch_ptr = pp.download();
+  {
+    std::vector<int32_t> hd = dofs.download();
+    sm.h_patch_dofs.assign(hd.begin(), hd.begin() + ne);
+  }
+  sm.kmax = 0;
+  for (int64_t t = 0; t < m; ++t) sm.kmax = std::max(sm.kmax, sm.h_patch_ptr[(size_t)t + 1] - sm.h_patch_ptr[(size_t)t]);
+  if (sm.kmax > 32) throw Error(EUNSUPPORTED_, "patch with more than 32 DoFs (" + std::to_string(sm.kmax) + ")");
+  // ---- patch inverses (reference order)
+  DBuf<int64_t> sq(std::max<int64_t>(m, 1), s), boff(m + 1, s);
+  if (m) k_sq<<<grid_for(m, 256), 256, 0, s>>>(pp.p, m, sq.p);
+  HC_CHECK_LAUNCH();
+  const int64_t nb = exclusive_scan(sq.p, boff.p, m, s);
+  DBuf<double> blk(std::max<int64_t>(nb, 1), s), binv(std::max<int64_t>(nb, 1), s), piv(std::max<int64_t>(ne, 1), s);
+  blk.zero();
+  DBuf<DenseJob> jobs(std::max<int64_t>(m, 1), s);
+  DBuf<int64_t> status(std::max<int64_t>(m, 1), s);
+  if (m) {
+    k_patch_blocks<<<grid_for(m, 128), 128, 0, s>>>(A.ptr.p, A.idx.p, A.val.p, pp.p, dofs.p, m, boff.p, blk.p);
+    k_jobs<<<grid_for(m, 256), 256, 0, s>>>(pp.p, boff.p, m, jobs.p);
+    HC_CHECK_LAUNCH();
+    batched_small_spd_inverse(jobs.p, m, blk.p, binv.p, piv.p, status.p, s);
+    std::vector<int64_t> hs = status.download();
+    for (int64_t t = 0; t < m; ++t)
+      if (hs[(size_t)t] >= 0)
+        throw Error(ENOTSPD_, "singular patch block " + std::to_string(t), hs[(size_t)t]);
+  }
+  blk.release();
+  // ---- wavefront levels
+  DBuf<int> lastU(std::max<int64_t>(n, 1), s), lastP(std::max<int64_t>(n, 1), s);
+  DBuf<int32_t> level(std::max<int64_t>(m, 1), s);
+  if (n) {
+    k_fill_int<<<grid_for(n, 256), 256, 0, s>>>(lastU.p, n, -1);
+    k_fill_int<<<grid_for(n, 256), 256, 0, s>>>(lastP.p, n, -1);
+  }
+  if (m) k_wave_levels<<<1, 32, 0, s>>>(pp.p, dofs.p, m, AT.ptr.p, AT.idx.p, lastU.p, lastP.p, level.p);
+  HC_CHECK_LAUNCH();
+  // ---- reorder wave-major (stable in reference order)
+  DBuf<int32_t> iota(std::max<int64_t>(m, 1), s), order(std::max<int64_t>(m, 1), s), slev(std::max<int64_t>(m, 1), s);
+  if (m) {
+    k_iota_i32<<<grid_for(m, 256), 256, 0, s>>>(iota.p, m);
+    HC_CHECK_LAUNCH();
+    size_t bytes = 0;
+    HC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, level.p, slev.p, iota.p, order.p, m, 0, 32, s));
+    DBuf<unsigned char> ws((int64_t)bytes + 1, s);
+    HC_CUDA(cub::DeviceRadixSort::SortPairs(ws.p, bytes, level.p, slev.p, iota.p, order.p, m, 0, 32, s));
+  }
+  std::vector<int32_t> hslev = slev.download();
+  std::vector<int32_t> horder = order.download();
+  sm.nwave = m ? (int64_t)hslev[(size_t)m - 1] + 1 : 0;
+  sm.wave_ptr.assign((size_t)sm.nwave + 1, 0);
+  for (int64_t t = 0; t < m; ++t) sm.wave_ptr[(size_t)hslev[(size_t)t] + 1]++;
+  for (int64_t w = 0; w < sm.nwave; ++w) sm.wave_ptr[(size_t)w + 1] += sm.wave_ptr[(size_t)w];
+  sm.orig_of.assign(horder.begin(), horder.begin() + m);
+  DBuf<int64_t> nsz(std::max<int64_t>(m, 1), s), nsq(std::max<int64_t>(m, 1), s);
+  sm.patch_ptr.alloc(m + 1, s);
+  sm.binv_off.alloc(m + 1, s);
+  if (m) k_reorder_sizes<<<grid_for(m, 256), 256, 0, s>>>(order.p, pp.p, m, nsz.p, nsq.p);
+  HC_CHECK_LAUNCH();
+  exclusive_scan(nsz.p, sm.patch_ptr.p, m, s);
+  exclusive_scan(nsq.p, sm.binv_off.p, m, s);
+  sm.patch_dofs.alloc(std::max<int64_t>(ne, 1), s);
+  sm.binv.alloc(std::max<int64_t>(nb, 1), s);
+  DBuf<unsigned long long> mkeys_in(std::max<int64_t>(ne, 1), s), mkeys(std::max<int64_t>(ne, 1), s);
+  DBuf<int32_t> mvals_in(std::max<int64_t>(ne, 1), s), mvals(std::max<int64_t>(ne, 1), s);
+  if (m)
+    k_reorder_fill<<<grid_for(m, 128), 128, 0, s>>>(order.p, pp.p, dofs.p, boff.p, binv.p, m, sm.patch_ptr.p,
+                                                    sm.binv_off.p, sm.patch_dofs.p, sm.binv.p, level.p, mkeys_in.p,
+                                                    mvals_in.p);
+  HC_CHECK_LAUNCH();
+  binv.release();
+  // membership (wave, dof) -> entry, sorted
+  if (ne) {
+    size_t bytes = 0;
+    HC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, mkeys_in.p, mkeys.p, mvals_in.p, mvals.p, ne, 0, 64, s));
+    DBuf<unsigned char> ws((int64_t)bytes + 1, s);
+    HC_CUDA(cub::DeviceRadixSort::SortPairs(ws.p, bytes, mkeys_in.p, mkeys.p, mvals_in.p, mvals.p, ne, 0, 64, s));
+  }
+  // ---- gather triples (w, u, j, A[u, j]) over every patch entry
+  DBuf<int32_t> ewave(std::max<int64_t>(ne, 1), s);
+  if (m) k_entry_wave<<<grid_for(m, 256), 256, 0, s>>>(sm.patch_ptr.p, order.p, level.p, m, ewave.p);
+  DBuf<int64_t> tcnt(std::max<int64_t>(ne, 1), s), toff(ne + 1, s);
+  if (ne) k_trip_count<<<grid_for(ne, 256), 256, 0, s>>>(sm.patch_dofs.p, ne, AT.ptr.p, tcnt.p);
+  HC_CHECK_LAUNCH();
+  const int64_t nt = exclusive_scan(tcnt.p, toff.p, ne, s);
+  require(nt < (int64_t(1) << 31), "smoother gather lists exceed int32 indexing");
+  DBuf<unsigned long long> tkeys(std::max<int64_t>(nt, 1), s), skeys(std::max<int64_t>(nt, 1), s);
+  DBuf<int32_t> tcol(std::max<int64_t>(nt, 1), s), tid(std::max<int64_t>(nt, 1), s), perm(std::max<int64_t>(nt, 1), s);
+  DBuf<double> tval(std::max<int64_t>(nt, 1), s);
+  if (ne) k_trip_fill<<<grid_for(ne, 128), 128, 0, s>>>(sm.patch_dofs.p, ewave.p, ne, AT.ptr.p, AT.idx.p, AT.val.p,
+                                                       toff.p, tkeys.p, tcol.p, tval.p, tid.p);
+  HC_CHECK_LAUNCH();
+  if (nt) {
+    size_t bytes = 0;
+    HC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, tkeys.p, skeys.p, tid.p, perm.p, nt, 0, 64, s));
+    DBuf<unsigned char> ws((int64_t)bytes + 1, s);
+    HC_CUDA(cub::DeviceRadixSort::SortPairs(ws.p, bytes, tkeys.p, skeys.p, tid.p, perm.p, nt, 0, 64, s));
+  }
+  sm.gcol.alloc(std::max<int64_t>(nt, 1), s);
+  sm.gval.alloc(std::max<int64_t>(nt, 1), s);
+  if (nt) k_trip_gather<<<grid_for(nt, 256), 256, 0, s>>>(perm.p, tcol.p, tval.p, nt, sm.gcol.p, sm.gval.p);
+  HC_CHECK_LAUNCH();
+  // run-length encode the sorted keys -> gather rows
+  DBuf<unsigned long long> gkeys(std::max<int64_t>(nt, 1), s);
+  DBuf<int64_t> gcnt(std::max<int64_t>(nt, 1), s), ngr(1, s);
+  ngr.zero();
+  if (nt) {
+    size_t bytes = 0;
+    HC_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, bytes, skeys.p, gkeys.p, gcnt.p, ngr.p, nt, s));
+    DBuf<unsigned char> ws((int64_t)bytes + 1, s);
+    HC_CUDA(cub::DeviceRunLengthEncode::Encode(ws.p, bytes, skeys.p, gkeys.p, gcnt.p, ngr.p, nt, s));
+  }
+  const int64_t ng = read_scalar(ngr.p, s);
+  sm.grow_ptr.alloc(ng + 1, s);
+  exclusive_scan(gcnt.p, sm.grow_ptr.p, ng, s);
+  sm.grow_u.alloc(std::max<int64_t>(ng, 1), s);
+  sm.own_fw.alloc(std::max<int64_t>(ne, 1), s);
+  sm.own_bw.alloc(std::max<int64_t>(ne, 1), s);
+  sm.last_row.alloc(std::max<int64_t>(n, 1), s);
+  sm.own_fw.fill_bytes(0xff);
+  sm.own_bw.fill_bytes(0xff);
+  sm.last_row.fill_bytes(0xff);
+  DBuf<int64_t> gff(std::max<int64_t>(ng, 1), s), gbf(std::max<int64_t>(ng, 1), s);
+  if (ng)
+    k_classify<<<grid_for(ng, 256), 256, 0, s>>>(gkeys.p, ng, mkeys.p, mvals.p, ne, sm.nwave, sm.own_fw.p,
+                                                 sm.own_bw.p, gff.p, gbf.p, sm.last_row.p, sm.grow_u.p);
+  HC_CHECK_LAUNCH();
+  for (int dir = 0; dir < 2; ++dir) {
+    DBuf<int64_t> lst;
+    const int64_t cnt = compact_flags(dir == 0 ? gff.p : gbf.p, ng, lst, s);
+    DBuf<int64_t> wh(std::max<int64_t>(sm.nwave, 1), s), wp(sm.nwave + 1, s);
+    wh.zero();
+    if (cnt) k_wave_hist<<<grid_for(cnt, 256), 256, 0, s>>>(gkeys.p, lst.p, cnt, wh.p);
+    HC_CHECK_LAUNCH();
+    exclusive_scan(wh.p, wp.p, sm.nwave, s);
+    DBuf<int32_t>& out = dir == 0 ? sm.gen_fw : sm.gen_bw;
+    out.alloc(std::max<int64_t>(cnt, 1), s);
+    if (cnt) k_to_i32<<<grid_for(cnt, 256), 256, 0, s>>>(lst.p, cnt, out.p);
+    HC_CHECK_LAUNCH();
+    (dir == 0 ? sm.gen_fw_ptr : sm.gen_bw_ptr) = wp.download();
+  }
+  sm.in_first.alloc(std::max<int64_t>(n, 1), s);
+  sm.in_first.zero();
+  if (ne) k_in_first<<<grid_for(ne, 256), 256, 0, s>>>(mkeys.p, ne, sm.in_first.p);
+  HC_CHECK_LAUNCH();
+  HC_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace hcamg

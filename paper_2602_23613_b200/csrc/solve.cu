@@ -1,0 +1,714 @@
+// Solve-phase kernels and their recording into CUDA graphs.
+//
+// V(1,1) cycle (multilevel.py:177-196) per non-coarsest level:
+//   forward OSS-l1 (smoothers.py:112-137, x = 0): one k_wave launch per
+//     wavefront of the multiplicative patch sweep, then the l1-Jacobi step as
+//     k_fw_final (applies the last wave's pending update, d = r / l1, x += d)
+//     and an SpMV-update r -= A d;
+//   restriction b_c = P^T r (maintained residual; the reference recomputes
+//     b - A x, the same vector up to roundoff);
+//   recursion, prolongation x += P x_c;
+//   backward OSS-l1: r = b - A x fused with d = r / l1, then r -= A d and
+//     x += d, then the sweep in reverse wave order;
+// coarsest level: x = A^{-1} b with the explicit dense inverse.
+// PCG (multilevel.py:238-281) and the AMG iteration (204-235) keep every
+// scalar on the device; reductions are deterministic (per-block partials
+// summed in block order by the last block to finish).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "solve.cuh"
+
+namespace hcamg {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  }
+  return t;  // valid in thread 0
+}
+
+// Publish this block's partial(s); returns true in the last block to finish,
+// which then sees every partial.  Deterministic: the caller sums in order.
+__device__ __forceinline__ bool publish(double v, double v2, double* part, double* part2, unsigned* ticket) {
+  __shared__ double sh[32];
+  __shared__ bool last;
+  double s = block_sum(v, sh);
+  double s2 = part2 ? block_sum(v2, sh) : 0.0;
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = s;
+    if (part2) part2[blockIdx.x] = s2;
+    __threadfence();
+    unsigned t = atomicAdd(ticket, 1u);
+    last = t == gridDim.x - 1;
+  }
+  __syncthreads();
+  return last;
+}
+
+__device__ __forceinline__ double ordered_sum(const double* part, int n) {
+  // fixed order: thread-strided partial sums, then a fixed tree
+  __shared__ double sh[32];
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v += ((volatile const double*)part)[i];
+  return block_sum(v, sh);
+}
+
+__device__ __forceinline__ void set_cond(unsigned long long cond, unsigned v) {
+  if (cond) cudaGraphSetConditional((cudaGraphConditionalHandle)cond, v);
+}
+
+// ----------------------------------------------------------------------------- smoother kernels
+
+struct WaveArgs {
+  const int* stop;
+  int64_t n;
+  // generic pulled rows
+  const int32_t* gen;
+  int64_t ngen;
+  const int64_t* grow_ptr;
+  const int32_t* grow_u;
+  const int32_t* gcol;
+  const double* gval;
+  const double* dsrc;
+  // patches of the destination wave
+  int64_t p0, p1;
+  const int64_t* patch_ptr;
+  const int32_t* dofs;
+  const int64_t* binv_off;
+  const double* binv;
+  const int32_t* own;
+  double* r;
+  double* x;
+  double* ddst;
+  const double* b;            // init step only
+  const uint8_t* in_first;    // init step only
+  int gen_blocks;
+};
+
+__device__ __forceinline__ double pull(int32_t rho, const int64_t* __restrict__ gp, const int32_t* __restrict__ gc,
+                                       const double* __restrict__ gv, const double* __restrict__ d) {
+  double acc = 0.0;
+  for (int64_t e = gp[rho]; e < gp[rho + 1]; ++e) acc = fma(gv[e], d[gc[e]], acc);
+  return acc;
+}
+
+template <bool kInit>
+__global__ void __launch_bounds__(kThreads) k_wave(WaveArgs a) {
+  if (*a.stop) return;
+  if ((int)blockIdx.x < a.gen_blocks) {
+    const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (kInit) {
+      for (int64_t u = t; u < a.n; u += (int64_t)a.gen_blocks * kThreads) {
+        a.r[u] = a.b[u];
+        if (!a.in_first[u]) a.x[u] = 0.0;
+      }
+    } else if (t < a.ngen) {
+      const int32_t rho = a.gen[t];
+      const int32_t u = a.grow_u[rho];
+      a.r[u] -= pull(rho, a.grow_ptr, a.gcol, a.gval, a.dsrc);
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t p = a.p0 + ((int64_t)(blockIdx.x - a.gen_blocks) * kThreads + threadIdx.x) / 32;
+  if (p >= a.p1) return;
+  const int64_t e0 = a.patch_ptr[p];
+  const int k = (int)(a.patch_ptr[p + 1] - e0);
+  int32_t i = 0;
+  double v = 0.0;
+  if (lane < k) {
+    i = a.dofs[e0 + lane];
+    if (kInit) {
+      v = a.b[i];
+    } else {
+      v = a.r[i];
+      if (a.own) {
+        const int32_t rho = a.own[e0 + lane];
+        if (rho >= 0) {
+          v -= pull(rho, a.grow_ptr, a.gcol, a.gval, a.dsrc);
+          a.r[i] = v;
+        }
+      }
+    }
+  }
+  // d = B_p^{-1} r[patch]  (column-major inverse: coalesced over the lanes)
+  const double* Bi = a.binv + a.binv_off[p];
+  double d = 0.0;
+  for (int c = 0; c < k; ++c) {
+    const double vc = __shfl_sync(0xffffffffu, v, c);
+    if (lane < k) d = fma(Bi[(int64_t)c * k + lane], vc, d);
+  }
+  if (lane < k) {
+    a.x[i] = kInit ? d : a.x[i] + d;
+    a.ddst[i] = d;
+  }
+}
+
+struct FinalArgs {
+  const int* stop;
+  int64_t n;
+  const int32_t* last_row;
+  const int64_t* grow_ptr;
+  const int32_t* gcol;
+  const double* gval;
+  const double* dsrc;
+  const double* l1;
+  double* r;
+  double* x;
+  double* dj;
+};
+
+__global__ void __launch_bounds__(kThreads) k_fw_final(FinalArgs a) {
+  if (*a.stop) return;
+  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < a.n; u += (int64_t)gridDim.x * kThreads) {
+    double v = a.r[u];
+    if (a.last_row) {
+      const int32_t rho = a.last_row[u];
+      if (rho >= 0) v -= pull(rho, a.grow_ptr, a.gcol, a.gval, a.dsrc);
+    }
+    const double d = v / a.l1[u];
+    a.x[u] += d;
+    a.r[u] = v;
+    a.dj[u] = d;
+  }
+}
+
+__global__ void k_init_rb(const int* stop, int64_t n, const double* __restrict__ b, double* __restrict__ r,
+                          double* __restrict__ x) {
+  if (*stop) return;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    r[u] = b[u];
+    x[u] = 0.0;
+  }
+}
+
+// ----------------------------------------------------------------------------- SpMV with epilogues
+
+enum Epi : int {
+  EPI_SET = 0,       // y = s
+  EPI_ADD,           // y += s
+  EPI_JAC_FW,        // r -= s
+  EPI_RES_JAC,       // r = b - s; dj = r / l1
+  EPI_JAC_BW,        // r -= s; x += dj
+  EPI_AP,            // y = s; partial p.y -> pAp, alpha
+  EPI_PCG_INIT,      // r = b - s; partials r.r, b.b
+  EPI_AMG_INIT,      // r = b - s; partials r.r, b.b
+  EPI_AMG_RES,       // r = b - s; partial r.r -> rel, history, divergence guard
+  EPI_RES_PLAIN,     // r = b - s; partials r.r, b.b (generic PCG init)
+};
+
+struct SpmvArgs {
+  const int* stop;
+  int64_t nrows;
+  const int64_t* ptr;
+  const int32_t* idx;
+  const double* val;
+  const double* xin;   // vector multiplied
+  double* y;           // EPI_SET/ADD/AP output; r for residual kinds
+  const double* b;
+  const double* l1;
+  double* dj;
+  double* x;           // EPI_JAC_BW
+  Ctl* ctl;
+  double* part;
+  double* part2;
+  double* hist;
+  unsigned long long cond;
+};
+
+template <int G, int E>
+__global__ void __launch_bounds__(kThreads) k_spmv(SpmvArgs a) {
+  if (E != EPI_PCG_INIT && E != EPI_AMG_INIT && E != EPI_RES_PLAIN && *a.stop) {
+    if (E == EPI_AP && blockIdx.x == 0 && threadIdx.x == 0) set_cond(a.cond, 0);
+    return;
+  }
+  const int lg = threadIdx.x & (G - 1);
+  const int64_t grp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) / G;
+  const int64_t ngrp = (int64_t)gridDim.x * kThreads / G;
+  double part = 0.0, part2 = 0.0;
+  const int64_t rows_iter = ((a.nrows + ngrp - 1) / ngrp) * ngrp;
+  for (int64_t row = grp; row < rows_iter; row += ngrp) {
+    double s = 0.0;
+    if (row < a.nrows)
+      for (int64_t e = a.ptr[row] + lg; e < a.ptr[row + 1]; e += G) s = fma(a.val[e], a.xin[a.idx[e]], s);
+    for (int o = G / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+    if (lg != 0 || row >= a.nrows) continue;
+    if (E == EPI_SET) a.y[row] = s;
+    else if (E == EPI_ADD) a.y[row] += s;
+    else if (E == EPI_JAC_FW) a.y[row] -= s;
+    else if (E == EPI_RES_JAC) { const double r = a.b[row] - s; a.y[row] = r; a.dj[row] = r / a.l1[row]; }
+    else if (E == EPI_JAC_BW) { a.y[row] -= s; a.x[row] += a.dj[row]; }
+    else if (E == EPI_AP) { a.y[row] = s; part = fma(a.xin[row], s, part); }
+    else if (E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN) {
+      const double bb = a.b[row], r = bb - s;
+      a.y[row] = r;
+      part = fma(r, r, part);
+      part2 = fma(bb, bb, part2);
+    } else if (E == EPI_AMG_RES) { const double r = a.b[row] - s; a.y[row] = r; part = fma(r, r, part); }
+  }
+  if (E < EPI_AP) return;
+  const bool two = E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN;
+  Ctl* c = a.ctl;
+  if (!publish(part, part2, a.part, two ? a.part2 : nullptr, &c->ticket[E - EPI_AP])) return;
+  const double S = ordered_sum(a.part, gridDim.x);
+  const double S2 = two ? ordered_sum(a.part2, gridDim.x) : 0.0;
+  if (threadIdx.x != 0) return;
+  c->ticket[E - EPI_AP] = 0u;
+  if (E == EPI_AP) {
+    c->pAp = S;
+    if (!(S > 0.0)) { c->error = kErrPAp; c->stop = 1; set_cond(a.cond, 0); }
+    else c->alpha = c->rz / S;
+  } else if (E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN) {
+    c->bnorm = sqrt(S2);
+    c->it = 0;
+    c->error = kErrNone;
+    c->growth = 0;
+    c->converged = 0;
+    c->zero_b = 0;
+    c->stop = 0;
+    if (c->bnorm == 0.0) {
+      c->zero_b = 1; c->converged = 1; c->stop = 1;
+    } else {
+      c->rel = sqrt(S) / c->bnorm;
+      c->prev_rel = c->rel;
+      if (c->rel <= c->tol) { c->converged = 1; c->stop = 1; }
+      else if (c->maxit <= 0) c->stop = 1;
+    }
+    set_cond(a.cond, c->stop ? 0u : 1u);
+  } else if (E == EPI_AMG_RES) {
+    const double prev = c->rel;
+    const double rel = sqrt(S) / c->bnorm;
+    c->rel = rel;
+    a.hist[c->it] = rel;
+    c->it += 1;
+    if (rel <= c->tol) { c->converged = 1; c->stop = 1; }
+    else {
+      c->growth = rel > prev ? c->growth + 1 : 0;
+      if (c->growth >= 5) { c->error = 3; c->stop = 1; }
+      else if (c->it >= c->maxit) c->stop = 1;
+    }
+    set_cond(a.cond, c->stop ? 0u : 1u);
+  }
+}
+
+// ----------------------------------------------------------------------------- PCG vector kernels
+
+__global__ void __launch_bounds__(kThreads) k_pcg_update(const int* stop, int64_t n, double* __restrict__ x,
+                                                         double* __restrict__ r, const double* __restrict__ p,
+                                                         const double* __restrict__ Ap, Ctl* c, double* part,
+                                                         double* hist, unsigned long long cond) {
+  if (*stop) return;
+  const double alpha = c->alpha;
+  double acc = 0.0;
+  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < n; u += (int64_t)gridDim.x * kThreads) {
+    x[u] = fma(alpha, p[u], x[u]);
+    const double rv = fma(-alpha, Ap[u], r[u]);
+    r[u] = rv;
+    acc = fma(rv, rv, acc);
+  }
+  if (!publish(acc, 0.0, part, nullptr, &c->ticket[6])) return;
+  const double S = ordered_sum(part, gridDim.x);
+  if (threadIdx.x != 0) return;
+  c->ticket[6] = 0u;
+  const double rel = sqrt(S) / c->bnorm;
+  c->rel = rel;
+  hist[c->it] = rel;
+  c->it += 1;
+  if (rel <= c->tol) { c->converged = 1; c->stop = 1; }
+  else if (c->it >= c->maxit) c->stop = 1;
+  set_cond(cond, c->stop ? 0u : 1u);
+}
+
+template <bool kFirst>
+__global__ void __launch_bounds__(kThreads) k_dot_rz(const int* stop, int64_t n, const double* __restrict__ r,
+                                                     const double* __restrict__ z, double* __restrict__ p, Ctl* c,
+                                                     double* part, unsigned long long cond) {
+  if (*stop) return;
+  double acc = 0.0;
+  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < n; u += (int64_t)gridDim.x * kThreads) {
+    const double zv = z[u];
+    acc = fma(r[u], zv, acc);
+    if (kFirst) p[u] = zv;
+  }
+  if (!publish(acc, 0.0, part, nullptr, &c->ticket[7])) return;
+  const double S = ordered_sum(part, gridDim.x);
+  if (threadIdx.x != 0) return;
+  c->ticket[7] = 0u;
+  if (kFirst) { c->rz = S; return; }
+  if (!(S > 0.0)) { c->error = kErrRz; c->stop = 1; set_cond(cond, 0); return; }
+  c->beta = S / c->rz;
+  c->rz = S;
+}
+
+__global__ void __launch_bounds__(kThreads) k_p_update(const int* stop, int64_t n, const double* __restrict__ z,
+                                                       double* __restrict__ p, const Ctl* c) {
+  if (*stop) return;
+  const double beta = c->beta;
+  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < n; u += (int64_t)gridDim.x * kThreads)
+    p[u] = fma(beta, p[u], z[u]);
+}
+
+__global__ void k_loop_guard(const int* stop, unsigned long long cond) {
+  if (*stop && threadIdx.x == 0) set_cond(cond, 0);
+}
+
+__global__ void __launch_bounds__(kThreads) k_axpy1(const int* stop, int64_t n, const double* __restrict__ e,
+                                                    double* __restrict__ x) {
+  if (*stop) return;
+  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < n; u += (int64_t)gridDim.x * kThreads)
+    x[u] += e[u];
+}
+
+// coarsest: x = Ainv b (row-major, one warp per row)
+__global__ void __launch_bounds__(kThreads) k_gemv_dense(const int* stop, int64_t n, const double* __restrict__ M,
+                                                         const double* __restrict__ b, double* __restrict__ x) {
+  if (*stop) return;
+  const int lane = threadIdx.x & 31;
+  for (int64_t row = ((int64_t)blockIdx.x * kThreads + threadIdx.x) / 32; row < n;
+       row += (int64_t)gridDim.x * kThreads / 32) {
+    const double* m = M + row * n;
+    double s = 0.0;
+    for (int64_t c = lane; c < n; c += 32) s = fma(m[c], b[c], s);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) x[row] = s;
+  }
+}
+
+// ----------------------------------------------------------------------------- launch helpers
+
+int group_for(const DCsr& M) {
+  const double avg = M.nrows ? (double)M.nnz / (double)M.nrows : 0.0;
+  if (avg <= 6) return 4;
+  if (avg <= 20) return 8;
+  if (avg <= 64) return 16;
+  return 32;
+}
+
+unsigned spmv_grid(int64_t nrows, int G) {
+  const int64_t rows_per_block = kThreads / G;
+  int64_t g = (nrows + rows_per_block - 1) / rows_per_block;
+  g = std::max<int64_t>(1, std::min<int64_t>(g, kSMs * 8));
+  return (unsigned)g;
+}
+
+template <int E>
+void launch_spmv_g(int G, unsigned grid, SpmvArgs& a, cudaStream_t s) {
+  switch (G) {
+    case 4: k_spmv<4, E><<<grid, kThreads, 0, s>>>(a); break;
+    case 8: k_spmv<8, E><<<grid, kThreads, 0, s>>>(a); break;
+    case 16: k_spmv<16, E><<<grid, kThreads, 0, s>>>(a); break;
+    default: k_spmv<32, E><<<grid, kThreads, 0, s>>>(a); break;
+  }
+  HC_CHECK_LAUNCH();
+}
+
+template <int E>
+unsigned spmv(const DCsr& M, SpmvArgs a, cudaStream_t s) {
+  a.nrows = M.nrows;
+  a.ptr = M.ptr.p;
+  a.idx = M.idx.p;
+  a.val = M.val.p;
+  const int G = group_for(M);
+  const unsigned grid = spmv_grid(M.nrows, G);
+  launch_spmv_g<E>(G, grid, a, s);
+  return grid;
+}
+
+unsigned vec_grid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kThreads - 1) / kThreads, kSMs * 4)); }
+
+}  // namespace
+
+void Workspace::ensure(int64_t n_, int64_t maxit, cudaStream_t s) {
+  if (!ctl.p) {
+    ctl.alloc(1, s);
+    ctl.zero();
+    part.alloc(kSMs * 8 + 64, s);
+    part2.alloc(kSMs * 8 + 64, s);
+    zero_flag.alloc(1, s);
+    zero_flag.zero();
+  }
+  if (n_ != n) {
+    n = n_;
+    for (DBuf<double>* v : {&x, &r, &z, &p, &Ap, &b}) v->alloc(std::max<int64_t>(n, 1), s);
+  }
+  if (hist.n < maxit + 1) hist.alloc(maxit + 1, s);
+}
+
+// ----------------------------------------------------------------------------- V-cycle
+
+static int64_t record_level(std::vector<DevLevel*>& lv, size_t ell, const double* b, double* x, const int* stop,
+                            cudaStream_t s) {
+  DevLevel& L = *lv[ell];
+  int64_t launches = 0;
+  const int64_t n = L.n;
+  if (L.coarsest) {
+    if (n) {
+      k_gemv_dense<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, kSMs * 8)), kThreads, 0, s>>>(
+          stop, n, L.Ainv.p, b, x);
+      HC_CHECK_LAUNCH();
+      ++launches;
+    }
+    return launches;
+  }
+  Smoother& sm = L.sm;
+  double* dbuf[2] = {L.d0.p, L.d1.p};
+  const int64_t W = sm.nwave;
+  auto wave = [&](bool init, int64_t dst, int64_t src, int dir) {
+    WaveArgs a{};
+    a.stop = stop;
+    a.n = n;
+    a.grow_ptr = sm.grow_ptr.p;
+    a.grow_u = sm.grow_u.p;
+    a.gcol = sm.gcol.p;
+    a.gval = sm.gval.p;
+    a.p0 = sm.wave_ptr[(size_t)dst];
+    a.p1 = sm.wave_ptr[(size_t)dst + 1];
+    a.patch_ptr = sm.patch_ptr.p;
+    a.dofs = sm.patch_dofs.p;
+    a.binv_off = sm.binv_off.p;
+    a.binv = sm.binv.p;
+    a.r = L.r.p;
+    a.x = x;
+    a.ddst = dbuf[dst & 1];
+    if (init) {
+      a.b = b;
+      a.in_first = sm.in_first.p;
+      a.gen_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + kThreads - 1) / kThreads, kSMs * 4));
+    } else if (src >= 0) {
+      const std::vector<int64_t>& gp = dir == 0 ? sm.gen_fw_ptr : sm.gen_bw_ptr;
+      const int64_t g0 = gp[(size_t)src], g1 = gp[(size_t)src + 1];
+      a.gen = (dir == 0 ? sm.gen_fw.p : sm.gen_bw.p) + g0;
+      a.ngen = g1 - g0;
+      a.dsrc = dbuf[src & 1];
+      a.own = dir == 0 ? sm.own_fw.p : sm.own_bw.p;
+      a.gen_blocks = (int)((a.ngen + kThreads - 1) / kThreads);
+    }
+    const int64_t pb = (a.p1 - a.p0 + kThreads / 32 - 1) / (kThreads / 32);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, a.gen_blocks + pb);
+    if (init) k_wave<true><<<grid, kThreads, 0, s>>>(a);
+    else k_wave<false><<<grid, kThreads, 0, s>>>(a);
+    HC_CHECK_LAUNCH();
+    ++launches;
+  };
+  // ---- forward OSS-l1 from x = 0
+  if (W > 0) {
+    wave(true, 0, -1, 0);
+    for (int64_t d = 1; d < W; ++d) wave(false, d, d - 1, 0);
+  } else {
+    k_init_rb<<<vec_grid(n), kThreads, 0, s>>>(stop, n, b, L.r.p, x);
+    HC_CHECK_LAUNCH();
+    ++launches;
+  }
+  {
+    FinalArgs f{stop, n, W > 0 ? sm.last_row.p : nullptr, sm.grow_ptr.p, sm.gcol.p, sm.gval.p,
+                W > 0 ? dbuf[(W - 1) & 1] : nullptr, L.l1.p, L.r.p, x, L.dj.p};
+    k_fw_final<<<vec_grid(n), kThreads, 0, s>>>(f);
+    HC_CHECK_LAUNCH();
+    ++launches;
+  }
+  SpmvArgs a{};
+  a.stop = stop;
+  a.xin = L.dj.p;
+  a.y = L.r.p;
+  spmv<EPI_JAC_FW>(L.A, a, s);
+  ++launches;
+  // ---- coarse correction
+  DevLevel& C = *lv[ell + 1];
+  SpmvArgs rs{};
+  rs.stop = stop;
+  rs.xin = L.r.p;
+  rs.y = C.b.p;
+  spmv<EPI_SET>(L.Pt, rs, s);
+  ++launches;
+  launches += record_level(lv, ell + 1, C.b.p, C.x.p, stop, s);
+  SpmvArgs pr{};
+  pr.stop = stop;
+  pr.xin = C.x.p;
+  pr.y = x;
+  spmv<EPI_ADD>(L.P, pr, s);
+  ++launches;
+  // ---- backward OSS-l1
+  SpmvArgs rj{};
+  rj.stop = stop;
+  rj.xin = x;
+  rj.y = L.r.p;
+  rj.b = b;
+  rj.l1 = L.l1.p;
+  rj.dj = L.dj.p;
+  spmv<EPI_RES_JAC>(L.A, rj, s);
+  SpmvArgs jb{};
+  jb.stop = stop;
+  jb.xin = L.dj.p;
+  jb.y = L.r.p;
+  jb.dj = L.dj.p;
+  jb.x = x;
+  spmv<EPI_JAC_BW>(L.A, jb, s);
+  launches += 2;
+  for (int64_t d = W - 1; d >= 0; --d) wave(false, d, d == W - 1 ? -1 : d + 1, 1);
+  return launches;
+}
+
+int64_t record_vcycle(std::vector<DevLevel*>& lv, const double* b0, double* x0, const int* stop, cudaStream_t s) {
+  return record_level(lv, 0, b0, x0, stop, s);
+}
+
+// ----------------------------------------------------------------------------- PCG / AMG recording
+
+int64_t record_pcg_init(DevLevel& L0, Workspace& w, const double* b, const double* x0, cudaStream_t s,
+                        unsigned long long cond) {
+  (void)x0;
+  SpmvArgs a{};
+  a.stop = &w.ctl.p->stop;
+  a.xin = w.x.p;
+  a.y = w.r.p;
+  a.b = b;
+  a.ctl = w.ctl.p;
+  a.part = w.part.p;
+  a.part2 = w.part2.p;
+  a.cond = cond;
+  spmv<EPI_PCG_INIT>(L0.A, a, s);
+  return 1;
+}
+
+int64_t record_pcg_first(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s) {
+  const int* stop = &w.ctl.p->stop;
+  int64_t l = record_vcycle(lv, w.r.p, w.z.p, stop, s);
+  k_dot_rz<true><<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, 0);
+  HC_CHECK_LAUNCH();
+  return l + 1;
+}
+
+int64_t record_pcg_body(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s, unsigned long long cond) {
+  const int* stop = &w.ctl.p->stop;
+  DevLevel& L0 = *lv[0];
+  SpmvArgs a{};
+  a.stop = stop;
+  a.xin = w.p.p;
+  a.y = w.Ap.p;
+  a.ctl = w.ctl.p;
+  a.part = w.part.p;
+  a.cond = cond;
+  spmv<EPI_AP>(L0.A, a, s);
+  k_pcg_update<<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.x.p, w.r.p, w.p.p, w.Ap.p, w.ctl.p, w.part.p,
+                                                  w.hist.p, cond);
+  HC_CHECK_LAUNCH();
+  int64_t l = 2 + record_vcycle(lv, w.r.p, w.z.p, stop, s);
+  k_dot_rz<false><<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, cond);
+  k_p_update<<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.z.p, w.p.p, w.ctl.p);
+  HC_CHECK_LAUNCH();
+  return l + 2;
+}
+
+int64_t record_amg_init(DevLevel& L0, Workspace& w, const double* b, const double* x0, cudaStream_t s,
+                        unsigned long long cond) {
+  (void)x0;
+  SpmvArgs a{};
+  a.stop = &w.ctl.p->stop;
+  a.xin = w.x.p;
+  a.y = w.r.p;
+  a.b = b;
+  a.ctl = w.ctl.p;
+  a.part = w.part.p;
+  a.part2 = w.part2.p;
+  a.cond = cond;
+  spmv<EPI_AMG_INIT>(L0.A, a, s);
+  return 1;
+}
+
+int64_t record_amg_body(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s, unsigned long long cond) {
+  const int* stop = &w.ctl.p->stop;
+  k_loop_guard<<<1, 32, 0, s>>>(stop, cond);
+  HC_CHECK_LAUNCH();
+  int64_t l = 1 + record_vcycle(lv, w.r.p, w.z.p, stop, s);
+  k_axpy1<<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.z.p, w.x.p);
+  HC_CHECK_LAUNCH();
+  SpmvArgs a{};
+  a.stop = stop;
+  a.xin = w.x.p;
+  a.y = w.r.p;
+  a.b = w.b.p;
+  a.ctl = w.ctl.p;
+  a.part = w.part.p;
+  a.hist = w.hist.p;
+  a.cond = cond;
+  spmv<EPI_AMG_RES>(lv[0]->A, a, s);
+  return l + 2;
+}
+
+// ----------------------------------------------------------------------------- generic PCG helpers
+
+void apply_operator(const DCsr& A, const double* x, double* y, cudaStream_t s) {
+  DBuf<int> z(1, s);
+  z.zero();
+  SpmvArgs a{};
+  a.stop = z.p;
+  a.xin = x;
+  a.y = y;
+  spmv<EPI_SET>(A, a, s);
+}
+
+void generic_init(const DCsr& A, Workspace& w, cudaStream_t s) {
+  SpmvArgs a{};
+  a.stop = &w.ctl.p->stop;
+  a.xin = w.x.p;
+  a.y = w.r.p;
+  a.b = w.b.p;
+  a.ctl = w.ctl.p;
+  a.part = w.part.p;
+  a.part2 = w.part2.p;
+  spmv<EPI_RES_PLAIN>(A, a, s);
+}
+
+void generic_pap(const DCsr& A, Workspace& w, cudaStream_t s) {
+  SpmvArgs a{};
+  a.stop = w.zero_flag.p;
+  a.xin = w.p.p;
+  a.y = w.Ap.p;
+  a.ctl = w.ctl.p;
+  a.part = w.part.p;
+  spmv<EPI_AP>(A, a, s);
+}
+
+void generic_update(Workspace& w, cudaStream_t s) {
+  k_pcg_update<<<vec_grid(w.n), kThreads, 0, s>>>(w.zero_flag.p, w.n, w.x.p, w.r.p, w.p.p, w.Ap.p, w.ctl.p,
+                                                  w.part.p, w.hist.p, 0);
+  HC_CHECK_LAUNCH();
+}
+
+void generic_rz(Workspace& w, bool first, cudaStream_t s) {
+  if (first) k_dot_rz<true><<<vec_grid(w.n), kThreads, 0, s>>>(w.zero_flag.p, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, 0);
+  else k_dot_rz<false><<<vec_grid(w.n), kThreads, 0, s>>>(w.zero_flag.p, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, 0);
+  HC_CHECK_LAUNCH();
+}
+
+namespace {
+__global__ void k_vec_add(int64_t n, const double* __restrict__ a, const double* __restrict__ b, double* out) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+    out[u] = a[u] + b[u];
+}
+}  // namespace
+
+void vec_add(int64_t n, const double* a, const double* b, double* out, cudaStream_t s) {
+  if (n) k_vec_add<<<vec_grid(n), kThreads, 0, s>>>(n, a, b, out);
+  HC_CHECK_LAUNCH();
+}
+
+void generic_p(Workspace& w, cudaStream_t s) {
+  k_p_update<<<vec_grid(w.n), kThreads, 0, s>>>(w.zero_flag.p, w.n, w.z.p, w.p.p, w.ctl.p);
+  HC_CHECK_LAUNCH();
+}
+
+}  // namespace hcamg

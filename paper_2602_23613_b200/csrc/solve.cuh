@@ -1,0 +1,60 @@
+// Solve phase: V(1,1) cycle with the OSS-l1 smoother, PCG and stand-alone
+// AMG iteration, recorded into CUDA graphs (see solve.cu).
+#pragma once
+#include <vector>
+
+#include "level.cuh"
+
+namespace hcamg {
+
+// Device control block shared by the PCG / AMG kernels.
+struct Ctl {
+  double bnorm, rel, prev_rel, tol;
+  double rz, pAp, alpha, beta;
+  long long it, maxit;
+  int stop, converged, error, growth, zero_b, pad;
+  unsigned int ticket[8];
+};
+
+enum CtlError : int { kErrNone = 0, kErrPAp = 1, kErrRz = 2 };
+
+struct Workspace {
+  int64_t n = 0;
+  DBuf<Ctl> ctl;
+  DBuf<double> part, part2;   // per-block partial sums (deterministic reductions)
+  DBuf<double> hist;          // residual history (maxit)
+  DBuf<double> x, r, z, p, Ap, b;
+  DBuf<int> zero_flag;        // always-0 stop flag for stand-alone cycles
+  void ensure(int64_t n_, int64_t maxit, cudaStream_t s);
+};
+
+// Record one V-cycle on `stream`: x0 := V(b0) for the finest level, reading
+// b0 and writing x0 (level-0 work buffers are used for everything else).
+// Every kernel returns immediately when *stop != 0.
+int64_t record_vcycle(std::vector<DevLevel*>& lv, const double* b0, double* x0, const int* stop,
+                      cudaStream_t s);
+
+// PCG (multilevel.py:238-281) pieces.  `cond` is the WHILE-node handle
+// (0 when the loop is driven from the host).
+int64_t record_pcg_init(DevLevel& L0, Workspace& w, const double* b, const double* x0, cudaStream_t s,
+                        unsigned long long cond);
+int64_t record_pcg_first(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s);
+int64_t record_pcg_body(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s, unsigned long long cond);
+
+// Stand-alone AMG iteration (multilevel.py:204-235).
+int64_t record_amg_init(DevLevel& L0, Workspace& w, const double* b, const double* x0, cudaStream_t s,
+                        unsigned long long cond);
+int64_t record_amg_body(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s, unsigned long long cond);
+
+// y = A x (device), for the generic PCG path.
+void apply_operator(const DCsr& A, const double* x, double* y, cudaStream_t s);
+
+// Generic PCG vector kernels (arbitrary preconditioner driven from the host).
+void generic_init(const DCsr& A, Workspace& w, cudaStream_t s);    // r = b - A x, norms
+void generic_pap(const DCsr& A, Workspace& w, cudaStream_t s);     // Ap, pAp, alpha
+void generic_update(Workspace& w, cudaStream_t s);                 // x, r, rel, history
+void generic_rz(Workspace& w, bool first, cudaStream_t s);         // rz (first: p = z) / beta
+void generic_p(Workspace& w, cudaStream_t s);                      // p = z + beta p
+void vec_add(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);  // out = a + b
+
+}  // namespace hcamg
