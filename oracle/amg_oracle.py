@@ -416,7 +416,18 @@ class Transfer:
     Z_blocks: list = field(default_factory=list)   # (interior rows, keep cols, Z) per component
 
 
-def harmonic_interp(A, split, mode="refinement", G=None):
+def _alt_component_solve(Acc, rhs):
+    """Reproducibility-floor solver: LU of the reversed-order block (another
+    valid fp64 algorithm).  Used only to MEASURE how far
+    two correct fp64 implementations drift apart, never as the oracle."""
+    rev = np.arange(Acc.shape[0])[::-1]
+    lu = scipy.linalg.lu_factor(Acc[np.ix_(rev, rev)])
+    Z = np.empty_like(rhs)
+    Z[rev] = scipy.linalg.lu_solve(lu, rhs[rev])
+    return Z
+
+
+def harmonic_interp(A, split, mode="refinement", G=None, floor_solver=False):
     """sparse_ideal_interp (transfer.py:77-122): P = R^T - S_I A_II^{-1} S_I^T A R^T."""
     R = restriction(split)
     Rt = canon(R.T)
@@ -434,8 +445,12 @@ def harmonic_interp(A, split, mode="refinement", G=None):
             keep = np.flatnonzero(np.diff(Wc.indptr) > 0)
             if keep.size == 0:
                 continue
-            L = dense_chol(A_II[comp][:, comp].toarray())
-            Z = scipy.linalg.cho_solve((L, True), np.asarray(Wc[:, keep].todense()))
+            Acc = A_II[comp][:, comp].toarray()
+            rhs = np.asarray(Wc[:, keep].todense())
+            if floor_solver:
+                Z = _alt_component_solve(Acc, rhs)
+            else:
+                Z = scipy.linalg.cho_solve((dense_chol(Acc), True), rhs)
             blocks.append((inner[comp], keep, Z))
             nzr, nzc = np.nonzero(Z)
             ri.append(inner[comp[nzr]])
@@ -583,11 +598,13 @@ def sign_gradient(Gc):
 
 
 def hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse=32,
-              theta=0.25, smoother=True):
+              theta=0.25, smoother=True, floor_solver=False):
     """build_hierarchy (multilevel.py:78-164) for the "alg" and "ref" routes.
 
     ``smoother=False`` skips the patch factorisation (used when only the
     setup integers/operators are compared at sizes where it is slow).
+    ``floor_solver=True`` swaps the component Cholesky for a reversed-order
+    LU to measure the fp64 reproducibility floor of P, A_c and x.
     """
     if method in ("geo", "ref") and (meshes is None or rmaps is None):
         raise ValueError(f"method {method!r} requires the nested mesh chain")
@@ -616,7 +633,7 @@ def hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse
                 stalled = True
                 notes.append("refinement splitting produced no pairs")
                 break
-            tr = harmonic_interp(A, split, "refinement", G)
+            tr = harmonic_interp(A, split, "refinement", G, floor_solver)
             nxt = np.full(meshes[pos - 1].ne, -1, dtype=np.int64)
             nxt[split.pair_mesh_edges] = np.arange(split.n_pairs)
         else:
@@ -626,7 +643,7 @@ def hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse
                     stalled = True
                     notes.append("algebraic coarsening found no pairs")
                 break
-            tr = harmonic_interp(A, split, "algebraic", G)
+            tr = harmonic_interp(A, split, "algebraic", G, floor_solver)
             nxt = None
         P = tr.P
         if P.shape[1] == 0 or P.shape[1] >= n:

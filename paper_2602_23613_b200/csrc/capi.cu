@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -290,7 +291,11 @@ void build_loop_graph(hcamg_handle* h, Graph& G, bool pcg) {
   cudaGraph_t g = nullptr;
   HC_CUDA(cudaGraphCreate(&g, 0));
   cudaGraphConditionalHandle cond;
-  cudaError_t ce = cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault);
+  // HCAMG_HOST_LOOP=1 forces the host-driven loop (same kernels; lets ncu profile graph nodes,
+  // which it cannot do inside graphs that contain conditional nodes)
+  const char* hl = getenv("HCAMG_HOST_LOOP");
+  cudaError_t ce = (hl && hl[0] == '1') ? cudaErrorNotSupported
+                                        : cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault);
   if (ce == cudaSuccess) {
     HC_CUDA(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     int64_t lp = pcg ? record_pcg_init(*h->lv[0], w, b, nullptr, s, 0) + record_pcg_first(h->lv, w, s)

@@ -47,3 +47,23 @@ def load(name):
                   for i in range(k)]
         rmaps = [SimpleNamespace(coarse_edge_children=z[f"rmap{i}_children"]) for i in range(k - 1)]
     return SimpleNamespace(z=z, meta=meta, system=system, meshes=meshes, rmaps=rmaps)
+
+
+def api_system(key):
+    """(meshes, rmaps, system) of a 2D chain stored in golden/api_inputs.npz
+    (the reference tests' tri_setup(L[, stripes]))."""
+    z = np.load(os.path.join(GOLDEN, "api_inputs.npz"))
+    A, G = get_csr(z, key + "_A"), get_csr(z, key + "_G")
+    system = SimpleNamespace(A=A, G=G, free_edges=z[key + "_free_edges"], n=A.shape[0])
+    k = int(z[key + "_chain_len"][0])
+    meshes = [SimpleNamespace(edges=z[f"{key}_mesh{i}_edges"], ne=len(z[f"{key}_mesh{i}_edges"])) for i in range(k)]
+    rmaps = [SimpleNamespace(coarse_edge_children=z[f"{key}_rmap{i}_children"]) for i in range(k - 1)]
+    return meshes, rmaps, system
+
+
+def gpu_available():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False

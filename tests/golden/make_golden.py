@@ -159,8 +159,27 @@ def kats():
     np.savez_compressed(os.path.join(HERE, "kats.npz"), **out)
 
 
+def api_inputs():
+    """2D systems + nested mesh chains used by the ported reference API tests
+    (tests/test_multilevel.py:25-30 tri_setup)."""
+    out = {}
+    for L, stripes in ((1, False), (2, False), (3, False), (3, True)):
+        key = f"tri{L}{'s' if stripes else ''}"
+        meshes, rmaps, s = tri_chain(L, stripes=stripes)
+        put_csr(out, key + "_A", s.A)
+        put_csr(out, key + "_G", s.G)
+        out[key + "_free_edges"] = np.asarray(s.free_edges, dtype=np.int64)
+        out[key + "_chain_len"] = np.array([len(meshes)])
+        for i, m in enumerate(meshes):
+            out[f"{key}_mesh{i}_edges"] = np.asarray(m.edges, dtype=np.int64)
+        for i, rm in enumerate(rmaps):
+            out[f"{key}_rmap{i}_children"] = np.asarray(rm.coarse_edge_children, dtype=np.int64)
+    np.savez_compressed(os.path.join(HERE, "api_inputs.npz"), **out)
+
+
 def main():
     kats()
+    api_inputs()
     meshes, rmaps, s = tri_chain(2)
     run_case("tri2_alg", s, "alg")
     meshes, rmaps, s = tri_chain(3, stripes=True)
