@@ -135,6 +135,11 @@ int hcamg_pcg_device(hcamg_handle* h, const double* d_b, const double* d_x0_or_n
                      int64_t maxit, double* d_x, hcamg_report* report);
 /* Kernel launches recorded in the last PCG / V-cycle graph (gpu_launches). */
 int64_t hcamg_graph_launches(hcamg_handle* h, int32_t which /* 0 vcycle, 1 pcg init, 2 pcg body */);
+/* Time each piece of the V-cycle alone (warm, CUDA events on the handle's
+ * stream, reps launches each): kind 0 down leg, 1 restriction, 2 coarsest
+ * solve, 3 prolongation, 4 up leg; writes up to cap records, *count set. */
+int hcamg_profile_vcycle(hcamg_handle* h, int32_t reps, int32_t cap, int32_t* kind, int32_t* level, double* us,
+                         int64_t* launches, int32_t* count);
 /* Device stream of the handle (cudaStream_t) for event timing. */
 void* hcamg_stream(hcamg_handle* h);
 

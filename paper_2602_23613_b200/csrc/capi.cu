@@ -166,6 +166,11 @@ void finish_level(hcamg_handle* h, DevLevel& L) {
   if (L.has_P) {
     build_l1(L.A, L.l1, s);
     build_smoother(L.A, L.G, L.sm, s);
+    // restriction with long P^T rows (dense interior blocks): segmented plan
+    std::vector<int64_t> tp = L.Pt.ptr.download();
+    L.pt_maxrow = 0;
+    for (int64_t p = 0; p < L.Pt.nrows; ++p) L.pt_maxrow = std::max(L.pt_maxrow, tp[(size_t)p + 1] - tp[(size_t)p]);
+    if (L.pt_maxrow > 512) build_segments(L.Pt, L.pt_seg, s);
   }
 }
 
@@ -747,6 +752,49 @@ int64_t hcamg_graph_launches(hcamg_handle* h, int32_t which) {
   if (which == 3) return h->g_amg.launches_pre;
   if (which == 4) return h->g_amg.launches_body;
   return -1;
+}
+
+int hcamg_profile_vcycle(hcamg_handle* h, int32_t reps, int32_t cap, int32_t* kind, int32_t* level, double* us,
+                         int64_t* launches, int32_t* count) {
+  return guarded(h, [&] {
+    require_hierarchy(h);
+    require(reps > 0, "reps must be positive");
+    cudaStream_t s = h->stream;
+    ensure_ws(h, 1);
+    cudaEvent_t e0, e1;
+    HC_CUDA(cudaEventCreate(&e0));
+    HC_CUDA(cudaEventCreate(&e1));
+    int32_t k = 0;
+    const int* stop = h->ws.zero_flag.p;
+    for (size_t ell = 0; ell < h->lv.size(); ++ell) {
+      DevLevel& L = *h->lv[ell];
+      DevLevel* C = ell + 1 < h->lv.size() ? h->lv[ell + 1] : nullptr;
+      const double* b = ell == 0 ? h->ws.r.p : L.b.p;
+      double* x = ell == 0 ? h->ws.z.p : L.x.p;
+      const int pcs_fine[] = {PC_DOWN, PC_RESTRICT, PC_PROLONG, PC_UP};
+      const int pcs_coarse[] = {PC_COARSE};
+      const int* pcs = L.coarsest ? pcs_coarse : pcs_fine;
+      const int npc = L.coarsest ? 1 : 4;
+      for (int t = 0; t < npc && k < cap; ++t) {
+        int64_t nl = 0;
+        for (int wv = 0; wv < 2; ++wv) nl = record_piece(pcs[t], L, C, b, x, stop, s);
+        HC_CUDA(cudaEventRecord(e0, s));
+        for (int r = 0; r < reps; ++r) record_piece(pcs[t], L, C, b, x, stop, s);
+        HC_CUDA(cudaEventRecord(e1, s));
+        HC_CUDA(cudaEventSynchronize(e1));
+        float ms = 0;
+        HC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        kind[k] = pcs[t];
+        level[k] = (int32_t)ell;
+        us[k] = 1e3 * ms / reps;
+        launches[k] = nl;
+        ++k;
+      }
+    }
+    *count = k;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  });
 }
 
 int hcamg_spmv(hcamg_handle* h, const hcamg_csr* A, const double* x, double* y) {

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "split.cuh"
+#include "sweep.cuh"
 
 namespace hcamg {
 
@@ -35,6 +36,11 @@ struct Smoother {
   std::vector<int64_t> gen_fw_ptr, gen_bw_ptr;  // per source wave offsets (host)
   DBuf<int32_t> last_row;               // per DoF: gather row of the last wave (-1: none)
   DBuf<uint8_t> in_first;               // per DoF: member of a wave-0 patch
+  // flattened copies for the cluster sweep (one fewer dependent load per pull):
+  // genrow_*: (u, start, end) per generic row; ownr_*: (start, end) per patch
+  // entry or (-1, -1); lastr: (start, end) per DoF for the last forward wave
+  DBuf<int32_t> genrow_fw, genrow_bw, ownr_fw, ownr_bw, lastr;
+  DBuf<int64_t> d_wave_ptr, d_gen_fw_ptr, d_gen_bw_ptr;
   // host copies for export (reference PatchSet layout, original patch order)
   std::vector<int64_t> h_patch_ptr, h_patch_dofs;
 };
@@ -50,6 +56,8 @@ struct DevLevel {
   std::vector<int64_t> gc_cols;
   bool coarsest = false;
   DBuf<double> Ainv;     // coarsest: dense inverse (row-major n x n)
+  SegPlan pt_seg;        // segmented restriction plan when P^T has long rows
+  int64_t pt_maxrow = 0;
   // work vectors
   DBuf<double> b, x, r, d0, d1, dj;
 };

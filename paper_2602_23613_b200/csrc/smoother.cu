@@ -237,6 +237,25 @@ __global__ void k_in_first(const unsigned long long* __restrict__ mkeys, int64_t
     if ((mkeys[i] >> 32) == 0) f[mkeys[i] & 0xffffffffull] = 1;
 }
 
+__global__ void k_flat_gen(const int32_t* __restrict__ gen, int64_t n, const int32_t* __restrict__ grow_u,
+                           const int64_t* __restrict__ gp, int32_t* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = gen[t];
+    out[3 * t] = grow_u[r];
+    out[3 * t + 1] = (int32_t)gp[r];
+    out[3 * t + 2] = (int32_t)gp[r + 1];
+  }
+}
+
+__global__ void k_flat_range(const int32_t* __restrict__ rho, int64_t n, const int64_t* __restrict__ gp,
+                             int32_t* __restrict__ out) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = rho[t];
+    out[2 * t] = r >= 0 ? (int32_t)gp[r] : -1;
+    out[2 * t + 1] = r >= 0 ? (int32_t)gp[r + 1] : -1;
+  }
+}
+
 __global__ void k_l1(const int64_t* __restrict__ ap, const double* __restrict__ av, int64_t n, double* __restrict__ d) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -421,6 +440,26 @@ void build_smoother(const DCsr& A, const DCsr& G, Smoother& sm, cudaStream_t s) 
   sm.in_first.zero();
   if (ne) k_in_first<<<grid_for(ne, 256), 256, 0, s>>>(mkeys.p, ne, sm.in_first.p);
   HC_CHECK_LAUNCH();
+  // flattened layout for the cluster sweep
+  for (int dir = 0; dir < 2; ++dir) {
+    const std::vector<int64_t>& gp = dir == 0 ? sm.gen_fw_ptr : sm.gen_bw_ptr;
+    const int64_t cnt = gp.back();
+    DBuf<int32_t>& out = dir == 0 ? sm.genrow_fw : sm.genrow_bw;
+    out.alloc(3 * std::max<int64_t>(cnt, 1), s);
+    if (cnt) k_flat_gen<<<grid_for(cnt, 256), 256, 0, s>>>(dir == 0 ? sm.gen_fw.p : sm.gen_bw.p, cnt, sm.grow_u.p,
+                                                          sm.grow_ptr.p, out.p);
+    DBuf<int32_t>& ow = dir == 0 ? sm.ownr_fw : sm.ownr_bw;
+    ow.alloc(2 * std::max<int64_t>(ne, 1), s);
+    if (ne) k_flat_range<<<grid_for(ne, 256), 256, 0, s>>>(dir == 0 ? sm.own_fw.p : sm.own_bw.p, ne, sm.grow_ptr.p,
+                                                          ow.p);
+    HC_CHECK_LAUNCH();
+  }
+  sm.lastr.alloc(2 * std::max<int64_t>(n, 1), s);
+  if (n) k_flat_range<<<grid_for(n, 256), 256, 0, s>>>(sm.last_row.p, n, sm.grow_ptr.p, sm.lastr.p);
+  HC_CHECK_LAUNCH();
+  sm.d_wave_ptr.upload(sm.wave_ptr.data(), (int64_t)sm.wave_ptr.size(), s);
+  sm.d_gen_fw_ptr.upload(sm.gen_fw_ptr.data(), (int64_t)sm.gen_fw_ptr.size(), s);
+  sm.d_gen_bw_ptr.upload(sm.gen_bw_ptr.data(), (int64_t)sm.gen_bw_ptr.size(), s);
   HC_CUDA(cudaStreamSynchronize(s));
 }
 

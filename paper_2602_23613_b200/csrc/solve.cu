@@ -19,6 +19,8 @@
 #include <algorithm>
 
 #include "solve.cuh"
+#include "sweep.cuh"
+#include <cstdlib>
 
 namespace hcamg {
 
@@ -100,8 +102,22 @@ struct WaveArgs {
 
 __device__ __forceinline__ double pull(int32_t rho, const int64_t* __restrict__ gp, const int32_t* __restrict__ gc,
                                        const double* __restrict__ gv, const double* __restrict__ d) {
+  const int64_t s = gp[rho], e = gp[rho + 1];
   double acc = 0.0;
-  for (int64_t e = gp[rho]; e < gp[rho + 1]; ++e) acc = fma(gv[e], d[gc[e]], acc);
+  for (int64_t k0 = s; k0 < e; k0 += 8) {
+    int32_t c[8];
+    double v[8], dv[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const bool ok = k0 + t < e;
+      c[t] = ok ? __ldg(gc + k0 + t) : 0;
+      v[t] = ok ? __ldg(gv + k0 + t) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) dv[t] = k0 + t < e ? d[c[t]] : 0.0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) acc = fma(v[t], dv[t], acc);
+  }
   return acc;
 }
 
@@ -449,23 +465,51 @@ void Workspace::ensure(int64_t n_, int64_t maxit, cudaStream_t s) {
 
 // ----------------------------------------------------------------------------- V-cycle
 
-static int64_t record_level(std::vector<DevLevel*>& lv, size_t ell, const double* b, double* x, const int* stop,
-                            cudaStream_t s) {
-  DevLevel& L = *lv[ell];
-  int64_t launches = 0;
-  const int64_t n = L.n;
-  if (L.coarsest) {
-    if (n) {
-      k_gemv_dense<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, kSMs * 8)), kThreads, 0, s>>>(
-          stop, n, L.Ainv.p, b, x);
-      HC_CHECK_LAUNCH();
-      ++launches;
-    }
-    return launches;
-  }
+static const std::string& sweep_mode() {
+  static const std::string m = [] {
+    const char* e = getenv("HCAMG_SWEEP");
+    return std::string(e ? e : "auto");
+  }();
+  return m;
+}
+
+static SweepArgs sweep_args(DevLevel& L, const double* b, double* x, const int* stop, bool down) {
   Smoother& sm = L.sm;
+  SweepArgs sa{};
+  sa.stop = stop;
+  sa.n = L.n;
+  sa.nwave = sm.nwave;
+  sa.wave_ptr = sm.d_wave_ptr.p;
+  sa.lastr = sm.lastr.p;
+  sa.in_first = sm.in_first.p;
+  sa.patch_ptr = sm.patch_ptr.p;
+  sa.dofs = sm.patch_dofs.p;
+  sa.binv_off = sm.binv_off.p;
+  sa.binv = sm.binv.p;
+  sa.gcol = sm.gcol.p;
+  sa.gval = sm.gval.p;
+  sa.ap = L.A.ptr.p;
+  sa.ai = L.A.idx.p;
+  sa.av = L.A.val.p;
+  sa.l1 = L.l1.p;
+  sa.b = b;
+  sa.x = x;
+  sa.r = L.r.p;
+  sa.d0 = L.d0.p;
+  sa.d1 = L.d1.p;
+  sa.dj = L.dj.p;
+  sa.gen_ptr = down ? sm.d_gen_fw_ptr.p : sm.d_gen_bw_ptr.p;
+  sa.genrow = down ? sm.genrow_fw.p : sm.genrow_bw.p;
+  sa.ownr = down ? sm.ownr_fw.p : sm.ownr_bw.p;
+  return sa;
+}
+
+// per-wave kernel sequence of one smoothing leg (one launch per wavefront)
+static int64_t record_leg_waves(DevLevel& L, const double* b, double* x, const int* stop, bool down, cudaStream_t s) {
+  Smoother& sm = L.sm;
+  const int64_t n = L.n, W = sm.nwave;
   double* dbuf[2] = {L.d0.p, L.d1.p};
-  const int64_t W = sm.nwave;
+  int64_t launches = 0;
   auto wave = [&](bool init, int64_t dst, int64_t src, int dir) {
     WaveArgs a{};
     a.stop = stop;
@@ -503,44 +547,26 @@ static int64_t record_level(std::vector<DevLevel*>& lv, size_t ell, const double
     HC_CHECK_LAUNCH();
     ++launches;
   };
-  // ---- forward OSS-l1 from x = 0
-  if (W > 0) {
-    wave(true, 0, -1, 0);
-    for (int64_t d = 1; d < W; ++d) wave(false, d, d - 1, 0);
-  } else {
-    k_init_rb<<<vec_grid(n), kThreads, 0, s>>>(stop, n, b, L.r.p, x);
-    HC_CHECK_LAUNCH();
-    ++launches;
-  }
-  {
+  if (down) {
+    if (W > 0) {
+      wave(true, 0, -1, 0);
+      for (int64_t d = 1; d < W; ++d) wave(false, d, d - 1, 0);
+    } else {
+      k_init_rb<<<vec_grid(n), kThreads, 0, s>>>(stop, n, b, L.r.p, x);
+      HC_CHECK_LAUNCH();
+      ++launches;
+    }
     FinalArgs f{stop, n, W > 0 ? sm.last_row.p : nullptr, sm.grow_ptr.p, sm.gcol.p, sm.gval.p,
                 W > 0 ? dbuf[(W - 1) & 1] : nullptr, L.l1.p, L.r.p, x, L.dj.p};
     k_fw_final<<<vec_grid(n), kThreads, 0, s>>>(f);
     HC_CHECK_LAUNCH();
-    ++launches;
+    SpmvArgs a{};
+    a.stop = stop;
+    a.xin = L.dj.p;
+    a.y = L.r.p;
+    spmv<EPI_JAC_FW>(L.A, a, s);
+    return launches + 2;
   }
-  SpmvArgs a{};
-  a.stop = stop;
-  a.xin = L.dj.p;
-  a.y = L.r.p;
-  spmv<EPI_JAC_FW>(L.A, a, s);
-  ++launches;
-  // ---- coarse correction
-  DevLevel& C = *lv[ell + 1];
-  SpmvArgs rs{};
-  rs.stop = stop;
-  rs.xin = L.r.p;
-  rs.y = C.b.p;
-  spmv<EPI_SET>(L.Pt, rs, s);
-  ++launches;
-  launches += record_level(lv, ell + 1, C.b.p, C.x.p, stop, s);
-  SpmvArgs pr{};
-  pr.stop = stop;
-  pr.xin = C.x.p;
-  pr.y = x;
-  spmv<EPI_ADD>(L.P, pr, s);
-  ++launches;
-  // ---- backward OSS-l1
   SpmvArgs rj{};
   rj.stop = stop;
   rj.xin = x;
@@ -558,6 +584,62 @@ static int64_t record_level(std::vector<DevLevel*>& lv, size_t ell, const double
   spmv<EPI_JAC_BW>(L.A, jb, s);
   launches += 2;
   for (int64_t d = W - 1; d >= 0; --d) wave(false, d, d == W - 1 ? -1 : d + 1, 1);
+  return launches;
+}
+
+// One piece of a level's V-cycle work (separately launchable for profiling).
+int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* x, const int* stop, cudaStream_t s) {
+  const int64_t n = L.n;
+  if (pc == PC_COARSE) {
+    if (!n) return 0;
+    k_gemv_dense<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, kSMs * 8)), kThreads, 0, s>>>(
+        stop, n, L.Ainv.p, b, x);
+    HC_CHECK_LAUNCH();
+    return 1;
+  }
+  if (pc == PC_RESTRICT) {
+    if (L.pt_seg.nseg) {
+      launch_segmented(stop, L.Pt, L.pt_seg, L.r.p, C->b.p, s);
+      return 2;
+    }
+    SpmvArgs rs{};
+    rs.stop = stop;
+    rs.xin = L.r.p;
+    rs.y = C->b.p;
+    spmv<EPI_SET>(L.Pt, rs, s);
+    return 1;
+  }
+  if (pc == PC_PROLONG) {
+    SpmvArgs pr{};
+    pr.stop = stop;
+    pr.xin = C->x.p;
+    pr.y = x;
+    spmv<EPI_ADD>(L.P, pr, s);
+    return 1;
+  }
+  const bool down = pc == PC_DOWN;
+  const std::string& m = sweep_mode();
+  if ((m == "auto" || m == "smem") && n <= sweep_smem_max_n()) {
+    launch_sweep_smem(down, sweep_args(L, b, x, stop, down), s);
+    return 1;
+  }
+  if (m == "cluster") {
+    launch_sweep(down, sweep_args(L, b, x, stop, down), s);
+    return 1;
+  }
+  return record_leg_waves(L, b, x, stop, down, s);
+}
+
+static int64_t record_level(std::vector<DevLevel*>& lv, size_t ell, const double* b, double* x, const int* stop,
+                            cudaStream_t s) {
+  DevLevel& L = *lv[ell];
+  if (L.coarsest) return record_piece(PC_COARSE, L, nullptr, b, x, stop, s);
+  DevLevel& C = *lv[ell + 1];
+  int64_t launches = record_piece(PC_DOWN, L, &C, b, x, stop, s);
+  launches += record_piece(PC_RESTRICT, L, &C, b, x, stop, s);
+  launches += record_level(lv, ell + 1, C.b.p, C.x.p, stop, s);
+  launches += record_piece(PC_PROLONG, L, &C, b, x, stop, s);
+  launches += record_piece(PC_UP, L, &C, b, x, stop, s);
   return launches;
 }
 

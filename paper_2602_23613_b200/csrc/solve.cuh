@@ -28,6 +28,12 @@ struct Workspace {
   void ensure(int64_t n_, int64_t maxit, cudaStream_t s);
 };
 
+enum Piece : int { PC_DOWN = 0, PC_RESTRICT = 1, PC_COARSE = 2, PC_PROLONG = 3, PC_UP = 4 };
+
+// One piece of a level's V-cycle (down leg, restriction, coarsest solve,
+// prolongation, up leg); C is the next-coarser level (null on the coarsest).
+int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* x, const int* stop, cudaStream_t s);
+
 // Record one V-cycle on `stream`: x0 := V(b0) for the finest level, reading
 // b0 and writing x0 (level-0 work buffers are used for everything else).
 // Every kernel returns immediately when *stop != 0.

@@ -1,0 +1,60 @@
+// Cluster-resident smoothing legs (see sweep.cu).
+#pragma once
+#include "common.cuh"
+
+namespace hcamg {
+
+struct SweepArgs {
+  const int* stop;
+  int64_t n, nwave;
+  const int64_t* wave_ptr;   // device, nwave + 1
+  const int64_t* gen_ptr;    // device, direction-specific
+  const int32_t* genrow;     // (u, start, end) per generic row
+  const int32_t* ownr;       // (start, end) per patch entry
+  const int32_t* lastr;      // (start, end) per DoF (down leg)
+  const uint8_t* in_first;
+  const int64_t* patch_ptr;
+  const int32_t* dofs;
+  const int64_t* binv_off;
+  const double* binv;
+  const int32_t* gcol;
+  const double* gval;
+  const int64_t* ap;
+  const int32_t* ai;
+  const double* av;
+  const double* l1;
+  const double* b;
+  double* x;
+  double* r;
+  double* d0;
+  double* d1;
+  double* dj;
+  // optional fused transfer: P^T (down, rows tn) or P (up)
+  const int64_t* tp;
+  const int32_t* ti;
+  const double* tv;
+  int64_t tn;
+  double* tout;
+  const double* tin;
+};
+
+int sweep_cluster_size();
+void launch_sweep(bool down, const SweepArgs& args, cudaStream_t s);
+
+// single-CTA shared-memory legs (levels with n <= sweep_smem_max_n())
+int64_t sweep_smem_max_n();
+void launch_sweep_smem(bool down, const SweepArgs& args, cudaStream_t s);
+
+// y = T v for a CSR T with long rows: fixed 256-entry segments, one warp each,
+// then an in-order reduction of the segment partials (deterministic).
+struct SegPlan {
+  int64_t nseg = 0;
+  DBuf<int64_t> segoff;
+  DBuf<int32_t> seg_row;
+  DBuf<double> partial;
+};
+void build_segments(const DCsr& T, SegPlan& plan, cudaStream_t s);
+void launch_segmented(const int* stop, const DCsr& T, const SegPlan& plan, const double* v, double* y,
+                      cudaStream_t s);
+
+}  // namespace hcamg
