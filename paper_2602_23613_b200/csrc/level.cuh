@@ -10,6 +10,17 @@
 
 namespace hcamg {
 
+// Padded copy of the smoother structure for the prefetching cluster leg.
+struct SweepProgram {
+  int64_t m = 0;
+  DBuf<int8_t> pk;
+  DBuf<int32_t> pdof, ocnt, ogc;
+  DBuf<double> pbinv, ogv;
+  int64_t ng[2] = {0, 0};
+  DBuf<int32_t> gu[2], gcnt[2], ggc[2];
+  DBuf<double> ggv[2];
+};
+
 // OSS-l1 smoother data in wavefront order (smoothers.py:60-137).
 //
 // Patches are renumbered wave-major: wave w holds patches [wave_ptr[w],
@@ -43,7 +54,10 @@ struct Smoother {
   DBuf<int64_t> d_wave_ptr, d_gen_fw_ptr, d_gen_bw_ptr;
   // host copies for export (reference PatchSet layout, original patch order)
   std::vector<int64_t> h_patch_ptr, h_patch_dofs;
+  SweepProgram pg;
 };
+
+void build_program(Smoother& sm, SweepProgram& pg, cudaStream_t s);
 
 struct DevLevel {
   int64_t n = 0;

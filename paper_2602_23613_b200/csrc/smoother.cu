@@ -460,6 +460,7 @@ void build_smoother(const DCsr& A, const DCsr& G, Smoother& sm, cudaStream_t s) 
   sm.d_wave_ptr.upload(sm.wave_ptr.data(), (int64_t)sm.wave_ptr.size(), s);
   sm.d_gen_fw_ptr.upload(sm.gen_fw_ptr.data(), (int64_t)sm.gen_fw_ptr.size(), s);
   sm.d_gen_bw_ptr.upload(sm.gen_bw_ptr.data(), (int64_t)sm.gen_bw_ptr.size(), s);
+  build_program(sm, sm.pg, s);
   HC_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -143,6 +143,10 @@ __global__ void __launch_bounds__(kThreads) k_wave(WaveArgs a) {
   if (p >= a.p1) return;
   const int64_t e0 = a.patch_ptr[p];
   const int k = (int)(a.patch_ptr[p + 1] - e0);
+  const double* Bi = a.binv + a.binv_off[p];
+  double bcol[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) bcol[c] = (c < k && lane < k) ? __ldg(Bi + (int64_t)c * k + lane) : 0.0;
   int32_t i = 0;
   double v = 0.0;
   if (lane < k) {
@@ -161,9 +165,10 @@ __global__ void __launch_bounds__(kThreads) k_wave(WaveArgs a) {
     }
   }
   // d = B_p^{-1} r[patch]  (column-major inverse: coalesced over the lanes)
-  const double* Bi = a.binv + a.binv_off[p];
   double d = 0.0;
-  for (int c = 0; c < k; ++c) {
+#pragma unroll
+  for (int c = 0; c < 16; ++c) d = fma(bcol[c], __shfl_sync(0xffffffffu, v, c), d);
+  for (int c = 16; c < k; ++c) {
     const double vc = __shfl_sync(0xffffffffu, v, c);
     if (lane < k) d = fma(Bi[(int64_t)c * k + lane], vc, d);
   }
@@ -619,12 +624,61 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
   }
   const bool down = pc == PC_DOWN;
   const std::string& m = sweep_mode();
-  if ((m == "auto" || m == "smem") && n <= sweep_smem_max_n()) {
+  if (m == "smem" && n <= sweep_smem_max_n()) {
     launch_sweep_smem(down, sweep_args(L, b, x, stop, down), s);
     return 1;
   }
   if (m == "cluster") {
     launch_sweep(down, sweep_args(L, b, x, stop, down), s);
+    return 1;
+  }
+  if (m == "auto" || m == "leg") {
+    Smoother& sm = L.sm;
+    SweepProgram& pg = sm.pg;
+    LegArgs la{};
+    la.stop = stop;
+    la.n = n;
+    la.nwave = sm.nwave;
+    la.m = pg.m;
+    la.wave_ptr = sm.d_wave_ptr.p;
+    la.gen_fw_ptr = sm.d_gen_fw_ptr.p;
+    la.gen_bw_ptr = sm.d_gen_bw_ptr.p;
+    la.pk = pg.pk.p;
+    la.pdof = pg.pdof.p;
+    la.pbinv = pg.pbinv.p;
+    la.ocnt = pg.ocnt.p;
+    la.ogc = pg.ogc.p;
+    la.ogv = pg.ogv.p;
+    for (int d = 0; d < 2; ++d) {
+      la.ng[d] = pg.ng[d];
+      la.gu[d] = pg.gu[d].p;
+      la.gcnt[d] = pg.gcnt[d].p;
+      la.ggc[d] = pg.ggc[d].p;
+      la.ggv[d] = pg.ggv[d].p;
+    }
+    la.genrow_fw = sm.genrow_fw.p;
+    la.genrow_bw = sm.genrow_bw.p;
+    la.ownr_fw = sm.ownr_fw.p;
+    la.ownr_bw = sm.ownr_bw.p;
+    la.lastr = sm.lastr.p;
+    la.in_first = sm.in_first.p;
+    la.patch_ptr = sm.patch_ptr.p;
+    la.dofs = sm.patch_dofs.p;
+    la.binv_off = sm.binv_off.p;
+    la.binv = sm.binv.p;
+    la.gcol = sm.gcol.p;
+    la.gval = sm.gval.p;
+    la.ap = L.A.ptr.p;
+    la.ai = L.A.idx.p;
+    la.av = L.A.val.p;
+    la.l1 = L.l1.p;
+    la.b = b;
+    la.x = x;
+    la.r = L.r.p;
+    la.d0 = L.d0.p;
+    la.d1 = L.d1.p;
+    la.dj = L.dj.p;
+    launch_leg(down, la, s);
     return 1;
   }
   return record_leg_waves(L, b, x, stop, down, s);

@@ -56,6 +56,10 @@ __device__ __forceinline__ void patch_solve(const SweepArgs& a, int64_t p, const
                                             double* ddst, int lane) {
   const int64_t e0 = a.patch_ptr[p];
   const int k = (int)(a.patch_ptr[p + 1] - e0);
+  const double* Bi = a.binv + a.binv_off[p];
+  double bcol[16];  // this lane's row of B_p^{-1}, loaded before the pulls (memory-level parallelism)
+#pragma unroll
+  for (int c = 0; c < 16; ++c) bcol[c] = (c < k && lane < k) ? __ldg(Bi + (int64_t)c * k + lane) : 0.0;
   int32_t i = 0;
   double v = 0.0;
   if (lane < k) {
@@ -73,9 +77,10 @@ __device__ __forceinline__ void patch_solve(const SweepArgs& a, int64_t p, const
       }
     }
   }
-  const double* Bi = a.binv + a.binv_off[p];
   double d = 0.0;
-  for (int c = 0; c < k; ++c) {
+#pragma unroll
+  for (int c = 0; c < 16; ++c) d = fma(bcol[c], __shfl_sync(0xffffffffu, v, c), d);
+  for (int c = 16; c < k; ++c) {
     const double vc = __shfl_sync(0xffffffffu, v, c);
     if (lane < k) d = fma(Bi[(int64_t)c * k + lane], vc, d);
   }
@@ -96,8 +101,21 @@ __device__ __forceinline__ void rows8(const int64_t* __restrict__ mp, const int3
   for (int64_t it = 0; it < iters; ++it) {
     const int64_t row = g0 + it * ng;
     double s = 0.0;
-    if (row < nrows)
-      for (int64_t e = mp[row] + lg; e < mp[row + 1]; e += 8) s = fma(mv[e], v[mi[e]], s);
+    if (row < nrows) {
+      const int64_t e1 = mp[row + 1];
+      for (int64_t e0 = mp[row] + lg; e0 < e1; e0 += 32) {
+        int32_t c[4];
+        double w[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const bool ok = e0 + 8 * t < e1;
+          c[t] = ok ? __ldg(mi + e0 + 8 * t) : 0;
+          w[t] = ok ? __ldg(mv + e0 + 8 * t) : 0.0;
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) s = fma(w[t], e0 + 8 * t < e1 ? v[c[t]] : 0.0, s);
+      }
+    }
     s += __shfl_xor_sync(0xffffffffu, s, 4, 8);
     s += __shfl_xor_sync(0xffffffffu, s, 2, 8);
     s += __shfl_xor_sync(0xffffffffu, s, 1, 8);

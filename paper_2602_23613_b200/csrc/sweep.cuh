@@ -38,6 +38,50 @@ struct SweepArgs {
   const double* tin;
 };
 
+// Prefetching cluster leg (sweep2.cu): padded static structure per patch/row.
+struct LegArgs {
+  const int* stop;
+  int64_t n, nwave, m;
+  const int64_t* wave_ptr;
+  const int64_t* gen_fw_ptr;
+  const int64_t* gen_bw_ptr;
+  const int8_t* pk;
+  const int32_t* pdof;
+  const double* pbinv;
+  const int32_t* ocnt;
+  const int32_t* ogc;
+  const double* ogv;
+  int64_t ng[2];
+  const int32_t* gu[2];
+  const int32_t* gcnt[2];
+  const int32_t* ggc[2];
+  const double* ggv[2];
+  // fallbacks / overflow
+  const int32_t* genrow_fw;
+  const int32_t* genrow_bw;
+  const int32_t* ownr_fw;
+  const int32_t* ownr_bw;
+  const int32_t* lastr;
+  const uint8_t* in_first;
+  const int64_t* patch_ptr;
+  const int32_t* dofs;
+  const int64_t* binv_off;
+  const double* binv;
+  const int32_t* gcol;
+  const double* gval;
+  const int64_t* ap;
+  const int32_t* ai;
+  const double* av;
+  const double* l1;
+  const double* b;
+  double* x;
+  double* r;
+  double* d0;
+  double* d1;
+  double* dj;
+};
+void launch_leg(bool down, const LegArgs& args, cudaStream_t s);
+
 int sweep_cluster_size();
 void launch_sweep(bool down, const SweepArgs& args, cudaStream_t s);
 
