@@ -797,6 +797,25 @@ int hcamg_profile_vcycle(hcamg_handle* h, int32_t reps, int32_t cap, int32_t* ki
   });
 }
 
+// Debug (not in the public header): record per-phase timestamps of one
+// level-0 down leg into host buffer `out` (phases x warps x 2 int64).
+int hcamg_debug_trace_leg(hcamg_handle* h, int down, long long* out, int64_t cap) {
+  return guarded(h, [&] {
+    require_hierarchy(h);
+    cudaStream_t s = h->stream;
+    ensure_ws(h, 1);
+    DBuf<long long> tr(cap, s);
+    tr.zero();
+    hcamg::g_leg_trace = tr.p;
+    DevLevel& L = *h->lv[0];
+    DevLevel* C = h->lv.size() > 1 ? h->lv[1] : nullptr;
+    for (int r = 0; r < 3; ++r) record_piece(down ? PC_DOWN : PC_UP, L, C, h->ws.r.p, h->ws.z.p, h->ws.zero_flag.p, s);
+    hcamg::g_leg_trace = nullptr;
+    HC_CUDA(cudaMemcpyAsync(out, tr.p, sizeof(long long) * cap, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 int hcamg_spmv(hcamg_handle* h, const hcamg_csr* A, const double* x, double* y) {
   return guarded(h, [&] {
     cudaStream_t s = h->stream;

@@ -470,6 +470,8 @@ void Workspace::ensure(int64_t n_, int64_t maxit, cudaStream_t s) {
 
 // ----------------------------------------------------------------------------- V-cycle
 
+long long* g_leg_trace = nullptr;  // debug: set by hcamg_debug_trace
+
 static const std::string& sweep_mode() {
   static const std::string m = [] {
     const char* e = getenv("HCAMG_SWEEP");
@@ -678,6 +680,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     la.d0 = L.d0.p;
     la.d1 = L.d1.p;
     la.dj = L.dj.p;
+    la.trace = g_leg_trace;
     launch_leg(down, la, s);
     return 1;
   }

@@ -28,6 +28,8 @@ struct Workspace {
   void ensure(int64_t n_, int64_t maxit, cudaStream_t s);
 };
 
+extern long long* g_leg_trace;
+
 enum Piece : int { PC_DOWN = 0, PC_RESTRICT = 1, PC_COARSE = 2, PC_PROLONG = 3, PC_UP = 4 };
 
 // One piece of a level's V-cycle (down leg, restriction, coarsest solve,

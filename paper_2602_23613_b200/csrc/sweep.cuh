@@ -79,6 +79,7 @@ struct LegArgs {
   double* d0;
   double* d1;
   double* dj;
+  long long* trace;   // optional: per (phase, warp) [start, arrive] globaltimer stamps
 };
 void launch_leg(bool down, const LegArgs& args, cudaStream_t s);
 

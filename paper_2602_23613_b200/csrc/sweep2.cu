@@ -24,7 +24,7 @@ namespace hcamg {
 namespace {
 
 constexpr int kLegThreads = 512;
-constexpr int kSlots = 8;
+constexpr int kSlots = 12;
 
 // ---- program construction
 
@@ -82,8 +82,6 @@ struct PatchPre {
   int32_t i;
   int32_t cnt;
   int32_t gc[kSlots];
-  double gv[kSlots];
-  double bcol[16];
 };
 
 struct RowPre {
@@ -91,21 +89,20 @@ struct RowPre {
   int32_t u;
   int32_t cnt;
   int32_t gc[kSlots];
-  double gv[kSlots];
 };
 
+// Only the index structure is prefetched (it gates the dependent loads); the
+// coefficients (inverse column, gather weights) are loaded after the barrier
+// in parallel with the dynamic loads, keeping the register budget spill-free.
 __device__ __forceinline__ void load_patch(const LegArgs& a, int dir, int64_t p, int lane, bool own, PatchPre& q) {
   q.p = p;
   q.k = a.pk[p];
   q.i = a.pdof[p * 16 + (lane & 15)];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) q.bcol[c] = __ldg(a.pbinv + p * 256 + c * 16 + (lane & 15));
   q.cnt = own ? a.ocnt[(int64_t)dir * a.m * 16 + p * 16 + (lane & 15)] : -1;
 #pragma unroll
   for (int j = 0; j < kSlots; ++j) {
     const int64_t o = (((int64_t)dir * a.m + p) * kSlots + j) * 16 + (lane & 15);
     q.gc[j] = own ? __ldg(a.ogc + o) : 0;
-    q.gv[j] = own ? __ldg(a.ogv + o) : 0.0;
   }
 }
 
@@ -115,19 +112,21 @@ __device__ __forceinline__ void load_row(const LegArgs& a, int dir, int64_t t, R
   q.u = a.gu[dir][t];
   q.cnt = a.gcnt[dir][t];
 #pragma unroll
-  for (int j = 0; j < kSlots; ++j) {
-    q.gc[j] = __ldg(a.ggc[dir] + (int64_t)j * ng + t);
-    q.gv[j] = __ldg(a.ggv[dir] + (int64_t)j * ng + t);
-  }
+  for (int j = 0; j < kSlots; ++j) q.gc[j] = __ldg(a.ggc[dir] + (int64_t)j * ng + t);
 }
 
-__device__ __forceinline__ double slots_dot(const int32_t* gc, const double* gv, int cnt, const double* d) {
-  double dv[kSlots];
+// sum_j gv[j] d[gc[j]] with the weights streamed from `gv` (stride `gs`)
+__device__ __forceinline__ double slots_dot(const int32_t* gc, const double* __restrict__ gv, int64_t gs, int cnt,
+                                            const double* d) {
+  double dv[kSlots], w[kSlots];
 #pragma unroll
-  for (int j = 0; j < kSlots; ++j) dv[j] = j < cnt ? d[gc[j]] : 0.0;
+  for (int j = 0; j < kSlots; ++j) {
+    w[j] = j < cnt ? __ldg(gv + j * gs) : 0.0;
+    dv[j] = j < cnt ? d[gc[j]] : 0.0;
+  }
   double acc = 0.0;
 #pragma unroll
-  for (int j = 0; j < kSlots; ++j) acc = fma(gv[j], dv[j], acc);
+  for (int j = 0; j < kSlots; ++j) acc = fma(w[j], dv[j], acc);
   return acc;
 }
 
@@ -142,12 +141,17 @@ __device__ __forceinline__ double overflow_dot(const int32_t* rng, const int32_t
 __device__ __forceinline__ void solve_patch(const LegArgs& a, int dir, const PatchPre& q, int lane, bool init_x,
                                             const double* vin, const double* dsrc, double* ddst) {
   const bool act = lane < q.k;
+  const int l = lane & 15;
+  double bcol[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) bcol[c] = __ldg(a.pbinv + q.p * 256 + c * 16 + l);
   double v = 0.0, xo = 0.0;
   if (act) {
     if (!init_x) xo = a.x[q.i];
     v = vin[q.i];
     if (q.cnt >= 0) {
-      v -= slots_dot(q.gc, q.gv, q.cnt, dsrc);
+      const double* gv = a.ogv + (((int64_t)dir * a.m + q.p) * kSlots) * 16 + l;
+      v -= slots_dot(q.gc, gv, 16, q.cnt, dsrc);
       if (q.cnt > kSlots) {
         const int64_t e = a.patch_ptr[q.p] + lane;
         v -= overflow_dot((dir == 0 ? a.ownr_fw : a.ownr_bw) + 2 * e, a.gcol, a.gval, dsrc);
@@ -157,7 +161,7 @@ __device__ __forceinline__ void solve_patch(const LegArgs& a, int dir, const Pat
   }
   double d = 0.0;
 #pragma unroll
-  for (int c = 0; c < 16; ++c) d = fma(q.bcol[c], __shfl_sync(0xffffffffu, v, c), d);
+  for (int c = 0; c < 16; ++c) d = fma(bcol[c], __shfl_sync(0xffffffffu, v, c), d);
   if (act) {
     a.x[q.i] = xo + d;
     ddst[q.i] = d;
@@ -253,7 +257,9 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
     if (s > 0) {
       const int64_t src = kDown ? s - 1 : dst + 1;
       const int64_t g0 = kDown ? gp[src] : gp[src], g1 = kDown ? gp[src + 1] : gp[src + 1];
-      const int64_t t = g0 + gtid;
+      // rows go to the highest-numbered threads, patches to the lowest warps:
+      // a warp never serialises a row pull and a patch solve in one phase
+      const int64_t t = g0 + (nth - 1 - gtid);
       if (t < g1) load_row(a, dir, t, rq);
     }
   };
@@ -264,7 +270,15 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
       if (!a.in_first[u]) a.x[u] = 0.0;
     }
   }
+  auto stamp = [&](int64_t s, int which) {
+    if (a.trace && lane == 0) {
+      long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[(s * nw + wg) * 2 + which] = t;
+    }
+  };
   for (int64_t s = 0; s < W; ++s) {
+    stamp(s, 0);
     const int64_t dst = kDown ? s : W - 1 - s;
     const int64_t src = kDown ? s - 1 : dst + 1;
     const double* dsrc = s > 0 ? ((src & 1) ? dbuf1 : dbuf0) : nullptr;
@@ -275,12 +289,12 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
     if (s > 0) {
       if (rq.t >= 0) {
         const double r0 = a.r[rq.u];
-        double acc = slots_dot(rq.gc, rq.gv, rq.cnt, dsrc);
+        double acc = slots_dot(rq.gc, a.ggv[dir] + rq.t, a.ng[dir], rq.cnt, dsrc);
         if (rq.cnt > kSlots) acc += overflow_dot((kDown ? a.genrow_fw : a.genrow_bw) + 3 * rq.t + 1, a.gcol, a.gval, dsrc);
         a.r[rq.u] = r0 - acc;
       }
       const int64_t g0 = gp[src], g1 = gp[src + 1];
-      for (int64_t t = g0 + gtid + nth; t < g1; t += nth) {
+      for (int64_t t = g0 + (nth - 1 - gtid) + nth; t < g1; t += nth) {
         const int32_t* g = (kDown ? a.genrow_fw : a.genrow_bw) + 3 * t;
         double acc = 0.0;
         for (int32_t k = g[1]; k < g[2]; ++k) acc = fma(a.gval[k], dsrc[a.gcol[k]], acc);
@@ -298,6 +312,7 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
       // split cluster barrier: release this phase's stores, then prefetch the
       // next phase's static structure while waiting (the loads are issued
       // after the arrive, so the release does not wait for them)
+      stamp(s, 1);
       asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
       if (s + 1 < W) prefetch(s + 1);
       asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
