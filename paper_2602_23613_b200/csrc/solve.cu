@@ -634,7 +634,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     launch_sweep(down, sweep_args(L, b, x, stop, down), s);
     return 1;
   }
-  if (m == "auto" || m == "leg") {
+  if (m == "auto" || m == "leg" || m == "dsm") {
     Smoother& sm = L.sm;
     SweepProgram& pg = sm.pg;
     LegArgs la{};
@@ -681,7 +681,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     la.d1 = L.d1.p;
     la.dj = L.dj.p;
     la.trace = g_leg_trace;
-    launch_leg(down, la, s);
+    if (m == "leg" || g_leg_trace || !launch_leg_dsm(down, la, s)) launch_leg(down, la, s);
     return 1;
   }
   return record_leg_waves(L, b, x, stop, down, s);

@@ -82,6 +82,9 @@ struct LegArgs {
   long long* trace;   // optional: per (phase, warp) [start, arrive] globaltimer stamps
 };
 void launch_leg(bool down, const LegArgs& args, cudaStream_t s);
+// DSMEM-resident variant; returns false when the level does not fit (caller falls back)
+bool launch_leg_dsm(bool down, const LegArgs& args, cudaStream_t s);
+int64_t leg_dsm_max_n();
 
 int sweep_cluster_size();
 void launch_sweep(bool down, const SweepArgs& args, cudaStream_t s);
