@@ -315,10 +315,25 @@ __device__ __forceinline__ int64_t edge_of(int64_t u, int64_t v, const int64_t* 
 }
 
 constexpr int kMatchWarps = 4;
-constexpr int kMatchCap = 2048;  // two-hop candidates per coarse node held in shared memory
+constexpr int kMatchCap = 4096;  // (j, k) candidates per coarse node (global scratch per warp)
+
+__device__ __forceinline__ bool adjacent(int64_t u, int64_t v, const int64_t* __restrict__ np_,
+                                         const int32_t* __restrict__ ni) {
+  int64_t lo = np_[u], hi = np_[u + 1];
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (ni[m] < v) lo = m + 1; else hi = m;
+  }
+  return lo < np_[u + 1] && ni[lo] == v;
+}
 
 // Enumerate, for each coarse node i (ascending), the statically valid triples
-// (i, j, k) in the reference's (j asc, k asc) order.  kWrite=false counts.
+// (i, j, k) in the reference's (j asc, k asc) order.  Only paths whose two
+// edges exist in G~ can ever be accepted (splitting.py:283-286), so the
+// candidates are generated from the edge graph (k an edge-neighbour of i, j an
+// edge-neighbour of k) and filtered by the nodal adjacency k in N(i) & N(j):
+// the same set as the reference's two-hop scan, at O(edge degree^2) per node
+// even on dense coarse levels.  kWrite=false counts.
 template <bool kWrite>
 __global__ void __launch_bounds__(32 * kMatchWarps) k_match_enum(
     const int64_t* __restrict__ coarse, int64_t ncoarse, const int8_t* __restrict__ is_c,
@@ -326,85 +341,79 @@ __global__ void __launch_bounds__(32 * kMatchWarps) k_match_enum(
     const int64_t* __restrict__ tp, const int32_t* __restrict__ ti, const int64_t* __restrict__ gp,
     const int32_t* __restrict__ gi, const double* __restrict__ gv, int64_t* __restrict__ cnt,
     const int64_t* __restrict__ off, int64_t* __restrict__ trip /* 7 per triple */, int* overflow,
-    unsigned* __restrict__ gbits, int64_t words) {
-  __shared__ int32_t cand[kMatchWarps][kMatchCap];
+    unsigned long long* __restrict__ scratch) {
+  __shared__ int ncand[kMatchWarps];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int32_t* cw = cand[w];
-  int64_t gw = (int64_t)blockIdx.x * kMatchWarps + w;
-  int64_t nw = (int64_t)gridDim.x * kMatchWarps;
+  const int64_t gw = (int64_t)blockIdx.x * kMatchWarps + w;
+  const int64_t nw = (int64_t)gridDim.x * kMatchWarps;
+  unsigned long long* keys = scratch + gw * 2 * kMatchCap;
+  unsigned long long* sorted = keys + kMatchCap;
   for (int64_t t = gw; t < ncoarse; t += nw) {
     const int64_t i = coarse[t];
-    // gather the distinct two-hop coarse nodes j > i (bitmap dedupe)
-    unsigned* bits = gbits + gw * words;
-    int nc = 0;
-    for (int64_t e = np_[i]; e < np_[i + 1]; ++e) {
-      int32_t k = ni[e];
-      const int64_t fe = np_[k + 1];
-      for (int64_t f0 = np_[k]; f0 < fe; f0 += 32) {
-        const int64_t f = f0 + lane;
-        int32_t j = f < fe ? ni[f] : -1;
-        bool ok = f < fe && j > i && is_c[j] && !(in_b[i] && in_b[j]);
-        if (ok) {
-          unsigned bit = 1u << (j & 31);
-          ok = !(atomicOr(&bits[j >> 5], bit) & bit);
-        }
-        unsigned m = __ballot_sync(0xffffffffu, ok);
-        int pos = nc + __popc(m & ((1u << lane) - 1u));
-        if (ok && pos < kMatchCap) cw[pos] = j;
-        nc += __popc(m);
+    if (lane == 0) ncand[w] = 0;
+    __syncwarp();
+    // lanes over the rows incident to i
+    for (int64_t e = tp[i] + lane; e < tp[i + 1]; e += 32) {
+      const int64_t r = ti[e];
+      if (gp[r + 1] - gp[r] != 2) continue;
+      const int64_t k = gi[gp[r]] == i ? gi[gp[r] + 1] : gi[gp[r]];
+      if (!adjacent(i, k, np_, ni)) continue;
+      for (int64_t f = tp[k]; f < tp[k + 1]; ++f) {
+        const int64_t r2 = ti[f];
+        if (gp[r2 + 1] - gp[r2] != 2) continue;
+        const int64_t j = gi[gp[r2]] == k ? gi[gp[r2] + 1] : gi[gp[r2]];
+        if (j <= i || !is_c[j] || (in_b[i] && in_b[j])) continue;
+        if (!adjacent(j, k, np_, ni)) continue;
+        const int pos = atomicAdd(&ncand[w], 1);
+        if (pos < kMatchCap) keys[pos] = ((unsigned long long)j << 32) | (unsigned long long)k;
       }
     }
-    if (nc > kMatchCap) { if (lane == 0) *overflow = 1; nc = kMatchCap; }
     __syncwarp();
-    for (int q = lane; q < nc; q += 32) bits[cw[q] >> 5] = 0u;
+    int nc = ncand[w];
+    if (nc > kMatchCap) {
+      if (lane == 0) *overflow = 1;
+      nc = kMatchCap;
+    }
+    // rank sort (stable on position), then emit unique keys in order
+    for (int q = lane; q < nc; q += 32) {
+      const unsigned long long kq = keys[q];
+      int rank = 0;
+      for (int o = 0; o < nc; ++o) {
+        const unsigned long long ko = keys[o];
+        rank += ko < kq || (ko == kq && o < q);
+      }
+      sorted[rank] = kq;
+    }
     __syncwarp();
     int64_t emitted = 0;
-    int64_t base = kWrite ? off[t] : 0;
-    // process candidates in ascending order: repeatedly extract the minimum > last
-    int32_t last = -1;
-    while (true) {
-      int32_t mn = INT32_MAX;
-      for (int q = lane; q < nc; q += 32) {
-        int32_t v = cw[q];
-        if (v > last && v < mn) mn = v;
-      }
-      for (int o = 16; o; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-      if (mn == INT32_MAX) break;
-      last = mn;
-      const int64_t j = mn;
-      // k in sorted(N(i) & N(j)): merge the two sorted neighbour lists (lane 0)
-      if (lane == 0) {
-        int64_t a = np_[i], ae = np_[i + 1], b = np_[j], be = np_[j + 1];
-        while (a < ae && b < be) {
-          int32_t ka = ni[a], kb = ni[b];
-          if (ka < kb) { ++a; continue; }
-          if (kb < ka) { ++b; continue; }
-          const int64_t k = ka;
-          ++a; ++b;
+    const int64_t base = kWrite ? off[t] : 0;
+    if (lane == 0) {
+      unsigned long long prev = ~0ull;
+      for (int q = 0; q < nc; ++q) {
+        const unsigned long long key = sorted[q];
+        if (key == prev) continue;
+        prev = key;
+        const int64_t j = (int64_t)(key >> 32), k = (int64_t)(key & 0xffffffffull);
+        if (kWrite) {
           double d0, d1;
-          int64_t e1 = edge_of(i < k ? i : k, i < k ? k : i, tp, ti, gp, gi, &d0, &d1);
-          if (e1 < 0) continue;
-          int64_t e2 = edge_of(k < j ? k : j, k < j ? j : k, tp, ti, gp, gi, &d0, &d1);
-          if (e2 < 0 || e1 == e2) continue;
-          if (kWrite) {
-            // sign1 = sign(Gt[e1, k]); sign2 = -sign(Gt[e2, k])
-            double g1 = gi[gp[e1]] == k ? gv[gp[e1]] : gv[gp[e1] + 1];
-            double g2 = gi[gp[e2]] == k ? gv[gp[e2]] : gv[gp[e2] + 1];
-            int64_t* o = trip + 7 * (base + emitted);
-            o[0] = i; o[1] = j; o[2] = k; o[3] = e1; o[4] = e2;
-            o[5] = (g1 > 0) - (g1 < 0);
-            o[6] = -((g2 > 0) - (g2 < 0));
-          }
-          ++emitted;
+          const int64_t e1 = edge_of(i < k ? i : k, i < k ? k : i, tp, ti, gp, gi, &d0, &d1);
+          const int64_t e2 = edge_of(k < j ? k : j, k < j ? j : k, tp, ti, gp, gi, &d0, &d1);
+          const double g1 = gi[gp[e1]] == k ? gv[gp[e1]] : gv[gp[e1] + 1];
+          const double g2 = gi[gp[e2]] == k ? gv[gp[e2]] : gv[gp[e2] + 1];
+          int64_t* o = trip + 7 * (base + emitted);
+          o[0] = i; o[1] = j; o[2] = k; o[3] = e1; o[4] = e2;
+          o[5] = (g1 > 0) - (g1 < 0);
+          o[6] = -((g2 > 0) - (g2 < 0));
         }
+        ++emitted;
       }
-      emitted = __shfl_sync(0xffffffffu, emitted, 0);
+      if (!kWrite) cnt[t] = emitted;
     }
-    if (!kWrite && lane == 0) cnt[t] = emitted;
     __syncwarp();
   }
 }
 
+// e1 == e2 (parallel duplicate path) is rejected at acceptance like the reference.
 // In-order acceptance scan (splitting.py:277-295): the first statically valid
 // k of each (i, j) whose mid node is unused and whose two DoFs are still free.
 __global__ void k_match_accept(const int64_t* __restrict__ trip, int64_t ntrip, uint8_t* used_mid,
@@ -418,7 +427,7 @@ __global__ void k_match_accept(const int64_t* __restrict__ trip, int64_t ntrip, 
     int64_t i = q[0], j = q[1];
     if (i == li && j == lj) continue;
     int64_t k = q[2], e1 = q[3], e2 = q[4];
-    if (used_mid[k] || !avail[e1] || !avail[e2]) continue;
+    if (e1 == e2 || used_mid[k] || !avail[e1] || !avail[e2]) continue;
     int64_t* o = pairs + 7 * cnt;
     o[0] = e1; o[1] = e2; o[2] = q[5]; o[3] = q[6]; o[4] = i; o[5] = k; o[6] = j;
     avail[e1] = 0;
@@ -505,21 +514,19 @@ void algebraic_splitting(const DCsr& A, const DCsr& G, double theta, SplitResult
   DBuf<int> overflow(1, s);
   overflow.zero();
   int blocks = (int)std::min<int64_t>(std::max<int64_t>((ncoarse + kMatchWarps - 1) / kMatchWarps, 1), kSMs * 8);
-  const int64_t words = (mt + 31) / 32;
-  DBuf<unsigned> gbits((int64_t)blocks * kMatchWarps * words, s);
-  gbits.zero();
+  DBuf<unsigned long long> scratch((int64_t)blocks * kMatchWarps * 2 * kMatchCap, s);
   if (ncoarse)
     k_match_enum<false><<<blocks, 32 * kMatchWarps, 0, s>>>(
         coarse.p, ncoarse, is_c.p, in_b.p, nbr.ptr.p, nbr.idx.p, GtT.ptr.p, GtT.idx.p, Gt.ptr.p, Gt.idx.p,
-        Gt.val.p, cnt.p, nullptr, nullptr, overflow.p, gbits.p, words);
+        Gt.val.p, cnt.p, nullptr, nullptr, overflow.p, scratch.p);
   HC_CHECK_LAUNCH();
   int64_t ntrip = exclusive_scan(cnt.p, off.p, ncoarse, s);
-  if (read_scalar(overflow.p, s)) throw Error(EUNSUPPORTED_, "matching: two-hop candidate list overflow");
+  if (read_scalar(overflow.p, s)) throw Error(EUNSUPPORTED_, "matching: candidate list overflow");
   DBuf<int64_t> trip(7 * std::max<int64_t>(ntrip, 1), s);
   if (ncoarse && ntrip)
     k_match_enum<true><<<blocks, 32 * kMatchWarps, 0, s>>>(
         coarse.p, ncoarse, is_c.p, in_b.p, nbr.ptr.p, nbr.idx.p, GtT.ptr.p, GtT.idx.p, Gt.ptr.p, Gt.idx.p,
-        Gt.val.p, nullptr, off.p, trip.p, overflow.p, gbits.p, words);
+        Gt.val.p, nullptr, off.p, trip.p, overflow.p, scratch.p);
   HC_CHECK_LAUNCH();
   DBuf<uint8_t> used_mid(mt, s), avail(n, s);
   used_mid.zero();
