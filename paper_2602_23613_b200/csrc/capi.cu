@@ -13,6 +13,7 @@
 
 #include "../../include/hcamg.h"
 #include "dense.cuh"
+#include "giant.cuh"
 #include "interp.cuh"
 #include "smoother.cuh"
 #include "solve.cuh"
@@ -241,7 +242,10 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
       break;
     }
     auto next = std::make_unique<DevLevel>();
-    galerkin(ip.P, ip.Pt, cur->A, next->A, s);
+    if (ip.hp.on) galerkin_hybrid(h->cublas, cur->A, ip.P, ip.Pt, ip.hp, next->A, s);
+    else galerkin(ip.P, ip.Pt, cur->A, next->A, s);
+    cur->hp = std::move(ip.hp);
+    if (cur->hp.on) hybrid_prepare(cur->hp, s);
     next->G = std::move(ip.Gc);
     cur->has_P = true;
     cur->P = std::move(ip.P);
@@ -581,7 +585,9 @@ int hcamg_level(hcamg_handle* h, int32_t level, hcamg_level_info* o) {
     o->nnz_A = L.A.nnz;
     o->ncols_G = L.G.ncols;
     o->nnz_G = L.G.nnz;
-    o->nnz_P = L.has_P ? L.P.nnz : 0;
+    o->nnz_P = L.has_P ? (L.hp.on ? hybrid_nnz(L.P, L.hp, h->stream) : L.P.nnz) : 0;
+    o->n_components = L.hp.on ? 1 : 0;
+    o->max_component = L.hp.on ? L.hp.nG : 0;
     o->n_pairs = L.split.n_pairs();
     o->n_interior = (int64_t)L.split.interior.size();
     o->n_coarse_nodes = (int64_t)(h->method == 0 ? L.split.pair_mesh_edges.size() : L.split.coarse_nodes.size());
@@ -599,6 +605,11 @@ int hcamg_export_csr(hcamg_handle* h, int32_t level, int32_t which, int64_t* ind
     DevLevel& L = *h->levels[(size_t)level];
     const DCsr* M = which == 0 ? &L.A : which == 1 ? (L.has_P ? &L.P : nullptr) : &L.G;
     require(M != nullptr, "level has no P");
+    DCsr full;
+    if (which == 1 && L.hp.on) {
+      hybrid_to_csr(L.P, L.hp, full, h->stream);
+      M = &full;
+    }
     cudaStream_t s = h->stream;
     if (indptr) HC_CUDA(cudaMemcpyAsync(indptr, M->ptr.p, 8 * (M->nrows + 1), cudaMemcpyDeviceToHost, s));
     if (M->nnz && indices) HC_CUDA(cudaMemcpyAsync(indices, M->idx.p, 4 * M->nnz, cudaMemcpyDeviceToHost, s));

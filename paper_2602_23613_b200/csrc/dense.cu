@@ -154,27 +154,21 @@ void batched_small_spd_inverse(const DenseJob* d_jobs, int64_t njobs, double* A,
   HC_CHECK_LAUNCH();
 }
 
-int64_t dense_cholesky(cublasHandle_t h, double* A, int64_t k, int64_t ld, cudaStream_t s) {
-  if (k == 0) return -1;
+int64_t dense_cholesky_raw(cublasHandle_t h, double* A, int64_t k, int64_t ld, double* piv, cudaStream_t s) {
+  if (k == 0) return 0;
   cublas_check(cublasSetStream(h, s), "setStream");
-  DBuf<unsigned long long> mx(1, s);
-  mx.zero();
-  k_diag_absmax<<<grid_for(k, 256), 256, 0, s>>>(A, k, ld, mx.p);
-  HC_CHECK_LAUNCH();
-  DBuf<double> piv(k, s);
   DBuf<int> bad(1, s);
   bad.fill_bytes(0xff);
   const size_t smem = sizeof(double) * kTile * (kTile + 1);
   HC_CUDA(cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const double one = 1.0, mone = -1.0;
-  int64_t j0 = k;
   for (int64_t kb = 0; kb < k; kb += kTile) {
     const int nb = (int)std::min<int64_t>(kTile, k - kb);
     double* Akk = A + kb + kb * ld;
-    k_potrf_tile<<<1, kTileThreads, smem, s>>>(Akk, ld, nb, piv.p + kb, bad.p);
+    k_potrf_tile<<<1, kTileThreads, smem, s>>>(Akk, ld, nb, piv + kb, bad.p);
     HC_CHECK_LAUNCH();
     int b = read_scalar(bad.p, s);
-    if (b >= 0) { j0 = kb + b; break; }
+    if (b >= 0) return kb + b;
     const int64_t rest = k - kb - nb;
     if (rest > 0) {
       double* A21 = Akk + nb;
@@ -185,20 +179,36 @@ int64_t dense_cholesky(cublasHandle_t h, double* A, int64_t k, int64_t ld, cudaS
                                A22, (int)ld), "dsyrk");
     }
   }
-  unsigned long long hm = read_scalar(mx.p, s);
-  double scale;
-  memcpy(&scale, &hm, 8);
+  return k;
+}
+
+int64_t pivot_verdict(const std::vector<double>& hp, int64_t k, int64_t j0, double scale) {
   const double floor_ = kPivotRtol * scale;
-  std::vector<double> hp = piv.download();
   if (j0 < k) {
     for (int64_t j = 0; j <= j0; ++j)
       if (!(hp[(size_t)j] > floor_) || !std::isfinite(hp[(size_t)j])) return j;
     return j0;
   }
+  if (k == 0) return -1;
   int64_t am = 0;
   for (int64_t j = 1; j < k; ++j)
     if (hp[(size_t)j] < hp[(size_t)am]) am = j;
   return hp[(size_t)am] <= floor_ ? am : -1;
+}
+
+int64_t dense_cholesky(cublasHandle_t h, double* A, int64_t k, int64_t ld, cudaStream_t s) {
+  if (k == 0) return -1;
+  DBuf<unsigned long long> mx(1, s);
+  mx.zero();
+  k_diag_absmax<<<grid_for(k, 256), 256, 0, s>>>(A, k, ld, mx.p);
+  HC_CHECK_LAUNCH();
+  DBuf<double> piv(k, s);
+  const int64_t j0 = dense_cholesky_raw(h, A, k, ld, piv.p, s);
+  unsigned long long hm = read_scalar(mx.p, s);
+  double scale;
+  memcpy(&scale, &hm, 8);
+  std::vector<double> hp = piv.download();
+  return pivot_verdict(hp, k, j0, scale);
 }
 
 void dense_cholesky_solve(cublasHandle_t h, const double* L, int64_t k, int64_t ld, double* B, int64_t nrhs,

@@ -7,6 +7,8 @@
 #pragma once
 #include <cublas_v2.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace hcamg {
@@ -32,6 +34,12 @@ void batched_small_spd_inverse(const DenseJob* d_jobs, int64_t njobs, double* A,
 // Large SPD factor in place (column-major, lower, leading dim ld).  Returns
 // -1 on success or the failing pivot index (reference semantics).
 int64_t dense_cholesky(cublasHandle_t h, double* A, int64_t k, int64_t ld, cudaStream_t s);
+
+// Factor in place and write the pivots; returns the index of the first
+// non-positive / non-finite pivot, or k.  No verdict.
+int64_t dense_cholesky_raw(cublasHandle_t h, double* A, int64_t k, int64_t ld, double* piv, cudaStream_t s);
+// Reference breakdown verdict from the pivots (-1: fine).
+int64_t pivot_verdict(const std::vector<double>& hp, int64_t k, int64_t j0, double scale);
 
 // B := A^{-1} B using the factor produced by dense_cholesky.
 void dense_cholesky_solve(cublasHandle_t h, const double* L, int64_t k, int64_t ld, double* B, int64_t nrhs,

@@ -1,0 +1,532 @@
+// Dense-interpolation regime (see giant.cuh).
+//
+// In 3D the interior block A_II of the reference's harmonic extension
+// (transfer.py:77-122) is one connected component with ~80 % of the DoFs
+// (SURVEY.md F3), so P has dense interior rows and the work is dense linear
+// algebra:
+//   * Cholesky of A_GG in packed lower tiles (NB = 1024, only the T(T+1)/2
+//     lower tiles are stored: 113 GB instead of 225 GB at n = 32), right-
+//     looking: own POTRF on the diagonal tile, batched cuBLAS DTRSM/DGEMM
+//     panels (FP64; cuBLAS only for these plain level-3 calls);
+//   * Z = A_GG^{-1} W' solved in place on the row-major RHS (= the
+//     column-major transpose), tile by tile from the right;
+//   * P = P_s - S_G Z applied as CSR + a dense row-major block streamed at
+//     HBM bandwidth (prolongation: one warp per row; restriction: chunked
+//     column sums reduced in a fixed order);
+//   * Galerkin A_c = P^T A P in Schur form with the solve residual
+//     rho = W' - A_GG Z (exact in exact arithmetic, second order in the
+//     component-solve error like the reference's P^T (A P)).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <vector>
+
+#include "dense.cuh"
+#include "giant.cuh"
+#include "sparse.cuh"
+
+namespace hcamg {
+
+namespace {
+
+constexpr int64_t kNB = 1024;
+
+void cb(cublasStatus_t st, const char* what) {
+  if (st != CUBLAS_STATUS_SUCCESS) throw Error(ECUDA_, std::string("cuBLAS failure in ") + what);
+}
+
+struct Packed {
+  int64_t n = 0, T = 0;
+  DBuf<double> buf;
+  double* tile(int64_t I, int64_t J) const { return buf.p + ((I * (I + 1)) / 2 + J) * kNB * kNB; }
+};
+
+__global__ void k_pack_lower(const int64_t* __restrict__ ap, const int32_t* __restrict__ ai,
+                             const double* __restrict__ av, int64_t n, int64_t T, double* __restrict__ buf) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < T * kNB;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t I = q / kNB, li = q % kNB;
+    if (q >= n) {  // identity padding keeps the padded matrix SPD
+      buf[((I * (I + 1)) / 2 + I) * kNB * kNB + li + li * kNB] = 1.0;
+      continue;
+    }
+    for (int64_t e = ap[q]; e < ap[q + 1]; ++e) {
+      const int64_t j = ai[e];
+      if (j > q) break;
+      const int64_t J = j / kNB, lj = j % kNB;
+      buf[((I * (I + 1)) / 2 + J) * kNB * kNB + li + lj * kNB] = av[e];
+    }
+  }
+}
+
+__global__ void k_csr_diag_absmax(const int64_t* __restrict__ ap, const int32_t* __restrict__ ai,
+                                  const double* __restrict__ av, int64_t n, unsigned long long* out) {
+  double m = 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = ap[q]; e < ap[q + 1]; ++e)
+      if (ai[e] == q) m = fmax(m, fabs(av[e]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+template <class T>
+const T** upload_ptrs(std::vector<const T*>& h, DBuf<const T*>& d, cudaStream_t s) {
+  d.alloc((int64_t)h.size(), s);
+  HC_CUDA(cudaMemcpyAsync(d.p, h.data(), sizeof(T*) * h.size(), cudaMemcpyHostToDevice, s));
+  return d.p;
+}
+
+// ---- hybrid P kernels
+
+// Prolongation, dense part: x[rows[q]] -= Z[q, :] . e.  One warp per row,
+// e staged in shared memory when it fits (n_c <= 25k), 4 independent 16-byte
+// loads in flight per lane.
+template <bool kSmemE>
+__global__ void __launch_bounds__(512) k_z_rows(const int* stop, int64_t nG, int64_t nc,
+                                                const double* __restrict__ Z, const int32_t* __restrict__ rows,
+                                                const double* __restrict__ e, double* __restrict__ x) {
+  if (*stop) return;
+  extern __shared__ double es[];
+  const double* ev = e;
+  if (kSmemE) {
+    for (int64_t c = threadIdx.x; c < nc; c += blockDim.x) es[c] = e[c];
+    __syncthreads();
+    ev = es;
+  }
+  const int lane = threadIdx.x & 31;
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nG;
+       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const double* z = Z + q * nc;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t c = 2 * lane;
+    for (; c + 192 + 1 < nc; c += 256) {
+      const double2 z0 = __ldcs(reinterpret_cast<const double2*>(z + c));
+      const double2 z1 = __ldcs(reinterpret_cast<const double2*>(z + c + 64));
+      const double2 z2 = __ldcs(reinterpret_cast<const double2*>(z + c + 128));
+      const double2 z3 = __ldcs(reinterpret_cast<const double2*>(z + c + 192));
+      a0 = fma(z0.x, ev[c], fma(z0.y, ev[c + 1], a0));
+      a1 = fma(z1.x, ev[c + 64], fma(z1.y, ev[c + 65], a1));
+      a2 = fma(z2.x, ev[c + 128], fma(z2.y, ev[c + 129], a2));
+      a3 = fma(z3.x, ev[c + 192], fma(z3.y, ev[c + 193], a3));
+    }
+    for (; c + 1 < nc; c += 64) {
+      const double2 z0 = __ldcs(reinterpret_cast<const double2*>(z + c));
+      a0 = fma(z0.x, ev[c], fma(z0.y, ev[c + 1], a0));
+    }
+    if (c < nc) a0 = fma(z[c], ev[c], a0);
+    double acc = (a0 + a1) + (a2 + a3);
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) x[rows[q]] -= acc;
+  }
+}
+
+// Restriction, dense part: partial[ch][c] = sum_{q in chunk ch} Z[q, c] r[rows[q]].
+// CTA = (1024-column tile, row chunk); 4 columns per thread (two 16-byte loads),
+// two rows in flight.
+constexpr int kZtCols = 1024;
+
+__global__ void __launch_bounds__(256) k_zt_partial(const int* stop, int64_t nG, int64_t nc, int64_t chunk,
+                                                    const double* __restrict__ Z, const int32_t* __restrict__ rows,
+                                                    const double* __restrict__ r, double* __restrict__ partial) {
+  if (*stop) return;
+  extern __shared__ double rv[];
+  const int64_t ch = blockIdx.y;
+  const int64_t q0 = ch * chunk, q1 = min(nG, q0 + chunk);
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) rv[q - q0] = r[rows[q]];
+  __syncthreads();
+  const int64_t c = (int64_t)blockIdx.x * kZtCols + 4 * threadIdx.x;
+  if (c >= nc) return;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  if (c + 3 < nc && (nc & 1) == 0) {
+    int64_t q = q0;
+    for (; q + 1 < q1; q += 2) {
+      const double2 u0 = __ldcs(reinterpret_cast<const double2*>(Z + q * nc + c));
+      const double2 u1 = __ldcs(reinterpret_cast<const double2*>(Z + q * nc + c + 2));
+      const double2 w0 = __ldcs(reinterpret_cast<const double2*>(Z + (q + 1) * nc + c));
+      const double2 w1 = __ldcs(reinterpret_cast<const double2*>(Z + (q + 1) * nc + c + 2));
+      const double s0 = rv[q - q0], s1 = rv[q + 1 - q0];
+      a0 = fma(w0.x, s1, fma(u0.x, s0, a0));
+      a1 = fma(w0.y, s1, fma(u0.y, s0, a1));
+      a2 = fma(w1.x, s1, fma(u1.x, s0, a2));
+      a3 = fma(w1.y, s1, fma(u1.y, s0, a3));
+    }
+    for (; q < q1; ++q) {
+      const double s0 = rv[q - q0];
+      a0 = fma(Z[q * nc + c], s0, a0);
+      a1 = fma(Z[q * nc + c + 1], s0, a1);
+      a2 = fma(Z[q * nc + c + 2], s0, a2);
+      a3 = fma(Z[q * nc + c + 3], s0, a3);
+    }
+    double* o = partial + ch * nc + c;
+    o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
+  } else {
+    for (int t = 0; t < 4 && c + t < nc; ++t) {
+      double a = 0.0;
+      for (int64_t q = q0; q < q1; ++q) a = fma(Z[q * nc + c + t], rv[q - q0], a);
+      partial[ch * nc + c + t] = a;
+    }
+  }
+}
+
+__global__ void k_zt_reduce(const int* stop, int64_t nc, int64_t nchunk, const double* __restrict__ partial,
+                            double* __restrict__ bc) {
+  if (*stop) return;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t ch = 0; ch < nchunk; ++ch) acc += partial[ch * nc + c];
+    bc[c] -= acc;
+  }
+}
+
+// ---- Galerkin helpers
+
+// Y = A_GG Z (row-major), one CTA per output row, threads over columns
+__global__ void __launch_bounds__(256) k_spmm_rows(const int64_t* __restrict__ ap, const int32_t* __restrict__ ai,
+                                                   const double* __restrict__ av, int64_t n, int64_t nc,
+                                                   const double* __restrict__ Z, double* __restrict__ Y) {
+  for (int64_t q = blockIdx.x; q < n; q += gridDim.x) {
+    for (int64_t c = threadIdx.x; c < nc; c += blockDim.x) {
+      double acc = 0.0;
+      for (int64_t e = ap[q]; e < ap[q + 1]; ++e) acc = fma(av[e], Z[(int64_t)ai[e] * nc + c], acc);
+      Y[q * nc + c] = -acc;  // rho = W' - A_GG Z: start from -A_GG Z
+    }
+  }
+}
+
+__global__ void k_add_csr_dense(const int64_t* __restrict__ wp, const int32_t* __restrict__ wi,
+                                const double* __restrict__ wv, int64_t n, int64_t nc, double* __restrict__ Y) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = wp[q]; e < wp[q + 1]; ++e) Y[q * nc + wi[e]] += wv[e];
+}
+
+// D1[:, c] = sum_q W'[q, c] Z[q, :]  (column-major nc x nc; W'^T given as CSR rows c)
+__global__ void __launch_bounds__(256) k_zt_w(const int64_t* __restrict__ tp, const int32_t* __restrict__ ti,
+                                              const double* __restrict__ tv, int64_t nc, const double* __restrict__ Z,
+                                              double* __restrict__ D1) {
+  for (int64_t c = blockIdx.x; c < nc; c += gridDim.x) {
+    for (int64_t a = threadIdx.x; a < nc; a += blockDim.x) {
+      double acc = 0.0;
+      for (int64_t e = tp[c]; e < tp[c + 1]; ++e) acc = fma(tv[e], Z[(int64_t)ti[e] * nc + a], acc);
+      D1[a + c * nc] = acc;
+    }
+  }
+}
+
+// Ac = -0.5 (D1 + D1^T) - 0.5 (E + E^T)  (exactly symmetric by construction)
+__global__ void k_combine(int64_t nc, const double* __restrict__ D1, const double* __restrict__ E,
+                          double* __restrict__ Ac) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nc * nc; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = t % nc, c = t / nc;
+    const double d = D1[a + c * nc] + D1[c + a * nc];
+    const double e = E[a + c * nc] + E[c + a * nc];
+    Ac[t] = -0.5 * d - 0.5 * e;
+  }
+}
+
+__global__ void k_add_sym_csr(const int64_t* __restrict__ sp, const int32_t* __restrict__ si,
+                              const double* __restrict__ sv, int64_t nc, double* __restrict__ Ac) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < nc; a += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = sp[a]; e < sp[a + 1]; ++e) Ac[a + (int64_t)si[e] * nc] += sv[e];
+}
+
+template <bool kWrite>
+__global__ void k_dense_to_csr(int64_t nc, const double* __restrict__ D, int64_t* __restrict__ cnt,
+                               const int64_t* __restrict__ op, int32_t* __restrict__ oi, double* __restrict__ ov) {
+  // row a of a column-major symmetric matrix = column a
+  for (int64_t a = blockIdx.x; a < nc; a += gridDim.x) {
+    __shared__ int64_t base;
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    int64_t out0 = kWrite ? op[a] : 0;
+    for (int64_t c0 = 0; c0 < nc; c0 += blockDim.x) {
+      const int64_t c = c0 + threadIdx.x;
+      const double v = c < nc ? D[c + a * nc] : 0.0;
+      const bool nz = c < nc && v != 0.0;
+      // block-wide ordered compaction
+      __shared__ int wsum[32];
+      const unsigned m = __ballot_sync(0xffffffffu, nz);
+      const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+      if (lane == 0) wsum[w] = __popc(m);
+      __syncthreads();
+      int before = 0;
+      for (int k = 0; k < w; ++k) before += wsum[k];
+      int total = 0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) total += wsum[k];
+      if (kWrite && nz) {
+        const int64_t pos = out0 + base + before + __popc(m & ((1u << lane) - 1u));
+        oi[pos] = (int32_t)c;
+        ov[pos] = v;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) base += total;
+      __syncthreads();
+    }
+    if (!kWrite && threadIdx.x == 0) cnt[a] = base;
+    __syncthreads();
+  }
+}
+
+template <bool kWrite>
+__global__ void k_hybrid_csr(int64_t n, const int64_t* __restrict__ pp, const int32_t* __restrict__ pi,
+                             const double* __restrict__ pv, const int32_t* __restrict__ rowmap, int64_t nc,
+                             const double* __restrict__ Z, int64_t* __restrict__ cnt, const int64_t* __restrict__ op,
+                             int32_t* __restrict__ oi, double* __restrict__ ov) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c_ = 0, o = kWrite ? op[u] : 0;
+    for (int64_t e = pp[u]; e < pp[u + 1]; ++e) {
+      if (kWrite) { oi[o + c_] = pi[e]; ov[o + c_] = pv[e]; }
+      ++c_;
+    }
+    const int32_t q = rowmap[u];
+    if (q >= 0) {
+      for (int64_t c = 0; c < nc; ++c) {
+        const double z = Z[(int64_t)q * nc + c];
+        if (z != 0.0) {
+          if (kWrite) { oi[o + c_] = (int32_t)c; ov[o + c_] = -z; }
+          ++c_;
+        }
+      }
+    }
+    if (!kWrite) cnt[u] = c_;
+  }
+}
+
+__global__ void k_rowmap(const int32_t* __restrict__ rows, int64_t nG, int32_t* __restrict__ map) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nG; q += (int64_t)gridDim.x * blockDim.x)
+    map[rows[q]] = (int32_t)q;
+}
+
+__global__ void k_fill_m1(int32_t* v, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] = -1;
+}
+
+}  // namespace
+
+void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m, cudaStream_t s) {
+  const int64_t n = Agg.nrows;
+  Packed L;
+  L.n = n;
+  L.T = (n + kNB - 1) / kNB;
+  const int64_t T = L.T;
+  const int64_t ntiles = T * (T + 1) / 2;
+  L.buf.alloc(ntiles * kNB * kNB, s);
+  L.buf.zero();
+  k_pack_lower<<<grid_for(T * kNB, 256), 256, 0, s>>>(Agg.ptr.p, Agg.idx.p, Agg.val.p, n, T, L.buf.p);
+  HC_CHECK_LAUNCH();
+  DBuf<unsigned long long> mx(1, s);
+  mx.zero();
+  k_csr_diag_absmax<<<grid_for(n, 256), 256, 0, s>>>(Agg.ptr.p, Agg.idx.p, Agg.val.p, n, mx.p);
+  HC_CHECK_LAUNCH();
+  unsigned long long hm = read_scalar(mx.p, s);
+  double scale;
+  memcpy(&scale, &hm, 8);
+  DBuf<double> piv(T * kNB, s);
+  cb(cublasSetStream(h, s), "setStream");
+  const double one = 1.0, mone = -1.0;
+  DBuf<const double*> dA, dB;
+  DBuf<const double*> dC;
+  int64_t fail = -1;
+  for (int64_t K = 0; K < T; ++K) {
+    const int64_t j0 = dense_cholesky_raw(h, L.tile(K, K), kNB, kNB, piv.p + K * kNB, s);
+    if (j0 < kNB) {
+      fail = K * kNB + j0;
+      break;
+    }
+    const int64_t rest = T - K - 1;
+    if (rest == 0) break;
+    {
+      std::vector<const double*> ha((size_t)rest, L.tile(K, K)), hb;
+      for (int64_t I = K + 1; I < T; ++I) hb.push_back(L.tile(I, K));
+      const double** pa = upload_ptrs(ha, dA, s);
+      const double** pb = upload_ptrs(hb, dB, s);
+      cb(cublasDtrsmBatched(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)kNB,
+                            (int)kNB, &one, pa, (int)kNB, (double* const*)pb, (int)kNB, (int)rest),
+         "dtrsmBatched");
+    }
+    {
+      std::vector<const double*> ha, hb, hc;
+      for (int64_t I = K + 1; I < T; ++I)
+        for (int64_t J = K + 1; J <= I; ++J) {
+          ha.push_back(L.tile(I, K));
+          hb.push_back(L.tile(J, K));
+          hc.push_back(L.tile(I, J));
+        }
+      const double** pa = upload_ptrs(ha, dA, s);
+      const double** pb = upload_ptrs(hb, dB, s);
+      const double** pc = upload_ptrs(hc, dC, s);
+      cb(cublasDgemmBatched(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)kNB, (int)kNB, (int)kNB, &mone, pa, (int)kNB, pb,
+                            (int)kNB, &one, (double* const*)pc, (int)kNB, (int)ha.size()),
+         "dgemmBatched");
+      HC_CUDA(cudaStreamSynchronize(s));  // host pointer vectors go out of scope
+    }
+  }
+  {
+    std::vector<double> hp = piv.download();
+    const int64_t j0 = fail >= 0 ? fail : n;
+    const int64_t bad = pivot_verdict(hp, n, std::min(j0, n), scale);
+    if (bad >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(bad) + ")", bad);
+    if (fail >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(fail) + ")", fail);
+  }
+  // Solve (A Z = B with B row-major n x m)  <=>  Z^T L L^T = B^T on the column-major m x n view.
+  auto nbk = [&](int64_t K) { return std::min(kNB, n - K * kNB); };
+  auto blk = [&](int64_t K) { return B + K * kNB * m; };
+  for (int64_t J = 0; J < T; ++J) {  // U^T = B^T L^{-T}
+    cb(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)m, (int)nbk(J),
+                   &one, L.tile(J, J), (int)kNB, blk(J), (int)m),
+       "dtrsm fwd");
+    for (int64_t I = J + 1; I < T; ++I)
+      cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)m, (int)nbk(I), (int)nbk(J), &mone, blk(J), (int)m,
+                     L.tile(I, J), (int)kNB, &one, blk(I), (int)m),
+         "dgemm fwd");
+  }
+  for (int64_t K = T - 1; K >= 0; --K) {  // Z^T = U^T L^{-1}
+    cb(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m, (int)nbk(K),
+                   &one, L.tile(K, K), (int)kNB, blk(K), (int)m),
+       "dtrsm bwd");
+    for (int64_t I = 0; I < K; ++I)
+      cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)m, (int)kNB, (int)nbk(K), &mone, blk(K), (int)m, L.tile(K, I),
+                     (int)kNB, &one, blk(I), (int)m),
+         "dgemm bwd");
+  }
+  HC_CUDA(cudaStreamSynchronize(s));
+}
+
+void hybrid_prolong(const int* stop, const HybridP& hp, const double* e, double* x, cudaStream_t s) {
+  const bool smem = hp.nc * 8 <= 200 * 1024;
+  static bool init = false;
+  if (!init) {
+    HC_CUDA(cudaFuncSetAttribute(k_z_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    init = true;
+  }
+  if (smem) {
+    // e staged once per CTA; as many 512-thread CTAs per SM as shared memory allows (<= 4)
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / std::max<int64_t>(8 * hp.nc, 1)));
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((hp.nG + 15) / 16, kSMs * per_sm));
+    k_z_rows<true><<<g, 512, sizeof(double) * hp.nc, s>>>(stop, hp.nG, hp.nc, hp.Z.p, hp.rows.p, e, x);
+  } else {
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((hp.nG + 15) / 16, kSMs * 4));
+    k_z_rows<false><<<g, 512, 0, s>>>(stop, hp.nG, hp.nc, hp.Z.p, hp.rows.p, e, x);
+  }
+  HC_CHECK_LAUNCH();
+}
+
+void hybrid_prepare(HybridP& hp, cudaStream_t s) {
+  const int64_t ct = (hp.nc + kZtCols - 1) / kZtCols;
+  const int64_t want = std::max<int64_t>(1, (4 * kSMs + ct - 1) / ct);
+  hp.chunk = std::max<int64_t>(16, std::min<int64_t>(4096, (hp.nG + want - 1) / want));
+  hp.nchunk = (hp.nG + hp.chunk - 1) / hp.chunk;
+  hp.partial.alloc(std::max<int64_t>(hp.nchunk * hp.nc, 1), s);
+}
+
+void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, cudaStream_t s) {
+  require(hp.nchunk > 0, "hybrid_restrict: plan not prepared");
+  dim3 grid((unsigned)((hp.nc + kZtCols - 1) / kZtCols), (unsigned)hp.nchunk);
+  k_zt_partial<<<grid, 256, sizeof(double) * hp.chunk, s>>>(stop, hp.nG, hp.nc, hp.chunk, hp.Z.p, hp.rows.p, r,
+                                                             hp.partial.p);
+  k_zt_reduce<<<grid_for(hp.nc, 256), 256, 0, s>>>(stop, hp.nc, hp.nchunk, hp.partial.p, bc);
+  HC_CHECK_LAUNCH();
+}
+
+void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr& Pst, const HybridP& hp, DCsr& Ac,
+                     cudaStream_t s) {
+  const int64_t nG = hp.nG, nc = hp.nc, n = A.nrows;
+  // W' = A[G, :] P_s ; A_GG
+  DBuf<int32_t> gmap(n, s);
+  k_fill_m1<<<grid_for(n, 256), 256, 0, s>>>(gmap.p, n);
+  k_rowmap<<<grid_for(nG, 256), 256, 0, s>>>(hp.rows.p, nG, gmap.p);
+  HC_CHECK_LAUNCH();
+  DCsr AG, Wp0, Wp, Agg, WpT;
+  csr_extract(A, hp.rows.p, nG, nullptr, n, AG, s);
+  spgemm(AG, Ps, Wp0, s);
+  drop_zeros(Wp0, Wp, s);
+  Wp0 = DCsr();
+  csr_extract(A, hp.rows.p, nG, gmap.p, nG, Agg, s);
+  AG = DCsr();
+  csr_transpose(Wp, WpT, s);
+  // rho = W' - A_GG Z  (row-major nG x nc)
+  DBuf<double> rho(nG * nc, s);
+  k_spmm_rows<<<(unsigned)std::min<int64_t>(nG, kSMs * 16), 256, 0, s>>>(Agg.ptr.p, Agg.idx.p, Agg.val.p, nG, nc,
+                                                                         hp.Z.p, rho.p);
+  k_add_csr_dense<<<grid_for(nG, 256), 256, 0, s>>>(Wp.ptr.p, Wp.idx.p, Wp.val.p, nG, nc, rho.p);
+  HC_CHECK_LAUNCH();
+  // E = Z^T rho (column-major nc x nc)
+  DBuf<double> E(nc * nc, s);
+  {
+    cb(cublasSetStream(h, s), "setStream");
+    const double one = 1.0, zero = 0.0;
+    cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)nc, (int)nc, (int)nG, &one, hp.Z.p, (int)nc, rho.p, (int)nc,
+                   &zero, E.p, (int)nc),
+       "dgemm Z^T rho");
+  }
+  rho.release();
+  // D1 = Z^T W'
+  DBuf<double> D1(nc * nc, s);
+  k_zt_w<<<(unsigned)std::min<int64_t>(nc, kSMs * 16), 256, 0, s>>>(WpT.ptr.p, WpT.idx.p, WpT.val.p, nc, hp.Z.p, D1.p);
+  HC_CHECK_LAUNCH();
+  // sym(P_s^T A P_s)
+  DCsr APs, Ms, Ss;
+  spgemm(A, Ps, APs, s);
+  spgemm(Pst, APs, Ms, s);
+  APs = DCsr();
+  symmetrize(Ms, Ss, s);
+  DBuf<double> Ad(nc * nc, s);
+  k_combine<<<grid_for(nc * nc, 256), 256, 0, s>>>(nc, D1.p, E.p, Ad.p);
+  k_add_sym_csr<<<grid_for(nc, 256), 256, 0, s>>>(Ss.ptr.p, Ss.idx.p, Ss.val.p, nc, Ad.p);
+  HC_CHECK_LAUNCH();
+  D1.release();
+  E.release();
+  // dense -> canonical CSR (exact zeros dropped)
+  Ac.nrows = Ac.ncols = nc;
+  Ac.ptr.alloc(nc + 1, s);
+  DBuf<int64_t> cnt(nc, s);
+  const unsigned g = (unsigned)std::min<int64_t>(nc, kSMs * 8);
+  k_dense_to_csr<false><<<g, 256, 0, s>>>(nc, Ad.p, cnt.p, nullptr, nullptr, nullptr);
+  HC_CHECK_LAUNCH();
+  Ac.nnz = exclusive_scan(cnt.p, Ac.ptr.p, nc, s);
+  Ac.idx.alloc(Ac.nnz, s);
+  Ac.val.alloc(Ac.nnz, s);
+  k_dense_to_csr<true><<<g, 256, 0, s>>>(nc, Ad.p, nullptr, Ac.ptr.p, Ac.idx.p, Ac.val.p);
+  HC_CHECK_LAUNCH();
+}
+
+namespace {
+__global__ void k_count_nz(const double* __restrict__ v, int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += v[i] != 0.0;
+  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+}
+}  // namespace
+
+int64_t hybrid_nnz(const DCsr& Ps, const HybridP& hp, cudaStream_t s) {
+  DBuf<unsigned long long> c(1, s);
+  c.zero();
+  if (hp.nG * hp.nc) k_count_nz<<<grid_for(hp.nG * hp.nc, 256, kSMs * 8), 256, 0, s>>>(hp.Z.p, hp.nG * hp.nc, c.p);
+  HC_CHECK_LAUNCH();
+  return Ps.nnz + (int64_t)read_scalar(c.p, s);
+}
+
+void hybrid_to_csr(const DCsr& Ps, const HybridP& hp, DCsr& P, cudaStream_t s) {
+  const int64_t n = Ps.nrows;
+  DBuf<int32_t> map(n, s);
+  k_fill_m1<<<grid_for(n, 256), 256, 0, s>>>(map.p, n);
+  k_rowmap<<<grid_for(hp.nG, 256), 256, 0, s>>>(hp.rows.p, hp.nG, map.p);
+  HC_CHECK_LAUNCH();
+  P.nrows = n;
+  P.ncols = Ps.ncols;
+  P.ptr.alloc(n + 1, s);
+  DBuf<int64_t> cnt(n, s);
+  k_hybrid_csr<false><<<grid_for(n, 128), 128, 0, s>>>(n, Ps.ptr.p, Ps.idx.p, Ps.val.p, map.p, hp.nc, hp.Z.p, cnt.p,
+                                                       nullptr, nullptr, nullptr);
+  HC_CHECK_LAUNCH();
+  P.nnz = exclusive_scan(cnt.p, P.ptr.p, n, s);
+  require(P.nnz < (int64_t(1) << 31), "P too large to materialise as CSR");
+  P.idx.alloc(P.nnz, s);
+  P.val.alloc(P.nnz, s);
+  k_hybrid_csr<true><<<grid_for(n, 128), 128, 0, s>>>(n, Ps.ptr.p, Ps.idx.p, Ps.val.p, map.p, hp.nc, hp.Z.p, nullptr,
+                                                      P.ptr.p, P.idx.p, P.val.p);
+  HC_CHECK_LAUNCH();
+}
+
+}  // namespace hcamg

@@ -1,0 +1,51 @@
+// Dense-interpolation regime (3D): one interior component with thousands of
+// DoFs.  Its A_GG block is factored in packed lower-triangular tiles, the
+// harmonic extension Z = A_GG^{-1} W' is kept as a dense row-major block, P
+// is applied in hybrid form (sparse part + dense block) and the Galerkin
+// product uses the Schur form with the solve residual (see giant.cu).
+#pragma once
+#include <cublas_v2.h>
+
+#include "common.cuh"
+
+namespace hcamg {
+
+constexpr int64_t kGiantMin = 4096;   // = the reference's _DENSE_COMPONENT_CUTOFF (transfer.py:35)
+
+// Factor the SPD matrix given as CSR (positions 0..n-1) into packed tiles and
+// solve A Z = B for the row-major n x m right-hand side B (overwritten by Z).
+// Throws Error(ENOTSPD_) with the reference's pivot semantics (scale =
+// max |diag|, floor 1e-13 * scale).
+void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B_rowmajor, int64_t m, cudaStream_t s);
+
+// Hybrid interpolation data of one level.
+struct HybridP {
+  bool on = false;
+  int64_t nG = 0, nc = 0;
+  DBuf<int32_t> rows;   // DoF of each dense row (ascending)
+  DBuf<double> Z;       // nG x nc row-major; P[rows[q], c] = -Z[q, c]
+  // restriction partials (deterministic chunked column reduction)
+  int64_t chunk = 512, nchunk = 0;
+  DBuf<double> partial;
+};
+
+// allocate the restriction partials (outside any graph capture)
+void hybrid_prepare(HybridP& hp, cudaStream_t s);
+// x[rows[q]] -= Z[q,:] . e   (prolongation, dense part)
+void hybrid_prolong(const int* stop, const HybridP& hp, const double* e, double* x, cudaStream_t s);
+// bc -= Z^T r[rows]            (restriction, dense part; bc already holds P_s^T r)
+void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, cudaStream_t s);
+
+// A_c = sym(P_s^T A P_s) - sym(W'^T Z) - sym(Z^T rho), rho = W' - A_GG Z
+// (= P^T A P for P = P_s - S_G Z, exactly, including the residual of the
+// component solve).  Output canonical CSR (exact zeros dropped).
+void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr& Pst, const HybridP& hp,
+                     DCsr& Ac, cudaStream_t s);
+
+// nnz of the materialised P (exact zeros of Z excluded)
+int64_t hybrid_nnz(const DCsr& Ps, const HybridP& hp, cudaStream_t s);
+
+// Materialise P = P_s - S_G Z as canonical CSR (exact zeros of Z dropped).
+void hybrid_to_csr(const DCsr& Ps, const HybridP& hp, DCsr& P, cudaStream_t s);
+
+}  // namespace hcamg

@@ -128,9 +128,11 @@ __global__ void k_fill_dense(const int64_t* __restrict__ aip, const int32_t* __r
                              const int32_t* __restrict__ label, const int32_t* __restrict__ pos,
                              const int64_t* __restrict__ cptr, const int64_t* __restrict__ kptr,
                              const int32_t* __restrict__ kcols, const int64_t* __restrict__ a_off,
-                             const int64_t* __restrict__ b_off, double* __restrict__ Ad, double* __restrict__ Bd) {
+                             const int64_t* __restrict__ b_off, double* __restrict__ Ad, double* __restrict__ Bd,
+                             int giant) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ni; q += (int64_t)gridDim.x * blockDim.x) {
     const int c = label[q];
+    if (c == giant) continue;               // dense-regime component: handled separately
     if (kptr[c + 1] == kptr[c]) continue;  // component without coarse columns: skipped
     const int64_t k = cptr[c + 1] - cptr[c];
     const int64_t a = pos[q];
@@ -150,7 +152,7 @@ __global__ void k_assemble_P(int64_t n, const int32_t* __restrict__ ext_p, const
                              const int32_t* __restrict__ int_pos, const int32_t* __restrict__ label,
                              const int32_t* __restrict__ pos, const int64_t* __restrict__ cptr,
                              const int64_t* __restrict__ kptr, const int32_t* __restrict__ kcols,
-                             const int64_t* __restrict__ b_off, const double* __restrict__ Bd,
+                             const int64_t* __restrict__ b_off, const double* __restrict__ Bd, int giant,
                              int64_t* __restrict__ cnt, const int64_t* __restrict__ pp, int32_t* __restrict__ pi,
                              double* __restrict__ pv) {
   for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n; d += (int64_t)gridDim.x * blockDim.x) {
@@ -161,6 +163,7 @@ __global__ void k_assemble_P(int64_t n, const int32_t* __restrict__ ext_p, const
     } else if (label != nullptr && int_pos[d] >= 0) {
       const int64_t q = int_pos[d];
       const int c = label[q];
+      if (c == giant) { if (!kWrite) cnt[d] = 0; continue; }
       const int64_t k = cptr[c + 1] - cptr[c];
       const int64_t nk = kptr[c + 1] - kptr[c];
       const double* Z = Bd + b_off[c] + pos[q];
@@ -192,6 +195,31 @@ __global__ void k_int_maps(const int64_t* __restrict__ interior, int64_t ni, int
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < ni; q += (int64_t)gridDim.x * blockDim.x) {
     int_pos[interior[q]] = (int32_t)q;
     rows32[q] = (int32_t)interior[q];
+  }
+}
+
+// positions of the giant component: gmap[q] = local index (or -1), mpos = member
+// positions (ascending), rows = their DoFs
+__global__ void k_giant_maps(const int32_t* __restrict__ label, const int32_t* __restrict__ pos, int64_t ni, int giant,
+                             int32_t* __restrict__ gmap, const int32_t* __restrict__ members, int64_t nG,
+                             const int64_t* __restrict__ interior, int32_t* __restrict__ mpos,
+                             int32_t* __restrict__ rows) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ni || t < nG;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    if (t < ni) gmap[t] = label[t] == giant ? pos[t] : -1;
+    if (t < nG) {
+      mpos[t] = members[t];
+      rows[t] = (int32_t)interior[members[t]];
+    }
+  }
+}
+
+__global__ void k_giant_rhs(const int32_t* __restrict__ mpos, int64_t nG, const int64_t* __restrict__ wp,
+                            const int32_t* __restrict__ wi, const double* __restrict__ wv, int64_t nc,
+                            double* __restrict__ Z) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nG; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = mpos[t];
+    for (int64_t e = wp[q]; e < wp[q + 1]; ++e) Z[t * nc + wi[e]] = wv[e];
   }
 }
 
@@ -271,6 +299,7 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
   DBuf<double> Ad, Bd;
   out.ncomp = out.max_comp = out.ncomp_large = 0;
   const bool extend = ni > 0 && npair > 0;
+  int giant = -1;
   if (extend) {
     DCsr Ai, W0, W, Aii;
     csr_extract(A, rows32.p, ni, nullptr, n, Ai, s);
@@ -337,6 +366,11 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
       a_off[(size_t)c] = at;
       b_off[(size_t)c] = bt;
       if (nk == 0) continue;
+      if (k > kGiantMin) {
+        if (giant >= 0) throw Error(EUNSUPPORTED_, "more than one interior component above the dense-regime cutoff");
+        giant = (int)c;
+        continue;
+      }
       if (k <= 32) {
         small.push_back(DenseJob{at, bt, pt, (int32_t)k, (int32_t)nk});
         small_comp.push_back(c);
@@ -356,7 +390,7 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
     Bd.zero();
     k_fill_dense<<<grid_for(ni, 128), 128, 0, s>>>(Aii.ptr.p, Aii.idx.p, Aii.val.p, W.ptr.p, W.idx.p, W.val.p, ni,
                                                    label.p, pos.p, cptr.p, kptr.p, kcols.p, a_off_d.p, b_off_d.p,
-                                                   Ad.p, Bd.p);
+                                                   Ad.p, Bd.p, giant);
     HC_CHECK_LAUNCH();
     // solves; failures reported for the first component in component order
     int64_t fail_comp = INT64_MAX, fail_piv = -1;
@@ -380,6 +414,32 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
       }
       dense_cholesky_solve(h, Ad.p + a_off[(size_t)c], k, k, Bd.p + b_off[(size_t)c], nk, k, s);
     }
+    if (giant >= 0 && giant < fail_comp) {
+      // dense-regime component: packed tiled Cholesky, Z kept dense (row-major nG x n_c)
+      const int64_t g0 = hc[(size_t)giant], nG = hc[(size_t)giant + 1] - g0;
+      HybridP& hp = out.hp;
+      hp.on = true;
+      hp.nG = nG;
+      hp.nc = npair;
+      DBuf<int32_t> gmap(ni, s), mpos(nG, s);
+      hp.rows.alloc(nG, s);
+      k_giant_maps<<<grid_for(std::max<int64_t>(ni, nG), 256), 256, 0, s>>>(label.p, pos.p, ni, giant, gmap.p,
+                                                                            members.p + g0, nG, interior.p, mpos.p,
+                                                                            hp.rows.p);
+      HC_CHECK_LAUNCH();
+      DCsr Agg;
+      csr_extract(Aii, mpos.p, nG, gmap.p, nG, Agg, s);
+      hp.Z.alloc(nG * npair, s);
+      hp.Z.zero();
+      k_giant_rhs<<<grid_for(nG, 128), 128, 0, s>>>(mpos.p, nG, W.ptr.p, W.idx.p, W.val.p, npair, hp.Z.p);
+      HC_CHECK_LAUNCH();
+      try {
+        giant_factor_solve(h, Agg, hp.Z.p, npair, s);
+      } catch (const Error& e) {
+        if (e.code == ENOTSPD_ && giant < fail_comp) { fail_comp = giant; fail_piv = e.index; }
+        else throw;
+      }
+    }
     if (fail_comp != INT64_MAX)
       throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(fail_piv) + ")", fail_piv);
     Ad.release();
@@ -393,7 +453,7 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
   int32_t* lab_p = extend ? label.p : nullptr;
   if (n)
     k_assemble_P<false><<<grid_for(n, 128), 128, 0, s>>>(n, ext_p.p, ext_v.p, int_pos.p, lab_p,
-                                                         pos.p, cptr.p, kptr.p, kcols.p, b_off_d.p, Bd.p, pc.p,
+                                                         pos.p, cptr.p, kptr.p, kcols.p, b_off_d.p, Bd.p, giant, pc.p,
                                                          nullptr, nullptr, nullptr);
   HC_CHECK_LAUNCH();
   P.nnz = exclusive_scan(pc.p, P.ptr.p, n, s);
@@ -401,7 +461,7 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
   P.val.alloc(P.nnz, s);
   if (n)
     k_assemble_P<true><<<grid_for(n, 128), 128, 0, s>>>(n, ext_p.p, ext_v.p, int_pos.p, lab_p,
-                                                        pos.p, cptr.p, kptr.p, kcols.p, b_off_d.p, Bd.p, nullptr,
+                                                        pos.p, cptr.p, kptr.p, kcols.p, b_off_d.p, Bd.p, giant, nullptr,
                                                         P.ptr.p, P.idx.p, P.val.p);
   HC_CHECK_LAUNCH();
   csr_transpose(P, out.Pt, s);

@@ -2,6 +2,7 @@
 #pragma once
 #include <cublas_v2.h>
 
+#include "giant.cuh"
 #include "split.cuh"
 
 namespace hcamg {
@@ -13,6 +14,9 @@ struct InterpResult {
   DCsr Gc;   // next-level gradient, sign-normalised (multilevel.py:71-75)
   std::vector<int64_t> gc_cols;  // nodal columns of R G kept (coarse_node_cols)
   int64_t ncomp = 0, max_comp = 0, ncomp_large = 0;
+  // dense-interpolation regime: one component above kGiantMin is kept as the
+  // dense block Z (P = P - S_G Z with P above holding only the sparse part)
+  HybridP hp;
 };
 
 // transfer.py:77-122 (+ coarse_gradient 55-74).  mode: 0 = refinement, 1 = algebraic.

@@ -5,6 +5,7 @@
 #include <string>
 #include <vector>
 
+#include "giant.cuh"
 #include "split.cuh"
 #include "sweep.cuh"
 
@@ -71,6 +72,7 @@ struct DevLevel {
   bool coarsest = false;
   DBuf<double> Ainv;     // coarsest: dense inverse (row-major n x n)
   SegPlan pt_seg;        // segmented restriction plan when P^T has long rows
+  HybridP hp;            // dense-regime interpolation block (P/Pt then hold the sparse part)
   int64_t pt_maxrow = 0;
   // work vectors
   DBuf<double> b, x, r, d0, d1, dj;

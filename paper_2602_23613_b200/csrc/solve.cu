@@ -605,6 +605,15 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     return 1;
   }
   if (pc == PC_RESTRICT) {
+    if (L.hp.on) {  // b_c = P_s^T r - Z^T r_G
+      SpmvArgs rs{};
+      rs.stop = stop;
+      rs.xin = L.r.p;
+      rs.y = C->b.p;
+      spmv<EPI_SET>(L.Pt, rs, s);
+      hybrid_restrict(stop, L.hp, L.r.p, C->b.p, s);
+      return 3;
+    }
     if (L.pt_seg.nseg) {
       launch_segmented(stop, L.Pt, L.pt_seg, L.r.p, C->b.p, s);
       return 2;
@@ -622,6 +631,10 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     pr.xin = C->x.p;
     pr.y = x;
     spmv<EPI_ADD>(L.P, pr, s);
+    if (L.hp.on) {  // x[G] -= Z x_c
+      hybrid_prolong(stop, L.hp, C->x.p, x, s);
+      return 2;
+    }
     return 1;
   }
   const bool down = pc == PC_DOWN;
@@ -681,7 +694,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     la.d1 = L.d1.p;
     la.dj = L.dj.p;
     la.trace = g_leg_trace;
-    if (m == "leg" || g_leg_trace || !launch_leg_dsm(down, la, s)) launch_leg(down, la, s);
+    if (m != "dsm" || g_leg_trace || !launch_leg_dsm(down, la, s)) launch_leg(down, la, s);
     return 1;
   }
   return record_leg_waves(L, b, x, stop, down, s);
