@@ -81,7 +81,7 @@ const T** upload_ptrs(std::vector<const T*>& h, DBuf<const T*>& d, cudaStream_t 
 // Prolongation, dense part: x[rows[q]] -= Z[q, :] . e.  One warp per row,
 // e staged in shared memory when it fits (n_c <= 25k), 4 independent 16-byte
 // loads in flight per lane.
-template <bool kSmemE>
+template <bool kSmemE, bool kSet>
 __global__ void __launch_bounds__(512) k_z_rows(const int* stop, int64_t nG, int64_t nc,
                                                 const double* __restrict__ Z, const int32_t* __restrict__ rows,
                                                 const double* __restrict__ e, double* __restrict__ x) {
@@ -116,7 +116,10 @@ __global__ void __launch_bounds__(512) k_z_rows(const int* stop, int64_t nG, int
     if (c < nc) a0 = fma(z[c], ev[c], a0);
     double acc = (a0 + a1) + (a2 + a3);
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) x[rows[q]] -= acc;
+    if (lane == 0) {
+      if (kSet) x[q] = acc;
+      else x[rows[q]] -= acc;
+    }
   }
 }
 
@@ -391,23 +394,34 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
   HC_CUDA(cudaStreamSynchronize(s));
 }
 
-void hybrid_prolong(const int* stop, const HybridP& hp, const double* e, double* x, cudaStream_t s) {
-  const bool smem = hp.nc * 8 <= 200 * 1024;
+template <bool kSet>
+static void launch_rows(const int* stop, int64_t nrows, int64_t nc, const double* Z, const int32_t* rows,
+                        const double* e, double* x, cudaStream_t s) {
+  const bool smem = nc * 8 <= 200 * 1024;
   static bool init = false;
   if (!init) {
-    HC_CUDA(cudaFuncSetAttribute(k_z_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HC_CUDA(cudaFuncSetAttribute(k_z_rows<true, kSet>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     init = true;
   }
   if (smem) {
     // e staged once per CTA; as many 512-thread CTAs per SM as shared memory allows (<= 4)
-    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / std::max<int64_t>(8 * hp.nc, 1)));
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((hp.nG + 15) / 16, kSMs * per_sm));
-    k_z_rows<true><<<g, 512, sizeof(double) * hp.nc, s>>>(stop, hp.nG, hp.nc, hp.Z.p, hp.rows.p, e, x);
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / std::max<int64_t>(8 * nc, 1)));
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nrows + 15) / 16, kSMs * per_sm));
+    k_z_rows<true, kSet><<<g, 512, sizeof(double) * nc, s>>>(stop, nrows, nc, Z, rows, e, x);
   } else {
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((hp.nG + 15) / 16, kSMs * 4));
-    k_z_rows<false><<<g, 512, 0, s>>>(stop, hp.nG, hp.nc, hp.Z.p, hp.rows.p, e, x);
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nrows + 15) / 16, kSMs * 4));
+    k_z_rows<false, kSet><<<g, 512, 0, s>>>(stop, nrows, nc, Z, rows, e, x);
   }
   HC_CHECK_LAUNCH();
+}
+
+void hybrid_prolong(const int* stop, const HybridP& hp, const double* e, double* x, cudaStream_t s) {
+  launch_rows<false>(stop, hp.nG, hp.nc, hp.Z.p, hp.rows.p, e, x, s);
+}
+
+void dense_gemv_rows(const int* stop, int64_t n, int64_t m, const double* M, const double* e, double* x,
+                     cudaStream_t s) {
+  launch_rows<true>(stop, n, m, M, nullptr, e, x, s);
 }
 
 void hybrid_prepare(HybridP& hp, cudaStream_t s) {

@@ -33,6 +33,9 @@ struct HybridP {
 void hybrid_prepare(HybridP& hp, cudaStream_t s);
 // x[rows[q]] -= Z[q,:] . e   (prolongation, dense part)
 void hybrid_prolong(const int* stop, const HybridP& hp, const double* e, double* x, cudaStream_t s);
+// x = M e for a dense row-major n x m matrix (HBM-streaming GEMV)
+void dense_gemv_rows(const int* stop, int64_t n, int64_t m, const double* M, const double* e, double* x,
+                     cudaStream_t s);
 // bc -= Z^T r[rows]            (restriction, dense part; bc already holds P_s^T r)
 void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, cudaStream_t s);
 

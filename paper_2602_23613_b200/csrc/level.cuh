@@ -33,6 +33,7 @@ struct SweepProgram {
 // next wave are pulled by that patch's warp, the others by generic threads.
 struct Smoother {
   int64_t npatch = 0, nwave = 0, kmax = 0;
+  int64_t max_wave_patches = 0, max_gen_rows = 0;  // cluster-leg eligibility
   std::vector<int64_t> wave_ptr;        // host copy (launch geometry)
   DBuf<int64_t> patch_ptr;              // reordered patches -> entries
   DBuf<int32_t> patch_dofs;             // entry -> DoF

@@ -461,6 +461,12 @@ void build_smoother(const DCsr& A, const DCsr& G, Smoother& sm, cudaStream_t s) 
   sm.d_gen_fw_ptr.upload(sm.gen_fw_ptr.data(), (int64_t)sm.gen_fw_ptr.size(), s);
   sm.d_gen_bw_ptr.upload(sm.gen_bw_ptr.data(), (int64_t)sm.gen_bw_ptr.size(), s);
   build_program(sm, sm.pg, s);
+  sm.max_wave_patches = sm.max_gen_rows = 0;
+  for (int64_t w = 0; w < sm.nwave; ++w) {
+    sm.max_wave_patches = std::max(sm.max_wave_patches, sm.wave_ptr[(size_t)w + 1] - sm.wave_ptr[(size_t)w]);
+    sm.max_gen_rows = std::max(sm.max_gen_rows, sm.gen_fw_ptr[(size_t)w + 1] - sm.gen_fw_ptr[(size_t)w]);
+    sm.max_gen_rows = std::max(sm.max_gen_rows, sm.gen_bw_ptr[(size_t)w + 1] - sm.gen_bw_ptr[(size_t)w]);
+  }
   HC_CUDA(cudaStreamSynchronize(s));
 }
 

@@ -599,9 +599,13 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
   const int64_t n = L.n;
   if (pc == PC_COARSE) {
     if (!n) return 0;
-    k_gemv_dense<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, kSMs * 8)), kThreads, 0, s>>>(
-        stop, n, L.Ainv.p, b, x);
-    HC_CHECK_LAUNCH();
+    if (n >= 8192) {
+      dense_gemv_rows(stop, n, n, L.Ainv.p, b, x, s);
+    } else {
+      k_gemv_dense<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, kSMs * 8)), kThreads, 0, s>>>(
+          stop, n, L.Ainv.p, b, x);
+      HC_CHECK_LAUNCH();
+    }
     return 1;
   }
   if (pc == PC_RESTRICT) {
@@ -647,7 +651,8 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     launch_sweep(down, sweep_args(L, b, x, stop, down), s);
     return 1;
   }
-  if (m == "auto" || m == "leg" || m == "dsm") {
+  const bool wide = L.sm.max_wave_patches > 256 || L.sm.max_gen_rows > 8192;
+  if ((m == "auto" && !wide) || m == "leg" || m == "dsm") {
     Smoother& sm = L.sm;
     SweepProgram& pg = sm.pg;
     LegArgs la{};

@@ -95,6 +95,7 @@ class Level:
 
     def __init__(self, A=None, G=None, P=None, patches=None, l1=None, coarse_factor=None, splitting=None):
         self._dev, self._idx, self._info = None, None, None
+        self._version = 0  # bumped by user assignments (not by lazy materialisation)
         self._vals = dict(A=A, G=G, P=P, patches=patches, l1=l1, coarse_factor=coarse_factor,
                           splitting=splitting)
 
@@ -120,6 +121,7 @@ def _field(name):
 
     def put(self, value):
         self._vals[name] = value
+        self._version += 1
 
     return property(get, put)
 
@@ -307,13 +309,13 @@ def build_hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_
     h = Hierarchy(levels, method, bool(info.stalled), dev.notes())
     h._dev = dev
     h._key = _hier_key(h)
+    h._host_A = (system.A, A)
     h.setup_seconds = float(info.setup_seconds)
     return h
 
 
 def _hier_key(h):
-    return tuple((id(lv),) + tuple(id(lv._vals.get(f)) for f in ("A", "G", "P", "coarse_factor"))
-                 for lv in h.levels)
+    return tuple((id(lv), lv._version) for lv in h.levels)
 
 
 def _device_for(h):
@@ -431,7 +433,9 @@ def pcg(A, b, precond, x0=None, tol=1e-8, maxit=500, oc=1.0):
     rep = _lib.Report()
     x = np.empty_like(b)
     h = _candidate_hierarchy(precond)
-    if h is not None and h.levels[0].n == b.shape[0] and _same_matrix(A, h.levels[0].A):
+    host_A = getattr(h, "_host_A", ()) if h is not None else ()
+    if h is not None and h.levels[0].n == b.shape[0] and (
+            any(A is M for M in host_A) or _same_matrix(A, host_A[1] if host_A else h.levels[0].A)):
         dev = _device_for(h)
         probe = np.random.default_rng(12345).standard_normal(b.shape[0])
         if isinstance(precond, Hierarchy) or np.array_equal(precond(probe), vcycle(h, probe)):
