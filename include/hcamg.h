@@ -115,6 +115,11 @@ int hcamg_export_csr(hcamg_handle* h, int32_t level, int32_t which, int64_t* ind
 int hcamg_export_splitting(hcamg_handle* h, int32_t level, int64_t* pairs, int64_t* interior,
                            int64_t* coarse_nodes);
 int hcamg_export_l1(hcamg_handle* h, int32_t level, double* d);
+/* Dense-regime data: which 0 = interpolation block Z (n_G x n_c row-major,
+ * P[rows[q], c] = -Z[q, c]), 1 = its DoF rows (int64), 2 = the coarsest
+ * level's dense inverse (n x n).  hcamg_export_csr which = 3 gives the sparse
+ * part of a hybrid P; hcamg_level_info.max_component = n_G, .pad = its nnz. */
+int hcamg_export_dense(hcamg_handle* h, int32_t level, int32_t which, void* out);
 /* patches in reference order: ptr (n_patches + 1), dofs (n_patch_entries), wave of each patch */
 int hcamg_export_patches(hcamg_handle* h, int32_t level, int64_t* ptr, int64_t* dofs, int64_t* wave);
 int hcamg_export_coarse_cols(hcamg_handle* h, int32_t level, int64_t* cols);

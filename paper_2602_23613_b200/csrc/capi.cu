@@ -588,6 +588,7 @@ int hcamg_level(hcamg_handle* h, int32_t level, hcamg_level_info* o) {
     o->nnz_P = L.has_P ? (L.hp.on ? hybrid_nnz(L.P, L.hp, h->stream) : L.P.nnz) : 0;
     o->n_components = L.hp.on ? 1 : 0;
     o->max_component = L.hp.on ? L.hp.nG : 0;
+    o->pad = L.hp.on ? L.P.nnz : 0;  // nnz of the sparse part of a hybrid P
     o->n_pairs = L.split.n_pairs();
     o->n_interior = (int64_t)L.split.interior.size();
     o->n_coarse_nodes = (int64_t)(h->method == 0 ? L.split.pair_mesh_edges.size() : L.split.coarse_nodes.size());
@@ -603,8 +604,12 @@ int hcamg_export_csr(hcamg_handle* h, int32_t level, int32_t which, int64_t* ind
   return guarded(h, [&] {
     require(level >= 0 && level < (int32_t)h->levels.size(), "level out of range");
     DevLevel& L = *h->levels[(size_t)level];
-    const DCsr* M = which == 0 ? &L.A : which == 1 ? (L.has_P ? &L.P : nullptr) : &L.G;
+    const DCsr* M = which == 0 ? &L.A : (which == 1 || which == 3) ? (L.has_P ? &L.P : nullptr) : &L.G;
     require(M != nullptr, "level has no P");
+    if (which == 3) {  // sparse part of a hybrid P (the whole P otherwise)
+      require(L.has_P, "level has no P");
+      M = &L.P;
+    }
     DCsr full;
     if (which == 1 && L.hp.on) {
       hybrid_to_csr(L.P, L.hp, full, h->stream);
@@ -626,6 +631,30 @@ int hcamg_export_splitting(hcamg_handle* h, int32_t level, int64_t* pairs, int64
     if (interior && !sp.interior.empty()) memcpy(interior, sp.interior.data(), 8 * sp.interior.size());
     const std::vector<int64_t>& cn = h->method == 0 ? sp.pair_mesh_edges : sp.coarse_nodes;
     if (coarse_nodes && !cn.empty()) memcpy(coarse_nodes, cn.data(), 8 * cn.size());
+  });
+}
+
+int hcamg_export_dense(hcamg_handle* h, int32_t level, int32_t which, void* out) {
+  return guarded(h, [&] {
+    require(level >= 0 && level < (int32_t)h->levels.size(), "level out of range");
+    DevLevel& L = *h->levels[(size_t)level];
+    cudaStream_t s = h->stream;
+    if (which == 0) {
+      require(L.hp.on, "level has no dense interpolation block");
+      HC_CUDA(cudaMemcpyAsync(out, L.hp.Z.p, 8 * L.hp.nG * L.hp.nc, cudaMemcpyDeviceToHost, s));
+    } else if (which == 1) {
+      require(L.hp.on, "level has no dense interpolation block");
+      std::vector<int32_t> r((size_t)L.hp.nG);
+      HC_CUDA(cudaMemcpyAsync(r.data(), L.hp.rows.p, 4 * L.hp.nG, cudaMemcpyDeviceToHost, s));
+      HC_CUDA(cudaStreamSynchronize(s));
+      for (int64_t q = 0; q < L.hp.nG; ++q) static_cast<int64_t*>(out)[q] = r[(size_t)q];
+    } else if (which == 2) {
+      require(L.coarsest && L.Ainv.p, "not the coarsest level");
+      HC_CUDA(cudaMemcpyAsync(out, L.Ainv.p, 8 * L.n * L.n, cudaMemcpyDeviceToHost, s));
+    } else {
+      require(false, "unknown dense export");
+    }
+    HC_CUDA(cudaStreamSynchronize(s));
   });
 }
 
