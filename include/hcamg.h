@@ -102,6 +102,13 @@ int hcamg_hier_end(hcamg_handle* h, hcamg_info* info);
  * matrix whose Cholesky factor the user attached as Level.coarse_factor. */
 int hcamg_hier_end_with(hcamg_handle* h, const hcamg_csr* coarse_matrix, hcamg_info* info);
 
+/* ---- level-0 splitting only: build_algebraic_splitting (splitting.py:246-298)
+ * on (A, G) without the interpolation; sizes[4] = n_pairs, n_interior,
+ * n_coarse_nodes, n_candidate_triples.  Lets the bit-exact integer parity be
+ * checked at sizes whose full hierarchy is infeasible. */
+int hcamg_split_alg(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* G, double theta, int64_t* sizes);
+int hcamg_split_export(hcamg_handle* h, int64_t* pairs, int64_t* interior, int64_t* coarse_nodes);
+
 /* ---- queries / exports (lazily materialised Level fields) -------------- */
 int hcamg_info_get(hcamg_handle* h, hcamg_info* info);
 int hcamg_notes(hcamg_handle* h, char* buf, int64_t cap);   /* '\n'-separated Hierarchy.notes */

@@ -57,6 +57,8 @@ struct hcamg_handle {
   int64_t err_index = -1;
   // user-assembled hierarchy under construction
   std::vector<std::unique_ptr<DevLevel>> pending;
+  // result of the last hcamg_split_alg (level-0 splitting only)
+  SplitResult last_split;
 };
 
 namespace {
@@ -559,6 +561,31 @@ int hcamg_hier_end_with(hcamg_handle* h, const hcamg_csr* coarse_matrix, hcamg_i
 }
 
 int hcamg_hier_end(hcamg_handle* h, hcamg_info* info) { return hcamg_hier_end_with(h, nullptr, info); }
+
+int hcamg_split_alg(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* G, double theta, int64_t* sizes) {
+  return guarded(h, [&] {
+    require(A && G && sizes, "A, G and sizes are required");
+    DCsr dA, dG;
+    upload_csr(A, dA, h->stream);
+    upload_csr(G, dG, h->stream);
+    h->last_split = SplitResult();
+    algebraic_splitting(dA, dG, theta, h->last_split, h->stream);
+    sizes[0] = h->last_split.n_pairs();
+    sizes[1] = (int64_t)h->last_split.interior.size();
+    sizes[2] = (int64_t)h->last_split.coarse_nodes.size();
+    sizes[3] = h->last_split.n_triples;
+  });
+}
+
+int hcamg_split_export(hcamg_handle* h, int64_t* pairs, int64_t* interior, int64_t* coarse_nodes) {
+  return guarded(h, [&] {
+    const SplitResult& sp = h->last_split;
+    if (pairs && !sp.pairs.empty()) memcpy(pairs, sp.pairs.data(), 8 * sp.pairs.size());
+    if (interior && !sp.interior.empty()) memcpy(interior, sp.interior.data(), 8 * sp.interior.size());
+    if (coarse_nodes && !sp.coarse_nodes.empty())
+      memcpy(coarse_nodes, sp.coarse_nodes.data(), 8 * sp.coarse_nodes.size());
+  });
+}
 
 int hcamg_info_get(hcamg_handle* h, hcamg_info* info) {
   return guarded(h, [&] { fill_info(h, info); });

@@ -467,3 +467,20 @@ def pcg(A, b, precond, x0=None, tol=1e-8, maxit=500, oc=1.0):
         raise err[0]
     dev.check(rc)
     return x, SolveReport(int(rep.iterations), hist[:int(rep.iterations)].copy(), bool(rep.converged), oc)
+
+
+def algebraic_splitting(A, G, theta=0.25, device=0):
+    """Level-0 ``build_algebraic_splitting`` (splitting.py:246-298) on the GPU,
+    without the interpolation: returns a :class:`Splitting`."""
+    A, G = csr(A), csr(G)
+    dev = _Device(device)
+    hA, hG = HostCSR(A), HostCSR(G)
+    sizes = np.zeros(4, dtype=np.int64)
+    dev.check(dev.lib.hcamg_split_alg(dev.h, hA.ref(), hG.ref(), float(theta), ptr(sizes)))
+    npair, nint, ncg = (int(v) for v in sizes[:3])
+    pairs = np.empty((max(npair, 1), 7), dtype=np.int64)
+    interior = np.empty(max(nint, 1), dtype=np.int64)
+    cg = np.empty(max(ncg, 1), dtype=np.int64)
+    dev.check(dev.lib.hcamg_split_export(dev.h, ptr(pairs), ptr(interior), ptr(cg)))
+    return Splitting([ExteriorPair(*(int(v) for v in row)) for row in pairs[:npair]], interior[:nint].copy(),
+                     A.shape[0], coarse_nodes=cg[:ncg].copy())
