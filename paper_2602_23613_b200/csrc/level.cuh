@@ -20,6 +20,7 @@ struct SweepProgram {
   int64_t ng[2] = {0, 0};
   DBuf<int32_t> gu[2], gcnt[2], ggc[2];
   DBuf<double> ggv[2];
+  DBuf<unsigned> gbar;  // grid-barrier word of the cooperative leg (sense-reversing, starts 0)
 };
 
 // OSS-l1 smoother data in wavefront order (smoothers.py:60-137).

@@ -652,7 +652,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     return 1;
   }
   const bool wide = L.sm.max_wave_patches > 256 || L.sm.max_gen_rows > 8192;
-  if ((m == "auto" && !wide) || m == "leg" || m == "dsm") {
+  if (m == "auto" || m == "leg" || m == "dsm" || m == "grid") {
     Smoother& sm = L.sm;
     SweepProgram& pg = sm.pg;
     LegArgs la{};
@@ -699,7 +699,9 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     la.d1 = L.d1.p;
     la.dj = L.dj.p;
     la.trace = g_leg_trace;
-    if (m != "dsm" || g_leg_trace || !launch_leg_dsm(down, la, s)) launch_leg(down, la, s);
+    la.gbar = pg.gbar.p;
+    if ((m == "auto" && wide) || m == "grid") launch_leg_grid(down, la, s);
+    else if (m != "dsm" || g_leg_trace || !launch_leg_dsm(down, la, s)) launch_leg(down, la, s);
     return 1;
   }
   return record_leg_waves(L, b, x, stop, down, s);

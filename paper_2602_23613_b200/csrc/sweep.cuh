@@ -79,9 +79,12 @@ struct LegArgs {
   double* d0;
   double* d1;
   double* dj;
+  unsigned* gbar;     // grid-barrier word (cooperative leg only)
   long long* trace;   // optional: per (phase, warp) [start, arrive] globaltimer stamps
 };
 void launch_leg(bool down, const LegArgs& args, cudaStream_t s);
+// whole-GPU cooperative variant (grid.sync between wavefronts)
+void launch_leg_grid(bool down, const LegArgs& args, cudaStream_t s);
 // DSMEM-resident variant; returns false when the level does not fit (caller falls back)
 bool launch_leg_dsm(bool down, const LegArgs& args, cudaStream_t s);
 int64_t leg_dsm_max_n();

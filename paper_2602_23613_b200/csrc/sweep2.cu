@@ -205,10 +205,52 @@ __device__ void solve_patch_slow(const LegArgs& a, int dir, int64_t p, int lane,
   }
 }
 
-template <bool kDown>
+// kGrid = false: one 16-CTA cluster (split barrier.cluster); kGrid = true: the
+// whole GPU as one cooperative grid (grid.sync), for levels whose waves are
+// wider than a cluster.
+template <bool kDown, bool kGrid = false>
 __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
   if (*a.stop) return;
-  cg::cluster_group cl = cg::this_cluster();
+  // Grid barrier in two halves (arrive / wait) so the next phase's index
+  // prefetch overlaps the barrier latency, as the cluster barrier does.  The
+  // word is sense-reversing: block 0 adds 0x80000000 - (blocks - 1), the
+  // others add 1, so each barrier flips bit 31 and leaves the low bits as
+  // they were (no reset between launches).
+  struct Sync {
+    cg::cluster_group cl;
+    unsigned* bar;
+    unsigned old;
+    __device__ void arrive() {
+      if (kGrid) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+          asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(inc) : "memory");
+        }
+      } else {
+        asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      }
+    }
+    __device__ void wait() {
+      if (kGrid) {
+        if (threadIdx.x == 0) {
+          unsigned cur;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+          } while (((cur ^ old) & 0x80000000u) == 0);
+        }
+        __syncthreads();
+      } else {
+        asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      }
+    }
+    __device__ void sync() {
+      arrive();
+      wait();
+    }
+    __device__ unsigned rank() const { return kGrid ? blockIdx.x : cl.block_rank(); }
+    __device__ unsigned blocks() const { return kGrid ? gridDim.x : cl.num_blocks(); }
+  } cl{cg::this_cluster(), a.gbar, 0u};
   extern __shared__ int64_t sh_ptrs[];  // wave_ptr (W+1) then gen_ptr (W+1)
   const int64_t W = a.nwave, n = a.n;
   int64_t* wp = sh_ptrs;
@@ -218,8 +260,8 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
     wp[t] = a.wave_ptr[t];
     gp[t] = kDown ? a.gen_fw_ptr[t] : a.gen_bw_ptr[t];
   }
-  const int64_t nth = (int64_t)cl.num_blocks() * blockDim.x;
-  const int64_t gtid = (int64_t)cl.block_rank() * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)cl.blocks() * blockDim.x;
+  const int64_t gtid = (int64_t)cl.rank() * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int64_t wg = gtid >> 5, nw = nth >> 5;
   double* dbuf0 = a.d0;
@@ -313,9 +355,9 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
       // next phase's static structure while waiting (the loads are issued
       // after the arrive, so the release does not wait for them)
       stamp(s, 1);
-      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+      cl.arrive();
       if (s + 1 < W) prefetch(s + 1);
-      asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+      cl.wait();
     }
   }
   if (!kDown) return;
@@ -625,6 +667,8 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg_dsm(LegArgs a) {
 void build_program(Smoother& sm, SweepProgram& pg, cudaStream_t s) {
   const int64_t m = sm.npatch;
   pg.m = m;
+  pg.gbar.alloc(1, s);
+  pg.gbar.zero();
   pg.pk.alloc(std::max<int64_t>(m, 1), s);
   pg.pdof.alloc(std::max<int64_t>(m * 16, 1), s);
   pg.pbinv.alloc(std::max<int64_t>(m * 256, 1), s);
@@ -681,6 +725,35 @@ bool launch_leg_dsm(bool down, const LegArgs& args, cudaStream_t s) {
   if (down) HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg_dsm<true>, args));
   else HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg_dsm<false>, args));
   return true;
+}
+
+void launch_leg_grid(bool down, const LegArgs& args, cudaStream_t s) {
+  const size_t smem = sizeof(int64_t) * 2 * (size_t)(args.nwave + 1);
+  static int per_sm = 0;
+  if (!per_sm) {
+    int a = 0, b = 0;
+    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_leg<true, true>, kLegThreads, 16 * 1024));
+    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_leg<false, true>, kLegThreads, 16 * 1024));
+    per_sm = std::max(1, std::min(a, b));
+  }
+  require(smem <= 16 * 1024, "too many wavefronts for the grid leg");
+  int dev = 0, sms = kSMs;
+  HC_CUDA(cudaGetDevice(&dev));
+  HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  cudaLaunchConfig_t cfg = {};
+  int blocks = sms * per_sm;
+  if (const char* e = getenv("HCAMG_GRID_BLOCKS")) blocks = std::min(blocks, std::max(1, atoi(e)));
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(kLegThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (down) HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<true, true>, args));
+  else HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<false, true>, args));
 }
 
 void launch_leg(bool down, const LegArgs& args, cudaStream_t s) {
