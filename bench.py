@@ -135,9 +135,10 @@ class Clocks:
 PIECES = {0: "down leg", 1: "restriction", 2: "coarsest solve", 3: "prolongation", 4: "up leg"}
 
 
-def kernel_roofline(h, reps=None):
+def kernel_roofline(h, reps=None, rank=0, nranks=1):
     """Dominant V-cycle piece timed live with CUDA events (hcamg_profile_vcycle)
-    and its algorithmic bytes per launch."""
+    and its algorithmic bytes per launch (this rank's share of the dense rows
+    in the row-partitioned solve; the call is collective there)."""
     import ctypes as C
 
     from paper_2602_23613_b200 import _lib
@@ -164,11 +165,17 @@ def kernel_roofline(h, reps=None):
     if pc in (1, 3):
         nc = int(h.levels[ell + 1]._info.n)
         if int(info.max_component) > 0:
-            nbytes = 8 * int(info.max_component) * nc + B(int(info.pad), n) + 8 * (n + nc)
+            nG = int(info.max_component)
+            q0, q1 = (0, nG)
+            if nranks > 1:
+                from paper_2602_23613_b200 import dist as D
+                q0, q1 = D.plan(nG, nc, rank, nranks).rows
+            nbytes = 8 * (q1 - q0) * nc + B(int(info.pad), n) + 8 * (n + nc)
         else:
             nbytes = B(int(info.nnz_P), n) + 8 * (n + nc)
     elif pc == 2:
-        nbytes = 8 * n * n + 16 * n
+        rows = n if nranks == 1 or n < 8192 else (n * (rank + 1) // nranks - n * rank // nranks)
+        nbytes = 8 * rows * n + 16 * n
     else:
         A = lv.A
         colnnz = np.diff(A.tocsc().indptr)
@@ -423,6 +430,12 @@ def run_ours(args, world, rank, local, dist):
         h = P.build_hierarchy(system, "alg", device=local)
         setups.append(h.setup_seconds)
     log(f"setup {setups} s; levels {[lv.n for lv in h.levels]}")
+    partitioned = world > 1 and not args.replicas
+    if partitioned:
+        # one system solved by all ranks: rows of the dense blocks split, results
+        # exchanged through NVLink peer memory (paper_2602_23613_b200/dist.py)
+        from paper_2602_23613_b200 import dist as D
+        D.distribute(h)
     dev = h._dev
     lib = dev.lib
     stream = torch.cuda.ExternalStream(int(lib.hcamg_stream(dev.h)), device=f"cuda:{local}")
@@ -461,7 +474,8 @@ def run_ours(args, world, rank, local, dist):
     t_total = reduce_max(dist, sum(t_steps))
     solve_dev(rep)
     assert int(rep.iterations) == iters
-    work_total = reduce_sum(dist, float(n * iters * args.steps))
+    # replicas: every rank solves its own copy; partitioned: all ranks solve one system
+    work_total = float(n * iters * args.steps) if partitioned else reduce_sum(dist, float(n * iters * args.steps))
     value = work_total / t_total
     ms_per_step = 1e3 * t_total / args.steps
 
@@ -495,7 +509,11 @@ def run_ours(args, world, rank, local, dist):
     t_step = t_total / args.steps
     achieved_iter = B_iter * iters / t_step / 1e9
     peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
-    kr = kernel_roofline(h)
+    kr = kernel_roofline(h, rank=rank if partitioned else 0, nranks=world if partitioned else 1)
+    if partitioned:  # the iteration model counts every rank's bytes: compare with the aggregate peak
+        peak_iter = peak * world
+    else:
+        peak_iter = peak
     traffic = None
     tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tpath):
@@ -507,7 +525,7 @@ def run_ours(args, world, rank, local, dist):
     line = {
         "metric": "AMG-PCG solve DoF*iters/s", "value": value, "unit": "DoF*iters/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {
             "workload": f"BASELINE {args.config}: unit cube, {kuhn.CONFIGS[args.config]['n']}^3 hexes x 6 Kuhn tets, "
                         f"{n} free edge DoFs, alg hierarchy, PCG tol 1e-8 from x0=0, rhs uniform[-1,1] seed 0",
@@ -517,12 +535,14 @@ def run_ours(args, world, rank, local, dist):
             "final_relres": float(rep.final_relres), "true_relres": true_rel,
             "l2": "flushed (256 MiB write) before every timed step"
                   + ("; per-iteration traffic (%.1f GB) is also far above L2" % (B_iter / 1e9) if B_iter > 2e8 else ""),
-            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"row-partitioned x{world} (dense blocks and coarsest inverse split by rows, "
+                            "NVLink peer-memory exchange; smoother replicated)") if partitioned
+                           else (f"replicas x{world}" if world > 1 else "single GPU"),
         },
         "roofline": {"bound": "hbm", "achieved": kr["gbs"], "peak": peak, "unit": "GB/s", "frac": kr["gbs"] / peak,
                      "traffic": traffic, "kernel": kr["name"], "algorithmic_bytes_per_launch": kr["bytes"],
                      "avg_launch_us": kr["us"], "share_of_vcycle": kr["share"], "peak_kind": peak_kind,
-                     "iteration": {"achieved": achieved_iter, "frac": achieved_iter / peak,
+                     "iteration": {"achieved": achieved_iter, "frac": achieved_iter / peak_iter,
                                    "algorithmic_bytes_per_iteration": B_iter,
                                    "model": "SURVEY.md 8(d) B_iter, device time per PCG iteration"}},
         "e2e": {"value": e2e_value, "unit": "DoF*iters/s", "h2d_bytes_per_step": 8 * n + 128,
@@ -558,6 +578,8 @@ def main():
     ap.add_argument("--config", default="c2", help="BASELINE config: c1 (configs[0]) or c2 (configs[1], default)")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent replicas (weak scaling) instead of one row-partitioned solve")
     args = ap.parse_args()
     world, rank, local, dist = dist_setup(args.gpus)
     if args.impl == "reference":

@@ -164,6 +164,29 @@ int hcamg_pcg_generic(hcamg_handle* h, const hcamg_csr* A, const double* b, cons
 /* y = A x on the device (A uploaded per call; used by the drop-in for A @ x). */
 int hcamg_spmv(hcamg_handle* h, const hcamg_csr* A, const double* x, double* y);
 
+/* ---- Row-partitioned solve across GPUs (one process per GPU, NVLink peer memory).
+ * the reference is single-process; this replaces nothing in it
+ * and is what a multi-GPU caller of pcg / vcycle / amg_solve (multilevel.py:238,
+ * 187, 204) adds after build_hierarchy (multilevel.py:78).  Every rank builds the
+ * same hierarchy (setup is replicated); in the solve each rank streams only its
+ * rows of the dense interpolation blocks and of the coarsest inverse and
+ * exchanges the results through a symmetric buffer mapped by every rank.  The
+ * solution is bit-identical to the single-GPU solve for every rank count.
+ * Protocol: every rank calls hcamg_dist_prepare (after setup), the callers
+ * all-gather the 64-byte IPC handles in rank order, every rank calls
+ * hcamg_dist_connect; from then on vcycle / pcg / amg_solve on the handle are
+ * collective (all ranks must call them in the same order). */
+/* Allocate this rank's exchange buffer; ipc_handle (64 bytes, may be NULL)
+ * receives its CUDA IPC handle, dev_ptr (may be NULL) its device address. */
+int hcamg_dist_prepare(hcamg_handle* h, int32_t rank, int32_t nranks, void* ipc_handle, void** dev_ptr);
+/* Map the peers' buffers: ipc_handles = nranks x 64 bytes in rank order. */
+int hcamg_dist_connect(hcamg_handle* h, const void* ipc_handles);
+/* Same, for ranks living in one process on one device (bufs[r] = rank r's dev_ptr). */
+int hcamg_dist_connect_ptrs(hcamg_handle* h, void* const* bufs);
+/* Back to the single-GPU solve. */
+int hcamg_dist_disconnect(hcamg_handle* h);
+int hcamg_dist_info(hcamg_handle* h, int32_t* rank, int32_t* nranks, int32_t* connected, int64_t* buffer_bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,6 +26,7 @@ EXPORTS = [
     "hcamg_export_splitting", "hcamg_export_l1", "hcamg_export_patches", "hcamg_export_coarse_cols",
     "hcamg_vcycle", "hcamg_pcg", "hcamg_amg_solve", "hcamg_pcg_device", "hcamg_graph_launches",
     "hcamg_stream", "hcamg_pcg_generic", "hcamg_spmv", "hcamg_profile_vcycle", "hcamg_export_dense", "hcamg_split_alg", "hcamg_split_export",
+    "hcamg_dist_prepare", "hcamg_dist_connect", "hcamg_dist_connect_ptrs", "hcamg_dist_disconnect", "hcamg_dist_info",
 ]
 
 
@@ -106,6 +107,13 @@ def load(required=True):
         "hcamg_export_dense": (C.c_int, [P, C.c_int32, C.c_int32, P]),
         "hcamg_split_alg": (C.c_int, [P, C.POINTER(CSR), C.POINTER(CSR), C.c_double, P]),
         "hcamg_split_export": (C.c_int, [P, P, P, P]),
+        "hcamg_dist_prepare": (C.c_int, [P, C.c_int32, C.c_int32, P, C.POINTER(C.c_void_p)]),
+        "hcamg_dist_connect": (C.c_int, [P, P]),
+        "hcamg_dist_connect_ptrs": (C.c_int, [P, P]),
+        "hcamg_dist_disconnect": (C.c_int, [P]),
+        "hcamg_dist_info": (C.c_int, [P, P, P, P, P]),
+        # debug entry points (not in the public header)
+        "hcamg_debug_dist_piece": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

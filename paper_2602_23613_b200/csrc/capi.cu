@@ -13,6 +13,7 @@
 
 #include "../../include/hcamg.h"
 #include "dense.cuh"
+#include "dist.cuh"
 #include "giant.cuh"
 #include "interp.cuh"
 #include "smoother.cuh"
@@ -59,6 +60,8 @@ struct hcamg_handle {
   std::vector<std::unique_ptr<DevLevel>> pending;
   // result of the last hcamg_split_alg (level-0 splitting only)
   SplitResult last_split;
+  // row-partitioned solve across processes (dist.cuh)
+  Dist dist;
 };
 
 namespace {
@@ -77,6 +80,7 @@ void invalidate(hcamg_handle* h) {
 }
 
 void refresh_views(hcamg_handle* h) {
+  h->dist.release();  // a new hierarchy needs a new exchange layout
   h->lv.clear();
   for (auto& l : h->levels) h->lv.push_back(l.get());
 }
@@ -423,6 +427,19 @@ int guarded(hcamg_handle* h, F&& f) {
   }
 }
 
+// Distributed solve: a consumer that waited ~60 s for a peer flags the
+// handle (the solve then finishes on stale data); report it as an error.
+void check_dist(hcamg_handle* h) {
+  if (!h->dist.on) return;
+  int e = 0;
+  HC_CUDA(cudaMemcpyAsync(&e, h->dist.err.p, sizeof e, cudaMemcpyDeviceToHost, h->stream));
+  HC_CUDA(cudaStreamSynchronize(h->stream));
+  if (e) {
+    h->dist.err.zero();
+    throw Error(ECUDA_, "distributed solve: timed out waiting for a peer rank's exchange");
+  }
+}
+
 int pcg_breakdown(hcamg_handle* h, int error) {
   if (error == kErrPAp) {
     Ctl c = read_scalar(h->ws.ctl.p, h->stream);
@@ -476,6 +493,10 @@ void hcamg_destroy(hcamg_handle* h) {
   h->ws = Workspace();
   h->vc_b.release();
   h->vc_x.release();
+  h->dist.release();
+  h->dist.ep.release();
+  h->dist.cta.release();
+  h->dist.err.release();
   cudaStreamSynchronize(h->stream);
   if (h->cublas) cublasDestroy(h->cublas);
   if (h->aux) cudaStreamDestroy(h->aux);
@@ -743,6 +764,7 @@ int hcamg_vcycle(hcamg_handle* h, const double* b, const double* x_or_null, doub
     if (x_or_null) vec_add(n, h->ws.x.p, h->ws.z.p, h->ws.z.p, s);
     HC_CUDA(cudaMemcpyAsync(out, h->ws.z.p, 8 * n, cudaMemcpyDeviceToHost, s));
     HC_CUDA(cudaStreamSynchronize(s));
+    check_dist(h);
   });
 }
 
@@ -772,6 +794,7 @@ static int pcg_impl(hcamg_handle* h, const double* b, bool b_dev, const double* 
     if (history && rep.iterations)
       HC_CUDA(cudaMemcpyAsync(history, h->ws.hist.p, 8 * rep.iterations, cudaMemcpyDeviceToHost, s));
     HC_CUDA(cudaStreamSynchronize(s));
+    check_dist(h);
     if (report) *report = rep;
   });
 }
@@ -807,6 +830,7 @@ int hcamg_amg_solve(hcamg_handle* h, const double* b, const double* x0, double t
     if (history && rep.iterations)
       HC_CUDA(cudaMemcpyAsync(history, h->ws.hist.p, 8 * rep.iterations, cudaMemcpyDeviceToHost, s));
     HC_CUDA(cudaStreamSynchronize(s));
+    check_dist(h);
     if (report) *report = rep;
   });
 }
@@ -951,6 +975,143 @@ int hcamg_pcg_generic(hcamg_handle* h, const hcamg_csr* A, const double* b, cons
     HC_CUDA(cudaStreamSynchronize(s));
     if (rep.zero_rhs) memset(x, 0, 8 * n);
     if (report) *report = rep;
+  });
+}
+
+// ---- row-partitioned solve across processes (dist.cuh)
+
+static void dist_attach(hcamg_handle* h) {
+  for (DevLevel* L : h->lv) L->dist = &h->dist;
+  h->dist.on = true;
+  invalidate(h);
+}
+
+int hcamg_dist_prepare(hcamg_handle* h, int32_t rank, int32_t nranks, void* ipc_handle, void** dev_ptr) {
+  return guarded(h, [&] {
+    require_hierarchy(h);
+    require(nranks >= 1 && nranks <= kMaxRanks, "nranks must be in 1..8");
+    require(rank >= 0 && rank < nranks, "rank out of range");
+    cudaStream_t s = h->stream;
+    HC_CUDA(cudaStreamSynchronize(s));
+    Dist& d = h->dist;
+    d.release();
+    for (DevLevel* L : h->lv) L->dist = nullptr;
+    invalidate(h);
+    d.rank = rank;
+    d.nranks = nranks;
+    // exchange sites of every level, 256-byte aligned, identical on all ranks
+    size_t off = 0;
+    auto take = [&](int64_t nd) {
+      const size_t o = off;
+      off += ((size_t)std::max<int64_t>(nd, 1) * 8 + 255) / 256 * 256;
+      return o;
+    };
+    for (DevLevel* L : h->lv) {
+      L->xoff_g = L->xoff_y = L->xoff_c = DevLevel::kNoSite;
+      if (L->hp.on) {
+        L->xoff_g = take(kGroups * L->hp.nc);
+        L->xoff_y = take(L->hp.nG);
+      }
+      if (L->coarsest && L->n >= coarse_gemv_min()) L->xoff_c = take(L->n);
+    }
+    d.area_bytes = std::max<size_t>(off, 256);
+    d.sym_bytes = kFlagBytes + 2 * d.area_bytes;
+    HC_CUDA(cudaMalloc(&d.sym, d.sym_bytes));  // not pool memory: exported through CUDA IPC
+    HC_CUDA(cudaMemset(d.sym, 0, d.sym_bytes));
+    if (!d.ep.p) {
+      d.ep.alloc(1, s);
+      d.cta.alloc(1, s);
+      d.err.alloc(1, s);
+    }
+    d.ep.zero();
+    d.cta.zero();
+    d.err.zero();
+    HC_CUDA(cudaStreamSynchronize(s));
+    if (ipc_handle) {
+      cudaIpcMemHandle_t mh;
+      HC_CUDA(cudaIpcGetMemHandle(&mh, d.sym));
+      memcpy(ipc_handle, &mh, sizeof mh);
+    }
+    if (dev_ptr) *dev_ptr = d.sym;
+  });
+}
+
+int hcamg_dist_connect(hcamg_handle* h, const void* ipc_handles) {
+  return guarded(h, [&] {
+    Dist& d = h->dist;
+    require(d.sym != nullptr, "hcamg_dist_prepare must be called first");
+    require(ipc_handles != nullptr, "missing peer handles");
+    for (int r = 0; r < d.nranks; ++r) {
+      if (r == d.rank) {
+        d.base[r] = d.sym;
+        continue;
+      }
+      cudaIpcMemHandle_t mh;
+      memcpy(&mh, static_cast<const char*>(ipc_handles) + (size_t)r * sizeof mh, sizeof mh);
+      void* p = nullptr;
+      HC_CUDA(cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess));
+      d.base[r] = static_cast<char*>(p);
+      d.opened[r] = true;
+    }
+    dist_attach(h);
+  });
+}
+
+int hcamg_dist_connect_ptrs(hcamg_handle* h, void* const* bufs) {
+  return guarded(h, [&] {
+    Dist& d = h->dist;
+    require(d.sym != nullptr, "hcamg_dist_prepare must be called first");
+    require(bufs != nullptr, "missing peer buffers");
+    for (int r = 0; r < d.nranks; ++r) {
+      require(bufs[r] != nullptr, "null peer buffer");
+      d.base[r] = static_cast<char*>(bufs[r]);
+    }
+    require(d.base[d.rank] == d.sym, "bufs[rank] must be this handle's own buffer");
+    dist_attach(h);
+  });
+}
+
+int hcamg_dist_disconnect(hcamg_handle* h) {
+  return guarded(h, [&] {
+    HC_CUDA(cudaStreamSynchronize(h->stream));
+    h->dist.release();
+    for (DevLevel* L : h->lv) L->dist = nullptr;
+    invalidate(h);
+  });
+}
+
+int hcamg_dist_info(hcamg_handle* h, int32_t* rank, int32_t* nranks, int32_t* connected, int64_t* buffer_bytes) {
+  return guarded(h, [&] {
+    if (rank) *rank = h->dist.rank;
+    if (nranks) *nranks = h->dist.nranks;
+    if (connected) *connected = h->dist.on ? 1 : 0;
+    if (buffer_bytes) *buffer_bytes = (int64_t)h->dist.sym_bytes;
+  });
+}
+
+// Debug (not in the public header): run one piece (or one half of a piece,
+// `part` 1 = up to its exchange signal, 2 = from its wait on) of the V-cycle
+// of level `level` on the V-cycle buffers; b (host, level-0 input) is loaded
+// first when given, x (host) receives the level-0 result when given.  Lets a
+// test emulate several ranks on one GPU: every rank's part 1, then every
+// rank's part 2, so no kernel ever waits on a kernel that has not run.
+int hcamg_debug_dist_piece(hcamg_handle* h, int32_t level, int32_t piece, int32_t part, const double* b, double* x) {
+  return guarded(h, [&] {
+    require_hierarchy(h);
+    require(level >= 0 && level < (int32_t)h->lv.size(), "level out of range");
+    require(part >= 0 && part <= 2, "part must be 0, 1 or 2");
+    cudaStream_t s = h->stream;
+    ensure_ws(h, 1);
+    const int64_t n = h->levels[0]->n;
+    if (b) HC_CUDA(cudaMemcpyAsync(h->ws.r.p, b, 8 * n, cudaMemcpyHostToDevice, s));
+    DevLevel& L = *h->lv[(size_t)level];
+    DevLevel* C = (size_t)level + 1 < h->lv.size() ? h->lv[(size_t)level + 1] : nullptr;
+    const double* bb = level == 0 ? h->ws.r.p : L.b.p;
+    double* xx = level == 0 ? h->ws.z.p : L.x.p;
+    if (piece >= 0) record_piece(piece, L, C, bb, xx, h->ws.zero_flag.p, s, part);
+    if (x) HC_CUDA(cudaMemcpyAsync(x, h->ws.z.p, 8 * n, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+    check_dist(h);
   });
 }
 

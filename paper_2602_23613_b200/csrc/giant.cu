@@ -23,6 +23,7 @@
 
 #include "dense.cuh"
 #include "giant.cuh"
+#include "dist.cuh"
 #include "sparse.cuh"
 
 namespace hcamg {
@@ -78,13 +79,16 @@ const T** upload_ptrs(std::vector<const T*>& h, DBuf<const T*>& d, cudaStream_t 
 
 // ---- hybrid P kernels
 
-// Prolongation, dense part: x[rows[q]] -= Z[q, :] . e.  One warp per row,
-// e staged in shared memory when it fits (n_c <= 25k), 4 independent 16-byte
-// loads in flight per lane.
-template <bool kSmemE, bool kSet>
-__global__ void __launch_bounds__(512) k_z_rows(const int* stop, int64_t nG, int64_t nc,
+// Prolongation, dense part, rows [q0, q1): one warp per row, e staged in
+// shared memory when it fits (n_c <= 25k), 4 independent 16-byte loads in
+// flight per lane.  kMode 0: x[rows[q]] -= Z[q,:].e; 1: x[q] = M[q,:].e;
+// 2: the row results go to every rank's exchange area at q (distributed
+// solve), then the last CTA signals.  The per-row arithmetic does not depend
+// on the row range, so a row-partitioned product is bit-identical.
+template <bool kSmemE, int kMode>
+__global__ void __launch_bounds__(512) k_z_rows(const int* stop, int64_t q0, int64_t q1, int64_t nc,
                                                 const double* __restrict__ Z, const int32_t* __restrict__ rows,
-                                                const double* __restrict__ e, double* __restrict__ x) {
+                                                const double* __restrict__ e, double* __restrict__ x, Xchg xc) {
   if (*stop) return;
   extern __shared__ double es[];
   const double* ev = e;
@@ -93,8 +97,10 @@ __global__ void __launch_bounds__(512) k_z_rows(const int* stop, int64_t nG, int
     __syncthreads();
     ev = es;
   }
+  unsigned long long ep = 0;
+  if (kMode == 2) ep = xepoch(xc);
   const int lane = threadIdx.x & 31;
-  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nG;
+  for (int64_t q = q0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < q1;
        q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const double* z = Z + q * nc;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -116,24 +122,28 @@ __global__ void __launch_bounds__(512) k_z_rows(const int* stop, int64_t nG, int
     if (c < nc) a0 = fma(z[c], ev[c], a0);
     double acc = (a0 + a1) + (a2 + a3);
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      if (kSet) x[q] = acc;
+    if (kMode == 2) {
+      if (lane < xc.nranks) xarea(xc, lane, ep + 1)[q] = acc;
+    } else if (lane == 0) {
+      if (kMode == 1) x[q] = acc;
       else x[rows[q]] -= acc;
     }
   }
+  if (kMode == 2) xsignal(xc, ep);
 }
 
-// Restriction, dense part: partial[ch][c] = sum_{q in chunk ch} Z[q, c] r[rows[q]].
-// CTA = (1024-column tile, row chunk); 4 columns per thread (two 16-byte loads),
-// two rows in flight.
+// Restriction, dense part: partial[ch][c] = sum_{q in chunk ch} Z[q, c] r[rows[q]]
+// for chunks [ch0, ch0 + gridDim.y).  CTA = (1024-column tile, row chunk);
+// 4 columns per thread (two 16-byte loads), two rows in flight.
 constexpr int kZtCols = 1024;
 
 __global__ void __launch_bounds__(256) k_zt_partial(const int* stop, int64_t nG, int64_t nc, int64_t chunk,
-                                                    const double* __restrict__ Z, const int32_t* __restrict__ rows,
-                                                    const double* __restrict__ r, double* __restrict__ partial) {
+                                                    int64_t ch0, const double* __restrict__ Z,
+                                                    const int32_t* __restrict__ rows, const double* __restrict__ r,
+                                                    double* __restrict__ partial) {
   if (*stop) return;
   extern __shared__ double rv[];
-  const int64_t ch = blockIdx.y;
+  const int64_t ch = ch0 + blockIdx.y;
   const int64_t q0 = ch * chunk, q1 = min(nG, q0 + chunk);
   for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) rv[q - q0] = r[rows[q]];
   __syncthreads();
@@ -171,12 +181,22 @@ __global__ void __launch_bounds__(256) k_zt_partial(const int* stop, int64_t nG,
   }
 }
 
-__global__ void k_zt_reduce(const int* stop, int64_t nc, int64_t nchunk, const double* __restrict__ partial,
+struct GrpBounds {
+  int64_t b[kGroups + 1];
+};
+
+// bc[c] -= sum_g (sum_{ch in group g} partial[ch][c])  -- the same two-level
+// order as the distributed group sums (dist.cu), hence bit-identical to them
+__global__ void k_zt_reduce(const int* stop, int64_t nc, const double* __restrict__ partial, GrpBounds grp,
                             double* __restrict__ bc) {
   if (*stop) return;
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
     double acc = 0.0;
-    for (int64_t ch = 0; ch < nchunk; ++ch) acc += partial[ch * nc + c];
+    for (int g = 0; g < kGroups; ++g) {
+      double gs = 0.0;
+      for (int64_t ch = grp.b[g]; ch < grp.b[g + 1]; ++ch) gs += partial[ch * nc + c];
+      acc += gs;
+    }
     bc[c] -= acc;
   }
 }
@@ -394,51 +414,107 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
   HC_CUDA(cudaStreamSynchronize(s));
 }
 
-template <bool kSet>
-static void launch_rows(const int* stop, int64_t nrows, int64_t nc, const double* Z, const int32_t* rows,
-                        const double* e, double* x, cudaStream_t s) {
+template <int kMode>
+static void launch_rows(const int* stop, int64_t q0, int64_t q1, int64_t nc, const double* Z, const int32_t* rows,
+                        const double* e, double* x, const Xchg& xc, cudaStream_t s) {
   const bool smem = nc * 8 <= 200 * 1024;
+  const int64_t nrows = std::max<int64_t>(q1 - q0, 0);
   static bool init = false;
   if (!init) {
-    HC_CUDA(cudaFuncSetAttribute(k_z_rows<true, kSet>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HC_CUDA(cudaFuncSetAttribute(k_z_rows<true, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     init = true;
   }
   if (smem) {
     // e staged once per CTA; as many 512-thread CTAs per SM as shared memory allows (<= 4)
     const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / std::max<int64_t>(8 * nc, 1)));
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nrows + 15) / 16, kSMs * per_sm));
-    k_z_rows<true, kSet><<<g, 512, sizeof(double) * nc, s>>>(stop, nrows, nc, Z, rows, e, x);
+    k_z_rows<true, kMode><<<g, 512, sizeof(double) * nc, s>>>(stop, q0, q1, nc, Z, rows, e, x, xc);
   } else {
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nrows + 15) / 16, kSMs * 4));
-    k_z_rows<false, kSet><<<g, 512, 0, s>>>(stop, nrows, nc, Z, rows, e, x);
+    k_z_rows<false, kMode><<<g, 512, 0, s>>>(stop, q0, q1, nc, Z, rows, e, x, xc);
   }
   HC_CHECK_LAUNCH();
 }
 
-void hybrid_prolong(const int* stop, const HybridP& hp, const double* e, double* x, cudaStream_t s) {
-  launch_rows<false>(stop, hp.nG, hp.nc, hp.Z.p, hp.rows.p, e, x, s);
+static bool dist_on(const Dist* d) { return d && d->on; }
+
+// rows [q0, q1) of Z owned by this rank: the rows of its chunk groups
+static void rank_rows(const HybridP& hp, const Dist& d, int64_t& q0, int64_t& q1) {
+  int g0, g1;
+  rank_groups(d.rank, d.nranks, g0, g1);
+  q0 = std::min(hp.nG, hp.grp[g0] * hp.chunk);
+  q1 = std::min(hp.nG, hp.grp[g1] * hp.chunk);
+}
+
+void hybrid_prolong(const int* stop, const HybridP& hp, const double* e, double* x, cudaStream_t s, const Dist* d,
+                    size_t off, int part) {
+  if (!dist_on(d)) {
+    if (part != 2) launch_rows<0>(stop, 0, hp.nG, hp.nc, hp.Z.p, hp.rows.p, e, x, Xchg{}, s);
+    return;
+  }
+  const Xchg xc = d->site(off);
+  if (part != 2) {
+    int64_t q0, q1;
+    rank_rows(hp, *d, q0, q1);
+    launch_rows<2>(stop, q0, q1, hp.nc, hp.Z.p, hp.rows.p, e, nullptr, xc, s);
+  }
+  if (part != 1) xchg_scatter(stop, xc, hp.nG, hp.rows.p, x, s);
 }
 
 void dense_gemv_rows(const int* stop, int64_t n, int64_t m, const double* M, const double* e, double* x,
-                     cudaStream_t s) {
-  launch_rows<true>(stop, n, m, M, nullptr, e, x, s);
+                     cudaStream_t s, const Dist* d, size_t off, int part) {
+  if (!dist_on(d)) {
+    if (part != 2) launch_rows<1>(stop, 0, n, m, M, nullptr, e, x, Xchg{}, s);
+    return;
+  }
+  const Xchg xc = d->site(off);
+  if (part != 2) {
+    int64_t r0, r1;
+    even_rows(n, d->rank, d->nranks, r0, r1);
+    launch_rows<2>(stop, r0, r1, m, M, nullptr, e, nullptr, xc, s);
+  }
+  if (part != 1) xchg_scatter(stop, xc, n, nullptr, x, s);
 }
 
 void hybrid_prepare(HybridP& hp, cudaStream_t s) {
+  // Row chunks, grouped into kGroups groups of whole chunks.  Enough chunks per
+  // group that one group alone (one rank of eight) fills the GPU: ~4 CTAs
+  // per SM over the column tiles.
   const int64_t ct = (hp.nc + kZtCols - 1) / kZtCols;
-  const int64_t want = std::max<int64_t>(1, (4 * kSMs + ct - 1) / ct);
+  const int64_t per_group = std::max<int64_t>(1, (4 * kSMs + ct - 1) / std::max<int64_t>(ct, 1));
+  const int64_t want = kGroups * per_group;
   hp.chunk = std::max<int64_t>(16, std::min<int64_t>(4096, (hp.nG + want - 1) / want));
   hp.nchunk = (hp.nG + hp.chunk - 1) / hp.chunk;
+  for (int g = 0; g <= kGroups; ++g) hp.grp[g] = hp.nchunk * g / kGroups;
   hp.partial.alloc(std::max<int64_t>(hp.nchunk * hp.nc, 1), s);
 }
 
-void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, cudaStream_t s) {
+void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, cudaStream_t s, const Dist* d,
+                     size_t off, int part) {
   require(hp.nchunk > 0, "hybrid_restrict: plan not prepared");
-  dim3 grid((unsigned)((hp.nc + kZtCols - 1) / kZtCols), (unsigned)hp.nchunk);
-  k_zt_partial<<<grid, 256, sizeof(double) * hp.chunk, s>>>(stop, hp.nG, hp.nc, hp.chunk, hp.Z.p, hp.rows.p, r,
-                                                             hp.partial.p);
-  k_zt_reduce<<<grid_for(hp.nc, 256), 256, 0, s>>>(stop, hp.nc, hp.nchunk, hp.partial.p, bc);
-  HC_CHECK_LAUNCH();
+  const unsigned tiles = (unsigned)((hp.nc + kZtCols - 1) / kZtCols);
+  if (!dist_on(d)) {
+    if (part == 2) return;
+    k_zt_partial<<<dim3(tiles, (unsigned)hp.nchunk), 256, sizeof(double) * hp.chunk, s>>>(
+        stop, hp.nG, hp.nc, hp.chunk, 0, hp.Z.p, hp.rows.p, r, hp.partial.p);
+    GrpBounds g{};
+    for (int t = 0; t <= kGroups; ++t) g.b[t] = hp.grp[t];
+    k_zt_reduce<<<grid_for(hp.nc, 256), 256, 0, s>>>(stop, hp.nc, hp.partial.p, g, bc);
+    HC_CHECK_LAUNCH();
+    return;
+  }
+  const Xchg xc = d->site(off);
+  if (part != 2) {
+    int g0, g1;
+    rank_groups(d->rank, d->nranks, g0, g1);
+    const int64_t c0 = hp.grp[g0], c1 = hp.grp[g1];
+    if (c1 > c0)
+      k_zt_partial<<<dim3(tiles, (unsigned)(c1 - c0)), 256, sizeof(double) * hp.chunk, s>>>(
+          stop, hp.nG, hp.nc, hp.chunk, c0, hp.Z.p, hp.rows.p, r, hp.partial.p);
+    HC_CHECK_LAUNCH();
+    xchg_group_sums(stop, xc, hp.nc, hp.partial.p, hp.grp, g0, g1, s);
+  }
+  if (part != 1) xchg_group_final(stop, xc, hp.nc, bc, s);
 }
 
 void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr& Pst, const HybridP& hp, DCsr& Ac,

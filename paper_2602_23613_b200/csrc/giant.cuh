@@ -7,6 +7,7 @@
 #include <cublas_v2.h>
 
 #include "common.cuh"
+#include "dist.cuh"
 
 namespace hcamg {
 
@@ -26,18 +27,26 @@ struct HybridP {
   DBuf<double> Z;       // nG x nc row-major; P[rows[q], c] = -Z[q, c]
   // restriction partials (deterministic chunked column reduction)
   int64_t chunk = 512, nchunk = 0;
+  int64_t grp[kGroups + 1] = {};  // chunk boundaries of the kGroups reduction groups
   DBuf<double> partial;
 };
 
 // allocate the restriction partials (outside any graph capture)
 void hybrid_prepare(HybridP& hp, cudaStream_t s);
+// The three products below take an optional distributed context `d` (rows
+// split across ranks, results exchanged through exchange site `off`, see
+// dist.cuh) and `part`: 0 = all, 1 = up to the exchange signal (producer),
+// 2 = from the exchange wait on (consumer) -- the split lets tests emulate
+// several ranks on one GPU without kernels that wait on each other.
 // x[rows[q]] -= Z[q,:] . e   (prolongation, dense part)
-void hybrid_prolong(const int* stop, const HybridP& hp, const double* e, double* x, cudaStream_t s);
+void hybrid_prolong(const int* stop, const HybridP& hp, const double* e, double* x, cudaStream_t s,
+                    const Dist* d = nullptr, size_t off = 0, int part = 0);
 // x = M e for a dense row-major n x m matrix (HBM-streaming GEMV)
 void dense_gemv_rows(const int* stop, int64_t n, int64_t m, const double* M, const double* e, double* x,
-                     cudaStream_t s);
+                     cudaStream_t s, const Dist* d = nullptr, size_t off = 0, int part = 0);
 // bc -= Z^T r[rows]            (restriction, dense part; bc already holds P_s^T r)
-void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, cudaStream_t s);
+void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, cudaStream_t s,
+                     const Dist* d = nullptr, size_t off = 0, int part = 0);
 
 // A_c = sym(P_s^T A P_s) - sym(W'^T Z) - sym(Z^T rho), rho = W' - A_GG Z
 // (= P^T A P for P = P_s - S_G Z, exactly, including the residual of the

@@ -75,6 +75,10 @@ struct DevLevel {
   DBuf<double> Ainv;     // coarsest: dense inverse (row-major n x n)
   SegPlan pt_seg;        // segmented restriction plan when P^T has long rows
   HybridP hp;            // dense-regime interpolation block (P/Pt then hold the sparse part)
+  // distributed solve (dist.cuh): context and exchange-site offsets of this level
+  const Dist* dist = nullptr;
+  static constexpr size_t kNoSite = ~(size_t)0;
+  size_t xoff_g = kNoSite, xoff_y = kNoSite, xoff_c = kNoSite;
   int64_t pt_maxrow = 0;
   // work vectors
   DBuf<double> b, x, r, d0, d1, dj;

@@ -594,13 +594,29 @@ static int64_t record_leg_waves(DevLevel& L, const double* b, double* x, const i
   return launches;
 }
 
+// Coarsest levels of at least this size apply their inverse with the
+// HBM-streaming row GEMV (row-partitioned in the distributed solve); smaller
+// ones with the latency-oriented k_gemv_dense.  HCAMG_COARSE_GEMV_MIN
+// overrides (tests use it to exercise the coarse exchange on small cases).
+int64_t coarse_gemv_min() {
+  const char* e = getenv("HCAMG_COARSE_GEMV_MIN");
+  return e ? atoll(e) : 8192;
+}
+
 // One piece of a level's V-cycle work (separately launchable for profiling).
-int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* x, const int* stop, cudaStream_t s) {
+int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* x, const int* stop, cudaStream_t s,
+                     int part) {
   const int64_t n = L.n;
+  const bool xd = L.dist && L.dist->on;  // this piece may exchange
+  if (part == 2 && !xd) return 0;
+  if (part == 2 && !(pc == PC_COARSE && n >= coarse_gemv_min()) && !((pc == PC_RESTRICT || pc == PC_PROLONG) && L.hp.on))
+    return 0;
   if (pc == PC_COARSE) {
     if (!n) return 0;
-    if (n >= 8192) {
-      dense_gemv_rows(stop, n, n, L.Ainv.p, b, x, s);
+    if (n >= coarse_gemv_min()) {
+      require(!xd || L.xoff_c != DevLevel::kNoSite, "distributed layout is stale (call hcamg_dist_prepare again)");
+      dense_gemv_rows(stop, n, n, L.Ainv.p, b, x, s, L.dist, L.xoff_c, part);
+      return xd ? (part == 0 ? 2 : 1) : 1;
     } else {
       k_gemv_dense<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, kSMs * 8)), kThreads, 0, s>>>(
           stop, n, L.Ainv.p, b, x);
@@ -610,13 +626,17 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
   }
   if (pc == PC_RESTRICT) {
     if (L.hp.on) {  // b_c = P_s^T r - Z^T r_G
-      SpmvArgs rs{};
-      rs.stop = stop;
-      rs.xin = L.r.p;
-      rs.y = C->b.p;
-      spmv<EPI_SET>(L.Pt, rs, s);
-      hybrid_restrict(stop, L.hp, L.r.p, C->b.p, s);
-      return 3;
+      if (part != 2) {
+        SpmvArgs rs{};
+        rs.stop = stop;
+        rs.xin = L.r.p;
+        rs.y = C->b.p;
+        spmv<EPI_SET>(L.Pt, rs, s);
+      }
+      require(!xd || L.xoff_g != DevLevel::kNoSite, "distributed layout is stale (call hcamg_dist_prepare again)");
+      hybrid_restrict(stop, L.hp, L.r.p, C->b.p, s, L.dist, L.xoff_g, part);
+      if (!xd) return 3;
+      return part == 0 ? 4 : (part == 1 ? 3 : 1);
     }
     if (L.pt_seg.nseg) {
       launch_segmented(stop, L.Pt, L.pt_seg, L.r.p, C->b.p, s);
@@ -630,14 +650,18 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     return 1;
   }
   if (pc == PC_PROLONG) {
-    SpmvArgs pr{};
-    pr.stop = stop;
-    pr.xin = C->x.p;
-    pr.y = x;
-    spmv<EPI_ADD>(L.P, pr, s);
+    if (part != 2) {
+      SpmvArgs pr{};
+      pr.stop = stop;
+      pr.xin = C->x.p;
+      pr.y = x;
+      spmv<EPI_ADD>(L.P, pr, s);
+    }
     if (L.hp.on) {  // x[G] -= Z x_c
-      hybrid_prolong(stop, L.hp, C->x.p, x, s);
-      return 2;
+      require(!xd || L.xoff_y != DevLevel::kNoSite, "distributed layout is stale (call hcamg_dist_prepare again)");
+      hybrid_prolong(stop, L.hp, C->x.p, x, s, L.dist, L.xoff_y, part);
+      if (!xd) return 2;
+      return part == 0 ? 3 : (part == 1 ? 2 : 1);
     }
     return 1;
   }

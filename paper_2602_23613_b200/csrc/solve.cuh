@@ -30,11 +30,17 @@ struct Workspace {
 
 extern long long* g_leg_trace;
 
+int64_t coarse_gemv_min();
+
 enum Piece : int { PC_DOWN = 0, PC_RESTRICT = 1, PC_COARSE = 2, PC_PROLONG = 3, PC_UP = 4 };
 
 // One piece of a level's V-cycle (down leg, restriction, coarsest solve,
 // prolongation, up leg); C is the next-coarser level (null on the coarsest).
-int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* x, const int* stop, cudaStream_t s);
+// `part` (distributed solve only): 0 = whole piece, 1 = up to its exchange
+// signal, 2 = from its exchange wait on (pieces without an exchange run
+// entirely in part 1).
+int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* x, const int* stop, cudaStream_t s,
+                     int part = 0);
 
 // Record one V-cycle on `stream`: x0 := V(b0) for the finest level, reading
 // b0 and writing x0 (level-0 work buffers are used for everything else).
