@@ -30,7 +30,8 @@ from dataclasses import dataclass
 import numpy as np
 import scipy.sparse as sp
 
-__all__ = ["KuhnSystem", "kuhn_mesh", "assemble_kuhn", "config_system", "CONFIGS", "rhs"]
+__all__ = ["KuhnSystem", "kuhn_mesh", "kuhn_chain", "assemble_kuhn", "config_system", "config_chain",
+           "CONFIGS", "rhs"]
 
 
 def _canon(a, shape=None):
@@ -91,13 +92,25 @@ class KuhnSystem:
 _LOCAL_EDGES = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))
 
 
-def kuhn_mesh(n):
-    """Unit cube, n^3 hexes, 6 Kuhn tets each (conforming, nested under 2x)."""
+def kuhn_mesh(n, order=None):
+    """Unit cube, n^3 hexes, 6 Kuhn tets each (conforming, nested under 2x).
+
+    ``order`` (optional) numbers the vertices: ``order[lex]`` is the number of
+    the grid vertex with lexicographic index lex (default: the identity).  Tets
+    stay cube-major / permutation-minor over the grid; edges are numbered by
+    the (tail, head) sort of the renumbered vertices."""
     if n < 1:
         raise ValueError("n must be >= 1")
     N = n + 1
     idx = np.arange(N ** 3, dtype=np.int64)
-    gi, gj, gk = idx % N, (idx // N) % N, idx // (N * N)
+    if order is None:
+        order = idx
+    order = np.asarray(order, dtype=np.int64)
+    if order.shape != idx.shape or not np.array_equal(np.sort(order), idx):
+        raise ValueError("order must be a permutation of the grid vertices")
+    lex_of = np.empty_like(order)
+    lex_of[order] = idx                       # vertex number -> lexicographic index
+    gi, gj, gk = lex_of % N, (lex_of // N) % N, lex_of // (N * N)
     vertices = np.stack([gi, gj, gk], axis=1).astype(np.float64) / n
     step = np.array([1, N, N * N], dtype=np.int64)
     ck, cj, ci = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
@@ -107,7 +120,7 @@ def kuhn_mesh(n):
     for a, b, _ in itertools.permutations(range(3)):
         tets.append(np.stack([v0, v0 + step[a], v0 + step[a] + step[b], far], axis=1))
     # cube-major / permutation-minor order
-    tets = np.stack(tets, axis=1).reshape(-1, 4)
+    tets = order[np.stack(tets, axis=1).reshape(-1, 4)]
 
     loc = np.array(_LOCAL_EDGES)
     ends = tets[:, loc]                      # (nt, 6, 2)
@@ -241,6 +254,78 @@ CONFIGS = {
     "c4": dict(n=128, beta=1e-4, field=lambda m: _inclusions(m, 64, seed=0), route="alg"),
     "c5": dict(n=256, beta=1e-3, field=lambda m: _checkerboard(m, 8, 1.0, 1e6), route="alg"),
 }
+
+
+@dataclass
+class KuhnRefinement:
+    """Duck-typed ``RefinementMap`` (reference mesh.py:187-193): the two fine
+    children (tail side, head side) of every coarse edge."""
+
+    coarse_edge_children: np.ndarray
+
+
+def kuhn_chain(n_base, nrefine):
+    """Nested Kuhn meshes n_base -> 2 n_base -> ... (``nrefine`` refinements)
+    numbered like the reference's ``refine`` (mesh.py:201-257): the fine mesh
+    keeps the coarse vertices first, in coarse order, followed by the midpoint
+    of every coarse edge in coarse edge order (every fine vertex is a coarse
+    vertex or the midpoint of exactly one Kuhn edge, since all diagonals point
+    the same way).  Returns (meshes coarse -> fine, refinement maps)."""
+    mesh = kuhn_mesh(n_base)
+    meshes, rmaps = [mesh], []
+    n = n_base
+    for _ in range(nrefine):
+        N = n + 1
+        lex = np.arange(N ** 3, dtype=np.int64)
+        cur_lex_of = np.empty(N ** 3, dtype=np.int64)
+        cur_lex_of[_vertex_numbers(mesh)] = lex
+        g = np.stack([cur_lex_of % N, (cur_lex_of // N) % N, cur_lex_of // (N * N)], axis=1)  # by vertex number
+        t, h = mesh.edges[:, 0], mesh.edges[:, 1]
+        fine_g = np.vstack([2 * g, g[t] + g[h]])           # fine grid coords of fine vertex numbers
+        n2, N2 = 2 * n, 2 * n + 1
+        if len(fine_g) != N2 ** 3:
+            raise AssertionError("Kuhn refinement does not cover the fine grid")
+        flex = (fine_g[:, 2] * N2 + fine_g[:, 1]) * N2 + fine_g[:, 0]
+        order = np.empty(N2 ** 3, dtype=np.int64)
+        order[flex] = np.arange(N2 ** 3, dtype=np.int64)
+        fine = kuhn_mesh(n2, order)
+        keys = {(int(a), int(b)): e for e, (a, b) in enumerate(fine.edges)}
+        mid = mesh.nv + np.arange(mesh.ne)
+        kids = np.empty((mesh.ne, 2), dtype=np.int64)
+        for e in range(mesh.ne):
+            m = int(mid[e])
+            kids[e, 0] = keys[(min(int(t[e]), m), max(int(t[e]), m))]
+            kids[e, 1] = keys[(min(int(h[e]), m), max(int(h[e]), m))]
+        meshes.append(fine)
+        rmaps.append(KuhnRefinement(kids))
+        mesh, n = fine, n2
+    return meshes, rmaps
+
+
+def _vertex_numbers(mesh):
+    """order[lex] of a KuhnMesh, recovered from its vertex coordinates."""
+    N = mesh.n + 1
+    g = np.rint(mesh.vertices * mesh.n).astype(np.int64)
+    lex = (g[:, 2] * N + g[:, 1]) * N + g[:, 0]
+    order = np.empty(N ** 3, dtype=np.int64)
+    order[lex] = np.arange(N ** 3, dtype=np.int64)
+    return order
+
+
+def config_chain(name, n_fine=None, n_base=None):
+    """A config on a nested chain (the "ref" route): (system, meshes, rmaps).
+    Defaults: BASELINE's chain for the config (c3: 8 -> 16 -> 32 -> 64)."""
+    cfg = CONFIGS[name]
+    n_fine = cfg["n"] if n_fine is None else n_fine
+    n_base = 8 if n_base is None else n_base
+    nref = 0
+    while n_base * 2 ** nref < n_fine:
+        nref += 1
+    if n_base * 2 ** nref != n_fine:
+        raise ValueError("n_fine must be n_base * 2^k")
+    meshes, rmaps = kuhn_chain(n_base, nref)
+    fine = meshes[-1]
+    return assemble_kuhn(fine, cfg["field"](fine), cfg["beta"]), meshes, rmaps
 
 
 def config_system(name, n=None):

@@ -39,3 +39,39 @@ def test_config1_matches_survey():
 def test_rhs_seed():
     b = kuhn.rhs(10, seed=0)
     assert np.array_equal(b, np.random.default_rng(0).uniform(-1, 1, 10))
+
+
+def test_chain_refine_numbering_and_children():
+    meshes, rmaps = kuhn.kuhn_chain(2, 2)
+    assert [m.n for m in meshes] == [2, 4, 8]
+    for c, f, r in zip(meshes, meshes[1:], rmaps):
+        # coarse vertices keep their numbers, midpoints follow in coarse edge order
+        assert np.array_equal(f.vertices[: c.nv], c.vertices)
+        t, h = c.edges[:, 0], c.edges[:, 1]
+        mid = c.nv + np.arange(c.ne)
+        assert np.allclose(f.vertices[mid], 0.5 * (c.vertices[t] + c.vertices[h]))
+        assert f.nv == c.nv + c.ne
+        # children: fine edges (tail, mid) and (head, mid), stored tail < head
+        k0, k1 = f.edges[r.coarse_edge_children[:, 0]], f.edges[r.coarse_edge_children[:, 1]]
+        assert np.array_equal(np.sort(k0, axis=1), np.sort(np.stack([t, mid], 1), axis=1))
+        assert np.array_equal(np.sort(k1, axis=1), np.sort(np.stack([h, mid], 1), axis=1))
+        # the renumbered mesh is the same geometric Kuhn mesh (tet by tet)
+        ref = kuhn.kuhn_mesh(f.n)
+        assert np.allclose(f.vertices[f.tets], ref.vertices[ref.tets])
+        assert f.ne == ref.ne and int(f.boundary_edge.sum()) == int(ref.boundary_edge.sum())
+
+
+def test_chain_system_is_the_same_operator_up_to_renumbering():
+    s_chain, meshes, _ = kuhn.config_chain("c1", 8, 2)
+    s_lex = kuhn.config_system("c1", 8)
+    assert s_chain.n == s_lex.n == 3032
+    # match edges geometrically (midpoint) and compare |A| entries
+    def mids(s):
+        m = s.mesh
+        fe = np.flatnonzero(~m.boundary_edge)
+        return np.round(0.5 * (m.vertices[m.edges[fe, 0]] + m.vertices[m.edges[fe, 1]]) * 16).astype(int)
+    key = lambda g: (g[:, 2] * 17 + g[:, 1]) * 17 + g[:, 0]
+    pc, pl = np.argsort(key(mids(s_chain))), np.argsort(key(mids(s_lex)))
+    Ac = abs(s_chain.A[pc][:, pc]).toarray()
+    Al = abs(s_lex.A[pl][:, pl]).toarray()
+    assert np.allclose(Ac, Al, rtol=1e-12, atol=1e-14)
