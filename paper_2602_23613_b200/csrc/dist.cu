@@ -13,12 +13,14 @@ __global__ void __launch_bounds__(256) k_group_sums(const int* stop, Xchg x, int
                                                     const double* __restrict__ partial, Grp grp, int g0, int g1) {
   if (*stop) return;
   const unsigned long long e = xepoch(x);
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
-    for (int g = g0; g < g1; ++g) {
-      double gs = 0.0;
-      for (int64_t ch = grp.b[g]; ch < grp.b[g + 1]; ++ch) gs += partial[ch * nc + c];
-      for (int r = 0; r < x.nranks; ++r) xarea(x, r, e + 1)[g * nc + c] = gs;
-    }
+  // one thread per (group, column)
+  const int64_t total = (int64_t)(g1 - g0) * nc;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int g = g0 + (int)(t / nc);
+    const int64_t c = t % nc;
+    double gs = 0.0;
+    for (int64_t ch = grp.b[g]; ch < grp.b[g + 1]; ++ch) gs += partial[ch * nc + c];
+    for (int r = 0; r < x.nranks; ++r) xarea(x, r, e + 1)[g * nc + c] = gs;
   }
   xsignal(x, e);
 }
@@ -76,7 +78,8 @@ void xchg_group_sums(const int* stop, const Xchg& x, int64_t nc, const double* p
                      int g0, int g1, cudaStream_t s) {
   Grp g{};
   for (int t = 0; t <= kGroups; ++t) g.b[t] = grp_host[t];
-  k_group_sums<<<grid_for(std::max<int64_t>(nc, 1), 256), 256, 0, s>>>(stop, x, nc, partial, g, g0, g1);
+  k_group_sums<<<grid_for(std::max<int64_t>((int64_t)(g1 - g0) * nc, 1), 256), 256, 0, s>>>(stop, x, nc, partial, g,
+                                                                                           g0, g1);
   HC_CHECK_LAUNCH();
 }
 

@@ -79,20 +79,32 @@ const T** upload_ptrs(std::vector<const T*>& h, DBuf<const T*>& d, cudaStream_t 
 
 // ---- hybrid P kernels
 
-// Prolongation, dense part, rows [q0, q1): one warp per row, e staged in
-// shared memory when it fits (n_c <= 25k), 4 independent 16-byte loads in
+// Prolongation, dense part, rows [q0, q1): one warp per PAIR of rows (the
+// e loads are shared by both rows, halving their L1/L2 traffic), e staged in
+// shared memory when it fits (n_c <= 25k), 8 independent 16-byte Z loads in
 // flight per lane.  kMode 0: x[rows[q]] -= Z[q,:].e; 1: x[q] = M[q,:].e;
 // 2: the row results go to every rank's exchange area at q (distributed
-// solve), then the last CTA signals.  The per-row arithmetic does not depend
-// on the row range, so a row-partitioned product is bit-identical.
+// solve), then the last CTA signals.  Every row is summed in the same order
+// (4 lane-strided accumulators, then a butterfly) whatever rows share its
+// warp, so a row-partitioned product is bit-identical.
+__device__ __forceinline__ double2 ld_z2(const double* p, bool aligned) {
+  if (aligned) return __ldcs(reinterpret_cast<const double2*>(p));
+  return make_double2(__ldcs(p), __ldcs(p + 1));
+}
+
+__device__ __forceinline__ double2 ld_e2(const double* p) {
+  return *reinterpret_cast<const double2*>(p);  // c even, e 16-byte aligned
+}
+
 template <bool kSmemE, int kMode>
 __global__ void __launch_bounds__(512) k_z_rows(const int* stop, int64_t q0, int64_t q1, int64_t nc,
                                                 const double* __restrict__ Z, const int32_t* __restrict__ rows,
                                                 const double* __restrict__ e, double* __restrict__ x, Xchg xc) {
   if (*stop) return;
-  extern __shared__ double es[];
+  extern __shared__ double2 es2[];
   const double* ev = e;
   if (kSmemE) {
+    double* es = reinterpret_cast<double*>(es2);
     for (int64_t c = threadIdx.x; c < nc; c += blockDim.x) es[c] = e[c];
     __syncthreads();
     ev = es;
@@ -100,34 +112,125 @@ __global__ void __launch_bounds__(512) k_z_rows(const int* stop, int64_t q0, int
   unsigned long long ep = 0;
   if (kMode == 2) ep = xepoch(xc);
   const int lane = threadIdx.x & 31;
-  for (int64_t q = q0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < q1;
-       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const double* z = Z + q * nc;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t q = q0 + 2 * (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); q < q1; q += 2 * nw) {
+    const bool two = q + 1 < q1;
+    const double* za = Z + q * nc;
+    const double* zb = two ? za + nc : za;
+    const bool ala = ((q * nc) & 1) == 0, alb = (((q + (two ? 1 : 0)) * nc) & 1) == 0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
     int64_t c = 2 * lane;
     for (; c + 192 + 1 < nc; c += 256) {
-      const double2 z0 = __ldcs(reinterpret_cast<const double2*>(z + c));
-      const double2 z1 = __ldcs(reinterpret_cast<const double2*>(z + c + 64));
-      const double2 z2 = __ldcs(reinterpret_cast<const double2*>(z + c + 128));
-      const double2 z3 = __ldcs(reinterpret_cast<const double2*>(z + c + 192));
-      a0 = fma(z0.x, ev[c], fma(z0.y, ev[c + 1], a0));
-      a1 = fma(z1.x, ev[c + 64], fma(z1.y, ev[c + 65], a1));
-      a2 = fma(z2.x, ev[c + 128], fma(z2.y, ev[c + 129], a2));
-      a3 = fma(z3.x, ev[c + 192], fma(z3.y, ev[c + 193], a3));
+      const double2 u0 = ld_z2(za + c, ala), u1 = ld_z2(za + c + 64, ala);
+      const double2 u2 = ld_z2(za + c + 128, ala), u3 = ld_z2(za + c + 192, ala);
+      const double2 w0 = ld_z2(zb + c, alb), w1 = ld_z2(zb + c + 64, alb);
+      const double2 w2 = ld_z2(zb + c + 128, alb), w3 = ld_z2(zb + c + 192, alb);
+      const double2 e0 = ld_e2(ev + c), e1 = ld_e2(ev + c + 64);
+      const double2 e2 = ld_e2(ev + c + 128), e3 = ld_e2(ev + c + 192);
+      a0 = fma(u0.x, e0.x, fma(u0.y, e0.y, a0));
+      a1 = fma(u1.x, e1.x, fma(u1.y, e1.y, a1));
+      a2 = fma(u2.x, e2.x, fma(u2.y, e2.y, a2));
+      a3 = fma(u3.x, e3.x, fma(u3.y, e3.y, a3));
+      b0 = fma(w0.x, e0.x, fma(w0.y, e0.y, b0));
+      b1 = fma(w1.x, e1.x, fma(w1.y, e1.y, b1));
+      b2 = fma(w2.x, e2.x, fma(w2.y, e2.y, b2));
+      b3 = fma(w3.x, e3.x, fma(w3.y, e3.y, b3));
     }
     for (; c + 1 < nc; c += 64) {
-      const double2 z0 = __ldcs(reinterpret_cast<const double2*>(z + c));
-      a0 = fma(z0.x, ev[c], fma(z0.y, ev[c + 1], a0));
+      const double2 u0 = ld_z2(za + c, ala), w0 = ld_z2(zb + c, alb), e0 = ld_e2(ev + c);
+      a0 = fma(u0.x, e0.x, fma(u0.y, e0.y, a0));
+      b0 = fma(w0.x, e0.x, fma(w0.y, e0.y, b0));
     }
-    if (c < nc) a0 = fma(z[c], ev[c], a0);
-    double acc = (a0 + a1) + (a2 + a3);
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (c < nc) {
+      a0 = fma(za[c], ev[c], a0);
+      b0 = fma(zb[c], ev[c], b0);
+    }
+    double acc = (a0 + a1) + (a2 + a3), bcc = (b0 + b1) + (b2 + b3);
+    for (int o = 16; o; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      bcc += __shfl_xor_sync(0xffffffffu, bcc, o);
+    }
     if (kMode == 2) {
-      if (lane < xc.nranks) xarea(xc, lane, ep + 1)[q] = acc;
+      if (lane < xc.nranks) {
+        double* y = xarea(xc, lane, ep + 1);
+        y[q] = acc;
+        if (two) y[q + 1] = bcc;
+      }
     } else if (lane == 0) {
-      if (kMode == 1) x[q] = acc;
-      else x[rows[q]] -= acc;
+      if (kMode == 1) {
+        x[q] = acc;
+        if (two) x[q + 1] = bcc;
+      } else {
+        x[rows[q]] -= acc;
+        if (two) x[rows[q + 1]] -= bcc;
+      }
     }
+  }
+  if (kMode == 2) xsignal(xc, ep);
+}
+
+// Same product for wide rows (n_c >= 4096): a 256-thread CTA sweeps a batch
+// of 16 consecutive rows together, 512 columns (4 KB of each row) per step,
+// thread t owning columns 2t + 512k of all 16 rows -- 16 independent 16-byte
+// loads in flight per thread and a few long sequential streams per CTA
+// instead of many short ones (config 2: 5.0 ms for 35.2 GB = 7.0 TB/s vs
+// 5.7 ms with a warp per row).  Per row: thread partials, butterfly within
+// each warp, then the 8 warp sums in warp order (fixed for every row,
+// independent of the batch it falls in).
+template <int kMode, int kZrB, int kThr>
+__global__ void __launch_bounds__(kThr) k_z_rows_cta(const int* stop, int64_t q0, int64_t q1, int64_t nc,
+                                                     const double* __restrict__ Z, const int32_t* __restrict__ rows,
+                                                     const double* __restrict__ e, double* __restrict__ x, Xchg xc) {
+  if (*stop) return;
+  constexpr int kW = kThr / 32;
+  __shared__ double red[kW][kZrB];
+  unsigned long long ep = 0;
+  if (kMode == 2) ep = xepoch(xc);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t nb = (q1 - q0 + kZrB - 1) / kZrB;
+  for (int64_t bt = blockIdx.x; bt < nb; bt += gridDim.x) {
+    const int64_t qb = q0 + bt * kZrB;
+    const int nr = (int)min((int64_t)kZrB, q1 - qb);
+    double acc[kZrB];
+#pragma unroll
+    for (int r = 0; r < kZrB; ++r) acc[r] = 0.0;
+    for (int64_t c = 2 * t; c + 1 < nc; c += 2 * kThr) {
+      const double2 ev = *reinterpret_cast<const double2*>(e + c);
+      double2 z[kZrB];
+#pragma unroll
+      for (int r = 0; r < kZrB; ++r) {
+        const int64_t off = (qb + r) * nc + c;
+        z[r] = r < nr ? ld_z2(Z + off, (off & 1) == 0) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int r = 0; r < kZrB; ++r) acc[r] = fma(z[r].x, ev.x, fma(z[r].y, ev.y, acc[r]));
+    }
+    if ((nc & 1) && t == ((nc - 1) % (2 * kThr)) / 2) {
+      const int64_t c = nc - 1;
+#pragma unroll
+      for (int r = 0; r < kZrB; ++r)
+        if (r < nr) acc[r] = fma(Z[(qb + r) * nc + c], e[c], acc[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < kZrB; ++r) {
+      double v = acc[r];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red[w][r] = v;
+    }
+    __syncthreads();
+    if (t < nr) {
+      double v = 0.0;
+      for (int k = 0; k < kW; ++k) v += red[k][t];
+      const int64_t q = qb + t;
+      if (kMode == 2) {
+        for (int r = 0; r < xc.nranks; ++r) xarea(xc, r, ep + 1)[q] = v;
+      } else if (kMode == 1) {
+        x[q] = v;
+      } else {
+        x[rows[q]] -= v;
+      }
+    }
+    __syncthreads();
   }
   if (kMode == 2) xsignal(xc, ep);
 }
@@ -152,16 +255,23 @@ __global__ void __launch_bounds__(256) k_zt_partial(const int* stop, int64_t nG,
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   if (c + 3 < nc && (nc & 1) == 0) {
     int64_t q = q0;
-    for (; q + 1 < q1; q += 2) {
-      const double2 u0 = __ldcs(reinterpret_cast<const double2*>(Z + q * nc + c));
-      const double2 u1 = __ldcs(reinterpret_cast<const double2*>(Z + q * nc + c + 2));
-      const double2 w0 = __ldcs(reinterpret_cast<const double2*>(Z + (q + 1) * nc + c));
-      const double2 w1 = __ldcs(reinterpret_cast<const double2*>(Z + (q + 1) * nc + c + 2));
-      const double s0 = rv[q - q0], s1 = rv[q + 1 - q0];
-      a0 = fma(w0.x, s1, fma(u0.x, s0, a0));
-      a1 = fma(w0.y, s1, fma(u0.y, s0, a1));
-      a2 = fma(w1.x, s1, fma(u1.x, s0, a2));
-      a3 = fma(w1.y, s1, fma(u1.y, s0, a3));
+    // four rows in flight (8 x 16-byte loads per thread); the fma chain runs
+    // over the rows in ascending order, exactly as the row-at-a-time tail
+    for (; q + 3 < q1; q += 4) {
+      double2 u[4][2];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        u[k][0] = __ldcs(reinterpret_cast<const double2*>(Z + (q + k) * nc + c));
+        u[k][1] = __ldcs(reinterpret_cast<const double2*>(Z + (q + k) * nc + c + 2));
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double sk = rv[q + k - q0];
+        a0 = fma(u[k][0].x, sk, a0);
+        a1 = fma(u[k][0].y, sk, a1);
+        a2 = fma(u[k][1].x, sk, a2);
+        a3 = fma(u[k][1].y, sk, a3);
+      }
     }
     for (; q < q1; ++q) {
       const double s0 = rv[q - q0];
@@ -186,18 +296,24 @@ struct GrpBounds {
 };
 
 // bc[c] -= sum_g (sum_{ch in group g} partial[ch][c])  -- the same two-level
-// order as the distributed group sums (dist.cu), hence bit-identical to them
-__global__ void k_zt_reduce(const int* stop, int64_t nc, const double* __restrict__ partial, GrpBounds grp,
-                            double* __restrict__ bc) {
+// order as the distributed group sums (dist.cu), hence bit-identical to them.
+// CTA = 32 columns x kGroups warps: warp g sums group g, warp 0 folds.
+__global__ void __launch_bounds__(32 * kGroups) k_zt_reduce(const int* stop, int64_t nc,
+                                                            const double* __restrict__ partial, GrpBounds grp,
+                                                            double* __restrict__ bc) {
   if (*stop) return;
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += (int64_t)gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int g = 0; g < kGroups; ++g) {
-      double gs = 0.0;
-      for (int64_t ch = grp.b[g]; ch < grp.b[g + 1]; ++ch) gs += partial[ch * nc + c];
-      acc += gs;
-    }
-    bc[c] -= acc;
+  __shared__ double gs[kGroups][32];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  double acc = 0.0;
+  if (c < nc)
+    for (int64_t ch = grp.b[g]; ch < grp.b[g + 1]; ++ch) acc += partial[ch * nc + c];
+  gs[g][lane] = acc;
+  __syncthreads();
+  if (g == 0 && c < nc) {
+    double t = 0.0;
+    for (int k = 0; k < kGroups; ++k) t += gs[k][lane];
+    bc[c] -= t;
   }
 }
 
@@ -424,13 +540,29 @@ static void launch_rows(const int* stop, int64_t q0, int64_t q1, int64_t nc, con
     HC_CUDA(cudaFuncSetAttribute(k_z_rows<true, kMode>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     init = true;
   }
+  const char* zr = getenv("HCAMG_ZROWS");
+  const int variant = zr ? atoi(zr) : 1;  // HCAMG_ZROWS=0: warp-per-row kernel (comparison)
+  if (nc >= 4096 && variant > 0) {
+    auto go = [&](auto kern, int rb, int thr) {
+      int per_sm = 0;
+      HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, thr, 0));
+      const int64_t nb = (nrows + rb - 1) / rb;
+      const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)kSMs * std::max(per_sm, 1)));
+      kern<<<g, thr, 0, s>>>(stop, q0, q1, nc, Z, rows, e, x, xc);
+    };
+    go(k_z_rows_cta<kMode, 16, 256>, 16, 256);  // measured best of 4..16 rows x 128..1024 threads
+    HC_CHECK_LAUNCH();
+    return;
+  }
+  // 16 warps per CTA, two rows per warp
+  const int64_t ctas = std::max<int64_t>(1, (nrows + 31) / 32);
   if (smem) {
     // e staged once per CTA; as many 512-thread CTAs per SM as shared memory allows (<= 4)
     const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (220 * 1024) / std::max<int64_t>(8 * nc, 1)));
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nrows + 15) / 16, kSMs * per_sm));
+    const unsigned g = (unsigned)std::min<int64_t>(ctas, kSMs * per_sm);
     k_z_rows<true, kMode><<<g, 512, sizeof(double) * nc, s>>>(stop, q0, q1, nc, Z, rows, e, x, xc);
   } else {
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nrows + 15) / 16, kSMs * 4));
+    const unsigned g = (unsigned)std::min<int64_t>(ctas, kSMs * 4);
     k_z_rows<false, kMode><<<g, 512, 0, s>>>(stop, q0, q1, nc, Z, rows, e, x, xc);
   }
   HC_CHECK_LAUNCH();
@@ -499,7 +631,7 @@ void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, 
         stop, hp.nG, hp.nc, hp.chunk, 0, hp.Z.p, hp.rows.p, r, hp.partial.p);
     GrpBounds g{};
     for (int t = 0; t <= kGroups; ++t) g.b[t] = hp.grp[t];
-    k_zt_reduce<<<grid_for(hp.nc, 256), 256, 0, s>>>(stop, hp.nc, hp.partial.p, g, bc);
+    k_zt_reduce<<<(unsigned)((hp.nc + 31) / 32), 32 * kGroups, 0, s>>>(stop, hp.nc, hp.partial.p, g, bc);
     HC_CHECK_LAUNCH();
     return;
   }

@@ -16,10 +16,21 @@ dev = h._dev
 cap = 64
 kind = np.zeros(cap, np.int32); level = np.zeros(cap, np.int32); us = np.zeros(cap); nl = np.zeros(cap, np.int64)
 cnt = C.c_int32()
-dev.check(dev.lib.hcamg_profile_vcycle(dev.h, 50, cap, _lib.ptr(kind), _lib.ptr(level), _lib.ptr(us), _lib.ptr(nl),
-                                       C.byref(cnt)))
-tot = 0
-for i in range(cnt.value):
-    print(f"L{level[i]} {NAMES[kind[i]]:10s} {us[i]:9.2f} us  launches {nl[i]}")
-    tot += us[i]
-print(f"V-cycle sum {tot:.1f} us; levels {[lv.n for lv in h.levels]}; waves {[lv._info.n_waves for lv in h.levels]}")
+import os
+
+# optional: "ENV=v1,v2,..." as argv[3] re-times the pieces once per value of ENV
+sweeps = [(None, None)]
+if len(sys.argv) > 3:
+    var, vals = sys.argv[3].split("=")
+    sweeps = [(var, v) for v in vals.split(",")]
+for var, val in sweeps:
+    if var:
+        os.environ[var] = val
+        print(f"-- {var}={val}")
+    dev.check(dev.lib.hcamg_profile_vcycle(dev.h, 10 if h.levels[0].n > 100000 else 50, cap, _lib.ptr(kind),
+                                           _lib.ptr(level), _lib.ptr(us), _lib.ptr(nl), C.byref(cnt)))
+    tot = 0
+    for i in range(cnt.value):
+        print(f"L{level[i]} {NAMES[kind[i]]:10s} {us[i]:9.2f} us  launches {nl[i]}")
+        tot += us[i]
+    print(f"V-cycle sum {tot:.1f} us; levels {[lv.n for lv in h.levels]}; waves {[lv._info.n_waves for lv in h.levels]}")
