@@ -145,3 +145,45 @@ def test_prepare_validates(system16):
     assert dev.lib.hcamg_dist_prepare(dev.h, 2, 2, None, C.byref(p)) != 0
     assert dev.lib.hcamg_dist_prepare(dev.h, 0, 9, None, C.byref(p)) != 0
     assert dev.lib.hcamg_dist_connect_ptrs(dev.h, None) != 0
+
+
+def _odd_dense_system(n=4097):
+    import scipy.sparse as sp
+    rng = np.random.default_rng(11)
+    main = 2.5 + rng.uniform(0, 1, n)
+    off = -np.ones(n - 1)
+    return sp.csr_matrix(sp.diags([off, main, off], [-1, 0, 1]))
+
+
+@pytest.mark.parametrize("zrows", ["1", "0"])
+def test_row_gemv_odd_width_unaligned_rows(monkeypatch, zrows):
+    """n = 4097 (odd): every other row of the row-major inverse starts 8 bytes
+    off a 16-byte boundary; both row-GEMV kernels must handle it."""
+    monkeypatch.setenv("HCAMG_COARSE_GEMV_MIN", "0")
+    monkeypatch.setenv("HCAMG_ZROWS", zrows)
+    A = _odd_dense_system()
+    h = P.Hierarchy([P.Level(A=A)], "alg")
+    b = np.random.default_rng(2).uniform(-1, 1, A.shape[0])
+    x = P.vcycle(h, b)
+    xr = np.linalg.solve(A.toarray(), b)
+    assert np.linalg.norm(x - xr) <= 1e-12 * np.linalg.norm(xr)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_emulated_ranks_wide_coarse_exchange(monkeypatch, nranks):
+    """Row-batched GEMV (n >= 4096, odd n) in exchange mode, emulated ranks."""
+    monkeypatch.setenv("HCAMG_COARSE_GEMV_MIN", "0")
+    A = _odd_dense_system()
+    b = np.random.default_rng(4).uniform(-1, 1, A.shape[0])
+    x_ref = P.vcycle(P.Hierarchy([P.Level(A=A)], "alg"), b)
+    ranks = [P.Hierarchy([P.Level(A=A.copy())], "alg") for _ in range(nranks)]
+    ptrs = [_prepare(h, r, nranks) for r, h in enumerate(ranks)]
+    for h in ranks:
+        _connect_ptrs(h, ptrs)
+    for part in (1, 2):
+        for h in ranks:
+            _piece(h, 0, PC_COARSE, part, b=b if part == 1 else None)
+    for h in ranks:
+        x = np.empty(A.shape[0])
+        _piece(h, 0, -1, 0, x=x)
+        assert np.array_equal(x, x_ref)
