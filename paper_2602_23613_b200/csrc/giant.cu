@@ -236,10 +236,14 @@ __global__ void __launch_bounds__(kThr) k_z_rows_cta(const int* stop, int64_t q0
 }
 
 // Restriction, dense part: partial[ch][c] = sum_{q in chunk ch} Z[q, c] r[rows[q]]
-// for chunks [ch0, ch0 + gridDim.y).  CTA = (1024-column tile, row chunk);
-// 4 columns per thread (two 16-byte loads), two rows in flight.
+// for chunks [ch0, ch0 + gridDim.y).  CTA = (256 * kCpt-column tile, row
+// chunk); kCpt contiguous columns per thread (kCpt/2 16-byte loads per row),
+// kRif rows in flight.  Every column's fma chain runs over the chunk's rows
+// in ascending order whatever kCpt / kRif are, so the variants agree bit for
+// bit.  kZtCols is the tile width the chunk plan assumes (dist.py mirrors it).
 constexpr int kZtCols = 1024;
 
+template <int kCpt, int kRif>
 __global__ void __launch_bounds__(256) k_zt_partial(const int* stop, int64_t nG, int64_t nc, int64_t chunk,
                                                     int64_t ch0, const double* __restrict__ Z,
                                                     const int32_t* __restrict__ rows, const double* __restrict__ r,
@@ -250,45 +254,57 @@ __global__ void __launch_bounds__(256) k_zt_partial(const int* stop, int64_t nG,
   const int64_t q0 = ch * chunk, q1 = min(nG, q0 + chunk);
   for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) rv[q - q0] = r[rows[q]];
   __syncthreads();
-  const int64_t c = (int64_t)blockIdx.x * kZtCols + 4 * threadIdx.x;
+  const int64_t c = (int64_t)blockIdx.x * (256 * kCpt) + kCpt * threadIdx.x;
   if (c >= nc) return;
-  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-  if (c + 3 < nc && (nc & 1) == 0) {
+  double a[kCpt];
+#pragma unroll
+  for (int j = 0; j < kCpt; ++j) a[j] = 0.0;
+  if (c + kCpt - 1 < nc && (nc & 1) == 0) {
     int64_t q = q0;
-    // four rows in flight (8 x 16-byte loads per thread); the fma chain runs
-    // over the rows in ascending order, exactly as the row-at-a-time tail
-    for (; q + 3 < q1; q += 4) {
-      double2 u[4][2];
+    for (; q + kRif - 1 < q1; q += kRif) {
+      double2 u[kRif][kCpt / 2];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        u[k][0] = __ldcs(reinterpret_cast<const double2*>(Z + (q + k) * nc + c));
-        u[k][1] = __ldcs(reinterpret_cast<const double2*>(Z + (q + k) * nc + c + 2));
-      }
+      for (int k = 0; k < kRif; ++k)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+        for (int j = 0; j < kCpt / 2; ++j) u[k][j] = __ldcs(reinterpret_cast<const double2*>(Z + (q + k) * nc + c + 2 * j));
+#pragma unroll
+      for (int k = 0; k < kRif; ++k) {
         const double sk = rv[q + k - q0];
-        a0 = fma(u[k][0].x, sk, a0);
-        a1 = fma(u[k][0].y, sk, a1);
-        a2 = fma(u[k][1].x, sk, a2);
-        a3 = fma(u[k][1].y, sk, a3);
+#pragma unroll
+        for (int j = 0; j < kCpt / 2; ++j) {
+          a[2 * j] = fma(u[k][j].x, sk, a[2 * j]);
+          a[2 * j + 1] = fma(u[k][j].y, sk, a[2 * j + 1]);
+        }
       }
     }
     for (; q < q1; ++q) {
       const double s0 = rv[q - q0];
-      a0 = fma(Z[q * nc + c], s0, a0);
-      a1 = fma(Z[q * nc + c + 1], s0, a1);
-      a2 = fma(Z[q * nc + c + 2], s0, a2);
-      a3 = fma(Z[q * nc + c + 3], s0, a3);
+#pragma unroll
+      for (int j = 0; j < kCpt; ++j) a[j] = fma(Z[q * nc + c + j], s0, a[j]);
     }
     double* o = partial + ch * nc + c;
-    o[0] = a0; o[1] = a1; o[2] = a2; o[3] = a3;
+#pragma unroll
+    for (int j = 0; j < kCpt; ++j) o[j] = a[j];
   } else {
-    for (int t = 0; t < 4 && c + t < nc; ++t) {
-      double a = 0.0;
-      for (int64_t q = q0; q < q1; ++q) a = fma(Z[q * nc + c + t], rv[q - q0], a);
-      partial[ch * nc + c + t] = a;
+    for (int t = 0; t < kCpt && c + t < nc; ++t) {
+      double acc = 0.0;
+      for (int64_t q = q0; q < q1; ++q) acc = fma(Z[q * nc + c + t], rv[q - q0], acc);
+      partial[ch * nc + c + t] = acc;
     }
   }
+}
+
+// launch the partials of chunks [c0, c1)
+static void launch_zt_partial(const int* stop, const HybridP& hp, int64_t c0, int64_t c1, const double* r,
+                              cudaStream_t s) {
+  if (c1 <= c0) return;
+  // 4 columns x 4 rows in flight per thread; measured on config 2 against
+  // 2/8/16 columns and 2/8 rows: wider tiles are slower, the rest equal
+  constexpr int kCpt = 4;
+  const unsigned tiles = (unsigned)((hp.nc + 256 * kCpt - 1) / (256 * kCpt));
+  k_zt_partial<kCpt, 4><<<dim3(tiles, (unsigned)(c1 - c0)), 256, sizeof(double) * hp.chunk, s>>>(
+      stop, hp.nG, hp.nc, hp.chunk, c0, hp.Z.p, hp.rows.p, r, hp.partial.p);
+  HC_CHECK_LAUNCH();
 }
 
 struct GrpBounds {
@@ -624,11 +640,9 @@ void hybrid_prepare(HybridP& hp, cudaStream_t s) {
 void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, cudaStream_t s, const Dist* d,
                      size_t off, int part) {
   require(hp.nchunk > 0, "hybrid_restrict: plan not prepared");
-  const unsigned tiles = (unsigned)((hp.nc + kZtCols - 1) / kZtCols);
   if (!dist_on(d)) {
     if (part == 2) return;
-    k_zt_partial<<<dim3(tiles, (unsigned)hp.nchunk), 256, sizeof(double) * hp.chunk, s>>>(
-        stop, hp.nG, hp.nc, hp.chunk, 0, hp.Z.p, hp.rows.p, r, hp.partial.p);
+    launch_zt_partial(stop, hp, 0, hp.nchunk, r, s);
     GrpBounds g{};
     for (int t = 0; t <= kGroups; ++t) g.b[t] = hp.grp[t];
     k_zt_reduce<<<(unsigned)((hp.nc + 31) / 32), 32 * kGroups, 0, s>>>(stop, hp.nc, hp.partial.p, g, bc);
@@ -639,11 +653,7 @@ void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, 
   if (part != 2) {
     int g0, g1;
     rank_groups(d->rank, d->nranks, g0, g1);
-    const int64_t c0 = hp.grp[g0], c1 = hp.grp[g1];
-    if (c1 > c0)
-      k_zt_partial<<<dim3(tiles, (unsigned)(c1 - c0)), 256, sizeof(double) * hp.chunk, s>>>(
-          stop, hp.nG, hp.nc, hp.chunk, c0, hp.Z.p, hp.rows.p, r, hp.partial.p);
-    HC_CHECK_LAUNCH();
+    launch_zt_partial(stop, hp, hp.grp[g0], hp.grp[g1], r, s);
     xchg_group_sums(stop, xc, hp.nc, hp.partial.p, hp.grp, g0, g1, s);
   }
   if (part != 1) xchg_group_final(stop, xc, hp.nc, bc, s);
