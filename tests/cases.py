@@ -12,7 +12,8 @@ import scipy.sparse as sp
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 CASES = ["tri2_alg", "tri3s_alg", "tri3s_ref", "tri5s_alg", "tri5s_ref", "quad3_alg",
-         "quad3_ref", "kuhn4_c1", "kuhn8_c2", "kuhn8_c1", "kuhn8_c3ref", "kuhn8_c2ref"]
+         "quad3_ref", "kuhn4_c1", "kuhn8_c2", "kuhn8_c1", "kuhn8_c3ref", "kuhn8_c2ref",
+         "kuhn8_c4", "kuhn8_c5"]
 
 
 def sha(*arrays):

@@ -25,5 +25,16 @@ def main():
     run_case("kuhn8_c2ref", s, "ref", meshes, rmaps, full=False)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not (len(sys.argv) > 1 and sys.argv[1] == "more"):
     main()
+
+
+def more_fields():
+    """configs[3] (64 seeded inclusions, beta 1e-4) and configs[4] (8^3
+    checkerboard 1 / 1e6) coefficient fields on the n = 8 cube, "alg" route."""
+    run_case("kuhn8_c4", kuhn.config_system("c4", n=8), "alg", full=False)
+    run_case("kuhn8_c5", kuhn.config_system("c5", n=8), "alg", full=False)
+
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "more":
+    more_fields()
