@@ -75,6 +75,19 @@ def test_hierarchy_integers_bit_exact(pair):
         assert all(np.array_equal(a, b) for a, b in zip(lg.patches.patches, lo.patches.patches))
 
 
+def test_splitting_text_matches_reference_dump(pair):
+    """The GPU splittings written in the reference's text format
+    (splitting.py:375-380) hash to the reference's own dumps."""
+    import hashlib
+
+    from paper_2602_23613_b200.formats import dump_splitting
+    name, c, ho, hg = pair
+    for ell, ref in enumerate(c.meta["levels"]):
+        if "dump_sha" in ref:
+            text = dump_splitting(hg.levels[ell].splitting)
+            assert hashlib.sha256(text.encode()).hexdigest() == ref["dump_sha"], f"level {ell}"
+
+
 def test_hierarchy_values(pair):
     name, c, ho, hg = pair
     tol = c.tol
