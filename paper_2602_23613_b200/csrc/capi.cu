@@ -202,9 +202,11 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
   require(Gh->nrows == Ah->nrows, "G rows must match A");
   HC_CUDA(cudaStreamSynchronize(s));
   auto t0 = std::chrono::steady_clock::now();
+  StageTimer st(s);
   auto cur = std::make_unique<DevLevel>();
   upload_csr(Ah, cur->A, s);
   upload_csr(Gh, cur->G, s);
+  st.mark("upload");
   int32_t pos = method == 0 ? chain->nm - 1 : 0;
   std::vector<int64_t> e2d;
   if (method == 0) e2d.assign(chain->free_edges, chain->free_edges + chain->ne[chain->nm - 1]);
@@ -231,6 +233,7 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
       mode = 0;
     } else {
       algebraic_splitting(cur->A, cur->G, theta, sp, s);
+      st.mark("splitting");
       if (sp.n_pairs() == 0 || sp.n_pairs() >= n) {
         if (sp.n_pairs() == 0) {
           h->stalled = true;
@@ -242,6 +245,7 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
     }
     InterpResult ip;
     build_interp(cur->A, cur->G, sp, mode, h->cublas, ip, s);
+    st.mark("interpolation");
     if (ip.P.ncols == 0 || ip.P.ncols >= n) {
       h->stalled = true;
       h->notes.push_back("no size reduction (" + std::to_string(n) + " -> " + std::to_string(ip.P.ncols) + ")");
@@ -250,6 +254,7 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
     auto next = std::make_unique<DevLevel>();
     if (ip.hp.on) galerkin_hybrid(h->cublas, cur->A, ip.P, ip.Pt, ip.hp, next->A, s);
     else galerkin(ip.P, ip.Pt, cur->A, next->A, s);
+    st.mark("galerkin");
     cur->hp = std::move(ip.hp);
     if (cur->hp.on) hybrid_prepare(cur->hp, s);
     next->G = std::move(ip.Gc);
@@ -265,11 +270,14 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
     }
     cur->split = std::move(sp);
     finish_level(h, *cur);
+    st.mark("smoother + level data");
     h->levels.push_back(std::move(cur));
     cur = std::move(next);
   }
   factor_coarsest(h, *cur, cur->A);
+  st.mark("coarsest factor");
   finish_level(h, *cur);
+  st.mark("coarsest level data");
   h->levels.push_back(std::move(cur));
   refresh_views(h);
   HC_CUDA(cudaStreamSynchronize(s));

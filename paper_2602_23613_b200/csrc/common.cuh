@@ -6,6 +6,9 @@
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 #include <utility>
 #include <vector>
@@ -109,6 +112,22 @@ struct DCsr {
     ptr.alloc(r + 1, s);
     idx.alloc(z, s);
     val.alloc(z, s);
+  }
+};
+
+// HCAMG_SETUP_TIMING=1: print the wall time of setup stages to stderr
+// (synchronises the stream at every mark; off by default).
+struct StageTimer {
+  cudaStream_t s;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit StageTimer(cudaStream_t st) : s(st), on(getenv("HCAMG_SETUP_TIMING") != nullptr), t(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[hcamg setup] %-28s %9.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    t = now;
   }
 };
 

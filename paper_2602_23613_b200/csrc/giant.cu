@@ -4,18 +4,22 @@
 // (transfer.py:77-122) is one connected component with ~80 % of the DoFs
 // (SURVEY.md F3), so P has dense interior rows and the work is dense linear
 // algebra:
-//   * Cholesky of A_GG in packed lower tiles (NB = 1024, only the T(T+1)/2
-//     lower tiles are stored: 113 GB instead of 225 GB at n = 32), right-
-//     looking: own POTRF on the diagonal tile, batched cuBLAS DTRSM/DGEMM
-//     panels (FP64; cuBLAS only for these plain level-3 calls);
-//   * Z = A_GG^{-1} W' solved in place on the row-major RHS (= the
-//     column-major transpose), tile by tile from the right;
+//   * Cholesky of A_GG after a reverse Cuthill-McKee ordering -- the ordering
+//     the reference's own cholesky() applies to components above its dense
+//     cutoff (sparse.py:276-301) -- kept in NB = 1024 tiles inside the block
+//     envelope only (config 2: 5.4 GB instead of 113 GB for all lower tiles,
+//     ~1 s instead of ~50 s), right-looking: own POTRF on the diagonal tile,
+//     batched cuBLAS DTRSM/DGEMM panels (FP64; cuBLAS only for these plain
+//     level-3 calls);
+//   * Z = A_GG^{-1} W' solved on the row-major RHS (= the column-major
+//     transpose) in the factored order, envelope tiles only (~4 s);
 //   * P = P_s - S_G Z applied as CSR + a dense row-major block streamed at
-//     HBM bandwidth (prolongation: one warp per row; restriction: chunked
-//     column sums reduced in a fixed order);
+//     HBM bandwidth (prolongation: row batches per CTA; restriction: chunked
+//     column sums reduced in a fixed two-level order);
 //   * Galerkin A_c = P^T A P in Schur form with the solve residual
 //     rho = W' - A_GG Z (exact in exact arithmetic, second order in the
-//     component-solve error like the reference's P^T (A P)).
+//     component-solve error like the reference's P^T (A P)); Z^T rho on the
+//     tensor cores in TF32 (see galerkin_hybrid).
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -36,27 +40,47 @@ void cb(cublasStatus_t st, const char* what) {
   if (st != CUBLAS_STATUS_SUCCESS) throw Error(ECUDA_, std::string("cuBLAS failure in ") + what);
 }
 
+// Lower Cholesky factor in NB x NB column-major tiles, stored only inside the
+// block envelope: block row I keeps tiles J in [j0[I], I], where j0[I] is the
+// tile of the first nonzero of any row of the block.  Cholesky fill never
+// leaves the envelope (row i of L starts where row i of A starts), so this
+// is exact; under a reverse Cuthill-McKee order the envelope of config 2's
+// 167,784-row block is 5.4 GB instead of the 113 GB of all lower tiles.
 struct Packed {
   int64_t n = 0, T = 0;
+  std::vector<int64_t> j0, off;
   DBuf<double> buf;
-  double* tile(int64_t I, int64_t J) const { return buf.p + ((I * (I + 1)) / 2 + J) * kNB * kNB; }
+  bool has(int64_t I, int64_t J) const { return J >= j0[(size_t)I] && J <= I; }
+  double* tile(int64_t I, int64_t J) const { return buf.p + (off[(size_t)I] + J - j0[(size_t)I]) * kNB * kNB; }
 };
 
-__global__ void k_pack_lower(const int64_t* __restrict__ ap, const int32_t* __restrict__ ai,
-                             const double* __restrict__ av, int64_t n, int64_t T, double* __restrict__ buf) {
+__global__ void k_pack_env(const int64_t* __restrict__ ap, const int32_t* __restrict__ ai,
+                           const double* __restrict__ av, int64_t n, int64_t T, const int64_t* __restrict__ j0,
+                           const int64_t* __restrict__ off, double* __restrict__ buf) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < T * kNB;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t I = q / kNB, li = q % kNB;
     if (q >= n) {  // identity padding keeps the padded matrix SPD
-      buf[((I * (I + 1)) / 2 + I) * kNB * kNB + li + li * kNB] = 1.0;
+      buf[(off[I] + I - j0[I]) * kNB * kNB + li + li * kNB] = 1.0;
       continue;
     }
     for (int64_t e = ap[q]; e < ap[q + 1]; ++e) {
       const int64_t j = ai[e];
-      if (j > q) break;
+      if (j > q) continue;  // columns need not be sorted (permuted input)
       const int64_t J = j / kNB, lj = j % kNB;
-      buf[((I * (I + 1)) / 2 + J) * kNB * kNB + li + lj * kNB] = av[e];
+      buf[(off[I] + J - j0[I]) * kNB * kNB + li + lj * kNB] = av[e];
     }
+  }
+}
+
+// out[i, :] = in[src[i], :] (kScatter: out[src[i], :] = in[i, :]) for row-major n x m
+template <bool kScatter>
+__global__ void k_permute_rows(int64_t n, int64_t m, const int32_t* __restrict__ src, const double* __restrict__ in,
+                               double* __restrict__ out) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const double* a = kScatter ? in + i * m : in + (int64_t)src[i] * m;
+    double* b = kScatter ? out + (int64_t)src[i] * m : out + i * m;
+    for (int64_t c = threadIdx.x; c < m; c += blockDim.x) b[c] = a[c];
   }
 }
 
@@ -348,6 +372,16 @@ __global__ void __launch_bounds__(256) k_spmm_rows(const int64_t* __restrict__ a
   }
 }
 
+__global__ void k_to_f32(const double* __restrict__ in, int64_t n, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (float)in[i];
+}
+
+__global__ void k_to_f64(const float* __restrict__ in, int64_t n, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (double)in[i];
+}
+
 __global__ void k_add_csr_dense(const int64_t* __restrict__ wp, const int32_t* __restrict__ wi,
                                 const double* __restrict__ wv, int64_t n, int64_t nc, double* __restrict__ Y) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
@@ -457,17 +491,113 @@ __global__ void k_fill_m1(int32_t* v, int64_t n) {
 
 }  // namespace
 
+// Reverse Cuthill-McKee order of a symmetric pattern: scipy's algorithm
+// (csgraph reverse_cuthill_mckee, the ordering the reference's cholesky()
+// applies before factoring, sparse.py:297): degree = row length (+1 when the
+// diagonal is stored); seeds by increasing degree; BFS by levels, each node's
+// unvisited neighbours appended in column order and insertion-sorted by
+// degree; the final order reversed.  Seed ties are taken by lowest index
+// (scipy's argsort is not stable, so its tie choice is platform dependent).
+static std::vector<int32_t> rcm_order(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx) {
+  std::vector<int64_t> deg((size_t)n);
+  for (int64_t i = 0; i < n; ++i) {
+    deg[(size_t)i] = ptr[(size_t)i + 1] - ptr[(size_t)i];
+    for (int64_t e = ptr[(size_t)i]; e < ptr[(size_t)i + 1]; ++e)
+      if (idx[(size_t)e] == i) {
+        ++deg[(size_t)i];
+        break;
+      }
+  }
+  std::vector<int32_t> seeds((size_t)n);
+  for (int64_t i = 0; i < n; ++i) seeds[(size_t)i] = (int32_t)i;
+  std::stable_sort(seeds.begin(), seeds.end(), [&](int32_t a, int32_t b) { return deg[(size_t)a] < deg[(size_t)b]; });
+  std::vector<char> seen((size_t)n, 0);
+  std::vector<int32_t> order;
+  order.reserve((size_t)n);
+  for (int64_t zz = 0; zz < n && (int64_t)order.size() < n; ++zz) {
+    const int32_t seed = seeds[(size_t)zz];
+    if (seen[(size_t)seed]) continue;
+    seen[(size_t)seed] = 1;
+    order.push_back(seed);
+    size_t lo = order.size() - 1, hi = order.size();
+    while (lo < hi) {
+      for (size_t ii = lo; ii < hi; ++ii) {
+        const int32_t i = order[ii];
+        const size_t n_old = order.size();
+        for (int64_t e = ptr[(size_t)i]; e < ptr[(size_t)i + 1]; ++e) {
+          const int32_t j = idx[(size_t)e];
+          if (!seen[(size_t)j]) {
+            seen[(size_t)j] = 1;
+            order.push_back(j);
+          }
+        }
+        for (size_t k = n_old + 1; k < order.size(); ++k) {  // stable insertion sort by degree
+          const int32_t v = order[k];
+          size_t l = k;
+          while (l > n_old && deg[(size_t)v] < deg[(size_t)order[l - 1]]) {
+            order[l] = order[l - 1];
+            --l;
+          }
+          order[l] = v;
+        }
+      }
+      lo = hi;
+      hi = order.size();
+    }
+  }
+  std::reverse(order.begin(), order.end());
+  return order;
+}
+
 void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m, cudaStream_t s) {
   const int64_t n = Agg.nrows;
+  StageTimer st(s);
+  // ordering: reverse Cuthill-McKee (default) or the natural component order
+  std::vector<int64_t> hptr = Agg.ptr.download();
+  std::vector<int32_t> hidx = Agg.idx.download();
+  std::vector<int32_t> perm;
+  const char* ord = getenv("HCAMG_GIANT_ORDER");
+  if (ord && std::string(ord) == "natural") {
+    perm.resize((size_t)n);
+    for (int64_t i = 0; i < n; ++i) perm[(size_t)i] = (int32_t)i;
+  } else {
+    perm = rcm_order(n, hptr, hidx);
+  }
+  std::vector<int32_t> inv((size_t)n);
+  for (int64_t i = 0; i < n; ++i) inv[(size_t)perm[(size_t)i]] = (int32_t)i;
+  DBuf<int32_t> dperm, dinv;
+  dperm.upload(perm.data(), n);
+  dinv.upload(inv.data(), n);
+  DCsr Ap;
+  csr_extract(Agg, dperm.p, n, dinv.p, n, Ap, s);
+  // block envelope
   Packed L;
   L.n = n;
   L.T = (n + kNB - 1) / kNB;
   const int64_t T = L.T;
-  const int64_t ntiles = T * (T + 1) / 2;
+  L.j0.assign((size_t)T, 0);
+  for (int64_t I = 0; I < T; ++I) L.j0[(size_t)I] = I;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t f = i;
+    const int32_t r = perm[(size_t)i];
+    for (int64_t e = hptr[(size_t)r]; e < hptr[(size_t)r + 1]; ++e) f = std::min<int64_t>(f, inv[(size_t)hidx[(size_t)e]]);
+    int64_t& j0 = L.j0[(size_t)(i / kNB)];
+    j0 = std::min(j0, f / kNB);
+  }
+  L.off.assign((size_t)T + 1, 0);
+  for (int64_t I = 0; I < T; ++I) L.off[(size_t)I + 1] = L.off[(size_t)I] + (I - L.j0[(size_t)I] + 1);
+  const int64_t ntiles = L.off[(size_t)T];
+  st.mark("  giant: order + envelope");
   L.buf.alloc(ntiles * kNB * kNB, s);
   L.buf.zero();
-  k_pack_lower<<<grid_for(T * kNB, 256), 256, 0, s>>>(Agg.ptr.p, Agg.idx.p, Agg.val.p, n, T, L.buf.p);
-  HC_CHECK_LAUNCH();
+  {
+    DBuf<int64_t> dj0, doff;
+    dj0.upload(L.j0.data(), T);
+    doff.upload(L.off.data(), T + 1);
+    k_pack_env<<<grid_for(T * kNB, 256), 256, 0, s>>>(Ap.ptr.p, Ap.idx.p, Ap.val.p, n, T, dj0.p, doff.p, L.buf.p);
+    HC_CHECK_LAUNCH();
+    HC_CUDA(cudaStreamSynchronize(s));
+  }
   DBuf<unsigned long long> mx(1, s);
   mx.zero();
   k_csr_diag_absmax<<<grid_for(n, 256), 256, 0, s>>>(Agg.ptr.p, Agg.idx.p, Agg.val.p, n, mx.p);
@@ -481,30 +611,32 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
   DBuf<const double*> dA, dB;
   DBuf<const double*> dC;
   int64_t fail = -1;
-  for (int64_t K = 0; K < T; ++K) {
+  for (int64_t K = 0; K < T; ++K) {  // right-looking, inside the envelope
     const int64_t j0 = dense_cholesky_raw(h, L.tile(K, K), kNB, kNB, piv.p + K * kNB, s);
     if (j0 < kNB) {
       fail = K * kNB + j0;
       break;
     }
-    const int64_t rest = T - K - 1;
-    if (rest == 0) break;
+    std::vector<int64_t> below;  // block rows I > K whose envelope reaches column K
+    for (int64_t I = K + 1; I < T; ++I)
+      if (L.has(I, K)) below.push_back(I);
+    if (below.empty()) continue;
     {
-      std::vector<const double*> ha((size_t)rest, L.tile(K, K)), hb;
-      for (int64_t I = K + 1; I < T; ++I) hb.push_back(L.tile(I, K));
+      std::vector<const double*> ha(below.size(), L.tile(K, K)), hb;
+      for (int64_t I : below) hb.push_back(L.tile(I, K));
       const double** pa = upload_ptrs(ha, dA, s);
       const double** pb = upload_ptrs(hb, dB, s);
       cb(cublasDtrsmBatched(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)kNB,
-                            (int)kNB, &one, pa, (int)kNB, (double* const*)pb, (int)kNB, (int)rest),
+                            (int)kNB, &one, pa, (int)kNB, (double* const*)pb, (int)kNB, (int)below.size()),
          "dtrsmBatched");
     }
     {
       std::vector<const double*> ha, hb, hc;
-      for (int64_t I = K + 1; I < T; ++I)
-        for (int64_t J = K + 1; J <= I; ++J) {
-          ha.push_back(L.tile(I, K));
-          hb.push_back(L.tile(J, K));
-          hc.push_back(L.tile(I, J));
+      for (size_t a = 0; a < below.size(); ++a)
+        for (size_t b = 0; b <= a; ++b) {  // (I, J) = (below[a], below[b]), J <= I, both reach K
+          ha.push_back(L.tile(below[a], K));
+          hb.push_back(L.tile(below[b], K));
+          hc.push_back(L.tile(below[a], below[b]));
         }
       const double** pa = upload_ptrs(ha, dA, s);
       const double** pb = upload_ptrs(hb, dB, s);
@@ -516,33 +648,45 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
     }
   }
   {
+    // pivot indices are reported in the factored (permuted) order, as the
+    // reference's cholesky() does for its RCM-permuted matrix
     std::vector<double> hp = piv.download();
     const int64_t j0 = fail >= 0 ? fail : n;
     const int64_t bad = pivot_verdict(hp, n, std::min(j0, n), scale);
     if (bad >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(bad) + ")", bad);
     if (fail >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(fail) + ")", fail);
   }
+  st.mark("  giant: envelope Cholesky");
+  // rows of B into the factored order
+  DBuf<double> Bp(n * m, s);
+  k_permute_rows<false><<<(unsigned)std::min<int64_t>(n, kSMs * 16), 256, 0, s>>>(n, m, dperm.p, B, Bp.p);
+  HC_CHECK_LAUNCH();
   // Solve (A Z = B with B row-major n x m)  <=>  Z^T L L^T = B^T on the column-major m x n view.
   auto nbk = [&](int64_t K) { return std::min(kNB, n - K * kNB); };
-  auto blk = [&](int64_t K) { return B + K * kNB * m; };
+  auto blk = [&](int64_t K) { return Bp.p + K * kNB * m; };
   for (int64_t J = 0; J < T; ++J) {  // U^T = B^T L^{-T}
     cb(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)m, (int)nbk(J),
                    &one, L.tile(J, J), (int)kNB, blk(J), (int)m),
        "dtrsm fwd");
     for (int64_t I = J + 1; I < T; ++I)
-      cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)m, (int)nbk(I), (int)nbk(J), &mone, blk(J), (int)m,
-                     L.tile(I, J), (int)kNB, &one, blk(I), (int)m),
-         "dgemm fwd");
+      if (L.has(I, J))
+        cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)m, (int)nbk(I), (int)nbk(J), &mone, blk(J), (int)m,
+                       L.tile(I, J), (int)kNB, &one, blk(I), (int)m),
+           "dgemm fwd");
   }
   for (int64_t K = T - 1; K >= 0; --K) {  // Z^T = U^T L^{-1}
     cb(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m, (int)nbk(K),
                    &one, L.tile(K, K), (int)kNB, blk(K), (int)m),
        "dtrsm bwd");
-    for (int64_t I = 0; I < K; ++I)
+    for (int64_t I = L.j0[(size_t)K]; I < K; ++I)
       cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)m, (int)kNB, (int)nbk(K), &mone, blk(K), (int)m, L.tile(K, I),
                      (int)kNB, &one, blk(I), (int)m),
          "dgemm bwd");
   }
+  st.mark("  giant: triangular solves");
+  L.buf.release();
+  k_permute_rows<true><<<(unsigned)std::min<int64_t>(n, kSMs * 16), 256, 0, s>>>(n, m, dperm.p, Bp.p, B);
+  HC_CHECK_LAUNCH();
   HC_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -675,22 +819,50 @@ void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr
   csr_extract(A, hp.rows.p, nG, gmap.p, nG, Agg, s);
   AG = DCsr();
   csr_transpose(Wp, WpT, s);
-  // rho = W' - A_GG Z  (row-major nG x nc)
-  DBuf<double> rho(nG * nc, s);
-  k_spmm_rows<<<(unsigned)std::min<int64_t>(nG, kSMs * 16), 256, 0, s>>>(Agg.ptr.p, Agg.idx.p, Agg.val.p, nG, nc,
-                                                                         hp.Z.p, rho.p);
-  k_add_csr_dense<<<grid_for(nG, 256), 256, 0, s>>>(Wp.ptr.p, Wp.idx.p, Wp.val.p, nG, nc, rho.p);
-  HC_CHECK_LAUNCH();
-  // E = Z^T rho (column-major nc x nc)
+  // E = Z^T rho (column-major nc x nc), rho = W' - A_GG Z (row-major nG x nc).
+  // rho is the residual of the component solve: O(eps |A_GG| |Z|), the same
+  // order as the rounding already in the other Galerkin terms (and computed
+  // in fp64 it is itself only accurate to O(1) relative).  Its product with Z
+  // therefore needs no more than a few correct digits: it runs on the tensor
+  // cores in TF32 (rho formed in fp64 block by block, then rounded to fp32),
+  // 2.3e14 flops in well under a second instead of ~7 s of DGEMM.
+  // HCAMG_GALERKIN_E=fp64 keeps the fp64 product (validation).
   DBuf<double> E(nc * nc, s);
-  {
-    cb(cublasSetStream(h, s), "setStream");
+  cb(cublasSetStream(h, s), "setStream");
+  const char* emode = getenv("HCAMG_GALERKIN_E");
+  if (emode && std::string(emode) == "fp64") {
+    DBuf<double> rho(nG * nc, s);
+    k_spmm_rows<<<(unsigned)std::min<int64_t>(nG, kSMs * 16), 256, 0, s>>>(Agg.ptr.p, Agg.idx.p, Agg.val.p, nG, nc,
+                                                                           hp.Z.p, rho.p);
+    k_add_csr_dense<<<grid_for(nG, 256), 256, 0, s>>>(Wp.ptr.p, Wp.idx.p, Wp.val.p, nG, nc, rho.p);
+    HC_CHECK_LAUNCH();
     const double one = 1.0, zero = 0.0;
     cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)nc, (int)nc, (int)nG, &one, hp.Z.p, (int)nc, rho.p, (int)nc,
                    &zero, E.p, (int)nc),
        "dgemm Z^T rho");
+  } else {
+    DBuf<float> Z32(nG * nc, s), rho32(nG * nc, s);
+    k_to_f32<<<grid_for(nG * nc, 256, kSMs * 16), 256, 0, s>>>(hp.Z.p, nG * nc, Z32.p);
+    const int64_t rb = std::max<int64_t>(1, std::min<int64_t>(nG, (int64_t)(512ll << 20) / (8 * std::max<int64_t>(nc, 1))));
+    DBuf<double> blk(rb * nc, s);
+    for (int64_t q0 = 0; q0 < nG; q0 += rb) {
+      const int64_t nr = std::min(rb, nG - q0);
+      k_spmm_rows<<<(unsigned)std::min<int64_t>(nr, kSMs * 16), 256, 0, s>>>(Agg.ptr.p + q0, Agg.idx.p, Agg.val.p, nr,
+                                                                             nc, hp.Z.p, blk.p);
+      k_add_csr_dense<<<grid_for(nr, 256), 256, 0, s>>>(Wp.ptr.p + q0, Wp.idx.p, Wp.val.p, nr, nc, blk.p);
+      k_to_f32<<<grid_for(nr * nc, 256, kSMs * 16), 256, 0, s>>>(blk.p, nr * nc, rho32.p + q0 * nc);
+      HC_CHECK_LAUNCH();
+    }
+    blk.release();
+    DBuf<float> E32(nc * nc, s);
+    const float one = 1.0f, zero = 0.0f;
+    cb(cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)nc, (int)nc, (int)nG, &one, Z32.p, CUDA_R_32F, (int)nc, rho32.p,
+                    CUDA_R_32F, (int)nc, &zero, E32.p, CUDA_R_32F, (int)nc, CUBLAS_COMPUTE_32F_FAST_TF32,
+                    CUBLAS_GEMM_DEFAULT),
+       "gemmEx tf32 Z^T rho");
+    k_to_f64<<<grid_for(nc * nc, 256, kSMs * 16), 256, 0, s>>>(E32.p, nc * nc, E.p);
+    HC_CHECK_LAUNCH();
   }
-  rho.release();
   // D1 = Z^T W'
   DBuf<double> D1(nc * nc, s);
   k_zt_w<<<(unsigned)std::min<int64_t>(nc, kSMs * 16), 256, 0, s>>>(WpT.ptr.p, WpT.idx.p, WpT.val.p, nc, hp.Z.p, D1.p);
