@@ -127,10 +127,6 @@ __global__ void k_densify(const int64_t* __restrict__ p, const int32_t* __restri
     for (int64_t e = p[r]; e < p[r + 1]; ++e) D[r + (int64_t)ix[e] * n] = v[e];  // column-major
 }
 
-__global__ void k_eye(double* D, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * n; i += (int64_t)gridDim.x * blockDim.x)
-    D[i] = (i % (n + 1) == 0) ? 1.0 : 0.0;
-}
 
 // Coarsest level: cholesky(A) (sparse.py:276-301) -> explicit inverse.
 void factor_coarsest(hcamg_handle* h, DevLevel& L, const DCsr& M) {
@@ -158,12 +154,13 @@ void factor_coarsest(hcamg_handle* h, DevLevel& L, const DCsr& M) {
   D.zero();
   k_densify<<<grid_for(n, 128), 128, 0, s>>>(M.ptr.p, M.idx.p, M.val.p, n, D.p);
   HC_CHECK_LAUNCH();
+  StageTimer st(s);
   int64_t bad = dense_cholesky(h->cublas, D.p, n, n, s);
+  st.mark("  coarsest: cholesky");
   if (bad >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(bad) + ")", bad);
   L.Ainv.alloc(n * n, s);
-  k_eye<<<grid_for(n * n, 256), 256, 0, s>>>(L.Ainv.p, n);
-  HC_CHECK_LAUNCH();
-  dense_cholesky_solve(h->cublas, D.p, n, n, L.Ainv.p, n, n, s);
+  dense_spd_inverse(h->cublas, D.p, n, L.Ainv.p, s);
+  st.mark("  coarsest: inverse");
 }
 
 void finish_level(hcamg_handle* h, DevLevel& L) {

@@ -211,6 +211,57 @@ int64_t dense_cholesky(cublasHandle_t h, double* A, int64_t k, int64_t ld, cudaS
   return pivot_verdict(hp, k, j0, scale);
 }
 
+namespace {
+__global__ void k_sym_from_lower(const double* __restrict__ Lw, int64_t n, double* __restrict__ out) {
+  // out (n x n, symmetric) from the lower triangle of Lw (column-major)
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % n, j = t / n;
+    out[t] = i >= j ? Lw[i + j * n] : Lw[j + i * n];
+  }
+}
+__global__ void k_eye_panel(double* __restrict__ X, int64_t n, int64_t j0, int64_t nb) {
+  // X = columns [j0, j0 + nb) of the identity, rows [j0, n) (column-major, ld n)
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (n - j0) * nb; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = j0 + t % (n - j0), c = j0 + t / (n - j0);
+    X[r + c * n] = r == c ? 1.0 : 0.0;
+  }
+}
+}  // namespace
+
+// A^{-1} from its Cholesky factor L (lower, column-major in Lbuf, ld = n),
+// exactly symmetric: Y = L^{-1} block column by block column (TRSM on the
+// trailing panel only, n^3/3 flops), then the lower triangle of Y^T Y block
+// column by block column with TRMM (Y[J:, J] is all of column block J, and
+// Y[J:, J:] is triangular: another n^3/3), written over Lbuf; the full
+// symmetric inverse goes to Ainv.  (Two full TRSMs against the identity
+// cost 2 n^3.)
+void dense_spd_inverse(cublasHandle_t h, double* Lbuf, int64_t n, double* Ainv, cudaStream_t s) {
+  if (n == 0) return;
+  cublas_check(cublasSetStream(h, s), "setStream");
+  constexpr int64_t NB = 1024;
+  const double one = 1.0;
+  // Y = L^{-1} into Ainv (zero above the diagonal blocks)
+  HC_CUDA(cudaMemsetAsync(Ainv, 0, sizeof(double) * (size_t)(n * n), s));
+  for (int64_t j0 = 0; j0 < n; j0 += NB) {
+    const int64_t nb = std::min(NB, n - j0), m = n - j0;
+    k_eye_panel<<<grid_for(m * nb, 256), 256, 0, s>>>(Ainv, n, j0, nb);
+    HC_CHECK_LAUNCH();
+    cublas_check(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m,
+                             (int)nb, &one, Lbuf + j0 + j0 * n, (int)n, Ainv + j0 + j0 * n, (int)n),
+                 "dtrsm L^-1 panel");
+  }
+  // lower(Y^T Y) block column J: Y[J:, J:]^T Y[J:, J]  -> Lbuf[J:, J]
+  for (int64_t j0 = 0; j0 < n; j0 += NB) {
+    const int64_t nb = std::min(NB, n - j0), m = n - j0;
+    cublas_check(cublasDtrmm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)m,
+                             (int)nb, &one, Ainv + j0 + j0 * n, (int)n, Ainv + j0 + j0 * n, (int)n,
+                             Lbuf + j0 + j0 * n, (int)n),
+                 "dtrmm Y^T Y");
+  }
+  k_sym_from_lower<<<grid_for(n * n, 256, kSMs * 32), 256, 0, s>>>(Lbuf, n, Ainv);
+  HC_CHECK_LAUNCH();
+}
+
 void dense_cholesky_solve(cublasHandle_t h, const double* L, int64_t k, int64_t ld, double* B, int64_t nrhs,
                           int64_t ldb, cudaStream_t s) {
   if (k == 0 || nrhs == 0) return;

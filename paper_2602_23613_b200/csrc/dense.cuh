@@ -42,6 +42,9 @@ int64_t dense_cholesky_raw(cublasHandle_t h, double* A, int64_t k, int64_t ld, d
 int64_t pivot_verdict(const std::vector<double>& hp, int64_t k, int64_t j0, double scale);
 
 // B := A^{-1} B using the factor produced by dense_cholesky.
+// A^{-1} (exactly symmetric, n x n into Ainv) from the lower Cholesky factor in Lbuf (ld n;
+// overwritten).
+void dense_spd_inverse(cublasHandle_t h, double* Lbuf, int64_t n, double* Ainv, cudaStream_t s);
 void dense_cholesky_solve(cublasHandle_t h, const double* L, int64_t k, int64_t ld, double* B, int64_t nrhs,
                           int64_t ldb, cudaStream_t s);
 

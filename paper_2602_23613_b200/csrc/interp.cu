@@ -274,6 +274,7 @@ int64_t connected_components(const DCsr& M, DBuf<int32_t>& label, cudaStream_t s
 void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode, cublasHandle_t h,
                   InterpResult& out, cudaStream_t s) {
   const int64_t n = A.nrows, npair = sp.n_pairs(), ni = (int64_t)sp.interior.size();
+  StageTimer st(s);
   DBuf<int64_t> pairs(7 * std::max<int64_t>(npair, 1), s), interior(std::max<int64_t>(ni, 1), s);
   if (npair) pairs.upload(sp.pairs.data(), 7 * npair);
   if (ni) interior.upload(sp.interior.data(), ni);
@@ -293,6 +294,7 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
   if (ni) k_int_maps<<<grid_for(ni, 256), 256, 0, s>>>(interior.p, ni, int_pos.p, rows32.p);
   HC_CHECK_LAUNCH();
 
+  st.mark("  interp: R, maps");
   // component data (empty when there is nothing to extend)
   DBuf<int32_t> label, pos, kcols;
   DBuf<int64_t> cptr, kptr, a_off_d, b_off_d;
@@ -429,6 +431,7 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
       HC_CHECK_LAUNCH();
       DCsr Agg;
       csr_extract(Aii, mpos.p, nG, gmap.p, nG, Agg, s);
+      st.mark("  interp: components, small solves");
       hp.Z.alloc(nG * npair, s);
       hp.Z.zero();
       k_giant_rhs<<<grid_for(nG, 128), 128, 0, s>>>(mpos.p, nG, W.ptr.p, W.idx.p, W.val.p, npair, hp.Z.p);
@@ -444,6 +447,7 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
       throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(fail_piv) + ")", fail_piv);
     Ad.release();
   }
+  st.mark("  interp: components + solves");
   // assemble P = R^T + correction (transfer.py:111-116)
   DCsr& P = out.P;
   P.nrows = n;
@@ -466,6 +470,7 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
   HC_CHECK_LAUNCH();
   csr_transpose(P, out.Pt, s);
 
+  st.mark("  interp: P assembly + P^T");
   // coarse gradient (transfer.py:55-74) + sign normalisation (multilevel.py:71-75)
   DCsr RG0, RG;
   spgemm(R, G, RG0, s);
