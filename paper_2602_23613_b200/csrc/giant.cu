@@ -73,15 +73,64 @@ __global__ void k_pack_env(const int64_t* __restrict__ ap, const int32_t* __rest
   }
 }
 
-// out[i, :] = in[src[i], :] (kScatter: out[src[i], :] = in[i, :]) for row-major n x m
+// out[i, k] = in[src[i], col[k]]  (kScatter: out[src[i], col[k]] = in[i, k]) for row-major n x m
 template <bool kScatter>
-__global__ void k_permute_rows(int64_t n, int64_t m, const int32_t* __restrict__ src, const double* __restrict__ in,
-                               double* __restrict__ out) {
+__global__ void k_permute_rc(int64_t n, int64_t m, const int32_t* __restrict__ src, const int32_t* __restrict__ col,
+                             const double* __restrict__ in, double* __restrict__ out) {
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
     const double* a = kScatter ? in + i * m : in + (int64_t)src[i] * m;
     double* b = kScatter ? out + (int64_t)src[i] * m : out + i * m;
-    for (int64_t c = threadIdx.x; c < m; c += blockDim.x) b[c] = a[c];
+    if (kScatter)
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) b[col[k]] = a[k];
+    else
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) b[k] = a[col[k]];
   }
+}
+
+// Same, one row per CTA staged in shared memory (m * 8 bytes <= 227 KB):
+// coalesced global traffic, the column permutation done in shared memory.
+template <bool kScatter>
+__global__ void __launch_bounds__(1024) k_permute_rc_smem(int64_t n, int64_t m, const int32_t* __restrict__ src,
+                                                           const int32_t* __restrict__ col,
+                                                           const double* __restrict__ in, double* __restrict__ out) {
+  extern __shared__ double row[];
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const double* a = kScatter ? in + i * m : in + (int64_t)src[i] * m;
+    double* b = kScatter ? out + (int64_t)src[i] * m : out + i * m;
+    if (kScatter) {
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) row[col[k]] = a[k];
+    } else {
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) row[k] = a[k];
+    }
+    __syncthreads();
+    if (kScatter) {
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) b[k] = row[k];
+    } else {
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) b[k] = row[col[k]];
+    }
+    __syncthreads();
+  }
+}
+
+template <bool kScatter>
+void permute_rc(int64_t n, int64_t m, const int32_t* src, const int32_t* col, const double* in, double* out,
+                cudaStream_t s) {
+  const size_t smem = sizeof(double) * (size_t)m;
+  if (smem <= 227 * 1024) {
+    HC_CUDA(cudaFuncSetAttribute(k_permute_rc_smem<kScatter>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_permute_rc_smem<kScatter><<<(unsigned)std::min<int64_t>(n, kSMs * 2), 1024, smem, s>>>(n, m, src, col, in, out);
+  } else {
+    k_permute_rc<kScatter><<<(unsigned)std::min<int64_t>(n, kSMs * 16), 256, 0, s>>>(n, m, src, col, in, out);
+  }
+  HC_CHECK_LAUNCH();
+}
+
+// first[c] = min over rows r with B[r, c] != 0 of rank[r]  (first = n when the column is empty)
+__global__ void k_first_row(int64_t n, int64_t m, const double* __restrict__ B, const int32_t* __restrict__ rank,
+                            int* __restrict__ first) {
+  for (int64_t r = blockIdx.x; r < n; r += gridDim.x)
+    for (int64_t c = threadIdx.x; c < m; c += blockDim.x)
+      if (B[r * m + c] != 0.0) atomicMin(first + c, rank[r]);
 }
 
 __global__ void k_csr_diag_absmax(const int64_t* __restrict__ ap, const int32_t* __restrict__ ai,
@@ -657,20 +706,45 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
     if (fail >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(fail) + ")", fail);
   }
   st.mark("  giant: envelope Cholesky");
-  // rows of B into the factored order
+  // Rows of B into the factored order; columns sorted by the first (factored)
+  // row of their right-hand side, so that in the forward sweep block J only
+  // involves the prefix of columns whose right-hand side starts at or above
+  // block J -- the rest of the block is still zero (RCM keeps every coarse
+  // DoF's coupling rows together, so this skips about half the forward work).
+  std::vector<int32_t> colperm((size_t)m);
+  std::vector<int64_t> active((size_t)T, m);
+  {
+    DBuf<int> first(m, s);
+    HC_CUDA(cudaMemsetAsync(first.p, 0x7f, sizeof(int) * (size_t)m, s));
+    k_first_row<<<(unsigned)std::min<int64_t>(n, kSMs * 16), 256, 0, s>>>(n, m, B, dinv.p, first.p);
+    HC_CHECK_LAUNCH();
+    st.mark("  giant: column order");
+    std::vector<int> hf = first.download();
+    for (int64_t c = 0; c < m; ++c) colperm[(size_t)c] = (int32_t)c;
+    std::stable_sort(colperm.begin(), colperm.end(), [&](int32_t a, int32_t b) { return hf[(size_t)a] < hf[(size_t)b]; });
+    int64_t k = 0;
+    for (int64_t J = 0; J < T; ++J) {
+      while (k < m && hf[(size_t)colperm[(size_t)k]] < (J + 1) * kNB) ++k;
+      active[(size_t)J] = k;
+    }
+  }
+  DBuf<int32_t> dcol;
+  dcol.upload(colperm.data(), m);
   DBuf<double> Bp(n * m, s);
-  k_permute_rows<false><<<(unsigned)std::min<int64_t>(n, kSMs * 16), 256, 0, s>>>(n, m, dperm.p, B, Bp.p);
-  HC_CHECK_LAUNCH();
+  permute_rc<false>(n, m, dperm.p, dcol.p, B, Bp.p, s);
+  st.mark("  giant: permute in");
   // Solve (A Z = B with B row-major n x m)  <=>  Z^T L L^T = B^T on the column-major m x n view.
   auto nbk = [&](int64_t K) { return std::min(kNB, n - K * kNB); };
   auto blk = [&](int64_t K) { return Bp.p + K * kNB * m; };
-  for (int64_t J = 0; J < T; ++J) {  // U^T = B^T L^{-T}
-    cb(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)m, (int)nbk(J),
+  for (int64_t J = 0; J < T; ++J) {  // U^T = B^T L^{-T}; columns >= active[J] of blocks <= J are zero
+    const int ma = (int)active[(size_t)J];
+    if (ma == 0) continue;
+    cb(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, ma, (int)nbk(J),
                    &one, L.tile(J, J), (int)kNB, blk(J), (int)m),
        "dtrsm fwd");
     for (int64_t I = J + 1; I < T; ++I)
       if (L.has(I, J))
-        cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)m, (int)nbk(I), (int)nbk(J), &mone, blk(J), (int)m,
+        cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, ma, (int)nbk(I), (int)nbk(J), &mone, blk(J), (int)m,
                        L.tile(I, J), (int)kNB, &one, blk(I), (int)m),
            "dgemm fwd");
   }
@@ -685,9 +759,9 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
   }
   st.mark("  giant: triangular solves");
   L.buf.release();
-  k_permute_rows<true><<<(unsigned)std::min<int64_t>(n, kSMs * 16), 256, 0, s>>>(n, m, dperm.p, Bp.p, B);
-  HC_CHECK_LAUNCH();
+  permute_rc<true>(n, m, dperm.p, dcol.p, Bp.p, B, s);
   HC_CUDA(cudaStreamSynchronize(s));
+  st.mark("  giant: permute out");
 }
 
 template <int kMode>
