@@ -52,7 +52,8 @@ def measured_peaks():
 def algorithmic_bytes(h):
     """B_iter of SURVEY.md §8(d): bytes one PCG iteration must move, whatever
     the implementation.  B(M) = 12 nnz + 4 (rows + 1); B(P) = min(CSR, hybrid
-    dense-block); S_l = sum_p [8 k_p (k_p+1)/2 + 12 nnz(A[:, patch_p])]; 3 A
+    dense-block, factored: the envelope-factor operators of one A_GG^{-1}
+    application + the sparse part); S_l = sum_p [8 k_p (k_p+1)/2 + 12 nnz(A[:, patch_p])]; 3 A
     applications per smoothed level; 2 * 8 * n_c (n_c+1)/2 for the coarsest."""
     def B(nnz, rows):
         return 12 * nnz + 4 * (rows + 1)
@@ -75,7 +76,10 @@ def algorithmic_bytes(h):
         n_int = int(info.n_interior)
         csr_p = B(int(info.nnz_P), n)
         hybrid = 8 * n_int * nc + B(2 * int(info.n_pairs), n)
-        total += 3 * B(int(info.nnz_A), n) + 2 * min(csr_p, hybrid) + 2 * S + 96 * n
+        reps = [csr_p, hybrid]
+        if int(info.factor_bytes) > 0:  # P through the envelope factor of A_GG (csrc/trisolve.cu)
+            reps.append(int(info.factor_bytes) + B(int(info.pad), n))
+        total += 3 * B(int(info.nnz_A), n) + 2 * min(reps) + 2 * S + 96 * n
     return int(total)
 
 
@@ -164,7 +168,9 @@ def kernel_roofline(h, reps=None, rank=0, nranks=1):
 
     if pc in (1, 3):
         nc = int(h.levels[ell + 1]._info.n)
-        if int(info.max_component) > 0:
+        if int(info.factor_bytes) > 0 and nranks == 1:
+            nbytes = int(info.factor_bytes) + B(int(info.pad), n) + 8 * (n + nc)
+        elif int(info.max_component) > 0:
             nG = int(info.max_component)
             q0, q1 = (0, nG)
             if nranks > 1:

@@ -69,6 +69,10 @@ typedef struct {
 typedef struct {
   int64_t n, nnz_A, ncols_G, nnz_G, nnz_P, n_pairs, n_interior, n_coarse_nodes;
   int64_t n_patches, n_patch_entries, n_waves, n_gc_cols, coarsest, n_components, max_component, pad;
+  /* dense regime, single GPU: the V-cycle applies A_GG^{-1} through the
+   * envelope Cholesky factor (two blocked sweeps of factor_steps steps);
+   * factor_bytes = operator bytes one application reads (0: explicit Z). */
+  int64_t factor_bytes, factor_steps;
 } hcamg_level_info;
 
 /* ---- lifetime ---------------------------------------------------------- */
@@ -127,6 +131,10 @@ int hcamg_export_l1(hcamg_handle* h, int32_t level, double* d);
  * level's dense inverse (n x n).  hcamg_export_csr which = 3 gives the sparse
  * part of a hybrid P; hcamg_level_info.max_component = n_G, .pad = its nnz. */
 int hcamg_export_dense(hcamg_handle* h, int32_t level, int32_t which, void* out);
+/* out = A_GG^{-1} v through the factored block (two blocked triangular sweeps,
+ * csrc/trisolve.cu); v, out of length n_G in the member order of
+ * hcamg_export_dense(which = 1).  Test/inspection entry (transfer.py:104). */
+int hcamg_component_solve(hcamg_handle* h, int32_t level, const double* v, double* out);
 /* patches in reference order: ptr (n_patches + 1), dofs (n_patch_entries), wave of each patch */
 int hcamg_export_patches(hcamg_handle* h, int32_t level, int64_t* ptr, int64_t* dofs, int64_t* wave);
 int hcamg_export_coarse_cols(hcamg_handle* h, int32_t level, int64_t* cols);

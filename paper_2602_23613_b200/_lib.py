@@ -25,7 +25,7 @@ EXPORTS = [
     "hcamg_hier_end_with", "hcamg_info_get", "hcamg_notes", "hcamg_level", "hcamg_export_csr",
     "hcamg_export_splitting", "hcamg_export_l1", "hcamg_export_patches", "hcamg_export_coarse_cols",
     "hcamg_vcycle", "hcamg_pcg", "hcamg_amg_solve", "hcamg_pcg_device", "hcamg_graph_launches",
-    "hcamg_stream", "hcamg_pcg_generic", "hcamg_spmv", "hcamg_profile_vcycle", "hcamg_export_dense", "hcamg_split_alg", "hcamg_split_export",
+    "hcamg_stream", "hcamg_pcg_generic", "hcamg_spmv", "hcamg_profile_vcycle", "hcamg_export_dense", "hcamg_component_solve", "hcamg_split_alg", "hcamg_split_export",
     "hcamg_dist_prepare", "hcamg_dist_connect", "hcamg_dist_connect_ptrs", "hcamg_dist_disconnect", "hcamg_dist_info",
 ]
 
@@ -53,7 +53,7 @@ class LevelInfo(C.Structure):
     _fields_ = [(name, C.c_int64) for name in (
         "n", "nnz_A", "ncols_G", "nnz_G", "nnz_P", "n_pairs", "n_interior", "n_coarse_nodes",
         "n_patches", "n_patch_entries", "n_waves", "n_gc_cols", "coarsest", "n_components",
-        "max_component", "pad")]
+        "max_component", "pad", "factor_bytes", "factor_steps")]
 
 
 PRECOND_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64, C.c_void_p)
@@ -105,6 +105,7 @@ def load(required=True):
         "hcamg_spmv": (C.c_int, [P, C.POINTER(CSR), P, P]),
         "hcamg_profile_vcycle": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P, P, P]),
         "hcamg_export_dense": (C.c_int, [P, C.c_int32, C.c_int32, P]),
+        "hcamg_component_solve": (C.c_int, [P, C.c_int32, P, P]),
         "hcamg_split_alg": (C.c_int, [P, C.POINTER(CSR), C.POINTER(CSR), C.c_double, P]),
         "hcamg_split_export": (C.c_int, [P, P, P, P]),
         "hcamg_dist_prepare": (C.c_int, [P, C.c_int32, C.c_int32, P, C.POINTER(C.c_void_p)]),
@@ -114,6 +115,7 @@ def load(required=True):
         "hcamg_dist_info": (C.c_int, [P, P, P, P, P]),
         # debug entry points (not in the public header)
         "hcamg_debug_dist_piece": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, P, P]),
+        "hcamg_debug_apply_p": (C.c_int, [P, C.c_int32, C.c_int32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -641,6 +641,8 @@ int hcamg_level(hcamg_handle* h, int32_t level, hcamg_level_info* o) {
     o->nnz_P = L.has_P ? (L.hp.on ? hybrid_nnz(L.P, L.hp, h->stream) : L.P.nnz) : 0;
     o->n_components = L.hp.on ? 1 : 0;
     o->max_component = L.hp.on ? L.hp.nG : 0;
+    o->factor_bytes = L.hp.on && L.hp.fac.on ? L.hp.fac.sweep_bytes[0] + L.hp.fac.sweep_bytes[1] : 0;
+    o->factor_steps = L.hp.on && L.hp.fac.on ? L.hp.fac.T : 0;
     o->pad = L.hp.on ? L.P.nnz : 0;  // nnz of the sparse part of a hybrid P
     o->n_pairs = L.split.n_pairs();
     o->n_interior = (int64_t)L.split.interior.size();
@@ -708,6 +710,26 @@ int hcamg_export_dense(hcamg_handle* h, int32_t level, int32_t which, void* out)
       require(false, "unknown dense export");
     }
     HC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int hcamg_component_solve(hcamg_handle* h, int32_t level, const double* v, double* out) {
+  return guarded(h, [&] {
+    require(level >= 0 && level < (int32_t)h->levels.size(), "level out of range");
+    DevLevel& L = *h->levels[(size_t)level];
+    require(L.hp.on && L.hp.fac.on, "level has no factored interpolation block");
+    FactorP& f = L.hp.fac;
+    cudaStream_t s = h->stream;
+    std::vector<int32_t> perm = f.perm.download();
+    std::vector<double> hv((size_t)(f.T * kTriNB), 0.0);
+    for (int64_t i = 0; i < f.nG; ++i) hv[(size_t)i] = v[perm[(size_t)i]];
+    HC_CUDA(cudaMemcpyAsync(f.v0.p, hv.data(), 8 * hv.size(), cudaMemcpyHostToDevice, s));
+    DBuf<int> stop(1, s);
+    stop.zero();
+    factorp_solve(stop.p, f, f.v0.p, f.v2.p, s);
+    HC_CUDA(cudaMemcpyAsync(hv.data(), f.v2.p, 8 * hv.size(), cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < f.nG; ++i) out[perm[(size_t)i]] = hv[(size_t)i];
   });
 }
 
@@ -1117,6 +1139,32 @@ int hcamg_debug_dist_piece(hcamg_handle* h, int32_t level, int32_t piece, int32_
     if (x) HC_CUDA(cudaMemcpyAsync(x, h->ws.z.p, 8 * n, cudaMemcpyDeviceToHost, s));
     HC_CUDA(cudaStreamSynchronize(s));
     check_dist(h);
+  });
+}
+
+// Debug (not in the public header): the interpolation of level `level` as the
+// V-cycle applies it (record_piece): kind 0: out = P in (in: n_c, out: n);
+// kind 1: out = P^T in (in: n, out: n_c).  Host buffers.
+int hcamg_debug_apply_p(hcamg_handle* h, int32_t level, int32_t kind, const double* in, double* out) {
+  return guarded(h, [&] {
+    require_hierarchy(h);
+    require(level >= 0 && level + 1 < (int32_t)h->lv.size(), "level has no interpolation");
+    cudaStream_t s = h->stream;
+    ensure_ws(h, 1);
+    DevLevel& L = *h->lv[(size_t)level];
+    DevLevel* C = h->lv[(size_t)level + 1];
+    if (kind == 0) {
+      DBuf<double> x(L.n, s);
+      x.zero();
+      HC_CUDA(cudaMemcpyAsync(C->x.p, in, 8 * C->n, cudaMemcpyHostToDevice, s));
+      record_piece(PC_PROLONG, L, C, nullptr, x.p, h->ws.zero_flag.p, s, 0);
+      HC_CUDA(cudaMemcpyAsync(out, x.p, 8 * L.n, cudaMemcpyDeviceToHost, s));
+    } else {
+      HC_CUDA(cudaMemcpyAsync(L.r.p, in, 8 * L.n, cudaMemcpyHostToDevice, s));
+      record_piece(PC_RESTRICT, L, C, nullptr, nullptr, h->ws.zero_flag.p, s, 0);
+      HC_CUDA(cudaMemcpyAsync(out, C->b.p, 8 * C->n, cudaMemcpyDeviceToHost, s));
+    }
+    HC_CUDA(cudaStreamSynchronize(s));
   });
 }
 

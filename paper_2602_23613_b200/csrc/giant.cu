@@ -538,6 +538,183 @@ __global__ void k_fill_m1(int32_t* v, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] = -1;
 }
 
+// dst[z] = src[z]^T for NB x NB column-major tiles (32 x 32 blocks through shared memory)
+__global__ void __launch_bounds__(256) k_tiles_transpose(const double* const* __restrict__ src,
+                                                         double* const* __restrict__ dst) {
+  __shared__ double sm[32][33];
+  const double* S = src[blockIdx.z];
+  double* D = dst[blockIdx.z];
+  const int64_t bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) sm[j][threadIdx.x] = S[(bx + threadIdx.x) + (by + j) * kNB];
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += 8) D[(by + threadIdx.x) + (bx + j) * kNB] = sm[threadIdx.x][j];
+}
+
+__global__ void k_tiles_eye(double* const* __restrict__ dst) {
+  double* D = dst[blockIdx.y];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < kNB * kNB; t += (int64_t)gridDim.x * blockDim.x)
+    D[t] = t % (kNB + 1) == 0 ? 1.0 : 0.0;
+}
+
+void tiles_transpose(std::vector<const double*>& src, std::vector<double*>& dst, cudaStream_t s) {
+  for (size_t z0 = 0; z0 < src.size(); z0 += 32768) {
+    const size_t nz = std::min<size_t>(32768, src.size() - z0);
+    DBuf<const double*> ds;
+    DBuf<double*> dd;
+    ds.upload(src.data() + z0, (int64_t)nz, s);
+    dd.upload(dst.data() + z0, (int64_t)nz, s);
+    k_tiles_transpose<<<dim3(kNB / 32, kNB / 32, (unsigned)nz), dim3(32, 8), 0, s>>>(ds.p, dd.p);
+    HC_CHECK_LAUNCH();
+    HC_CUDA(cudaStreamSynchronize(s));
+  }
+}
+
+// Operators of the blocked sweeps (trisolve.cuh) from the envelope factor:
+// Linv_kk = L_kk^{-1} (TRSM on identity tiles), M_k = Linv_kk L_{k,k-1},
+// N_k = Linv_kk^T L_{k+1,k}^T, and the forward fold tiles L_{i,k-1} copied
+// row-major.  The backward fold tiles are L's own column-major tiles.
+void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_t s) {
+  const int64_t T = L.T, NN = kNB * kNB;
+  std::vector<int64_t> mslot((size_t)T, -1), nslot((size_t)T, -1);
+  int64_t nM = 0, nN = 0;
+  for (int64_t k = 1; k < T; ++k)
+    if (L.has(k, k - 1)) mslot[(size_t)k] = nM++;
+  for (int64_t k = 0; k + 1 < T; ++k)
+    if (L.has(k + 1, k)) nslot[(size_t)k] = nN++;
+  std::vector<std::vector<int64_t>> ffold((size_t)T);  // forward step k: blocks i >= k+1 reached by column k-1
+  int64_t nF = 0;
+  for (int64_t k = 1; k < T; ++k)
+    for (int64_t i = k + 1; i < T; ++i)
+      if (L.has(i, k - 1)) {
+        ffold[(size_t)k].push_back(i);
+        ++nF;
+      }
+  f.fpool.alloc((T + nM + nF) * NN, s);
+  f.bpool.alloc((T + nN) * NN, s);
+  auto fp = [&](int64_t slot) { return f.fpool.p + slot * NN; };
+  auto bp = [&](int64_t slot) { return f.bpool.p + slot * NN; };
+  cb(cublasSetStream(h, s), "setStream");
+  const double one = 1.0, zero = 0.0;
+  {  // Linv_kk, column-major, in bpool[k]
+    std::vector<double*> eye;
+    std::vector<const double*> lkk;
+    for (int64_t k = 0; k < T; ++k) {
+      eye.push_back(bp(k));
+      lkk.push_back(L.tile(k, k));
+    }
+    DBuf<double*> de;
+    de.upload(eye.data(), T, s);
+    k_tiles_eye<<<dim3(256, (unsigned)T), 256, 0, s>>>(de.p);
+    HC_CHECK_LAUNCH();
+    DBuf<const double*> dl;
+    dl.upload(lkk.data(), T, s);
+    cb(cublasDtrsmBatched(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)kNB,
+                          (int)kNB, &one, dl.p, (int)kNB, de.p, (int)kNB, (int)T),
+       "dtrsmBatched Linv");
+    HC_CUDA(cudaStreamSynchronize(s));
+    // forward Linv row-major = transpose
+    std::vector<const double*> src;
+    std::vector<double*> dst;
+    for (int64_t k = 0; k < T; ++k) {
+      src.push_back(bp(k));
+      dst.push_back(fp(k));
+    }
+    tiles_transpose(src, dst, s);
+  }
+  if (nM) {  // row-major M_k = column-major (L_{k,k-1}^T Linv_kk^T)
+    std::vector<const double*> ha, hb;
+    std::vector<double*> hc;
+    for (int64_t k = 1; k < T; ++k)
+      if (mslot[(size_t)k] >= 0) {
+        ha.push_back(L.tile(k, k - 1));
+        hb.push_back(bp(k));
+        hc.push_back(fp(T + mslot[(size_t)k]));
+      }
+    DBuf<const double*> da, db;
+    DBuf<double*> dc;
+    da.upload(ha.data(), nM, s);
+    db.upload(hb.data(), nM, s);
+    dc.upload(hc.data(), nM, s);
+    cb(cublasDgemmBatched(h, CUBLAS_OP_T, CUBLAS_OP_T, (int)kNB, (int)kNB, (int)kNB, &one, da.p, (int)kNB, db.p,
+                          (int)kNB, &zero, dc.p, (int)kNB, (int)nM),
+       "dgemmBatched M");
+    HC_CUDA(cudaStreamSynchronize(s));
+  }
+  if (nN) {  // row-major N_k = column-major (L_{k+1,k} Linv_kk)
+    std::vector<const double*> ha, hb;
+    std::vector<double*> hc;
+    for (int64_t k = 0; k + 1 < T; ++k)
+      if (nslot[(size_t)k] >= 0) {
+        ha.push_back(L.tile(k + 1, k));
+        hb.push_back(bp(k));
+        hc.push_back(bp(T + nslot[(size_t)k]));
+      }
+    DBuf<const double*> da, db;
+    DBuf<double*> dc;
+    da.upload(ha.data(), nN, s);
+    db.upload(hb.data(), nN, s);
+    dc.upload(hc.data(), nN, s);
+    cb(cublasDgemmBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)kNB, (int)kNB, (int)kNB, &one, da.p, (int)kNB, db.p,
+                          (int)kNB, &zero, dc.p, (int)kNB, (int)nN),
+       "dgemmBatched N");
+    HC_CUDA(cudaStreamSynchronize(s));
+  }
+  std::vector<TriStep> fs, bs;
+  std::vector<TriTile> ft, bt;
+  {  // forward fold tiles (row-major copies) and steps
+    std::vector<const double*> src;
+    std::vector<double*> dst;
+    int64_t slot = T + nM;
+    for (int64_t k = 0; k < T; ++k) {
+      TriStep S{};
+      S.k = (int32_t)k;
+      S.c = k >= 1 ? (int32_t)(k - 1) : -1;
+      S.tri = 0;
+      S.a = fp(k);
+      S.b = mslot[(size_t)k] >= 0 ? fp(T + mslot[(size_t)k]) : nullptr;
+      S.t0 = (int64_t)ft.size();
+      for (int64_t i : ffold[(size_t)k]) {
+        src.push_back(L.tile(i, k - 1));
+        dst.push_back(fp(slot));
+        ft.push_back(TriTile{fp(slot), i});
+        ++slot;
+      }
+      S.t1 = (int64_t)ft.size();
+      f.fw.max_tiles = std::max(f.fw.max_tiles, S.t1 - S.t0);
+      fs.push_back(S);
+    }
+    if (!src.empty()) tiles_transpose(src, dst, s);
+  }
+  for (int64_t k = T - 1; k >= 0; --k) {  // backward steps: fold tiles are L's tiles (k+1, j), j < k
+    TriStep S{};
+    S.k = (int32_t)k;
+    S.c = k + 1 < T ? (int32_t)(k + 1) : -1;
+    S.tri = 1;
+    S.a = bp(k);
+    S.b = nslot[(size_t)k] >= 0 ? bp(T + nslot[(size_t)k]) : nullptr;
+    S.t0 = (int64_t)bt.size();
+    if (k + 1 < T)
+      for (int64_t j = L.j0[(size_t)k + 1]; j < k; ++j) bt.push_back(TriTile{L.tile(k + 1, j), j});
+    S.t1 = (int64_t)bt.size();
+    f.bw.max_tiles = std::max(f.bw.max_tiles, S.t1 - S.t0);
+    bs.push_back(S);
+  }
+  // operator bytes per sweep: triangular rows are read in 64-column chunks
+  const int64_t tri_bytes = 512 * 64 * (kNB / 64) * (kNB / 64 + 1) / 2;
+  for (int d = 0; d < 2; ++d) {
+    const std::vector<TriStep>& v = d == 0 ? fs : bs;
+    int64_t b = 0;
+    for (const TriStep& S : v) b += tri_bytes + (S.b ? 8 * NN : 0) + 8 * NN * (S.t1 - S.t0);
+    f.sweep_bytes[d] = b;
+  }
+  f.fw.nstep = f.bw.nstep = T;
+  f.fw.steps.upload(fs.data(), T, s);
+  f.bw.steps.upload(bs.data(), T, s);
+  f.fw.tiles.upload(ft.data(), (int64_t)ft.size(), s);
+  f.bw.tiles.upload(bt.data(), (int64_t)bt.size(), s);
+  HC_CUDA(cudaStreamSynchronize(s));
+}
+
 }  // namespace
 
 // Reverse Cuthill-McKee order of a symmetric pattern: scipy's algorithm
@@ -598,7 +775,7 @@ static std::vector<int32_t> rcm_order(int64_t n, const std::vector<int64_t>& ptr
   return order;
 }
 
-void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m, cudaStream_t s) {
+void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m, cudaStream_t s, FactorP* fac) {
   const int64_t n = Agg.nrows;
   StageTimer st(s);
   // ordering: reverse Cuthill-McKee (default) or the natural component order
@@ -706,6 +883,12 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
     if (fail >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(fail) + ")", fail);
   }
   st.mark("  giant: envelope Cholesky");
+  if (fac) {
+    build_factor_ops(h, L, *fac, s);
+    fac->nG = n;
+    fac->T = T;
+    st.mark("  giant: sweep operators");
+  }
   // Rows of B into the factored order; columns sorted by the first (factored)
   // row of their right-hand side, so that in the forward sweep block J only
   // involves the prefix of columns whose right-hand side starts at or above
@@ -758,9 +941,11 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
          "dgemm bwd");
   }
   st.mark("  giant: triangular solves");
-  L.buf.release();
+  if (fac) fac->Lc = std::move(L.buf);
+  else L.buf.release();
   permute_rc<true>(n, m, dperm.p, dcol.p, Bp.p, B, s);
   HC_CUDA(cudaStreamSynchronize(s));
+  if (fac) fac->perm = std::move(dperm);
   st.mark("  giant: permute out");
 }
 

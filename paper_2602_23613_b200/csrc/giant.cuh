@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "dist.cuh"
+#include "trisolve.cuh"
 
 namespace hcamg {
 
@@ -16,8 +17,11 @@ constexpr int64_t kGiantMin = 4096;   // = the reference's _DENSE_COMPONENT_CUTO
 // Factor the SPD matrix given as CSR (positions 0..n-1) into packed tiles and
 // solve A Z = B for the row-major n x m right-hand side B (overwritten by Z).
 // Throws Error(ENOTSPD_) with the reference's pivot semantics (scale =
-// max |diag|, floor 1e-13 * scale).
-void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B_rowmajor, int64_t m, cudaStream_t s);
+// max |diag|, floor 1e-13 * scale).  With `fac`, the factor is kept and the
+// blocked-sweep operators of trisolve.cuh are built from it (perm, Lc, pools,
+// sweeps; the caller finishes with factorp_attach).
+void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B_rowmajor, int64_t m, cudaStream_t s,
+                        FactorP* fac = nullptr);
 
 // Hybrid interpolation data of one level.
 struct HybridP {
@@ -29,6 +33,7 @@ struct HybridP {
   int64_t chunk = 512, nchunk = 0;
   int64_t grp[kGroups + 1] = {};  // chunk boundaries of the kGroups reduction groups
   DBuf<double> partial;
+  FactorP fac;          // A_GG^{-1} through its envelope factor (single-GPU solve)
 };
 
 // allocate the restriction partials (outside any graph capture)

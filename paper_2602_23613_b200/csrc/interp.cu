@@ -437,7 +437,8 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
       k_giant_rhs<<<grid_for(nG, 128), 128, 0, s>>>(mpos.p, nG, W.ptr.p, W.idx.p, W.val.p, npair, hp.Z.p);
       HC_CHECK_LAUNCH();
       try {
-        giant_factor_solve(h, Agg, hp.Z.p, npair, s);
+        giant_factor_solve(h, Agg, hp.Z.p, npair, s, factorp_enabled() ? &hp.fac : nullptr);
+        if (hp.fac.T) factorp_attach(hp.fac, W, mpos.p, hp.rows.p, s);
       } catch (const Error& e) {
         if (e.code == ENOTSPD_ && giant < fail_comp) { fail_comp = giant; fail_piv = e.index; }
         else throw;

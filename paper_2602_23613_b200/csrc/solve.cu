@@ -633,6 +633,10 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
         rs.y = C->b.p;
         spmv<EPI_SET>(L.Pt, rs, s);
       }
+      if (!xd && L.hp.fac.on) {  // bc -= W'^T A_GG^{-1} r_G through the factor
+        factorp_restrict(stop, L.hp.fac, L.r.p, C->b.p, s);
+        return 5;
+      }
       require(!xd || L.xoff_g != DevLevel::kNoSite, "distributed layout is stale (call hcamg_dist_prepare again)");
       hybrid_restrict(stop, L.hp, L.r.p, C->b.p, s, L.dist, L.xoff_g, part);
       if (!xd) return 3;
@@ -656,6 +660,10 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
       pr.xin = C->x.p;
       pr.y = x;
       spmv<EPI_ADD>(L.P, pr, s);
+    }
+    if (L.hp.on && !xd && L.hp.fac.on) {  // x[G] -= A_GG^{-1} W' x_c through the factor
+      factorp_prolong(stop, L.hp.fac, C->x.p, x, s);
+      return 5;
     }
     if (L.hp.on) {  // x[G] -= Z x_c
       require(!xd || L.xoff_y != DevLevel::kNoSite, "distributed layout is stale (call hcamg_dist_prepare again)");

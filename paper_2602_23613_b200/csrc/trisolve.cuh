@@ -1,0 +1,79 @@
+// Factored interpolation block: P = P_s - S_G A_GG^{-1} W' applied through
+// the envelope Cholesky factor of A_GG instead of the explicit dense block Z.
+//
+// The reference stores the harmonic extension explicitly (transfer.py:104-116:
+// Z = cho_solve(A_cc, W[comp, keep]), P = R^T - Z scattered into P).  In the
+// 3D dense regime Z is n_G x n_c dense (config 2: 35.2 GB) and every V-cycle
+// streams it twice (P e and P^T r).  The same linear map is
+//   P e   = P_s e   - S_G  A_GG^{-1} (W' e)
+//   P^T r = P_s^T r - W'^T A_GG^{-1} (S_G^T r)
+// and A_GG^{-1} v = perm^T L^{-T} L^{-1} perm v with L the RCM-envelope
+// Cholesky factor (config 2: 5.7 GB of tiles).  Two triangular sweeps per
+// application read ~2 x 5.7 GB instead of 35.2 GB.
+//
+// Each sweep is one cooperative kernel over the whole GPU, one step per
+// NB-row block, one grid barrier per step.  Forward step k computes
+//   y_k = Linv_kk u_k - M_k y_{k-1},  M_k = Linv_kk L_{k,k-1}
+// (u_k already holds the contributions of y_0..y_{k-2}) and, in the same
+// phase, folds y_{k-1} into the later blocks: u_i -= L_{i,k-1} y_{k-1}
+// (i >= k+1).  The backward sweep is the same with Linv_kk^T, N_k =
+// Linv_kk^T L_{k+1,k}^T and the transposed tiles.  Every output row is one
+// warp's dot product in a fixed order, so a sweep is deterministic.
+#pragma once
+#include "common.cuh"
+
+namespace hcamg {
+
+constexpr int64_t kTriNB = 1024;
+
+// One step of a blocked sweep: rows of block k are the "critical" rows
+// y_k = A u_k - B y_c (A row-major, lower (tri 0) or upper (tri 1)
+// triangular; B row-major or null); tiles [t0, t1) fold y_c into other blocks.
+struct TriStep {
+  int32_t k, c, tri, pad;
+  const double* a;
+  const double* b;
+  int64_t t0, t1;
+};
+struct TriTile {
+  const double* a;  // row-major NB x NB
+  int64_t blk;      // output block: u[blk*NB + r] -= a[r, :] . y_c
+};
+
+struct TriSweep {
+  int64_t nstep = 0, max_tiles = 0;
+  DBuf<TriStep> steps;
+  DBuf<TriTile> tiles;
+};
+
+struct FactorP {
+  bool on = false;
+  int64_t nG = 0, nc = 0, T = 0;
+  DBuf<int32_t> perm;   // factored position -> position in the component (RCM order)
+  DBuf<double> Lc;      // Cholesky tiles, column-major, block envelope (backward fold tiles)
+  DBuf<double> fpool;   // forward: Linv_kk, M_k and fold tiles, row-major
+  DBuf<double> bpool;   // backward: Linv_kk (column-major = Linv^T row-major), N_k
+  TriSweep fw, bw;
+  DBuf<int32_t> dof;    // factored position -> DoF of the level
+  DCsr Wp, Wpt;         // W' with rows in factored order, and its transpose (n_c x n_G)
+  DBuf<double> v0, v1, v2;  // T*NB work vectors
+  DBuf<unsigned> bar;       // grid-barrier word (sense-reversing)
+  int64_t sweep_bytes[2] = {0, 0};  // operator bytes the forward / backward sweep reads
+  int64_t pool_bytes() const { return 8 * (Lc.n + fpool.n + bpool.n); }
+};
+
+// Rows of W (in the component's member order given by mpos) and the level
+// DoFs of the members (rows), both taken into factored order.
+void factorp_attach(FactorP& f, const DCsr& W, const int32_t* mpos, const int32_t* rows, cudaStream_t s);
+
+// bc -= W'^T A_GG^{-1} r[G]          (restriction, dense part)
+void factorp_restrict(const int* stop, FactorP& f, const double* r, double* bc, cudaStream_t s);
+// x[G] -= A_GG^{-1} W' e             (prolongation, dense part)
+void factorp_prolong(const int* stop, FactorP& f, const double* e, double* x, cudaStream_t s);
+// y = A_GG^{-1} v in factored order (v, y of length T*NB; v is overwritten)
+void factorp_solve(const int* stop, FactorP& f, double* v, double* y, cudaStream_t s);
+
+// HCAMG_PAPPLY=z keeps the explicit-Z kernels (comparison); default: factor.
+bool factorp_enabled();
+
+}  // namespace hcamg

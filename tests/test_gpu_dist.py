@@ -38,6 +38,14 @@ def vcycle_pieces(depth):
     return seq
 
 
+@pytest.fixture(autouse=True)
+def explicit_z(monkeypatch):
+    # the row-partitioned solve streams the explicit block Z; compare it with the
+    # single-GPU V-cycle on the same representation (the single-GPU default
+    # applies A_GG^{-1} through the factor, tests/test_gpu_factor_sweep.py)
+    monkeypatch.setenv("HCAMG_PAPPLY", "z")
+
+
 @pytest.fixture(scope="module")
 def system16():
     return kuhn.config_system("c1", 16)

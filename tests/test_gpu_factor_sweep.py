@@ -1,0 +1,117 @@
+"""Factored interpolation block (csrc/trisolve.cu): in the dense regime the
+V-cycle applies P = P_s - S_G A_GG^{-1} W' through the envelope Cholesky
+factor (two blocked triangular sweeps) instead of streaming the explicit
+block Z = A_GG^{-1} W' (the reference's representation, transfer.py:104-116).
+Same linear map, different rounding: the V-cycles must agree to roundoff, the
+PCG iteration counts exactly, and repeated applications bit for bit."""
+
+import os
+
+import numpy as np
+import pytest
+
+import paper_2602_23613_b200 as P
+from paper_2602_23613_b200 import kuhn
+
+pytestmark = pytest.mark.gpu
+
+
+def _build(system, papply):
+    old = os.environ.get("HCAMG_PAPPLY")
+    os.environ["HCAMG_PAPPLY"] = papply
+    try:
+        return P.build_hierarchy(system, "alg")
+    finally:
+        if old is None:
+            del os.environ["HCAMG_PAPPLY"]
+        else:
+            os.environ["HCAMG_PAPPLY"] = old
+
+
+@pytest.fixture(scope="module", params=["c1", "c2"])
+def pair(request):
+    s = kuhn.config_system(request.param, n=16)
+    return request.param, s, _build(s, "factor"), _build(s, "z")
+
+
+def test_vcycle_factor_matches_z(pair):
+    field, s, hf, hz = pair
+    assert hf.levels[0].n == hz.levels[0].n and [lv.n for lv in hf.levels] == [lv.n for lv in hz.levels]
+    rng = np.random.default_rng(7)
+    for _ in range(3):
+        b = rng.uniform(-1, 1, s.n)
+        xf = P.vcycle(hf, b)
+        xz = P.vcycle(hz, b)
+        # c1: isotropic coefficients, kappa(A_GG) modest; c2: 1e6 contrast
+        tol = 1e-10 if field == "c1" else 1e-4
+        assert np.linalg.norm(xf - xz) <= tol * np.linalg.norm(xz)
+
+
+def test_vcycle_factor_deterministic(pair):
+    field, s, hf, hz = pair
+    b = np.random.default_rng(3).uniform(-1, 1, s.n)
+    x1 = P.vcycle(hf, b)
+    x2 = P.vcycle(hf, b)
+    assert np.array_equal(x1, x2)
+
+
+def test_pcg_factor_matches_z(pair):
+    field, s, hf, hz = pair
+    b = kuhn.rhs(s.n, seed=0)
+    xf, rf = P.pcg(s.A, b, precond=lambda r: P.vcycle(hf, r), tol=1e-8)
+    xz, rz = P.pcg(s.A, b, precond=lambda r: P.vcycle(hz, r), tol=1e-8)
+    assert rf.converged and rz.converged and rf.iterations == rz.iterations
+    assert np.allclose(rf.residual_history, rz.residual_history, rtol=1e-5, atol=0)
+    # the solutions agree to the conditioning floor
+    tol = 1e-10 if field == "c1" else 1e-4
+    assert np.linalg.norm(xf - xz) <= tol * np.linalg.norm(xz)
+
+
+def test_component_solve_matches_scipy(pair):
+    """A_GG^{-1} v through the two sweeps vs a sparse direct solve of the
+    component block A[G, G] (G = the giant component's DoFs)."""
+    import scipy.sparse.linalg as spla
+
+    from paper_2602_23613_b200 import _lib
+
+    field, s, hf, hz = pair
+    dev = hf._dev
+    info = hf.levels[0]._info
+    nG = int(info.max_component)
+    rows = np.zeros(nG, np.int64)
+    dev.check(dev.lib.hcamg_export_dense(dev.h, 0, 1, _lib.ptr(rows)))
+    Agg = s.A[rows][:, rows].tocsc()
+    v = np.random.default_rng(11).uniform(-1, 1, nG)
+    out = np.zeros(nG)
+    dev.check(dev.lib.hcamg_component_solve(dev.h, 0, _lib.ptr(v), _lib.ptr(out)))
+    # backward error: conditioning-independent (c2: kappa(A_GG) ~ 1e12)
+    res = np.linalg.norm(Agg @ out - v) / (spla.norm(Agg, 1) * np.linalg.norm(out))
+    assert res <= 1e-14, res
+    if field == "c1":  # forward error against SuperLU where the block is well conditioned
+        ref = spla.spsolve(Agg, v)
+        assert np.linalg.norm(out - ref) <= 1e-10 * np.linalg.norm(ref)
+
+
+@pytest.mark.parametrize("which", ["factor", "z"])
+def test_apply_p_matches_exported_p(pair, which):
+    """P e and P^T r exactly as the V-cycle applies them vs the exported P."""
+    from paper_2602_23613_b200 import _lib
+
+    field, s, hf, hz = pair
+    h = hf if which == "factor" else hz
+    dev = h._dev
+    Pm = h.levels[0].P
+    n, nc = Pm.shape
+    rng = np.random.default_rng(5)
+    e = rng.uniform(-1, 1, nc)
+    r = rng.uniform(-1, 1, n)
+    pe = np.zeros(n)
+    ptr_ = np.zeros(nc)
+    dev.check(dev.lib.hcamg_debug_apply_p(dev.h, 0, 0, _lib.ptr(e), _lib.ptr(pe)))
+    dev.check(dev.lib.hcamg_debug_apply_p(dev.h, 0, 1, _lib.ptr(r), _lib.ptr(ptr_)))
+    # c2 (1e6 contrast): Z (TRSM) and the sweeps differ by eps * kappa(A_GG)
+    tol = 1e-11 if field == "c1" else 1e-4
+    ref = Pm @ e
+    assert np.linalg.norm(pe - ref) <= tol * np.linalg.norm(ref), np.linalg.norm(pe - ref) / np.linalg.norm(ref)
+    ref = Pm.T @ r
+    assert np.linalg.norm(ptr_ - ref) <= tol * np.linalg.norm(ref), np.linalg.norm(ptr_ - ref) / np.linalg.norm(ref)
