@@ -641,7 +641,7 @@ int hcamg_level(hcamg_handle* h, int32_t level, hcamg_level_info* o) {
     o->nnz_P = L.has_P ? (L.hp.on ? hybrid_nnz(L.P, L.hp, h->stream) : L.P.nnz) : 0;
     o->n_components = L.hp.on ? 1 : 0;
     o->max_component = L.hp.on ? L.hp.nG : 0;
-    o->factor_bytes = L.hp.on && L.hp.fac.on ? L.hp.fac.sweep_bytes[0] + L.hp.fac.sweep_bytes[1] : 0;
+    o->factor_bytes = L.hp.on && L.hp.fac.on ? L.hp.fac.fw.bytes + L.hp.fac.bw.bytes : 0;
     o->factor_steps = L.hp.on && L.hp.fac.on ? L.hp.fac.T : 0;
     o->pad = L.hp.on ? L.P.nnz : 0;  // nnz of the sparse part of a hybrid P
     o->n_pairs = L.split.n_pairs();

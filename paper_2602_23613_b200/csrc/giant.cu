@@ -556,6 +556,26 @@ __global__ void k_tiles_eye(double* const* __restrict__ dst) {
     D[t] = t % (kNB + 1) == 0 ? 1.0 : 0.0;
 }
 
+// Per row of each row-major NB x NB tile in [base, base + ntiles): the
+// 64-column chunk range [j0, j1) holding its nonzeros (0, 0 when empty).
+__global__ void __launch_bounds__(1024) k_row_ranges(const double* __restrict__ base, uint8_t* __restrict__ out) {
+  const double* T = base + (int64_t)blockIdx.x * kNB * kNB;
+  const int lane = threadIdx.x & 31;
+  for (int r = threadIdx.x >> 5; r < kNB; r += 32) {
+    const double* row = T + (int64_t)r * kNB;
+    unsigned m = 0;
+    for (int j = 0; j < kNB / 64; ++j) {
+      const double2 v = *reinterpret_cast<const double2*>(row + 64 * j + 2 * lane);
+      if (__any_sync(0xffffffffu, v.x != 0.0 || v.y != 0.0)) m |= 1u << j;
+    }
+    if (lane == 0) {
+      uint8_t* o = out + ((int64_t)blockIdx.x * kNB + r) * 2;
+      o[0] = m ? (uint8_t)(__ffs(m) - 1) : 0;
+      o[1] = m ? (uint8_t)(32 - __clz(m)) : 0;
+    }
+  }
+}
+
 void tiles_transpose(std::vector<const double*>& src, std::vector<double*>& dst, cudaStream_t s) {
   for (size_t z0 = 0; z0 < src.size(); z0 += 32768) {
     const size_t nz = std::min<size_t>(32768, src.size() - z0);
@@ -571,8 +591,9 @@ void tiles_transpose(std::vector<const double*>& src, std::vector<double*>& dst,
 
 // Operators of the blocked sweeps (trisolve.cuh) from the envelope factor:
 // Linv_kk = L_kk^{-1} (TRSM on identity tiles), M_k = Linv_kk L_{k,k-1},
-// N_k = Linv_kk^T L_{k+1,k}^T, and the forward fold tiles L_{i,k-1} copied
-// row-major.  The backward fold tiles are L's own column-major tiles.
+// N_k = Linv_kk^T L_{k+1,k}^T, the forward fold tiles L_{i,k-1} and the
+// backward fold tiles L_{k+1,j}^T, all as row-major tiles, then compacted
+// (row ranges, step order) by tri_compact.
 void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_t s) {
   const int64_t T = L.T, NN = kNB * kNB;
   std::vector<int64_t> mslot((size_t)T, -1), nslot((size_t)T, -1);
@@ -589,13 +610,15 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
         ffold[(size_t)k].push_back(i);
         ++nF;
       }
-  f.fpool.alloc((T + nM + nF) * NN, s);
-  f.bpool.alloc((T + nN) * NN, s);
-  auto fp = [&](int64_t slot) { return f.fpool.p + slot * NN; };
-  auto bp = [&](int64_t slot) { return f.bpool.p + slot * NN; };
+  // fpool: Linv_kk row-major (T), M_k (nM), forward folds (nF); bpool:
+  // Linv_kk column-major = Linv^T row-major (T), N_k (nN); the backward folds
+  // are L's own column-major tiles.
+  DBuf<double> fpool((T + nM + nF) * NN, s), bpool((T + nN) * NN, s);
+  auto fp = [&](int64_t slot) { return fpool.p + slot * NN; };
+  auto bp = [&](int64_t slot) { return bpool.p + slot * NN; };
   cb(cublasSetStream(h, s), "setStream");
   const double one = 1.0, zero = 0.0;
-  {  // Linv_kk, column-major, in bpool[k]
+  {
     std::vector<double*> eye;
     std::vector<const double*> lkk;
     for (int64_t k = 0; k < T; ++k) {
@@ -612,7 +635,6 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
                           (int)kNB, &one, dl.p, (int)kNB, de.p, (int)kNB, (int)T),
        "dtrsmBatched Linv");
     HC_CUDA(cudaStreamSynchronize(s));
-    // forward Linv row-major = transpose
     std::vector<const double*> src;
     std::vector<double*> dst;
     for (int64_t k = 0; k < T; ++k) {
@@ -621,7 +643,20 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
     }
     tiles_transpose(src, dst, s);
   }
-  if (nM) {  // row-major M_k = column-major (L_{k,k-1}^T Linv_kk^T)
+  auto batched_gemm = [&](cublasOperation_t ta, std::vector<const double*>& ha, std::vector<const double*>& hb,
+                          std::vector<double*>& hc, const char* what) {
+    if (ha.empty()) return;
+    DBuf<const double*> da, db;
+    DBuf<double*> dc;
+    da.upload(ha.data(), (int64_t)ha.size(), s);
+    db.upload(hb.data(), (int64_t)hb.size(), s);
+    dc.upload(hc.data(), (int64_t)hc.size(), s);
+    cb(cublasDgemmBatched(h, ta, ta, (int)kNB, (int)kNB, (int)kNB, &one, da.p, (int)kNB, db.p, (int)kNB, &zero, dc.p,
+                          (int)kNB, (int)ha.size()),
+       what);
+    HC_CUDA(cudaStreamSynchronize(s));
+  };
+  {  // row-major M_k = column-major (L_{k,k-1}^T Linv_kk^T)
     std::vector<const double*> ha, hb;
     std::vector<double*> hc;
     for (int64_t k = 1; k < T; ++k)
@@ -630,17 +665,9 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
         hb.push_back(bp(k));
         hc.push_back(fp(T + mslot[(size_t)k]));
       }
-    DBuf<const double*> da, db;
-    DBuf<double*> dc;
-    da.upload(ha.data(), nM, s);
-    db.upload(hb.data(), nM, s);
-    dc.upload(hc.data(), nM, s);
-    cb(cublasDgemmBatched(h, CUBLAS_OP_T, CUBLAS_OP_T, (int)kNB, (int)kNB, (int)kNB, &one, da.p, (int)kNB, db.p,
-                          (int)kNB, &zero, dc.p, (int)kNB, (int)nM),
-       "dgemmBatched M");
-    HC_CUDA(cudaStreamSynchronize(s));
+    batched_gemm(CUBLAS_OP_T, ha, hb, hc, "dgemmBatched M");
   }
-  if (nN) {  // row-major N_k = column-major (L_{k+1,k} Linv_kk)
+  {  // row-major N_k = column-major (L_{k+1,k} Linv_kk)
     std::vector<const double*> ha, hb;
     std::vector<double*> hc;
     for (int64_t k = 0; k + 1 < T; ++k)
@@ -649,70 +676,53 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
         hb.push_back(bp(k));
         hc.push_back(bp(T + nslot[(size_t)k]));
       }
-    DBuf<const double*> da, db;
-    DBuf<double*> dc;
-    da.upload(ha.data(), nN, s);
-    db.upload(hb.data(), nN, s);
-    dc.upload(hc.data(), nN, s);
-    cb(cublasDgemmBatched(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)kNB, (int)kNB, (int)kNB, &one, da.p, (int)kNB, db.p,
-                          (int)kNB, &zero, dc.p, (int)kNB, (int)nN),
-       "dgemmBatched N");
-    HC_CUDA(cudaStreamSynchronize(s));
+    batched_gemm(CUBLAS_OP_N, ha, hb, hc, "dgemmBatched N");
   }
-  std::vector<TriStep> fs, bs;
-  std::vector<TriTile> ft, bt;
-  {  // forward fold tiles (row-major copies) and steps
+  std::vector<TriSrcStep> fs, bs;
+  {
     std::vector<const double*> src;
     std::vector<double*> dst;
     int64_t slot = T + nM;
     for (int64_t k = 0; k < T; ++k) {
-      TriStep S{};
-      S.k = (int32_t)k;
-      S.c = k >= 1 ? (int32_t)(k - 1) : -1;
-      S.tri = 0;
-      S.a = fp(k);
-      S.b = mslot[(size_t)k] >= 0 ? fp(T + mslot[(size_t)k]) : nullptr;
-      S.t0 = (int64_t)ft.size();
+      TriSrcStep S{(int32_t)k, k >= 1 ? (int32_t)(k - 1) : -1, fp(k),
+                   mslot[(size_t)k] >= 0 ? fp(T + mslot[(size_t)k]) : nullptr, {}};
       for (int64_t i : ffold[(size_t)k]) {
         src.push_back(L.tile(i, k - 1));
         dst.push_back(fp(slot));
-        ft.push_back(TriTile{fp(slot), i});
+        S.folds.emplace_back(fp(slot), i);
         ++slot;
       }
-      S.t1 = (int64_t)ft.size();
-      f.fw.max_tiles = std::max(f.fw.max_tiles, S.t1 - S.t0);
-      fs.push_back(S);
+      fs.push_back(std::move(S));
     }
     if (!src.empty()) tiles_transpose(src, dst, s);
   }
-  for (int64_t k = T - 1; k >= 0; --k) {  // backward steps: fold tiles are L's tiles (k+1, j), j < k
-    TriStep S{};
-    S.k = (int32_t)k;
-    S.c = k + 1 < T ? (int32_t)(k + 1) : -1;
-    S.tri = 1;
-    S.a = bp(k);
-    S.b = nslot[(size_t)k] >= 0 ? bp(T + nslot[(size_t)k]) : nullptr;
-    S.t0 = (int64_t)bt.size();
+  for (int64_t k = T - 1; k >= 0; --k) {
+    TriSrcStep S{(int32_t)k, k + 1 < T ? (int32_t)(k + 1) : -1, bp(k),
+                 nslot[(size_t)k] >= 0 ? bp(T + nslot[(size_t)k]) : nullptr, {}};
     if (k + 1 < T)
-      for (int64_t j = L.j0[(size_t)k + 1]; j < k; ++j) bt.push_back(TriTile{L.tile(k + 1, j), j});
-    S.t1 = (int64_t)bt.size();
-    f.bw.max_tiles = std::max(f.bw.max_tiles, S.t1 - S.t0);
-    bs.push_back(S);
+      for (int64_t j = L.j0[(size_t)k + 1]; j < k; ++j) S.folds.emplace_back(L.tile(k + 1, j), j);
+    bs.push_back(std::move(S));
   }
-  // operator bytes per sweep: triangular rows are read in 64-column chunks
-  const int64_t tri_bytes = 512 * 64 * (kNB / 64) * (kNB / 64 + 1) / 2;
-  for (int d = 0; d < 2; ++d) {
-    const std::vector<TriStep>& v = d == 0 ? fs : bs;
-    int64_t b = 0;
-    for (const TriStep& S : v) b += tri_bytes + (S.b ? 8 * NN : 0) + 8 * NN * (S.t1 - S.t0);
-    f.sweep_bytes[d] = b;
-  }
-  f.fw.nstep = f.bw.nstep = T;
-  f.fw.steps.upload(fs.data(), T, s);
-  f.bw.steps.upload(bs.data(), T, s);
-  f.fw.tiles.upload(ft.data(), (int64_t)ft.size(), s);
-  f.bw.tiles.upload(bt.data(), (int64_t)bt.size(), s);
-  HC_CUDA(cudaStreamSynchronize(s));
+  // row ranges of every tile (data final), host copy for the compaction
+  const int64_t nft = fpool.n / NN, nbt = bpool.n / NN, nlt = L.buf.n / NN;
+  DBuf<uint8_t> rng((nft + nbt + nlt) * kNB * 2, s);
+  k_row_ranges<<<(unsigned)nft, 1024, 0, s>>>(fpool.p, rng.p);
+  k_row_ranges<<<(unsigned)nbt, 1024, 0, s>>>(bpool.p, rng.p + nft * kNB * 2);
+  k_row_ranges<<<(unsigned)nlt, 1024, 0, s>>>(L.buf.p, rng.p + (nft + nbt) * kNB * 2);
+  HC_CHECK_LAUNCH();
+  const std::vector<uint8_t> hr = rng.download();
+  auto ranges = [&](const double* p) -> const uint8_t* {
+    int64_t t;
+    if (p >= fpool.p && p < fpool.p + fpool.n) t = (p - fpool.p) / NN;
+    else if (p >= bpool.p && p < bpool.p + bpool.n) t = nft + (p - bpool.p) / NN;
+    else t = nft + nbt + (p - L.buf.p) / NN;
+    return hr.data() + t * kNB * 2;
+  };
+  tri_compact(fs, ranges, f.fw, s);
+  tri_compact(bs, ranges, f.bw, s);
+  if (getenv("HCAMG_SETUP_TIMING"))
+    fprintf(stderr, "[hcamg setup]   sweeps: T=%lld, fwd %.3f GB, bwd %.3f GB (source tiles: %lld + %lld + %lld L)\n",
+            (long long)T, f.fw.bytes / 1e9, f.bw.bytes / 1e9, (long long)nft, (long long)nbt, (long long)nlt);
 }
 
 }  // namespace
@@ -941,8 +951,7 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
          "dgemm bwd");
   }
   st.mark("  giant: triangular solves");
-  if (fac) fac->Lc = std::move(L.buf);
-  else L.buf.release();
+  L.buf.release();
   permute_rc<true>(n, m, dperm.p, dcol.p, Bp.p, B, s);
   HC_CUDA(cudaStreamSynchronize(s));
   if (fac) fac->perm = std::move(dperm);

@@ -11,36 +11,43 @@ namespace hcamg {
 
 namespace {
 
-constexpr int kTriThreads = 512;
 constexpr int kNB = (int)kTriNB;
-constexpr int kChunks = kNB / 64;  // a warp covers 64 columns (32 lanes x double2) per load
 
 struct TriArgs {
   const int* stop;
   int64_t nstep;
-  const TriStep* steps;
-  const TriTile* tiles;
+  const TriStepD* steps;
+  const TriTask* tasks;
+  const double* pool;
   double* u;  // right-hand side, folded in place
   double* y;  // solution
   unsigned* bar;
+  int64_t pf;  // prefetch distance in steps
+  int pfmode;  // 0: no prefetch, 1: at the start of a step (pf ahead), 2: between barrier arrive and wait (1 ahead)
+  int dbg;     // measurement only: 1 = skip the grid barrier, 2 = skip the row work
 };
 
 // Sum over chunks [j0, j1) of row[64 j + 2 lane .. +1] * x[...] (x in shared
-// memory), butterfly-reduced: every lane returns the row's dot product, summed
-// in the same order whichever warp computes it.
+// memory), 8 chunks in flight per lane, butterfly-reduced: every lane returns
+// the row's dot product, summed in the same order whichever warp computes it.
+template <int kB>
 __device__ __forceinline__ double warp_dot(const double* __restrict__ row, const double* x, int j0, int j1, int lane) {
   double acc0 = 0.0, acc1 = 0.0;
-  double2 v[kChunks];
+  const double2* rp = reinterpret_cast<const double2*>(row + 2 * lane);
+  const double2* xp = reinterpret_cast<const double2*>(x + 2 * lane);
+  for (int j = j0; j < j1; j += kB) {
+    double2 v[kB];
 #pragma unroll
-  for (int j = 0; j < kChunks; ++j)
-    if (j >= j0 && j < j1) v[j] = __ldg(reinterpret_cast<const double2*>(row + 64 * j + 2 * lane));
+    for (int q = 0; q < kB; ++q)
+      if (j + q < j1) v[q] = __ldg(rp + 32 * (j + q));
 #pragma unroll
-  for (int j = 0; j < kChunks; ++j)
-    if (j >= j0 && j < j1) {
-      const double2 xv = *reinterpret_cast<const double2*>(x + 64 * j + 2 * lane);
-      acc0 = fma(v[j].x, xv.x, acc0);
-      acc1 = fma(v[j].y, xv.y, acc1);
-    }
+    for (int q = 0; q < kB; ++q)
+      if (j + q < j1) {
+        const double2 xv = xp[32 * (j + q)];
+        acc0 = fma(v[q].x, xv.x, acc0);
+        acc1 = fma(v[q].y, xv.y, acc1);
+      }
+  }
   double acc = acc0 + acc1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -51,41 +58,30 @@ __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
-// column range [c0, c1) (in 64-column chunks) of a critical row
-__device__ __forceinline__ void crit_chunks(int tri, int r, int& j0, int& j1) {
-  if (tri == 0) {
-    j0 = 0;
-    j1 = r / 64 + 1;
-  } else {
-    j0 = r / 64;
-    j1 = kChunks;
-  }
+// This warp's equal slice of a contiguous byte range [b0, b1) of base into L2.
+__device__ __forceinline__ void prefetch_slice(const char* base, int64_t b0, int64_t b1, int64_t gw, int64_t W) {
+  b0 &= ~int64_t(15);  // bulk prefetch: 16-byte aligned address and size
+  const int64_t len = b1 - b0;
+  if (len <= 0) return;
+  const int64_t sl = ((len + W - 1) / W + 15) & ~int64_t(15);
+  const int64_t p0 = b0 + gw * sl;
+  if (p0 >= b1) return;
+  prefetch_l2(base + p0, (unsigned)(std::min(sl, b1 - p0) & ~int64_t(15)));
 }
 
-__device__ __forceinline__ int64_t step_tasks(const TriStep& S) { return (int64_t)kNB * (1 + (S.t1 - S.t0)); }
-
-// L2 prefetch of the matrix rows this warp reads in step S (lane 0 issues).
-__device__ __forceinline__ void prefetch_step(const TriArgs& a, const TriStep& S, int64_t gw, int64_t W, int lane) {
+__device__ __forceinline__ void prefetch_step(const TriArgs& a, const TriStepD& S, int64_t gw, int64_t W, int lane) {
   if (lane != 0) return;
-  const int64_t nt = step_tasks(S);
-  for (int64_t t = gw; t < nt; t += W) {
-    if (t < kNB) {
-      const int r = (int)t;
-      int j0, j1;
-      crit_chunks(S.tri, r, j0, j1);
-      prefetch_l2(S.a + (int64_t)r * kNB + 64 * j0, (unsigned)(512 * (j1 - j0)));
-      if (S.b) prefetch_l2(S.b + (int64_t)r * kNB, kNB * 8);
-    } else {
-      const TriTile tt = a.tiles[S.t0 + (t - kNB) / kNB];
-      prefetch_l2(tt.a + ((t - kNB) % kNB) * kNB, kNB * 8);
-    }
-  }
+  prefetch_slice(reinterpret_cast<const char*>(a.pool), S.pf0, S.pf1, gw, W);
+  prefetch_slice(reinterpret_cast<const char*>(a.tasks), S.t0 * (int64_t)sizeof(TriTask),
+                 S.t1 * (int64_t)sizeof(TriTask), gw, W);
 }
 
 // One blocked triangular sweep.  Cooperative launch (all CTAs co-resident);
 // steps are separated by a sense-reversing grid barrier split into arrive /
-// wait so the next step's L2 prefetch overlaps the barrier.
-__global__ void __launch_bounds__(kTriThreads, 1) k_tri_sweep(TriArgs a) {
+// wait.  The word is shared by all sweeps of a handle and returns to its
+// low bits after each barrier, so no reset is needed between launches.
+template <int kThr, int kB>
+__global__ void __launch_bounds__(kThr, 1) k_tri_sweep(TriArgs a) {
   if (*a.stop) return;
   __shared__ __align__(16) double su[kNB];
   __shared__ __align__(16) double sy[kNB];
@@ -93,40 +89,36 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_tri_sweep(TriArgs a) {
   const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   unsigned old = 0;
-  if (a.nstep > 0) prefetch_step(a, a.steps[0], gw, W, lane);
+  const int64_t pf = a.pfmode == 1 ? a.pf : (a.pfmode == 2 ? 1 : 0);
+  for (int64_t q = 0; q < pf && q < a.nstep; ++q) prefetch_step(a, a.steps[q], gw, W, lane);
   for (int64_t st = 0; st < a.nstep; ++st) {
-    const TriStep S = a.steps[st];
+    const TriStepD S = a.steps[st];
+    if (a.pfmode == 1 && st + pf < a.nstep) prefetch_step(a, a.steps[st + pf], gw, W, lane);
     for (int t = threadIdx.x; t < kNB; t += blockDim.x) {
       su[t] = __ldcg(a.u + (int64_t)S.k * kNB + t);
       sy[t] = S.c >= 0 ? __ldcg(a.y + (int64_t)S.c * kNB + t) : 0.0;
     }
     __syncthreads();
-    const int64_t nt = step_tasks(S);
-    for (int64_t t = gw; t < nt; t += W) {
-      if (t < kNB) {
-        const int r = (int)t;
-        int j0, j1;
-        crit_chunks(S.tri, r, j0, j1);
-        const double da = warp_dot(S.a + (int64_t)r * kNB, su, j0, j1, lane);
-        const double db = S.b ? warp_dot(S.b + (int64_t)r * kNB, sy, 0, kChunks, lane) : 0.0;
-        if (lane == 0) a.y[(int64_t)S.k * kNB + r] = da - db;
+    const int64_t tend = a.dbg == 2 ? S.t0 : S.t1;
+    for (int64_t t = S.t0 + gw; t < tend; t += W) {
+      const TriTask T = a.tasks[t];
+      if (T.b == -1) {  // fold (row bases are multiples of 64, never -1)
+        const double d = warp_dot<kB>(a.pool + T.a, sy, T.ja0, T.ja1, lane);
+        if (lane == 0) a.u[T.out] = __ldcg(a.u + T.out) - d;
       } else {
-        const TriTile tt = a.tiles[S.t0 + (t - kNB) / kNB];
-        const int r = (int)((t - kNB) % kNB);
-        const double d = warp_dot(tt.a + (int64_t)r * kNB, sy, 0, kChunks, lane);
-        if (lane == 0) {
-          double* o = a.u + tt.blk * kNB + r;
-          *o = __ldcg(o) - d;
-        }
+        const double da = warp_dot<kB>(a.pool + T.a, su, T.ja0, T.ja1, lane);
+        const double db = warp_dot<kB>(a.pool + T.b, sy, T.jb0, T.jb1, lane);
+        if (lane == 0) a.y[T.out] = da - db;
       }
     }
     if (st + 1 == a.nstep) break;
+    if (a.dbg == 1) continue;
     __syncthreads();
     if (threadIdx.x == 0) {
       const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
       asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(a.bar), "r"(inc) : "memory");
     }
-    prefetch_step(a, a.steps[st + 1], gw, W, lane);
+    if (a.pfmode == 2) prefetch_step(a, a.steps[st + 1], gw, W, lane);
     if (threadIdx.x == 0) {
       unsigned cur;
       do {
@@ -134,6 +126,26 @@ __global__ void __launch_bounds__(kTriThreads, 1) k_tri_sweep(TriArgs a) {
       } while (((cur ^ old) & 0x80000000u) == 0);
     }
     __syncthreads();
+  }
+}
+
+struct CopyJob {
+  const double* src;
+  int64_t dst;   // offset in the pool (doubles)
+  int32_t n;     // doubles
+  int32_t pad;
+};
+
+// warp per job: pool[dst .. dst + n) = src[0 .. n)
+__global__ void k_compact_copy(const CopyJob* __restrict__ jobs, int64_t njobs, double* __restrict__ pool) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = w0; j < njobs; j += nw) {
+    const CopyJob J = jobs[j];
+    const double2* sp = reinterpret_cast<const double2*>(J.src);
+    double2* dp = reinterpret_cast<double2*>(pool + J.dst);
+    for (int q = lane; q < J.n / 2; q += 32) dp[q] = sp[q];
   }
 }
 
@@ -185,19 +197,19 @@ __global__ void k_fp_rowsel(int64_t nG, const int32_t* __restrict__ perm, const 
   }
 }
 
-void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double* y, unsigned* bar, cudaStream_t s) {
+template <int kThr, int kB>
+void launch_sweep_t(const TriArgs& a, cudaStream_t s) {
   static int blocks = 0;
   if (!blocks) {
     int per_sm = 0, dev = 0, sms = kSMs;
-    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tri_sweep, kTriThreads, 0));
+    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tri_sweep<kThr, kB>, kThr, 0));
     HC_CUDA(cudaGetDevice(&dev));
     HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     blocks = sms * std::max(1, per_sm);
   }
-  TriArgs a{stop, sw.nstep, sw.steps.p, sw.tiles.p, u, y, bar};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)blocks);
-  cfg.blockDim = dim3(kTriThreads);
+  cfg.blockDim = dim3(kThr);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -205,10 +217,79 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_sweep, a));
+  HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_sweep<kThr, kB>, a));
+}
+
+void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double* y, unsigned* bar, cudaStream_t s) {
+  auto env = [](const char* k, int d) {
+    const char* v = getenv(k);
+    return v ? atoi(v) : d;
+  };
+  // measurement knobs: HCAMG_TRI_PFMODE / HCAMG_TRI_PF (L2 prefetch placement), HCAMG_TRI_DBG
+  TriArgs a{stop, sw.nstep, sw.steps.p, sw.tasks.p, sw.pool.p, u, y, bar, std::max(1, env("HCAMG_TRI_PF", 1)),
+            env("HCAMG_TRI_PFMODE", 2), env("HCAMG_TRI_DBG", 0)};
+  launch_sweep_t<512, 8>(a, s);
 }
 
 }  // namespace
+
+void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const uint8_t*(const double*)>& ranges,
+                 TriSweep& out, cudaStream_t s) {
+  std::vector<TriStepD> steps;
+  std::vector<TriTask> tasks;
+  std::vector<CopyJob> jobs;
+  int64_t off = 0;  // pool offset (doubles)
+  auto place = [&](const double* tile, int r, uint8_t& j0, uint8_t& j1) -> int64_t {
+    const uint8_t* rg = ranges(tile) + 2 * r;
+    j0 = rg[0];
+    j1 = rg[1];
+    if (j0 >= j1) {
+      j0 = j1 = 0;
+      return 0;
+    }
+    const int32_t n = 64 * (j1 - j0);
+    jobs.push_back(CopyJob{tile + (int64_t)r * kNB + 64 * j0, off, n, 0});
+    const int64_t base = off - 64 * (int64_t)j0;
+    off += n;
+    return base;
+  };
+  for (const TriSrcStep& S : src) {
+    TriStepD d{};
+    d.k = S.k;
+    d.c = S.c;
+    d.t0 = (int64_t)tasks.size();
+    d.pf0 = 8 * off;
+    for (int r = 0; r < kNB; ++r) {
+      TriTask t{};
+      t.out = (int32_t)((int64_t)S.k * kNB + r);
+      t.a = place(S.a, r, t.ja0, t.ja1);
+      t.b = S.b ? place(S.b, r, t.jb0, t.jb1) : 0;
+      tasks.push_back(t);
+    }
+    for (const auto& fo : S.folds)
+      for (int r = 0; r < kNB; ++r) {
+        TriTask t{};
+        t.a = place(fo.first, r, t.ja0, t.ja1);
+        if (t.ja0 >= t.ja1) continue;  // an all-zero fold row changes nothing
+        t.b = -1;
+        t.out = (int32_t)(fo.second * kNB + r);
+        tasks.push_back(t);
+      }
+    d.t1 = (int64_t)tasks.size();
+    d.pf1 = 8 * off;
+    steps.push_back(d);
+  }
+  out.nstep = (int64_t)steps.size();
+  out.bytes = 8 * off;
+  out.pool.alloc(std::max<int64_t>(off, 2), s);
+  out.steps.upload(steps.data(), out.nstep, s);
+  out.tasks.upload(tasks.data(), (int64_t)tasks.size(), s);
+  DBuf<CopyJob> dj;
+  dj.upload(jobs.data(), (int64_t)jobs.size(), s);
+  if (!jobs.empty()) k_compact_copy<<<grid_for((int64_t)jobs.size() * 32, 256), 256, 0, s>>>(dj.p, (int64_t)jobs.size(), out.pool.p);
+  HC_CHECK_LAUNCH();
+  HC_CUDA(cudaStreamSynchronize(s));
+}
 
 bool factorp_enabled() {
   const char* e = getenv("HCAMG_PAPPLY");

@@ -20,6 +20,10 @@
 // Linv_kk^T L_{k+1,k}^T and the transposed tiles.  Every output row is one
 // warp's dot product in a fixed order, so a sweep is deterministic.
 #pragma once
+#include <functional>
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 
 namespace hcamg {
@@ -29,37 +33,54 @@ constexpr int64_t kTriNB = 1024;
 // One step of a blocked sweep: rows of block k are the "critical" rows
 // y_k = A u_k - B y_c (A row-major, lower (tri 0) or upper (tri 1)
 // triangular; B row-major or null); tiles [t0, t1) fold y_c into other blocks.
-struct TriStep {
-  int32_t k, c, tri, pad;
+// Source description of one sweep step (setup only): the critical rows of
+// block k are y_k = A u_k - B y_c (A, B row-major NB x NB tiles; B may be
+// null), and each fold (tile, blk) does u[blk] -= tile y_c.
+struct TriSrcStep {
+  int32_t k, c;
   const double* a;
   const double* b;
-  int64_t t0, t1;
+  std::vector<std::pair<const double*, int64_t>> folds;
 };
-struct TriTile {
-  const double* a;  // row-major NB x NB
-  int64_t blk;      // output block: u[blk*NB + r] -= a[r, :] . y_c
+
+// Device form.  Every operator row is stored compactly (only its 64-column
+// chunks [j0, j1) that hold nonzeros, so the envelope zeros and the zero half
+// of the triangular Linv rows are never read), rows of one step contiguous
+// and steps in execution order: a step's operator data is one contiguous
+// region, which the kernel prefetches into L2 in equal slices per warp.
+struct TriTask {
+  int64_t a, b;   // row bases in the pool (chunk j at base + 64 j); b = -1: fold task
+  int32_t out;    // crit: y[out] = A.su - B.sy; fold: u[out] -= A.sy
+  uint8_t ja0, ja1, jb0, jb1;
+};
+struct TriStepD {
+  int32_t k, c;
+  int64_t t0, t1;    // tasks
+  int64_t pf0, pf1;  // byte range of the step's rows in the pool
 };
 
 struct TriSweep {
-  int64_t nstep = 0, max_tiles = 0;
-  DBuf<TriStep> steps;
-  DBuf<TriTile> tiles;
+  int64_t nstep = 0;
+  DBuf<TriStepD> steps;
+  DBuf<TriTask> tasks;
+  DBuf<double> pool;
+  int64_t bytes = 0;  // operator bytes one sweep reads
 };
+
+// Compact the source tiles into a sweep.  ranges(tile) returns the host copy
+// of the tile's row-range table (NB x {j0, j1}).
+void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const uint8_t*(const double*)>& ranges,
+                 TriSweep& out, cudaStream_t s);
 
 struct FactorP {
   bool on = false;
   int64_t nG = 0, nc = 0, T = 0;
   DBuf<int32_t> perm;   // factored position -> position in the component (RCM order)
-  DBuf<double> Lc;      // Cholesky tiles, column-major, block envelope (backward fold tiles)
-  DBuf<double> fpool;   // forward: Linv_kk, M_k and fold tiles, row-major
-  DBuf<double> bpool;   // backward: Linv_kk (column-major = Linv^T row-major), N_k
   TriSweep fw, bw;
   DBuf<int32_t> dof;    // factored position -> DoF of the level
   DCsr Wp, Wpt;         // W' with rows in factored order, and its transpose (n_c x n_G)
   DBuf<double> v0, v1, v2;  // T*NB work vectors
   DBuf<unsigned> bar;       // grid-barrier word (sense-reversing)
-  int64_t sweep_bytes[2] = {0, 0};  // operator bytes the forward / backward sweep reads
-  int64_t pool_bytes() const { return 8 * (Lc.n + fpool.n + bpool.n); }
 };
 
 // Rows of W (in the component's member order given by mpos) and the level
