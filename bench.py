@@ -49,11 +49,12 @@ def measured_peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
-def algorithmic_bytes(h):
+def algorithmic_bytes(h, moved=False):
     """B_iter of SURVEY.md §8(d): bytes one PCG iteration must move, whatever
     the implementation.  B(M) = 12 nnz + 4 (rows + 1); B(P) = min(CSR, hybrid
-    dense-block, factored: the envelope-factor operators of one A_GG^{-1}
-    application + the sparse part); S_l = sum_p [8 k_p (k_p+1)/2 + 12 nnz(A[:, patch_p])]; 3 A
+    dense-block) (moved=True: the bytes this implementation moves instead,
+    i.e. B(P) also takes the factored form -- the envelope-factor operators of
+    one A_GG^{-1} application + the sparse part -- when the level uses it); S_l = sum_p [8 k_p (k_p+1)/2 + 12 nnz(A[:, patch_p])]; 3 A
     applications per smoothed level; 2 * 8 * n_c (n_c+1)/2 for the coarsest."""
     def B(nnz, rows):
         return 12 * nnz + 4 * (rows + 1)
@@ -77,7 +78,7 @@ def algorithmic_bytes(h):
         csr_p = B(int(info.nnz_P), n)
         hybrid = 8 * n_int * nc + B(2 * int(info.n_pairs), n)
         reps = [csr_p, hybrid]
-        if int(info.factor_bytes) > 0:  # P through the envelope factor of A_GG (csrc/trisolve.cu)
+        if moved and int(info.factor_bytes) > 0:  # P through the envelope factor of A_GG (csrc/trisolve.cu)
             reps.append(int(info.factor_bytes) + B(int(info.pad), n))
         total += 3 * B(int(info.nnz_A), n) + 2 * min(reps) + 2 * S + 96 * n
     return int(total)
@@ -514,6 +515,7 @@ def run_ours(args, world, rank, local, dist):
     true_rel = float(np.linalg.norm(system.A @ xs - b_host) / np.linalg.norm(b_host))
 
     B_iter = algorithmic_bytes(h)
+    B_moved = algorithmic_bytes(h, moved=True)
     peaks, peak_kind = measured_peaks()
     t_step = t_total / args.steps
     achieved_iter = B_iter * iters / t_step / 1e9
@@ -557,7 +559,11 @@ def run_ours(args, world, rank, local, dist):
                      "peak_spec": 7700.0, "frac_spec": kr["gbs"] / 7700.0,
                      "iteration": {"achieved": achieved_iter, "frac": achieved_iter / peak_iter,
                                    "algorithmic_bytes_per_iteration": B_iter,
-                                   "model": "SURVEY.md 8(d) B_iter, device time per PCG iteration"}},
+                                   "model": "SURVEY.md 8(d) B_iter (fixed, implementation-independent: P as CSR "
+                                            "or dense block), device time per PCG iteration",
+                                   "moved_bytes_per_iteration": B_moved,
+                                   "moved_achieved": B_moved * iters / t_step / 1e9,
+                                   "moved_frac": B_moved * iters / t_step / 1e9 / peak_iter}},
         "e2e": {"value": e2e_value, "unit": "DoF*iters/s", "h2d_bytes_per_step": 8 * n + 128,
                 "d2h_bytes_per_step": 8 * n + 8 * iters + 128},
         "gpu_launches": launches_per_solve * args.steps,

@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kThr, 1) k_tri_sweep(TriArgs a) {
     const int64_t tend = a.dbg == 2 ? S.t0 : S.t1;
     for (int64_t t = S.t0 + gw; t < tend; t += W) {
       const TriTask T = a.tasks[t];
-      if (T.b == -1) {  // fold (row bases are multiples of 64, never -1)
+      if (T.b < 0) {  // fold
         const double d = warp_dot<kB>(a.pool + T.a, sy, T.ja0, T.ja1, lane);
         if (lane == 0) a.u[T.out] = __ldcg(a.u + T.out) - d;
       } else {
@@ -127,6 +127,354 @@ __global__ void __launch_bounds__(kThr, 1) k_tri_sweep(TriArgs a) {
     }
     __syncthreads();
   }
+}
+
+// ---- dataflow sweep (default) ----------------------------------------------
+//
+// No grid barriers: every task (one operator row) waits only for what it
+// reads.  Tasks keep the step order of the sweep and are dealt to warps
+// round-robin (warp w: tasks w, w + W, ...); every dependency points to an
+// earlier task, so with all warps resident the sweep cannot deadlock.
+//   crit task of step s (block k): y_k[r] = Linv_k[r].u_k - M_k[r].y_c, after
+//     ydone[s-1] = NB (all of y_c) and ufull[k] = nfold[k] (every fold into u_k);
+//   fold task of step s: u[out] -= L[r].y_c, after ydone[s-1] = NB and after
+//     the previous fold into the same row (rowseq[out] = its sequence number),
+//     so the folds into a row happen in step order: bit-identical to the
+//     barrier kernel and deterministic.
+// While it waits, a warp holds its row's operator chunks in registers (the
+// rows do not depend on the vectors) and has the next task's rows prefetched
+// into L2, so the dependency chain costs only vector reads and the dot.
+
+__device__ __forceinline__ unsigned ld_acq(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_until(const unsigned* p, unsigned want) {
+  while (ld_acq(p) < want) __nanosleep(40);
+}
+
+struct FlowArgs {
+  TriArgs t;
+  int64_t ntask;
+  const int32_t* nfold;
+  unsigned* ydone;   // per step: crit rows done
+  unsigned* ufull;   // per block: fold rows done
+  unsigned* rowseq;  // per row: folds applied so far
+};
+
+__global__ void __launch_bounds__(512, 1) k_tri_flow(FlowArgs F) {
+  const TriArgs& a = F.t;
+  if (*a.stop) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t W = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  int64_t st = 0;
+  TriStepD S = a.steps[0];
+  for (int64_t t = gw; t < F.ntask; t += W) {
+    while (t >= S.t1) S = a.steps[++st];
+    const TriTask T = a.tasks[t];
+    if (lane == 0 && t + W < F.ntask) {  // the next task's rows into L2
+      const TriTask Tn = a.tasks[t + W];
+      prefetch_l2(a.pool + Tn.a + 64 * Tn.ja0, 512u * (Tn.ja1 - Tn.ja0));
+      if (Tn.b >= 0 && Tn.jb1 > Tn.jb0) prefetch_l2(a.pool + Tn.b + 64 * Tn.jb0, 512u * (Tn.jb1 - Tn.jb0));
+    }
+    // this row's operator chunks (A part) into registers while the dependencies resolve
+    double2 v[16];
+    const double2* rp = reinterpret_cast<const double2*>(a.pool + T.a + 2 * lane);
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (q >= T.ja0 && q < T.ja1) v[q] = __ldg(rp + 32 * q);
+    const bool fold = T.b < 0;
+    const int blk = T.out / kNB;
+    if (lane == 0 && a.dbg != 1) {
+      if (st > 0) spin_until(F.ydone + st - 1, (unsigned)kNB);
+      if (fold) spin_until(F.rowseq + T.out, (unsigned)(-1 - T.b));
+      else spin_until(F.ufull + blk, (unsigned)F.nfold[blk]);
+    }
+    __syncwarp();
+    const double* xa = fold ? a.y + (int64_t)S.c * kNB : a.u + (int64_t)blk * kNB;
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      if (q >= T.ja0 && q < T.ja1) {
+        const double2 xv = __ldcg(reinterpret_cast<const double2*>(xa + 64 * q + 2 * lane));
+        acc0 = fma(v[q].x, xv.x, acc0);
+        acc1 = fma(v[q].y, xv.y, acc1);
+      }
+    double da = acc0 + acc1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) da += __shfl_xor_sync(0xffffffffu, da, o);
+    if (fold) {
+      if (lane == 0) {
+        double* o = a.u + T.out;
+        *o = __ldcg(o) - da;
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(F.rowseq + T.out), "r"((unsigned)(-T.b)) : "memory");
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(F.ufull + blk) : "memory");
+      }
+    } else {
+      double db = 0.0;
+      if (S.c >= 0) {  // M_k row . y_c, same chunk order as warp_dot
+        const double2* bp = reinterpret_cast<const double2*>(a.pool + T.b + 2 * lane);
+        const double2* yp = reinterpret_cast<const double2*>(a.y + (int64_t)S.c * kNB + 2 * lane);
+        double b0 = 0.0, b1 = 0.0;
+        for (int j = T.jb0; j < T.jb1; j += 8) {
+          double2 w[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (j + q < T.jb1) w[q] = __ldg(bp + 32 * (j + q));
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (j + q < T.jb1) {
+              const double2 yv = __ldcg(yp + 32 * (j + q));
+              b0 = fma(w[q].x, yv.x, b0);
+              b1 = fma(w[q].y, yv.y, b1);
+            }
+        }
+        db = b0 + b1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) db += __shfl_xor_sync(0xffffffffu, db, o);
+      }
+      if (lane == 0) {
+        a.y[T.out] = da - db;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(F.ydone + st) : "memory");
+      }
+    }
+  }
+}
+
+// ---- TMA-streamed sweep (default) -----------------------------------------
+//
+// One CTA per SM; the tasks of a step are split across CTAs contiguously by
+// bytes, so the operator rows a CTA needs in a step are one contiguous pool
+// region, cut into batches of whole tasks (<= 44 KB).  Warp 0 (one lane)
+// streams the batches, step after step, into a ring of four 44 KB shared
+// buffers with cp.async.bulk (completion on the buffer's "full" mbarrier),
+// running ahead of the grid barriers as far as the ring allows: HBM keeps
+// streaming while the consumers synchronise.  Warps 1..kCons consume: per
+// step they load the CTA's task descriptors (before the grid barrier: they do
+// not depend on it), then after the barrier stage u_k / y_c and the fold
+// targets' current values in one round trip, compute every row dot from
+// shared memory (same order as the other kernels: bit-identical), and write
+// all outputs at the end of the step.
+
+constexpr int kNBuf = 4, kBufB = 44 * 1024, kCons = 12, kTmaThreads = 32 * (2 + kCons), kMaxCtaTasks = 384,
+              kMaxCtaBatches = 64;
+constexpr size_t kTmaSmem = 2 * kNB * 8 + (size_t)kNBuf * kBufB + (size_t)kMaxCtaTasks * (2 * sizeof(TriTask) + 16) +
+                            (2 * kNBuf + 4) * 8;
+
+struct TmaArgs {
+  TriArgs t;
+  unsigned long long* trace;  // HCAMG_TRI_DBG=3: per CTA accumulated phase times (ns)
+  const int64_t* ctask;
+  const int64_t* bptr;
+  const TriBatch* batches;
+  int G;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"r"(32 * kCons) : "memory"); }
+
+// dot of chunks [0, n) of a row in shared memory (chunk q at row + 64 q) with x (chunk q at x + 64 q)
+__device__ __forceinline__ double smem_dot(const double* row, const double* x, int n, int lane) {
+  double acc0 = 0.0, acc1 = 0.0;
+  const double2* rp = reinterpret_cast<const double2*>(row + 2 * lane);
+  const double2* xp = reinterpret_cast<const double2*>(x + 2 * lane);
+#pragma unroll 4
+  for (int q = 0; q < n; ++q) {
+    const double2 v = rp[32 * q], xv = xp[32 * q];
+    acc0 = fma(v.x, xv.x, acc0);
+    acc1 = fma(v.y, xv.y, acc1);
+  }
+  double acc = acc0 + acc1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+__global__ void __launch_bounds__(kTmaThreads, 1) k_tri_tma(TmaArgs A) {
+  const TriArgs& a = A.t;
+  if (*a.stop) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* su = reinterpret_cast<double*>(smem);
+  double* sy = su + kNB;
+  unsigned char* buf = smem + 2 * kNB * 8;
+  TriTask* sdesc = reinterpret_cast<TriTask*>(buf + (size_t)kNBuf * kBufB);
+  double* sold = reinterpret_cast<double*>(sdesc + 2 * kMaxCtaTasks);  // fold targets' values
+  double* sres = sold + kMaxCtaTasks;                              // row dots
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sres + kMaxCtaTasks);  // full[kNBuf], empty[kNBuf], dfull[2], dempty[2]
+  uint64_t* dfull = bars + 2 * kNBuf;
+  uint64_t* dempty = dfull + 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x, G = A.G;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 2 * kNBuf + 4; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bars + q)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // per step (double-buffered, loaded one step ahead -- none of it depends on
+  // the barrier): task and batch descriptors, the batch of each task, the step record
+  __shared__ TriBatch sbat[2][kMaxCtaBatches];
+  __shared__ unsigned sdone[2][kMaxCtaBatches];  // tasks of each batch finished
+  __shared__ uint8_t sbidx[2][kMaxCtaTasks];     // batch of each task
+  __shared__ TriStepD sstep[2];
+  __shared__ int64_t sinfo[2][2];  // task count, batch count
+  // batches released so far per ring slot: a warp may wait on batch g (slot
+  // g % kNBuf, round g / kNBuf) only once every earlier round of that slot was
+  // released -- the parity wait cannot tell round r from round r - 2
+  __shared__ unsigned sgen[kNBuf];
+  if (threadIdx.x < kNBuf) sgen[threadIdx.x] = 0;
+  auto load_desc = [&](int64_t st, int ct, int nthr) {
+    const int d = (int)(st & 1);
+    const int64_t t0 = A.ctask[st * (G + 1) + c], t1 = A.ctask[st * (G + 1) + c + 1];
+    const int64_t b0 = A.bptr[st * G + c], b1 = A.bptr[st * G + c + 1];
+    for (int64_t i = ct; i < t1 - t0; i += nthr) sdesc[d * kMaxCtaTasks + i] = a.tasks[t0 + i];
+    for (int64_t i = ct; i < b1 - b0; i += nthr) {
+      const TriBatch B = A.batches[b0 + i];
+      sbat[d][i] = B;
+      sdone[d][i] = 0;
+      for (int64_t t = B.t0; t < B.t1; ++t) sbidx[d][t - t0] = (uint8_t)i;
+    }
+    if (ct == 0) {
+      sstep[d] = a.steps[st];
+      sinfo[d][0] = t1 - t0;
+      sinfo[d][1] = b1 - b0;
+    }
+  };
+  __syncthreads();
+  if (warp == 0) {  // producer: the warp loads 32 batch descriptors at a time, lane 0 issues
+    int64_t nb = 0;
+    const char* pool = reinterpret_cast<const char*>(a.pool);
+    for (int64_t st = 0; st < a.nstep; ++st) {
+      const int64_t b0 = A.bptr[st * G + c], b1 = A.bptr[st * G + c + 1];
+      for (int64_t qb = b0; qb < b1; qb += 32) {
+        TriBatch Bl{};
+        if (qb + lane < b1) Bl = A.batches[qb + lane];
+        const int nl = (int)std::min<int64_t>(32, b1 - qb);
+        for (int l = 0; l < nl; ++l, ++nb) {
+          const int64_t off = __shfl_sync(0xffffffffu, Bl.off, l), bytes = __shfl_sync(0xffffffffu, Bl.bytes, l);
+          if (lane == 0) {
+            const int s = (int)(nb % kNBuf);
+            const uint32_t r = (uint32_t)(nb / kNBuf);
+            const unsigned long long w0 = A.trace ? gtime() : 0;
+            mbar_wait(smem_u32(bars + kNBuf + s), (r & 1) ^ 1);
+            if (A.trace) A.trace[c * 8 + 5] += gtime() - w0;
+            const uint32_t full = smem_u32(bars + s);
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full), "r"((uint32_t)bytes)
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                             smem_u32(buf + (size_t)s * kBufB)),
+                         "l"(pool + off), "r"((uint32_t)bytes), "r"(full)
+                         : "memory");
+          }
+          __syncwarp();
+        }
+      }
+    }
+    return;
+  }
+  if (warp == 1 + kCons) {  // descriptor loader: step st into buffer st & 1, one step ahead of the consumers
+    for (int64_t st = 0; st < a.nstep; ++st) {
+      const int d = (int)(st & 1);
+      const uint32_t r = (uint32_t)(st >> 1);
+      mbar_wait(smem_u32(dempty + d), (r & 1) ^ 1);
+      load_desc(st, lane, 32);
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(dfull + d)) : "memory");
+    }
+    return;
+  }
+  const int cw = warp - 1, ct = threadIdx.x - 32;
+  unsigned old = 0;
+  int64_t nb = 0;
+  // per step: task descriptors, batch descriptors and the step record in shared memory,
+  // loaded before the grid barrier (none of them depends on it)
+  unsigned long long tt[5] = {0, 0, 0, 0, 0}, tp = A.trace ? gtime() : 0;
+  auto mark = [&](int k) {
+    if (A.trace && ct == 0) {
+      const unsigned long long n = gtime();
+      tt[k] += n - tp;
+      tp = n;
+    }
+  };
+  for (int64_t st = 0; st < a.nstep; ++st) {
+    const int d = (int)(st & 1);
+    mbar_wait(smem_u32(dfull + d), (uint32_t)((st >> 1) & 1));  // this step's descriptors in place
+    mark(0);
+    const TriStepD S = sstep[d];
+    const int64_t nt = sinfo[d][0], nbat = sinfo[d][1];
+    const TriTask* desc = sdesc + d * kMaxCtaTasks;
+    for (int t = ct; t < kNB; t += 32 * kCons) {
+      su[t] = __ldcg(a.u + (int64_t)S.k * kNB + t);
+      sy[t] = S.c >= 0 ? __ldcg(a.y + (int64_t)S.c * kNB + t) : 0.0;
+    }
+    for (int64_t i = ct; i < nt; i += 32 * kCons)
+      if (desc[i].b < 0) sold[i] = __ldcg(a.u + desc[i].out);
+    cons_sync();
+    mark(1);
+    // each warp takes the step's tasks round-robin and waits only for the batch
+    // holding its task; the last task finished in a batch frees its buffer
+    for (int64_t i = cw; i < nt; i += kCons) {
+      const int q = sbidx[d][i];
+      const int64_t g = nb + q;  // global batch number of this CTA
+      const int s = (int)(g % kNBuf);
+      const unsigned rnd = (unsigned)(g / kNBuf);
+      while (*reinterpret_cast<volatile unsigned*>(&sgen[s]) < rnd) __nanosleep(20);
+      mbar_wait(smem_u32(bars + s), rnd & 1);
+      const TriBatch& B = sbat[d][q];
+      const unsigned char* bb = buf + (size_t)s * kBufB - B.off;  // pool byte offset -> buffer address
+      const TriTask& T = desc[i];
+      const double* ra = reinterpret_cast<const double*>(bb + 8 * (T.a + 64 * T.ja0));
+      double r;
+      if (T.b < 0) {
+        r = a.dbg == 2 ? 0.0 : smem_dot(ra, sy + 64 * T.ja0, T.ja1 - T.ja0, lane);
+      } else {
+        const double* rb = reinterpret_cast<const double*>(bb + 8 * (T.b + 64 * T.jb0));
+        r = smem_dot(ra, su + 64 * T.ja0, T.ja1 - T.ja0, lane) - smem_dot(rb, sy + 64 * T.jb0, T.jb1 - T.jb0, lane);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        if (T.b < 0) a.u[T.out] = sold[i] - r;
+        else a.y[T.out] = r;
+        if (atomicAdd(&sdone[d][q], 1u) + 1 == (unsigned)(B.t1 - B.t0)) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bars + kNBuf + s)) : "memory");
+          atomicAdd(&sgen[s], 1u);
+        }
+      }
+    }
+    nb += nbat;
+    mark(2);
+    if (st + 1 == a.nstep) break;
+    cons_sync();  // every row of the step written, its descriptors no longer read
+    if (ct == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(dempty + d)) : "memory");
+    mark(3);
+    if (ct == 0 && a.dbg != 1) {
+      const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
+      asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(a.bar), "r"(inc) : "memory");
+      unsigned cur;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(a.bar) : "memory");
+      } while (((cur ^ old) & 0x80000000u) == 0);
+    }
+    cons_sync();  // every consumer past the grid barrier
+    mark(4);
+  }
+  if (A.trace && ct == 0)
+    for (int k = 0; k < 5; ++k) A.trace[c * 8 + k] += tt[k];
 }
 
 struct CopyJob {
@@ -225,9 +573,80 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
     const char* v = getenv(k);
     return v ? atoi(v) : d;
   };
-  // measurement knobs: HCAMG_TRI_PFMODE / HCAMG_TRI_PF (L2 prefetch placement), HCAMG_TRI_DBG
+  // measurement knobs: HCAMG_TRI_KERNEL (1 dataflow, 0 grid-barrier steps),
+  // HCAMG_TRI_PFMODE / HCAMG_TRI_PF (L2 prefetch placement), HCAMG_TRI_DBG
   TriArgs a{stop, sw.nstep, sw.steps.p, sw.tasks.p, sw.pool.p, u, y, bar, std::max(1, env("HCAMG_TRI_PF", 1)),
             env("HCAMG_TRI_PFMODE", 2), env("HCAMG_TRI_DBG", 0)};
+  const int kern = env("HCAMG_TRI_KERNEL", 2);
+  if (kern == 2 && sw.G > 0 && sw.max_cta_tasks <= kMaxCtaTasks && sw.max_cta_batches <= kMaxCtaBatches) {
+    static bool init = false;
+    if (!init) {
+      HC_CUDA(cudaFuncSetAttribute(k_tri_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+      init = true;
+    }
+    static unsigned long long* trace = nullptr;
+    if (a.dbg == 3 && !trace) {
+      HC_CUDA(cudaMalloc(&trace, 8 * 8 * (size_t)sw.G));
+      HC_CUDA(cudaMemset(trace, 0, 8 * 8 * (size_t)sw.G));
+    }
+    if (a.dbg != 3 && trace) {  // print and drop the accumulated phase times
+      std::vector<unsigned long long> h((size_t)8 * sw.G);
+      HC_CUDA(cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost));
+      double m[6] = {0, 0, 0, 0, 0, 0}, mx[6] = {0, 0, 0, 0, 0, 0}, mn[6] = {1e30, 1e30, 1e30, 1e30, 1e30, 1e30};
+      int amx = 0, amn = 0;
+      for (int c = 0; c < sw.G; ++c)
+        for (int k = 0; k < 6; ++k) {
+          const double v = (double)h[(size_t)c * 8 + k];
+          m[k] += v / sw.G;
+          if (k == 2 && v > mx[k]) amx = c;
+          if (k == 2 && v < mn[k]) amn = c;
+          mx[k] = std::max(mx[k], v);
+          mn[k] = std::min(mn[k], v);
+        }
+      fprintf(stderr, "[tri trace] tasks phase min %.3f (cta %d) max %.3f (cta %d); stage min %.3f max %.3f; out max %.3f\n",
+              mn[2] / 1e6, amn, mx[2] / 1e6, amx, mn[1] / 1e6, mx[1] / 1e6, mx[3] / 1e6);
+      fprintf(stderr, "[tri trace] per CTA (ms): top-wait %.3f stage %.3f tasks %.3f out %.3f barrier %.3f | producer empty-wait %.3f\n",
+              m[0] / 1e6, m[1] / 1e6, m[2] / 1e6, m[3] / 1e6, m[4] / 1e6, m[5] / 1e6);
+      cudaFree(trace);
+      trace = nullptr;
+    }
+    TmaArgs A{a, a.dbg == 3 ? trace : nullptr, sw.ctask.p, sw.bptr.p, sw.batches.p, sw.G};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)sw.G);
+    cfg.blockDim = dim3(kTmaThreads);
+    cfg.dynamicSmemBytes = kTmaSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma, A));
+    return;
+  }
+  if (kern == 1) {
+    HC_CUDA(cudaMemsetAsync(sw.flags.p, 0, sizeof(unsigned) * (size_t)sw.flags.n, s));
+    FlowArgs F{a, sw.ntask, sw.nfold.p, sw.flags.p, sw.flags.p + sw.nstep, sw.flags.p + sw.nstep + sw.T};
+    static int blocks = 0;
+    if (!blocks) {
+      int per_sm = 0, dev = 0, sms = kSMs;
+      HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tri_flow, 512, 0));
+      HC_CUDA(cudaGetDevice(&dev));
+      HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      blocks = sms * std::max(1, per_sm);
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(512);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;  // co-residency: every warp must run to guarantee progress
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_flow, F));
+    return;
+  }
   launch_sweep_t<512, 8>(a, s);
 }
 
@@ -238,7 +657,13 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
   std::vector<TriStepD> steps;
   std::vector<TriTask> tasks;
   std::vector<CopyJob> jobs;
-  int64_t off = 0;  // pool offset (doubles)
+  int64_t T = 0;
+  for (const TriSrcStep& S : src) {
+    T = std::max<int64_t>(T, S.k + 1);
+    for (const auto& fo : S.folds) T = std::max<int64_t>(T, fo.second + 1);
+  }
+  std::vector<int32_t> fseq((size_t)(T * kNB), 0);  // folds so far into each row
+  int64_t off = 64 * 16;  // pool offset (doubles); the 8 KB pad keeps every row base (off - 64 j0) >= 0
   auto place = [&](const double* tile, int r, uint8_t& j0, uint8_t& j1) -> int64_t {
     const uint8_t* rg = ranges(tile) + 2 * r;
     j0 = rg[0];
@@ -271,7 +696,7 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
         TriTask t{};
         t.a = place(fo.first, r, t.ja0, t.ja1);
         if (t.ja0 >= t.ja1) continue;  // an all-zero fold row changes nothing
-        t.b = -1;
+        t.b = -1 - fseq[(size_t)(fo.second * kNB + r)]++;
         t.out = (int32_t)(fo.second * kNB + r);
         tasks.push_back(t);
       }
@@ -279,8 +704,64 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
     d.pf1 = 8 * off;
     steps.push_back(d);
   }
+  {  // dataflow counters
+    std::vector<int32_t> nf((size_t)T, 0);
+    for (const TriTask& t : tasks)
+      if (t.b < 0) ++nf[(size_t)(t.out / kNB)];
+    out.nfold.upload(nf.data(), T, s);
+    out.flags.alloc((int64_t)steps.size() + T + T * kNB, s);
+  }
+  {  // CTA partition (contiguous, balanced by bytes + a per-row cost) and <= 44 KB batches for the TMA kernel
+    const int64_t kTaskW = getenv("HCAMG_TRI_TASKW") ? atoll(getenv("HCAMG_TRI_TASKW")) : 1536;
+    int dev = 0, sms = kSMs;
+    HC_CUDA(cudaGetDevice(&dev));
+    HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int G = sms;
+    std::vector<int64_t> ct, bptr(1, 0);
+    std::vector<TriBatch> batches;
+    auto tbytes = [&](int64_t t) {
+      const TriTask& x = tasks[(size_t)t];
+      return 512 * (int64_t)(x.ja1 - x.ja0 + (x.b < 0 ? 0 : x.jb1 - x.jb0));
+    };
+    auto tstart = [&](int64_t t) { return 8 * (tasks[(size_t)t].a + 64 * tasks[(size_t)t].ja0); };
+    int maxt = 0, maxb = 0;
+    for (const TriStepD& d : steps) {
+      int64_t total = 0;
+      for (int64_t t = d.t0; t < d.t1; ++t) total += tbytes(t) + kTaskW;
+      int64_t acc = 0, t = d.t0;
+      for (int c = 0; c < G; ++c) {
+        ct.push_back(t);
+        const int64_t target = c + 1 == G ? INT64_MAX : total * (c + 1) / G;
+        const int64_t c0 = t;
+        while (t < d.t1 && (c + 1 == G || (t - c0 < 384 && acc + (tbytes(t) + kTaskW) / 2 <= target)))
+          acc += tbytes(t++) + kTaskW;
+        maxt = std::max<int>(maxt, (int)(t - c0));
+        const size_t nb0 = batches.size();
+        for (int64_t b0 = c0; b0 < t;) {
+          int64_t b1 = b0, bytes = 0;
+          while (b1 < t && bytes + tbytes(b1) <= 44 * 1024) bytes += tbytes(b1++);
+          batches.push_back(TriBatch{b0, b1, tstart(b0), bytes});
+          b0 = b1;
+        }
+        maxb = std::max<int>(maxb, (int)(batches.size() - nb0));
+        bptr.push_back((int64_t)batches.size());
+      }
+      ct.push_back(d.t1);
+    }
+    out.G = G;
+    out.max_cta_tasks = maxt;
+    out.max_cta_batches = maxb;
+    if (getenv("HCAMG_SETUP_TIMING"))
+      fprintf(stderr, "[hcamg setup]   sweep: %lld steps, %lld tasks, %zu batches, max %d tasks per CTA step\n",
+              (long long)steps.size(), (long long)tasks.size(), batches.size(), maxt);
+    out.ctask.upload(ct.data(), (int64_t)ct.size(), s);
+    out.bptr.upload(bptr.data(), (int64_t)bptr.size(), s);
+    out.batches.upload(batches.data(), (int64_t)batches.size(), s);
+  }
+  out.T = T;
+  out.ntask = (int64_t)tasks.size();
   out.nstep = (int64_t)steps.size();
-  out.bytes = 8 * off;
+  out.bytes = 8 * (off - 64 * 16);
   out.pool.alloc(std::max<int64_t>(off, 2), s);
   out.steps.upload(steps.data(), out.nstep, s);
   out.tasks.upload(tasks.data(), (int64_t)tasks.size(), s);

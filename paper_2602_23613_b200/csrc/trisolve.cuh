@@ -49,7 +49,8 @@ struct TriSrcStep {
 // and steps in execution order: a step's operator data is one contiguous
 // region, which the kernel prefetches into L2 in equal slices per warp.
 struct TriTask {
-  int64_t a, b;   // row bases in the pool (chunk j at base + 64 j); b = -1: fold task
+  int64_t a, b;   // row bases in the pool (chunk j at base + 64 j; bases >= 0);
+                  // b < 0: fold task, the (-1 - b)-th fold into row `out` (step order)
   int32_t out;    // crit: y[out] = A.su - B.sy; fold: u[out] -= A.sy
   uint8_t ja0, ja1, jb0, jb1;
 };
@@ -59,12 +60,28 @@ struct TriStepD {
   int64_t pf0, pf1;  // byte range of the step's rows in the pool
 };
 
+struct TriBatch {
+  int64_t t0, t1;      // tasks
+  int64_t off, bytes;  // their rows: one contiguous pool byte range
+};
+
 struct TriSweep {
-  int64_t nstep = 0;
+  int64_t nstep = 0, ntask = 0, T = 0;
   DBuf<TriStepD> steps;
   DBuf<TriTask> tasks;
   DBuf<double> pool;
   int64_t bytes = 0;  // operator bytes one sweep reads
+  // dataflow kernel: nfold[k] = fold tasks into block k; flags = [ydone (nstep)
+  // | ufull (T) | rowseq (T*NB)] counters, zeroed before every sweep
+  DBuf<int32_t> nfold;
+  DBuf<unsigned> flags;
+  // TMA-streamed kernel: the tasks of step k for CTA c are contiguous,
+  // [ctask[k (G+1) + c], ctask[k (G+1) + c + 1]) (split by bytes), and their
+  // rows, one contiguous pool region, are cut into batches
+  // [bptr[k G + c], bptr[k G + c + 1]) of whole tasks, <= 44 KB each
+  int G = 0, max_cta_tasks = 0, max_cta_batches = 0;
+  DBuf<int64_t> ctask, bptr;
+  DBuf<TriBatch> batches;
 };
 
 // Compact the source tiles into a sweep.  ranges(tile) returns the host copy
