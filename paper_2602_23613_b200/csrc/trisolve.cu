@@ -269,7 +269,9 @@ struct TmaArgs {
   const int64_t* ctask;
   const int64_t* bptr;
   const TriBatch* batches;
-  int G;
+  const int64_t* cptr;   // the same batches per CTA in stream order
+  const TriBatch* cbat;
+  int G, pfd;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -357,32 +359,37 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_tri_tma(TmaArgs A) {
   };
   __syncthreads();
   if (warp == 0) {  // producer: the warp loads 32 batch descriptors at a time, lane 0 issues
+    // the CTA's batches in order are cbat[cptr[c] .. cptr[c+1]); batch i + pfd is
+    // prefetched into L2 when batch i enters the ring (a second lookahead level
+    // behind the 176 KB ring, across steps and barriers)
     int64_t nb = 0;
     const char* pool = reinterpret_cast<const char*>(a.pool);
-    for (int64_t st = 0; st < a.nstep; ++st) {
-      const int64_t b0 = A.bptr[st * G + c], b1 = A.bptr[st * G + c + 1];
-      for (int64_t qb = b0; qb < b1; qb += 32) {
-        TriBatch Bl{};
-        if (qb + lane < b1) Bl = A.batches[qb + lane];
-        const int nl = (int)std::min<int64_t>(32, b1 - qb);
-        for (int l = 0; l < nl; ++l, ++nb) {
-          const int64_t off = __shfl_sync(0xffffffffu, Bl.off, l), bytes = __shfl_sync(0xffffffffu, Bl.bytes, l);
-          if (lane == 0) {
-            const int s = (int)(nb % kNBuf);
-            const uint32_t r = (uint32_t)(nb / kNBuf);
-            const unsigned long long w0 = A.trace ? gtime() : 0;
-            mbar_wait(smem_u32(bars + kNBuf + s), (r & 1) ^ 1);
-            if (A.trace) A.trace[c * 8 + 5] += gtime() - w0;
-            const uint32_t full = smem_u32(bars + s);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full), "r"((uint32_t)bytes)
-                         : "memory");
-            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                             smem_u32(buf + (size_t)s * kBufB)),
-                         "l"(pool + off), "r"((uint32_t)bytes), "r"(full)
-                         : "memory");
-          }
-          __syncwarp();
+    const int64_t i0 = A.cptr[c], i1 = A.cptr[c + 1];
+    const int pfd = A.pfd;
+    for (int64_t qb = i0; qb < i1; qb += 32) {
+      TriBatch Bl{}, Bp{};
+      if (qb + lane < i1) Bl = A.cbat[qb + lane];
+      if (pfd > 0 && qb + lane + pfd < i1) Bp = A.cbat[qb + lane + pfd];
+      const int nl = (int)std::min<int64_t>(32, i1 - qb);
+      for (int l = 0; l < nl; ++l, ++nb) {
+        const int64_t off = __shfl_sync(0xffffffffu, Bl.off, l), bytes = __shfl_sync(0xffffffffu, Bl.bytes, l);
+        const int64_t poff = __shfl_sync(0xffffffffu, Bp.off, l), pbytes = __shfl_sync(0xffffffffu, Bp.bytes, l);
+        if (lane == 0) {
+          if (pbytes > 0) prefetch_l2(pool + poff, (unsigned)pbytes);
+          const int s = (int)(nb % kNBuf);
+          const uint32_t r = (uint32_t)(nb / kNBuf);
+          const unsigned long long w0 = A.trace ? gtime() : 0;
+          mbar_wait(smem_u32(bars + kNBuf + s), (r & 1) ^ 1);
+          if (A.trace) A.trace[c * 8 + 5] += gtime() - w0;
+          const uint32_t full = smem_u32(bars + s);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(full), "r"((uint32_t)bytes)
+                       : "memory");
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                           smem_u32(buf + (size_t)s * kBufB)),
+                       "l"(pool + off), "r"((uint32_t)bytes), "r"(full)
+                       : "memory");
         }
+        __syncwarp();
       }
     }
     return;
@@ -610,7 +617,8 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
       cudaFree(trace);
       trace = nullptr;
     }
-    TmaArgs A{a, a.dbg == 3 ? trace : nullptr, sw.ctask.p, sw.bptr.p, sw.batches.p, sw.G};
+    TmaArgs A{a, a.dbg == 3 ? trace : nullptr, sw.ctask.p, sw.bptr.p, sw.batches.p, sw.cptr.p, sw.cbat.p, sw.G,
+              env("HCAMG_TRI_L2PF", 4)};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)sw.G);
     cfg.blockDim = dim3(kTmaThreads);
@@ -747,6 +755,17 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
         bptr.push_back((int64_t)batches.size());
       }
       ct.push_back(d.t1);
+    }
+    {
+      std::vector<int64_t> cptr(1, 0);
+      std::vector<TriBatch> cbat;
+      for (int c = 0; c < G; ++c) {
+        for (size_t k = 0; k < steps.size(); ++k)
+          for (int64_t q = bptr[k * G + c]; q < bptr[k * G + c + 1]; ++q) cbat.push_back(batches[(size_t)q]);
+        cptr.push_back((int64_t)cbat.size());
+      }
+      out.cptr.upload(cptr.data(), (int64_t)cptr.size(), s);
+      out.cbat.upload(cbat.data(), (int64_t)cbat.size(), s);
     }
     out.G = G;
     out.max_cta_tasks = maxt;

@@ -80,8 +80,8 @@ struct TriSweep {
   // rows, one contiguous pool region, are cut into batches
   // [bptr[k G + c], bptr[k G + c + 1]) of whole tasks, <= 44 KB each
   int G = 0, max_cta_tasks = 0, max_cta_batches = 0;
-  DBuf<int64_t> ctask, bptr;
-  DBuf<TriBatch> batches;
+  DBuf<int64_t> ctask, bptr, cptr;
+  DBuf<TriBatch> batches, cbat;  // cbat: the batches again, per CTA in stream order ([cptr[c], cptr[c+1]))
 };
 
 // Compact the source tiles into a sweep.  ranges(tile) returns the host copy
