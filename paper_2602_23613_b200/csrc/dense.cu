@@ -250,6 +250,8 @@ void dense_spd_inverse(cublasHandle_t h, double* Lbuf, int64_t n, double* Ainv, 
                              (int)nb, &one, Lbuf + j0 + j0 * n, (int)n, Ainv + j0 + j0 * n, (int)n),
                  "dtrsm L^-1 panel");
   }
+  StageTimer st(s);
+  st.mark("    inverse: Y = L^-1");
   // lower(Y^T Y) block column J: Y[J:, J:]^T Y[J:, J]  -> Lbuf[J:, J]
   for (int64_t j0 = 0; j0 < n; j0 += NB) {
     const int64_t nb = std::min(NB, n - j0), m = n - j0;
@@ -258,6 +260,7 @@ void dense_spd_inverse(cublasHandle_t h, double* Lbuf, int64_t n, double* Ainv, 
                              Lbuf + j0 + j0 * n, (int)n),
                  "dtrmm Y^T Y");
   }
+  st.mark("    inverse: lower(Y^T Y)");
   k_sym_from_lower<<<grid_for(n * n, 256, kSMs * 32), 256, 0, s>>>(Lbuf, n, Ainv);
   HC_CHECK_LAUNCH();
 }

@@ -478,18 +478,23 @@ void algebraic_splitting(const DCsr& A, const DCsr& G, double theta, SplitResult
     for (int64_t t = 0; t < k; ++t) h[(size_t)t] = G.ncols + t;
     bcols.upload(h.data(), k);
   }
+  StageTimer stt(s);
   // nodal dual  G~^T (A G~), symmetrised
   DCsr X, GtT, M, An;
   spgemm(A, Gt, X, s);
+  stt.mark("    split: A G~");
   csr_transpose(Gt, GtT, s);
   spgemm(GtT, X, M, s);
+  stt.mark("    split: G~^T (A G~)");
   X = DCsr();
   symmetrize(M, An, s);
   M = DCsr();
+  stt.mark("    split: symmetrise");
   require(An.nrows == mt, "nodal dual size mismatch");
   DCsr nbr;
   DBuf<int8_t> state;
   nodal_cf(An, bcols, theta, nbr, state, s);
+  stt.mark("    split: graph + C/F");
   // c_G = C \ B ; coarse = C (B is prescribed coarse)
   DBuf<int8_t> in_b(mt, s), is_c(mt, s);
   in_b.zero();
@@ -534,6 +539,7 @@ void algebraic_splitting(const DCsr& A, const DCsr& G, double theta, SplitResult
   DBuf<int64_t> pairs(7 * std::max<int64_t>(std::min(ntrip, n), 1), s), npairs(1, s);
   k_match_accept<<<1, 32, 0, s>>>(trip.p, ntrip, used_mid.p, avail.p, pairs.p, npairs.p);
   HC_CHECK_LAUNCH();
+  stt.mark("    split: matching");
   int64_t np_h = read_scalar(npairs.p, s);
   out.pairs.resize((size_t)(7 * np_h));
   if (np_h)

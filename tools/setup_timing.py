@@ -1,0 +1,10 @@
+"""Setup stage times (HCAMG_SETUP_TIMING=1) for one configuration."""
+import os, sys, time
+os.environ["HCAMG_SETUP_TIMING"] = "1"
+sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+import paper_2602_23613_b200 as P
+from paper_2602_23613_b200 import kuhn
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+s = kuhn.config_system(cfg)
+for rep in range(2):
+    t = time.perf_counter(); h = P.build_hierarchy(s, "alg"); print(f"== build {rep}: {time.perf_counter() - t:.3f} s", file=sys.stderr)
