@@ -251,14 +251,14 @@ __global__ void __launch_bounds__(512, 1) k_tri_flow(FlowArgs F) {
 // streams the batches, step after step, into a ring of four 44 KB shared
 // buffers with cp.async.bulk (completion on the buffer's "full" mbarrier),
 // running ahead of the grid barriers as far as the ring allows: HBM keeps
-// streaming while the consumers synchronise.  Warps 1..kCons consume: per
+// streaming while the consumers synchronise.  Warps 1..kCons (16) consume: per
 // step they load the CTA's task descriptors (before the grid barrier: they do
 // not depend on it), then after the barrier stage u_k / y_c and the fold
 // targets' current values in one round trip, compute every row dot from
 // shared memory (same order as the other kernels: bit-identical), and write
 // all outputs at the end of the step.
 
-constexpr int kNBuf = 4, kBufB = 44 * 1024, kCons = 12, kTmaThreads = 32 * (2 + kCons), kMaxCtaTasks = 384,
+constexpr int kNBuf = 4, kBufB = 44 * 1024, kMaxCtaTasks = 384,
               kMaxCtaBatches = 64;
 constexpr size_t kTmaSmem = 2 * kNB * 8 + (size_t)kNBuf * kBufB + (size_t)kMaxCtaTasks * (2 * sizeof(TriTask) + 16) +
                             (2 * kNBuf + 4) * 8;
@@ -290,6 +290,7 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+template <int kCons>
 __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"r"(32 * kCons) : "memory"); }
 
 // dot of chunks [0, n) of a row in shared memory (chunk q at row + 64 q) with x (chunk q at x + 64 q)
@@ -309,7 +310,8 @@ __device__ __forceinline__ double smem_dot(const double* row, const double* x, i
   return acc;
 }
 
-__global__ void __launch_bounds__(kTmaThreads, 1) k_tri_tma(TmaArgs A) {
+template <int kCons>
+__global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
   const TriArgs& a = A.t;
   if (*a.stop) return;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_tri_tma(TmaArgs A) {
     }
     for (int64_t i = ct; i < nt; i += 32 * kCons)
       if (desc[i].b < 0) sold[i] = __ldcg(a.u + desc[i].out);
-    cons_sync();
+    cons_sync<kCons>();
     mark(1);
     // each warp takes the step's tasks round-robin and waits only for the batch
     // holding its task; the last task finished in a batch frees its buffer
@@ -466,7 +468,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_tri_tma(TmaArgs A) {
     nb += nbat;
     mark(2);
     if (st + 1 == a.nstep) break;
-    cons_sync();  // every row of the step written, its descriptors no longer read
+    cons_sync<kCons>();  // every row of the step written, its descriptors no longer read
     if (ct == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(dempty + d)) : "memory");
     mark(3);
     if (ct == 0 && a.dbg != 1) {
@@ -477,7 +479,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) k_tri_tma(TmaArgs A) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(a.bar) : "memory");
       } while (((cur ^ old) & 0x80000000u) == 0);
     }
-    cons_sync();  // every consumer past the grid barrier
+    cons_sync<kCons>();  // every consumer past the grid barrier
     mark(4);
   }
   if (A.trace && ct == 0)
@@ -586,9 +588,12 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
             env("HCAMG_TRI_PFMODE", 2), env("HCAMG_TRI_DBG", 0)};
   const int kern = env("HCAMG_TRI_KERNEL", 2);
   if (kern == 2 && sw.G > 0 && sw.max_cta_tasks <= kMaxCtaTasks && sw.max_cta_batches <= kMaxCtaBatches) {
+    const int cons = env("HCAMG_TRI_CONS", 16);
     static bool init = false;
     if (!init) {
-      HC_CUDA(cudaFuncSetAttribute(k_tri_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
       init = true;
     }
     static unsigned long long* trace = nullptr;
@@ -621,7 +626,7 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
               env("HCAMG_TRI_L2PF", 4)};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)sw.G);
-    cfg.blockDim = dim3(kTmaThreads);
+    cfg.blockDim = dim3(32 * (2 + cons));
     cfg.dynamicSmemBytes = kTmaSmem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -629,7 +634,9 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma, A));
+    if (cons == 8) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<8>, A));
+    else if (cons == 16) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16>, A));
+    else HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<12>, A));
     return;
   }
   if (kern == 1) {

@@ -1,6 +1,6 @@
 # time the dense-regime sweeps (level-0 restriction / prolongation) under kernel knobs
 run() { echo "== $*"; env "$@" timeout 120 python tools/profile_pieces.py c2 2>&1 | grep -E "L0 (prolong)|rror"; }
-run HCAMG_TRI_L2PF=0
-run HCAMG_TRI_L2PF=4
-run HCAMG_TRI_L2PF=8
-run HCAMG_TRI_L2PF=16
+run HCAMG_TRI_CONS=12
+run HCAMG_TRI_CONS=8
+run HCAMG_TRI_CONS=16
+run HCAMG_TRI_CONS=12
