@@ -728,6 +728,7 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
   }
   {  // CTA partition (contiguous, balanced by bytes + a per-row cost) and <= 44 KB batches for the TMA kernel
     const int64_t kTaskW = getenv("HCAMG_TRI_TASKW") ? atoll(getenv("HCAMG_TRI_TASKW")) : 1536;
+    const int64_t kCritPct = getenv("HCAMG_TRI_CRITW") ? atoll(getenv("HCAMG_TRI_CRITW")) : 140;
     int dev = 0, sms = kSMs;
     HC_CUDA(cudaGetDevice(&dev));
     HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -738,18 +739,21 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
       const TriTask& x = tasks[(size_t)t];
       return 512 * (int64_t)(x.ja1 - x.ja0 + (x.b < 0 ? 0 : x.jb1 - x.jb0));
     };
+    auto tcost = [&](int64_t t) {  // partition weight: bytes (crit rows scaled) + a per-row cost
+      const int64_t b = tbytes(t);
+      return (tasks[(size_t)t].b < 0 ? b : b * kCritPct / 100) + kTaskW;
+    };
     auto tstart = [&](int64_t t) { return 8 * (tasks[(size_t)t].a + 64 * tasks[(size_t)t].ja0); };
     int maxt = 0, maxb = 0;
     for (const TriStepD& d : steps) {
       int64_t total = 0;
-      for (int64_t t = d.t0; t < d.t1; ++t) total += tbytes(t) + kTaskW;
+      for (int64_t t = d.t0; t < d.t1; ++t) total += tcost(t);
       int64_t acc = 0, t = d.t0;
       for (int c = 0; c < G; ++c) {
         ct.push_back(t);
         const int64_t target = c + 1 == G ? INT64_MAX : total * (c + 1) / G;
         const int64_t c0 = t;
-        while (t < d.t1 && (c + 1 == G || (t - c0 < 384 && acc + (tbytes(t) + kTaskW) / 2 <= target)))
-          acc += tbytes(t++) + kTaskW;
+        while (t < d.t1 && (c + 1 == G || (t - c0 < 384 && acc + tcost(t) / 2 <= target))) acc += tcost(t++);
         maxt = std::max<int>(maxt, (int)(t - c0));
         const size_t nb0 = batches.size();
         for (int64_t b0 = c0; b0 < t;) {
