@@ -247,8 +247,8 @@ __global__ void __launch_bounds__(512, 1) k_tri_flow(FlowArgs F) {
 //
 // One CTA per SM; the tasks of a step are split across CTAs contiguously by
 // bytes, so the operator rows a CTA needs in a step are one contiguous pool
-// region, cut into batches of whole tasks (<= 44 KB).  Warp 0 (one lane)
-// streams the batches, step after step, into a ring of four 44 KB shared
+// region, cut into batches of whole tasks (<= 46 KB).  Warp 0 (one lane)
+// streams the batches, step after step, into a ring of four 46 KB shared
 // buffers with cp.async.bulk (completion on the buffer's "full" mbarrier),
 // running ahead of the grid barriers as far as the ring allows: HBM keeps
 // streaming while the consumers synchronise.  Warps 1..kCons (16) consume: per
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(512, 1) k_tri_flow(FlowArgs F) {
 // shared memory (same order as the other kernels: bit-identical), and write
 // all outputs at the end of the step.
 
-constexpr int kNBuf = 4, kBufB = 44 * 1024, kMaxCtaTasks = 384,
+constexpr int kNBuf = 4, kBufB = 46 * 1024, kMaxCtaTasks = 256,
               kMaxCtaBatches = 64;
 constexpr size_t kTmaSmem = 2 * kNB * 8 + (size_t)kNBuf * kBufB + (size_t)kMaxCtaTasks * (2 * sizeof(TriTask) + 16) +
                             (2 * kNBuf + 4) * 8;
@@ -753,12 +753,12 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
         ct.push_back(t);
         const int64_t target = c + 1 == G ? INT64_MAX : total * (c + 1) / G;
         const int64_t c0 = t;
-        while (t < d.t1 && (c + 1 == G || (t - c0 < 384 && acc + tcost(t) / 2 <= target))) acc += tcost(t++);
+        while (t < d.t1 && (c + 1 == G || (t - c0 < kMaxCtaTasks && acc + tcost(t) / 2 <= target))) acc += tcost(t++);
         maxt = std::max<int>(maxt, (int)(t - c0));
         const size_t nb0 = batches.size();
         for (int64_t b0 = c0; b0 < t;) {
           int64_t b1 = b0, bytes = 0;
-          while (b1 < t && bytes + tbytes(b1) <= 44 * 1024) bytes += tbytes(b1++);
+          while (b1 < t && bytes + tbytes(b1) <= kBufB) bytes += tbytes(b1++);
           batches.push_back(TriBatch{b0, b1, tstart(b0), bytes});
           b0 = b1;
         }
