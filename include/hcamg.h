@@ -135,6 +135,17 @@ int hcamg_export_dense(hcamg_handle* h, int32_t level, int32_t which, void* out)
  * csrc/trisolve.cu); v, out of length n_G in the member order of
  * hcamg_export_dense(which = 1).  Test/inspection entry (transfer.py:104). */
 int hcamg_component_solve(hcamg_handle* h, int32_t level, const double* v, double* out);
+/* ---- input generation: 3D Kuhn-cube curl-curl system on the GPU ---------
+ * (the 3D analogue of fem.py:143-195 assemble(); lexicographic vertex numbering;
+ * paper_2602_23613_b200/kuhn.py is the host restatement).  muinv: 6 n^3 per-tet
+ * mu^{-1} (cube-major, permutation-minor); S6, M6: 6 x 36 element matrices of the
+ * six tet shapes.  sizes[6] = {n_free_edges, nnz(A), n_free_nodes, nnz(G),
+ * n_edges, n_vertices}; hcamg_kuhn_export then copies A, G (canonical CSR) and the
+ * full -> free index maps (-1: eliminated) into caller buffers. */
+int hcamg_kuhn_assemble(hcamg_handle* h, int64_t n, const double* muinv, double beta, const double* S6,
+                        const double* M6, int64_t* sizes);
+int hcamg_kuhn_export(hcamg_handle* h, int64_t* a_ptr, int32_t* a_idx, double* a_val, int64_t* g_ptr,
+                      int32_t* g_idx, double* g_val, int64_t* free_edges, int64_t* free_nodes);
 /* patches in reference order: ptr (n_patches + 1), dofs (n_patch_entries), wave of each patch */
 int hcamg_export_patches(hcamg_handle* h, int32_t level, int64_t* ptr, int64_t* dofs, int64_t* wave);
 int hcamg_export_coarse_cols(hcamg_handle* h, int32_t level, int64_t* cols);

@@ -25,7 +25,7 @@ EXPORTS = [
     "hcamg_hier_end_with", "hcamg_info_get", "hcamg_notes", "hcamg_level", "hcamg_export_csr",
     "hcamg_export_splitting", "hcamg_export_l1", "hcamg_export_patches", "hcamg_export_coarse_cols",
     "hcamg_vcycle", "hcamg_pcg", "hcamg_amg_solve", "hcamg_pcg_device", "hcamg_graph_launches",
-    "hcamg_stream", "hcamg_pcg_generic", "hcamg_spmv", "hcamg_profile_vcycle", "hcamg_export_dense", "hcamg_component_solve", "hcamg_split_alg", "hcamg_split_export",
+    "hcamg_stream", "hcamg_pcg_generic", "hcamg_spmv", "hcamg_profile_vcycle", "hcamg_export_dense", "hcamg_component_solve", "hcamg_kuhn_assemble", "hcamg_kuhn_export", "hcamg_split_alg", "hcamg_split_export",
     "hcamg_dist_prepare", "hcamg_dist_connect", "hcamg_dist_connect_ptrs", "hcamg_dist_disconnect", "hcamg_dist_info",
 ]
 
@@ -106,6 +106,8 @@ def load(required=True):
         "hcamg_profile_vcycle": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P, P, P]),
         "hcamg_export_dense": (C.c_int, [P, C.c_int32, C.c_int32, P]),
         "hcamg_component_solve": (C.c_int, [P, C.c_int32, P, P]),
+        "hcamg_kuhn_assemble": (C.c_int, [P, C.c_int64, P, C.c_double, P, P, P]),
+        "hcamg_kuhn_export": (C.c_int, [P, P, P, P, P, P, P, P, P]),
         "hcamg_split_alg": (C.c_int, [P, C.POINTER(CSR), C.POINTER(CSR), C.c_double, P]),
         "hcamg_split_export": (C.c_int, [P, P, P, P]),
         "hcamg_dist_prepare": (C.c_int, [P, C.c_int32, C.c_int32, P, C.POINTER(C.c_void_p)]),

@@ -15,6 +15,7 @@
 #include "dense.cuh"
 #include "dist.cuh"
 #include "giant.cuh"
+#include "kuhn.cuh"
 #include "interp.cuh"
 #include "smoother.cuh"
 #include "solve.cuh"
@@ -62,6 +63,9 @@ struct hcamg_handle {
   SplitResult last_split;
   // row-partitioned solve across processes (dist.cuh)
   Dist dist;
+  // last hcamg_kuhn_assemble result (kuhn.cuh)
+  DCsr kuhn_A, kuhn_G;
+  std::vector<int64_t> kuhn_fe, kuhn_fv;
 };
 
 namespace {
@@ -730,6 +734,42 @@ int hcamg_component_solve(hcamg_handle* h, int32_t level, const double* v, doubl
     HC_CUDA(cudaMemcpyAsync(hv.data(), f.v2.p, 8 * hv.size(), cudaMemcpyDeviceToHost, s));
     HC_CUDA(cudaStreamSynchronize(s));
     for (int64_t i = 0; i < f.nG; ++i) out[perm[(size_t)i]] = hv[(size_t)i];
+  });
+}
+
+int hcamg_kuhn_assemble(hcamg_handle* h, int64_t n, const double* muinv, double beta, const double* S6,
+                        const double* M6, int64_t* sizes) {
+  return guarded(h, [&] {
+    require(muinv && S6 && M6 && sizes, "null argument");
+    require(beta >= 0, "shift must be nonnegative");
+    kuhn_assemble(n, muinv, beta, S6, M6, h->kuhn_A, h->kuhn_G, h->kuhn_fe, h->kuhn_fv, h->stream);
+    sizes[0] = h->kuhn_A.nrows;
+    sizes[1] = h->kuhn_A.nnz;
+    sizes[2] = h->kuhn_G.ncols;
+    sizes[3] = h->kuhn_G.nnz;
+    sizes[4] = (int64_t)h->kuhn_fe.size();
+    sizes[5] = (int64_t)h->kuhn_fv.size();
+  });
+}
+
+int hcamg_kuhn_export(hcamg_handle* h, int64_t* a_ptr, int32_t* a_idx, double* a_val, int64_t* g_ptr, int32_t* g_idx,
+                      double* g_val, int64_t* free_edges, int64_t* free_nodes) {
+  return guarded(h, [&] {
+    require(h->kuhn_A.nrows > 0, "no assembled system (call hcamg_kuhn_assemble first)");
+    cudaStream_t s = h->stream;
+    const DCsr& A = h->kuhn_A;
+    const DCsr& G = h->kuhn_G;
+    HC_CUDA(cudaMemcpyAsync(a_ptr, A.ptr.p, 8 * (A.nrows + 1), cudaMemcpyDeviceToHost, s));
+    if (A.nnz) HC_CUDA(cudaMemcpyAsync(a_idx, A.idx.p, 4 * A.nnz, cudaMemcpyDeviceToHost, s));
+    if (A.nnz) HC_CUDA(cudaMemcpyAsync(a_val, A.val.p, 8 * A.nnz, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaMemcpyAsync(g_ptr, G.ptr.p, 8 * (G.nrows + 1), cudaMemcpyDeviceToHost, s));
+    if (G.nnz) HC_CUDA(cudaMemcpyAsync(g_idx, G.idx.p, 4 * G.nnz, cudaMemcpyDeviceToHost, s));
+    if (G.nnz) HC_CUDA(cudaMemcpyAsync(g_val, G.val.p, 8 * G.nnz, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+    if (free_edges) memcpy(free_edges, h->kuhn_fe.data(), 8 * h->kuhn_fe.size());
+    if (free_nodes) memcpy(free_nodes, h->kuhn_fv.data(), 8 * h->kuhn_fv.size());
+    h->kuhn_A = DCsr();
+    h->kuhn_G = DCsr();
   });
 }
 

@@ -31,7 +31,7 @@ import numpy as np
 import scipy.sparse as sp
 
 __all__ = ["KuhnSystem", "kuhn_mesh", "kuhn_chain", "assemble_kuhn", "config_system", "config_chain",
-           "CONFIGS", "rhs"]
+           "CONFIGS", "rhs", "assemble_kuhn_gpu", "config_system_gpu"]
 
 
 def _canon(a, shape=None):
@@ -333,6 +333,91 @@ def config_system(name, n=None):
     cfg = CONFIGS[name]
     mesh = kuhn_mesh(cfg["n"] if n is None else n)
     return assemble_kuhn(mesh, cfg["field"](mesh), cfg["beta"])
+
+
+# --------------------------------------------------------------- GPU assembly
+
+class _KuhnCells:
+    """The cells of ``kuhn_mesh(n)`` (lexicographic numbering) without its edge
+    table: enough for the coefficient fields (``n``, ``nc``, ``tet_centroids``),
+    with the centroids computed from the same float coordinates in the same
+    order, hence bit-identical to ``KuhnMesh.tet_centroids``."""
+
+    def __init__(self, n):
+        self.n = int(n)
+
+    @property
+    def nc(self):
+        return 6 * self.n ** 3
+
+    def tet_corners(self):
+        n = self.n
+        ck, cj, ci = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+        g0 = np.stack([ci.ravel(), cj.ravel(), ck.ravel()], axis=1)         # hex lower corners, cube-major
+        eye = np.eye(3, dtype=np.int64)
+        corners = []
+        for a, b, _ in itertools.permutations(range(3)):
+            corners.append(np.stack([g0, g0 + eye[a], g0 + eye[a] + eye[b], g0 + 1], axis=1))
+        return np.stack(corners, axis=1).reshape(-1, 4, 3)                  # (nt, 4, 3) grid coords
+
+    def tet_centroids(self):
+        return (self.tet_corners().astype(np.float64) / self.n).mean(axis=1)
+
+
+def _element_matrices(n):
+    """S, M of the six tet shapes of hex 0, exactly as assemble_kuhn computes them."""
+    N = n + 1
+    lex = np.arange(N ** 3, dtype=np.int64)
+    g = np.stack([lex % N, (lex // N) % N, lex // (N * N)], axis=1)
+    verts = g.astype(np.float64) / n
+    step = np.array([1, N, N * N], dtype=np.int64)
+    S6, M6 = [], []
+    for a, b, _ in itertools.permutations(range(3)):
+        tet = np.array([0, step[a], step[a] + step[b], step.sum()])
+        S, M = _tet_element(verts[tet])
+        S6.append(S)
+        M6.append(M)
+    return np.ascontiguousarray(S6, np.float64), np.ascontiguousarray(M6, np.float64)
+
+
+def assemble_kuhn_gpu(n, muinv, beta, device=0):
+    """``assemble_kuhn(kuhn_mesh(n), muinv, beta)`` on the GPU (csrc/kuhn.cu):
+    same pattern, G and index maps; an entry of A can differ from the host
+    assembly in the last bit (duplicates are summed in tet order here, in the
+    order of scipy's unstable sort there).  ``As``/``Am`` are not returned."""
+    import ctypes as C
+
+    from .multilevel import _Device
+    from . import _lib
+
+    muinv = np.ascontiguousarray(muinv, dtype=np.float64)
+    if muinv.shape != (6 * n ** 3,):
+        raise ValueError("coefficient field does not match the mesh")
+    if np.any(muinv <= 0):
+        raise ValueError("coefficient values must be positive")
+    if beta < 0:
+        raise ValueError("shift must be nonnegative")
+    S6, M6 = _element_matrices(n)
+    dev = _Device(device)
+    sizes = np.zeros(6, np.int64)
+    dev.check(dev.lib.hcamg_kuhn_assemble(dev.h, int(n), _lib.ptr(muinv), C.c_double(beta), _lib.ptr(S6),
+                                          _lib.ptr(M6), _lib.ptr(sizes)))
+    nfe, nnz_a, nfv, nnz_g, ne, nv = (int(x) for x in sizes)
+    ap, ai, av = np.empty(nfe + 1, np.int64), np.empty(nnz_a, np.int32), np.empty(nnz_a, np.float64)
+    gp, gi, gv = np.empty(nfe + 1, np.int64), np.empty(nnz_g, np.int32), np.empty(nnz_g, np.float64)
+    fe, fv = np.empty(ne, np.int64), np.empty(nv, np.int64)
+    dev.check(dev.lib.hcamg_kuhn_export(dev.h, _lib.ptr(ap), _lib.ptr(ai), _lib.ptr(av), _lib.ptr(gp), _lib.ptr(gi),
+                                        _lib.ptr(gv), _lib.ptr(fe), _lib.ptr(fv)))
+    A = sp.csr_matrix((av, ai, ap), shape=(nfe, nfe))
+    G = sp.csr_matrix((gv, gi, gp), shape=(nfe, nfv))
+    return KuhnSystem(A, None, None, G, float(beta), fe, fv, None)
+
+
+def config_system_gpu(name, n=None, device=0):
+    """``config_system`` with the assembly on the GPU ("alg" configs, lexicographic numbering)."""
+    cfg = CONFIGS[name]
+    n = cfg["n"] if n is None else n
+    return assemble_kuhn_gpu(n, cfg["field"](_KuhnCells(n)), cfg["beta"], device=device)
 
 
 def rhs(n, seed=0):

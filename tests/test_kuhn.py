@@ -1,6 +1,7 @@
 """3D Kuhn-cube input generator (SURVEY.md §A.2 / §A.4 sanity values)."""
 
 import numpy as np
+import pytest
 
 from paper_2602_23613_b200 import kuhn
 
@@ -75,3 +76,21 @@ def test_chain_system_is_the_same_operator_up_to_renumbering():
     Ac = abs(s_chain.A[pc][:, pc]).toarray()
     Al = abs(s_lex.A[pl][:, pl]).toarray()
     assert np.allclose(Ac, Al, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.parametrize("n", [2, 5, 8])
+def test_gpu_assembly_host_inputs_match_mesh(n):
+    """The host inputs of the GPU assembler (csrc/kuhn.cu): tet corners, centroids
+    (for the coefficient fields) and the six element matrices equal those of
+    kuhn_mesh / assemble_kuhn bit for bit."""
+    m = kuhn.kuhn_mesh(n)
+    cells = kuhn._KuhnCells(n)
+    N = n + 1
+    c = cells.tet_corners()
+    assert np.array_equal((c[:, :, 2] * N + c[:, :, 1]) * N + c[:, :, 0], m.tets)
+    assert np.array_equal(cells.tet_centroids(), m.tet_centroids())
+    S6, M6 = kuhn._element_matrices(n)
+    for p in range(6):
+        S, M = kuhn._tet_element(m.vertices[m.tets[p]])
+        assert np.array_equal(S, S6[p]) and np.array_equal(M, M6[p])
+    assert np.all(m.tet_edge_signs == 1)  # lexicographic numbering: every local edge rises
