@@ -247,8 +247,8 @@ __global__ void __launch_bounds__(512, 1) k_tri_flow(FlowArgs F) {
 //
 // One CTA per SM; the tasks of a step are split across CTAs contiguously by
 // bytes, so the operator rows a CTA needs in a step are one contiguous pool
-// region, cut into batches of whole tasks (<= 46 KB).  Warp 0 (one lane)
-// streams the batches, step after step, into a ring of four 46 KB shared
+// region, cut into batches of whole tasks (<= one ring slot).  Warp 0 (one lane)
+// streams the batches, step after step, into a ring of 3 x 61 KB shared
 // buffers with cp.async.bulk (completion on the buffer's "full" mbarrier),
 // running ahead of the grid barriers as far as the ring allows: HBM keeps
 // streaming while the consumers synchronise.  Warps 1..kCons (16) consume: per
@@ -258,10 +258,10 @@ __global__ void __launch_bounds__(512, 1) k_tri_flow(FlowArgs F) {
 // shared memory (same order as the other kernels: bit-identical), and write
 // all outputs at the end of the step.
 
-constexpr int kNBuf = 4, kBufB = 46 * 1024, kMaxCtaTasks = 256,
+constexpr int kRingB = 184 * 1024, kMaxCtaTasks = 256,
               kMaxCtaBatches = 64;
-constexpr size_t kTmaSmem = 2 * kNB * 8 + (size_t)kNBuf * kBufB + (size_t)kMaxCtaTasks * (2 * sizeof(TriTask) + 16) +
-                            (2 * kNBuf + 4) * 8;
+constexpr size_t kTmaSmem = 2 * kNB * 8 + (size_t)kRingB + (size_t)kMaxCtaTasks * (2 * sizeof(TriTask) + 16) +
+                            (2 * 8 + 4) * 8;
 
 struct TmaArgs {
   TriArgs t;
@@ -310,15 +310,16 @@ __device__ __forceinline__ double smem_dot(const double* row, const double* x, i
   return acc;
 }
 
-template <int kCons>
+template <int kCons, int kNBuf>
 __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
+  constexpr int kBufB = (kRingB / kNBuf) & ~511;  // slot stride (= the host batch cap)
   const TriArgs& a = A.t;
   if (*a.stop) return;
   extern __shared__ __align__(128) unsigned char smem[];
   double* su = reinterpret_cast<double*>(smem);
   double* sy = su + kNB;
   unsigned char* buf = smem + 2 * kNB * 8;
-  TriTask* sdesc = reinterpret_cast<TriTask*>(buf + (size_t)kNBuf * kBufB);
+  TriTask* sdesc = reinterpret_cast<TriTask*>(buf + (size_t)kRingB);
   double* sold = reinterpret_cast<double*>(sdesc + 2 * kMaxCtaTasks);  // fold targets' values
   double* sres = sold + kMaxCtaTasks;                              // row dots
   uint64_t* bars = reinterpret_cast<uint64_t*>(sres + kMaxCtaTasks);  // full[kNBuf], empty[kNBuf], dfull[2], dempty[2]
@@ -587,13 +588,18 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
   TriArgs a{stop, sw.nstep, sw.steps.p, sw.tasks.p, sw.pool.p, u, y, bar, std::max(1, env("HCAMG_TRI_PF", 1)),
             env("HCAMG_TRI_PFMODE", 2), env("HCAMG_TRI_DBG", 0)};
   const int kern = env("HCAMG_TRI_KERNEL", 2);
-  if (kern == 2 && sw.G > 0 && sw.max_cta_tasks <= kMaxCtaTasks && sw.max_cta_batches <= kMaxCtaBatches) {
+  if (kern == 2 && sw.G > 0 && sw.max_cta_tasks <= kMaxCtaTasks && sw.max_cta_batches <= kMaxCtaBatches &&
+      (env("HCAMG_TRI_CONS", 16) != 12 || sw.nbuf == 4)) {
     const int cons = env("HCAMG_TRI_CONS", 16);
     static bool init = false;
     if (!init) {
-      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
-      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem));
+      const int sm = (int)kTmaSmem;
+      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<12, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<16, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      HC_CUDA(cudaFuncSetAttribute(k_tri_tma<16, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       init = true;
     }
     static unsigned long long* trace = nullptr;
@@ -626,7 +632,7 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
               env("HCAMG_TRI_L2PF", 4)};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)sw.G);
-    cfg.blockDim = dim3(32 * (2 + cons));
+    cfg.blockDim = dim3(32 * (2 + (cons == 12 ? 12 : 16)));
     cfg.dynamicSmemBytes = kTmaSmem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -634,9 +640,12 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    if (cons == 8) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<8>, A));
-    else if (cons == 16) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16>, A));
-    else HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<12>, A));
+    if (cons == 12) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<12, 4>, A));
+    else if (sw.nbuf == 6) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16, 6>, A));
+    else if (sw.nbuf == 8) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16, 8>, A));
+    else if (sw.nbuf == 2) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16, 2>, A));
+    else if (sw.nbuf == 3) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16, 3>, A));
+    else HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16, 4>, A));
     return;
   }
   if (kern == 1) {
@@ -727,8 +736,12 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
     out.flags.alloc((int64_t)steps.size() + T + T * kNB, s);
   }
   {  // CTA partition (contiguous, balanced by bytes + a per-row cost) and <= 44 KB batches for the TMA kernel
-    const int64_t kTaskW = getenv("HCAMG_TRI_TASKW") ? atoll(getenv("HCAMG_TRI_TASKW")) : 1536;
+    const int64_t kTaskW = getenv("HCAMG_TRI_TASKW") ? atoll(getenv("HCAMG_TRI_TASKW")) : 3072;
     const int64_t kCritPct = getenv("HCAMG_TRI_CRITW") ? atoll(getenv("HCAMG_TRI_CRITW")) : 140;
+    const int nbuf = getenv("HCAMG_TRI_SLOTS") ? atoi(getenv("HCAMG_TRI_SLOTS")) : 3;
+    require(nbuf >= 2 && nbuf <= 8 && nbuf != 5 && nbuf != 7, "HCAMG_TRI_SLOTS must be 2, 3, 4, 6 or 8");
+    const int64_t slotb = (kRingB / nbuf) & ~int64_t(511);
+    out.nbuf = nbuf;
     int dev = 0, sms = kSMs;
     HC_CUDA(cudaGetDevice(&dev));
     HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -758,7 +771,7 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
         const size_t nb0 = batches.size();
         for (int64_t b0 = c0; b0 < t;) {
           int64_t b1 = b0, bytes = 0;
-          while (b1 < t && bytes + tbytes(b1) <= kBufB) bytes += tbytes(b1++);
+          while (b1 < t && bytes + tbytes(b1) <= slotb) bytes += tbytes(b1++);
           batches.push_back(TriBatch{b0, b1, tstart(b0), bytes});
           b0 = b1;
         }
