@@ -271,7 +271,7 @@ struct TmaArgs {
   const TriBatch* batches;
   const int64_t* cptr;   // the same batches per CTA in stream order
   const TriBatch* cbat;
-  int G, pfd;
+  int G, pfd, barmode;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -476,9 +476,21 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
       const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
       asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(a.bar), "r"(inc) : "memory");
       unsigned cur;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(a.bar) : "memory");
-      } while (((cur ^ old) & 0x80000000u) == 0);
+      if (A.barmode == 1) {  // relaxed polling, one acquire fence after
+        do {
+          asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(a.bar) : "memory");
+        } while (((cur ^ old) & 0x80000000u) == 0);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      } else if (A.barmode == 2) {  // acquire polling with a short back-off
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(a.bar) : "memory");
+          if (((cur ^ old) & 0x80000000u) == 0) __nanosleep(32);
+        } while (((cur ^ old) & 0x80000000u) == 0);
+      } else {
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(a.bar) : "memory");
+        } while (((cur ^ old) & 0x80000000u) == 0);
+      }
     }
     cons_sync<kCons>();  // every consumer past the grid barrier
     mark(4);
@@ -623,13 +635,16 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
         }
       fprintf(stderr, "[tri trace] tasks phase min %.3f (cta %d) max %.3f (cta %d); stage min %.3f max %.3f; out max %.3f\n",
               mn[2] / 1e6, amn, mx[2] / 1e6, amx, mn[1] / 1e6, mx[1] / 1e6, mx[3] / 1e6);
+      fprintf(stderr, "[tri trace] tasks+out per CTA (ms):");
+      for (int c = 0; c < sw.G; ++c) fprintf(stderr, " %.2f", (h[(size_t)c * 8 + 2] + h[(size_t)c * 8 + 3]) / 1e6);
+      fprintf(stderr, "\n");
       fprintf(stderr, "[tri trace] per CTA (ms): top-wait %.3f stage %.3f tasks %.3f out %.3f barrier %.3f | producer empty-wait %.3f\n",
               m[0] / 1e6, m[1] / 1e6, m[2] / 1e6, m[3] / 1e6, m[4] / 1e6, m[5] / 1e6);
       cudaFree(trace);
       trace = nullptr;
     }
     TmaArgs A{a, a.dbg == 3 ? trace : nullptr, sw.ctask.p, sw.bptr.p, sw.batches.p, sw.cptr.p, sw.cbat.p, sw.G,
-              env("HCAMG_TRI_L2PF", 4)};
+              env("HCAMG_TRI_L2PF", 2), env("HCAMG_TRI_BAR", 0)};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)sw.G);
     cfg.blockDim = dim3(32 * (2 + (cons == 12 ? 12 : 16)));
