@@ -23,6 +23,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <unordered_map>
 #include <vector>
 
 #include "dense.cuh"
@@ -538,110 +539,124 @@ __global__ void k_fill_m1(int32_t* v, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) v[i] = -1;
 }
 
-// dst[z] = src[z]^T for NB x NB column-major tiles (32 x 32 blocks through shared memory)
-__global__ void __launch_bounds__(256) k_tiles_transpose(const double* const* __restrict__ src,
-                                                         double* const* __restrict__ dst) {
+constexpr int64_t kSB = kTriSB;  // sweep block (half a factor tile)
+
+// dst[z] (SB x SB, ld SB) = src[z]^T, src[z] an SB x SB column-major block with
+// leading dimension lds (32 x 32 sub-blocks through shared memory)
+__global__ void __launch_bounds__(256) k_blocks_transpose(const double* const* __restrict__ src, int64_t lds,
+                                                          double* const* __restrict__ dst) {
   __shared__ double sm[32][33];
   const double* S = src[blockIdx.z];
   double* D = dst[blockIdx.z];
   const int64_t bx = blockIdx.x * 32, by = blockIdx.y * 32;
-  for (int j = threadIdx.y; j < 32; j += 8) sm[j][threadIdx.x] = S[(bx + threadIdx.x) + (by + j) * kNB];
+  for (int j = threadIdx.y; j < 32; j += 8) sm[j][threadIdx.x] = S[(bx + threadIdx.x) + (by + j) * lds];
   __syncthreads();
-  for (int j = threadIdx.y; j < 32; j += 8) D[(by + threadIdx.x) + (bx + j) * kNB] = sm[threadIdx.x][j];
+  for (int j = threadIdx.y; j < 32; j += 8) D[(by + threadIdx.x) + (bx + j) * kSB] = sm[threadIdx.x][j];
 }
 
-__global__ void k_tiles_eye(double* const* __restrict__ dst) {
+__global__ void k_blocks_eye(double* const* __restrict__ dst) {
   double* D = dst[blockIdx.y];
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < kNB * kNB; t += (int64_t)gridDim.x * blockDim.x)
-    D[t] = t % (kNB + 1) == 0 ? 1.0 : 0.0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < kSB * kSB; t += (int64_t)gridDim.x * blockDim.x)
+    D[t] = t % (kSB + 1) == 0 ? 1.0 : 0.0;
 }
 
-// Per row of each row-major NB x NB tile in [base, base + ntiles): the
+// Per row of each source block (SB rows of SB doubles at p + r ld): the
 // 64-column chunk range [j0, j1) holding its nonzeros (0, 0 when empty).
-__global__ void __launch_bounds__(1024) k_row_ranges(const double* __restrict__ base, uint8_t* __restrict__ out) {
-  const double* T = base + (int64_t)blockIdx.x * kNB * kNB;
+__global__ void __launch_bounds__(1024) k_block_ranges(const TriSrc* __restrict__ blocks, uint8_t* __restrict__ out) {
+  const TriSrc B = blocks[blockIdx.x];
   const int lane = threadIdx.x & 31;
-  for (int r = threadIdx.x >> 5; r < kNB; r += 32) {
-    const double* row = T + (int64_t)r * kNB;
+  for (int r = threadIdx.x >> 5; r < kSB; r += 32) {
+    const double* row = B.p + (int64_t)r * B.ld;
     unsigned m = 0;
-    for (int j = 0; j < kNB / 64; ++j) {
+    for (int j = 0; j < kSB / 64; ++j) {
       const double2 v = *reinterpret_cast<const double2*>(row + 64 * j + 2 * lane);
       if (__any_sync(0xffffffffu, v.x != 0.0 || v.y != 0.0)) m |= 1u << j;
     }
     if (lane == 0) {
-      uint8_t* o = out + ((int64_t)blockIdx.x * kNB + r) * 2;
+      uint8_t* o = out + ((int64_t)blockIdx.x * kSB + r) * 2;
       o[0] = m ? (uint8_t)(__ffs(m) - 1) : 0;
       o[1] = m ? (uint8_t)(32 - __clz(m)) : 0;
     }
   }
 }
 
-void tiles_transpose(std::vector<const double*>& src, std::vector<double*>& dst, cudaStream_t s) {
+void blocks_transpose(std::vector<const double*>& src, int64_t lds, std::vector<double*>& dst, cudaStream_t s) {
   for (size_t z0 = 0; z0 < src.size(); z0 += 32768) {
     const size_t nz = std::min<size_t>(32768, src.size() - z0);
     DBuf<const double*> ds;
     DBuf<double*> dd;
     ds.upload(src.data() + z0, (int64_t)nz, s);
     dd.upload(dst.data() + z0, (int64_t)nz, s);
-    k_tiles_transpose<<<dim3(kNB / 32, kNB / 32, (unsigned)nz), dim3(32, 8), 0, s>>>(ds.p, dd.p);
+    k_blocks_transpose<<<dim3(kSB / 32, kSB / 32, (unsigned)nz), dim3(32, 8), 0, s>>>(ds.p, lds, dd.p);
     HC_CHECK_LAUNCH();
     HC_CUDA(cudaStreamSynchronize(s));
   }
 }
 
-// Operators of the blocked sweeps (trisolve.cuh) from the envelope factor:
-// Linv_kk = L_kk^{-1} (TRSM on identity tiles), M_k = Linv_kk L_{k,k-1},
-// N_k = Linv_kk^T L_{k+1,k}^T, the forward fold tiles L_{i,k-1} and the
-// backward fold tiles L_{k+1,j}^T, all as row-major tiles, then compacted
-// (row ranges, step order) by tri_compact.
+// Operators of the blocked sweeps (trisolve.cuh) from the envelope factor, on
+// sweep blocks of SB rows (SB = NB, or NB / 2 for twice the steps with half
+// the rows each -- measured slower: the per-step synchronisation dominates).
+// Sub-block (I, J) of L is rows (I%SP) SB.., cols (J%SP) SB.. of tile
+// (I/SP, J/SP) (column-major, ld NB); above-diagonal sub-blocks of a diagonal
+// tile are not part of L.  Linv_II = L_II^{-1} (TRSM on identity blocks), M_I = Linv_II
+// L_{I,I-1}, N_I = Linv_II^T L_{I+1,I}^T, forward folds L_{i,I-1} copied
+// row-major; the backward folds are columns of L, read in place.
 void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_t s) {
-  const int64_t T = L.T, NN = kNB * kNB;
-  std::vector<int64_t> mslot((size_t)T, -1), nslot((size_t)T, -1);
+  constexpr int64_t SP = kNB / kSB;  // sweep blocks per factor tile (1 or 2)
+  static_assert(SP * kSB == kNB, "the sweep block must divide the factor tile");
+  const int64_t T = L.T, TS = SP * T, SS = kSB * kSB;
+  auto valid = [&](int64_t I, int64_t J) {
+    const int64_t K = I / SP, Jt = J / SP;
+    return J <= I && L.has(K, Jt) && !(K == Jt && (I % SP) < (J % SP));
+  };
+  auto sub = [&](int64_t I, int64_t J) {  // column-major, ld NB
+    return L.tile(I / SP, J / SP) + (J % SP) * kSB * kNB + (I % SP) * kSB;
+  };
+  std::vector<int64_t> mslot((size_t)TS, -1), nslot((size_t)TS, -1);
   int64_t nM = 0, nN = 0;
-  for (int64_t k = 1; k < T; ++k)
-    if (L.has(k, k - 1)) mslot[(size_t)k] = nM++;
-  for (int64_t k = 0; k + 1 < T; ++k)
-    if (L.has(k + 1, k)) nslot[(size_t)k] = nN++;
-  std::vector<std::vector<int64_t>> ffold((size_t)T);  // forward step k: blocks i >= k+1 reached by column k-1
+  for (int64_t I = 1; I < TS; ++I)
+    if (valid(I, I - 1)) mslot[(size_t)I] = nM++;
+  for (int64_t I = 0; I + 1 < TS; ++I)
+    if (valid(I + 1, I)) nslot[(size_t)I] = nN++;
+  std::vector<std::vector<int64_t>> ffold((size_t)TS);
   int64_t nF = 0;
-  for (int64_t k = 1; k < T; ++k)
-    for (int64_t i = k + 1; i < T; ++i)
-      if (L.has(i, k - 1)) {
-        ffold[(size_t)k].push_back(i);
+  for (int64_t I = 1; I < TS; ++I)
+    for (int64_t i = I + 1; i < TS; ++i)
+      if (valid(i, I - 1)) {
+        ffold[(size_t)I].push_back(i);
         ++nF;
       }
-  // fpool: Linv_kk row-major (T), M_k (nM), forward folds (nF); bpool:
-  // Linv_kk column-major = Linv^T row-major (T), N_k (nN); the backward folds
-  // are L's own column-major tiles.
-  DBuf<double> fpool((T + nM + nF) * NN, s), bpool((T + nN) * NN, s);
-  auto fp = [&](int64_t slot) { return fpool.p + slot * NN; };
-  auto bp = [&](int64_t slot) { return bpool.p + slot * NN; };
+  // fpool: Linv_II row-major (TS), M_I (nM), forward folds (nF); bpool:
+  // Linv_II column-major = Linv^T row-major (TS), N_I (nN)
+  DBuf<double> fpool((TS + nM + nF) * SS, s), bpool((TS + nN) * SS, s);
+  auto fp = [&](int64_t slot) { return fpool.p + slot * SS; };
+  auto bp = [&](int64_t slot) { return bpool.p + slot * SS; };
   cb(cublasSetStream(h, s), "setStream");
   const double one = 1.0, zero = 0.0;
   {
     std::vector<double*> eye;
-    std::vector<const double*> lkk;
-    for (int64_t k = 0; k < T; ++k) {
-      eye.push_back(bp(k));
-      lkk.push_back(L.tile(k, k));
+    std::vector<const double*> lii;
+    for (int64_t I = 0; I < TS; ++I) {
+      eye.push_back(bp(I));
+      lii.push_back(sub(I, I));
     }
     DBuf<double*> de;
-    de.upload(eye.data(), T, s);
-    k_tiles_eye<<<dim3(256, (unsigned)T), 256, 0, s>>>(de.p);
+    de.upload(eye.data(), TS, s);
+    k_blocks_eye<<<dim3(128, (unsigned)TS), 256, 0, s>>>(de.p);
     HC_CHECK_LAUNCH();
     DBuf<const double*> dl;
-    dl.upload(lkk.data(), T, s);
-    cb(cublasDtrsmBatched(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)kNB,
-                          (int)kNB, &one, dl.p, (int)kNB, de.p, (int)kNB, (int)T),
+    dl.upload(lii.data(), TS, s);
+    cb(cublasDtrsmBatched(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)kSB,
+                          (int)kSB, &one, dl.p, (int)kNB, de.p, (int)kSB, (int)TS),
        "dtrsmBatched Linv");
     HC_CUDA(cudaStreamSynchronize(s));
     std::vector<const double*> src;
     std::vector<double*> dst;
-    for (int64_t k = 0; k < T; ++k) {
-      src.push_back(bp(k));
-      dst.push_back(fp(k));
+    for (int64_t I = 0; I < TS; ++I) {
+      src.push_back(bp(I));
+      dst.push_back(fp(I));
     }
-    tiles_transpose(src, dst, s);
+    blocks_transpose(src, kSB, dst, s);
   }
   auto batched_gemm = [&](cublasOperation_t ta, std::vector<const double*>& ha, std::vector<const double*>& hb,
                           std::vector<double*>& hc, const char* what) {
@@ -651,30 +666,30 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
     da.upload(ha.data(), (int64_t)ha.size(), s);
     db.upload(hb.data(), (int64_t)hb.size(), s);
     dc.upload(hc.data(), (int64_t)hc.size(), s);
-    cb(cublasDgemmBatched(h, ta, ta, (int)kNB, (int)kNB, (int)kNB, &one, da.p, (int)kNB, db.p, (int)kNB, &zero, dc.p,
-                          (int)kNB, (int)ha.size()),
+    cb(cublasDgemmBatched(h, ta, ta, (int)kSB, (int)kSB, (int)kSB, &one, da.p, (int)kNB, db.p, (int)kSB, &zero, dc.p,
+                          (int)kSB, (int)ha.size()),
        what);
     HC_CUDA(cudaStreamSynchronize(s));
   };
-  {  // row-major M_k = column-major (L_{k,k-1}^T Linv_kk^T)
+  {  // row-major M_I = column-major (L_{I,I-1}^T Linv_II^T)
     std::vector<const double*> ha, hb;
     std::vector<double*> hc;
-    for (int64_t k = 1; k < T; ++k)
-      if (mslot[(size_t)k] >= 0) {
-        ha.push_back(L.tile(k, k - 1));
-        hb.push_back(bp(k));
-        hc.push_back(fp(T + mslot[(size_t)k]));
+    for (int64_t I = 1; I < TS; ++I)
+      if (mslot[(size_t)I] >= 0) {
+        ha.push_back(sub(I, I - 1));
+        hb.push_back(bp(I));
+        hc.push_back(fp(TS + mslot[(size_t)I]));
       }
     batched_gemm(CUBLAS_OP_T, ha, hb, hc, "dgemmBatched M");
   }
-  {  // row-major N_k = column-major (L_{k+1,k} Linv_kk)
+  {  // row-major N_I = column-major (L_{I+1,I} Linv_II)
     std::vector<const double*> ha, hb;
     std::vector<double*> hc;
-    for (int64_t k = 0; k + 1 < T; ++k)
-      if (nslot[(size_t)k] >= 0) {
-        ha.push_back(L.tile(k + 1, k));
-        hb.push_back(bp(k));
-        hc.push_back(bp(T + nslot[(size_t)k]));
+    for (int64_t I = 0; I + 1 < TS; ++I)
+      if (nslot[(size_t)I] >= 0) {
+        ha.push_back(sub(I + 1, I));
+        hb.push_back(bp(I));
+        hc.push_back(bp(TS + nslot[(size_t)I]));
       }
     batched_gemm(CUBLAS_OP_N, ha, hb, hc, "dgemmBatched N");
   }
@@ -682,47 +697,77 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
   {
     std::vector<const double*> src;
     std::vector<double*> dst;
-    int64_t slot = T + nM;
-    for (int64_t k = 0; k < T; ++k) {
-      TriSrcStep S{(int32_t)k, k >= 1 ? (int32_t)(k - 1) : -1, fp(k),
-                   mslot[(size_t)k] >= 0 ? fp(T + mslot[(size_t)k]) : nullptr, {}};
-      for (int64_t i : ffold[(size_t)k]) {
-        src.push_back(L.tile(i, k - 1));
+    int64_t slot = TS + nM;
+    for (int64_t I = 0; I < TS; ++I) {
+      TriSrcStep S;
+      S.k = (int32_t)I;
+      S.c = I >= 1 ? (int32_t)(I - 1) : -1;
+      S.a.p = fp(I);
+      S.a.ld = kSB;
+      if (mslot[(size_t)I] >= 0) {
+        S.b.p = fp(TS + mslot[(size_t)I]);
+        S.b.ld = kSB;
+      }
+      for (int64_t i : ffold[(size_t)I]) {
+        src.push_back(sub(i, I - 1));
         dst.push_back(fp(slot));
-        S.folds.emplace_back(fp(slot), i);
+        TriSrc fo;
+        fo.p = fp(slot);
+        fo.ld = kSB;
+        S.folds.emplace_back(fo, i);
         ++slot;
       }
       fs.push_back(std::move(S));
     }
-    if (!src.empty()) tiles_transpose(src, dst, s);
+    if (!src.empty()) blocks_transpose(src, kNB, dst, s);
   }
-  for (int64_t k = T - 1; k >= 0; --k) {
-    TriSrcStep S{(int32_t)k, k + 1 < T ? (int32_t)(k + 1) : -1, bp(k),
-                 nslot[(size_t)k] >= 0 ? bp(T + nslot[(size_t)k]) : nullptr, {}};
-    if (k + 1 < T)
-      for (int64_t j = L.j0[(size_t)k + 1]; j < k; ++j) S.folds.emplace_back(L.tile(k + 1, j), j);
+  for (int64_t I = TS - 1; I >= 0; --I) {
+    TriSrcStep S;
+    S.k = (int32_t)I;
+    S.c = I + 1 < TS ? (int32_t)(I + 1) : -1;
+    S.a.p = bp(I);
+    S.a.ld = kSB;
+    if (nslot[(size_t)I] >= 0) {
+      S.b.p = bp(TS + nslot[(size_t)I]);
+      S.b.ld = kSB;
+    }
+    if (I + 1 < TS)  // rows of L_{I+1,j}^T = columns of the column-major sub-block (stride NB)
+      for (int64_t j = SP * L.j0[(size_t)((I + 1) / SP)]; j < I; ++j)
+        if (valid(I + 1, j)) {
+          TriSrc fo;
+          fo.p = sub(I + 1, j);
+          fo.ld = kNB;
+          S.folds.emplace_back(fo, j);
+        }
     bs.push_back(std::move(S));
   }
-  // row ranges of every tile (data final), host copy for the compaction
-  const int64_t nft = fpool.n / NN, nbt = bpool.n / NN, nlt = L.buf.n / NN;
-  DBuf<uint8_t> rng((nft + nbt + nlt) * kNB * 2, s);
-  k_row_ranges<<<(unsigned)nft, 1024, 0, s>>>(fpool.p, rng.p);
-  k_row_ranges<<<(unsigned)nbt, 1024, 0, s>>>(bpool.p, rng.p + nft * kNB * 2);
-  k_row_ranges<<<(unsigned)nlt, 1024, 0, s>>>(L.buf.p, rng.p + (nft + nbt) * kNB * 2);
-  HC_CHECK_LAUNCH();
-  const std::vector<uint8_t> hr = rng.download();
-  auto ranges = [&](const double* p) -> const uint8_t* {
-    int64_t t;
-    if (p >= fpool.p && p < fpool.p + fpool.n) t = (p - fpool.p) / NN;
-    else if (p >= bpool.p && p < bpool.p + bpool.n) t = nft + (p - bpool.p) / NN;
-    else t = nft + nbt + (p - L.buf.p) / NN;
-    return hr.data() + t * kNB * 2;
+  // row ranges of every source block (data final), host copies for the compaction
+  std::vector<TriSrc> blocks;
+  std::unordered_map<const double*, size_t> index;
+  auto add = [&](const TriSrc& b) {
+    if (b.p && index.emplace(b.p, blocks.size()).second) blocks.push_back(b);
   };
+  for (int d = 0; d < 2; ++d)
+    for (const TriSrcStep& S : d == 0 ? fs : bs) {
+      add(S.a);
+      add(S.b);
+      for (const auto& fo : S.folds) add(fo.first);
+    }
+  DBuf<TriSrc> dblocks;
+  dblocks.upload(blocks.data(), (int64_t)blocks.size(), s);
+  DBuf<uint8_t> rng((int64_t)blocks.size() * kSB * 2, s);
+  for (size_t z0 = 0; z0 < blocks.size(); z0 += 65535) {
+    const size_t nz = std::min<size_t>(65535, blocks.size() - z0);
+    k_block_ranges<<<(unsigned)nz, 1024, 0, s>>>(dblocks.p + z0, rng.p + z0 * kSB * 2);
+    HC_CHECK_LAUNCH();
+  }
+  const std::vector<uint8_t> hr = rng.download();
+  auto ranges = [&](const double* p) -> const uint8_t* { return hr.data() + index.at(p) * kSB * 2; };
   tri_compact(fs, ranges, f.fw, s);
   tri_compact(bs, ranges, f.bw, s);
   if (getenv("HCAMG_SETUP_TIMING"))
-    fprintf(stderr, "[hcamg setup]   sweeps: T=%lld, fwd %.3f GB, bwd %.3f GB (source tiles: %lld + %lld + %lld L)\n",
-            (long long)T, f.fw.bytes / 1e9, f.bw.bytes / 1e9, (long long)nft, (long long)nbt, (long long)nlt);
+    fprintf(stderr, "[hcamg setup]   sweeps: %lld blocks of %lld rows, fwd %.3f GB, bwd %.3f GB\n", (long long)TS,
+            (long long)kSB, f.fw.bytes / 1e9, f.bw.bytes / 1e9);
 }
 
 }  // namespace

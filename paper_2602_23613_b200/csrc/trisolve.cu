@@ -11,7 +11,7 @@ namespace hcamg {
 
 namespace {
 
-constexpr int kNB = (int)kTriNB;
+constexpr int kNB = (int)kTriSB;  // rows per sweep step
 
 struct TriArgs {
   const int* stop;
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(512, 1) k_tri_flow(FlowArgs F) {
 // shared memory (same order as the other kernels: bit-identical), and write
 // all outputs at the end of the step.
 
-constexpr int kRingB = 184 * 1024, kMaxCtaTasks = 256,
+constexpr int kRingB = (kNB == 512 ? 192 : 184) * 1024, kMaxCtaTasks = 256,
               kMaxCtaBatches = 64;
 constexpr size_t kTmaSmem = 2 * kNB * 8 + (size_t)kRingB + (size_t)kMaxCtaTasks * (2 * sizeof(TriTask) + 16) +
                             (2 * 8 + 4) * 8;
@@ -703,8 +703,8 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
   }
   std::vector<int32_t> fseq((size_t)(T * kNB), 0);  // folds so far into each row
   int64_t off = 64 * 16;  // pool offset (doubles); the 8 KB pad keeps every row base (off - 64 j0) >= 0
-  auto place = [&](const double* tile, int r, uint8_t& j0, uint8_t& j1) -> int64_t {
-    const uint8_t* rg = ranges(tile) + 2 * r;
+  auto place = [&](const TriSrc& src, int r, uint8_t& j0, uint8_t& j1) -> int64_t {
+    const uint8_t* rg = ranges(src.p) + 2 * r;
     j0 = rg[0];
     j1 = rg[1];
     if (j0 >= j1) {
@@ -712,7 +712,7 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
       return 0;
     }
     const int32_t n = 64 * (j1 - j0);
-    jobs.push_back(CopyJob{tile + (int64_t)r * kNB + 64 * j0, off, n, 0});
+    jobs.push_back(CopyJob{src.p + (int64_t)r * src.ld + 64 * j0, off, n, 0});
     const int64_t base = off - 64 * (int64_t)j0;
     off += n;
     return base;
@@ -727,7 +727,7 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
       TriTask t{};
       t.out = (int32_t)((int64_t)S.k * kNB + r);
       t.a = place(S.a, r, t.ja0, t.ja1);
-      t.b = S.b ? place(S.b, r, t.jb0, t.jb1) : 0;
+      t.b = S.b.p ? place(S.b, r, t.jb0, t.jb1) : 0;
       tasks.push_back(t);
     }
     for (const auto& fo : S.folds)

@@ -28,7 +28,10 @@
 
 namespace hcamg {
 
-constexpr int64_t kTriNB = 1024;
+constexpr int64_t kTriNB = 1024;  // factor tile (giant.cu); work vectors are padded to T * kTriNB
+// sweep block: one step solves kTriSB rows (kTriNB or kTriNB / 2; measured on
+// config 2: 1024 -> 2.62 ms, 512 -> 3.2-3.3 ms per restriction/prolongation)
+constexpr int64_t kTriSB = 1024;
 
 // One step of a blocked sweep: rows of block k are the "critical" rows
 // y_k = A u_k - B y_c (A row-major, lower (tri 0) or upper (tri 1)
@@ -36,11 +39,15 @@ constexpr int64_t kTriNB = 1024;
 // Source description of one sweep step (setup only): the critical rows of
 // block k are y_k = A u_k - B y_c (A, B row-major NB x NB tiles; B may be
 // null), and each fold (tile, blk) does u[blk] -= tile y_c.
+// A kTriSB x kTriSB operator block as rows: row r = p[r * ld .. r * ld + kTriSB).
+struct TriSrc {
+  const double* p = nullptr;
+  int64_t ld = 0;
+};
 struct TriSrcStep {
-  int32_t k, c;
-  const double* a;
-  const double* b;
-  std::vector<std::pair<const double*, int64_t>> folds;
+  int32_t k, c;  // sweep blocks (kTriSB rows each)
+  TriSrc a, b;   // b.p == nullptr: no coupling block
+  std::vector<std::pair<TriSrc, int64_t>> folds;
 };
 
 // Device form.  Every operator row is stored compactly (only its 64-column
@@ -84,8 +91,8 @@ struct TriSweep {
   DBuf<TriBatch> batches, cbat;  // cbat: the batches again, per CTA in stream order ([cptr[c], cptr[c+1]))
 };
 
-// Compact the source tiles into a sweep.  ranges(tile) returns the host copy
-// of the tile's row-range table (NB x {j0, j1}).
+// Compact the source blocks into a sweep.  ranges(p) returns the host copy of
+// the row-range table (kTriSB x {j0, j1}, 64-column chunks) of the block at p.
 void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const uint8_t*(const double*)>& ranges,
                  TriSweep& out, cudaStream_t s);
 
