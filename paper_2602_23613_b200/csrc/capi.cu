@@ -482,6 +482,18 @@ int hcamg_create(hcamg_handle** out, int device, void* cuda_stream) {
     }
     HC_CUDA(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
     if (cublasCreate(&h->cublas) != CUBLAS_STATUS_SUCCESS) throw Error(ECUDA_, "cublasCreate failed");
+    {
+      // keep freed device memory in the stream-ordered pool (the setup's
+      // transient tens-of-GB buffers are then not re-mapped on the next build);
+      // HCAMG_POOL_RELEASE=1 restores the driver default (release at sync)
+      const char* e = getenv("HCAMG_POOL_RELEASE");
+      if (!(e && atoi(e) == 1)) {
+        cudaMemPool_t pool;
+        HC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        HC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      }
+    }
   } catch (const Error& e) {
     fprintf(stderr, "hcamg_create: %s\n", e.what());
     delete h;

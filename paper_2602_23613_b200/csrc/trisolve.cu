@@ -703,8 +703,9 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
   }
   std::vector<int32_t> fseq((size_t)(T * kNB), 0);  // folds so far into each row
   int64_t off = 64 * 16;  // pool offset (doubles); the 8 KB pad keeps every row base (off - 64 j0) >= 0
-  auto place = [&](const TriSrc& src, int r, uint8_t& j0, uint8_t& j1) -> int64_t {
-    const uint8_t* rg = ranges(src.p) + 2 * r;
+  // rgt: the block's range table (looked up once per block, not per row)
+  auto place = [&](const TriSrc& src, const uint8_t* rgt, int r, uint8_t& j0, uint8_t& j1) -> int64_t {
+    const uint8_t* rg = rgt + 2 * r;
     j0 = rg[0];
     j1 = rg[1];
     if (j0 >= j1) {
@@ -723,22 +724,26 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
     d.c = S.c;
     d.t0 = (int64_t)tasks.size();
     d.pf0 = 8 * off;
+    const uint8_t* rga = ranges(S.a.p);
+    const uint8_t* rgb = S.b.p ? ranges(S.b.p) : nullptr;
     for (int r = 0; r < kNB; ++r) {
       TriTask t{};
       t.out = (int32_t)((int64_t)S.k * kNB + r);
-      t.a = place(S.a, r, t.ja0, t.ja1);
-      t.b = S.b.p ? place(S.b, r, t.jb0, t.jb1) : 0;
+      t.a = place(S.a, rga, r, t.ja0, t.ja1);
+      t.b = S.b.p ? place(S.b, rgb, r, t.jb0, t.jb1) : 0;
       tasks.push_back(t);
     }
-    for (const auto& fo : S.folds)
+    for (const auto& fo : S.folds) {
+      const uint8_t* rgf = ranges(fo.first.p);
       for (int r = 0; r < kNB; ++r) {
         TriTask t{};
-        t.a = place(fo.first, r, t.ja0, t.ja1);
+        t.a = place(fo.first, rgf, r, t.ja0, t.ja1);
         if (t.ja0 >= t.ja1) continue;  // an all-zero fold row changes nothing
         t.b = -1 - fseq[(size_t)(fo.second * kNB + r)]++;
         t.out = (int32_t)(fo.second * kNB + r);
         tasks.push_back(t);
       }
+    }
     d.t1 = (int64_t)tasks.size();
     d.pf1 = 8 * off;
     steps.push_back(d);

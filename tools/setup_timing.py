@@ -1,4 +1,4 @@
-"""Setup stage times (HCAMG_SETUP_TIMING=1) for one configuration."""
+"""Setup stage times (HCAMG_SETUP_TIMING=1) for one configuration; three builds."""
 import os, sys, time
 os.environ["HCAMG_SETUP_TIMING"] = "1"
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
@@ -6,5 +6,7 @@ import paper_2602_23613_b200 as P
 from paper_2602_23613_b200 import kuhn
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 s = kuhn.config_system(cfg)
-for rep in range(2):
+h = None
+for rep in range(3):
+    h = None
     t = time.perf_counter(); h = P.build_hierarchy(s, "alg"); print(f"== build {rep}: {time.perf_counter() - t:.3f} s", file=sys.stderr)
