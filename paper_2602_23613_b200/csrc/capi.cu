@@ -737,7 +737,7 @@ int hcamg_component_solve(hcamg_handle* h, int32_t level, const double* v, doubl
     FactorP& f = L.hp.fac;
     cudaStream_t s = h->stream;
     std::vector<int32_t> perm = f.perm.download();
-    std::vector<double> hv((size_t)(f.T * kTriNB), 0.0);
+    std::vector<double> hv((size_t)factorp_npad(f), 0.0);
     for (int64_t i = 0; i < f.nG; ++i) hv[(size_t)i] = v[perm[(size_t)i]];
     HC_CUDA(cudaMemcpyAsync(f.v0.p, hv.data(), 8 * hv.size(), cudaMemcpyHostToDevice, s));
     DBuf<int> stop(1, s);

@@ -580,6 +580,22 @@ __global__ void __launch_bounds__(1024) k_block_ranges(const TriSrc* __restrict_
   }
 }
 
+// dst[z] (an NB x NB quadrant of an SB-wide column-major block) = src[z] (an NB x NB tile)
+__global__ void __launch_bounds__(256) k_tile_into_block(const double* const* __restrict__ src,
+                                                         double* const* __restrict__ dst) {
+  const double* S = src[blockIdx.z];
+  double* D = dst[blockIdx.z];
+  const int64_t bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += 8) D[(bx + threadIdx.x) + (by + j) * kSB] = S[(bx + threadIdx.x) + (by + j) * kNB];
+}
+
+// identity NB x NB quadrant of an SB-wide column-major block (padding past the last tile)
+__global__ void k_tile_eye_in_block(double* const* __restrict__ dst) {
+  double* D = dst[blockIdx.y];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < kNB; t += (int64_t)gridDim.x * blockDim.x)
+    D[t + t * kSB] = 1.0;
+}
+
 void blocks_transpose(std::vector<const double*>& src, int64_t lds, std::vector<double*>& dst, cudaStream_t s) {
   for (size_t z0 = 0; z0 < src.size(); z0 += 32768) {
     const size_t nz = std::min<size_t>(32768, src.size() - z0);
@@ -602,14 +618,73 @@ void blocks_transpose(std::vector<const double*>& src, int64_t lds, std::vector<
 // L_{I,I-1}, N_I = Linv_II^T L_{I+1,I}^T, forward folds L_{i,I-1} copied
 // row-major; the backward folds are columns of L, read in place.
 void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_t s) {
-  constexpr int64_t SP = kNB / kSB;  // sweep blocks per factor tile (1 or 2)
-  static_assert(SP * kSB == kNB, "the sweep block must divide the factor tile");
-  const int64_t T = L.T, TS = SP * T, SS = kSB * kSB;
+  // SP sweep blocks per factor tile (SB <= NB) or Q factor tiles per sweep block (SB = Q NB)
+  constexpr int64_t SP = kSB <= kNB ? kNB / kSB : 1, Q = kSB > kNB ? kSB / kNB : 1;
+  static_assert(SP * kSB == kNB || Q * kNB == kSB, "sweep block and factor tile must nest");
+  const int64_t T = L.T, TS = Q > 1 ? (T + Q - 1) / Q : SP * T, SS = kSB * kSB;
+  auto tile_ok = [&](int64_t I, int64_t J) { return I < T && J < T && J <= I && L.has(I, J); };
   auto valid = [&](int64_t I, int64_t J) {
+    if (J > I) return false;
+    if (Q > 1) {
+      for (int64_t a = 0; a < Q; ++a)
+        for (int64_t b = 0; b < Q; ++b)
+          if (Q * J + b <= Q * I + a && tile_ok(Q * I + a, Q * J + b)) return true;
+      return I == J;  // (a virtual identity diagonal block past the last tile)
+    }
     const int64_t K = I / SP, Jt = J / SP;
-    return J <= I && L.has(K, Jt) && !(K == Jt && (I % SP) < (J % SP));
+    return L.has(K, Jt) && !(K == Jt && (I % SP) < (J % SP));
   };
-  auto sub = [&](int64_t I, int64_t J) {  // column-major, ld NB
+  // SB = Q NB: the sweep blocks of L are assembled into dense column-major
+  // SB x SB slots (missing tiles zero, blocks above the diagonal dropped, an
+  // identity past the last tile); SB <= NB: they are views into the tiles
+  std::vector<int64_t> lslot((size_t)(TS * TS), -1);
+  int64_t nL = 0;
+  if (Q > 1)
+    for (int64_t I = 0; I < TS; ++I)
+      for (int64_t J = 0; J <= I; ++J)
+        if (valid(I, J)) lslot[(size_t)(I * TS + J)] = nL++;
+  DBuf<double> Lsb(std::max<int64_t>(nL, 1) * SS, s);
+  if (Q > 1) {
+    Lsb.zero();
+    std::vector<const double*> src;
+    std::vector<double*> dst;
+    std::vector<double*> eye;
+    for (int64_t I = 0; I < TS; ++I)
+      for (int64_t J = 0; J <= I; ++J) {
+        const int64_t sl = lslot[(size_t)(I * TS + J)];
+        if (sl < 0) continue;
+        for (int64_t a = 0; a < Q; ++a)
+          for (int64_t b = 0; b < Q; ++b) {
+            double* d = Lsb.p + sl * SS + (b * kNB) * kSB + a * kNB;
+            if (Q * J + b <= Q * I + a && tile_ok(Q * I + a, Q * J + b)) {
+              src.push_back(L.tile(Q * I + a, Q * J + b));
+              dst.push_back(d);
+            } else if (I == J && a == b && Q * I + a >= T) {
+              eye.push_back(d);
+            }
+          }
+      }
+    for (size_t z0 = 0; z0 < src.size(); z0 += 32768) {  // NB x NB tile copies into the SB-wide slots
+      const size_t nz = std::min<size_t>(32768, src.size() - z0);
+      DBuf<const double*> ds;
+      DBuf<double*> dd;
+      ds.upload(src.data() + z0, (int64_t)nz, s);
+      dd.upload(dst.data() + z0, (int64_t)nz, s);
+      k_tile_into_block<<<dim3(kNB / 32, kNB / 32, (unsigned)nz), dim3(32, 8), 0, s>>>(ds.p, dd.p);
+      HC_CHECK_LAUNCH();
+      HC_CUDA(cudaStreamSynchronize(s));
+    }
+    if (!eye.empty()) {
+      DBuf<double*> de;
+      de.upload(eye.data(), (int64_t)eye.size(), s);
+      k_tile_eye_in_block<<<dim3(64, (unsigned)eye.size()), 256, 0, s>>>(de.p);
+      HC_CHECK_LAUNCH();
+      HC_CUDA(cudaStreamSynchronize(s));
+    }
+  }
+  const int64_t LDS = Q > 1 ? kSB : kNB;  // leading dimension of the blocks of L
+  auto sub = [&](int64_t I, int64_t J) -> double* {  // column-major, ld LDS
+    if (Q > 1) return Lsb.p + lslot[(size_t)(I * TS + J)] * SS;
     return L.tile(I / SP, J / SP) + (J % SP) * kSB * kNB + (I % SP) * kSB;
   };
   std::vector<int64_t> mslot((size_t)TS, -1), nslot((size_t)TS, -1);
@@ -647,7 +722,7 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
     DBuf<const double*> dl;
     dl.upload(lii.data(), TS, s);
     cb(cublasDtrsmBatched(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)kSB,
-                          (int)kSB, &one, dl.p, (int)kNB, de.p, (int)kSB, (int)TS),
+                          (int)kSB, &one, dl.p, (int)LDS, de.p, (int)kSB, (int)TS),
        "dtrsmBatched Linv");
     HC_CUDA(cudaStreamSynchronize(s));
     std::vector<const double*> src;
@@ -666,7 +741,7 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
     da.upload(ha.data(), (int64_t)ha.size(), s);
     db.upload(hb.data(), (int64_t)hb.size(), s);
     dc.upload(hc.data(), (int64_t)hc.size(), s);
-    cb(cublasDgemmBatched(h, ta, ta, (int)kSB, (int)kSB, (int)kSB, &one, da.p, (int)kNB, db.p, (int)kSB, &zero, dc.p,
+    cb(cublasDgemmBatched(h, ta, ta, (int)kSB, (int)kSB, (int)kSB, &one, da.p, (int)LDS, db.p, (int)kSB, &zero, dc.p,
                           (int)kSB, (int)ha.size()),
        what);
     HC_CUDA(cudaStreamSynchronize(s));
@@ -719,7 +794,7 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
       }
       fs.push_back(std::move(S));
     }
-    if (!src.empty()) blocks_transpose(src, kNB, dst, s);
+    if (!src.empty()) blocks_transpose(src, LDS, dst, s);
   }
   for (int64_t I = TS - 1; I >= 0; --I) {
     TriSrcStep S;
@@ -731,12 +806,12 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
       S.b.p = bp(TS + nslot[(size_t)I]);
       S.b.ld = kSB;
     }
-    if (I + 1 < TS)  // rows of L_{I+1,j}^T = columns of the column-major sub-block (stride NB)
-      for (int64_t j = SP * L.j0[(size_t)((I + 1) / SP)]; j < I; ++j)
+    if (I + 1 < TS)  // rows of L_{I+1,j}^T = columns of the column-major block (stride LDS)
+      for (int64_t j = 0; j < I; ++j)
         if (valid(I + 1, j)) {
           TriSrc fo;
           fo.p = sub(I + 1, j);
-          fo.ld = kNB;
+          fo.ld = LDS;
           S.folds.emplace_back(fo, j);
         }
     bs.push_back(std::move(S));

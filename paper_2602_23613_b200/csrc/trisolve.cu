@@ -202,6 +202,13 @@ __global__ void __launch_bounds__(512, 1) k_tri_flow(FlowArgs F) {
         acc0 = fma(v[q].x, xv.x, acc0);
         acc1 = fma(v[q].y, xv.y, acc1);
       }
+    for (int q = 16; q < T.ja1; ++q)  // rows longer than 16 chunks (sweep blocks above 1024 rows)
+      if (q >= T.ja0) {
+        const double2 w = __ldg(rp + 32 * q);
+        const double2 xv = __ldcg(reinterpret_cast<const double2*>(xa + 64 * q + 2 * lane));
+        acc0 = fma(w.x, xv.x, acc0);
+        acc1 = fma(w.y, xv.y, acc1);
+      }
     double da = acc0 + acc1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) da += __shfl_xor_sync(0xffffffffu, da, o);
@@ -258,7 +265,7 @@ __global__ void __launch_bounds__(512, 1) k_tri_flow(FlowArgs F) {
 // shared memory (same order as the other kernels: bit-identical), and write
 // all outputs at the end of the step.
 
-constexpr int kRingB = (kNB == 512 ? 192 : 184) * 1024, kMaxCtaTasks = 256,
+constexpr int kRingB = (kNB == 512 ? 192 : kNB == 1024 ? 184 : 168) * 1024, kMaxCtaTasks = 256,
               kMaxCtaBatches = 64;
 constexpr size_t kTmaSmem = 2 * kNB * 8 + (size_t)kRingB + (size_t)kMaxCtaTasks * (2 * sizeof(TriTask) + 16) +
                             (2 * 8 + 4) * 8;
@@ -758,7 +765,8 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
   {  // CTA partition (contiguous, balanced by bytes + a per-row cost) and <= 44 KB batches for the TMA kernel
     const int64_t kTaskW = getenv("HCAMG_TRI_TASKW") ? atoll(getenv("HCAMG_TRI_TASKW")) : 3072;
     const int64_t kCritPct = getenv("HCAMG_TRI_CRITW") ? atoll(getenv("HCAMG_TRI_CRITW")) : 140;
-    const int nbuf = getenv("HCAMG_TRI_SLOTS") ? atoi(getenv("HCAMG_TRI_SLOTS")) : 3;
+    // ring slots (measured on config 2: 1024-row steps best with 3, 2048-row steps with 2)
+  const int nbuf = getenv("HCAMG_TRI_SLOTS") ? atoi(getenv("HCAMG_TRI_SLOTS")) : (kNB >= 2048 ? 2 : 3);
     require(nbuf >= 2 && nbuf <= 8 && nbuf != 5 && nbuf != 7, "HCAMG_TRI_SLOTS must be 2, 3, 4, 6 or 8");
     const int64_t slotb = (kRingB / nbuf) & ~int64_t(511);
     out.nbuf = nbuf;
@@ -835,6 +843,8 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
   HC_CUDA(cudaStreamSynchronize(s));
 }
 
+int64_t factorp_npad(const FactorP& f) { return (f.T * kTriNB + kTriSB - 1) / kTriSB * kTriSB; }
+
 bool factorp_enabled() {
   const char* e = getenv("HCAMG_PAPPLY");
   return !(e && std::string(e) == "z");
@@ -849,7 +859,7 @@ void factorp_attach(FactorP& f, const DCsr& W, const int32_t* mpos, const int32_
   HC_CHECK_LAUNCH();
   csr_extract(W, sel.p, nG, nullptr, W.ncols, f.Wp, s);
   csr_transpose(f.Wp, f.Wpt, s);
-  const int64_t npad = f.T * kTriNB;
+  const int64_t npad = factorp_npad(f);
   f.v0.alloc(npad, s);
   f.v1.alloc(npad, s);
   f.v2.alloc(npad, s);
@@ -867,7 +877,7 @@ void factorp_solve(const int* stop, FactorP& f, double* v, double* y, cudaStream
 }
 
 void factorp_restrict(const int* stop, FactorP& f, const double* r, double* bc, cudaStream_t s) {
-  const int64_t npad = f.T * kTriNB;
+  const int64_t npad = factorp_npad(f);
   k_fp_gather<<<grid_for(npad, 256), 256, 0, s>>>(stop, f.nG, npad, f.dof.p, r, f.v0.p);
   HC_CHECK_LAUNCH();
   factorp_solve(stop, f, f.v0.p, f.v2.p, s);
@@ -877,7 +887,7 @@ void factorp_restrict(const int* stop, FactorP& f, const double* r, double* bc, 
 }
 
 void factorp_prolong(const int* stop, FactorP& f, const double* e, double* x, cudaStream_t s) {
-  const int64_t npad = f.T * kTriNB;
+  const int64_t npad = factorp_npad(f);
   k_fp_spmv<false><<<grid_for(npad * 32, 256), 256, 0, s>>>(stop, f.nG, npad, f.Wp.ptr.p, f.Wp.idx.p, f.Wp.val.p, e,
                                                             f.v0.p);
   HC_CHECK_LAUNCH();

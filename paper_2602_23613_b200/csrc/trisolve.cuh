@@ -29,9 +29,10 @@
 namespace hcamg {
 
 constexpr int64_t kTriNB = 1024;  // factor tile (giant.cu); work vectors are padded to T * kTriNB
-// sweep block: one step solves kTriSB rows (kTriNB or kTriNB / 2; measured on
-// config 2: 1024 -> 2.62 ms, 512 -> 3.2-3.3 ms per restriction/prolongation)
-constexpr int64_t kTriSB = 1024;
+// sweep block: one step solves kTriSB rows (kTriNB / 2, kTriNB or 2 kTriNB;
+// measured on config 2 per restriction/prolongation: 512 -> 3.2-3.3 ms,
+// 1024 -> 2.62 ms, 2048 -> 2.43 ms: fewer grid barriers for 7 % more bytes)
+constexpr int64_t kTriSB = 2048;
 
 // One step of a blocked sweep: rows of block k are the "critical" rows
 // y_k = A u_k - B y_c (A row-major, lower (tri 0) or upper (tri 1)
@@ -120,5 +121,7 @@ void factorp_solve(const int* stop, FactorP& f, double* v, double* y, cudaStream
 
 // HCAMG_PAPPLY=z keeps the explicit-Z kernels (comparison); default: factor.
 bool factorp_enabled();
+// length of the padded work vectors (whole sweep blocks)
+int64_t factorp_npad(const FactorP& f);
 
 }  // namespace hcamg
