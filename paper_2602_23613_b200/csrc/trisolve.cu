@@ -279,6 +279,7 @@ struct TmaArgs {
   const int64_t* cptr;   // the same batches per CTA in stream order
   const TriBatch* cbat;
   int G, pfd, barmode;
+  int tmem;  // stage the next step's first rows in tensor memory across the barrier
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -297,6 +298,38 @@ __device__ __forceinline__ unsigned long long gtime() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+// tensor memory (TMEM) as a second staging level: a warp's 32 lanes x 4
+// columns of 32 bits hold one 64-column chunk of a row (lane l: doubles 2l, 2l+1)
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, double2 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+               "r"((uint32_t)__double2loint(v.x)), "r"((uint32_t)__double2hiint(v.x)),
+               "r"((uint32_t)__double2loint(v.y)), "r"((uint32_t)__double2hiint(v.y))
+               : "memory");
+}
+__device__ __forceinline__ double2 tmem_ld4(uint32_t taddr) {
+  uint32_t r0, r1, r2, r3;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return make_double2(__hiloint2double((int)r1, (int)r0), __hiloint2double((int)r3, (int)r2));
+}
+// dot of n chunks held in TMEM (chunk q at column col + 4 q) with x, in smem_dot's order
+__device__ __forceinline__ double tmem_dot(uint32_t taddr, const double* x, int n, int lane) {
+  double acc0 = 0.0, acc1 = 0.0;
+  const double2* xp = reinterpret_cast<const double2*>(x + 2 * lane);
+  for (int q = 0; q < n; ++q) {
+    const double2 v = tmem_ld4(taddr + 4 * q), xv = xp[32 * q];
+    acc0 = fma(v.x, xv.x, acc0);
+    acc1 = fma(v.y, xv.y, acc1);
+  }
+  double acc = acc0 + acc1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
 template <int kCons>
 __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;" ::"r"(32 * kCons) : "memory"); }
 
@@ -367,7 +400,15 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
       sinfo[d][1] = b1 - b0;
     }
   };
+  __shared__ uint32_t s_tmem;
+  const bool use_tmem = A.tmem && kCons == 16;
+  if (use_tmem && warp == 1) {  // 512 columns = one 2048-column row per consumer warp (4 per lane quadrant)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 0) {  // producer: the warp loads 32 batch descriptors at a time, lane 0 issues
     // the CTA's batches in order are cbat[cptr[c] .. cptr[c+1]); batch i + pfd is
     // prefetched into L2 when batch i enters the ring (a second lookahead level
@@ -418,6 +459,9 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
   const int cw = warp - 1, ct = threadIdx.x - 32;
   unsigned old = 0;
   int64_t nb = 0;
+  // this warp's TMEM columns: lane quadrant warp % 4, 128 columns (32 chunks) each
+  const uint32_t tb = use_tmem ? s_tmem + ((uint32_t)(32 * (warp % 4)) << 16) + 128u * (uint32_t)(cw / 4) : 0u;
+  bool staged = false;  // the warp's first row of this step is already in TMEM (and counted for its batch)
   // per step: task descriptors, batch descriptors and the step record in shared memory,
   // loaded before the grid barrier (none of them depends on it)
   unsigned long long tt[5] = {0, 0, 0, 0, 0}, tp = A.trace ? gtime() : 0;
@@ -446,6 +490,19 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
     // each warp takes the step's tasks round-robin and waits only for the batch
     // holding its task; the last task finished in a batch frees its buffer
     for (int64_t i = cw; i < nt; i += kCons) {
+      if (staged && i == cw) {  // staged across the barrier: operator row from TMEM
+        const TriTask& T = desc[i];
+        const int na = T.ja1 - T.ja0;
+        double r;
+        if (T.b < 0) r = tmem_dot(tb, sy + 64 * T.ja0, na, lane);
+        else r = tmem_dot(tb, su + 64 * T.ja0, na, lane) - tmem_dot(tb + 4 * na, sy + 64 * T.jb0, T.jb1 - T.jb0, lane);
+        __syncwarp();
+        if (lane == 0) {
+          if (T.b < 0) a.u[T.out] = sold[i] - r;
+          else a.y[T.out] = r;
+        }
+        continue;
+      }
       const int q = sbidx[d][i];
       const int64_t g = nb + q;  // global batch number of this CTA
       const int s = (int)(g % kNBuf);
@@ -482,6 +539,45 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
     if (ct == 0 && a.dbg != 1) {
       const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
       asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(a.bar), "r"(inc) : "memory");
+    }
+    // between arrive and wait: copy this warp's first row of the next step from
+    // the ring into TMEM when its batch is one of the first kNBuf (those arrive
+    // without any release) -- fully staged batches free their slots, so the
+    // producer streams further into the next step across the barrier
+    staged = false;
+    if (use_tmem) {
+      const int64_t st1 = st + 1;
+      const int d1 = (int)(st1 & 1);
+      mbar_wait(smem_u32(dfull + d1), (uint32_t)((st1 >> 1) & 1));
+      if (cw < sinfo[d1][0]) {
+        const int q = sbidx[d1][cw];
+        const TriTask& T = sdesc[d1 * kMaxCtaTasks + cw];
+        const int na = T.ja1 - T.ja0, nbb = T.b < 0 ? 0 : T.jb1 - T.jb0;
+        if (q < kNBuf && na + nbb <= 32) {
+          const int64_t g = nb + q;
+          const int sl = (int)(g % kNBuf);
+          const unsigned rnd = (unsigned)(g / kNBuf);
+          while (*reinterpret_cast<volatile unsigned*>(&sgen[sl]) < rnd) __nanosleep(20);
+          mbar_wait(smem_u32(bars + sl), rnd & 1);
+          const TriBatch& B = sbat[d1][q];
+          const unsigned char* bb = buf + (size_t)sl * kBufB - B.off;
+          const double2* ra = reinterpret_cast<const double2*>(bb + 8 * (T.a + 64 * T.ja0)) + lane;
+          for (int k = 0; k < na; ++k) tmem_st4(tb + 4 * k, ra[32 * k]);
+          if (nbb) {
+            const double2* rb = reinterpret_cast<const double2*>(bb + 8 * (T.b + 64 * T.jb0)) + lane;
+            for (int k = 0; k < nbb; ++k) tmem_st4(tb + 4 * (na + k), rb[32 * k]);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          __syncwarp();
+          if (lane == 0 && atomicAdd(&sdone[d1][q], 1u) + 1 == (unsigned)(B.t1 - B.t0)) {
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bars + kNBuf + sl)) : "memory");
+            atomicAdd(&sgen[sl], 1u);
+          }
+          staged = true;
+        }
+      }
+    }
+    if (ct == 0 && a.dbg != 1) {
       unsigned cur;
       if (A.barmode == 1) {  // relaxed polling, one acquire fence after
         do {
@@ -504,6 +600,12 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
   }
   if (A.trace && ct == 0)
     for (int k = 0; k < 5; ++k) A.trace[c * 8 + k] += tt[k];
+  if (use_tmem) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    cons_sync<kCons>();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem));
+  }
 }
 
 struct CopyJob {
@@ -651,7 +753,7 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
       trace = nullptr;
     }
     TmaArgs A{a, a.dbg == 3 ? trace : nullptr, sw.ctask.p, sw.bptr.p, sw.batches.p, sw.cptr.p, sw.cbat.p, sw.G,
-              env("HCAMG_TRI_L2PF", 2), env("HCAMG_TRI_BAR", 0)};
+              env("HCAMG_TRI_L2PF", 2), env("HCAMG_TRI_BAR", 0), env("HCAMG_TRI_TMEM", 0)};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)sw.G);
     cfg.blockDim = dim3(32 * (2 + (cons == 12 ? 12 : 16)));

@@ -121,8 +121,9 @@ def test_apply_p_matches_exported_p(pair, which):
 
 
 def test_sweep_kernels_bit_identical(pair, monkeypatch):
-    """The three sweep kernels (grid-barrier steps, dataflow, TMA-streamed)
-    compute every row dot in the same order: P e and P^T r agree bit for bit."""
+    """The three sweep kernels (grid-barrier steps, dataflow, TMA-streamed, the
+    latter also with TMEM staging) compute every row dot in the same order:
+    P e and P^T r agree bit for bit."""
     from paper_2602_23613_b200 import _lib
 
     field, s, hf, hz = pair
@@ -132,11 +133,12 @@ def test_sweep_kernels_bit_identical(pair, monkeypatch):
     e = rng.uniform(-1, 1, nc)
     r = rng.uniform(-1, 1, n)
     res = {}
-    for kern in ("0", "1", "2"):
-        monkeypatch.setenv("HCAMG_TRI_KERNEL", kern)
+    for kern in ("0", "1", "2", "2t"):  # 2t: TMA kernel with TMEM staging across the barrier
+        monkeypatch.setenv("HCAMG_TRI_KERNEL", kern[0])
+        monkeypatch.setenv("HCAMG_TRI_TMEM", "1" if kern.endswith("t") else "0")
         pe, pt = np.zeros(n), np.zeros(nc)
         dev.check(dev.lib.hcamg_debug_apply_p(dev.h, 0, 0, _lib.ptr(e), _lib.ptr(pe)))
         dev.check(dev.lib.hcamg_debug_apply_p(dev.h, 0, 1, _lib.ptr(r), _lib.ptr(pt)))
         res[kern] = (pe, pt)
-    for kern in ("0", "1"):
+    for kern in ("0", "1", "2t"):
         assert np.array_equal(res[kern][0], res["2"][0]) and np.array_equal(res[kern][1], res["2"][1]), kern
