@@ -49,6 +49,21 @@ def measured_peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
+def coarse_symv(n, nranks=1):
+    """The single-GPU coarsest solve of n >= 8192 reads the packed lower
+    triangle of the inverse (csrc/symv.cu) unless HCAMG_COARSE_SYMV=0."""
+    return nranks == 1 and n >= int(os.environ.get("HCAMG_COARSE_GEMV_MIN", "8192")) and \
+        os.environ.get("HCAMG_COARSE_SYMV", "1") != "0"
+
+
+def sym_packed_bytes(n):
+    """Bytes of the packed triangle (32 x 32 sub-tiles, 4 x 4 per item, full
+    diagonal sub-tiles) plus its row/column partials written and read back."""
+    nb = -(-n // 128)
+    items = nb * (nb + 1) // 2
+    return 8 * 1024 * (16 * (items - nb) + 10 * nb) + 4 * 8 * 128 * items
+
+
 def algorithmic_bytes(h, moved=False):
     """B_iter of SURVEY.md §8(d): bytes one PCG iteration must move, whatever
     the implementation.  B(M) = 12 nnz + 4 (rows + 1); B(P) = min(CSR, hybrid
@@ -65,7 +80,7 @@ def algorithmic_bytes(h, moved=False):
         info = lv._info
         n = int(info.n)
         if info.coarsest:
-            total += 2 * 8 * n * (n + 1) // 2
+            total += sym_packed_bytes(n) if moved and coarse_symv(n) else 2 * 8 * n * (n + 1) // 2
             continue
         A = lv.A
         colnnz = np.diff(A.tocsc().indptr)
@@ -182,7 +197,7 @@ def kernel_roofline(h, reps=None, rank=0, nranks=1):
             nbytes = B(int(info.nnz_P), n) + 8 * (n + nc)
     elif pc == 2:
         rows = n if nranks == 1 or n < 8192 else (n * (rank + 1) // nranks - n * rank // nranks)
-        nbytes = 8 * rows * n + 16 * n
+        nbytes = (sym_packed_bytes(n) if coarse_symv(n, nranks) else 8 * rows * n) + 16 * n
     else:
         A = lv.A
         colnnz = np.diff(A.tocsc().indptr)

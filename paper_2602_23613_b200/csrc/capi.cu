@@ -165,6 +165,8 @@ void factor_coarsest(hcamg_handle* h, DevLevel& L, const DCsr& M) {
   L.Ainv.alloc(n * n, s);
   dense_spd_inverse(h->cublas, D.p, n, L.Ainv.p, s);
   st.mark("  coarsest: inverse");
+  if (n >= coarse_gemv_min() && !(getenv("HCAMG_COARSE_SYMV") && atoi(getenv("HCAMG_COARSE_SYMV")) == 0))
+    symv_build(L.Ainv.p, n, L.Asym, s);
 }
 
 void finish_level(hcamg_handle* h, DevLevel& L) {

@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "giant.cuh"
+#include "symv.cuh"
 #include "split.cuh"
 #include "sweep.cuh"
 
@@ -73,6 +74,7 @@ struct DevLevel {
   std::vector<int64_t> gc_cols;
   bool coarsest = false;
   DBuf<double> Ainv;     // coarsest: dense inverse (row-major n x n)
+  SymPacked Asym;        // coarsest: its lower triangle (single-GPU GEMV reading it once)
   SegPlan pt_seg;        // segmented restriction plan when P^T has long rows
   HybridP hp;            // dense-regime interpolation block (P/Pt then hold the sparse part)
   // distributed solve (dist.cuh): context and exchange-site offsets of this level

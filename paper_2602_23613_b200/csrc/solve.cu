@@ -613,6 +613,10 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     return 0;
   if (pc == PC_COARSE) {
     if (!n) return 0;
+    if (n >= coarse_gemv_min() && !xd && L.Asym.on) {  // lower triangle read once (symv.cu)
+      symv_apply(stop, L.Asym, b, x, s);
+      return 2;
+    }
     if (n >= coarse_gemv_min()) {
       require(!xd || L.xoff_c != DevLevel::kNoSite, "distributed layout is stale (call hcamg_dist_prepare again)");
       dense_gemv_rows(stop, n, n, L.Ainv.p, b, x, s, L.dist, L.xoff_c, part);

@@ -44,6 +44,9 @@ def explicit_z(monkeypatch):
     # single-GPU V-cycle on the same representation (the single-GPU default
     # applies A_GG^{-1} through the factor, tests/test_gpu_factor_sweep.py)
     monkeypatch.setenv("HCAMG_PAPPLY", "z")
+    # likewise the coarsest inverse: the row-partitioned solve streams the full
+    # matrix; the single-GPU default reads its lower triangle (test_gpu_symv.py)
+    monkeypatch.setenv("HCAMG_COARSE_SYMV", "0")
 
 
 @pytest.fixture(scope="module")
