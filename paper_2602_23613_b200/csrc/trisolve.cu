@@ -280,6 +280,7 @@ struct TmaArgs {
   const TriBatch* cbat;
   int G, pfd, barmode;
   int tmem;  // stage the next step's first rows in tensor memory across the barrier
+  unsigned long long* tl;  // HCAMG_TRI_DBG=4: per step and CTA, tasks done / barrier passed (globaltimer)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -452,6 +453,7 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
       mbar_wait(smem_u32(dempty + d), (r & 1) ^ 1);
       load_desc(st, lane, 32);
       __syncwarp();
+
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(dfull + d)) : "memory");
     }
     return;
@@ -464,11 +466,11 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
   bool staged = false;  // the warp's first row of this step is already in TMEM (and counted for its batch)
   // per step: task descriptors, batch descriptors and the step record in shared memory,
   // loaded before the grid barrier (none of them depends on it)
-  unsigned long long tt[5] = {0, 0, 0, 0, 0}, tp = A.trace ? gtime() : 0;
+  unsigned long long tp = A.trace ? gtime() : 0;
   auto mark = [&](int k) {
     if (A.trace && ct == 0) {
       const unsigned long long n = gtime();
-      tt[k] += n - tp;
+      A.trace[c * 8 + k] += n - tp;
       tp = n;
     }
   };
@@ -479,12 +481,29 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
     const TriStepD S = sstep[d];
     const int64_t nt = sinfo[d][0], nbat = sinfo[d][1];
     const TriTask* desc = sdesc + d * kMaxCtaTasks;
-    for (int t = ct; t < kNB; t += 32 * kCons) {
-      su[t] = __ldcg(a.u + (int64_t)S.k * kNB + t);
-      sy[t] = S.c >= 0 ? __ldcg(a.y + (int64_t)S.c * kNB + t) : 0.0;
+    {  // u_k, y_c and the fold targets' values: every load issued before any is used (one L2 round trip)
+      constexpr int kPer = (kNB + 32 * kCons - 1) / (32 * kCons);
+      const bool hv = ct < nt && desc[ct].b < 0;
+      const double ov = hv ? __ldcg(a.u + desc[ct].out) : 0.0;
+      double uu[kPer], yy[kPer];
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int t = ct + q * 32 * kCons;
+        uu[q] = t < kNB ? __ldcg(a.u + (int64_t)S.k * kNB + t) : 0.0;
+        yy[q] = t < kNB && S.c >= 0 ? __ldcg(a.y + (int64_t)S.c * kNB + t) : 0.0;
+      }
+      if (hv) sold[ct] = ov;
+      for (int64_t i = ct + 32 * kCons; i < nt; i += 32 * kCons)
+        if (desc[i].b < 0) sold[i] = __ldcg(a.u + desc[i].out);
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int t = ct + q * 32 * kCons;
+        if (t < kNB) {
+          su[t] = uu[q];
+          sy[t] = yy[q];
+        }
+      }
     }
-    for (int64_t i = ct; i < nt; i += 32 * kCons)
-      if (desc[i].b < 0) sold[i] = __ldcg(a.u + desc[i].out);
     cons_sync<kCons>();
     mark(1);
     // each warp takes the step's tasks round-robin and waits only for the batch
@@ -532,6 +551,7 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
     }
     nb += nbat;
     mark(2);
+    if (A.tl && ct == 0) A.tl[(st * G + c) * 2] = gtime();
     if (st + 1 == a.nstep) break;
     cons_sync<kCons>();  // every row of the step written, its descriptors no longer read
     if (ct == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(dempty + d)) : "memory");
@@ -597,9 +617,8 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
     }
     cons_sync<kCons>();  // every consumer past the grid barrier
     mark(4);
+    if (A.tl && ct == 0) A.tl[(st * G + c) * 2 + 1] = gtime();
   }
-  if (A.trace && ct == 0)
-    for (int k = 0; k < 5; ++k) A.trace[c * 8 + k] += tt[k];
   if (use_tmem) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     cons_sync<kCons>();
@@ -753,7 +772,13 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
       trace = nullptr;
     }
     TmaArgs A{a, a.dbg == 3 ? trace : nullptr, sw.ctask.p, sw.bptr.p, sw.batches.p, sw.cptr.p, sw.cbat.p, sw.G,
-              env("HCAMG_TRI_L2PF", 2), env("HCAMG_TRI_BAR", 0), env("HCAMG_TRI_TMEM", 0)};
+              env("HCAMG_TRI_L2PF", 2), env("HCAMG_TRI_BAR", 0), env("HCAMG_TRI_TMEM", 0), nullptr};
+    DBuf<unsigned long long> tl;
+    if (a.dbg == 4) {  // timeline dump (not graph-capturable): HCAMG_TRI_DUMP.<n>.bin
+      tl.alloc(2 * sw.nstep * sw.G, s);
+      tl.zero();
+      A.tl = tl.p;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)sw.G);
     cfg.blockDim = dim3(32 * (2 + (cons == 12 ? 12 : 16)));
@@ -770,6 +795,32 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
     else if (sw.nbuf == 2) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16, 2>, A));
     else if (sw.nbuf == 3) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16, 3>, A));
     else HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16, 4>, A));
+    if (A.tl) {
+      static int seq = 0;
+      HC_CUDA(cudaStreamSynchronize(s));
+      std::vector<unsigned long long> ht((size_t)tl.n);
+      std::vector<int64_t> ct((size_t)sw.ctask.n), bp((size_t)sw.bptr.n);
+      std::vector<TriBatch> bt((size_t)sw.batches.n);
+      HC_CUDA(cudaMemcpy(ht.data(), tl.p, 8 * ht.size(), cudaMemcpyDeviceToHost));
+      HC_CUDA(cudaMemcpy(ct.data(), sw.ctask.p, 8 * ct.size(), cudaMemcpyDeviceToHost));
+      HC_CUDA(cudaMemcpy(bp.data(), sw.bptr.p, 8 * bp.size(), cudaMemcpyDeviceToHost));
+      HC_CUDA(cudaMemcpy(bt.data(), sw.batches.p, sizeof(TriBatch) * bt.size(), cudaMemcpyDeviceToHost));
+      const char* base = getenv("HCAMG_TRI_DUMP");
+      const std::string fn = std::string(base ? base : "tri_timeline") + "." + std::to_string(seq++) + ".bin";
+      if (FILE* f = fopen(fn.c_str(), "wb")) {  // nstep, G, then per (step, cta): t_done, t_pass, tasks, bytes
+        const int64_t hdr[2] = {sw.nstep, sw.G};
+        fwrite(hdr, 8, 2, f);
+        for (int64_t st = 0; st < sw.nstep; ++st)
+          for (int c = 0; c < sw.G; ++c) {
+            int64_t by = 0;
+            for (int64_t q = bp[(size_t)(st * sw.G + c)]; q < bp[(size_t)(st * sw.G + c + 1)]; ++q) by += bt[(size_t)q].bytes;
+            const int64_t rec[4] = {(int64_t)ht[(size_t)(st * sw.G + c) * 2], (int64_t)ht[(size_t)(st * sw.G + c) * 2 + 1],
+                                    ct[(size_t)(st * (sw.G + 1) + c + 1)] - ct[(size_t)(st * (sw.G + 1) + c)], by};
+            fwrite(rec, 8, 4, f);
+          }
+        fclose(f);
+      }
+    }
     return;
   }
   if (kern == 1) {
