@@ -265,9 +265,9 @@ __global__ void __launch_bounds__(512, 1) k_tri_flow(FlowArgs F) {
 // shared memory (same order as the other kernels: bit-identical), and write
 // all outputs at the end of the step.
 
-constexpr int kRingB = (kNB == 512 ? 192 : kNB == 1024 ? 184 : 168) * 1024, kMaxCtaTasks = 256,
+constexpr int kRingB = (kNB == 512 ? 192 : kNB == 1024 ? 184 : 168) * 1024, kMaxCtaTasks = 352,
               kMaxCtaBatches = 64;
-constexpr size_t kTmaSmem = 2 * kNB * 8 + (size_t)kRingB + (size_t)kMaxCtaTasks * (2 * sizeof(TriTask) + 16) +
+constexpr size_t kTmaSmem = 2 * kNB * 8 + (size_t)kRingB + (size_t)kMaxCtaTasks * (2 * sizeof(TriTask) + 8) +
                             (2 * 8 + 4) * 8;
 
 struct TmaArgs {
@@ -362,8 +362,7 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
   unsigned char* buf = smem + 2 * kNB * 8;
   TriTask* sdesc = reinterpret_cast<TriTask*>(buf + (size_t)kRingB);
   double* sold = reinterpret_cast<double*>(sdesc + 2 * kMaxCtaTasks);  // fold targets' values
-  double* sres = sold + kMaxCtaTasks;                              // row dots
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sres + kMaxCtaTasks);  // full[kNBuf], empty[kNBuf], dfull[2], dempty[2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sold + kMaxCtaTasks);  // full[kNBuf], empty[kNBuf], dfull[2], dempty[2]
   uint64_t* dfull = bars + 2 * kNBuf;
   uint64_t* dempty = dfull + 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -728,6 +727,13 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
   TriArgs a{stop, sw.nstep, sw.steps.p, sw.tasks.p, sw.pool.p, u, y, bar, std::max(1, env("HCAMG_TRI_PF", 1)),
             env("HCAMG_TRI_PFMODE", 2), env("HCAMG_TRI_DBG", 0)};
   const int kern = env("HCAMG_TRI_KERNEL", 2);
+  if (kern == 2 && !(sw.max_cta_tasks <= kMaxCtaTasks && sw.max_cta_batches <= kMaxCtaBatches)) {
+    static bool warned = false;
+    if (!warned)
+      fprintf(stderr, "[hcamg] sweep partition exceeds the TMA kernel's per-CTA limits (%d tasks, %d batches); "
+                      "using the grid-barrier sweep kernel\n", sw.max_cta_tasks, sw.max_cta_batches);
+    warned = true;
+  }
   if (kern == 2 && sw.G > 0 && sw.max_cta_tasks <= kMaxCtaTasks && sw.max_cta_batches <= kMaxCtaBatches &&
       (env("HCAMG_TRI_CONS", 16) != 12 || sw.nbuf == 4)) {
     const int cons = env("HCAMG_TRI_CONS", 16);
@@ -933,33 +939,58 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
       const TriTask& x = tasks[(size_t)t];
       return 512 * (int64_t)(x.ja1 - x.ja0 + (x.b < 0 ? 0 : x.jb1 - x.jb0));
     };
+    int64_t taskw = kTaskW;
     auto tcost = [&](int64_t t) {  // partition weight: bytes (crit rows scaled) + a per-row cost
       const int64_t b = tbytes(t);
-      return (tasks[(size_t)t].b < 0 ? b : b * kCritPct / 100) + kTaskW;
+      return (tasks[(size_t)t].b < 0 ? b : b * kCritPct / 100) + taskw;
     };
     auto tstart = [&](int64_t t) { return 8 * (tasks[(size_t)t].a + 64 * tasks[(size_t)t].ja0); };
     int maxt = 0, maxb = 0;
     for (const TriStepD& d : steps) {
-      int64_t total = 0;
-      for (int64_t t = d.t0; t < d.t1; ++t) total += tcost(t);
-      int64_t acc = 0, t = d.t0;
-      for (int c = 0; c < G; ++c) {
-        ct.push_back(t);
-        const int64_t target = c + 1 == G ? INT64_MAX : total * (c + 1) / G;
-        const int64_t c0 = t;
-        while (t < d.t1 && (c + 1 == G || (t - c0 < kMaxCtaTasks && acc + tcost(t) / 2 <= target))) acc += tcost(t++);
-        maxt = std::max<int>(maxt, (int)(t - c0));
-        const size_t nb0 = batches.size();
-        for (int64_t b0 = c0; b0 < t;) {
-          int64_t b1 = b0, bytes = 0;
-          while (b1 < t && bytes + tbytes(b1) <= slotb) bytes += tbytes(b1++);
-          batches.push_back(TriBatch{b0, b1, tstart(b0), bytes});
-          b0 = b1;
+      // a step whose partition exceeds the kernel's per-CTA limits (the last CTA
+      // takes the remainder) is re-cut with a heavier per-row weight, which
+      // spreads the many short fold rows more evenly
+      std::vector<int64_t> sct;
+      std::vector<TriBatch> sbat;
+      std::vector<int64_t> sbn;
+      for (int attempt = 0;; ++attempt) {
+        sct.clear();
+        sbat.clear();
+        sbn.clear();
+        int st_maxt = 0, st_maxb = 0;
+        int64_t total = 0;
+        for (int64_t t = d.t0; t < d.t1; ++t) total += tcost(t);
+        int64_t acc = 0, t = d.t0;
+        for (int c = 0; c < G; ++c) {
+          sct.push_back(t);
+          const int64_t target = c + 1 == G ? INT64_MAX : total * (c + 1) / G;
+          const int64_t c0 = t;
+          while (t < d.t1 && (c + 1 == G || (t - c0 < kMaxCtaTasks && acc + tcost(t) / 2 <= target))) acc += tcost(t++);
+          st_maxt = std::max<int>(st_maxt, (int)(t - c0));
+          const size_t nb0 = sbat.size();
+          for (int64_t b0 = c0; b0 < t;) {
+            int64_t b1 = b0, bytes = 0;
+            while (b1 < t && bytes + tbytes(b1) <= slotb) bytes += tbytes(b1++);
+            sbat.push_back(TriBatch{b0, b1, tstart(b0), bytes});
+            b0 = b1;
+          }
+          st_maxb = std::max<int>(st_maxb, (int)(sbat.size() - nb0));
+          sbn.push_back((int64_t)sbat.size());
         }
-        maxb = std::max<int>(maxb, (int)(batches.size() - nb0));
-        bptr.push_back((int64_t)batches.size());
+        const bool fits = st_maxt <= kMaxCtaTasks && st_maxb <= kMaxCtaBatches;
+        if (fits || attempt == 40) {
+          maxt = std::max(maxt, st_maxt);
+          maxb = std::max(maxb, st_maxb);
+          break;
+        }
+        taskw = taskw * 5 / 4 + 256;
       }
+      taskw = kTaskW;
+      const int64_t nb0 = (int64_t)batches.size();
+      for (int64_t x : sct) ct.push_back(x);
       ct.push_back(d.t1);
+      for (const TriBatch& b : sbat) batches.push_back(b);
+      for (int64_t x : sbn) bptr.push_back(nb0 + x);
     }
     {
       std::vector<int64_t> cptr(1, 0);
