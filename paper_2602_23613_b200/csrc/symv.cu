@@ -107,9 +107,26 @@ __global__ void k_symv_reduce(const int* stop, int64_t n, int nb, const double* 
   if (*stop) return;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     const int bi = (int)(j / kR), o = (int)(j % kR);
+    // loads in groups of 8 (independent), added in order
     double s = 0.0;
-    for (int q = 0; q <= bi; ++q) s += rowpart[(int64_t)item_of(bi, q) * kR + o];
-    for (int q = bi; q < nb; ++q) s += colpart[(int64_t)item_of(q, bi) * kR + o];
+    const double* rp = rowpart + (int64_t)item_of(bi, 0) * kR + o;  // items (bi, 0..bi) are consecutive
+    for (int q0 = 0; q0 <= bi; q0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = q0 + u <= bi ? __ldcs(rp + (int64_t)(q0 + u) * kR) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + u <= bi) s += v[u];
+    }
+    for (int q0 = bi; q0 < nb; q0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = q0 + u < nb ? __ldcs(colpart + (int64_t)item_of(q0 + u, bi) * kR + o) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (q0 + u < nb) s += v[u];
+    }
     x[j] = s;
   }
 }
@@ -162,7 +179,7 @@ void symv_apply(const int* stop, const SymPacked& sp, const double* b, double* x
   k_symv_items<<<(unsigned)sp.grid, kSymThreads, 0, s>>>(stop, sp.n, sp.nb, sp.items, sp.val.p, sp.ioff.p, b,
                                                          sp.rowpart.p, sp.colpart.p);
   HC_CHECK_LAUNCH();
-  k_symv_reduce<<<grid_for(sp.n, 256), 256, 0, s>>>(stop, sp.n, sp.nb, sp.rowpart.p, sp.colpart.p, x);
+  k_symv_reduce<<<grid_for(sp.n, 128), 128, 0, s>>>(stop, sp.n, sp.nb, sp.rowpart.p, sp.colpart.p, x);
   HC_CHECK_LAUNCH();
 }
 
