@@ -61,13 +61,15 @@ def test_vcycle_symmetric(c2):
     assert bx @ x > 0 and by @ y > 0
 
 
-def test_pcg_converges_and_is_deterministic(c2):
+def test_pcg_converges_and_is_deterministic(c2, capfd):
     s, h = c2
     b = kuhn.rhs(s.n, seed=0)
     x1, r1 = P.pcg(s.A, b, precond=lambda r: P.vcycle(h, r), tol=1e-8)
     x2, r2 = P.pcg(s.A, b, precond=lambda r: P.vcycle(h, r), tol=1e-8)
     assert r1.converged and r1.iterations <= 15 and r1.residual_history[-1] <= 1e-8
     assert np.array_equal(x1, x2) and r1.iterations == r2.iterations
+    # the sweeps ran on the TMA-streamed kernel (no fallback to the grid-barrier kernel)
+    assert "exceeds the TMA kernel" not in capfd.readouterr().err
     # the true residual sits at the conditioning floor the reference itself
     # shows on this field (4.6e-5 at n = 8, 1.3e-4 at n = 12)
     assert np.linalg.norm(s.A @ x1 - b) / np.linalg.norm(b) <= 5e-3
