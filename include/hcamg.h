@@ -71,8 +71,10 @@ typedef struct {
   int64_t n_patches, n_patch_entries, n_waves, n_gc_cols, coarsest, n_components, max_component, pad;
   /* dense regime, single GPU: the V-cycle applies A_GG^{-1} through the
    * envelope Cholesky factor (two blocked sweeps of factor_steps steps);
-   * factor_bytes = operator bytes one application reads (0: explicit Z). */
-  int64_t factor_bytes, factor_steps;
+   * factor_bytes = operator bytes one application reads (0: explicit Z);
+   * factor_tma = 1 when both sweeps fit the TMA-streamed kernel's per-CTA
+   * limits (otherwise they run on the grid-barrier kernel). */
+  int64_t factor_bytes, factor_steps, factor_tma;
 } hcamg_level_info;
 
 /* ---- lifetime ---------------------------------------------------------- */

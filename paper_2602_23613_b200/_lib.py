@@ -53,7 +53,7 @@ class LevelInfo(C.Structure):
     _fields_ = [(name, C.c_int64) for name in (
         "n", "nnz_A", "ncols_G", "nnz_G", "nnz_P", "n_pairs", "n_interior", "n_coarse_nodes",
         "n_patches", "n_patch_entries", "n_waves", "n_gc_cols", "coarsest", "n_components",
-        "max_component", "pad", "factor_bytes", "factor_steps")]
+        "max_component", "pad", "factor_bytes", "factor_steps", "factor_tma")]
 
 
 PRECOND_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64, C.c_void_p)

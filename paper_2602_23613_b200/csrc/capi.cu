@@ -661,6 +661,7 @@ int hcamg_level(hcamg_handle* h, int32_t level, hcamg_level_info* o) {
     o->max_component = L.hp.on ? L.hp.nG : 0;
     o->factor_bytes = L.hp.on && L.hp.fac.on ? L.hp.fac.fw.bytes + L.hp.fac.bw.bytes : 0;
     o->factor_steps = L.hp.on && L.hp.fac.on ? L.hp.fac.T : 0;
+    o->factor_tma = L.hp.on && L.hp.fac.on && tri_tma_fits(L.hp.fac.fw) && tri_tma_fits(L.hp.fac.bw);
     o->pad = L.hp.on ? L.P.nnz : 0;  // nnz of the sparse part of a hybrid P
     o->n_pairs = L.split.n_pairs();
     o->n_interior = (int64_t)L.split.interior.size();

@@ -1027,6 +1027,10 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
   HC_CUDA(cudaStreamSynchronize(s));
 }
 
+bool tri_tma_fits(const TriSweep& sw) {
+  return sw.G > 0 && sw.max_cta_tasks <= kMaxCtaTasks && sw.max_cta_batches <= kMaxCtaBatches;
+}
+
 int64_t factorp_npad(const FactorP& f) { return (f.T * kTriNB + kTriSB - 1) / kTriSB * kTriSB; }
 
 bool factorp_enabled() {

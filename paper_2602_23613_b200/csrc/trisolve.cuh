@@ -119,6 +119,9 @@ void factorp_prolong(const int* stop, FactorP& f, const double* e, double* x, cu
 // y = A_GG^{-1} v in factored order (v, y of length T*NB; v is overwritten)
 void factorp_solve(const int* stop, FactorP& f, double* v, double* y, cudaStream_t s);
 
+// the sweep fits the TMA-streamed kernel's per-CTA limits (else: grid-barrier kernel)
+bool tri_tma_fits(const TriSweep& sw);
+
 // HCAMG_PAPPLY=z keeps the explicit-Z kernels (comparison); default: factor.
 bool factorp_enabled();
 // length of the padded work vectors (whole sweep blocks)
