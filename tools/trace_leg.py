@@ -32,3 +32,5 @@ for s in range(W):
     work = t[s, :, 1] - t[s, :, 0]
     nxt = t[s + 1, :, 0].min() if s + 1 < W else t[s, :, 1].max()
     print(f"{s:5d} {(st - t0) / 1e3:9.2f} {work.max() / 1e3:12.2f} {work[: nw // 4].max() / 1e3:14.2f} {work[3 * nw // 4 :].max() / 1e3:13.2f} {(nxt - st) / 1e3:12.2f}")
+if os.environ.get("TRACE_DUMP"):
+    np.save(os.environ["TRACE_DUMP"], t)
