@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
   if (warp == 0) {  // producer: the warp loads 32 batch descriptors at a time, lane 0 issues
     // the CTA's batches in order are cbat[cptr[c] .. cptr[c+1]); batch i + pfd is
     // prefetched into L2 when batch i enters the ring (a second lookahead level
-    // behind the 176 KB ring, across steps and barriers)
+    // behind the 168 KB ring, across steps and barriers)
     int64_t nb = 0;
     const char* pool = reinterpret_cast<const char*>(a.pool);
     const int64_t i0 = A.cptr[c], i1 = A.cptr[c + 1];
@@ -921,7 +921,7 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
     out.nfold.upload(nf.data(), T, s);
     out.flags.alloc((int64_t)steps.size() + T + T * kNB, s);
   }
-  {  // CTA partition (contiguous, balanced by bytes + a per-row cost) and <= 44 KB batches for the TMA kernel
+  {  // CTA partition (contiguous, balanced by bytes + a per-row cost) and <= one-ring-slot batches for the TMA kernel
     const int64_t kTaskW = getenv("HCAMG_TRI_TASKW") ? atoll(getenv("HCAMG_TRI_TASKW")) : 3072;
     const int64_t kCritPct = getenv("HCAMG_TRI_CRITW") ? atoll(getenv("HCAMG_TRI_CRITW")) : 140;
     // ring slots (measured on config 2: 1024-row steps best with 3, 2048-row steps with 2)

@@ -86,7 +86,7 @@ struct TriSweep {
   // TMA-streamed kernel: the tasks of step k for CTA c are contiguous,
   // [ctask[k (G+1) + c], ctask[k (G+1) + c + 1]) (split by bytes), and their
   // rows, one contiguous pool region, are cut into batches
-  // [bptr[k G + c], bptr[k G + c + 1]) of whole tasks, <= 44 KB each
+  // [bptr[k G + c], bptr[k G + c + 1]) of whole tasks, <= one ring slot each
   int G = 0, max_cta_tasks = 0, max_cta_batches = 0, nbuf = 4;
   DBuf<int64_t> ctask, bptr, cptr;
   DBuf<TriBatch> batches, cbat;  // cbat: the batches again, per CTA in stream order ([cptr[c], cptr[c+1]))
