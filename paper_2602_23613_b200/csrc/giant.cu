@@ -838,8 +838,8 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
   }
   const std::vector<uint8_t> hr = rng.download();
   auto ranges = [&](const double* p) -> const uint8_t* { return hr.data() + index.at(p) * kSB * 2; };
-  tri_compact(fs, ranges, f.fw, s);
-  tri_compact(bs, ranges, f.bw, s);
+  tri_compact(fs, ranges, f.fw, s, 0);
+  tri_compact(bs, ranges, f.bw, s, 1);
   if (getenv("HCAMG_SETUP_TIMING"))
     fprintf(stderr, "[hcamg setup]   sweeps: %lld blocks of %lld rows, fwd %.3f GB, bwd %.3f GB\n", (long long)TS,
             (long long)kSB, f.fw.bytes / 1e9, f.bw.bytes / 1e9);

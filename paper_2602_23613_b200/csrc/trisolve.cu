@@ -550,9 +550,15 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
     }
     nb += nbat;
     mark(2);
-    if (A.tl && ct == 0) A.tl[(st * G + c) * 2] = gtime();
-    if (st + 1 == a.nstep) break;
+    if (st + 1 == a.nstep) {
+      if (A.tl) {
+        cons_sync<kCons>();
+        if (ct == 0) A.tl[(st * G + c) * 2] = gtime();
+      }
+      break;
+    }
     cons_sync<kCons>();  // every row of the step written, its descriptors no longer read
+    if (A.tl && ct == 0) A.tl[(st * G + c) * 2] = gtime();  // the CTA's step done
     if (ct == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(dempty + d)) : "memory");
     mark(3);
     if (ct == 0 && a.dbg != 1) {
@@ -717,7 +723,8 @@ void launch_sweep_t(const TriArgs& a, cudaStream_t s) {
   HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_sweep<kThr, kB>, a));
 }
 
-void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double* y, unsigned* bar, cudaStream_t s) {
+void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double* y, unsigned* bar, cudaStream_t s,
+                         unsigned long long* tl_out = nullptr) {
   auto env = [](const char* k, int d) {
     const char* v = getenv(k);
     return v ? atoi(v) : d;
@@ -780,7 +787,9 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
     TmaArgs A{a, a.dbg == 3 ? trace : nullptr, sw.ctask.p, sw.bptr.p, sw.batches.p, sw.cptr.p, sw.cbat.p, sw.G,
               env("HCAMG_TRI_L2PF", 2), env("HCAMG_TRI_BAR", 0), env("HCAMG_TRI_TMEM", 0), nullptr};
     DBuf<unsigned long long> tl;
-    if (a.dbg == 4) {  // timeline dump (not graph-capturable): HCAMG_TRI_DUMP.<n>.bin
+    if (tl_out) {
+      A.tl = tl_out;
+    } else if (a.dbg == 4) {  // timeline dump (not graph-capturable): HCAMG_TRI_DUMP.<n>.bin
       tl.alloc(2 * sw.nstep * sw.G, s);
       tl.zero();
       A.tl = tl.p;
@@ -801,7 +810,7 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
     else if (sw.nbuf == 2) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16, 2>, A));
     else if (sw.nbuf == 3) HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16, 3>, A));
     else HC_CUDA(cudaLaunchKernelEx(&cfg, k_tri_tma<16, 4>, A));
-    if (A.tl) {
+    if (A.tl && !tl_out) {
       static int seq = 0;
       HC_CUDA(cudaStreamSynchronize(s));
       std::vector<unsigned long long> ht((size_t)tl.n);
@@ -857,8 +866,106 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
 
 }  // namespace
 
+// Contiguous CTA partition of every step's tasks and their batches (<= one
+// ring slot) for the TMA kernel.  A task weighs its bytes (critical rows
+// scaled by critpct %) + taskw; CTA c's share of a step's weight is 1/G, or
+// share[k G + c] after calibration (tri_calibrate).  A step whose cut exceeds
+// the kernel's per-CTA limits (the last CTA takes the remainder) is re-cut with
+// a heavier per-row weight, which spreads the many short fold rows.
+void tri_partition(TriSweep& out, cudaStream_t s) {
+  const std::vector<TriTask>& tasks = out.htasks;
+  const int G = out.G;
+  const int64_t slotb = (kRingB / out.nbuf) & ~int64_t(511);
+  auto tbytes = [&](int64_t t) {
+    const TriTask& x = tasks[(size_t)t];
+    return 512 * (int64_t)(x.ja1 - x.ja0 + (x.b < 0 ? 0 : x.jb1 - x.jb0));
+  };
+  int64_t taskw = out.taskw;
+  auto tcost = [&](int64_t t) {
+    const int64_t b = tbytes(t);
+    return (tasks[(size_t)t].b < 0 ? b : b * out.critpct / 100) + taskw;
+  };
+  auto tstart = [&](int64_t t) { return 8 * (tasks[(size_t)t].a + 64 * tasks[(size_t)t].ja0); };
+  std::vector<int64_t> ct, bptr(1, 0);
+  std::vector<TriBatch> batches;
+  out.hcost.assign(out.hsteps.size() * (size_t)G, 0.0);
+  int maxt = 0, maxb = 0;
+  for (size_t k = 0; k < out.hsteps.size(); ++k) {
+    const TriStepD& d = out.hsteps[k];
+    const bool calib = !out.share.empty();
+    std::vector<int64_t> sct, sbn;
+    std::vector<TriBatch> sbat;
+    std::vector<double> scost;
+    for (int attempt = 0;; ++attempt) {
+      sct.clear();
+      sbat.clear();
+      sbn.clear();
+      scost.clear();
+      int st_maxt = 0, st_maxb = 0;
+      int64_t total = 0;
+      for (int64_t t = d.t0; t < d.t1; ++t) total += tcost(t);
+      int64_t acc = 0, t = d.t0;
+      double cum = 0.0;
+      for (int c = 0; c < G; ++c) {
+        sct.push_back(t);
+        cum += calib ? out.share[k * G + c] : 1.0 / G;
+        const int64_t target = c + 1 == G ? INT64_MAX : (int64_t)((double)total * std::min(1.0, cum));
+        const int64_t c0 = t, a0 = acc;
+        while (t < d.t1 && (c + 1 == G || (t - c0 < kMaxCtaTasks && acc + tcost(t) / 2 <= target))) acc += tcost(t++);
+        scost.push_back((double)(acc - a0));
+        st_maxt = std::max<int>(st_maxt, (int)(t - c0));
+        const size_t nb0 = sbat.size();
+        for (int64_t b0 = c0; b0 < t;) {
+          int64_t b1 = b0, bytes = 0;
+          while (b1 < t && bytes + tbytes(b1) <= slotb) bytes += tbytes(b1++);
+          sbat.push_back(TriBatch{b0, b1, tstart(b0), bytes});
+          b0 = b1;
+        }
+        st_maxb = std::max<int>(st_maxb, (int)(sbat.size() - nb0));
+        sbn.push_back((int64_t)sbat.size());
+      }
+      const bool fits = st_maxt <= kMaxCtaTasks && st_maxb <= kMaxCtaBatches;
+      if (fits || attempt == 40) {
+        maxt = std::max(maxt, st_maxt);
+        maxb = std::max(maxb, st_maxb);
+        break;
+      }
+      taskw = taskw * 5 / 4 + 256;
+    }
+    // each CTA's weight under the base model (what the calibration rescales)
+    taskw = out.taskw;
+    for (int c = 0; c < G; ++c) {
+      const int64_t e = c + 1 < G ? sct[(size_t)c + 1] : d.t1;
+      double w = 0.0;
+      for (int64_t t = sct[(size_t)c]; t < e; ++t) w += (double)tcost(t);
+      out.hcost[k * G + c] = w;
+    }
+    const int64_t nb0 = (int64_t)batches.size();
+    for (int64_t x : sct) ct.push_back(x);
+    ct.push_back(d.t1);
+    for (const TriBatch& b : sbat) batches.push_back(b);
+    for (int64_t x : sbn) bptr.push_back(nb0 + x);
+  }
+  std::vector<int64_t> cptr(1, 0);
+  std::vector<TriBatch> cbat;
+  for (int c = 0; c < G; ++c) {
+    for (size_t k = 0; k < out.hsteps.size(); ++k)
+      for (int64_t q = bptr[k * G + c]; q < bptr[k * G + c + 1]; ++q) cbat.push_back(batches[(size_t)q]);
+    cptr.push_back((int64_t)cbat.size());
+  }
+  out.cptr.upload(cptr.data(), (int64_t)cptr.size(), s);
+  if (cbat.empty()) cbat.push_back(TriBatch{});
+  out.cbat.upload(cbat.data(), (int64_t)cbat.size(), s);
+  out.max_cta_tasks = maxt;
+  out.max_cta_batches = maxb;
+  out.ctask.upload(ct.data(), (int64_t)ct.size(), s);
+  out.bptr.upload(bptr.data(), (int64_t)bptr.size(), s);
+  if (batches.empty()) batches.push_back(TriBatch{});
+  out.batches.upload(batches.data(), (int64_t)batches.size(), s);
+}
+
 void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const uint8_t*(const double*)>& ranges,
-                 TriSweep& out, cudaStream_t s) {
+                 TriSweep& out, cudaStream_t s, int dir) {
   std::vector<TriStepD> steps;
   std::vector<TriTask> tasks;
   std::vector<CopyJob> jobs;
@@ -921,97 +1028,30 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
     out.nfold.upload(nf.data(), T, s);
     out.flags.alloc((int64_t)steps.size() + T + T * kNB, s);
   }
-  {  // CTA partition (contiguous, balanced by bytes + a per-row cost) and <= one-ring-slot batches for the TMA kernel
-    const int64_t kTaskW = getenv("HCAMG_TRI_TASKW") ? atoll(getenv("HCAMG_TRI_TASKW")) : 3072;
-    const int64_t kCritPct = getenv("HCAMG_TRI_CRITW") ? atoll(getenv("HCAMG_TRI_CRITW")) : 140;
+  {  // CTA partition and batches for the TMA kernel (tri_partition)
+    // (HCAMG_TRI_TASKW / HCAMG_TRI_CRITW, and *_BW for the backward sweep: measurement knobs)
+    auto knob = [&](const char* k, int64_t d) {
+      const std::string kb = std::string(k) + "_BW";
+      const char* v = dir == 1 && getenv(kb.c_str()) ? getenv(kb.c_str()) : getenv(k);
+      return v ? atoll(v) : d;
+    };
+    out.taskw = knob("HCAMG_TRI_TASKW", 3072);
+    out.critpct = knob("HCAMG_TRI_CRITW", 140);
     // ring slots (measured on config 2: 1024-row steps best with 3, 2048-row steps with 2)
-  const int nbuf = getenv("HCAMG_TRI_SLOTS") ? atoi(getenv("HCAMG_TRI_SLOTS")) : (kNB >= 2048 ? 2 : 3);
+    const int nbuf = getenv("HCAMG_TRI_SLOTS") ? atoi(getenv("HCAMG_TRI_SLOTS")) : (kNB >= 2048 ? 2 : 3);
     require(nbuf >= 2 && nbuf <= 8 && nbuf != 5 && nbuf != 7, "HCAMG_TRI_SLOTS must be 2, 3, 4, 6 or 8");
-    const int64_t slotb = (kRingB / nbuf) & ~int64_t(511);
     out.nbuf = nbuf;
     int dev = 0, sms = kSMs;
     HC_CUDA(cudaGetDevice(&dev));
     HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    const int G = sms;
-    std::vector<int64_t> ct, bptr(1, 0);
-    std::vector<TriBatch> batches;
-    auto tbytes = [&](int64_t t) {
-      const TriTask& x = tasks[(size_t)t];
-      return 512 * (int64_t)(x.ja1 - x.ja0 + (x.b < 0 ? 0 : x.jb1 - x.jb0));
-    };
-    int64_t taskw = kTaskW;
-    auto tcost = [&](int64_t t) {  // partition weight: bytes (crit rows scaled) + a per-row cost
-      const int64_t b = tbytes(t);
-      return (tasks[(size_t)t].b < 0 ? b : b * kCritPct / 100) + taskw;
-    };
-    auto tstart = [&](int64_t t) { return 8 * (tasks[(size_t)t].a + 64 * tasks[(size_t)t].ja0); };
-    int maxt = 0, maxb = 0;
-    for (const TriStepD& d : steps) {
-      // a step whose partition exceeds the kernel's per-CTA limits (the last CTA
-      // takes the remainder) is re-cut with a heavier per-row weight, which
-      // spreads the many short fold rows more evenly
-      std::vector<int64_t> sct;
-      std::vector<TriBatch> sbat;
-      std::vector<int64_t> sbn;
-      for (int attempt = 0;; ++attempt) {
-        sct.clear();
-        sbat.clear();
-        sbn.clear();
-        int st_maxt = 0, st_maxb = 0;
-        int64_t total = 0;
-        for (int64_t t = d.t0; t < d.t1; ++t) total += tcost(t);
-        int64_t acc = 0, t = d.t0;
-        for (int c = 0; c < G; ++c) {
-          sct.push_back(t);
-          const int64_t target = c + 1 == G ? INT64_MAX : total * (c + 1) / G;
-          const int64_t c0 = t;
-          while (t < d.t1 && (c + 1 == G || (t - c0 < kMaxCtaTasks && acc + tcost(t) / 2 <= target))) acc += tcost(t++);
-          st_maxt = std::max<int>(st_maxt, (int)(t - c0));
-          const size_t nb0 = sbat.size();
-          for (int64_t b0 = c0; b0 < t;) {
-            int64_t b1 = b0, bytes = 0;
-            while (b1 < t && bytes + tbytes(b1) <= slotb) bytes += tbytes(b1++);
-            sbat.push_back(TriBatch{b0, b1, tstart(b0), bytes});
-            b0 = b1;
-          }
-          st_maxb = std::max<int>(st_maxb, (int)(sbat.size() - nb0));
-          sbn.push_back((int64_t)sbat.size());
-        }
-        const bool fits = st_maxt <= kMaxCtaTasks && st_maxb <= kMaxCtaBatches;
-        if (fits || attempt == 40) {
-          maxt = std::max(maxt, st_maxt);
-          maxb = std::max(maxb, st_maxb);
-          break;
-        }
-        taskw = taskw * 5 / 4 + 256;
-      }
-      taskw = kTaskW;
-      const int64_t nb0 = (int64_t)batches.size();
-      for (int64_t x : sct) ct.push_back(x);
-      ct.push_back(d.t1);
-      for (const TriBatch& b : sbat) batches.push_back(b);
-      for (int64_t x : sbn) bptr.push_back(nb0 + x);
-    }
-    {
-      std::vector<int64_t> cptr(1, 0);
-      std::vector<TriBatch> cbat;
-      for (int c = 0; c < G; ++c) {
-        for (size_t k = 0; k < steps.size(); ++k)
-          for (int64_t q = bptr[k * G + c]; q < bptr[k * G + c + 1]; ++q) cbat.push_back(batches[(size_t)q]);
-        cptr.push_back((int64_t)cbat.size());
-      }
-      out.cptr.upload(cptr.data(), (int64_t)cptr.size(), s);
-      out.cbat.upload(cbat.data(), (int64_t)cbat.size(), s);
-    }
-    out.G = G;
-    out.max_cta_tasks = maxt;
-    out.max_cta_batches = maxb;
+    out.G = sms;
+    out.htasks = tasks;
+    out.hsteps = steps;
+    out.share.clear();
+    tri_partition(out, s);
     if (getenv("HCAMG_SETUP_TIMING"))
-      fprintf(stderr, "[hcamg setup]   sweep: %lld steps, %lld tasks, %zu batches, max %d tasks per CTA step\n",
-              (long long)steps.size(), (long long)tasks.size(), batches.size(), maxt);
-    out.ctask.upload(ct.data(), (int64_t)ct.size(), s);
-    out.bptr.upload(bptr.data(), (int64_t)bptr.size(), s);
-    out.batches.upload(batches.data(), (int64_t)batches.size(), s);
+      fprintf(stderr, "[hcamg setup]   sweep: %zu steps, %zu tasks, max %d tasks / %d batches per CTA step\n",
+              steps.size(), tasks.size(), out.max_cta_tasks, out.max_cta_batches);
   }
   out.T = T;
   out.ntask = (int64_t)tasks.size();
@@ -1024,6 +1064,81 @@ void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const u
   dj.upload(jobs.data(), (int64_t)jobs.size(), s);
   if (!jobs.empty()) k_compact_copy<<<grid_for((int64_t)jobs.size() * 32, 256), 256, 0, s>>>(dj.p, (int64_t)jobs.size(), out.pool.p);
   HC_CHECK_LAUNCH();
+  HC_CUDA(cudaStreamSynchronize(s));
+}
+
+// Calibrate the TMA sweep's CTA partition on the device.  A step ends when its
+// slowest CTA arrives at the grid barrier, and which CTA that is depends less on
+// its bytes than on how much it could stream ahead during the previous barrier
+// -- a pattern that repeats run to run (per-(step, CTA) work correlates 0.99
+// between runs).  Each round times every (step, CTA) (one launch with the
+// timeline stamps) and moves weight from the slow CTAs of a step to the fast
+// ones (share *= (mean / own work)^0.8, damped); the best of the rounds is
+// kept.  Only the assignment of rows to CTAs changes, never a row's dot
+// order, so results are bit-identical whatever the partition.
+// HCAMG_TRI_CALIB = rounds (0: off).
+void tri_calibrate(TriSweep& sw, double* u, double* y, unsigned* bar, int rounds, cudaStream_t s) {
+  if (rounds <= 0 || sw.nstep < 3 || !tri_tma_fits(sw) || sw.htasks.empty()) return;
+  const char* ke = getenv("HCAMG_TRI_KERNEL");
+  if (ke && atoi(ke) != 2) return;
+  const int G = sw.G;
+  const int64_t K = sw.nstep;
+  DBuf<int> stop(1, s);
+  stop.zero();
+  DBuf<unsigned long long> tl(2 * K * G, s);
+  std::vector<unsigned long long> h((size_t)(2 * K * G));
+  std::vector<double> best_share = sw.share;
+  double best = 1e300;
+  const double alpha = getenv("HCAMG_TRI_CALIB_ALPHA") ? atof(getenv("HCAMG_TRI_CALIB_ALPHA")) : 0.8;
+  for (int r = 0; r <= rounds; ++r) {
+    if (!tri_tma_fits(sw)) break;
+    for (int rep = 0; rep < 2; ++rep) {
+      tl.zero();
+      launch_sweep_kernel(stop.p, sw, u, y, bar, s, tl.p);
+    }
+    HC_CUDA(cudaStreamSynchronize(s));
+    HC_CUDA(cudaMemcpy(h.data(), tl.p, 8 * h.size(), cudaMemcpyDeviceToHost));
+    auto done = [&](int64_t k, int c) { return (double)h[(size_t)(k * G + c) * 2]; };
+    auto pass = [&](int64_t k, int c) { return (double)h[(size_t)(k * G + c) * 2 + 1]; };
+    double t0 = 1e300, t1 = 0;
+    for (int c = 0; c < G; ++c) {
+      t0 = std::min(t0, pass(0, c));
+      t1 = std::max(t1, done(K - 1, c));
+    }
+    const double span = t1 - t0;
+    if (getenv("HCAMG_SETUP_TIMING"))
+      fprintf(stderr, "[hcamg setup]   sweep calibration round %d: %.1f us for steps 1..%lld\n", r, span / 1e3,
+              (long long)(K - 1));
+    if (span < best) {
+      best = span;
+      best_share = sw.share;
+    }
+    if (r == rounds) break;
+    std::vector<double> ns((size_t)(K * G));
+    for (int64_t k = 0; k < K; ++k) {
+      double tot = 0.0;
+      for (int c = 0; c < G; ++c) tot += sw.hcost[(size_t)(k * G + c)];
+      std::vector<double> w((size_t)G);
+      double wbar = 0.0;
+      for (int c = 0; c < G; ++c) {
+        w[(size_t)c] = k == 0 ? 1.0 : std::max(1.0, done(k, c) - pass(k - 1, c));
+        wbar += w[(size_t)c] / G;
+      }
+      double sum = 0.0;
+      for (int c = 0; c < G; ++c) {
+        const double base = std::max(sw.hcost[(size_t)(k * G + c)] / std::max(tot, 1.0), 1e-4 / G);
+        ns[(size_t)(k * G + c)] = base * std::pow(wbar / w[(size_t)c], alpha);
+        sum += ns[(size_t)(k * G + c)];
+      }
+      for (int c = 0; c < G; ++c) ns[(size_t)(k * G + c)] /= sum;
+    }
+    sw.share = ns;
+    tri_partition(sw, s);
+  }
+  if (best_share != sw.share) {
+    sw.share = best_share;
+    tri_partition(sw, s);
+  }
   HC_CUDA(cudaStreamSynchronize(s));
 }
 
@@ -1056,6 +1171,12 @@ void factorp_attach(FactorP& f, const DCsr& W, const int32_t* mpos, const int32_
   f.v2.zero();
   f.bar.alloc(1, s);
   f.bar.zero();
+  const int rounds = getenv("HCAMG_TRI_CALIB") ? atoi(getenv("HCAMG_TRI_CALIB")) : 4;
+  tri_calibrate(f.fw, f.v0.p, f.v1.p, f.bar.p, rounds, s);
+  tri_calibrate(f.bw, f.v1.p, f.v2.p, f.bar.p, rounds, s);
+  f.v0.zero();
+  f.v1.zero();
+  f.v2.zero();
   f.on = true;
 }
 

@@ -90,12 +90,19 @@ struct TriSweep {
   int G = 0, max_cta_tasks = 0, max_cta_batches = 0, nbuf = 4;
   DBuf<int64_t> ctask, bptr, cptr;
   DBuf<TriBatch> batches, cbat;  // cbat: the batches again, per CTA in stream order ([cptr[c], cptr[c+1]))
+  // host copies for re-partitioning (tri_partition / tri_calibrate): the tasks and
+  // steps, the partition weights, per-(step, CTA) shares (empty: 1/G) and the
+  // weight each CTA got
+  std::vector<TriTask> htasks;
+  std::vector<TriStepD> hsteps;
+  int64_t taskw = 3072, critpct = 140;
+  std::vector<double> share, hcost;
 };
 
 // Compact the source blocks into a sweep.  ranges(p) returns the host copy of
 // the row-range table (kTriSB x {j0, j1}, 64-column chunks) of the block at p.
 void tri_compact(const std::vector<TriSrcStep>& src, const std::function<const uint8_t*(const double*)>& ranges,
-                 TriSweep& out, cudaStream_t s);
+                 TriSweep& out, cudaStream_t s, int dir);  // dir: 0 forward, 1 backward sweep
 
 struct FactorP {
   bool on = false;
@@ -121,6 +128,10 @@ void factorp_solve(const int* stop, FactorP& f, double* v, double* y, cudaStream
 
 // the sweep fits the TMA-streamed kernel's per-CTA limits (else: grid-barrier kernel)
 bool tri_tma_fits(const TriSweep& sw);
+// (re)build the CTA partition and batches from the host copies (uses sw.share when set)
+void tri_partition(TriSweep& sw, cudaStream_t s);
+// time the sweep per (step, CTA) and re-partition to balance the CTAs (rounds; see trisolve.cu)
+void tri_calibrate(TriSweep& sw, double* u, double* y, unsigned* bar, int rounds, cudaStream_t s);
 
 // HCAMG_PAPPLY=z keeps the explicit-Z kernels (comparison); default: factor.
 bool factorp_enabled();

@@ -10,4 +10,5 @@ for _ in range(3):
     dev.check(dev.lib.hcamg_debug_apply_p(dev.h, 0, 0, _lib.ptr(e), _lib.ptr(out)))
 os.environ["HCAMG_TRI_DBG"] = "4"
 os.environ["HCAMG_TRI_DUMP"] = "gpurun_out/tl"
-dev.check(dev.lib.hcamg_debug_apply_p(dev.h, 0, 0, _lib.ptr(e), _lib.ptr(out)))
+for _ in range(int(os.environ.get("TL_REPS", "1"))):
+    dev.check(dev.lib.hcamg_debug_apply_p(dev.h, 0, 0, _lib.ptr(e), _lib.ptr(out)))
