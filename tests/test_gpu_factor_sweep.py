@@ -142,3 +142,14 @@ def test_sweep_kernels_bit_identical(pair, monkeypatch):
         res[kern] = (pe, pt)
     for kern in ("0", "1", "2t"):
         assert np.array_equal(res[kern][0], res["2"][0]) and np.array_equal(res[kern][1], res["2"][1]), kern
+
+
+def test_calibrated_partition_bit_identical(pair, monkeypatch):
+    """The setup calibration (tri_calibrate) only moves rows between CTAs: a
+    hierarchy built without it applies the V-cycle bit for bit the same."""
+    field, s, hf, hz = pair
+    monkeypatch.setenv("HCAMG_TRI_CALIB", "0")
+    h0 = _build(s, "factor")
+    monkeypatch.delenv("HCAMG_TRI_CALIB")
+    b = np.random.default_rng(13).uniform(-1, 1, s.n)
+    assert np.array_equal(P.vcycle(h0, b), P.vcycle(hf, b))
