@@ -170,8 +170,14 @@ def kernel_roofline(h, reps=None, rank=0, nranks=1):
     nl = np.zeros(cap, np.int64)
     cnt = C.c_int32()
     big = h.levels[0].n > 100000
-    dev.check(dev.lib.hcamg_profile_vcycle(dev.h, reps or (5 if big else 50), cap, _lib.ptr(kind), _lib.ptr(level),
-                                           _lib.ptr(us), _lib.ptr(nl), C.byref(cnt)))
+    # three trials of back-to-back launches per piece; per piece the fastest
+    # trial's average (a trial can catch a transient slowdown of the box)
+    best = None
+    for _ in range(3):
+        dev.check(dev.lib.hcamg_profile_vcycle(dev.h, reps or (5 if big else 50), cap, _lib.ptr(kind),
+                                               _lib.ptr(level), _lib.ptr(us), _lib.ptr(nl), C.byref(cnt)))
+        best = us.copy() if best is None else np.minimum(best, us)
+    us[:] = best
     k = cnt.value
     i = int(np.argmax(us[:k]))
     ell, pc = int(level[i]), int(kind[i])
