@@ -1,6 +1,7 @@
 // Blocked triangular sweeps over the envelope Cholesky factor of A_GG, and
 // the factored interpolation block built on them (see trisolve.cuh).
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <string>
 
