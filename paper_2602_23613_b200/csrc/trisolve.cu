@@ -282,6 +282,7 @@ struct TmaArgs {
   int G, pfd, barmode;
   int tmem;  // stage the next step's first rows in tensor memory across the barrier
   unsigned long long* tl;  // HCAMG_TRI_DBG=4: per step and CTA, tasks done / barrier passed (globaltimer)
+  long long* tlb;          // HCAMG_TRI_DBG=4: batches of later steps already issued to the ring, at done / at pass
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -402,6 +403,8 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
     }
   };
   __shared__ uint32_t s_tmem;
+  __shared__ long long s_issued;  // (HCAMG_TRI_DBG=4) batches the producer has issued
+  if (threadIdx.x == 0) s_issued = 0;
   const bool use_tmem = A.tmem && kCons == 16;
   if (use_tmem && warp == 1) {  // 512 columns = one 2048-column row per consumer warp (4 per lane quadrant)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)));
@@ -440,6 +443,7 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
                            smem_u32(buf + (size_t)s * kBufB)),
                        "l"(pool + off), "r"((uint32_t)bytes), "r"(full)
                        : "memory");
+          if (A.tlb) *reinterpret_cast<volatile long long*>(&s_issued) = nb + 1;
         }
         __syncwarp();
       }
@@ -560,6 +564,7 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
     }
     cons_sync<kCons>();  // every row of the step written, its descriptors no longer read
     if (A.tl && ct == 0) A.tl[(st * G + c) * 2] = gtime();  // the CTA's step done
+    if (A.tlb && ct == 0) A.tlb[(st * G + c) * 2] = *reinterpret_cast<volatile long long*>(&s_issued) - nb;
     if (ct == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(dempty + d)) : "memory");
     mark(3);
     if (ct == 0 && a.dbg != 1) {
@@ -624,6 +629,7 @@ __global__ void __launch_bounds__(32 * (2 + kCons), 1) k_tri_tma(TmaArgs A) {
     cons_sync<kCons>();  // every consumer past the grid barrier
     mark(4);
     if (A.tl && ct == 0) A.tl[(st * G + c) * 2 + 1] = gtime();
+    if (A.tlb && ct == 0) A.tlb[(st * G + c) * 2 + 1] = *reinterpret_cast<volatile long long*>(&s_issued) - nb;
   }
   if (use_tmem) {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -786,14 +792,18 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
       trace = nullptr;
     }
     TmaArgs A{a, a.dbg == 3 ? trace : nullptr, sw.ctask.p, sw.bptr.p, sw.batches.p, sw.cptr.p, sw.cbat.p, sw.G,
-              env("HCAMG_TRI_L2PF", 2), env("HCAMG_TRI_BAR", 0), env("HCAMG_TRI_TMEM", 0), nullptr};
+              env("HCAMG_TRI_L2PF", 2), env("HCAMG_TRI_BAR", 0), env("HCAMG_TRI_TMEM", 0), nullptr, nullptr};
     DBuf<unsigned long long> tl;
+    DBuf<long long> tlb;
     if (tl_out) {
       A.tl = tl_out;
     } else if (a.dbg == 4) {  // timeline dump (not graph-capturable): HCAMG_TRI_DUMP.<n>.bin
       tl.alloc(2 * sw.nstep * sw.G, s);
       tl.zero();
       A.tl = tl.p;
+      tlb.alloc(2 * sw.nstep * sw.G, s);
+      tlb.zero();
+      A.tlb = tlb.p;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)sw.G);
@@ -823,6 +833,12 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
       HC_CUDA(cudaMemcpy(bt.data(), sw.batches.p, sizeof(TriBatch) * bt.size(), cudaMemcpyDeviceToHost));
       const char* base = getenv("HCAMG_TRI_DUMP");
       const std::string fn = std::string(base ? base : "tri_timeline") + "." + std::to_string(seq++) + ".bin";
+      std::vector<long long> hb((size_t)tlb.n);
+      HC_CUDA(cudaMemcpy(hb.data(), tlb.p, 8 * hb.size(), cudaMemcpyDeviceToHost));
+      if (FILE* fb = fopen((fn + ".bank").c_str(), "wb")) {  // per (step, cta): batches issued ahead at done, at pass
+        fwrite(hb.data(), 8, hb.size(), fb);
+        fclose(fb);
+      }
       if (FILE* f = fopen(fn.c_str(), "wb")) {  // nstep, G, then per (step, cta): t_done, t_pass, tasks, bytes
         const int64_t hdr[2] = {sw.nstep, sw.G};
         fwrite(hdr, 8, 2, f);
