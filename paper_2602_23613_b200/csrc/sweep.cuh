@@ -81,6 +81,7 @@ struct LegArgs {
   double* dj;
   unsigned* gbar;     // grid-barrier word (cooperative leg only)
   long long* trace;   // optional: per (phase, warp) [start, arrive] globaltimer stamps
+  int l2pf;           // grid leg: L2-prefetch the static data of the wave this many waves ahead (0: off)
 };
 void launch_leg(bool down, const LegArgs& args, cudaStream_t s);
 // whole-GPU cooperative variant (grid.sync between wavefronts)

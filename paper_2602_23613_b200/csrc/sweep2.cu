@@ -137,6 +137,38 @@ __device__ __forceinline__ double overflow_dot(const int32_t* rng, const int32_t
   return acc;
 }
 
+__device__ __forceinline__ void pf_l2(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+
+// L2 prefetch of everything static that phase `dst` (a patch of this warp, the
+// pulled row of this thread) will load: on the wide levels the leg's static
+// data (~230 MB on config 2) does not survive the dense sweeps in L2, so
+// without it every phase's coefficient loads are HBM misses after the barrier.
+__device__ __forceinline__ void l2_prefetch_phase(const LegArgs& a, int dir, int64_t p, bool own, int64_t t,
+                                                  int lane) {
+  if (p >= 0) {
+    pf_l2(a.pbinv + p * 256 + (lane & 15) * 16);  // 2 KB inverse: 16 lines
+    if (own) {
+      if (lane < kSlots) pf_l2(a.ogv + (((int64_t)dir * a.m + p) * kSlots + lane) * 16);
+      else if (lane < kSlots + (kSlots + 1) / 2)
+        pf_l2(a.ogc + (((int64_t)dir * a.m + p) * kSlots + 2 * (lane - kSlots)) * 16);
+      else if (lane == 31) pf_l2(a.ocnt + (int64_t)dir * a.m * 16 + p * 16);
+    }
+    if (lane == 30) pf_l2(a.pdof + p * 16);
+  }
+  if (t >= 0) {
+    const int64_t ng = a.ng[dir];
+    pf_l2(a.gu[dir] + t);
+    pf_l2(a.gcnt[dir] + t);
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) {
+      pf_l2(a.ggc[dir] + (int64_t)j * ng + t);
+      pf_l2(a.ggv[dir] + (int64_t)j * ng + t);
+    }
+  }
+}
+
 // one patch solve from prefetched structure
 __device__ __forceinline__ void solve_patch(const LegArgs& a, int dir, const PatchPre& q, int lane, bool init_x,
                                             const double* vin, const double* dsrc, double* ddst) {
@@ -305,6 +337,19 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
       if (t < g1) load_row(a, dir, t, rq);
     }
   };
+  auto l2pf = [&](int64_t s) {
+    if (!kGrid || s >= W) return;
+    const int64_t dst = kDown ? s : W - 1 - s;
+    int64_t p = wp[dst] + wg, t = -1;
+    if (p >= wp[dst + 1]) p = -1;
+    if (s > 0) {
+      const int64_t src = kDown ? s - 1 : dst + 1;
+      t = gp[src] + (nth - 1 - gtid);
+      if (t >= gp[src + 1]) t = -1;
+    }
+    l2_prefetch_phase(a, dir, p, s > 0, t, lane);
+  };
+  for (int64_t s = 1; s <= a.l2pf; ++s) l2pf(s);
   if (W > 0) prefetch(0);
   if (kDown) {
     for (int64_t u = gtid; u < n; u += nth) {
@@ -321,6 +366,7 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
   };
   for (int64_t s = 0; s < W; ++s) {
     stamp(s, 0);
+    if (a.l2pf > 0 && s > 0) l2pf(s + a.l2pf);
     const int64_t dst = kDown ? s : W - 1 - s;
     const int64_t src = kDown ? s - 1 : dst + 1;
     const double* dsrc = s > 0 ? ((src & 1) ? dbuf1 : dbuf0) : nullptr;
@@ -752,8 +798,12 @@ void launch_leg_grid(bool down, const LegArgs& args, cudaStream_t s) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (down) HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<true, true>, args));
-  else HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<false, true>, args));
+  // HCAMG_LEG_L2PF: L2 prefetch distance in waves (0: off)
+  static const int l2pf = getenv("HCAMG_LEG_L2PF") ? std::max(0, atoi(getenv("HCAMG_LEG_L2PF"))) : 1;
+  LegArgs ga = args;
+  ga.l2pf = l2pf;
+  if (down) HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<true, true>, ga));
+  else HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<false, true>, ga));
 }
 
 void launch_leg(bool down, const LegArgs& args, cudaStream_t s) {
