@@ -102,32 +102,39 @@ __global__ void __launch_bounds__(kSymThreads) k_symv_items(const int* stop, int
 }
 
 // x[j] = sum over bj <= bi of rowpart(bi, bj)[o] + sum over bi' >= bi of colpart(bi', bi)[o]
-__global__ void k_symv_reduce(const int* stop, int64_t n, int nb, const double* __restrict__ rowpart,
-                              const double* __restrict__ colpart, double* __restrict__ x) {
+// The nb + 1 terms of a row are split into kParts contiguous runs, one thread
+// each (32 consecutive rows per warp: coalesced, and one bi per warp since
+// 32 | kR), each run summed in order, then the runs in order: a fixed order,
+// so results are bit-identical run to run.  One thread per row was
+// latency-bound (~26 dependent L2 round trips).
+constexpr int kParts = 8;
+__global__ void __launch_bounds__(32 * kParts) k_symv_reduce(const int* stop, int64_t n, int nb,
+                                                             const double* __restrict__ rowpart,
+                                                             const double* __restrict__ colpart,
+                                                             double* __restrict__ x) {
   if (*stop) return;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    const int bi = (int)(j / kR), o = (int)(j % kR);
-    // loads in groups of 8 (independent), added in order
-    double s = 0.0;
+  __shared__ double part[kParts][32];
+  const int lane = threadIdx.x & 31, p = threadIdx.x >> 5;
+  const int64_t j = blockIdx.x * 32LL + lane;
+  const int bi = (int)((blockIdx.x * 32LL) / kR), o = (int)(j % kR);
+  const int T = nb + 1;  // bi + 1 row terms, then nb - bi column terms
+  const int t0 = (int)((int64_t)T * p / kParts), t1 = (int)((int64_t)T * (p + 1) / kParts);
+  double s = 0.0;
+  if (j < n) {
     const double* rp = rowpart + (int64_t)item_of(bi, 0) * kR + o;  // items (bi, 0..bi) are consecutive
-    for (int q0 = 0; q0 <= bi; q0 += 8) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = q0 + u <= bi ? __ldcs(rp + (int64_t)(q0 + u) * kR) : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (q0 + u <= bi) s += v[u];
+#pragma unroll 8
+    for (int t = t0; t < t1; ++t) {
+      const double v = t <= bi ? __ldcs(rp + (int64_t)t * kR) : __ldcs(colpart + (int64_t)item_of(t - 1, bi) * kR + o);
+      s += v;
     }
-    for (int q0 = bi; q0 < nb; q0 += 8) {
-      double v[8];
+  }
+  part[p][lane] = s;
+  __syncthreads();
+  if (p == 0 && j < n) {
+    double r = part[0][lane];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        v[u] = q0 + u < nb ? __ldcs(colpart + (int64_t)item_of(q0 + u, bi) * kR + o) : 0.0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (q0 + u < nb) s += v[u];
-    }
-    x[j] = s;
+    for (int q = 1; q < kParts; ++q) r += part[q][lane];
+    x[j] = r;
   }
 }
 
@@ -179,7 +186,7 @@ void symv_apply(const int* stop, const SymPacked& sp, const double* b, double* x
   k_symv_items<<<(unsigned)sp.grid, kSymThreads, 0, s>>>(stop, sp.n, sp.nb, sp.items, sp.val.p, sp.ioff.p, b,
                                                          sp.rowpart.p, sp.colpart.p);
   HC_CHECK_LAUNCH();
-  k_symv_reduce<<<grid_for(sp.n, 128), 128, 0, s>>>(stop, sp.n, sp.nb, sp.rowpart.p, sp.colpart.p, x);
+  k_symv_reduce<<<(unsigned)((sp.n + 31) / 32), 32 * kParts, 0, s>>>(stop, sp.n, sp.nb, sp.rowpart.p, sp.colpart.p, x);
   HC_CHECK_LAUNCH();
 }
 
