@@ -676,21 +676,22 @@ __global__ void k_fp_scatter_sub(const int* stop, int64_t nG, const int32_t* __r
 }
 
 // kSub = false: y[i] = M[i,:] x (rows >= nrows up to npad get 0);
-// kSub = true:  y[i] -= M[i,:] x.   Warp per row, fixed order.
-template <bool kSub>
+// kSub = true:  y[i] -= M[i,:] x.   kL lanes per row (32 / kL rows per warp:
+// W' has a handful of entries per row), fixed order.
+template <bool kSub, int kL = 32>
 __global__ void k_fp_spmv(const int* stop, int64_t nrows, int64_t npad, const int64_t* __restrict__ mp,
                           const int32_t* __restrict__ mi, const double* __restrict__ mv, const double* __restrict__ x,
                           double* __restrict__ y) {
   if (*stop) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & (kL - 1);
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kL;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) / kL;
   for (int64_t i = w0; i < npad; i += nw) {
     double acc = 0.0;
     if (i < nrows)
-      for (int64_t e = mp[i] + lane; e < mp[i + 1]; e += 32) acc = fma(mv[e], x[mi[e]], acc);
+      for (int64_t e = mp[i] + lane; e < mp[i + 1]; e += kL) acc = fma(mv[e], x[mi[e]], acc);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int o = kL / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, kL);
     if (lane == 0) {
       if (kSub) y[i] -= acc;
       else y[i] = acc;
@@ -792,7 +793,7 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
       trace = nullptr;
     }
     TmaArgs A{a, a.dbg == 3 ? trace : nullptr, sw.ctask.p, sw.bptr.p, sw.batches.p, sw.cptr.p, sw.cbat.p, sw.G,
-              env("HCAMG_TRI_L2PF", 2), env("HCAMG_TRI_BAR", 0), env("HCAMG_TRI_TMEM", 0), nullptr, nullptr};
+              env("HCAMG_TRI_L2PF", 2), env("HCAMG_TRI_BAR", 0), env("HCAMG_TRI_TMEM", 1), nullptr, nullptr};
     DBuf<unsigned long long> tl;
     DBuf<long long> tlb;
     if (tl_out) {
@@ -1214,7 +1215,7 @@ void factorp_restrict(const int* stop, FactorP& f, const double* r, double* bc, 
 
 void factorp_prolong(const int* stop, FactorP& f, const double* e, double* x, cudaStream_t s) {
   const int64_t npad = factorp_npad(f);
-  k_fp_spmv<false><<<grid_for(npad * 32, 256), 256, 0, s>>>(stop, f.nG, npad, f.Wp.ptr.p, f.Wp.idx.p, f.Wp.val.p, e,
+  k_fp_spmv<false, 8><<<grid_for(npad * 8, 256), 256, 0, s>>>(stop, f.nG, npad, f.Wp.ptr.p, f.Wp.idx.p, f.Wp.val.p, e,
                                                             f.v0.p);
   HC_CHECK_LAUNCH();
   factorp_solve(stop, f, f.v0.p, f.v2.p, s);
