@@ -793,7 +793,7 @@ void launch_sweep_kernel(const int* stop, const TriSweep& sw, double* u, double*
       trace = nullptr;
     }
     TmaArgs A{a, a.dbg == 3 ? trace : nullptr, sw.ctask.p, sw.bptr.p, sw.batches.p, sw.cptr.p, sw.cbat.p, sw.G,
-              env("HCAMG_TRI_L2PF", 2), env("HCAMG_TRI_BAR", 0), env("HCAMG_TRI_TMEM", 1), nullptr, nullptr};
+              env("HCAMG_TRI_L2PF", 1), env("HCAMG_TRI_BAR", 0), env("HCAMG_TRI_TMEM", 1), nullptr, nullptr};
     DBuf<unsigned long long> tl;
     DBuf<long long> tlb;
     if (tl_out) {
