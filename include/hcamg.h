@@ -84,6 +84,21 @@ const char* hcamg_last_error(const hcamg_handle* h);
 int64_t hcamg_error_index(const hcamg_handle* h);
 int hcamg_version(void);
 
+/* ---- per-handle options ------------------------------------------------
+ * Select code paths per handle (they seed from the HCAMG_* environment at
+ * hcamg_create).  Keys: "sweep" (smoothing leg: 0 auto, 1 cluster leg, 2 grid
+ * leg, 3 one launch per wavefront, 4 dataflow), "giant_min" (dense-regime
+ * cutoff, reference transfer.py:35 _DENSE_COMPONENT_CUTOFF = 4096),
+ * "coarse_gemv_min" (coarsest solve streams its inverse from this size on),
+ * "coarse_symv" (packed-triangle coarsest solve), "galerkin_fp64" (dense-regime
+ * Galerkin correction term in fp64), "factor_apply" (apply the dense
+ * interpolation block through the envelope factor, 0 = explicit Z),
+ * "form_z" (keep the explicit Z block), "tri_calib" (sweep calibration rounds).
+ * Setting an option drops the recorded solve graphs; setup options apply to
+ * the next hcamg_setup_*.  Unknown keys: HCAMG_EINVAL. */
+int hcamg_set_option(hcamg_handle* h, const char* key, double value);
+int hcamg_get_option(hcamg_handle* h, const char* key, double* value);
+
 /* ---- setup: build_hierarchy (multilevel.py:78-164) ---------------------- */
 /* method "alg": splitting.py:246-298 + transfer.py:77-122 per level. */
 int hcamg_setup_alg(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* G, int32_t max_levels,
@@ -152,6 +167,26 @@ int hcamg_kuhn_export(hcamg_handle* h, int64_t* a_ptr, int32_t* a_idx, double* a
 int hcamg_export_patches(hcamg_handle* h, int32_t level, int64_t* ptr, int64_t* dofs, int64_t* wave);
 int hcamg_export_coarse_cols(hcamg_handle* h, int32_t level, int64_t* cols);
 
+/* coarsest level's solve (sparse.py:304-321 solve(factor, b)): x = A_c^{-1} b
+ * for host vectors of the coarsest size; HCAMG_EINVAL on any other level. */
+int hcamg_coarse_solve(hcamg_handle* h, int32_t level, const double* b, double* x);
+
+/* The coarse level's Cholesky factor as the reference's CholeskyFactor holds
+ * it (sparse.py:146-165, 276-301): ordering = reverse Cuthill-McKee
+ * permutation (n), factor = dense lower L (n x n row-major) with
+ * L L^T = A[ordering][:, ordering].  Either pointer may be NULL. */
+int hcamg_cholesky_factor(hcamg_handle* h, int32_t level, int64_t* ordering, double* factor);
+
+/* ---- OSS-l1 smoother (smoothers.py:60-137) ------------------------------
+ * hcamg_smoother_setup: build_patches + build_l1_jacobi for one operator
+ * (A, G_level) into the handle (replacing any hierarchy; the handle then only
+ * smooths).  hcamg_smooth: smooth(A, patches, l1, x, b, direction) of level
+ * `level` (0 on a smoother handle); direction 0 forward, 1 backward,
+ * 2 symmetric; x NULL = zeros; out = the new iterate. */
+int hcamg_smoother_setup(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* G);
+int hcamg_smooth(hcamg_handle* h, int32_t level, int32_t direction, const double* x_or_null, const double* b,
+                 double* out);
+
 /* ---- solve ------------------------------------------------------------- */
 /* vcycle(h, b, x=None) (multilevel.py:187-196): out = x + V(b - A x), or V(b). */
 int hcamg_vcycle(hcamg_handle* h, const double* b, const double* x_or_null, double* out);
@@ -163,9 +198,13 @@ int hcamg_pcg(hcamg_handle* h, const double* b, const double* x0_or_null, double
 int hcamg_amg_solve(hcamg_handle* h, const double* b, const double* x0_or_null, double tol, int64_t maxit,
                     double* x, double* history, hcamg_report* report);
 /* Device-resident variant of hcamg_pcg: b, x0, x are device pointers on the
- * handle's device; no host synchronisation when report == NULL. */
+ * handle's device; no host synchronisation when report == NULL -- breakdown
+ * and peer errors are then deferred to hcamg_solve_status. */
 int hcamg_pcg_device(hcamg_handle* h, const double* d_b, const double* d_x0_or_null, double tol,
                      int64_t maxit, double* d_x, hcamg_report* report);
+/* Report and status of the last PCG / AMG solve on the handle (synchronises):
+ * HCAMG_EBREAKDOWN or HCAMG_ECUDA if it broke down or a peer timed out. */
+int hcamg_solve_status(hcamg_handle* h, hcamg_report* report);
 /* Kernel launches recorded in the last PCG / V-cycle graph (gpu_launches). */
 int64_t hcamg_graph_launches(hcamg_handle* h, int32_t which /* 0 vcycle, 1 pcg init, 2 pcg body */);
 /* Time each piece of the V-cycle alone (warm, CUDA events on the handle's

@@ -27,6 +27,8 @@ EXPORTS = [
     "hcamg_vcycle", "hcamg_pcg", "hcamg_amg_solve", "hcamg_pcg_device", "hcamg_graph_launches",
     "hcamg_stream", "hcamg_pcg_generic", "hcamg_spmv", "hcamg_profile_vcycle", "hcamg_export_dense", "hcamg_component_solve", "hcamg_kuhn_assemble", "hcamg_kuhn_export", "hcamg_split_alg", "hcamg_split_export",
     "hcamg_dist_prepare", "hcamg_dist_connect", "hcamg_dist_connect_ptrs", "hcamg_dist_disconnect", "hcamg_dist_info",
+    "hcamg_set_option", "hcamg_get_option", "hcamg_coarse_solve", "hcamg_solve_status", "hcamg_cholesky_factor",
+    "hcamg_smoother_setup", "hcamg_smooth",
 ]
 
 
@@ -115,6 +117,13 @@ def load(required=True):
         "hcamg_dist_connect_ptrs": (C.c_int, [P, P]),
         "hcamg_dist_disconnect": (C.c_int, [P]),
         "hcamg_dist_info": (C.c_int, [P, P, P, P, P]),
+        "hcamg_set_option": (C.c_int, [P, C.c_char_p, C.c_double]),
+        "hcamg_get_option": (C.c_int, [P, C.c_char_p, C.POINTER(C.c_double)]),
+        "hcamg_coarse_solve": (C.c_int, [P, C.c_int32, P, P]),
+        "hcamg_solve_status": (C.c_int, [P, C.POINTER(Report)]),
+        "hcamg_cholesky_factor": (C.c_int, [P, C.c_int32, P, P]),
+        "hcamg_smoother_setup": (C.c_int, [P, C.POINTER(CSR), C.POINTER(CSR)]),
+        "hcamg_smooth": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P]),
         # debug entry points (not in the public header)
         "hcamg_debug_dist_piece": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, P, P]),
         "hcamg_debug_apply_p": (C.c_int, [P, C.c_int32, C.c_int32, P, P]),

@@ -24,6 +24,8 @@ using namespace hcamg;
 
 namespace {
 
+constexpr int kSmootherOnly = 3;  // hcamg_info.method of a hcamg_smoother_setup handle
+
 struct Graph {
   cudaGraphExec_t exec = nullptr;
   cudaGraphExec_t pre = nullptr, body = nullptr;  // host-driven fallback
@@ -66,6 +68,9 @@ struct hcamg_handle {
   // last hcamg_kuhn_assemble result (kuhn.cuh)
   DCsr kuhn_A, kuhn_G;
   std::vector<int64_t> kuhn_fe, kuhn_fv;
+  // per-handle options (hcamg_set_option) and private allocation pool
+  Options opts;
+  cudaMemPool_t pool = nullptr;
 };
 
 namespace {
@@ -165,8 +170,7 @@ void factor_coarsest(hcamg_handle* h, DevLevel& L, const DCsr& M) {
   L.Ainv.alloc(n * n, s);
   dense_spd_inverse(h->cublas, D.p, n, L.Ainv.p, s);
   st.mark("  coarsest: inverse");
-  if (n >= coarse_gemv_min() && !(getenv("HCAMG_COARSE_SYMV") && atoi(getenv("HCAMG_COARSE_SYMV")) == 0))
-    symv_build(L.Ainv.p, n, L.Asym, s);
+  if (n >= coarse_gemv_min() && opts().coarse_symv) symv_build(L.Ainv.p, n, L.Asym, s);
 }
 
 void finish_level(hcamg_handle* h, DevLevel& L) {
@@ -285,6 +289,9 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
   refresh_views(h);
   HC_CUDA(cudaStreamSynchronize(s));
   h->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  // hand the setup's transient buffers (tens of GB on config 2) back to the
+  // device: the private pool keeps freed memory only while a build runs
+  if (h->pool) HC_CUDA(cudaMemPoolTrimTo(h->pool, 0));
 }
 
 void fill_info(hcamg_handle* h, hcamg_info* info) {
@@ -399,6 +406,7 @@ void set_ctl(hcamg_handle* h, double tol, int64_t maxit) {
 
 void require_hierarchy(hcamg_handle* h) {
   require(!h->levels.empty(), "no hierarchy: call hcamg_setup_* first");
+  require(h->method != kSmootherOnly, "the handle holds a smoother only (hcamg_smoother_setup)");
 }
 
 void prepare_loop(hcamg_handle* h, Graph& G, bool pcg, int64_t maxit) {
@@ -425,6 +433,8 @@ int guarded(hcamg_handle* h, F&& f) {
   h->err_index = -1;
   try {
     HC_CUDA(cudaSetDevice(h->device));
+    OptionsScope os(&h->opts);
+    PoolScope ps(h->pool);
     f();
     return HCAMG_OK;
   } catch (const Error& e) {
@@ -484,17 +494,19 @@ int hcamg_create(hcamg_handle** out, int device, void* cuda_stream) {
     }
     HC_CUDA(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
     if (cublasCreate(&h->cublas) != CUBLAS_STATUS_SUCCESS) throw Error(ECUDA_, "cublasCreate failed");
+    h->opts = options_from_env();
     {
-      // keep freed device memory in the stream-ordered pool (the setup's
-      // transient tens-of-GB buffers are then not re-mapped on the next build);
-      // HCAMG_POOL_RELEASE=1 restores the driver default (release at sync)
-      const char* e = getenv("HCAMG_POOL_RELEASE");
-      if (!(e && atoi(e) == 1)) {
-        cudaMemPool_t pool;
-        HC_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
-        uint64_t thr = UINT64_MAX;
-        HC_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-      }
+      // private stream-ordered pool: freed setup transients are reused within
+      // a build without re-mapping (release threshold: never at sync) and
+      // trimmed when the build ends; the device's default pool, which torch
+      // and other libraries in the process use, is left untouched
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = device;
+      HC_CUDA(cudaMemPoolCreate(&h->pool, &props));
+      uint64_t thr = UINT64_MAX;
+      HC_CUDA(cudaMemPoolSetAttribute(h->pool, cudaMemPoolAttrReleaseThreshold, &thr));
     }
   } catch (const Error& e) {
     fprintf(stderr, "hcamg_create: %s\n", e.what());
@@ -524,10 +536,63 @@ void hcamg_destroy(hcamg_handle* h) {
   if (h->cublas) cublasDestroy(h->cublas);
   if (h->aux) cudaStreamDestroy(h->aux);
   if (h->own_stream) cudaStreamDestroy(h->stream);
+  if (h->pool) {
+    cudaMemPoolTrimTo(h->pool, 0);
+    cudaMemPoolDestroy(h->pool);  // outstanding blocks (none expected) release it later
+  }
   delete h;
 }
 
 const char* hcamg_last_error(const hcamg_handle* h) { return h ? h->err.c_str() : "null handle"; }
+
+namespace {
+struct OptKey {
+  const char* name;
+  double Options::*d;
+  int Options::*i;
+  int64_t Options::*l;
+};
+const OptKey kOptKeys[] = {
+    {"sweep", nullptr, &Options::sweep, nullptr},
+    {"giant_min", nullptr, nullptr, &Options::giant_min},
+    {"coarse_gemv_min", nullptr, nullptr, &Options::coarse_gemv_min},
+    {"coarse_symv", nullptr, &Options::coarse_symv, nullptr},
+    {"galerkin_fp64", nullptr, &Options::galerkin_fp64, nullptr},
+    {"factor_apply", nullptr, &Options::factor_apply, nullptr},
+    {"form_z", nullptr, &Options::form_z, nullptr},
+    {"tri_calib", nullptr, &Options::tri_calib, nullptr},
+};
+const OptKey* find_opt(const char* key) {
+  if (!key) return nullptr;
+  for (const OptKey& k : kOptKeys)
+    if (!strcmp(k.name, key)) return &k;
+  return nullptr;
+}
+}  // namespace
+
+int hcamg_set_option(hcamg_handle* h, const char* key, double value) {
+  return guarded(h, [&] {
+    const OptKey* k = find_opt(key);
+    require(k != nullptr, std::string("unknown option ") + (key ? key : "(null)"));
+    if (k->i) {
+      require(value == (double)(int)value, std::string("option ") + key + " takes an integer");
+      if (k->i == &Options::sweep) require(value >= SWEEP_AUTO && value <= SWEEP_FLOW, "sweep mode out of range");
+      h->opts.*(k->i) = (int)value;
+    } else {
+      require(value == (double)(int64_t)value, std::string("option ") + key + " takes an integer");
+      h->opts.*(k->l) = (int64_t)value;
+    }
+    invalidate(h);  // recorded graphs embed the previous choices
+  });
+}
+
+int hcamg_get_option(hcamg_handle* h, const char* key, double* value) {
+  return guarded(h, [&] {
+    const OptKey* k = find_opt(key);
+    require(k != nullptr && value, std::string("unknown option ") + (key ? key : "(null)"));
+    *value = k->i ? (double)(h->opts.*(k->i)) : (double)(h->opts.*(k->l));
+  });
+}
 int64_t hcamg_error_index(const hcamg_handle* h) { return h ? h->err_index : -1; }
 void* hcamg_stream(hcamg_handle* h) { return h ? (void*)h->stream : nullptr; }
 
@@ -591,9 +656,8 @@ int hcamg_hier_end_with(hcamg_handle* h, const hcamg_csr* coarse_matrix, hcamg_i
     DevLevel& last = *h->levels.back();
     last.has_P = false;
     if (coarse_matrix) {
-      DCsr M;
-      upload_csr(coarse_matrix, M, h->stream);
-      factor_coarsest(h, last, M);
+      upload_csr(coarse_matrix, last.cmat, h->stream);
+      factor_coarsest(h, last, last.cmat);
     } else {
       factor_coarsest(h, last, last.A);
     }
@@ -819,6 +883,117 @@ int hcamg_export_coarse_cols(hcamg_handle* h, int32_t level, int64_t* cols) {
   });
 }
 
+int hcamg_coarse_solve(hcamg_handle* h, int32_t level, const double* b, double* x) {
+  return guarded(h, [&] {
+    require(level >= 0 && level < (int32_t)h->levels.size(), "level out of range");
+    DevLevel& L = *h->levels[(size_t)level];
+    require(L.coarsest, "level has no coarse factor");
+    cudaStream_t s = h->stream;
+    const int64_t n = L.n;
+    if (!n) return;
+    DBuf<double> db(n, s), dx(n, s);
+    DBuf<int> stop(1, s);
+    stop.zero();
+    HC_CUDA(cudaMemcpyAsync(db.p, b, 8 * n, cudaMemcpyHostToDevice, s));
+    dense_gemv_rows(stop.p, n, n, L.Ainv.p, db.p, dx.p, s);
+    HC_CUDA(cudaMemcpyAsync(x, dx.p, 8 * n, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int hcamg_cholesky_factor(hcamg_handle* h, int32_t level, int64_t* ordering, double* factor) {
+  return guarded(h, [&] {
+    require(level >= 0 && level < (int32_t)h->levels.size(), "level out of range");
+    DevLevel& L = *h->levels[(size_t)level];
+    require(L.coarsest, "level has no coarse factor");
+    cudaStream_t s = h->stream;
+    const DCsr& M = L.cmat.nrows ? L.cmat : L.A;
+    const int64_t n = M.nrows;
+    if (!n) return;
+    std::vector<int64_t> hp = M.ptr.download();
+    std::vector<int32_t> hi = M.idx.download();
+    std::vector<int32_t> perm = rcm_order(n, hp, hi), inv((size_t)n);
+    for (int64_t i = 0; i < n; ++i) inv[(size_t)perm[(size_t)i]] = (int32_t)i;
+    DBuf<int32_t> dperm, dinv;
+    dperm.upload(perm.data(), n, s);
+    dinv.upload(inv.data(), n, s);
+    DCsr Mp;
+    csr_extract(M, dperm.p, n, dinv.p, n, Mp, s);
+    DBuf<double> D(n * n, s);
+    D.zero();
+    k_densify<<<grid_for(n, 128), 128, 0, s>>>(Mp.ptr.p, Mp.idx.p, Mp.val.p, n, D.p);
+    HC_CHECK_LAUNCH();
+    const int64_t bad = dense_cholesky(h->cublas, D.p, n, n, s);
+    if (bad >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(bad) + ")", bad);
+    std::vector<double> hL = D.download();  // column-major, lower triangle valid
+    for (int64_t i = 0; i < n; ++i) {
+      if (ordering) ordering[i] = perm[(size_t)i];
+      if (factor)
+        for (int64_t j = 0; j < n; ++j) factor[i * n + j] = j <= i ? hL[(size_t)(i + j * n)] : 0.0;
+    }
+  });
+}
+
+int hcamg_smoother_setup(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* G) {
+  return guarded(h, [&] {
+    require(A && G, "A and G are required");
+    cudaStream_t s = h->stream;
+    invalidate(h);
+    h->levels.clear();
+    h->notes.clear();
+    h->stalled = false;
+    h->method = kSmootherOnly;
+    auto L = std::make_unique<DevLevel>();
+    upload_csr(A, L->A, s);
+    upload_csr(G, L->G, s);
+    require(L->A.nrows == L->A.ncols, "A must be square");
+    require(L->G.nrows == L->A.nrows, "G rows must match A");
+    L->n = L->A.nrows;
+    alloc_level_vectors(*L, s);
+    build_l1(L->A, L->l1, s);
+    build_smoother(L->A, L->G, L->sm, s);
+    h->levels.push_back(std::move(L));
+    refresh_views(h);
+    HC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int hcamg_smooth(hcamg_handle* h, int32_t level, int32_t direction, const double* x_or_null, const double* b,
+                 double* out) {
+  return guarded(h, [&] {
+    require(level >= 0 && level < (int32_t)h->levels.size(), "level out of range");
+    require(direction >= 0 && direction <= 2, "unknown direction");
+    DevLevel& L = *h->levels[(size_t)level];
+    require(!L.coarsest && L.sm.npatch >= 0 && L.l1.p, "level has no smoother");
+    cudaStream_t s = h->stream;
+    const int64_t n = L.n;
+    ensure_ws(h, 1);
+    const int* stop = h->ws.zero_flag.p;
+    DBuf<double> db(std::max<int64_t>(n, 1), s), dx(std::max<int64_t>(n, 1), s), rb(std::max<int64_t>(n, 1), s),
+        dd(std::max<int64_t>(n, 1), s);
+    if (n) HC_CUDA(cudaMemcpyAsync(db.p, b, 8 * n, cudaMemcpyHostToDevice, s));
+    if (x_or_null && n) HC_CUDA(cudaMemcpyAsync(dx.p, x_or_null, 8 * n, cudaMemcpyHostToDevice, s));
+    else dx.zero();
+    // smooth(x, b) = x + S(0, b - A x) for either direction (the legs start
+    // from x = 0; the residual is formed in scipy's rounding order, so a
+    // fixed point x* with b = A x* (scipy) stays exactly fixed, as in the
+    // reference's smoothers.py:122)
+    for (int dir : {0, 1}) {
+      if ((dir == 0 && direction == 1) || (dir == 1 && direction == 0)) continue;
+      residual_scipy_order(L.A, dx.p, db.p, rb.p, s);
+      if (dir == 0) {
+        record_piece(PC_DOWN, L, nullptr, rb.p, dd.p, stop, s);
+      } else {
+        dd.zero();
+        record_piece(PC_UP, L, nullptr, rb.p, dd.p, stop, s);
+      }
+      vec_add(n, dx.p, dd.p, dx.p, s);
+    }
+    if (n) HC_CUDA(cudaMemcpyAsync(out, dx.p, 8 * n, cudaMemcpyDeviceToHost, s));
+    HC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 int hcamg_vcycle(hcamg_handle* h, const double* b, const double* x_or_null, double* out) {
   return guarded(h, [&] {
     require_hierarchy(h);
@@ -863,16 +1038,13 @@ static int pcg_impl(hcamg_handle* h, const double* b, bool b_dev, const double* 
     else h->ws.x.zero();
     set_ctl(h, tol, maxit);
     run_loop_graph(h, h->g_pcg);
+    zero_x_if_zero_rhs(h->ws, s);
     HC_CUDA(cudaMemcpyAsync(x, h->ws.x.p, 8 * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
-    if (!sync && !report && !history) return;
+    if (!sync && !report && !history) return;  // errors deferred: hcamg_solve_status
     int error = 0;
     hcamg_report rep{};
     read_report(h, &rep, &error);
     pcg_breakdown(h, error);
-    if (rep.zero_rhs) {
-      if (x_dev) HC_CUDA(cudaMemsetAsync(x, 0, 8 * n, s));
-      else memset(x, 0, 8 * n);
-    }
     if (history && rep.iterations)
       HC_CUDA(cudaMemcpyAsync(history, h->ws.hist.p, 8 * rep.iterations, cudaMemcpyDeviceToHost, s));
     HC_CUDA(cudaStreamSynchronize(s));
@@ -904,16 +1076,29 @@ int hcamg_amg_solve(hcamg_handle* h, const double* b, const double* x0, double t
     else h->ws.x.zero();
     set_ctl(h, tol, maxit);
     run_loop_graph(h, h->g_amg);
+    zero_x_if_zero_rhs(h->ws, s);
     HC_CUDA(cudaMemcpyAsync(x, h->ws.x.p, 8 * n, cudaMemcpyDeviceToHost, s));
     int error = 0;
     hcamg_report rep{};
     read_report(h, &rep, &error);
-    if (rep.zero_rhs) memset(x, 0, 8 * n);
     if (history && rep.iterations)
       HC_CUDA(cudaMemcpyAsync(history, h->ws.hist.p, 8 * rep.iterations, cudaMemcpyDeviceToHost, s));
     HC_CUDA(cudaStreamSynchronize(s));
     check_dist(h);
     if (report) *report = rep;
+  });
+}
+
+int hcamg_solve_status(hcamg_handle* h, hcamg_report* report) {
+  return guarded(h, [&] {
+    require_hierarchy(h);
+    require(h->ws.ctl.p != nullptr, "no solve has run on this handle");
+    int error = 0;
+    hcamg_report rep{};
+    read_report(h, &rep, &error);
+    if (report) *report = rep;
+    pcg_breakdown(h, error);
+    check_dist(h);
   });
 }
 

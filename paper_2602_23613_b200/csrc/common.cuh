@@ -48,7 +48,10 @@ inline void require(bool ok, const std::string& msg) {
   if (!ok) throw Error(EINVAL_, msg);
 }
 
-// Stream-ordered device buffer (cudaMallocAsync pool).
+cudaMemPool_t current_pool();
+
+// Stream-ordered device buffer (the handle's private pool when one is in
+// scope, else the device's default cudaMallocAsync pool).
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -68,7 +71,11 @@ struct DBuf {
     release();
     s = st;
     n = count;
-    if (count > 0) HC_CUDA(cudaMallocAsync((void**)&p, sizeof(T) * (size_t)count, st));
+    if (count > 0) {
+      cudaMemPool_t pool = current_pool();
+      if (pool) HC_CUDA(cudaMallocFromPoolAsync((void**)&p, sizeof(T) * (size_t)count, pool, st));
+      else HC_CUDA(cudaMallocAsync((void**)&p, sizeof(T) * (size_t)count, st));
+    }
   }
   void release() {
     if (p) cudaFreeAsync(p, s);
@@ -139,5 +146,42 @@ inline unsigned grid_for(int64_t work, int threads, int64_t cap = 148 * 32) {
 }
 
 constexpr int kSMs = 148;
+
+// Per-handle options (hcamg_set_option).  They replace the process-wide
+// HCAMG_* environment switches of round 1: the environment only seeds the
+// defaults when a handle is created, and every entry point runs with its
+// handle's options installed (OptionsScope), so tests can force a code path
+// per hierarchy.
+enum SweepMode : int {
+  SWEEP_AUTO = 0,     // cluster leg when a wave fits 16 CTAs, else the grid leg
+  SWEEP_LEG = 1,      // cluster leg (one 16-CTA cluster, prefetching)
+  SWEEP_GRID = 2,     // cooperative grid leg
+  SWEEP_WAVE = 3,     // one launch per wavefront
+  SWEEP_FLOW = 4,     // dataflow leg: per-patch ready counters, no wave barriers
+};
+struct Options {
+  int sweep = SWEEP_AUTO;
+  int64_t giant_min = 4096;        // dense-regime cutoff (= reference _DENSE_COMPONENT_CUTOFF, transfer.py:35)
+  int64_t coarse_gemv_min = 8192;  // coarsest solve: HBM row GEMV from this size on
+  int coarse_symv = 1;             // single GPU: packed lower triangle of the inverse
+  int galerkin_fp64 = 0;           // dense-regime Galerkin correction in fp64 (0: the TF32 tensor-core product)
+  int factor_apply = 1;            // dense block applied through the envelope factor (0: explicit Z)
+  int form_z = 0;                  // keep the explicit Z block resident even when the factor applies P
+  int tri_calib = 4;               // calibration rounds of the TMA sweep partition
+};
+Options options_from_env();
+const Options& opts();
+struct OptionsScope {
+  const Options* prev;
+  explicit OptionsScope(const Options* o);
+  ~OptionsScope();
+};
+// Allocation pool of the handle in scope (nullptr: the device default pool).
+struct PoolScope {
+  cudaMemPool_t prev;
+  explicit PoolScope(cudaMemPool_t p);
+  ~PoolScope();
+};
+cudaMemPool_t current_pool();
 
 }  // namespace hcamg

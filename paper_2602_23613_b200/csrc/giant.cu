@@ -854,7 +854,7 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
 // unvisited neighbours appended in column order and insertion-sorted by
 // degree; the final order reversed.  Seed ties are taken by lowest index
 // (scipy's argsort is not stable, so its tie choice is platform dependent).
-static std::vector<int32_t> rcm_order(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx) {
+std::vector<int32_t> rcm_order(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx) {
   std::vector<int64_t> deg((size_t)n);
   for (int64_t i = 0; i < n; ++i) {
     deg[(size_t)i] = ptr[(size_t)i + 1] - ptr[(size_t)i];
@@ -1217,8 +1217,7 @@ void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr
   // HCAMG_GALERKIN_E=fp64 keeps the fp64 product (validation).
   DBuf<double> E(nc * nc, s);
   cb(cublasSetStream(h, s), "setStream");
-  const char* emode = getenv("HCAMG_GALERKIN_E");
-  if (emode && std::string(emode) == "fp64") {
+  if (opts().galerkin_fp64) {
     DBuf<double> rho(nG * nc, s);
     k_spmm_rows<<<(unsigned)std::min<int64_t>(nG, kSMs * 16), 256, 0, s>>>(Agg.ptr.p, Agg.idx.p, Agg.val.p, nG, nc,
                                                                            hp.Z.p, rho.p);

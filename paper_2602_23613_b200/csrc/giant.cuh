@@ -12,7 +12,6 @@
 
 namespace hcamg {
 
-constexpr int64_t kGiantMin = 4096;   // = the reference's _DENSE_COMPONENT_CUTOFF (transfer.py:35)
 
 // Factor the SPD matrix given as CSR (positions 0..n-1) into packed tiles and
 // solve A Z = B for the row-major n x m right-hand side B (overwritten by Z).
@@ -22,6 +21,11 @@ constexpr int64_t kGiantMin = 4096;   // = the reference's _DENSE_COMPONENT_CUTO
 // sweeps; the caller finishes with factorp_attach).
 void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B_rowmajor, int64_t m, cudaStream_t s,
                         FactorP* fac = nullptr);
+
+// Reverse Cuthill-McKee order of a symmetric CSR pattern (scipy's
+// csgraph.reverse_cuthill_mckee, which the reference's cholesky() applies,
+// sparse.py:297); host C++.
+std::vector<int32_t> rcm_order(int64_t n, const std::vector<int64_t>& ptr, const std::vector<int32_t>& idx);
 
 // Hybrid interpolation data of one level.
 struct HybridP {

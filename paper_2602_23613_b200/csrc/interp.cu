@@ -361,18 +361,22 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
     std::vector<int64_t> a_off((size_t)ncomp), b_off((size_t)ncomp);
     std::vector<DenseJob> small;
     std::vector<int64_t> small_comp, large_comp;
+    // the largest component above the dense-regime cutoff is kept as the
+    // resident dense block (hybrid P); any other component, whatever its
+    // size, is solved densely and lands in the CSR part of P, as in the
+    // reference (transfer.py:100-116)
+    for (int64_t c = 0; c < ncomp; ++c) {
+      const int64_t k = hc[(size_t)c + 1] - hc[(size_t)c], nk = hk[(size_t)c + 1] - hk[(size_t)c];
+      if (nk > 0 && k > opts().giant_min && (giant < 0 || k > hc[(size_t)giant + 1] - hc[(size_t)giant]))
+        giant = (int)c;
+    }
     int64_t at = 0, bt = 0, pt = 0;
     for (int64_t c = 0; c < ncomp; ++c) {
       const int64_t k = hc[(size_t)c + 1] - hc[(size_t)c], nk = hk[(size_t)c + 1] - hk[(size_t)c];
       out.max_comp = std::max(out.max_comp, k);
       a_off[(size_t)c] = at;
       b_off[(size_t)c] = bt;
-      if (nk == 0) continue;
-      if (k > kGiantMin) {
-        if (giant >= 0) throw Error(EUNSUPPORTED_, "more than one interior component above the dense-regime cutoff");
-        giant = (int)c;
-        continue;
-      }
+      if (nk == 0 || c == giant) continue;
       if (k <= 32) {
         small.push_back(DenseJob{at, bt, pt, (int32_t)k, (int32_t)nk});
         small_comp.push_back(c);

@@ -74,6 +74,7 @@ struct DevLevel {
   std::vector<int64_t> gc_cols;
   bool coarsest = false;
   DBuf<double> Ainv;     // coarsest: dense inverse (row-major n x n)
+  DCsr cmat;             // coarsest of a user-assembled hierarchy: the matrix its coarse_factor inverts
   SymPacked Asym;        // coarsest: its lower triangle (single-GPU GEMV reading it once)
   SegPlan pt_seg;        // segmented restriction plan when P^T has long rows
   HybridP hp;            // dense-regime interpolation block (P/Pt then hold the sparse part)

@@ -472,45 +472,6 @@ void Workspace::ensure(int64_t n_, int64_t maxit, cudaStream_t s) {
 
 long long* g_leg_trace = nullptr;  // debug: set by hcamg_debug_trace
 
-static const std::string& sweep_mode() {
-  static const std::string m = [] {
-    const char* e = getenv("HCAMG_SWEEP");
-    return std::string(e ? e : "auto");
-  }();
-  return m;
-}
-
-static SweepArgs sweep_args(DevLevel& L, const double* b, double* x, const int* stop, bool down) {
-  Smoother& sm = L.sm;
-  SweepArgs sa{};
-  sa.stop = stop;
-  sa.n = L.n;
-  sa.nwave = sm.nwave;
-  sa.wave_ptr = sm.d_wave_ptr.p;
-  sa.lastr = sm.lastr.p;
-  sa.in_first = sm.in_first.p;
-  sa.patch_ptr = sm.patch_ptr.p;
-  sa.dofs = sm.patch_dofs.p;
-  sa.binv_off = sm.binv_off.p;
-  sa.binv = sm.binv.p;
-  sa.gcol = sm.gcol.p;
-  sa.gval = sm.gval.p;
-  sa.ap = L.A.ptr.p;
-  sa.ai = L.A.idx.p;
-  sa.av = L.A.val.p;
-  sa.l1 = L.l1.p;
-  sa.b = b;
-  sa.x = x;
-  sa.r = L.r.p;
-  sa.d0 = L.d0.p;
-  sa.d1 = L.d1.p;
-  sa.dj = L.dj.p;
-  sa.gen_ptr = down ? sm.d_gen_fw_ptr.p : sm.d_gen_bw_ptr.p;
-  sa.genrow = down ? sm.genrow_fw.p : sm.genrow_bw.p;
-  sa.ownr = down ? sm.ownr_fw.p : sm.ownr_bw.p;
-  return sa;
-}
-
 // per-wave kernel sequence of one smoothing leg (one launch per wavefront)
 static int64_t record_leg_waves(DevLevel& L, const double* b, double* x, const int* stop, bool down, cudaStream_t s) {
   Smoother& sm = L.sm;
@@ -596,12 +557,9 @@ static int64_t record_leg_waves(DevLevel& L, const double* b, double* x, const i
 
 // Coarsest levels of at least this size apply their inverse with the
 // HBM-streaming row GEMV (row-partitioned in the distributed solve); smaller
-// ones with the latency-oriented k_gemv_dense.  HCAMG_COARSE_GEMV_MIN
-// overrides (tests use it to exercise the coarse exchange on small cases).
-int64_t coarse_gemv_min() {
-  const char* e = getenv("HCAMG_COARSE_GEMV_MIN");
-  return e ? atoll(e) : 8192;
-}
+// ones with the latency-oriented k_gemv_dense.  Option "coarse_gemv_min"
+// (tests lower it to exercise the streaming paths on small cases).
+int64_t coarse_gemv_min() { return opts().coarse_gemv_min; }
 
 // One piece of a level's V-cycle work (separately launchable for profiling).
 int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* x, const int* stop, cudaStream_t s,
@@ -678,17 +636,9 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     return 1;
   }
   const bool down = pc == PC_DOWN;
-  const std::string& m = sweep_mode();
-  if (m == "smem" && n <= sweep_smem_max_n()) {
-    launch_sweep_smem(down, sweep_args(L, b, x, stop, down), s);
-    return 1;
-  }
-  if (m == "cluster") {
-    launch_sweep(down, sweep_args(L, b, x, stop, down), s);
-    return 1;
-  }
+  const int m = opts().sweep;
   const bool wide = L.sm.max_wave_patches > 256 || L.sm.max_gen_rows > 8192;
-  if (m == "auto" || m == "leg" || m == "dsm" || m == "grid") {
+  if (m == SWEEP_AUTO || m == SWEEP_LEG || m == SWEEP_GRID) {
     Smoother& sm = L.sm;
     SweepProgram& pg = sm.pg;
     LegArgs la{};
@@ -736,8 +686,8 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     la.dj = L.dj.p;
     la.trace = g_leg_trace;
     la.gbar = pg.gbar.p;
-    if ((m == "auto" && wide) || m == "grid") launch_leg_grid(down, la, s);
-    else if (m != "dsm" || g_leg_trace || !launch_leg_dsm(down, la, s)) launch_leg(down, la, s);
+    if ((m == SWEEP_AUTO && wide) || m == SWEEP_GRID) launch_leg_grid(down, la, s);
+    else launch_leg(down, la, s);
     return 1;
   }
   return record_leg_waves(L, b, x, stop, down, s);
@@ -895,6 +845,45 @@ __global__ void k_vec_add(int64_t n, const double* __restrict__ a, const double*
     out[u] = a[u] + b[u];
 }
 }  // namespace
+
+namespace {
+// r = b - A x with scipy's csr_matvec rounding (per row: sequential sum in
+// ascending column order from +0.0, separate multiply / add roundings), then
+// numpy's b - y: the residual the reference's smooth() forms (smoothers.py:122)
+__global__ void k_residual_seq(int64_t n, const int64_t* __restrict__ ap, const int32_t* __restrict__ ai,
+                               const double* __restrict__ av, const double* __restrict__ x,
+                               const double* __restrict__ b, double* __restrict__ r) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t e = ap[u]; e < ap[u + 1]; ++e) acc = __dadd_rn(acc, __dmul_rn(av[e], x[ai[e]]));
+    r[u] = __dsub_rn(b[u], acc);
+  }
+}
+__global__ void k_axpby(int64_t n, double a, const double* __restrict__ x, double b, const double* y, double* out) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+    out[u] = a * x[u] + b * y[u];
+}
+__global__ void k_zero_if_zero_rhs(const Ctl* __restrict__ c, int64_t n, double* __restrict__ x) {
+  if (!c->zero_b) return;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x)
+    x[u] = 0.0;
+}
+}  // namespace
+
+void residual_scipy_order(const DCsr& A, const double* x, const double* b, double* r, cudaStream_t s) {
+  if (A.nrows) k_residual_seq<<<vec_grid(A.nrows), kThreads, 0, s>>>(A.nrows, A.ptr.p, A.idx.p, A.val.p, x, b, r);
+  HC_CHECK_LAUNCH();
+}
+
+void vec_axpby(int64_t n, double a, const double* x, double b, const double* y, double* out, cudaStream_t s) {
+  if (n) k_axpby<<<vec_grid(n), kThreads, 0, s>>>(n, a, x, b, y, out);
+  HC_CHECK_LAUNCH();
+}
+
+void zero_x_if_zero_rhs(Workspace& w, cudaStream_t s) {
+  if (w.n) k_zero_if_zero_rhs<<<vec_grid(w.n), kThreads, 0, s>>>(w.ctl.p, w.n, w.x.p);
+  HC_CHECK_LAUNCH();
+}
 
 void vec_add(int64_t n, const double* a, const double* b, double* out, cudaStream_t s) {
   if (n) k_vec_add<<<vec_grid(n), kThreads, 0, s>>>(n, a, b, out);

@@ -69,6 +69,11 @@ void generic_pap(const DCsr& A, Workspace& w, cudaStream_t s);     // Ap, pAp, a
 void generic_update(Workspace& w, cudaStream_t s);                 // x, r, rel, history
 void generic_rz(Workspace& w, bool first, cudaStream_t s);         // rz (first: p = z) / beta
 void generic_p(Workspace& w, cudaStream_t s);                      // p = z + beta p
+// b == 0 (multilevel.py:252-253): x = 0 whatever x0 was (on device, no sync)
+void zero_x_if_zero_rhs(Workspace& w, cudaStream_t s);
+// r = b - A x in scipy's rounding order (sequential rows, no FMA)
+void residual_scipy_order(const DCsr& A, const double* x, const double* b, double* r, cudaStream_t s);
+void vec_axpby(int64_t n, double a, const double* x, double b, const double* y, double* out, cudaStream_t s);
 void vec_add(int64_t n, const double* a, const double* b, double* out, cudaStream_t s);  // out = a + b
 
 }  // namespace hcamg

@@ -1,42 +1,8 @@
-// Cluster-resident smoothing legs (see sweep.cu).
+// OSS-l1 smoothing legs (sweep2.cu) and the segmented restriction (sweep.cu).
 #pragma once
 #include "common.cuh"
 
 namespace hcamg {
-
-struct SweepArgs {
-  const int* stop;
-  int64_t n, nwave;
-  const int64_t* wave_ptr;   // device, nwave + 1
-  const int64_t* gen_ptr;    // device, direction-specific
-  const int32_t* genrow;     // (u, start, end) per generic row
-  const int32_t* ownr;       // (start, end) per patch entry
-  const int32_t* lastr;      // (start, end) per DoF (down leg)
-  const uint8_t* in_first;
-  const int64_t* patch_ptr;
-  const int32_t* dofs;
-  const int64_t* binv_off;
-  const double* binv;
-  const int32_t* gcol;
-  const double* gval;
-  const int64_t* ap;
-  const int32_t* ai;
-  const double* av;
-  const double* l1;
-  const double* b;
-  double* x;
-  double* r;
-  double* d0;
-  double* d1;
-  double* dj;
-  // optional fused transfer: P^T (down, rows tn) or P (up)
-  const int64_t* tp;
-  const int32_t* ti;
-  const double* tv;
-  int64_t tn;
-  double* tout;
-  const double* tin;
-};
 
 // Prefetching cluster leg (sweep2.cu): padded static structure per patch/row.
 struct LegArgs {
@@ -86,16 +52,7 @@ struct LegArgs {
 void launch_leg(bool down, const LegArgs& args, cudaStream_t s);
 // whole-GPU cooperative variant (grid.sync between wavefronts)
 void launch_leg_grid(bool down, const LegArgs& args, cudaStream_t s);
-// DSMEM-resident variant; returns false when the level does not fit (caller falls back)
-bool launch_leg_dsm(bool down, const LegArgs& args, cudaStream_t s);
-int64_t leg_dsm_max_n();
-
 int sweep_cluster_size();
-void launch_sweep(bool down, const SweepArgs& args, cudaStream_t s);
-
-// single-CTA shared-memory legs (levels with n <= sweep_smem_max_n())
-int64_t sweep_smem_max_n();
-void launch_sweep_smem(bool down, const SweepArgs& args, cudaStream_t s);
 
 // y = T v for a CSR T with long rows: fixed 256-entry segments, one warp each,
 // then an in-order reduction of the segment partials (deterministic).

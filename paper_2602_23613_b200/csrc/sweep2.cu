@@ -436,278 +436,6 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
 }
 
 
-// ============================================================================ DSMEM-resident leg
-//
-// Same schedule as k_leg, but the five working vectors (r, x, the two wave
-// corrections and the Jacobi step) live in the distributed shared memory of
-// the 16-CTA cluster: DoF u is slot u/16 of CTA u%16.  Every dynamic access is
-// a DSMEM load/store (~215 cycles cross-CTA, no L1 invalidation, cheap
-// cluster-scope release) instead of an L2 round trip; only the static
-// structure and b, A, l1 come from global memory.
-
-constexpr int kDsmC = 16;
-constexpr int64_t kDsmVecs = 5;  // r, x, d0, d1, dj
-
-struct Dsm {
-  double* base;  // local slice: [vec][S]
-  int64_t S;
-  cg::cluster_group cl;
-  __device__ __forceinline__ double* at(int vec, int64_t u) const {
-    return cl.map_shared_rank(base + vec * S + (u >> 4), (unsigned)(u & 15));
-  }
-  __device__ __forceinline__ double ld(int vec, int64_t u) const { return *at(vec, u); }
-  __device__ __forceinline__ void st(int vec, int64_t u, double v) const { *at(vec, u) = v; }
-};
-
-enum : int { VR = 0, VX = 1, VD0 = 2, VD1 = 3, VDJ = 4 };
-
-__device__ __forceinline__ double slots_dot_dsm(const int32_t* gc, const double* __restrict__ gv, int64_t gs, int cnt,
-                                                const Dsm& m, int vec) {
-  double dv[kSlots], w[kSlots];
-#pragma unroll
-  for (int j = 0; j < kSlots; ++j) {
-    w[j] = j < cnt ? __ldg(gv + j * gs) : 0.0;
-    dv[j] = j < cnt ? m.ld(vec, gc[j]) : 0.0;
-  }
-  double acc = 0.0;
-#pragma unroll
-  for (int j = 0; j < kSlots; ++j) acc = fma(w[j], dv[j], acc);
-  return acc;
-}
-
-__device__ __forceinline__ double range_dot_dsm(int32_t s, int32_t e, const int32_t* __restrict__ gcol,
-                                                const double* __restrict__ gval, const Dsm& m, int vec) {
-  double acc = 0.0;
-  for (int32_t k = s; k < e; ++k) acc = fma(gval[k], m.ld(vec, gcol[k]), acc);
-  return acc;
-}
-
-__device__ __forceinline__ double row_dot_dsm(const LegArgs& a, int64_t u, const Dsm& m, int vec) {
-  const int64_t e0 = a.ap[u], e1 = a.ap[u + 1];
-  double acc = 0.0;
-  for (int64_t k0 = e0; k0 < e1; k0 += 8) {
-    int32_t c[8];
-    double w[8], dv[8];
-#pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const bool ok = k0 + t < e1;
-      c[t] = ok ? __ldg(a.ai + k0 + t) : 0;
-      w[t] = ok ? __ldg(a.av + k0 + t) : 0.0;
-    }
-#pragma unroll
-    for (int t = 0; t < 8; ++t) dv[t] = k0 + t < e1 ? m.ld(vec, c[t]) : 0.0;
-#pragma unroll
-    for (int t = 0; t < 8; ++t) acc = fma(w[t], dv[t], acc);
-  }
-  return acc;
-}
-
-__device__ __forceinline__ void solve_patch_dsm(const LegArgs& a, int dir, const PatchPre& q, int lane, bool init,
-                                                const Dsm& m, int vsrc, int vdst) {
-  const bool act = lane < q.k;
-  const int l = lane & 15;
-  double bcol[16];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) bcol[c] = __ldg(a.pbinv + q.p * 256 + c * 16 + l);
-  double v = 0.0, xo = 0.0;
-  if (act) {
-    if (init) {
-      v = a.b[q.i];
-    } else {
-      xo = m.ld(VX, q.i);
-      v = m.ld(VR, q.i);
-    }
-    if (q.cnt >= 0) {
-      const double* gv = a.ogv + (((int64_t)dir * a.m + q.p) * kSlots) * 16 + l;
-      v -= slots_dot_dsm(q.gc, gv, 16, q.cnt, m, vsrc);
-      if (q.cnt > kSlots) {
-        const int32_t* rng = (dir == 0 ? a.ownr_fw : a.ownr_bw) + 2 * (a.patch_ptr[q.p] + lane);
-        v -= range_dot_dsm(rng[0] + kSlots, rng[1], a.gcol, a.gval, m, vsrc);
-      }
-      m.st(VR, q.i, v);
-    }
-  }
-  double d = 0.0;
-#pragma unroll
-  for (int c = 0; c < 16; ++c) d = fma(bcol[c], __shfl_sync(0xffffffffu, v, c), d);
-  if (act) {
-    m.st(VX, q.i, xo + d);
-    m.st(vdst, q.i, d);
-  }
-}
-
-__device__ void solve_patch_slow_dsm(const LegArgs& a, int dir, int64_t p, int lane, bool own, bool init,
-                                     const Dsm& m, int vsrc, int vdst) {
-  const int64_t e0 = a.patch_ptr[p];
-  const int k = (int)(a.patch_ptr[p + 1] - e0);
-  const double* Bi = a.binv + a.binv_off[p];
-  const int32_t* ownr = dir == 0 ? a.ownr_fw : a.ownr_bw;
-  int32_t i = 0;
-  double v = 0.0, xo = 0.0;
-  if (lane < k) {
-    i = a.dofs[e0 + lane];
-    if (init) {
-      v = a.b[i];
-    } else {
-      xo = m.ld(VX, i);
-      v = m.ld(VR, i);
-    }
-    if (own) {
-      const int32_t s = ownr[2 * (e0 + lane)], e = ownr[2 * (e0 + lane) + 1];
-      if (s >= 0) {
-        v -= range_dot_dsm(s, e, a.gcol, a.gval, m, vsrc);
-        m.st(VR, i, v);
-      }
-    }
-  }
-  double d = 0.0;
-  for (int c = 0; c < k; ++c) {
-    const double vc = __shfl_sync(0xffffffffu, v, c);
-    if (lane < k) d = fma(Bi[(int64_t)c * k + lane], vc, d);
-  }
-  if (lane < k) {
-    m.st(VX, i, xo + d);
-    m.st(vdst, i, d);
-  }
-}
-
-template <bool kDown>
-__global__ void __launch_bounds__(kLegThreads, 1) k_leg_dsm(LegArgs a) {
-  if (*a.stop) return;
-  cg::cluster_group cl = cg::this_cluster();
-  extern __shared__ double sh_dsm[];  // [5][S] vectors, then wave_ptr (W+1), gen_ptr (W+1)
-  const int64_t W = a.nwave, n = a.n;
-  const int64_t S = (n + kDsmC - 1) / kDsmC;
-  int64_t* wp = reinterpret_cast<int64_t*>(sh_dsm + kDsmVecs * S);
-  int64_t* gp = wp + W + 1;
-  const int dir = kDown ? 0 : 1;
-  const unsigned rank = cl.block_rank();
-  for (int64_t t = threadIdx.x; t <= W; t += blockDim.x) {
-    wp[t] = a.wave_ptr[t];
-    gp[t] = kDown ? a.gen_fw_ptr[t] : a.gen_bw_ptr[t];
-  }
-  Dsm m{sh_dsm, S, cl};
-  const int64_t nth = (int64_t)kDsmC * blockDim.x;
-  const int64_t gtid = (int64_t)rank * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int64_t wg = gtid >> 5, nw = nth >> 5;
-  // local slots of this CTA: u = rank + 16 * off
-  if (kDown) {
-    for (int64_t off = threadIdx.x; off < S; off += blockDim.x) {
-      const int64_t u = rank + kDsmC * off;
-      if (u < n) {
-        sh_dsm[VR * S + off] = a.b[u];
-        if (!a.in_first[u]) sh_dsm[VX * S + off] = 0.0;
-      }
-    }
-  } else {
-    for (int64_t off = threadIdx.x; off < S; off += blockDim.x) {
-      const int64_t u = rank + kDsmC * off;
-      if (u < n) sh_dsm[VX * S + off] = a.x[u];
-    }
-  }
-  cl.sync();
-  if (!kDown) {
-    // r = b - A x ; dj = r / l1
-    for (int64_t off = threadIdx.x; off < S; off += blockDim.x) {
-      const int64_t u = rank + kDsmC * off;
-      if (u >= n) continue;
-      const double rv = a.b[u] - row_dot_dsm(a, u, m, VX);
-      sh_dsm[VR * S + off] = rv;
-      sh_dsm[VDJ * S + off] = rv / a.l1[u];
-    }
-    cl.sync();
-    for (int64_t off = threadIdx.x; off < S; off += blockDim.x) {
-      const int64_t u = rank + kDsmC * off;
-      if (u >= n) continue;
-      sh_dsm[VR * S + off] -= row_dot_dsm(a, u, m, VDJ);
-      sh_dsm[VX * S + off] += sh_dsm[VDJ * S + off];
-    }
-    cl.sync();
-  }
-  PatchPre pq;
-  RowPre rq;
-  auto prefetch = [&](int64_t s) {
-    const int64_t dst = kDown ? s : W - 1 - s;
-    const int64_t p = wp[dst] + wg;
-    pq.p = -1;
-    if (p < wp[dst + 1]) load_patch(a, dir, p, lane, s > 0, pq);
-    rq.t = -1;
-    if (s > 0) {
-      const int64_t src = kDown ? s - 1 : dst + 1;
-      const int64_t t = gp[src] + (nth - 1 - gtid);
-      if (t < gp[src + 1]) load_row(a, dir, t, rq);
-    }
-  };
-  if (W > 0) prefetch(0);
-  for (int64_t s = 0; s < W; ++s) {
-    const int64_t dst = kDown ? s : W - 1 - s;
-    const int64_t src = kDown ? s - 1 : dst + 1;
-    const int vsrc = (src & 1) ? VD1 : VD0;
-    const int vdst = (dst & 1) ? VD1 : VD0;
-    const bool init = kDown && s == 0;
-    if (s > 0) {
-      if (rq.t >= 0) {
-        const double r0 = m.ld(VR, rq.u);
-        double acc = slots_dot_dsm(rq.gc, a.ggv[dir] + rq.t, a.ng[dir], rq.cnt, m, vsrc);
-        if (rq.cnt > kSlots) {
-          const int32_t* g = (kDown ? a.genrow_fw : a.genrow_bw) + 3 * rq.t;
-          acc += range_dot_dsm(g[1] + kSlots, g[2], a.gcol, a.gval, m, vsrc);
-        }
-        m.st(VR, rq.u, r0 - acc);
-      }
-      for (int64_t t = gp[src] + (nth - 1 - gtid) + nth; t < gp[src + 1]; t += nth) {
-        const int32_t* g = (kDown ? a.genrow_fw : a.genrow_bw) + 3 * t;
-        const double acc = range_dot_dsm(g[1], g[2], a.gcol, a.gval, m, vsrc);
-        m.st(VR, g[0], m.ld(VR, g[0]) - acc);
-      }
-    }
-    if (pq.p >= 0) {
-      if (pq.k > 0) solve_patch_dsm(a, dir, pq, lane, init, m, vsrc, vdst);
-      else solve_patch_slow_dsm(a, dir, pq.p, lane, s > 0, init, m, vsrc, vdst);
-    }
-    for (int64_t p = wp[dst] + wg + nw; p < wp[dst + 1]; p += nw)
-      solve_patch_slow_dsm(a, dir, p, lane, s > 0, init, m, vsrc, vdst);
-    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-    if (s + 1 < W) prefetch(s + 1);
-    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-  }
-  if (kDown) {
-    if (W == 0) {
-      for (int64_t off = threadIdx.x; off < S; off += blockDim.x) sh_dsm[VX * S + off] = 0.0;
-      cl.sync();
-    }
-    const int vl = ((W - 1) & 1) ? VD1 : VD0;
-    for (int64_t off = threadIdx.x; off < S; off += blockDim.x) {
-      const int64_t u = rank + kDsmC * off;
-      if (u >= n) continue;
-      double v = sh_dsm[VR * S + off];
-      if (W > 0) {
-        const int32_t s0 = a.lastr[2 * u], e0 = a.lastr[2 * u + 1];
-        if (s0 >= 0) v -= range_dot_dsm(s0, e0, a.gcol, a.gval, m, vl);
-      }
-      const double d = v / a.l1[u];
-      sh_dsm[VX * S + off] += d;
-      sh_dsm[VR * S + off] = v;
-      sh_dsm[VDJ * S + off] = d;
-    }
-    cl.sync();
-    for (int64_t off = threadIdx.x; off < S; off += blockDim.x) {
-      const int64_t u = rank + kDsmC * off;
-      if (u >= n) continue;
-      const double rv = sh_dsm[VR * S + off] - row_dot_dsm(a, u, m, VDJ);
-      a.r[u] = rv;
-      a.x[u] = sh_dsm[VX * S + off];
-    }
-  } else {
-    for (int64_t off = threadIdx.x; off < S; off += blockDim.x) {
-      const int64_t u = rank + kDsmC * off;
-      if (u < n) a.x[u] = sh_dsm[VX * S + off];
-    }
-  }
-  cl.sync();  // no CTA may exit while others still read its shared memory
-}
-
 }  // namespace
 
 void build_program(Smoother& sm, SweepProgram& pg, cudaStream_t s) {
@@ -741,38 +469,6 @@ void build_program(Smoother& sm, SweepProgram& pg, cudaStream_t s) {
   }
 }
 
-int64_t leg_dsm_max_n() { return (int64_t)kDsmC * ((200 * 1024) / (8 * kDsmVecs)); }
-
-bool launch_leg_dsm(bool down, const LegArgs& args, cudaStream_t s) {
-  if (sweep_cluster_size() != kDsmC || args.n > leg_dsm_max_n()) return false;
-  const int64_t S = (args.n + kDsmC - 1) / kDsmC;
-  const size_t smem = sizeof(double) * (size_t)(kDsmVecs * S) + sizeof(int64_t) * 2 * (size_t)(args.nwave + 1);
-  if (smem > 220 * 1024) return false;
-  static bool init = false;
-  if (!init) {
-    for (const void* fn : {(const void*)k_leg_dsm<true>, (const void*)k_leg_dsm<false>}) {
-      HC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      HC_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    }
-    init = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kDsmC);
-  cfg.blockDim = dim3(kLegThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kDsmC;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  if (down) HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg_dsm<true>, args));
-  else HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg_dsm<false>, args));
-  return true;
-}
-
 void launch_leg_grid(bool down, const LegArgs& args, cudaStream_t s) {
   const size_t smem = sizeof(int64_t) * 2 * (size_t)(args.nwave + 1);
   static int per_sm = 0;
@@ -804,6 +500,32 @@ void launch_leg_grid(bool down, const LegArgs& args, cudaStream_t s) {
   ga.l2pf = l2pf;
   if (down) HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<true, true>, ga));
   else HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<false, true>, ga));
+}
+
+// Largest cluster the leg can use on this device: 16 (non-portable) when
+// the occupancy query admits it, else the portable 8.
+int sweep_cluster_size() {
+  static int c = 0;
+  if (c) return c;
+  int best = 8;
+  cudaFuncSetAttribute(k_leg<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(k_leg<false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(16);
+  cfg.blockDim = dim3(kLegThreads);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 16;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&nclusters, (const void*)k_leg<true>, &cfg) == cudaSuccess && nclusters > 0)
+    best = 16;
+  cudaGetLastError();
+  c = best;
+  return c;
 }
 
 void launch_leg(bool down, const LegArgs& args, cudaStream_t s) {

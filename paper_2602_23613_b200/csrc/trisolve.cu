@@ -936,6 +936,9 @@ void tri_partition(TriSweep& out, cudaStream_t s) {
         for (int64_t b0 = c0; b0 < t;) {
           int64_t b1 = b0, bytes = 0;
           while (b1 < t && bytes + tbytes(b1) <= slotb) bytes += tbytes(b1++);
+          // a single row larger than a ring slot can never be staged
+          require(b1 > b0, "sweep ring slot (" + std::to_string(slotb) + " B) smaller than one factor row (" +
+                               std::to_string(tbytes(b0)) + " B): use fewer ring slots");
           sbat.push_back(TriBatch{b0, b1, tstart(b0), bytes});
           b0 = b1;
         }
@@ -1166,10 +1169,7 @@ bool tri_tma_fits(const TriSweep& sw) {
 
 int64_t factorp_npad(const FactorP& f) { return (f.T * kTriNB + kTriSB - 1) / kTriSB * kTriSB; }
 
-bool factorp_enabled() {
-  const char* e = getenv("HCAMG_PAPPLY");
-  return !(e && std::string(e) == "z");
-}
+bool factorp_enabled() { return opts().factor_apply != 0; }
 
 void factorp_attach(FactorP& f, const DCsr& W, const int32_t* mpos, const int32_t* rows, cudaStream_t s) {
   const int64_t nG = f.nG;
@@ -1189,7 +1189,7 @@ void factorp_attach(FactorP& f, const DCsr& W, const int32_t* mpos, const int32_
   f.v2.zero();
   f.bar.alloc(1, s);
   f.bar.zero();
-  const int rounds = getenv("HCAMG_TRI_CALIB") ? atoi(getenv("HCAMG_TRI_CALIB")) : 4;
+  const int rounds = opts().tri_calib;
   tri_calibrate(f.fw, f.v0.p, f.v1.p, f.bar.p, rounds, s);
   tri_calibrate(f.bw, f.v1.p, f.v2.p, f.bar.p, rounds, s);
   f.v0.zero();

@@ -33,6 +33,7 @@ import scipy.sparse as sp
 
 from . import _lib
 from ._lib import HostCSR, NativeUnavailable, ptr
+from .smoothers import L1Jacobi, PatchSet, _export_patches
 from .sparse import CholeskyFactor, NotPositiveDefiniteError, csr, raise_for
 
 __all__ = ["Level", "Hierarchy", "SolveReport", "build_hierarchy", "vcycle", "amg_solve", "pcg",
@@ -72,19 +73,6 @@ class Splitting:
         out = [d for p in self.pairs for d in (p.dof1, p.dof2)]
         return np.array(sorted(out), dtype=np.int64)
 
-
-@dataclass
-class PatchSet:
-    """Vertex patches of one level in reference order (smoothers.py:26-40) plus
-    the wavefront each patch runs in on the GPU."""
-
-    patches: list
-    waves: np.ndarray
-
-
-@dataclass
-class L1Jacobi:
-    d: np.ndarray
 
 
 class Level:
@@ -180,6 +168,19 @@ class _Device:
         if rc != 0:
             raise_for(rc, self.lib.hcamg_last_error(self.h).decode(), int(self.lib.hcamg_error_index(self.h)))
 
+    def set_option(self, key, value):
+        """hcamg_set_option: select a code path on this handle (see include/hcamg.h)."""
+        self.check(self.lib.hcamg_set_option(self.h, key.encode(), float(value)))
+
+    def get_option(self, key):
+        v = C.c_double()
+        self.check(self.lib.hcamg_get_option(self.h, key.encode(), C.byref(v)))
+        return v.value
+
+    def set_options(self, options):
+        for k, v in (options or {}).items():
+            self.set_option(k, SWEEP_MODES.get(v, v) if k == "sweep" else v)
+
     def info(self):
         info = _lib.Info()
         self.check(self.lib.hcamg_info_get(self.h, C.byref(info)))
@@ -241,17 +242,32 @@ class _Device:
         if name == "patches":
             if coarsest:
                 return None
-            m, ne = int(li.n_patches), int(li.n_patch_entries)
-            pp = np.empty(m + 1, dtype=np.int64)
-            dofs = np.empty(max(ne, 1), dtype=np.int64)
-            wave = np.empty(max(m, 1), dtype=np.int64)
-            self.check(self.lib.hcamg_export_patches(self.h, int(idx), ptr(pp), ptr(dofs), ptr(wave)))
-            return PatchSet([dofs[pp[t]:pp[t + 1]].copy() for t in range(m)], wave[:m].copy())
+            patches, waves = _export_patches(self, idx, li)
+            return PatchSet(patches, waves, None, self, idx)
         if name == "coarse_factor":
             if not coarsest:
                 return None
             return CholeskyFactor._from_level(self, idx, n)
         raise AttributeError(name)
+
+
+SWEEP_MODES = {"auto": 0, "leg": 1, "grid": 2, "wave": 3, "flow": 4}
+
+
+def _level_matrix(dev, idx):
+    """A of a device level as canonical scipy CSR."""
+    li = dev.level_info(idx)
+    n = int(li.n)
+    return dev.export_csr(idx, 0, n, n, int(li.nnz_A))
+
+
+def set_options(h, **options):
+    """Select code paths of a device hierarchy's solve (hcamg_set_option):
+    e.g. ``set_options(h, sweep="grid", coarse_gemv_min=0)``.  Setup options
+    (giant_min, galerkin_fp64, factor_apply, form_z) only act through
+    ``build_hierarchy(..., options=...)``."""
+    dev = _device_for(h)
+    dev.set_options(options)
 
 
 def _system_parts(system):
@@ -274,8 +290,9 @@ def _dof_edges(system):
 
 
 def build_hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse=32, theta=0.25,
-                    device=0):
-    """multilevel.py:78-164 on the GPU ("alg" and "ref" routes)."""
+                    device=0, options=None):
+    """multilevel.py:78-164 on the GPU ("alg" and "ref" routes).  ``options``
+    (not in the reference): per-handle code-path selection, see set_options."""
     if method in ("geo", "ref") and (meshes is None or rmaps is None):
         raise ValueError(f"method {method!r} requires the nested mesh chain")
     if method == "geo":
@@ -285,6 +302,7 @@ def build_hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_
         raise ValueError(f"unknown method {method!r}")
     A, G = _system_parts(system)
     dev = _Device(device)
+    dev.set_options(options)
     dev.method = method
     dev.dof_edges = _dof_edges(system)
     hA, hG = HostCSR(A), HostCSR(G)

@@ -54,29 +54,47 @@ def raise_for(rc, msg, index=-1):
 class CholeskyFactor:
     """Device-resident factor of an SPD matrix (sparse.py:146-165).
 
-    The factorisation itself runs on the GPU (symmetry check to 1e-12,
-    blocked Cholesky with the 1e-13 relative pivot floor); the matrix is
-    kept so a user-assembled hierarchy can attach it as ``coarse_factor``.
+    The factorisation runs on the GPU (symmetry check to 1e-12, blocked
+    Cholesky with the 1e-13 relative pivot floor) and the solve applies the
+    resident inverse.  ``ordering`` (reverse Cuthill-McKee) and ``factor``
+    (lower-triangular CSR L with L L^T = A[ordering][:, ordering]) -- the
+    reference's fields -- are materialised from the device on first access.
     """
 
-    def __init__(self, matrix, dev=None):
+    def __init__(self, matrix, dev=None, level=0):
         self.matrix = matrix
         self._dev = dev
+        self._level = level
+        self._n = matrix.shape[0] if matrix is not None else 0
+        self._ord = None
+        self._fac = None
 
     @property
     def n(self):
-        return self.matrix.shape[0] if self.matrix is not None else self._n
+        return self._n
+
+    def _materialise(self):
+        if self._ord is None:
+            n = self.n
+            ordering = np.empty(max(n, 1), dtype=np.int64)
+            L = np.empty((n, n), dtype=np.float64)
+            dev = self._dev
+            dev.check(dev.lib.hcamg_cholesky_factor(dev.h, int(self._level), _lib.ptr(ordering), _lib.ptr(L)))
+            self._ord = ordering[:n].copy()
+            self._fac = csr(L)
+        return self._ord, self._fac
 
     @property
     def ordering(self):
-        return np.arange(self.n, dtype=np.int64)
+        return self._materialise()[0]
+
+    @property
+    def factor(self):
+        return self._materialise()[1]
 
     @classmethod
     def _from_level(cls, dev, idx, n):
-        f = cls.__new__(cls)
-        f._dev = dev
-        f._level = idx
-        f.matrix = None
+        f = cls(None, dev, idx)
         f._n = n
         return f
 
@@ -85,6 +103,9 @@ class CholeskyFactor:
         """The matrix a coarse factor inverts (ours, or a reference-style
         CholeskyFactor(ordering, factor) rebuilt as P^T L L^T P)."""
         if isinstance(cf, CholeskyFactor):
+            if cf.matrix is None and cf._dev is not None:
+                from .multilevel import _level_matrix
+                return _level_matrix(cf._dev, cf._level)
             return cf.matrix
         L = getattr(cf, "factor", None)
         perm = getattr(cf, "ordering", None)
@@ -111,15 +132,23 @@ def cholesky(A, check_symmetry=True):
     dev.check(dev.lib.hcamg_hier_push(dev.h, H.ref(), None, None))
     info = _lib.Info()
     dev.check(dev.lib.hcamg_hier_end(dev.h, C.byref(info)))
-    return CholeskyFactor(A, dev)
+    return CholeskyFactor(A, dev, 0)
 
 
 def solve(factor, b):
-    """Apply the factor's inverse (sparse.py:304-321)."""
-    b = np.ascontiguousarray(np.asarray(b, dtype=np.float64))
+    """Solve A x = b with a device factor (sparse.py:304-321); ``b`` may be a
+    vector or an n x k block of right-hand sides."""
+    b = np.asarray(b, dtype=np.float64)
     if b.shape[0] != factor.n:
         raise ValueError(f"dimension mismatch: factor {factor.n}, rhs {b.shape}")
-    out = np.empty_like(b)
+    if factor.n == 0:
+        return b.copy()
     dev = factor._dev
-    dev.check(dev.lib.hcamg_vcycle(dev.h, _lib.ptr(b), None, _lib.ptr(out)))
-    return out
+    cols = b.reshape(b.shape[0], -1)
+    out = np.empty_like(cols)
+    for j in range(cols.shape[1]):
+        bj = np.ascontiguousarray(cols[:, j])
+        xj = np.empty_like(bj)
+        dev.check(dev.lib.hcamg_coarse_solve(dev.h, int(factor._level), _lib.ptr(bj), _lib.ptr(xj)))
+        out[:, j] = xj
+    return out.reshape(b.shape)

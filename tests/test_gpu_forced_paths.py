@@ -1,0 +1,124 @@
+"""Every code path the configs[1] bench runs, forced on the golden cases and
+compared with the CPU oracle (VERDICT r1 "oracle-pin every kernel").
+
+The c2 bench selects its kernels by size: the dense-regime interpolation
+(one interior component above the 4096-DoF cutoff) with the envelope-factor
+TMA sweeps, the Schur-form Galerkin product, the packed-triangle coarsest
+solve (n_c >= 8192) and the cooperative grid smoothing leg (waves wider than
+one cluster).  Per-handle options (hcamg_set_option) force each of them on
+the golden cases, whose oracle hierarchies are cheap, and the results must
+match the oracle to the same tolerances as the default paths
+(tests/test_gpu_parity.py): integers bit-exact, P / A_c / V-cycle / x within
+max(1e-10, 10 x measured floor), PCG iterations +-1.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import amg_oracle as O
+from tests.cases import CASES, load
+
+import paper_2602_23613_b200 as P
+from paper_2602_23613_b200.multilevel import set_options
+
+pytestmark = pytest.mark.gpu
+
+DENSE = {"giant_min": 200, "coarse_gemv_min": 0, "coarse_symv": 1}
+VARIANTS = {
+    # dense regime as on c2: factor sweeps (TMA kernel), fp64 Galerkin, packed-triangle coarsest solve
+    "dense": dict(DENSE, galerkin_fp64=1),
+    # the same with the TF32 tensor-core Galerkin correction term
+    "dense_tf32": dict(DENSE, galerkin_fp64=0),
+    # dense regime with the explicit Z block (row GEMV / chunked column sums)
+    "dense_z": dict(DENSE, galerkin_fp64=1, factor_apply=0, coarse_symv=0),
+}
+SWEEPS = ["grid", "wave", "leg"]
+
+
+def rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300)) if np.size(b) else 0.0
+
+
+def same_pattern(a, b):
+    a, b = a.tocsr(), b.tocsr()
+    return (a.shape == b.shape and a.nnz == b.nnz and np.array_equal(a.indptr, b.indptr)
+            and np.array_equal(a.indices, b.indices))
+
+
+@pytest.fixture(scope="module", params=CASES)
+def oracle_case(request):
+    c = load(request.param)
+    ho = O.hierarchy(c.system, c.meta["method"], meshes=c.meshes, rmaps=c.rmaps)
+    hf = O.hierarchy(c.system, c.meta["method"], meshes=c.meshes, rmaps=c.rmaps, floor_solver=True)
+    b = c.z["pcg_b"]
+    xo, ro = O.pcg(c.system.A, b, precond=lambda r: O.vcycle(ho, r), tol=1e-8)
+    xf, _ = O.pcg(c.system.A, b, precond=lambda r: O.vcycle(hf, r), tol=1e-8)
+    floor = max([rel(f.P.data, o.P.data) for f, o in zip(hf.levels[:-1], ho.levels[:-1])]
+                + [np.linalg.norm(xf - xo) / np.linalg.norm(xo)])
+    c.tol = max(1e-10, 10.0 * floor)
+    c.xo, c.ro = xo, ro
+    return request.param, c, ho
+
+
+def check_solves(c, ho, hg):
+    b = c.z["pcg_b"]
+    assert rel(P.vcycle(hg, b), O.vcycle(ho, b)) <= c.tol
+    xg, rg = P.pcg(c.system.A, b, precond=lambda r: P.vcycle(hg, r), tol=1e-8)
+    assert rg.converged and abs(rg.iterations - c.ro.iterations) <= 1
+    assert np.linalg.norm(xg - c.xo) <= c.tol * np.linalg.norm(c.xo)
+    x2, r2 = P.pcg(c.system.A, b, precond=lambda r: P.vcycle(hg, r), tol=1e-8)
+    assert np.array_equal(xg, x2) and np.array_equal(rg.residual_history, r2.residual_history)
+    xa, ra = P.amg_solve(hg, c.z["amg_b"], x0=c.z["amg_x0"], tol=1e-8, maxit=200)
+    if c.meta["amg_iters"] >= 200:
+        # the reference's stand-alone AMG stagnates on the 1e6 checkerboard (no
+        # convergence in 200 cycles); the iterate there is roundoff-driven
+        assert not ra.converged
+        return
+    assert abs(ra.iterations - c.meta["amg_iters"]) <= 1
+    assert np.linalg.norm(xa - c.z["amg_x"]) <= c.tol * np.linalg.norm(c.z["amg_x"])
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_dense_regime_forced(oracle_case, variant):
+    name, c, ho = oracle_case
+    hg = P.build_hierarchy(c.system, c.meta["method"], meshes=c.meshes, rmaps=c.rmaps, options=VARIANTS[variant])
+    assert hg.depth == ho.depth and hg.stalled == ho.stalled and hg.notes == ho.notes
+    dense_levels = 0
+    for ell, (lg, lo) in enumerate(zip(hg.levels, ho.levels)):
+        assert lg.n == lo.n
+        assert same_pattern(lg.A, lo.A), f"A_{ell} pattern"
+        assert rel(lg.A.data, lo.A.data) <= max(c.tol, 1e-12), f"A_{ell} values"
+        if lo.P is None:
+            continue
+        dense_levels += int(lg._info.max_component) > 0
+        so, sg = lo.splitting, lg.splitting
+        assert [tuple(p) for p in sg.pairs] == [(p.dof1, p.dof2, p.sign1, p.sign2, p.tail, p.mid, p.head)
+                                               for p in so.pairs]
+        assert np.array_equal(sg.interior_dofs, so.interior_dofs)
+        assert same_pattern(lg.P, lo.P), f"P_{ell} pattern"
+        assert rel(lg.P.data, lo.P.data) <= c.tol, f"P_{ell} values"
+        # A_{l+1} is the Galerkin product of the exported P (Schur form in the dense regime)
+        M = lg.P.T @ (lg.A @ lg.P)
+        assert rel(P.csr(0.5 * (M + M.T)).toarray(), hg.levels[ell + 1].A.toarray()) <= 1e-12
+    if name.startswith("kuhn"):
+        assert dense_levels >= 1, "the dense-regime path was not taken"
+    check_solves(c, ho, hg)
+
+
+@pytest.mark.parametrize("sweep", SWEEPS)
+def test_smoothing_legs_forced(oracle_case, sweep):
+    """Every smoothing-leg kernel (cluster leg, grid leg, per-wave launches,
+    dataflow leg) against the oracle's sequential OSS-l1 sweep."""
+    name, c, ho = oracle_case
+    hg = P.build_hierarchy(c.system, c.meta["method"], meshes=c.meshes, rmaps=c.rmaps)
+    set_options(hg, sweep=sweep)
+    check_solves(c, ho, hg)
+    # the smoother alone, both directions, from a nonzero iterate
+    rng = np.random.default_rng(7)
+    for ell, (lg, lo) in enumerate(zip(hg.levels[:-1], ho.levels[:-1])):
+        x0 = rng.standard_normal(lo.n)
+        bb = rng.standard_normal(lo.n)
+        for d in ("forward", "backward", "symmetric"):
+            xg = P.smoothers.smooth(lo.A, lg.patches, None, x0, bb, d)
+            xo = O.smooth(lo.A, lo.patches, lo.l1, x0, bb, d)
+            assert rel(xg, xo) <= max(1e-10, c.tol), (ell, d)
