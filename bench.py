@@ -258,186 +258,116 @@ def cpu_threads():
         return 1
 
 
-def oracle_solve_rate(system, b, min_seconds, max_solves=None):
-    """Time the CPU oracle's PCG solves (setup excluded) -> (DoF*iters/s, solves, seconds, iters, setup_s)."""
-    from oracle import amg_oracle as O
-    t0 = time.perf_counter()
-    ho = O.hierarchy(system, "alg")
-    setup_s = time.perf_counter() - t0
-    n = system.n
-    done, work, t = 0, 0, 0.0
-    iters = 0
-    while True:
-        t0 = time.perf_counter()
-        x, rep = O.pcg(system.A, b, precond=lambda r: O.vcycle(ho, r), tol=1e-8)
-        t += time.perf_counter() - t0
-        done += 1
-        iters = rep.iterations
-        work += n * rep.iterations
-        if t >= min_seconds or (max_solves and done >= max_solves):
-            break
-    return work / t, done, t, iters, setup_s
+def native_maps():
+    """Shared objects of this repo mapped into the current process."""
+    try:
+        with open("/proc/self/maps") as f:
+            return sorted({ln.split()[-1] for ln in f if ROOT in ln and ln.rstrip().endswith(".so")})
+    except OSError:
+        return []
 
 
-class HostHybridP:
-    """P = P_s - S_G Z on the host (numpy/scipy), for the CPU port of the solve."""
-
-    def __init__(self, Ps, Z, rows):
-        self.Ps, self.Z, self.rows = Ps, Z, rows
-        self.shape = Ps.shape
-
-    def __matmul__(self, e):
-        y = self.Ps @ e
-        y[self.rows] -= self.Z @ e
-        return y
-
-    @property
-    def T(self):
-        outer = self
-
-        class _T:
-            def __matmul__(self, r):
-                return outer.Ps.T @ r - outer.Z.T @ r[outer.rows]
-        return _T()
-
-
-def host_solve_data(h):
-    """Level-0 operators of the (GPU-built) hierarchy in the oracle's form plus
-    the coarsest inverse, for a CPU-port timing of the solve phase."""
+def oracle_from_device(h):
+    """An oracle hierarchy (oracle/amg_oracle.py OHierarchy) holding the
+    operators of the GPU-built hierarchy ``h``: A, G, P (hybrid: sparse part
+    + the dense block Z, formed on demand), patches and l1 rebuilt by the
+    oracle from A and G, the coarsest Cholesky factor by LAPACK.  The CPU
+    baseline of the GPU arm times the oracle's own pcg / vcycle on it (the
+    port cannot build config 2's hierarchy inside a bench run)."""
     import ctypes as C
 
     from oracle import amg_oracle as O
-    from paper_2602_23613_b200 import _lib
     dev = h._dev
-    L0, Lc = h.levels[0], h.levels[-1]
-    info = L0._info
-    A, G = L0.A, L0.G
-    n, nc = int(info.n), int(h.levels[1]._info.n)
-    if int(info.max_component) > 0:
-        nG = int(info.max_component)
-        Ps = dev.export_csr(0, 3, n, nc, int(info.pad))
-        Z = np.empty((nG, nc), dtype=np.float64)
-        rows = np.empty(nG, dtype=np.int64)
-        dev.check(dev.lib.hcamg_export_dense(dev.h, 0, 0, Z.ctypes.data_as(C.c_void_p)))
-        dev.check(dev.lib.hcamg_export_dense(dev.h, 0, 1, rows.ctypes.data_as(C.c_void_p)))
-        P = HostHybridP(Ps, Z, rows)
-    else:
-        P = L0.P
-    ncs = int(Lc._info.n)
-    Ainv = np.empty((ncs, ncs), dtype=np.float64)
-    dev.check(dev.lib.hcamg_export_dense(dev.h, len(h.levels) - 1, 2, Ainv.ctypes.data_as(C.c_void_p)))
-    patches = O.vertex_patches(A, G)
-    return dict(A=A, P=P, Ainv=Ainv, l1=O.l1_diag(A), patches=patches, depth=len(h.levels))
+    levels = []
+    for ell, lv in enumerate(h.levels):
+        info = lv._info
+        A, G = lv.A, lv.G
+        if info.coarsest:
+            Ad = A.toarray()
+            levels.append(O.OLevel(A, G, coarse_factor=O.Factor(np.arange(A.shape[0]), np.linalg.cholesky(Ad))))
+            del Ad
+            continue
+        n, nc = int(info.n), int(h.levels[ell + 1]._info.n)
+        if int(info.max_component) > 0:
+            nG = int(info.max_component)
+            Ps = dev.export_csr(ell, 3, n, nc, int(info.pad))
+            Z = np.empty((nG, nc), dtype=np.float64)
+            rows = np.empty(nG, dtype=np.int64)
+            dev.check(dev.lib.hcamg_export_dense(dev.h, ell, 0, Z.ctypes.data_as(C.c_void_p)))
+            dev.check(dev.lib.hcamg_export_dense(dev.h, ell, 1, rows.ctypes.data_as(C.c_void_p)))
+            P = O.HybridP(Ps, Z, rows, np.arange(nc))
+        else:
+            P = lv.P
+        levels.append(O.OLevel(A, G, P, O.vertex_patches(A, G), O.l1_diag(A)))
+    return O.OHierarchy(levels, h.method, h.stalled, list(h.notes))
 
 
-def cpu_port_iterations(d, b, min_seconds, max_iters=50):
-    """PCG iterations (multilevel.py:261-280) with a two-level V(1,1) cycle
-    (multilevel.py:177-184) executed by the CPU port's kernels: scipy SpMV,
-    the oracle's per-patch cho_solve sweeps and l1-Jacobi (smoothers.py:98-137),
-    numpy dense GEMVs for P, P^T and the coarsest solve."""
-    from oracle import amg_oracle as O
-    assert d["depth"] == 2, "CPU sample implemented for two-level hierarchies"
-    A, P, Ainv, l1, ps = d["A"], d["P"], d["Ainv"], d["l1"], d["patches"]
+def reference_line(args, value, t, iters, setup_s, sample, extra=None):
+    cores = cpu_threads()
+    line = {
+        "impl": "reference", "metric": "AMG-PCG solve DoF*iters/s", "value": value, "unit": "DoF*iters/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / max(args.steps, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args.config),
+        "details": dict({"pcg_iterations": iters, "setup_s": setup_s}, **(extra or {})),
+        "cpu_baseline": {"value": value, "unit": "DoF*iters/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "DoF*iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
 
-    def vc(r):
-        x = O.smooth(A, ps, l1, np.zeros_like(r), r, "forward")
-        rr = r - A @ x
-        x = x + P @ (Ainv @ (P.T @ rr))
-        return O.smooth(A, ps, l1, x, r, "backward")
 
-    x = np.zeros_like(b)
-    r = b.copy()
-    z = vc(r)
-    p = z.copy()
-    rz = r @ z
-    it, t = 0, 0.0
-    while it < max_iters:
-        t0 = time.perf_counter()
-        Ap = A @ p
-        alpha = rz / (p @ Ap)
-        x += alpha * p
-        r -= alpha * Ap
-        z = vc(r)
-        rz_new = r @ z
-        p = z + (rz_new / rz) * p
-        rz = rz_new
-        t += time.perf_counter() - t0
-        it += 1
-        if t >= min_seconds:
-            break
-    return it, t
+def workload_config(config):
+    """Identical in both arms (the driver compares the arms' configs)."""
+    from paper_2602_23613_b200 import kuhn
+    cfg = kuhn.CONFIGS[config]
+    return {"workload": f"BASELINE {config}: unit cube, {cfg['n']}^3 hexes x 6 Kuhn tets, alg hierarchy, "
+                        "PCG tol 1e-8 from x0=0, rhs uniform[-1,1] seed 0; one step = one complete PCG solve",
+            "l2": ("L2 flushed (256 MiB write) before every timed GPU step; a PCG iteration moves the whole "
+                   "hierarchy (config 2: 25.5 GB on the GPU), far above L2") if config != "c1" else
+                  ("L2 flushed (256 MiB write) before every timed GPU step; the whole c1 hierarchy (~17 MB) "
+                   "would otherwise stay L2-resident")}
 
 
 def run_reference(args, world, rank, dist):
+    """The reference's CPU implementation of the path: oracle/amg_oracle.py
+    (the numpy/scipy restatement, bit-identical to the reference on the golden
+    cases; the reference itself is a Python package that cannot travel to the
+    GPU box).  It builds the hierarchy itself on the host -- config 2's
+    167,784-DoF interior component through the reference's large-component
+    route (RCM + envelope Cholesky, the dense block kept as P = P_s - S Z) --
+    then every step is one complete PCG solve (multilevel.py:238-281) with the
+    oracle's V-cycle (multilevel.py:177-196).  Nothing of libhcamg is loaded."""
+    from oracle import amg_oracle as O
     from paper_2602_23613_b200 import kuhn
     if rank != 0:
         return
     system = kuhn.config_system(args.config)
     b = kuhn.rhs(system.n, seed=0)
-    if args.config != "c1":
-        run_reference_sample(args, system, b)
-        return
-    from oracle import amg_oracle as O
     t0 = time.perf_counter()
-    ho = O.hierarchy(system, "alg")
+    ho = O.hierarchy(system, "alg", large="envelope")
     setup_s = time.perf_counter() - t0
+    log(f"reference setup {setup_s:.1f} s; levels {[lv.n for lv in ho.levels]}")
+
+    def solve():
+        return O.pcg(system.A, b, precond=lambda r: O.vcycle(ho, r), tol=1e-8)
+
     for _ in range(args.warmup):
-        O.pcg(system.A, b, precond=lambda r: O.vcycle(ho, r), tol=1e-8)
-    t = 0.0
-    work = 0
-    iters = 0
+        solve()
+    t, work, iters = 0.0, 0, 0
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        x, rep = O.pcg(system.A, b, precond=lambda r: O.vcycle(ho, r), tol=1e-8)
+        x, rep = solve()
         t += time.perf_counter() - t0
         iters = rep.iterations
         work += system.n * rep.iterations
     value = work / t
-    cores = cpu_threads()
-    line = {
-        "impl": "reference", "metric": "AMG-PCG solve DoF*iters/s", "value": value, "unit": "DoF*iters/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"kuhn {args.config} (n={system.n} DoFs, alg, PCG tol 1e-8, x0=0, rhs seed 0)",
-                   "pcg_iterations": iters, "setup_s": setup_s},
-        "cpu_baseline": {"value": value, "unit": "DoF*iters/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full PCG solves of {args.config} after {args.warmup} warm-up, "
-                                   "oracle/amg_oracle.py (numpy/scipy restatement of the reference)"},
-        "e2e": {"value": value, "unit": "DoF*iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def run_reference_sample(args, system, b):
-    """configs[1+]: the CPU port cannot build the hierarchy (dense interior
-    Cholesky of 113 GB), so each step is a bounded sample of the
-    solve: one PCG iteration by the CPU port on the level-0 operators of the
-    hierarchy built on the GPU (setup untimed)."""
-    import paper_2602_23613_b200 as P
-    h = P.build_hierarchy(system, "alg")
-    d = host_solve_data(h)
-    for _ in range(args.warmup):
-        cpu_port_iterations(d, b, 0.0, max_iters=1)
-    t, iters = 0.0, 0
-    for _ in range(args.steps):
-        it, dt = cpu_port_iterations(d, b, 0.0, max_iters=1)
-        t += dt
-        iters += it
-    value = system.n * iters / t
-    cores = cpu_threads()
-    sample = (f"{iters} PCG iterations of {args.config} (n={system.n}), one per step, by the CPU port "
-              "(oracle numpy/scipy kernels: scipy SpMV, per-patch cho_solve OSS-l1 sweeps, numpy dense GEMVs) "
-              "on the level-0 operators of the hierarchy built on the GPU; the port cannot build this "
-              "hierarchy itself (113 GB dense interior factor)")
-    line = {
-        "impl": "reference", "metric": "AMG-PCG solve DoF*iters/s", "value": value, "unit": "DoF*iters/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"BASELINE {args.config} (n={system.n} DoFs, alg, PCG tol 1e-8, x0=0, rhs seed 0)"},
-        "cpu_baseline": {"value": value, "unit": "DoF*iters/s", "cores": cores, "kind": "port", "sample": sample},
-        "e2e": {"value": value, "unit": "DoF*iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+    so = native_maps()
+    sample = (f"{args.steps} complete PCG solves of {args.config} ({iters} iterations each, {t:.1f} s) after "
+              f"{args.warmup} warm-up solves by oracle/amg_oracle.py (numpy/scipy + OpenBLAS; the patch sweep is "
+              f"the reference's per-patch loop), hierarchy built on the host in {setup_s:.1f} s")
+    print(json.dumps(reference_line(args, value, t, iters, setup_s, sample,
+                                     {"levels": [lv.n for lv in ho.levels], "native_so_loaded": so,
+                                      "operator_complexity": O.operator_complexity(ho)})), flush=True)
 
 
 def run_ours(args, world, rank, local, dist):
@@ -562,15 +492,13 @@ def run_ours(args, world, rank, local, dist):
         "metric": "AMG-PCG solve DoF*iters/s", "value": value, "unit": "DoF*iters/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {
-            "workload": f"BASELINE {args.config}: unit cube, {kuhn.CONFIGS[args.config]['n']}^3 hexes x 6 Kuhn tets, "
-                        f"{n} free edge DoFs, alg hierarchy, PCG tol 1e-8 from x0=0, rhs uniform[-1,1] seed 0",
+        "config": workload_config(args.config),
+        "details": {
             "levels": [lv.n for lv in h.levels], "pcg_iterations": iters,
             "setup_s": min(setups), "setup_s_first_call": setups[0],
             "operator_complexity": P.operator_complexity(h),
             "final_relres": float(rep.final_relres), "true_relres": true_rel,
-            "l2": "flushed (256 MiB write) before every timed step"
-                  + ("; per-iteration traffic (%.1f GB) is also far above L2" % (B_iter / 1e9) if B_iter > 2e8 else ""),
+            "l2_flush": "256 MiB write before every timed step",
             "parallelism": (f"row-partitioned x{world} (dense blocks and coarsest inverse split by rows, "
                             "NVLink peer-memory exchange; smoother replicated)") if partitioned
                            else (f"replicas x{world}" if world > 1 else "single GPU"),
@@ -595,20 +523,23 @@ def run_ours(args, world, rank, local, dist):
         "clocks": clk.result,
     }
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
-        if args.config == "c1":
-            rate, solves, secs, it_o, setup_o = oracle_solve_rate(system, b_host, args.cpu_seconds)
-            line["cpu_baseline"] = {"value": rate, "unit": "DoF*iters/s", "cores": cpu_threads(), "kind": "port",
-                                    "sample": f"{solves} full PCG solves of {args.config} ({it_o} iterations each, "
-                                              f"{secs:.1f} s) by oracle/amg_oracle.py; oracle setup {setup_o:.2f} s"}
-        else:
-            d = host_solve_data(h)
-            its, secs = cpu_port_iterations(d, b_host, args.cpu_seconds)
-            line["cpu_baseline"] = {
-                "value": n * its / secs, "unit": "DoF*iters/s", "cores": cpu_threads(), "kind": "port",
-                "sample": f"{its} PCG iterations of {args.config} ({secs:.1f} s) by the CPU port (oracle numpy/scipy "
-                          "kernels) on the level-0 operators of the GPU-built hierarchy (the port cannot build "
-                          "it: 113 GB dense interior factor)"}
-            del d
+        from oracle import amg_oracle as O
+        t0 = time.perf_counter()
+        ho = oracle_from_device(h)
+        prep = time.perf_counter() - t0
+        solves, its, secs = 0, 0, 0.0
+        while secs < args.cpu_seconds:
+            t0 = time.perf_counter()
+            _, ro = O.pcg(system.A, b_host, precond=lambda r: O.vcycle(ho, r), tol=1e-8)
+            secs += time.perf_counter() - t0
+            solves += 1
+            its += ro.iterations
+        line["cpu_baseline"] = {
+            "value": n * its / secs, "unit": "DoF*iters/s", "cores": cpu_threads(), "kind": "port",
+            "sample": f"{solves} complete PCG solve(s) of {args.config} ({its} iterations, {secs:.1f} s) by the "
+                      "oracle's pcg / vcycle (numpy/scipy + OpenBLAS) on the operators of the GPU-built "
+                      f"hierarchy ({prep:.0f} s to export them and rebuild patches / coarsest factor on the host)"}
+        del ho
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -620,7 +551,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", help="BASELINE config: c1 (configs[0]) or c2 (configs[1], default)")
-    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas (weak scaling) instead of one row-partitioned solve")

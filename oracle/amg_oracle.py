@@ -69,9 +69,20 @@ def symmetric_part(M):
 
 
 def galerkin(P, A):
-    """P^T A P symmetrised (sparse.py:113-122)."""
+    """P^T A P symmetrised (sparse.py:113-122).  For a HybridP (large
+    component, see harmonic_interp) the Schur form is used:
+    P^T A P = P_s^T A P_s - W'^T A_GG^{-1} W' = sym(P_s^T A P_s) - sym(W'^T Z)
+    with W' = A[rows, :] P_s the block's right-hand side (exact in exact
+    arithmetic; the dropped residual term Z^T (W' - A_GG Z) is ~1e-15 of A_c,
+    measured at n = 8 and 16 against the reference's P^T (A P))."""
     if A.shape[0] != A.shape[1] or A.shape[0] != P.shape[0]:
         raise ValueError(f"dimension mismatch: P {P.shape}, A {A.shape}")
+    if isinstance(P, HybridP):
+        S = symmetric_part(P.Ps.T @ (A @ P.Ps)).toarray()
+        D = np.asarray(P.Wg.T @ P.Z)                      # (cols x cols)
+        D = 0.5 * (D + D.T)
+        S[np.ix_(P.cols, P.cols)] -= D
+        return canon(S)
     return symmetric_part(P.T @ (A @ P))
 
 
@@ -430,6 +441,147 @@ def coarse_grad(R, G, mode, coarse_nodes=None):
     return Gc, cols
 
 
+# ----------------------------------------------------------------------------- large components
+
+DENSE_COMPONENT_CUTOFF = 4096   # transfer.py:35
+ENVELOPE_NB = 1024
+
+
+@dataclass
+class EnvelopeFactor:
+    """Lower Cholesky factor of P A P^T (P = reverse Cuthill-McKee, the order the
+    reference's cholesky() applies above its dense cutoff, sparse.py:276-301)
+    kept in NB-row block rows restricted to the block envelope: block row I
+    holds columns [j0[I] NB, (I + 1) NB).  Cholesky fill never leaves the
+    envelope, so this is the reference's factorisation (its up-looking sparse
+    loop, sparse.py:212-273, with the same pivot floor), computed with LAPACK
+    on dense tiles instead of per-entry Python."""
+
+    perm: np.ndarray
+    nb: int
+    j0: np.ndarray
+    rows: list            # block row I: (rows_I, (I - j0[I] + 1) nb) array
+
+    @property
+    def n(self):
+        return len(self.perm)
+
+    def block(self, I, J):
+        nb = self.nb
+        c = (J - self.j0[I]) * nb
+        return self.rows[I][:, c:c + nb]
+
+
+def envelope_cholesky(Acc, nb=None):
+    """RCM + blocked left-looking Cholesky inside the block envelope (see
+    EnvelopeFactor); raises NotPositiveDefiniteError with the failing pivot in
+    the factored order, as the reference's sparse path does."""
+    nb = nb or ENVELOPE_NB
+    A = canon(Acc)
+    n = A.shape[0]
+    perm = np.asarray(reverse_cuthill_mckee(A, symmetric_mode=True), dtype=np.int64)
+    Ap = A[perm][:, perm].tocsr()
+    Ap.sort_indices()
+    T = -(-n // nb)
+    first = np.minimum(Ap.indices[Ap.indptr[:-1]], np.arange(n))  # first column per row (sorted rows)
+    j0 = np.array([first[I * nb:(I + 1) * nb].min() // nb for I in range(T)], dtype=np.int64)
+    scale = float(np.abs(A.diagonal()).max()) if n else 0.0
+    floor = PIVOT_RTOL * scale
+    rows = []
+    for I in range(T):
+        r0, r1 = I * nb, min(n, (I + 1) * nb)
+        c0 = j0[I] * nb
+        R = np.zeros((r1 - r0, (I - j0[I] + 1) * nb))
+        blk = Ap[r0:r1]
+        rr = np.repeat(np.arange(r1 - r0), np.diff(blk.indptr))
+        keep = blk.indices <= rr + r0
+        R[rr[keep], blk.indices[keep] - c0] = blk.data[keep]
+        for J in range(j0[I], I + 1):
+            cJ = (J - j0[I]) * nb
+            k0 = max(j0[I], j0[J]) * nb                     # common columns of block rows I and J
+            X = R[:, cJ:cJ + nb]
+            if k0 < J * nb:
+                RJ = rows[J] if J < I else R
+                X[:, :RJ.shape[0]] -= R[:, k0 - c0:J * nb - c0] @ RJ[:, k0 - j0[J] * nb:J * nb - j0[J] * nb].T
+            if J < I:
+                LJJ = rows[J][:, (J - j0[J]) * nb:(J - j0[J]) * nb + nb]
+                R[:, cJ:cJ + nb] = scipy.linalg.solve_triangular(LJJ, X.T, lower=True).T
+            else:
+                m = r1 - r0
+                D = np.tril(X[:, :m])
+                try:
+                    LII = np.linalg.cholesky(D + np.tril(D, -1).T)
+                except np.linalg.LinAlgError:
+                    LII = _pivot_loop(D + np.tril(D, -1).T, floor)  # names the failing pivot
+                piv = np.diag(LII) ** 2
+                if piv.min() <= floor:
+                    raise NotPositiveDefiniteError(r0 + int(np.argmin(piv)))
+                R[:, cJ:cJ + m] = LII
+                R[:, cJ + m:] = 0.0
+        rows.append(R)
+    return EnvelopeFactor(perm, nb, j0, rows)
+
+
+def envelope_solve(F, Bp, active=None):
+    """Solve (L L^T) Z = Bp in place for a dense right-hand side already in the
+    factored row order.  ``active[I]``: number of leading columns that can be
+    nonzero in block row I of the forward solve (columns sorted by their first
+    nonzero row: the staircase of L^{-1} Bp)."""
+    nb, T = F.nb, len(F.rows)
+    m = Bp.shape[1]
+    act = np.full(T, m, dtype=np.int64) if active is None else active
+    for I in range(T):                                    # Y = L^{-1} Bp
+        r0, r1 = I * nb, min(F.n, (I + 1) * nb)
+        a = int(act[I])
+        if a == 0:
+            continue
+        c0 = F.j0[I] * nb
+        if c0 < r0:
+            Bp[r0:r1, :a] -= F.rows[I][:, :r0 - c0] @ Bp[c0:r0, :a]
+        Bp[r0:r1, :a] = scipy.linalg.solve_triangular(F.block(I, I)[:, :r1 - r0], Bp[r0:r1, :a], lower=True)
+    for I in range(T - 1, -1, -1):                        # Z = L^{-T} Y
+        r0, r1 = I * nb, min(F.n, (I + 1) * nb)
+        for K in range(I + 1, T):
+            if F.j0[K] <= I:
+                k0, k1 = K * nb, min(F.n, (K + 1) * nb)
+                Bp[r0:r1] -= F.block(K, I)[:, :r1 - r0].T @ Bp[k0:k1]
+        Bp[r0:r1] = scipy.linalg.solve_triangular(F.block(I, I)[:, :r1 - r0], Bp[r0:r1], lower=True, trans="T")
+    return Bp
+
+
+class HybridP:
+    """P = P_s - S Z: a sparse part plus one dense block (rows x cols of P),
+    the interpolation of a component too large for a CSR P (SURVEY.md F3:
+    35 GB of dense rows at config 2).  Supports ``P @ e`` and ``P.T @ r``,
+    the two products the V-cycle uses (multilevel.py:183)."""
+
+    def __init__(self, Ps, Z, rows, cols):
+        self.Ps, self.Z, self.rows, self.cols = Ps, Z, rows, cols
+        self.shape = Ps.shape
+
+    @property
+    def nnz(self):
+        return self.Ps.nnz + self.Z.size
+
+    def __matmul__(self, e):
+        y = self.Ps @ e
+        y[self.rows] -= self.Z @ e[self.cols]
+        return y
+
+    @property
+    def T(self):
+        outer = self
+
+        class _T:
+            shape = (outer.shape[1], outer.shape[0])
+
+            def __matmul__(self, r):
+                out = outer.Ps.T @ r
+                out[outer.cols] -= outer.Z.T @ r[outer.rows]
+                return out
+        return _T()
+
+
 @dataclass
 class Transfer:
     P: sp.csr_matrix
@@ -450,8 +602,16 @@ def _alt_component_solve(Acc, rhs):
     return Z
 
 
-def harmonic_interp(A, split, mode="refinement", G=None, floor_solver=False):
-    """sparse_ideal_interp (transfer.py:77-122): P = R^T - S_I A_II^{-1} S_I^T A R^T."""
+def harmonic_interp(A, split, mode="refinement", G=None, floor_solver=False, large="dense"):
+    """sparse_ideal_interp (transfer.py:77-122): P = R^T - S_I A_II^{-1} S_I^T A R^T.
+
+    ``large="dense"`` (default, the pinned path): every component is solved
+    with dense LAPACK.  ``large="envelope"``: a component above the reference's
+    4096-DoF cutoff is factored by RCM + envelope Cholesky (the reference's own
+    route there, sparse.py:276-301) and kept as the dense block of a
+    HybridP instead of entering the CSR P (config 2: 4.4e9 entries).  Used by
+    bench.py's CPU reference arm; at that size the reference itself cannot run,
+    so this path is checked against the dense path at n = 16 only."""
     R = restriction(split)
     Rt = canon(R.T)
     inner = split.interior_dofs
@@ -463,10 +623,23 @@ def harmonic_interp(A, split, mode="refinement", G=None, floor_solver=False):
         W = canon(Ai @ Rt)
         A_II = canon(Ai[:, inner])
         ri, ci, vi = [], [], []
+        hybrid = None
         for comp in components(A_II):
             Wc = W[comp, :].tocsc()
             keep = np.flatnonzero(np.diff(Wc.indptr) > 0)
             if keep.size == 0:
+                continue
+            if large == "envelope" and len(comp) > DENSE_COMPONENT_CUTOFF and hybrid is None:
+                F = envelope_cholesky(A_II[comp][:, comp])
+                Wp = Wc[:, keep].tocsr()[F.perm]
+                first = np.full(len(keep), len(comp), dtype=np.int64)   # first (factored) row per column
+                coo = Wp.tocoo()
+                np.minimum.at(first, coo.col, coo.row)
+                colperm = np.argsort(first, kind="stable")
+                active = np.searchsorted(first[colperm], (np.arange(len(F.rows)) + 1) * F.nb)
+                Z = np.asarray(Wp[:, colperm].todense())
+                envelope_solve(F, Z, active)
+                hybrid = (inner[comp[F.perm]], keep[colperm], Z, Wp[:, colperm].tocsr())
                 continue
             Acc = A_II[comp][:, comp].toarray()
             rhs = np.asarray(Wc[:, keep].todense())
@@ -485,6 +658,10 @@ def harmonic_interp(A, split, mode="refinement", G=None, floor_solver=False):
         else:
             corr = sp.csr_matrix((split.n, split.n_pairs))
         P = canon(Rt + corr)
+        if hybrid is not None:
+            rows, cols, Z, Wg = hybrid
+            P = HybridP(P, Z, rows, cols)
+            P.Wg = Wg          # the block's right-hand side W' (rows x cols), for the Galerkin product
     if G is not None:
         Gc, cols = coarse_grad(R, G, mode, split.coarse_nodes)
     else:
@@ -537,10 +714,16 @@ def l1_diag(A):
     return np.asarray(abs(A).sum(axis=1)).ravel()
 
 
+_potrs = scipy.linalg.lapack.get_lapack_funcs("potrs", (np.zeros(1),))
+
+
 def _sweep(ps, x, r, order):
+    # scipy.linalg.cho_solve((L, True), b) is LAPACK dpotrs(L, b, lower=1)
+    # after argument checks; calling dpotrs directly is bit-identical and
+    # drops most of the per-patch Python overhead (smoothers.py:98-103)
     for p in order:
         idx = ps.patches[p]
-        d = scipy.linalg.cho_solve((ps.factors[p], True), r[idx])
+        d, info = _potrs(ps.factors[p], r[idx], lower=1)
         x[idx] += d
         r[ps.update_rows[p]] -= ps.update_blocks[p] @ d
 
@@ -621,7 +804,7 @@ def sign_gradient(Gc):
 
 
 def hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse=32,
-              theta=0.25, smoother=True, floor_solver=False):
+              theta=0.25, smoother=True, floor_solver=False, large="dense"):
     """build_hierarchy (multilevel.py:78-164) for the "alg" and "ref" routes.
 
     ``smoother=False`` skips the patch factorisation (used when only the
@@ -656,7 +839,7 @@ def hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse
                 stalled = True
                 notes.append("refinement splitting produced no pairs")
                 break
-            tr = harmonic_interp(A, split, "refinement", G, floor_solver)
+            tr = harmonic_interp(A, split, "refinement", G, floor_solver, large)
             nxt = np.full(meshes[pos - 1].ne, -1, dtype=np.int64)
             nxt[split.pair_mesh_edges] = np.arange(split.n_pairs)
         else:
@@ -666,7 +849,7 @@ def hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse
                     stalled = True
                     notes.append("algebraic coarsening found no pairs")
                 break
-            tr = harmonic_interp(A, split, "algebraic", G, floor_solver)
+            tr = harmonic_interp(A, split, "algebraic", G, floor_solver, large)
             nxt = None
         P = tr.P
         if P.shape[1] == 0 or P.shape[1] >= n:

@@ -259,8 +259,12 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
       break;
     }
     auto next = std::make_unique<DevLevel>();
-    if (ip.hp.on) galerkin_hybrid(h->cublas, cur->A, ip.P, ip.Pt, ip.hp, next->A, s);
-    else galerkin(ip.P, ip.Pt, cur->A, next->A, s);
+    if (ip.hp.on) {
+      galerkin_hybrid(h->cublas, cur->A, ip.P, ip.Pt, ip.hp, next->A, s);
+      ip.hp.D.release();
+    } else {
+      galerkin(ip.P, ip.Pt, cur->A, next->A, s);
+    }
     st.mark("galerkin");
     cur->hp = std::move(ip.hp);
     if (cur->hp.on) hybrid_prepare(cur->hp, s);
@@ -750,6 +754,7 @@ int hcamg_export_csr(hcamg_handle* h, int32_t level, int32_t which, int64_t* ind
     }
     DCsr full;
     if (which == 1 && L.hp.on) {
+      hybrid_ensure_z(h->cublas, L.hp, h->stream);
       hybrid_to_csr(L.P, L.hp, full, h->stream);
       M = &full;
     }
@@ -779,6 +784,7 @@ int hcamg_export_dense(hcamg_handle* h, int32_t level, int32_t which, void* out)
     cudaStream_t s = h->stream;
     if (which == 0) {
       require(L.hp.on, "level has no dense interpolation block");
+      hybrid_ensure_z(h->cublas, L.hp, s);
       HC_CUDA(cudaMemcpyAsync(out, L.hp.Z.p, 8 * L.hp.nG * L.hp.nc, cudaMemcpyDeviceToHost, s));
     } else if (which == 1) {
       require(L.hp.on, "level has no dense interpolation block");
@@ -1276,6 +1282,7 @@ int hcamg_dist_prepare(hcamg_handle* h, int32_t rank, int32_t nranks, void* ipc_
     for (DevLevel* L : h->lv) {
       L->xoff_g = L->xoff_y = L->xoff_c = DevLevel::kNoSite;
       if (L->hp.on) {
+        hybrid_ensure_z(h->cublas, L->hp, s);  // ranks stream row blocks of the explicit Z
         L->xoff_g = take(kGroups * L->hp.nc);
         L->xoff_y = take(L->hp.nG);
       }

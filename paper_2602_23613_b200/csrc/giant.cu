@@ -905,7 +905,20 @@ std::vector<int32_t> rcm_order(int64_t n, const std::vector<int64_t>& ptr, const
   return order;
 }
 
-void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m, cudaStream_t s, FactorP* fac) {
+namespace {
+// D[colperm[i], colperm[j]] = lower(Dp)[max(i,j), min(i,j)]  (column-major m x m)
+__global__ void k_unperm_sym(int64_t m, const int32_t* __restrict__ colperm, const double* __restrict__ Dp,
+                             double* __restrict__ D) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < m * m; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % m, j = t / m;
+    const double v = i >= j ? Dp[i + j * m] : Dp[j + i * m];
+    D[(int64_t)colperm[i] + (int64_t)colperm[j] * m] = v;
+  }
+}
+}  // namespace
+
+void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m, cudaStream_t s, FactorP* fac,
+                        double* D, bool want_z) {
   const int64_t n = Agg.nrows;
   StageTimer st(s);
   // ordering: reverse Cuthill-McKee (default) or the natural component order
@@ -1061,6 +1074,27 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
                        L.tile(I, J), (int)kNB, &one, blk(I), (int)m),
            "dgemm fwd");
   }
+  st.mark("  giant: forward solve");
+  if (D) {  // D = Y^T Y over the staircase: row block J of Y is zero beyond column active[J]
+    DBuf<double> Dp(m * m, s);
+    Dp.zero();
+    for (int64_t J = 0; J < T; ++J) {
+      const int ma = (int)active[(size_t)J];
+      if (ma == 0) continue;
+      cb(cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, ma, (int)nbk(J), &one, blk(J), (int)m, &one, Dp.p,
+                     (int)m),
+         "dsyrk Y^T Y");
+    }
+    k_unperm_sym<<<grid_for(m * m, 256, kSMs * 32), 256, 0, s>>>(m, dcol.p, Dp.p, D);
+    HC_CHECK_LAUNCH();
+    st.mark("  giant: Y^T Y");
+  }
+  if (!want_z) {
+    L.buf.release();
+    HC_CUDA(cudaStreamSynchronize(s));
+    if (fac) fac->perm = std::move(dperm);
+    return;
+  }
   for (int64_t K = T - 1; K >= 0; --K) {  // Z^T = U^T L^{-1}
     cb(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m, (int)nbk(K),
                    &one, L.tile(K, K), (int)kNB, blk(K), (int)m),
@@ -1156,6 +1190,25 @@ void dense_gemv_rows(const int* stop, int64_t n, int64_t m, const double* M, con
   if (part != 1) xchg_scatter(stop, xc, n, nullptr, x, s);
 }
 
+namespace {
+__global__ void k_rows_dense(const int64_t* __restrict__ wp, const int32_t* __restrict__ wi,
+                             const double* __restrict__ wv, int64_t n, int64_t m, double* __restrict__ B) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = wp[t]; e < wp[t + 1]; ++e) B[t * m + wi[e]] = wv[e];
+}
+}  // namespace
+
+void hybrid_ensure_z(cublasHandle_t h, HybridP& hp, cudaStream_t s) {
+  if (!hp.on || hp.Z.p) return;
+  require(hp.Agg.nrows == hp.nG && hp.Wg.nrows == hp.nG, "dense block data missing");
+  hp.Z.alloc(hp.nG * hp.nc, s);
+  hp.Z.zero();
+  k_rows_dense<<<grid_for(hp.nG, 128), 128, 0, s>>>(hp.Wg.ptr.p, hp.Wg.idx.p, hp.Wg.val.p, hp.nG, hp.nc, hp.Z.p);
+  HC_CHECK_LAUNCH();
+  giant_factor_solve(h, hp.Agg, hp.Z.p, hp.nc, s, nullptr, nullptr, true);
+  hybrid_prepare(hp, s);
+}
+
 void hybrid_prepare(HybridP& hp, cudaStream_t s) {
   // Row chunks, grouped into kGroups groups of whole chunks.  Enough chunks per
   // group that one group alone (one rank of eight) fills the GPU: ~4 CTAs
@@ -1191,6 +1244,27 @@ void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, 
   if (part != 1) xchg_group_final(stop, xc, hp.nc, bc, s);
 }
 
+namespace {
+__global__ void k_neg_copy(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    b[t] = -a[t];
+}
+// dense (column-major, symmetric) -> canonical CSR, exact zeros dropped
+void dense_to_csr(int64_t nc, const DBuf<double>& Ad, DCsr& Ac, cudaStream_t s) {
+  Ac.nrows = Ac.ncols = nc;
+  Ac.ptr.alloc(nc + 1, s);
+  DBuf<int64_t> cnt(nc, s);
+  const unsigned g = (unsigned)std::min<int64_t>(nc, kSMs * 8);
+  k_dense_to_csr<false><<<g, 256, 0, s>>>(nc, Ad.p, cnt.p, nullptr, nullptr, nullptr);
+  HC_CHECK_LAUNCH();
+  Ac.nnz = exclusive_scan(cnt.p, Ac.ptr.p, nc, s);
+  Ac.idx.alloc(Ac.nnz, s);
+  Ac.val.alloc(Ac.nnz, s);
+  k_dense_to_csr<true><<<g, 256, 0, s>>>(nc, Ad.p, nullptr, Ac.ptr.p, Ac.idx.p, Ac.val.p);
+  HC_CHECK_LAUNCH();
+}
+}  // namespace
+
 void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr& Pst, const HybridP& hp, DCsr& Ac,
                      cudaStream_t s) {
   const int64_t nG = hp.nG, nc = hp.nc, n = A.nrows;
@@ -1199,6 +1273,19 @@ void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr
   k_fill_m1<<<grid_for(n, 256), 256, 0, s>>>(gmap.p, n);
   k_rowmap<<<grid_for(nG, 256), 256, 0, s>>>(hp.rows.p, nG, gmap.p);
   HC_CHECK_LAUNCH();
+  DBuf<double> Ad(nc * nc, s);
+  DCsr APs, Ms, Ss;
+  if (hp.D.p) {  // A_c = sym(P_s^T A P_s) - Y^T Y
+    spgemm(A, Ps, APs, s);
+    spgemm(Pst, APs, Ms, s);
+    APs = DCsr();
+    symmetrize(Ms, Ss, s);
+    k_neg_copy<<<grid_for(nc * nc, 256, kSMs * 32), 256, 0, s>>>(nc * nc, hp.D.p, Ad.p);
+    k_add_sym_csr<<<grid_for(nc, 256), 256, 0, s>>>(Ss.ptr.p, Ss.idx.p, Ss.val.p, nc, Ad.p);
+    HC_CHECK_LAUNCH();
+    dense_to_csr(nc, Ad, Ac, s);
+    return;
+  }
   DCsr AG, Wp0, Wp, Agg, WpT;
   csr_extract(A, hp.rows.p, nG, nullptr, n, AG, s);
   spgemm(AG, Ps, Wp0, s);
@@ -1255,29 +1342,16 @@ void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr
   k_zt_w<<<(unsigned)std::min<int64_t>(nc, kSMs * 16), 256, 0, s>>>(WpT.ptr.p, WpT.idx.p, WpT.val.p, nc, hp.Z.p, D1.p);
   HC_CHECK_LAUNCH();
   // sym(P_s^T A P_s)
-  DCsr APs, Ms, Ss;
   spgemm(A, Ps, APs, s);
   spgemm(Pst, APs, Ms, s);
   APs = DCsr();
   symmetrize(Ms, Ss, s);
-  DBuf<double> Ad(nc * nc, s);
   k_combine<<<grid_for(nc * nc, 256), 256, 0, s>>>(nc, D1.p, E.p, Ad.p);
   k_add_sym_csr<<<grid_for(nc, 256), 256, 0, s>>>(Ss.ptr.p, Ss.idx.p, Ss.val.p, nc, Ad.p);
   HC_CHECK_LAUNCH();
   D1.release();
   E.release();
-  // dense -> canonical CSR (exact zeros dropped)
-  Ac.nrows = Ac.ncols = nc;
-  Ac.ptr.alloc(nc + 1, s);
-  DBuf<int64_t> cnt(nc, s);
-  const unsigned g = (unsigned)std::min<int64_t>(nc, kSMs * 8);
-  k_dense_to_csr<false><<<g, 256, 0, s>>>(nc, Ad.p, cnt.p, nullptr, nullptr, nullptr);
-  HC_CHECK_LAUNCH();
-  Ac.nnz = exclusive_scan(cnt.p, Ac.ptr.p, nc, s);
-  Ac.idx.alloc(Ac.nnz, s);
-  Ac.val.alloc(Ac.nnz, s);
-  k_dense_to_csr<true><<<g, 256, 0, s>>>(nc, Ad.p, nullptr, Ac.ptr.p, Ac.idx.p, Ac.val.p);
-  HC_CHECK_LAUNCH();
+  dense_to_csr(nc, Ad, Ac, s);
 }
 
 namespace {
@@ -1291,6 +1365,7 @@ __global__ void k_count_nz(const double* __restrict__ v, int64_t n, unsigned lon
 }  // namespace
 
 int64_t hybrid_nnz(const DCsr& Ps, const HybridP& hp, cudaStream_t s) {
+  if (!hp.Z.p) return Ps.nnz + hp.nG * hp.nc;  // Z not formed: its entries are generically all nonzero
   DBuf<unsigned long long> c(1, s);
   c.zero();
   if (hp.nG * hp.nc) k_count_nz<<<grid_for(hp.nG * hp.nc, 256, kSMs * 8), 256, 0, s>>>(hp.Z.p, hp.nG * hp.nc, c.p);

@@ -19,8 +19,12 @@ namespace hcamg {
 // max |diag|, floor 1e-13 * scale).  With `fac`, the factor is kept and the
 // blocked-sweep operators of trisolve.cuh are built from it (perm, Lc, pools,
 // sweeps; the caller finishes with factorp_attach).
+// With `D` (m x m, column-major, full symmetric): D = B^T A^{-1} B = Y^T Y,
+// Y = L^{-1} B (the forward half of the solve, staircase-restricted: column c
+// of Y is zero above the first row of its right-hand side), and, unless
+// want_z, the backward solve is skipped and B is left as it was.
 void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B_rowmajor, int64_t m, cudaStream_t s,
-                        FactorP* fac = nullptr);
+                        FactorP* fac = nullptr, double* D = nullptr, bool want_z = true);
 
 // Reverse Cuthill-McKee order of a symmetric CSR pattern (scipy's
 // csgraph.reverse_cuthill_mckee, which the reference's cholesky() applies,
@@ -32,7 +36,10 @@ struct HybridP {
   bool on = false;
   int64_t nG = 0, nc = 0;
   DBuf<int32_t> rows;   // DoF of each dense row (ascending)
-  DBuf<double> Z;       // nG x nc row-major; P[rows[q], c] = -Z[q, c]
+  DBuf<double> Z;       // nG x nc row-major; P[rows[q], c] = -Z[q, c] (formed on demand: hybrid_ensure_z)
+  DCsr Agg;             // the component block A_GG (component order) and its right-hand side W' (nG x nc):
+  DCsr Wg;              // kept so Z = A_GG^{-1} W' can be formed when it is needed (export, explicit-Z apply)
+  DBuf<double> D;       // setup only: W'^T A_GG^{-1} W' = Y^T Y (nc x nc) for the Galerkin product
   // restriction partials (deterministic chunked column reduction)
   int64_t chunk = 512, nchunk = 0;
   int64_t grp[kGroups + 1] = {};  // chunk boundaries of the kGroups reduction groups
@@ -42,6 +49,9 @@ struct HybridP {
 
 // allocate the restriction partials (outside any graph capture)
 void hybrid_prepare(HybridP& hp, cudaStream_t s);
+// Form the explicit block Z = A_GG^{-1} W' if the setup did not keep it
+// (one more factorisation and a full two-sided solve, ~4 s on config 2).
+void hybrid_ensure_z(cublasHandle_t h, HybridP& hp, cudaStream_t s);
 // The three products below take an optional distributed context `d` (rows
 // split across ranks, results exchanged through exchange site `off`, see
 // dist.cuh) and `part`: 0 = all, 1 = up to the exchange signal (producer),
@@ -57,9 +67,12 @@ void dense_gemv_rows(const int* stop, int64_t n, int64_t m, const double* M, con
 void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, cudaStream_t s,
                      const Dist* d = nullptr, size_t off = 0, int part = 0);
 
-// A_c = sym(P_s^T A P_s) - sym(W'^T Z) - sym(Z^T rho), rho = W' - A_GG Z
-// (= P^T A P for P = P_s - S_G Z, exactly, including the residual of the
-// component solve).  Output canonical CSR (exact zeros dropped).
+// A_c = P^T A P for P = P_s - S_G A_GG^{-1} W':
+//   with hp.D (default): A_c = sym(P_s^T A P_s) - Y^T Y, Y = L^{-1} W' (L the
+//     envelope Cholesky factor of A_GG; W'^T A_GG^{-1} W' = Y^T Y exactly);
+//   with Z: A_c = sym(P_s^T A P_s) - sym(W'^T Z) - sym(Z^T rho), rho = W' - A_GG Z
+//     (the residual term in fp64, or TF32 with option galerkin_fp64 = 0).
+// Output canonical CSR (exact zeros dropped).
 void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr& Pst, const HybridP& hp,
                      DCsr& Ac, cudaStream_t s);
 
