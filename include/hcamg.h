@@ -63,6 +63,8 @@ typedef struct {
   int32_t pad;
   double operator_complexity;   /* multilevel.py:199-201 */
   double setup_seconds;         /* device-synchronised wall time of the setup */
+  double setup_flops;           /* FP64 flops of the dense setup work (Cholesky, triangular solves, Y^T Y,
+                                   coarsest factor and inverse), counted from the call dimensions */
 } hcamg_info;
 
 /* Per-level sizes for exports. */

@@ -804,7 +804,7 @@ def sign_gradient(Gc):
 
 
 def hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse=32,
-              theta=0.25, smoother=True, floor_solver=False, large="dense"):
+              theta=0.25, smoother=True, floor_solver=False, large="dense", log=None):
     """build_hierarchy (multilevel.py:78-164) for the "alg" and "ref" routes.
 
     ``smoother=False`` skips the patch factorisation (used when only the
@@ -825,6 +825,15 @@ def hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse
         dof_edges = np.full(system.n, -1, dtype=np.int64)
         live = np.flatnonzero(e2d >= 0)
         dof_edges[e2d[live]] = live
+    import time as _time
+    t_last = [_time.perf_counter()]
+
+    def mark(what):
+        if log is not None:
+            now = _time.perf_counter()
+            log(f"oracle setup: {what} {now - t_last[0]:.1f} s")
+            t_last[0] = now
+
     while True:
         n = A.shape[0]
         if n <= min_coarse or len(levels) + 1 >= max_levels:
@@ -844,12 +853,14 @@ def hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse
             nxt[split.pair_mesh_edges] = np.arange(split.n_pairs)
         else:
             split = algebraic_split(A, G, theta, dof_edges if not levels else None)
+            mark(f"level {len(levels)} splitting (n={n})")
             if split.n_pairs == 0 or split.n_pairs >= n:
                 if split.n_pairs == 0:
                     stalled = True
                     notes.append("algebraic coarsening found no pairs")
                 break
             tr = harmonic_interp(A, split, "algebraic", G, floor_solver, large)
+            mark(f"level {len(levels)} interpolation")
             nxt = None
         P = tr.P
         if P.shape[1] == 0 or P.shape[1] >= n:
@@ -858,11 +869,14 @@ def hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_coarse
             break
         levels.append(OLevel(A, G, P, vertex_patches(A, G) if smoother else None, l1_diag(A),
                              splitting=split, transfer=tr))
+        mark(f"level {len(levels) - 1} patches")
         A = galerkin(P, A)
+        mark(f"level {len(levels) - 1} galerkin")
         G = sign_gradient(tr.Gc)
         e2d = nxt
         pos -= 1
     levels.append(OLevel(A, G, coarse_factor=factor_coarsest(A)))
+    mark("coarsest factor")
     return OHierarchy(levels, method, stalled, notes)
 
 

@@ -48,7 +48,7 @@ class Report(C.Structure):
 
 class Info(C.Structure):
     _fields_ = [("depth", C.c_int32), ("stalled", C.c_int32), ("method", C.c_int32), ("pad", C.c_int32),
-                ("operator_complexity", C.c_double), ("setup_seconds", C.c_double)]
+                ("operator_complexity", C.c_double), ("setup_seconds", C.c_double), ("setup_flops", C.c_double)]
 
 
 class LevelInfo(C.Structure):

@@ -52,7 +52,7 @@ struct hcamg_handle {
   bool stalled = false;
   int method = 1;
   std::vector<std::string> notes;
-  double setup_seconds = 0.0;
+  double setup_seconds = 0.0, setup_flops = 0.0;
   Workspace ws;
   Graph g_vc, g_pcg, g_amg;
   DBuf<double> vc_b, vc_x;
@@ -209,6 +209,7 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
   require(Gh->nrows == Ah->nrows, "G rows must match A");
   HC_CUDA(cudaStreamSynchronize(s));
   auto t0 = std::chrono::steady_clock::now();
+  take_flops();
   StageTimer st(s);
   auto cur = std::make_unique<DevLevel>();
   upload_csr(Ah, cur->A, s);
@@ -293,6 +294,7 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
   refresh_views(h);
   HC_CUDA(cudaStreamSynchronize(s));
   h->setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  h->setup_flops = take_flops();
   // hand the setup's transient buffers (tens of GB on config 2) back to the
   // device: the private pool keeps freed memory only while a build runs
   if (h->pool) HC_CUDA(cudaMemPoolTrimTo(h->pool, 0));
@@ -307,6 +309,7 @@ void fill_info(hcamg_handle* h, hcamg_info* info) {
   for (auto& l : h->levels) tot += (double)l->A.nnz;
   info->operator_complexity = h->levels.empty() || h->levels[0]->A.nnz == 0 ? 0.0 : tot / (double)h->levels[0]->A.nnz;
   info->setup_seconds = h->setup_seconds;
+  info->setup_flops = h->setup_flops;
 }
 
 // ---- graphs
@@ -580,7 +583,12 @@ int hcamg_set_option(hcamg_handle* h, const char* key, double value) {
     require(k != nullptr, std::string("unknown option ") + (key ? key : "(null)"));
     if (k->i) {
       require(value == (double)(int)value, std::string("option ") + key + " takes an integer");
-      if (k->i == &Options::sweep) require(value >= SWEEP_AUTO && value <= SWEEP_FLOW, "sweep mode out of range");
+      if (k->i == &Options::sweep) {
+        require(value >= SWEEP_AUTO && value <= SWEEP_FLOW, "sweep mode out of range");
+        if (value == SWEEP_FLOW)  // the dataflow terms are built on first request
+          for (auto& l : h->levels)
+            if (!l->coarsest && l->l1.p) build_flow(l->A, l->sm, h->stream);
+      }
       h->opts.*(k->i) = (int)value;
     } else {
       require(value == (double)(int64_t)value, std::string("option ") + key + " takes an integer");

@@ -184,4 +184,9 @@ struct PoolScope {
 };
 cudaMemPool_t current_pool();
 
+// FP64 flops of the dense setup work issued while a handle's setup runs
+// (counted at each level-3 call from its dimensions; hcamg_info.setup_flops).
+void count_flops(double f);
+double take_flops();
+
 }  // namespace hcamg

@@ -166,6 +166,7 @@ int64_t dense_cholesky_raw(cublasHandle_t h, double* A, int64_t k, int64_t ld, d
     const int nb = (int)std::min<int64_t>(kTile, k - kb);
     double* Akk = A + kb + kb * ld;
     k_potrf_tile<<<1, kTileThreads, smem, s>>>(Akk, ld, nb, piv + kb, bad.p);
+    count_flops((double)nb * nb * nb / 3.0);
     HC_CHECK_LAUNCH();
     int b = read_scalar(bad.p, s);
     if (b >= 0) return kb + b;
@@ -175,6 +176,7 @@ int64_t dense_cholesky_raw(cublasHandle_t h, double* A, int64_t k, int64_t ld, d
       double* A22 = A21 + nb * ld;
       cublas_check(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
                                (int)rest, nb, &one, Akk, (int)ld, A21, (int)ld), "dtrsm");
+      count_flops((double)rest * nb * nb + (double)rest * rest * nb);
       cublas_check(cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, (int)rest, nb, &mone, A21, (int)ld, &one,
                                A22, (int)ld), "dsyrk");
     }
@@ -249,6 +251,7 @@ void dense_spd_inverse(cublasHandle_t h, double* Lbuf, int64_t n, double* Ainv, 
     cublas_check(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m,
                              (int)nb, &one, Lbuf + j0 + j0 * n, (int)n, Ainv + j0 + j0 * n, (int)n),
                  "dtrsm L^-1 panel");
+    count_flops((double)m * m * nb);
   }
   StageTimer st(s);
   st.mark("    inverse: Y = L^-1");
@@ -259,6 +262,7 @@ void dense_spd_inverse(cublasHandle_t h, double* Lbuf, int64_t n, double* Ainv, 
                              (int)nb, &one, Ainv + j0 + j0 * n, (int)n, Ainv + j0 + j0 * n, (int)n,
                              Lbuf + j0 + j0 * n, (int)n),
                  "dtrmm Y^T Y");
+    count_flops((double)m * m * nb);
   }
   st.mark("    inverse: lower(Y^T Y)");
   k_sym_from_lower<<<grid_for(n * n, 256, kSMs * 32), 256, 0, s>>>(Lbuf, n, Ainv);
@@ -274,6 +278,7 @@ void dense_cholesky_solve(cublasHandle_t h, const double* L, int64_t k, int64_t 
                            (int)nrhs, &one, L, (int)ld, B, (int)ldb), "dtrsm L");
   cublas_check(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)k,
                            (int)nrhs, &one, L, (int)ld, B, (int)ldb), "dtrsm L^T");
+  count_flops(2.0 * k * k * nrhs);
 }
 
 }  // namespace hcamg

@@ -724,6 +724,7 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
     cb(cublasDtrsmBatched(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)kSB,
                           (int)kSB, &one, dl.p, (int)LDS, de.p, (int)kSB, (int)TS),
        "dtrsmBatched Linv");
+    count_flops((double)TS * kSB * kSB * kSB);
     HC_CUDA(cudaStreamSynchronize(s));
     std::vector<const double*> src;
     std::vector<double*> dst;
@@ -744,6 +745,7 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
     cb(cublasDgemmBatched(h, ta, ta, (int)kSB, (int)kSB, (int)kSB, &one, da.p, (int)LDS, db.p, (int)kSB, &zero, dc.p,
                           (int)kSB, (int)ha.size()),
        what);
+    count_flops(2.0 * kSB * kSB * kSB * (double)ha.size());
     HC_CUDA(cudaStreamSynchronize(s));
   };
   {  // row-major M_I = column-major (L_{I,I-1}^T Linv_II^T)
@@ -981,7 +983,7 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
   DBuf<const double*> dC;
   int64_t fail = -1;
   for (int64_t K = 0; K < T; ++K) {  // right-looking, inside the envelope
-    const int64_t j0 = dense_cholesky_raw(h, L.tile(K, K), kNB, kNB, piv.p + K * kNB, s);
+    const int64_t j0 = dense_cholesky_raw(h, L.tile(K, K), kNB, kNB, piv.p + K * kNB, s);  // counts its own flops
     if (j0 < kNB) {
       fail = K * kNB + j0;
       break;
@@ -998,6 +1000,7 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
       cb(cublasDtrsmBatched(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)kNB,
                             (int)kNB, &one, pa, (int)kNB, (double* const*)pb, (int)kNB, (int)below.size()),
          "dtrsmBatched");
+      count_flops((double)kNB * kNB * kNB * (double)below.size());
     }
     {
       std::vector<const double*> ha, hb, hc;
@@ -1013,6 +1016,7 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
       cb(cublasDgemmBatched(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)kNB, (int)kNB, (int)kNB, &mone, pa, (int)kNB, pb,
                             (int)kNB, &one, (double* const*)pc, (int)kNB, (int)ha.size()),
          "dgemmBatched");
+      count_flops(2.0 * kNB * kNB * kNB * (double)ha.size());
       HC_CUDA(cudaStreamSynchronize(s));  // host pointer vectors go out of scope
     }
   }
@@ -1068,11 +1072,14 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
     cb(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, ma, (int)nbk(J),
                    &one, L.tile(J, J), (int)kNB, blk(J), (int)m),
        "dtrsm fwd");
+    count_flops((double)ma * nbk(J) * nbk(J));
     for (int64_t I = J + 1; I < T; ++I)
-      if (L.has(I, J))
+      if (L.has(I, J)) {
         cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, ma, (int)nbk(I), (int)nbk(J), &mone, blk(J), (int)m,
                        L.tile(I, J), (int)kNB, &one, blk(I), (int)m),
            "dgemm fwd");
+        count_flops(2.0 * ma * nbk(I) * nbk(J));
+      }
   }
   st.mark("  giant: forward solve");
   if (D) {  // D = Y^T Y over the staircase: row block J of Y is zero beyond column active[J]
@@ -1084,6 +1091,7 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
       cb(cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, ma, (int)nbk(J), &one, blk(J), (int)m, &one, Dp.p,
                      (int)m),
          "dsyrk Y^T Y");
+      count_flops((double)ma * (ma + 1) * nbk(J));
     }
     k_unperm_sym<<<grid_for(m * m, 256, kSMs * 32), 256, 0, s>>>(m, dcol.p, Dp.p, D);
     HC_CHECK_LAUNCH();
@@ -1099,10 +1107,13 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
     cb(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m, (int)nbk(K),
                    &one, L.tile(K, K), (int)kNB, blk(K), (int)m),
        "dtrsm bwd");
-    for (int64_t I = L.j0[(size_t)K]; I < K; ++I)
+    count_flops((double)m * nbk(K) * nbk(K));
+    for (int64_t I = L.j0[(size_t)K]; I < K; ++I) {
       cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)m, (int)kNB, (int)nbk(K), &mone, blk(K), (int)m, L.tile(K, I),
                      (int)kNB, &one, blk(I), (int)m),
          "dgemm bwd");
+      count_flops(2.0 * m * kNB * nbk(K));
+    }
   }
   st.mark("  giant: triangular solves");
   L.buf.release();

@@ -24,6 +24,17 @@ struct SweepProgram {
   DBuf<unsigned> gbar;  // grid-barrier word of the cooperative leg (sense-reversing, starts 0)
 };
 
+// Dataflow-leg program (flow.cu): per direction the pulled terms of every
+// patch entry and its correction slots.
+struct FlowProgram {
+  bool built = false;
+  int64_t ne = 0;
+  DBuf<int32_t> tp[2], tslot[2];
+  DBuf<double> tval[2], d[2];
+  DBuf<int2> ent;
+  DBuf<unsigned> bar;
+};
+
 // OSS-l1 smoother data in wavefront order (smoothers.py:60-137).
 //
 // Patches are renumbered wave-major: wave w holds patches [wave_ptr[w],
@@ -59,7 +70,14 @@ struct Smoother {
   // host copies for export (reference PatchSet layout, original patch order)
   std::vector<int64_t> h_patch_ptr, h_patch_dofs;
   SweepProgram pg;
+  FlowProgram fl;
 };
+
+// Build the dataflow-leg terms of a smoother (once; a no-op when a DoF lies
+// in more than two patches -- the leg then falls back to the grid leg).
+void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s);
+// Waves wider than one 16-CTA cluster (the auto mode runs such levels on the whole GPU).
+bool smoother_wide(const Smoother& sm);
 
 void build_program(Smoother& sm, SweepProgram& pg, cudaStream_t s);
 

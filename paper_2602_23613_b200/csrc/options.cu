@@ -43,6 +43,16 @@ const Options& opts() {
 OptionsScope::OptionsScope(const Options* o) : prev(t_opts) { t_opts = o; }
 OptionsScope::~OptionsScope() { t_opts = prev; }
 
+namespace {
+thread_local double t_flops = 0.0;
+}
+void count_flops(double f) { t_flops += f; }
+double take_flops() {
+  const double f = t_flops;
+  t_flops = 0.0;
+  return f;
+}
+
 PoolScope::PoolScope(cudaMemPool_t p) : prev(t_pool) { t_pool = p; }
 PoolScope::~PoolScope() { t_pool = prev; }
 cudaMemPool_t current_pool() { return t_pool; }

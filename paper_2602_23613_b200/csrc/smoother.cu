@@ -467,7 +467,77 @@ void build_smoother(const DCsr& A, const DCsr& G, Smoother& sm, cudaStream_t s) 
     sm.max_gen_rows = std::max(sm.max_gen_rows, sm.gen_fw_ptr[(size_t)w + 1] - sm.gen_fw_ptr[(size_t)w]);
     sm.max_gen_rows = std::max(sm.max_gen_rows, sm.gen_bw_ptr[(size_t)w + 1] - sm.gen_bw_ptr[(size_t)w]);
   }
+  if (smoother_wide(sm) || opts().sweep == SWEEP_FLOW) build_flow(A, sm, s);
   HC_CUDA(cudaStreamSynchronize(s));
+}
+
+bool smoother_wide(const Smoother& sm) { return sm.max_wave_patches > 256 || sm.max_gen_rows > 8192; }
+
+// Pulled terms of the dataflow leg (flow.cu).  Entry e = (patch q, DoF u) of
+// the wave-major patch list pulls, for every j coupled to u and every entry
+// e' = (patch p, DoF j) of a patch p != q that runs before q in the sweep
+// direction, the term (e', A[u, j]): the reference's residual update
+// r[upd_p] -= A[upd_p, patch_p] d_p (smoothers.py:101-103) restricted to the
+// rows q reads, in the order q sees them.  Conflicting patches lie in
+// different waves, and for them "runs before" is "lower wave" (forward) /
+// "higher wave" (backward).  Host C++, once per level.
+void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
+  FlowProgram& f = sm.fl;
+  if (f.built) return;
+  const int64_t n = A.nrows, m = sm.npatch;
+  if (m == 0) return;
+  const std::vector<int64_t> pp = sm.patch_ptr.download();
+  const int64_t ne = pp[(size_t)m];
+  const std::vector<int32_t> dofs = sm.patch_dofs.download();
+  const std::vector<int64_t> ap = A.ptr.download();
+  const std::vector<int32_t> ai = A.idx.download();
+  const std::vector<double> av = A.val.download();
+  std::vector<int32_t> lev((size_t)m), pe((size_t)ne);
+  for (int64_t w = 0; w < sm.nwave; ++w)
+    for (int64_t t = sm.wave_ptr[(size_t)w]; t < sm.wave_ptr[(size_t)w + 1]; ++t) lev[(size_t)t] = (int32_t)w;
+  for (int64_t t = 0; t < m; ++t)
+    for (int64_t e = pp[(size_t)t]; e < pp[(size_t)t + 1]; ++e) pe[(size_t)e] = (int32_t)t;
+  std::vector<int2> ent((size_t)n, make_int2(-1, -1));
+  for (int64_t e = 0; e < ne; ++e) {
+    int2& en = ent[(size_t)dofs[(size_t)e]];
+    if (en.x < 0) en.x = (int32_t)e;
+    else if (en.y < 0) en.y = (int32_t)e;
+    else return;  // a DoF in more than two patches: the flow leg does not apply (grid leg instead)
+  }
+  for (int dir = 0; dir < 2; ++dir) {
+    std::vector<int32_t> tp((size_t)ne + 1, 0), ts;
+    std::vector<double> tv;
+    ts.reserve((size_t)ne * 16);
+    tv.reserve((size_t)ne * 16);
+    for (int64_t e = 0; e < ne; ++e) {
+      const int32_t q = pe[(size_t)e], u = dofs[(size_t)e], lq = lev[(size_t)q];
+      for (int64_t k = ap[(size_t)u]; k < ap[(size_t)u + 1]; ++k) {
+        const int2 en = ent[(size_t)ai[(size_t)k]];
+        for (int32_t e2 : {en.x, en.y}) {
+          if (e2 < 0) continue;
+          const int32_t p = pe[(size_t)e2];
+          if (p == q) continue;
+          if (dir == 0 ? lev[(size_t)p] < lq : lev[(size_t)p] > lq) {
+            ts.push_back(e2);
+            tv.push_back(av[(size_t)k]);
+          }
+        }
+      }
+      require(ts.size() < (size_t)INT32_MAX, "flow leg terms exceed int32 indexing");
+      tp[(size_t)e + 1] = (int32_t)ts.size();
+    }
+    f.tp[dir].upload(tp.data(), (int64_t)tp.size(), s);
+    f.tslot[dir].upload(ts.data(), std::max<int64_t>((int64_t)ts.size(), 1), s);
+    f.tval[dir].upload(tv.data(), std::max<int64_t>((int64_t)tv.size(), 1), s);
+    f.d[dir].alloc(ne, s);
+    flow_reset_slots(f.d[dir].p, ne, s);
+  }
+  f.ent.upload(ent.data(), n, s);
+  f.bar.alloc(1, s);
+  f.bar.zero();
+  f.ne = ne;
+  HC_CUDA(cudaStreamSynchronize(s));
+  f.built = true;
 }
 
 }  // namespace hcamg

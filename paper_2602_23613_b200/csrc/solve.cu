@@ -636,8 +636,42 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     return 1;
   }
   const bool down = pc == PC_DOWN;
-  const int m = opts().sweep;
-  const bool wide = L.sm.max_wave_patches > 256 || L.sm.max_gen_rows > 8192;
+  const bool wide = smoother_wide(L.sm);
+  int m = opts().sweep;
+  if (m == SWEEP_AUTO && wide && L.sm.fl.built) m = SWEEP_FLOW;
+  if (m == SWEEP_FLOW && !L.sm.fl.built) m = SWEEP_GRID;  // a DoF in > 2 patches (or not prepared)
+  if (m == SWEEP_FLOW) {
+    Smoother& sm = L.sm;
+    FlowProgram& fl = sm.fl;
+    const int dir = down ? 0 : 1;
+    FlowArgs fa{};
+    fa.stop = stop;
+    fa.n = n;
+    fa.nwave = sm.nwave;
+    fa.ne = fl.ne;
+    fa.wave_ptr = sm.d_wave_ptr.p;
+    fa.patch_ptr = sm.patch_ptr.p;
+    fa.dofs = sm.patch_dofs.p;
+    fa.binv_off = sm.binv_off.p;
+    fa.binv = sm.binv.p;
+    fa.tp = fl.tp[dir].p;
+    fa.tslot = fl.tslot[dir].p;
+    fa.tval = fl.tval[dir].p;
+    fa.d = fl.d[dir].p;
+    fa.ent = fl.ent.p;
+    fa.ap = L.A.ptr.p;
+    fa.ai = L.A.idx.p;
+    fa.av = L.A.val.p;
+    fa.l1 = L.l1.p;
+    fa.b = b;
+    fa.x = x;
+    fa.r = L.r.p;
+    fa.r1 = L.d0.p;
+    fa.dj = L.dj.p;
+    fa.bar = fl.bar.p;
+    launch_flow_leg(down, fa, s);
+    return 1;
+  }
   if (m == SWEEP_AUTO || m == SWEEP_LEG || m == SWEEP_GRID) {
     Smoother& sm = L.sm;
     SweepProgram& pg = sm.pg;

@@ -54,6 +54,34 @@ void launch_leg(bool down, const LegArgs& args, cudaStream_t s);
 void launch_leg_grid(bool down, const LegArgs& args, cudaStream_t s);
 int sweep_cluster_size();
 
+// Dataflow leg (flow.cu): per-entry correction slots, no barrier inside the sweep.
+struct FlowArgs {
+  const int* stop;
+  int64_t n, nwave, ne;
+  const int64_t* wave_ptr;   // device, nwave + 1 (wave-major patch order)
+  const int64_t* patch_ptr;  // reordered patch -> entries
+  const int32_t* dofs;       // entry -> DoF
+  const int64_t* binv_off;
+  const double* binv;        // column-major k x k inverses
+  const int32_t* tp;         // entry -> range of pulled terms (this direction)
+  const int32_t* tslot;      // term -> slot of an earlier coupled patch entry
+  const double* tval;        // term -> A[u, j]
+  double* d;                 // slots (sentinel between legs)
+  const int2* ent;           // DoF -> its (<= 2) entries, -1 padded
+  const int64_t* ap;
+  const int32_t* ai;
+  const double* av;
+  const double* l1;
+  const double* b;
+  double* x;
+  double* r;
+  double* r1;
+  double* dj;
+  unsigned* bar;
+};
+void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s);
+void flow_reset_slots(double* d, int64_t ne, cudaStream_t s);
+
 // y = T v for a CSR T with long rows: fixed 256-entry segments, one warp each,
 // then an in-order reduction of the segment partials (deterministic).
 struct SegPlan {

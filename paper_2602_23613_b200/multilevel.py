@@ -329,6 +329,7 @@ def build_hierarchy(system, method, meshes=None, rmaps=None, max_levels=20, min_
     h._key = _hier_key(h)
     h._host_A = (system.A, A)
     h.setup_seconds = float(info.setup_seconds)
+    h.setup_flops = float(info.setup_flops)
     return h
 
 

@@ -32,7 +32,7 @@ VARIANTS = {
     # dense regime with the explicit Z block (row GEMV / chunked column sums)
     "dense_z": dict(DENSE, galerkin_fp64=1, factor_apply=0, coarse_symv=0),
 }
-SWEEPS = ["grid", "wave", "leg"]
+SWEEPS = ["grid", "wave", "leg", "flow"]
 
 
 def rel(a, b):
