@@ -455,12 +455,14 @@ class EnvelopeFactor:
     holds columns [j0[I] NB, (I + 1) NB).  Cholesky fill never leaves the
     envelope, so this is the reference's factorisation (its up-looking sparse
     loop, sparse.py:212-273, with the same pivot floor), computed with LAPACK
-    on dense tiles instead of per-entry Python."""
+    / BLAS-3 on dense tiles instead of per-entry Python.  ``inv[I]`` is the
+    inverse of the diagonal block (triangular solves become GEMMs)."""
 
     perm: np.ndarray
     nb: int
     j0: np.ndarray
     rows: list            # block row I: (rows_I, (I - j0[I] + 1) nb) array
+    inv: list             # inverse of the diagonal block of block row I
 
     @property
     def n(self):
@@ -487,7 +489,8 @@ def envelope_cholesky(Acc, nb=None):
     j0 = np.array([first[I * nb:(I + 1) * nb].min() // nb for I in range(T)], dtype=np.int64)
     scale = float(np.abs(A.diagonal()).max()) if n else 0.0
     floor = PIVOT_RTOL * scale
-    rows = []
+    potrf, trtri = scipy.linalg.lapack.dpotrf, scipy.linalg.lapack.dtrtri
+    rows, inv = [], []
     for I in range(T):
         r0, r1 = I * nb, min(n, (I + 1) * nb)
         c0 = j0[I] * nb
@@ -504,22 +507,24 @@ def envelope_cholesky(Acc, nb=None):
                 RJ = rows[J] if J < I else R
                 X[:, :RJ.shape[0]] -= R[:, k0 - c0:J * nb - c0] @ RJ[:, k0 - j0[J] * nb:J * nb - j0[J] * nb].T
             if J < I:
-                LJJ = rows[J][:, (J - j0[J]) * nb:(J - j0[J]) * nb + nb]
-                R[:, cJ:cJ + nb] = scipy.linalg.solve_triangular(LJJ, X.T, lower=True).T
+                R[:, cJ:cJ + nb] = X @ inv[J].T                  # L_IJ = A_IJ L_JJ^{-T}
             else:
                 m = r1 - r0
                 D = np.tril(X[:, :m])
-                try:
-                    LII = np.linalg.cholesky(D + np.tril(D, -1).T)
-                except np.linalg.LinAlgError:
-                    LII = _pivot_loop(D + np.tril(D, -1).T, floor)  # names the failing pivot
+                D = D + np.tril(D, -1).T
+                LII, info = potrf(D, lower=1, clean=1)
+                if info != 0:
+                    _pivot_loop(D, floor)                     # names the failing pivot
+                    raise NotPositiveDefiniteError(r0 + info - 1)
                 piv = np.diag(LII) ** 2
                 if piv.min() <= floor:
                     raise NotPositiveDefiniteError(r0 + int(np.argmin(piv)))
                 R[:, cJ:cJ + m] = LII
                 R[:, cJ + m:] = 0.0
+                Li, info = trtri(np.ascontiguousarray(LII), lower=1)
+                inv.append(np.tril(Li))
         rows.append(R)
-    return EnvelopeFactor(perm, nb, j0, rows)
+    return EnvelopeFactor(perm, nb, j0, rows, inv)
 
 
 def envelope_solve(F, Bp, active=None):
@@ -536,16 +541,18 @@ def envelope_solve(F, Bp, active=None):
         if a == 0:
             continue
         c0 = F.j0[I] * nb
+        X = Bp[r0:r1, :a]
         if c0 < r0:
-            Bp[r0:r1, :a] -= F.rows[I][:, :r0 - c0] @ Bp[c0:r0, :a]
-        Bp[r0:r1, :a] = scipy.linalg.solve_triangular(F.block(I, I)[:, :r1 - r0], Bp[r0:r1, :a], lower=True)
+            X -= F.rows[I][:, :r0 - c0] @ Bp[c0:r0, :a]
+        Bp[r0:r1, :a] = F.inv[I] @ X
     for I in range(T - 1, -1, -1):                        # Z = L^{-T} Y
         r0, r1 = I * nb, min(F.n, (I + 1) * nb)
+        X = Bp[r0:r1]
         for K in range(I + 1, T):
             if F.j0[K] <= I:
                 k0, k1 = K * nb, min(F.n, (K + 1) * nb)
-                Bp[r0:r1] -= F.block(K, I)[:, :r1 - r0].T @ Bp[k0:k1]
-        Bp[r0:r1] = scipy.linalg.solve_triangular(F.block(I, I)[:, :r1 - r0], Bp[r0:r1], lower=True, trans="T")
+                X -= F.block(K, I)[:, :r1 - r0].T @ Bp[k0:k1]
+        Bp[r0:r1] = F.inv[I].T @ X
     return Bp
 
 
