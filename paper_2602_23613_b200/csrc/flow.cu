@@ -72,82 +72,88 @@ struct GridBar {
   }
 };
 
-// sum of the pulled terms of one entry: spins on every slot still holding the sentinel
-__device__ __forceinline__ double pull_terms(const FlowArgs& a, int32_t t0, int32_t t1) {
-  double acc = 0.0;
-  for (int32_t t = t0; t < t1; t += 8) {
-    int32_t sl[8];
-    double w[8], v[8];
-    const int cnt = min(8, t1 - t);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      sl[i] = i < cnt ? __ldg(a.tslot + t + i) : -1;
-      w[i] = i < cnt ? __ldg(a.tval + t + i) : 0.0;
-    }
-    unsigned pending = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      v[i] = 0.0;
-      if (sl[i] >= 0) {
-        v[i] = ld_slot(a.d + sl[i]);
-        if (is_sentinel(v[i])) pending |= 1u << i;
-      }
-    }
-    while (pending) {
-      __nanosleep(32);
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        if (pending & (1u << i)) {
-          v[i] = ld_slot(a.d + sl[i]);
-          if (!is_sentinel(v[i])) pending &= ~(1u << i);
-        }
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc = fma(w[i], v[i], acc);
-  }
-  return acc;
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
 }
 
-__device__ __forceinline__ void flow_patch(const FlowArgs& a, int64_t p, int lane, const double* r0) {
-  const int64_t e0 = a.patch_ptr[p];
-  const int k = (int)(a.patch_ptr[p + 1] - e0);
+// Patch record (flow_record_layout, built by build_flow; 16-byte aligned):
+//   int32 {k, e0, nt, 0} | int32 dof[k4] | int32 tstart[kp4] | double binv[k*k] (row-major)
+//   | int32 tslot[nt4] | double tval[nt] | pad to 16
+__device__ __forceinline__ void rec_layout(int k, int nt, int& o_dof, int& o_ts, int& o_binv, int& o_slot,
+                                           int& o_val) {
+  const int k4 = (k + 3) & ~3, kp4 = (k + 1 + 3) & ~3, nt4 = (nt + 3) & ~3;
+  o_dof = 16;
+  o_ts = o_dof + 4 * k4;
+  o_binv = o_ts + 4 * kp4;
+  o_slot = o_binv + 8 * k * k;
+  o_val = o_slot + 4 * nt4;
+}
+
+// one patch from its staged record: v = r0[u] - sum of the pulled terms
+// (spinning on slots that still hold the sentinel), d = B_p^{-1} v
+__device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned char* rec, int lane, const double* r0) {
+  const int4 hd = *reinterpret_cast<const int4*>(rec);
+  const int k = hd.x, e0 = hd.y, nt = hd.z;
+  int o_dof, o_ts, o_binv, o_slot, o_val;
+  rec_layout(k, nt, o_dof, o_ts, o_binv, o_slot, o_val);
+  const int32_t* dof = reinterpret_cast<const int32_t*>(rec + o_dof);
+  const int32_t* ts = reinterpret_cast<const int32_t*>(rec + o_ts);
+  const double* binv = reinterpret_cast<const double*>(rec + o_binv);
+  const int32_t* tslot = reinterpret_cast<const int32_t*>(rec + o_slot);
+  const double* tval = reinterpret_cast<const double*>(rec + o_val);
   const bool act = lane < k;
-  const int64_t e = e0 + lane;
-  int32_t u = 0;
-  int32_t t0 = 0, t1 = 0;
   double v = 0.0;
   if (act) {
-    u = a.dofs[e];
-    t0 = a.tp[e];
-    t1 = a.tp[e + 1];
-    v = r0[u];
+    const double rv = r0[dof[lane]];
+    const int t0 = ts[lane], t1 = ts[lane + 1];
+    double acc = 0.0;
+    for (int t = t0; t < t1; t += 8) {
+      const int cnt = min(8, t1 - t);
+      double w[8], x[8];
+      int32_t sl[8];
+      unsigned pending = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        sl[i] = i < cnt ? tslot[t + i] : 0;
+        w[i] = i < cnt ? tval[t + i] : 0.0;
+        x[i] = 0.0;
+        if (i < cnt) {
+          x[i] = ld_slot(a.d + sl[i]);
+          if (is_sentinel(x[i])) pending |= 1u << i;
+        }
+      }
+      while (pending) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          if (pending & (1u << i)) {
+            x[i] = ld_slot(a.d + sl[i]);
+            if (!is_sentinel(x[i])) pending &= ~(1u << i);
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc = fma(w[i], x[i], acc);
+    }
+    v = rv - acc;
   }
-  // row `lane` of the k x k inverse (column-major), loaded before the spin
-  const double* Bi = a.binv + a.binv_off[p];
   double d = 0.0;
-  if (k <= 16) {
-    double brow[16];
-#pragma unroll
-    for (int c = 0; c < 16; ++c) brow[c] = (act && c < k) ? __ldg(Bi + (int64_t)c * k + lane) : 0.0;
-    if (act) v -= pull_terms(a, t0, t1);
-#pragma unroll
-    for (int c = 0; c < 16; ++c) d = fma(brow[c], __shfl_sync(0xffffffffu, v, c), d);
-  } else {
-    double brow[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) brow[c] = (act && c < k) ? __ldg(Bi + (int64_t)c * k + lane) : 0.0;
-    if (act) v -= pull_terms(a, t0, t1);
-#pragma unroll
-    for (int c = 0; c < 32; ++c) d = fma(brow[c], __shfl_sync(0xffffffffu, v, c), d);
-  }
-  if (act) st_slot(a.d + e, d);
+  const double* brow = binv + (act ? lane * k : 0);
+  for (int c = 0; c < k; ++c) d = fma(act ? brow[c] : 0.0, __shfl_sync(0xffffffffu, v, c), d);
+  if (act) st_slot(a.d + e0 + lane, d);
 }
 
 template <bool kDown>
 __global__ void __launch_bounds__(kFlowThreads, 1) k_flow_leg(FlowArgs a) {
   if (*a.stop) return;
   GridBar gb{a.bar};
-  const int64_t n = a.n, W = a.nwave;
+  const int64_t n = a.n;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -171,10 +177,43 @@ __global__ void __launch_bounds__(kFlowThreads, 1) k_flow_leg(FlowArgs a) {
     gb.sync();
   }
   const double* r0 = kDown ? a.b : a.r1;
-  for (int64_t s = 0; s < W; ++s) {
-    const int64_t w = kDown ? s : W - 1 - s;
-    const int64_t p0 = a.wave_ptr[w], p1 = a.wave_ptr[w + 1];
-    for (int64_t p = p0 + wg; p < p1; p += nw) flow_patch(a, p, lane, r0);
+  {
+    // each warp walks its patches (exec positions wg, wg + nw, ...) with the
+    // next record streamed into the other half of its double buffer by one
+    // cp.async.bulk while the current one waits on its predecessors
+    extern __shared__ __align__(16) unsigned char flow_smem[];
+    __shared__ __align__(8) unsigned long long bars[kFlowThreads / 32][2];
+    const int wl = threadIdx.x >> 5;
+    unsigned char* buf0 = flow_smem + (size_t)wl * 2 * a.recmax;
+    const uint32_t bar0 = smem_u32(&bars[wl][0]), bar1 = smem_u32(&bars[wl][1]);
+    if (lane == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    const unsigned char* recs = a.recs;
+    auto issue = [&](int64_t i, int b) {
+      const int64_t o = a.rec_off[i];
+      const uint32_t bytes = (uint32_t)(a.rec_off[i + 1] - o);
+      const uint32_t bar = b ? bar1 : bar0;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(buf0 + (size_t)b * a.recmax)),
+                   "l"(recs + o), "r"(bytes), "r"(bar)
+                   : "memory");
+    };
+    const int64_t m = a.npatch;
+    if (lane == 0 && wg < m) issue(wg, 0);
+    int64_t j = 0;
+    for (int64_t i = wg; i < m; i += nw, ++j) {
+      const int b = (int)(j & 1);
+      if (lane == 0 && i + nw < m) issue(i + nw, b ^ 1);
+      mbar_wait(b ? bar1 : bar0, (uint32_t)((j >> 1) & 1));
+      flow_patch(a, buf0 + (size_t)b * a.recmax, lane, r0);
+      __syncwarp();
+    }
   }
   gb.sync();
   if (kDown) {
@@ -232,14 +271,20 @@ void flow_reset_slots(double* d, int64_t ne, cudaStream_t s) {
   HC_CHECK_LAUNCH();
 }
 
+int64_t flow_smem_bytes(int64_t recmax) { return (kFlowThreads / 32) * 2 * recmax; }
+
 void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s) {
-  static int per_sm = 0;
-  if (!per_sm) {
-    int a = 0, b = 0;
-    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_flow_leg<true>, kFlowThreads, 0));
-    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_flow_leg<false>, kFlowThreads, 0));
-    per_sm = std::max(1, std::min(a, b));
+  const size_t smem = (size_t)flow_smem_bytes(args.recmax);
+  static size_t attr = 0;
+  if (smem > attr) {
+    HC_CUDA(cudaFuncSetAttribute(k_flow_leg<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HC_CUDA(cudaFuncSetAttribute(k_flow_leg<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
   }
+  int a = 0, b = 0;
+  HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_flow_leg<true>, kFlowThreads, smem));
+  HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_flow_leg<false>, kFlowThreads, smem));
+  const int per_sm = std::max(1, std::min(a, b));
   int dev = 0, sms = kSMs;
   HC_CUDA(cudaGetDevice(&dev));
   HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -248,6 +293,7 @@ void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)blocks);
   cfg.blockDim = dim3(kFlowThreads);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeCooperative;

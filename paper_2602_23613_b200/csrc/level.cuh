@@ -28,9 +28,10 @@ struct SweepProgram {
 // patch entry and its correction slots.
 struct FlowProgram {
   bool built = false;
-  int64_t ne = 0;
-  DBuf<int32_t> tp[2], tslot[2];
-  DBuf<double> tval[2], d[2];
+  int64_t ne = 0, recmax = 0;
+  DBuf<unsigned char> recs[2];   // per direction: one record per patch, in execution order
+  DBuf<int64_t> rec_off[2];
+  DBuf<double> d[2];
   DBuf<int2> ent;
   DBuf<unsigned> bar;
 };

@@ -11,6 +11,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstring>
 
 #include "dense.cuh"
 #include "smoother.cuh"
@@ -504,34 +505,81 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
     else if (en.y < 0) en.y = (int32_t)e;
     else return;  // a DoF in more than two patches: the flow leg does not apply (grid leg instead)
   }
+  const std::vector<int64_t> boff = sm.binv_off.download();
+  const std::vector<double> binv = sm.binv.download();
+  int64_t recmax = 0;
+  std::vector<std::vector<unsigned char>> recs(2);
+  std::vector<std::vector<int64_t>> offs(2);
   for (int dir = 0; dir < 2; ++dir) {
-    std::vector<int32_t> tp((size_t)ne + 1, 0), ts;
+    // execution order: waves ascending (forward) / descending (backward), patches ascending within a wave
+    std::vector<int64_t> order;
+    order.reserve((size_t)m);
+    for (int64_t s0 = 0; s0 < sm.nwave; ++s0) {
+      const int64_t w = dir == 0 ? s0 : sm.nwave - 1 - s0;
+      for (int64_t t = sm.wave_ptr[(size_t)w]; t < sm.wave_ptr[(size_t)w + 1]; ++t) order.push_back(t);
+    }
+    std::vector<unsigned char>& R = recs[(size_t)dir];
+    std::vector<int64_t>& off = offs[(size_t)dir];
+    off.assign(1, 0);
+    std::vector<int32_t> ts, tstart;
     std::vector<double> tv;
-    ts.reserve((size_t)ne * 16);
-    tv.reserve((size_t)ne * 16);
-    for (int64_t e = 0; e < ne; ++e) {
-      const int32_t q = pe[(size_t)e], u = dofs[(size_t)e], lq = lev[(size_t)q];
-      for (int64_t k = ap[(size_t)u]; k < ap[(size_t)u + 1]; ++k) {
-        const int2 en = ent[(size_t)ai[(size_t)k]];
-        for (int32_t e2 : {en.x, en.y}) {
-          if (e2 < 0) continue;
-          const int32_t p = pe[(size_t)e2];
-          if (p == q) continue;
-          if (dir == 0 ? lev[(size_t)p] < lq : lev[(size_t)p] > lq) {
-            ts.push_back(e2);
-            tv.push_back(av[(size_t)k]);
+    for (int64_t q : order) {
+      const int64_t e0 = pp[(size_t)q], k = pp[(size_t)q + 1] - e0;
+      const int32_t lq = lev[(size_t)q];
+      ts.clear();
+      tv.clear();
+      tstart.assign(1, 0);
+      for (int64_t a = 0; a < k; ++a) {
+        const int32_t u = dofs[(size_t)(e0 + a)];
+        for (int64_t kk = ap[(size_t)u]; kk < ap[(size_t)u + 1]; ++kk) {
+          const int2 en = ent[(size_t)ai[(size_t)kk]];
+          for (int32_t e2 : {en.x, en.y}) {
+            if (e2 < 0) continue;
+            const int32_t p = pe[(size_t)e2];
+            if (p == (int32_t)q) continue;
+            if (dir == 0 ? lev[(size_t)p] < lq : lev[(size_t)p] > lq) {
+              ts.push_back(e2);
+              tv.push_back(av[(size_t)kk]);
+            }
           }
         }
+        tstart.push_back((int32_t)ts.size());
       }
-      require(ts.size() < (size_t)INT32_MAX, "flow leg terms exceed int32 indexing");
-      tp[(size_t)e + 1] = (int32_t)ts.size();
+      const int64_t nt = (int64_t)ts.size();
+      const int64_t k4 = (k + 3) & ~3, kp4 = (k + 1 + 3) & ~3, nt4 = (nt + 3) & ~3;
+      const int64_t o_dof = 16, o_ts = o_dof + 4 * k4, o_binv = o_ts + 4 * kp4, o_slot = o_binv + 8 * k * k,
+                    o_val = o_slot + 4 * nt4, bytes = (o_val + 8 * nt + 15) & ~(int64_t)15;
+      const size_t base = R.size();
+      R.resize(base + (size_t)bytes, 0);
+      unsigned char* r = R.data() + base;
+      const int32_t hd[4] = {(int32_t)k, (int32_t)e0, (int32_t)nt, 0};
+      memcpy(r, hd, 16);
+      for (int64_t a = 0; a < k; ++a) {
+        const int32_t u = dofs[(size_t)(e0 + a)];
+        memcpy(r + o_dof + 4 * a, &u, 4);
+      }
+      memcpy(r + o_ts, tstart.data(), 4 * tstart.size());
+      for (int64_t a = 0; a < k; ++a)          // row-major: binv_rm[a k + c] = B^{-1}[a, c] (stored column-major)
+        for (int64_t c = 0; c < k; ++c) {
+          const double v = binv[(size_t)(boff[(size_t)q] + c * k + a)];
+          memcpy(r + o_binv + 8 * (a * k + c), &v, 8);
+        }
+      if (nt) {
+        memcpy(r + o_slot, ts.data(), 4 * (size_t)nt);
+        memcpy(r + o_val, tv.data(), 8 * (size_t)nt);
+      }
+      recmax = std::max(recmax, bytes);
+      off.push_back((int64_t)R.size());
     }
-    f.tp[dir].upload(tp.data(), (int64_t)tp.size(), s);
-    f.tslot[dir].upload(ts.data(), std::max<int64_t>((int64_t)ts.size(), 1), s);
-    f.tval[dir].upload(tv.data(), std::max<int64_t>((int64_t)tv.size(), 1), s);
+  }
+  if (flow_smem_bytes(recmax) > 200 * 1024) return;  // a patch record too large to double-buffer per warp
+  for (int dir = 0; dir < 2; ++dir) {
+    f.recs[dir].upload(recs[(size_t)dir].data(), (int64_t)recs[(size_t)dir].size(), s);
+    f.rec_off[dir].upload(offs[(size_t)dir].data(), (int64_t)offs[(size_t)dir].size(), s);
     f.d[dir].alloc(ne, s);
     flow_reset_slots(f.d[dir].p, ne, s);
   }
+  f.recmax = recmax;
   f.ent.upload(ent.data(), n, s);
   f.bar.alloc(1, s);
   f.bar.zero();

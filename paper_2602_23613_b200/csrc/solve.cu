@@ -649,14 +649,10 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     fa.n = n;
     fa.nwave = sm.nwave;
     fa.ne = fl.ne;
-    fa.wave_ptr = sm.d_wave_ptr.p;
-    fa.patch_ptr = sm.patch_ptr.p;
-    fa.dofs = sm.patch_dofs.p;
-    fa.binv_off = sm.binv_off.p;
-    fa.binv = sm.binv.p;
-    fa.tp = fl.tp[dir].p;
-    fa.tslot = fl.tslot[dir].p;
-    fa.tval = fl.tval[dir].p;
+    fa.npatch = sm.npatch;
+    fa.recmax = fl.recmax;
+    fa.recs = fl.recs[dir].p;
+    fa.rec_off = fl.rec_off[dir].p;
     fa.d = fl.d[dir].p;
     fa.ent = fl.ent.p;
     fa.ap = L.A.ptr.p;

@@ -57,16 +57,10 @@ int sweep_cluster_size();
 // Dataflow leg (flow.cu): per-entry correction slots, no barrier inside the sweep.
 struct FlowArgs {
   const int* stop;
-  int64_t n, nwave, ne;
-  const int64_t* wave_ptr;   // device, nwave + 1 (wave-major patch order)
-  const int64_t* patch_ptr;  // reordered patch -> entries
-  const int32_t* dofs;       // entry -> DoF
-  const int64_t* binv_off;
-  const double* binv;        // column-major k x k inverses
-  const int32_t* tp;         // entry -> range of pulled terms (this direction)
-  const int32_t* tslot;      // term -> slot of an earlier coupled patch entry
-  const double* tval;        // term -> A[u, j]
-  double* d;                 // slots (sentinel between legs)
+  int64_t n, nwave, ne, npatch, recmax;
+  const unsigned char* recs;  // patch records of this direction, in its execution order
+  const int64_t* rec_off;     // npatch + 1 byte offsets
+  double* d;                  // slots (sentinel between legs)
   const int2* ent;           // DoF -> its (<= 2) entries, -1 padded
   const int64_t* ap;
   const int32_t* ai;
@@ -80,6 +74,7 @@ struct FlowArgs {
   unsigned* bar;
 };
 void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s);
+int64_t flow_smem_bytes(int64_t recmax);
 void flow_reset_slots(double* d, int64_t ne, cudaStream_t s);
 
 // y = T v for a CSR T with long rows: fixed 256-entry segments, one warp each,

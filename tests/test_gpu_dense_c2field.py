@@ -29,7 +29,7 @@ def tol(floor):
     return max(1e-10, 10.0 * floor)
 
 
-@pytest.fixture(scope="module", params=["auto", "grid"])
+@pytest.fixture(scope="module", params=["auto", "grid", "flow"])
 def run(request):
     z = np.load(FIX)
     meta = json.loads(str(z["meta"]))
