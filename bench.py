@@ -337,12 +337,32 @@ def reference_line(args, value, t, iters, setup_s, sample, extra=None):
     return line
 
 
+def make_system(config):
+    """BASELINE configs c1..c5 (3D Kuhn cubes, paper_2602_23613_b200/kuhn.py) or
+    the supplementary 2D stripes family "2d-L<L>" (the reference's own sparse
+    regime, paper_2602_23613_b200/tri2d.py)."""
+    if config.startswith("2d-L"):
+        from paper_2602_23613_b200 import tri2d
+        return tri2d.stripes_system(int(config[4:]))
+    from paper_2602_23613_b200 import kuhn
+    return kuhn.config_system(config)
+
+
+def rhs(n):
+    return np.random.default_rng(0).uniform(-1.0, 1.0, n)
+
+
 def workload_config(config):
     """Identical in both arms (the driver compares the arms' configs)."""
-    from paper_2602_23613_b200 import kuhn
-    cfg = kuhn.CONFIGS[config]
-    return {"workload": f"BASELINE {config}: unit cube, {cfg['n']}^3 hexes x 6 Kuhn tets, alg hierarchy, "
-                        "PCG tol 1e-8 from x0=0, rhs uniform[-1,1] seed 0; one step = one complete PCG solve",
+    if config.startswith("2d-L"):
+        L = int(config[4:])
+        desc = (f"supplementary 2D stripes L={L} (not a BASELINE config): unit square, 2 x 4^{L} triangles, "
+                f"mu 10 / 0.1 per grid column, beta 1e-2, alg hierarchy")
+    else:
+        from paper_2602_23613_b200 import kuhn
+        cfg = kuhn.CONFIGS[config]
+        desc = f"BASELINE {config}: unit cube, {cfg['n']}^3 hexes x 6 Kuhn tets, alg hierarchy"
+    return {"workload": desc + ", PCG tol 1e-8 from x0=0, rhs uniform[-1,1] seed 0; one step = one complete PCG solve",
             "l2": ("L2 flushed (256 MiB write) before every timed GPU step; a PCG iteration moves the whole "
                    "hierarchy (config 2: 25.5 GB on the GPU), far above L2") if config != "c1" else
                   ("L2 flushed (256 MiB write) before every timed GPU step; the whole c1 hierarchy (~17 MB) "
@@ -362,8 +382,8 @@ def run_reference(args, world, rank, dist):
     from paper_2602_23613_b200 import kuhn
     if rank != 0:
         return
-    system = kuhn.config_system(args.config)
-    b = kuhn.rhs(system.n, seed=0)
+    system = make_system(args.config)
+    b = rhs(system.n)
     t0 = time.perf_counter()
     ho = O.hierarchy(system, "alg", large="envelope", log=log)
     setup_s = time.perf_counter() - t0
@@ -400,9 +420,9 @@ def run_ours(args, world, rank, local, dist):
     from paper_2602_23613_b200 import _lib, kuhn
 
     torch.cuda.set_device(local)
-    system = kuhn.config_system(args.config)
+    system = make_system(args.config)
     n = system.n
-    b_host = kuhn.rhs(n, seed=0)
+    b_host = rhs(n)
     # setup (the first call also pays context / module load; report the best of two)
     setups, setup_flops = [], []
     h = P.build_hierarchy(system, "alg", device=local)
@@ -583,7 +603,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", help="BASELINE config: c1 (configs[0]) or c2 (configs[1], default)")
+    ap.add_argument("--config", default="c2", help="BASELINE config: c1 (configs[0]) or c2 (configs[1], default); "
+                                                  "2d-L<L>: the supplementary 2D stripes family (e.g. 2d-L9)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--replicas", action="store_true",

@@ -99,7 +99,14 @@ __device__ __forceinline__ void rec_layout(int k, int nt, int& o_dof, int& o_ts,
 
 // one patch from its staged record: v = r0[u] - sum of the pulled terms
 // (spinning on slots that still hold the sentinel), d = B_p^{-1} v
-__device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned char* rec, int lane, const double* r0) {
+__device__ __forceinline__ long long gclock() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned char* rec, int lane, const double* r0,
+                                           long long* tr) {
   const int4 hd = *reinterpret_cast<const int4*>(rec);
   const int k = hd.x, e0 = hd.y, nt = hd.z;
   int o_dof, o_ts, o_binv, o_slot, o_val;
@@ -143,10 +150,18 @@ __device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned cha
     }
     v = rv - acc;
   }
+  if (tr) {
+    __syncwarp();
+    if (lane == 0) tr[1] = gclock();
+  }
   double d = 0.0;
   const double* brow = binv + (act ? lane * k : 0);
   for (int c = 0; c < k; ++c) d = fma(act ? brow[c] : 0.0, __shfl_sync(0xffffffffu, v, c), d);
   if (act) st_slot(a.d + e0 + lane, d);
+  if (tr) {
+    __syncwarp();
+    if (lane == 0) tr[2] = gclock();
+  }
 }
 
 template <bool kDown>
@@ -211,7 +226,12 @@ __global__ void __launch_bounds__(kFlowThreads, 1) k_flow_leg(FlowArgs a) {
       const int b = (int)(j & 1);
       if (lane == 0 && i + nw < m) issue(i + nw, b ^ 1);
       mbar_wait(b ? bar1 : bar0, (uint32_t)((j >> 1) & 1));
-      flow_patch(a, buf0 + (size_t)b * a.recmax, lane, r0);
+      long long* tr = a.trace ? a.trace + 4 * i : nullptr;
+      if (tr && lane == 0) {
+        tr[0] = gclock();
+        tr[3] = wg;
+      }
+      flow_patch(a, buf0 + (size_t)b * a.recmax, lane, r0, tr);
       __syncwarp();
     }
   }

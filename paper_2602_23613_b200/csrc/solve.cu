@@ -665,6 +665,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     fa.r1 = L.d0.p;
     fa.dj = L.dj.p;
     fa.bar = fl.bar.p;
+    fa.trace = g_leg_trace;
     launch_flow_leg(down, fa, s);
     return 1;
   }

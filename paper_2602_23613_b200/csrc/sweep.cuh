@@ -72,6 +72,7 @@ struct FlowArgs {
   double* r1;
   double* dj;
   unsigned* bar;
+  long long* trace;           // debug: per execution position {record ready, pulls done, stored, warp} (globaltimer)
 };
 void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s);
 int64_t flow_smem_bytes(int64_t recmax);
