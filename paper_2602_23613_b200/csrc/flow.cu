@@ -84,8 +84,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   } while (!done);
 }
 
-// Patch record (flow_record_layout, built by build_flow; 16-byte aligned):
-//   int32 {k, e0, nt, 0} | int32 dof[k4] | int32 tstart[kp4] | double binv[k*k] (row-major)
+// Patch record (built by build_flow; 16-byte aligned):
+//   int32 {k, e0, nt, gate}  (gate: a slot of the latest-wave predecessor, -1: none) | int32 dof[k4] | int32 tstart[kp4] | double binv[k*k] (row-major)
 //   | int32 tslot[nt4] | double tval[nt] | pad to 16
 __device__ __forceinline__ void rec_layout(int k, int nt, int& o_dof, int& o_ts, int& o_binv, int& o_slot,
                                            int& o_val) {
@@ -108,7 +108,20 @@ __device__ __forceinline__ long long gclock() {
 __device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned char* rec, int lane, const double* r0,
                                            long long* tr) {
   const int4 hd = *reinterpret_cast<const int4*>(rec);
-  const int k = hd.x, e0 = hd.y, nt = hd.z;
+  const int k = hd.x, e0 = hd.y, nt = hd.z, gate = hd.w;
+  // wait on ONE slot of the predecessor in the latest wave first (lane 0,
+  // with back-off): spinning lanes on every term flood the load path and
+  // delay the very stores they wait for
+  if (gate >= 0) {
+    if (lane == 0) {
+      unsigned ns = 32;
+      while (is_sentinel(ld_slot(a.d + gate))) {
+        __nanosleep(ns);
+        ns = min(ns * 2, 256u);
+      }
+    }
+    __syncwarp();
+  }
   int o_dof, o_ts, o_binv, o_slot, o_val;
   rec_layout(k, nt, o_dof, o_ts, o_binv, o_slot, o_val);
   const int32_t* dof = reinterpret_cast<const int32_t*>(rec + o_dof);
@@ -138,6 +151,7 @@ __device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned cha
         }
       }
       while (pending) {
+        __nanosleep(64);
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           if (pending & (1u << i)) {

@@ -529,6 +529,7 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
       ts.clear();
       tv.clear();
       tstart.assign(1, 0);
+      int32_t gate = -1, glev = dir == 0 ? -1 : INT32_MAX;
       for (int64_t a = 0; a < k; ++a) {
         const int32_t u = dofs[(size_t)(e0 + a)];
         for (int64_t kk = ap[(size_t)u]; kk < ap[(size_t)u + 1]; ++kk) {
@@ -540,6 +541,10 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
             if (dir == 0 ? lev[(size_t)p] < lq : lev[(size_t)p] > lq) {
               ts.push_back(e2);
               tv.push_back(av[(size_t)kk]);
+              if (dir == 0 ? lev[(size_t)p] > glev : lev[(size_t)p] < glev) {
+                glev = lev[(size_t)p];
+                gate = e2;
+              }
             }
           }
         }
@@ -552,7 +557,7 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
       const size_t base = R.size();
       R.resize(base + (size_t)bytes, 0);
       unsigned char* r = R.data() + base;
-      const int32_t hd[4] = {(int32_t)k, (int32_t)e0, (int32_t)nt, 0};
+      const int32_t hd[4] = {(int32_t)k, (int32_t)e0, (int32_t)nt, gate};
       memcpy(r, hd, 16);
       for (int64_t a = 0; a < k; ++a) {
         const int32_t u = dofs[(size_t)(e0 + a)];

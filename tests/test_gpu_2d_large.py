@@ -1,0 +1,82 @@
+"""The reference's own sparse regime at scale: 2D stripes L = 7 (48,896 DoFs,
+6 levels) and L = 9 (785,408 DoFs, the bench's supplementary config 2d-L9)
+against oracle fixtures (tests/golden/make_2d.py): every level's splitting
+and A / P / G patterns bit-exact (SHA-256), P, A_l and the PCG solution
+through 64 seeded random projections within 1e-8 relative (the measured
+fp64 floor on the 100-contrast stripes is 3e-10), PCG
+iterations +-1.  Exercises the many-level sparse path: CSR P / P^T, the
+sparse Galerkin SpGEMM, small harmonic-extension components and the 7-wave
+smoothing legs."""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2602_23613_b200 as P
+from paper_2602_23613_b200 import tri2d
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def sha(*arrays):
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def proj(v, k=64, seed=99):
+    return np.random.default_rng(seed).standard_normal((k, len(v))) @ v
+
+
+def close(a, b, tol=1e-8):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.abs(a - b).max() <= tol * np.abs(b).max()
+
+
+@pytest.fixture(scope="module", params=[7, 9])
+def run(request):
+    L = request.param
+    with open(os.path.join(HERE, f"tri{L}s_large.json")) as f:
+        meta = json.load(f)
+    meshes, rmaps, s = tri2d.tri_chain(L, stripes=True)
+    h = P.build_hierarchy(s, "alg")
+    b = np.random.default_rng(0).uniform(-1.0, 1.0, s.n)
+    x, rep = P.pcg(s.A, b, precond=lambda r: P.vcycle(h, r), tol=1e-8)
+    return s, h, x, rep, meta
+
+
+def test_hierarchy_integers(run):
+    s, h, x, rep, meta = run
+    assert [lv.n for lv in h.levels] == [d["n"] for d in meta["levels"]]
+    assert h.stalled == meta["stalled"] and h.notes == meta["notes"]
+    for lv, d in zip(h.levels, meta["levels"]):
+        assert sha(lv.A.indptr.astype(np.int64), lv.A.indices.astype(np.int64)) == d["A_pattern"]
+        assert sha(lv.G.indptr.astype(np.int64), lv.G.indices.astype(np.int64), lv.G.data) == d["G_pattern"]
+        if "pairs" in d:
+            sp = lv.splitting
+            assert sha(np.array([tuple(p) for p in sp.pairs], dtype=np.int64)) == d["pairs"]
+            assert sha(sp.interior_dofs.astype(np.int64)) == d["interior"]
+            assert sha(np.asarray(sp.coarse_nodes, dtype=np.int64)) == d["coarse_nodes"]
+            assert sha(lv.P.indptr.astype(np.int64), lv.P.indices.astype(np.int64)) == d["P_pattern"]
+            assert len(lv.patches.patches) == d["n_patches"]
+
+
+def test_hierarchy_values(run):
+    s, h, x, rep, meta = run
+    for lv, d in zip(h.levels, meta["levels"]):
+        assert close(proj(lv.A.data), d["A_proj"])
+        if "P_proj" in d:
+            assert close(proj(lv.P.data), d["P_proj"])
+    assert P.operator_complexity(h) == pytest.approx(meta["oc"], rel=1e-12)
+
+
+def test_pcg(run):
+    s, h, x, rep, meta = run
+    assert rep.converged and abs(rep.iterations - meta["pcg_iters"]) <= 1
+    assert close(proj(x), meta["x_proj"])
+    assert abs(np.linalg.norm(x) - meta["x_norm"]) <= 1e-8 * meta["x_norm"]
