@@ -41,6 +41,7 @@ namespace hcamg {
 namespace {
 
 constexpr int kFlowThreads = 256;
+constexpr int kFlowGates = 8;  // gate slots per record (one per predecessor patch of the latest wave)
 constexpr unsigned long long kSentinel = 0x7ff4dead5eed0001ull;  // a NaN no arithmetic produces
 
 __device__ __forceinline__ double ld_slot(const double* p) {
@@ -64,33 +65,41 @@ struct GridBar {
       const unsigned inc = blockIdx.x == 0 ? 0x80000000u - (gridDim.x - 1) : 1u;
       unsigned old, cur;
       asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(bar), "r"(inc) : "memory");
-      do {
+      // back-off: CTAs that finish their patches early would otherwise poll
+      // one L2 line for the rest of the sweep and stall the slot traffic
+      unsigned ns = 64;
+      while (true) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
-      } while (((cur ^ old) & 0x80000000u) == 0);
+        if ((cur ^ old) & 0x80000000u) break;
+        __nanosleep(ns);
+        ns = min(ns * 2, 1024u);
+      }
     }
     __syncthreads();
   }
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// every lane observes the phase (acquire of the bulk copy), and the loop ends
+// for the whole warp at once so the warp stays converged
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t done;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!done);
+  uint32_t done = 0;
+  while (!__all_sync(0xffffffffu, done != 0))
+    if (!done)
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(bar), "r"(parity)
+          : "memory");
 }
 
 // Patch record (built by build_flow; 16-byte aligned):
-//   int32 {k, e0, nt, gate}  (gate: a slot of the latest-wave predecessor, -1: none) | int32 dof[k4] | int32 tstart[kp4] | double binv[k*k] (row-major)
+//   int32 {k, e0, nt, ngate} | int32 gate[8] (a slot of each latest-wave predecessor) | int32 dof[k4] | int32 tstart[kp4] | double binv[k*k] (row-major)
 //   | int32 tslot[nt4] | double tval[nt] | pad to 16
 __device__ __forceinline__ void rec_layout(int k, int nt, int& o_dof, int& o_ts, int& o_binv, int& o_slot,
                                            int& o_val) {
   const int k4 = (k + 3) & ~3, kp4 = (k + 1 + 3) & ~3, nt4 = (nt + 3) & ~3;
-  o_dof = 16;
+  o_dof = 16 + 4 * kFlowGates;
   o_ts = o_dof + 4 * k4;
   o_binv = o_ts + 4 * kp4;
   o_slot = o_binv + 8 * k * k;
@@ -101,27 +110,14 @@ __device__ __forceinline__ void rec_layout(int k, int nt, int& o_dof, int& o_ts,
 // (spinning on slots that still hold the sentinel), d = B_p^{-1} v
 __device__ __forceinline__ long long gclock() {
   long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)::"memory");
   return t;
 }
 
 __device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned char* rec, int lane, const double* r0,
                                            long long* tr) {
   const int4 hd = *reinterpret_cast<const int4*>(rec);
-  const int k = hd.x, e0 = hd.y, nt = hd.z, gate = hd.w;
-  // wait on ONE slot of the predecessor in the latest wave first (lane 0,
-  // with back-off): spinning lanes on every term flood the load path and
-  // delay the very stores they wait for
-  if (gate >= 0) {
-    if (lane == 0) {
-      unsigned ns = 32;
-      while (is_sentinel(ld_slot(a.d + gate))) {
-        __nanosleep(ns);
-        ns = min(ns * 2, 256u);
-      }
-    }
-    __syncwarp();
-  }
+  const int k = hd.x, e0 = hd.y, nt = hd.z, ngate = a.gates ? hd.w : 0;
   int o_dof, o_ts, o_binv, o_slot, o_val;
   rec_layout(k, nt, o_dof, o_ts, o_binv, o_slot, o_val);
   const int32_t* dof = reinterpret_cast<const int32_t*>(rec + o_dof);
@@ -131,46 +127,91 @@ __device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned cha
   const double* tval = reinterpret_cast<const double*>(rec + o_val);
   const bool act = lane < k;
   double v = 0.0;
-  if (act) {
-    const double rv = r0[dof[lane]];
-    const int t0 = ts[lane], t1 = ts[lane + 1];
-    double acc = 0.0;
-    for (int t = t0; t < t1; t += 8) {
-      const int cnt = min(8, t1 - t);
-      double w[8], x[8];
-      int32_t sl[8];
-      unsigned pending = 0;
+  // r0 and the patch's row of B^{-1} are independent of the predecessors:
+  // in flight / in registers before the wait.  All control flow below is
+  // warp-uniform (spins end on __all_sync / __any_sync): a warp left
+  // diverged by per-lane spin loops runs the B^{-1} shuffles on the slow
+  // collective path (measured 4 us per patch instead of 0.5)
+  const double rv = act ? r0[dof[lane]] : 0.0;
+  double brow16[16];
+  if (k <= 16) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        sl[i] = i < cnt ? tslot[t + i] : 0;
-        w[i] = i < cnt ? tval[t + i] : 0.0;
-        x[i] = 0.0;
-        if (i < cnt) {
-          x[i] = ld_slot(a.d + sl[i]);
-          if (is_sentinel(x[i])) pending |= 1u << i;
-        }
-      }
-      while (pending) {
-        __nanosleep(64);
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          if (pending & (1u << i)) {
-            x[i] = ld_slot(a.d + sl[i]);
-            if (!is_sentinel(x[i])) pending &= ~(1u << i);
-          }
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc = fma(w[i], x[i], acc);
-    }
-    v = rv - acc;
+    for (int c = 0; c < 16; ++c) brow16[c] = (act && c < k) ? binv[lane * k + c] : 0.0;
   }
   if (tr) {
+    double t_;
+    asm volatile("mov.b64 %0, %1;" : "=d"(t_) : "d"(rv) : "memory");  // (trace: wait for it here)
     __syncwarp();
-    if (lane == 0) tr[1] = gclock();
+    if (lane == 0) tr[4] = gclock() + (t_ == 1.2345e300);
+  }
+  // lanes 0..ngate-1 wait on one slot of each predecessor patch of the
+  // latest wave (few polling lanes: polls from every term of every lane
+  // flood the L2 and delay the very stores being waited for)
+  if (ngate > 0) {
+    const int32_t g = lane < ngate ? reinterpret_cast<const int32_t*>(rec + 16)[lane] : 0;
+    bool ok = lane >= ngate;
+    while (!__all_sync(0xffffffffu, ok)) {
+      if (!ok) ok = !is_sentinel(ld_slot(a.d + g));
+      if (a.spin_ns && !__all_sync(0xffffffffu, ok)) __nanosleep(a.spin_ns);
+    }
+  }
+  // every pulled slot of the entry loaded at once (one L2 round trip); slots
+  // of earlier-wave predecessors that are still pending are polled again
+  const int t0 = act ? ts[lane] : 0, t1 = act ? ts[lane + 1] : 0;
+  const int cnt = min(32, t1 - t0);
+  double x[32];
+  unsigned pend = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    x[i] = 0.0;
+    if (i < cnt) {
+      x[i] = ld_slot(a.d + tslot[t0 + i]);
+      if (is_sentinel(x[i])) pend |= 1u << i;
+    }
+  }
+  while (__any_sync(0xffffffffu, pend != 0)) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (pend & (1u << i)) {
+        x[i] = ld_slot(a.d + tslot[t0 + i]);
+        if (!is_sentinel(x[i])) pend &= ~(1u << i);
+      }
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < cnt) acc = fma(tval[t0 + i], x[i], acc);
+  for (int t = t0 + 32; __any_sync(0xffffffffu, t < t1); ++t) {  // entries with more than 32 terms (rare)
+    bool done = t >= t1;
+    double y = 0.0;
+    while (!__all_sync(0xffffffffu, done))
+      if (!done) {
+        y = ld_slot(a.d + tslot[t]);
+        done = !is_sentinel(y);
+      }
+    if (t < t1) acc = fma(tval[t], y, acc);
+  }
+  v = act ? rv - acc : 0.0;
+  if (tr) {
+    double t_;
+    asm volatile("mov.b64 %0, %1;" : "=d"(t_) : "d"(v) : "memory");
+    __syncwarp();
+    if (lane == 0) tr[1] = gclock() + (t_ == 1.2345e300);
   }
   double d = 0.0;
-  const double* brow = binv + (act ? lane * k : 0);
-  for (int c = 0; c < k; ++c) d = fma(act ? brow[c] : 0.0, __shfl_sync(0xffffffffu, v, c), d);
+  if (k <= 16) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c) d = fma(brow16[c], __shfl_sync(0xffffffffu, v, c), d);
+  } else {
+    const double* brow = binv + (act ? lane * k : 0);
+    for (int c = 0; c < k; ++c) d = fma(act ? brow[c] : 0.0, __shfl_sync(0xffffffffu, v, c), d);
+  }
+  if (tr) {
+    double t_;
+    asm volatile("mov.b64 %0, %1;" : "=d"(t_) : "d"(d) : "memory");
+    __syncwarp();
+    if (lane == 0) tr[5] = gclock() + (t_ == 1.2345e300);
+  }
   if (act) st_slot(a.d + e0 + lane, d);
   if (tr) {
     __syncwarp();
@@ -239,8 +280,9 @@ __global__ void __launch_bounds__(kFlowThreads, 1) k_flow_leg(FlowArgs a) {
     for (int64_t i = wg; i < m; i += nw, ++j) {
       const int b = (int)(j & 1);
       if (lane == 0 && i + nw < m) issue(i + nw, b ^ 1);
+      __syncwarp();
       mbar_wait(b ? bar1 : bar0, (uint32_t)((j >> 1) & 1));
-      long long* tr = a.trace ? a.trace + 4 * i : nullptr;
+      long long* tr = a.trace ? a.trace + 6 * i : nullptr;
       if (tr && lane == 0) {
         tr[0] = gclock();
         tr[3] = wg;
@@ -324,6 +366,9 @@ void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s) {
   HC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int blocks = sms * std::min(per_sm, 2);
   if (const char* e = getenv("HCAMG_FLOW_BLOCKS")) blocks = std::min(blocks, std::max(1, atoi(e)));
+  FlowArgs fa = args;
+  fa.spin_ns = getenv("HCAMG_FLOW_NS") ? (unsigned)atoi(getenv("HCAMG_FLOW_NS")) : 0u;  // measurement knobs
+  fa.gates = getenv("HCAMG_FLOW_GATE") ? atoi(getenv("HCAMG_FLOW_GATE")) : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)blocks);
   cfg.blockDim = dim3(kFlowThreads);
@@ -334,8 +379,8 @@ void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (down) HC_CUDA(cudaLaunchKernelEx(&cfg, k_flow_leg<true>, args));
-  else HC_CUDA(cudaLaunchKernelEx(&cfg, k_flow_leg<false>, args));
+  if (down) HC_CUDA(cudaLaunchKernelEx(&cfg, k_flow_leg<true>, fa));
+  else HC_CUDA(cudaLaunchKernelEx(&cfg, k_flow_leg<false>, fa));
 }
 
 }  // namespace hcamg

@@ -529,7 +529,8 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
       ts.clear();
       tv.clear();
       tstart.assign(1, 0);
-      int32_t gate = -1, glev = dir == 0 ? -1 : INT32_MAX;
+      int32_t glev = dir == 0 ? -1 : INT32_MAX;
+      std::vector<std::pair<int32_t, int32_t>> gates;  // (predecessor patch, one of its slots) of the latest wave
       for (int64_t a = 0; a < k; ++a) {
         const int32_t u = dofs[(size_t)(e0 + a)];
         for (int64_t kk = ap[(size_t)u]; kk < ap[(size_t)u + 1]; ++kk) {
@@ -543,7 +544,12 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
               tv.push_back(av[(size_t)kk]);
               if (dir == 0 ? lev[(size_t)p] > glev : lev[(size_t)p] < glev) {
                 glev = lev[(size_t)p];
-                gate = e2;
+                gates.clear();
+              }
+              if (lev[(size_t)p] == glev) {
+                bool have = false;
+                for (auto& g : gates) have |= g.first == p;
+                if (!have) gates.emplace_back(p, e2);
               }
             }
           }
@@ -552,13 +558,15 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
       }
       const int64_t nt = (int64_t)ts.size();
       const int64_t k4 = (k + 3) & ~3, kp4 = (k + 1 + 3) & ~3, nt4 = (nt + 3) & ~3;
-      const int64_t o_dof = 16, o_ts = o_dof + 4 * k4, o_binv = o_ts + 4 * kp4, o_slot = o_binv + 8 * k * k,
+      const int64_t o_dof = 16 + 4 * 8, o_ts = o_dof + 4 * k4, o_binv = o_ts + 4 * kp4, o_slot = o_binv + 8 * k * k,
                     o_val = o_slot + 4 * nt4, bytes = (o_val + 8 * nt + 15) & ~(int64_t)15;
       const size_t base = R.size();
       R.resize(base + (size_t)bytes, 0);
       unsigned char* r = R.data() + base;
-      const int32_t hd[4] = {(int32_t)k, (int32_t)e0, (int32_t)nt, gate};
+      const int32_t ng = (int32_t)std::min<size_t>(gates.size(), 8);
+      const int32_t hd[4] = {(int32_t)k, (int32_t)e0, (int32_t)nt, ng};
       memcpy(r, hd, 16);
+      for (int32_t g = 0; g < ng; ++g) memcpy(r + 16 + 4 * g, &gates[(size_t)g].second, 4);
       for (int64_t a = 0; a < k; ++a) {
         const int32_t u = dofs[(size_t)(e0 + a)];
         memcpy(r + o_dof + 4 * a, &u, 4);

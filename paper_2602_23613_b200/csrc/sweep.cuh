@@ -72,6 +72,8 @@ struct FlowArgs {
   double* r1;
   double* dj;
   unsigned* bar;
+  unsigned spin_ns;           // back-off of the slot spin (0: pure spin)
+  int gates;                  // wait on the latest-wave predecessors first (1) or poll every term (0)
   long long* trace;           // debug: per execution position {record ready, pulls done, stored, warp} (globaltimer)
 };
 void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s);
