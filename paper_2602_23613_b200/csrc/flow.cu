@@ -94,14 +94,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 // Patch record (built by build_flow; 16-byte aligned):
-//   int32 {k, e0, nt, ngate} | int32 gate[8] (a slot of each latest-wave predecessor) | int32 dof[k4] | int32 tstart[kp4] | double binv[k*k] (row-major)
+//   int32 {k, e0, nt, ngate} | int32 gate[8] (a slot of each latest-wave predecessor) | int32 dof[k4]
+//   | int32 tstart[kp4] | int32 xpart[k4] (term index of the DoF's other patch entry when that patch ran
+//   earlier: this patch then writes x[u]; -1: the other patch runs later; -2: no other patch) | int32 tstart[kp4] | double binv[k*k] (row-major)
 //   | int32 tslot[nt4] | double tval[nt] | pad to 16
 __device__ __forceinline__ void rec_layout(int k, int nt, int& o_dof, int& o_ts, int& o_binv, int& o_slot,
                                            int& o_val) {
   const int k4 = (k + 3) & ~3, kp4 = (k + 1 + 3) & ~3, nt4 = (nt + 3) & ~3;
   o_dof = 16 + 4 * kFlowGates;
   o_ts = o_dof + 4 * k4;
-  o_binv = o_ts + 4 * kp4;
+  o_binv = o_ts + 4 * kp4 + 4 * k4;  // tstart, then xpart[k4]
   o_slot = o_binv + 8 * k * k;
   o_val = o_slot + 4 * nt4;
 }
@@ -115,13 +117,14 @@ __device__ __forceinline__ long long gclock() {
 }
 
 __device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned char* rec, int lane, const double* r0,
-                                           long long* tr) {
+                                           const double* x0, long long* tr) {
   const int4 hd = *reinterpret_cast<const int4*>(rec);
   const int k = hd.x, e0 = hd.y, nt = hd.z, ngate = a.gates ? hd.w : 0;
   int o_dof, o_ts, o_binv, o_slot, o_val;
   rec_layout(k, nt, o_dof, o_ts, o_binv, o_slot, o_val);
   const int32_t* dof = reinterpret_cast<const int32_t*>(rec + o_dof);
   const int32_t* ts = reinterpret_cast<const int32_t*>(rec + o_ts);
+  const int32_t* xpart = reinterpret_cast<const int32_t*>(rec + o_ts + 4 * ((k + 1 + 3) & ~3));
   const double* binv = reinterpret_cast<const double*>(rec + o_binv);
   const int32_t* tslot = reinterpret_cast<const int32_t*>(rec + o_slot);
   const double* tval = reinterpret_cast<const double*>(rec + o_val);
@@ -132,7 +135,10 @@ __device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned cha
   // warp-uniform (spins end on __all_sync / __any_sync): a warp left
   // diverged by per-lane spin loops runs the B^{-1} shuffles on the slow
   // collective path (measured 4 us per patch instead of 0.5)
-  const double rv = act ? r0[dof[lane]] : 0.0;
+  const int32_t u = act ? dof[lane] : 0;
+  const int32_t xp = act ? xpart[lane] : -1;
+  const double rv = act ? r0[u] : 0.0;
+  const double xv = (act && xp != -1 && x0) ? x0[u] : 0.0;
   double brow16[16];
   if (k <= 16) {
 #pragma unroll
@@ -177,10 +183,12 @@ __device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned cha
         if (!is_sentinel(x[i])) pend &= ~(1u << i);
       }
   }
-  double acc = 0.0;
+  double acc = 0.0, dpart = 0.0;
 #pragma unroll
-  for (int i = 0; i < 32; ++i)
+  for (int i = 0; i < 32; ++i) {
     if (i < cnt) acc = fma(tval[t0 + i], x[i], acc);
+    if (i == xp) dpart = x[i];
+  }
   for (int t = t0 + 32; __any_sync(0xffffffffu, t < t1); ++t) {  // entries with more than 32 terms (rare)
     bool done = t >= t1;
     double y = 0.0;
@@ -212,7 +220,13 @@ __device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned cha
     __syncwarp();
     if (lane == 0) tr[5] = gclock() + (t_ == 1.2345e300);
   }
-  if (act) st_slot(a.d + e0 + lane, d);
+  if (act) {
+    st_slot(a.d + e0 + lane, d);
+    // the last of the DoF's (<= 2) patches writes x: (x0 + d_earlier) + d,
+    // the reference's x[patch] += d order (smoothers.py:102)
+    if (xp >= 0) a.x[u] = x0 ? (xv + dpart) + d : dpart + d;
+    else if (xp == -2) a.x[u] = x0 ? xv + d : d;
+  }
   if (tr) {
     __syncwarp();
     if (lane == 0) tr[2] = gclock();
@@ -287,47 +301,28 @@ __global__ void __launch_bounds__(kFlowThreads, 1) k_flow_leg(FlowArgs a) {
         tr[0] = gclock();
         tr[3] = wg;
       }
-      flow_patch(a, buf0 + (size_t)b * a.recmax, lane, r0, tr);
+      flow_patch(a, buf0 + (size_t)b * a.recmax, lane, r0, kDown ? nullptr : a.x, tr);
       __syncwarp();
     }
   }
   gb.sync();
   if (kDown) {
-    // x = delta ; r1 = b - A delta ; dj = r1 / l1 ; x += dj
+    // x holds the sweep's result; r1 = b - A x ; dj = r1 / l1 ; x += dj
     for (int64_t u = gtid; u < n; u += nth) {
       double s = 0.0;
-      for (int64_t e = a.ap[u]; e < a.ap[u + 1]; ++e) {
-        const int2 en = a.ent[a.ai[e]];
-        double dl = 0.0;
-        if (en.x >= 0) dl = ld_slot(a.d + en.x);
-        if (en.y >= 0) dl += ld_slot(a.d + en.y);
-        s = fma(a.av[e], dl, s);
-      }
-      const int2 me = a.ent[u];
-      double xu = 0.0;
-      if (me.x >= 0) xu = ld_slot(a.d + me.x);
-      if (me.y >= 0) xu += ld_slot(a.d + me.y);
+      for (int64_t e = a.ap[u]; e < a.ap[u + 1]; ++e) s = fma(a.av[e], a.x[a.ai[e]], s);
       const double r1 = a.b[u] - s;
       const double dj = r1 / a.l1[u];
       a.r1[u] = r1;
       a.dj[u] = dj;
-      a.x[u] = xu + dj;
     }
     gb.sync();
     for (int64_t u = gtid; u < n; u += nth) {
       double s = 0.0;
       for (int64_t e = a.ap[u]; e < a.ap[u + 1]; ++e) s = fma(a.av[e], a.dj[a.ai[e]], s);
       a.r[u] = a.r1[u] - s;
+      a.x[u] += a.dj[u];
     }
-  } else {
-    for (int64_t u = gtid; u < n; u += nth) {
-      const int2 me = a.ent[u];
-      double dl = 0.0;
-      if (me.x >= 0) dl = ld_slot(a.d + me.x);
-      if (me.y >= 0) dl += ld_slot(a.d + me.y);
-      a.x[u] += dl;
-    }
-    gb.sync();  // the slot reads above must finish before the reset
   }
   // every slot was read above; hand them back to the sentinel for the next leg
   const double sent = __longlong_as_double((long long)kSentinel);

@@ -521,7 +521,7 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
     std::vector<unsigned char>& R = recs[(size_t)dir];
     std::vector<int64_t>& off = offs[(size_t)dir];
     off.assign(1, 0);
-    std::vector<int32_t> ts, tstart;
+    std::vector<int32_t> ts, tstart, xpart;
     std::vector<double> tv;
     for (int64_t q : order) {
       const int64_t e0 = pp[(size_t)q], k = pp[(size_t)q + 1] - e0;
@@ -529,6 +529,7 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
       ts.clear();
       tv.clear();
       tstart.assign(1, 0);
+      xpart.clear();
       int32_t glev = dir == 0 ? -1 : INT32_MAX;
       std::vector<std::pair<int32_t, int32_t>> gates;  // (predecessor patch, one of its slots) of the latest wave
       for (int64_t a = 0; a < k; ++a) {
@@ -554,11 +555,27 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
             }
           }
         }
+        // the DoF's other patch entry: if it ran earlier, its term (A[u, u] d) is in this
+        // entry's list and this patch writes x[u]
+        const int2 eu = ent[(size_t)u];
+        const int32_t other = eu.x == (int32_t)(e0 + a) ? eu.y : eu.x;
+        int32_t xp = -2;
+        if (other >= 0) {
+          xp = -1;
+          for (size_t t = (size_t)tstart.back(); t < ts.size(); ++t)
+            if (ts[t] == other) {
+              xp = (int32_t)(t - (size_t)tstart.back());
+              break;
+            }
+          if (xp > 31) return;  // beyond the unrolled term window of the kernel: flow leg not applicable
+        }
+        xpart.push_back(xp);
         tstart.push_back((int32_t)ts.size());
       }
       const int64_t nt = (int64_t)ts.size();
       const int64_t k4 = (k + 3) & ~3, kp4 = (k + 1 + 3) & ~3, nt4 = (nt + 3) & ~3;
-      const int64_t o_dof = 16 + 4 * 8, o_ts = o_dof + 4 * k4, o_binv = o_ts + 4 * kp4, o_slot = o_binv + 8 * k * k,
+      const int64_t o_dof = 16 + 4 * 8, o_ts = o_dof + 4 * k4, o_xp = o_ts + 4 * kp4, o_binv = o_xp + 4 * k4,
+                    o_slot = o_binv + 8 * k * k,
                     o_val = o_slot + 4 * nt4, bytes = (o_val + 8 * nt + 15) & ~(int64_t)15;
       const size_t base = R.size();
       R.resize(base + (size_t)bytes, 0);
@@ -572,6 +589,7 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
         memcpy(r + o_dof + 4 * a, &u, 4);
       }
       memcpy(r + o_ts, tstart.data(), 4 * tstart.size());
+      memcpy(r + o_xp, xpart.data(), 4 * xpart.size());
       for (int64_t a = 0; a < k; ++a)          // row-major: binv_rm[a k + c] = B^{-1}[a, c] (stored column-major)
         for (int64_t c = 0; c < k; ++c) {
           const double v = binv[(size_t)(boff[(size_t)q] + c * k + a)];
