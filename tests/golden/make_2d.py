@@ -4,7 +4,9 @@ regime): tri_chain(L, stripes=True), beta = 0.01,
 Integers are stored as SHA-256 digests (pairs, interior sets, every level's
 A / P / G patterns); floating point as seeded random projections (64 rows
 drawn from default_rng(99)) of x, of every P and of every A_l, so the test
-checks them to 1e-10 without a multi-MB fixture.  The system generator
+checks them to max(1e-10, 10 x the measured floor) without a multi-MB
+fixture; the floors (oracle vs the oracle with a reversed-order LU component
+solve) are stored with them.  The system generator
 (paper_2602_23613_b200/tri2d.py) is bit-identical to the reference's
 (tests/test_tri2d.py); the hierarchy and solve come from the ORACLE, pinned to
 the reference on the golden cases.  Run in the build container:
@@ -44,6 +46,16 @@ def main(L):
     t0 = time.time()
     x, rep = O.pcg(s.A, b, precond=lambda r: O.vcycle(h, r), tol=1e-8)
     tsol = time.time() - t0
+    # measured fp64 reproducibility floor: the same oracle with its component
+    # Cholesky swapped for a reversed-order LU
+    hf = O.hierarchy(s, "alg", floor_solver=True)
+    xf, _ = O.pcg(s.A, b, precond=lambda r: O.vcycle(hf, r), tol=1e-8)
+
+    def rel(a, c):
+        return float(np.abs(a - c).max() / np.abs(c).max())
+    floors = {"P": max(rel(f.P.data, o.P.data) for f, o in zip(hf.levels[:-1], h.levels[:-1])),
+              "A": max(rel(f.A.data, o.A.data) for f, o in zip(hf.levels, h.levels)),
+              "x": float(np.linalg.norm(xf - x) / np.linalg.norm(x))}
     levels = []
     for lv in h.levels:
         d = {"n": lv.n, "A_pattern": sha(lv.A.indptr.astype(np.int64), lv.A.indices.astype(np.int64)),
@@ -60,7 +72,8 @@ def main(L):
         levels.append(d)
     meta = {"L": L, "n": int(s.n), "levels": levels, "stalled": h.stalled, "notes": h.notes,
             "oc": O.operator_complexity(h), "pcg_iters": rep.iterations, "pcg_hist": rep.residual_history.tolist(),
-            "x_proj": proj(x).tolist(), "x_norm": float(np.linalg.norm(x)), "setup_s": ts, "solve_s": tsol}
+            "x_proj": proj(x).tolist(), "x_norm": float(np.linalg.norm(x)), "setup_s": ts, "solve_s": tsol,
+            "floors": floors}
     with open(os.path.join(HERE, f"tri{L}s_large.json"), "w") as f:
         json.dump(meta, f)
     print(L, s.n, [lv.n for lv in h.levels], rep.iterations, f"setup {ts:.1f}s solve {tsol:.1f}s")
