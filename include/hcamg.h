@@ -92,8 +92,7 @@ int hcamg_version(void);
  * leg, 3 one launch per wavefront, 4 dataflow), "giant_min" (dense-regime
  * cutoff, reference transfer.py:35 _DENSE_COMPONENT_CUTOFF = 4096),
  * "coarse_gemv_min" (coarsest solve streams its inverse from this size on),
- * "coarse_symv" (packed-triangle coarsest solve), "galerkin_fp64" (dense-regime
- * Galerkin correction term in fp64), "factor_apply" (apply the dense
+ * "coarse_symv" (packed-triangle coarsest solve), "factor_apply" (apply the dense
  * interpolation block through the envelope factor, 0 = explicit Z),
  * "form_z" (keep the explicit Z block), "tri_calib" (sweep calibration rounds).
  * Setting an option drops the recorded solve graphs; setup options apply to

@@ -1,7 +1,6 @@
 // C-ABI of libhcamg (include/hcamg.h): handle lifetime, the build_hierarchy
 // driver (hcurl_amg/multilevel.py:78-164) and the solve entry points
 // (multilevel.py:187-281) with their CUDA-graph executables.
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -46,7 +45,6 @@ struct hcamg_handle {
   int device = 0;
   cudaStream_t stream = nullptr, aux = nullptr;
   bool own_stream = false;
-  cublasHandle_t cublas = nullptr;
   std::vector<std::unique_ptr<DevLevel>> levels;
   std::vector<DevLevel*> lv;
   bool stalled = false;
@@ -164,11 +162,11 @@ void factor_coarsest(hcamg_handle* h, DevLevel& L, const DCsr& M) {
   k_densify<<<grid_for(n, 128), 128, 0, s>>>(M.ptr.p, M.idx.p, M.val.p, n, D.p);
   HC_CHECK_LAUNCH();
   StageTimer st(s);
-  int64_t bad = dense_cholesky(h->cublas, D.p, n, n, s);
+  int64_t bad = dense_cholesky(D.p, n, n, s);
   st.mark("  coarsest: cholesky");
   if (bad >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(bad) + ")", bad);
   L.Ainv.alloc(n * n, s);
-  dense_spd_inverse(h->cublas, D.p, n, L.Ainv.p, s);
+  dense_spd_inverse(D.p, n, L.Ainv.p, s);
   st.mark("  coarsest: inverse");
   if (n >= coarse_gemv_min() && opts().coarse_symv) symv_build(L.Ainv.p, n, L.Asym, s);
 }
@@ -252,7 +250,7 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
       mode = 1;
     }
     InterpResult ip;
-    build_interp(cur->A, cur->G, sp, mode, h->cublas, ip, s);
+    build_interp(cur->A, cur->G, sp, mode, ip, s);
     st.mark("interpolation");
     if (ip.P.ncols == 0 || ip.P.ncols >= n) {
       h->stalled = true;
@@ -261,7 +259,7 @@ void build_hierarchy(hcamg_handle* h, const hcamg_csr* Ah, const hcamg_csr* Gh, 
     }
     auto next = std::make_unique<DevLevel>();
     if (ip.hp.on) {
-      galerkin_hybrid(h->cublas, cur->A, ip.P, ip.Pt, ip.hp, next->A, s);
+      galerkin_hybrid(cur->A, ip.P, ip.Pt, ip.hp, next->A, s);
       ip.hp.D.release();
     } else {
       galerkin(ip.P, ip.Pt, cur->A, next->A, s);
@@ -500,7 +498,6 @@ int hcamg_create(hcamg_handle** out, int device, void* cuda_stream) {
       h->own_stream = true;
     }
     HC_CUDA(cudaStreamCreateWithFlags(&h->aux, cudaStreamNonBlocking));
-    if (cublasCreate(&h->cublas) != CUBLAS_STATUS_SUCCESS) throw Error(ECUDA_, "cublasCreate failed");
     h->opts = options_from_env();
     {
       // private stream-ordered pool: freed setup transients are reused within
@@ -540,7 +537,6 @@ void hcamg_destroy(hcamg_handle* h) {
   h->dist.cta.release();
   h->dist.err.release();
   cudaStreamSynchronize(h->stream);
-  if (h->cublas) cublasDestroy(h->cublas);
   if (h->aux) cudaStreamDestroy(h->aux);
   if (h->own_stream) cudaStreamDestroy(h->stream);
   if (h->pool) {
@@ -564,7 +560,6 @@ const OptKey kOptKeys[] = {
     {"giant_min", nullptr, nullptr, &Options::giant_min},
     {"coarse_gemv_min", nullptr, nullptr, &Options::coarse_gemv_min},
     {"coarse_symv", nullptr, &Options::coarse_symv, nullptr},
-    {"galerkin_fp64", nullptr, &Options::galerkin_fp64, nullptr},
     {"factor_apply", nullptr, &Options::factor_apply, nullptr},
     {"form_z", nullptr, &Options::form_z, nullptr},
     {"tri_calib", nullptr, &Options::tri_calib, nullptr},
@@ -762,7 +757,7 @@ int hcamg_export_csr(hcamg_handle* h, int32_t level, int32_t which, int64_t* ind
     }
     DCsr full;
     if (which == 1 && L.hp.on) {
-      hybrid_ensure_z(h->cublas, L.hp, h->stream);
+      hybrid_ensure_z(L.hp, h->stream);
       hybrid_to_csr(L.P, L.hp, full, h->stream);
       M = &full;
     }
@@ -792,7 +787,7 @@ int hcamg_export_dense(hcamg_handle* h, int32_t level, int32_t which, void* out)
     cudaStream_t s = h->stream;
     if (which == 0) {
       require(L.hp.on, "level has no dense interpolation block");
-      hybrid_ensure_z(h->cublas, L.hp, s);
+      hybrid_ensure_z(L.hp, s);
       HC_CUDA(cudaMemcpyAsync(out, L.hp.Z.p, 8 * L.hp.nG * L.hp.nc, cudaMemcpyDeviceToHost, s));
     } else if (which == 1) {
       require(L.hp.on, "level has no dense interpolation block");
@@ -937,7 +932,7 @@ int hcamg_cholesky_factor(hcamg_handle* h, int32_t level, int64_t* ordering, dou
     D.zero();
     k_densify<<<grid_for(n, 128), 128, 0, s>>>(Mp.ptr.p, Mp.idx.p, Mp.val.p, n, D.p);
     HC_CHECK_LAUNCH();
-    const int64_t bad = dense_cholesky(h->cublas, D.p, n, n, s);
+    const int64_t bad = dense_cholesky(D.p, n, n, s);
     if (bad >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(bad) + ")", bad);
     std::vector<double> hL = D.download();  // column-major, lower triangle valid
     for (int64_t i = 0; i < n; ++i) {
@@ -1290,7 +1285,7 @@ int hcamg_dist_prepare(hcamg_handle* h, int32_t rank, int32_t nranks, void* ipc_
     for (DevLevel* L : h->lv) {
       L->xoff_g = L->xoff_y = L->xoff_c = DevLevel::kNoSite;
       if (L->hp.on) {
-        hybrid_ensure_z(h->cublas, L->hp, s);  // ranks stream row blocks of the explicit Z
+        hybrid_ensure_z(L->hp, s);  // ranks stream row blocks of the explicit Z
         L->xoff_g = take(kGroups * L->hp.nc);
         L->xoff_y = take(L->hp.nG);
       }

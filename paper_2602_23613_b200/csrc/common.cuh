@@ -164,7 +164,6 @@ struct Options {
   int64_t giant_min = 4096;        // dense-regime cutoff (= reference _DENSE_COMPONENT_CUTOFF, transfer.py:35)
   int64_t coarse_gemv_min = 8192;  // coarsest solve: HBM row GEMV from this size on
   int coarse_symv = 1;             // single GPU: packed lower triangle of the inverse
-  int galerkin_fp64 = 0;           // dense-regime Galerkin correction in fp64 (0: the TF32 tensor-core product)
   int factor_apply = 1;            // dense block applied through the envelope factor (0: explicit Z)
   int form_z = 0;                  // keep the explicit Z block resident even when the factor applies P
   int tri_calib = 4;               // calibration rounds of the TMA sweep partition

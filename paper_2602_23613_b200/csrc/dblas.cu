@@ -1,0 +1,361 @@
+// FP64 level-3 kernels (see dblas.cuh).
+//
+// GEMM: 128 x 64 CTA tile, 8 warps of 32 x 32, each a 4 x 4 grid of DMMA
+// m8n8k4 fragments (mma.sync ... .f64, FP64 tensor cores); operands staged
+// through a 3-stage cp.async ring in shared memory with row strides = 4 (mod
+// 16) doubles, so the fragment loads (lane -> (k = lane & 3, m = lane >> 2))
+// are bank-conflict free.  Out-of-range elements are zero-filled by the copy.
+// Triangular solves and inverses are recursive: halves down to 64 x 64
+// diagonal blocks, inverted explicitly by one CTA each; everything else is GEMM.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "dblas.cuh"
+
+namespace hcamg {
+namespace dblas {
+
+namespace {
+
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, THREADS = 256;
+constexpr int LDA_S = BM + 4, LDB_S = BN + 4;
+constexpr int STAGE_DOUBLES = BK * LDA_S + BK * LDB_S;
+constexpr size_t SMEM = sizeof(double) * STAGES * STAGE_DOUBLES;
+constexpr int NB0 = 64;  // recursion leaf of the triangular routines
+
+struct GemmArgs {
+  int64_t m, n, k, lda, ldb, ldc;
+  double alpha, beta;
+  const double* A;
+  const double* B;
+  double* C;
+  const double* const* Ab;
+  const double* const* Bb;
+  double* const* Cb;
+  int lower;     // only C entries with row >= col
+  int kfromrow;  // op(A) is upper triangular in (row, k): k starts at the tile's first row
+};
+
+__device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int kN>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(kN) : "memory");
+}
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int TA, int TB>
+__global__ void __launch_bounds__(THREADS) k_dgemm(GemmArgs g) {
+  extern __shared__ __align__(16) double smem[];
+  const int64_t bz = blockIdx.z;
+  const double* A = g.Ab ? g.Ab[bz] : g.A;
+  const double* B = g.Bb ? g.Bb[bz] : g.B;
+  double* C = g.Cb ? g.Cb[bz] : g.C;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;
+  if (g.lower && m0 + BM <= n0) return;  // tile strictly above the diagonal
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int wm = w & 3, wn = w >> 2;
+  const int64_t kbeg = g.kfromrow ? (m0 / BK) * BK : 0;
+  const int64_t ktiles = g.k > kbeg ? (g.k - kbeg + BK - 1) / BK : 0;
+
+  auto load = [&](int64_t kt, int st) {
+    double* As = smem + (size_t)st * STAGE_DOUBLES;
+    double* Bs = As + BK * LDA_S;
+    const int64_t k0 = kbeg + kt * BK;
+#pragma unroll
+    for (int r = 0; r < (BM * BK) / THREADS; ++r) {
+      const int idx = t + THREADS * r;
+      int il, kl;
+      if (TA == 0) { il = idx % BM; kl = idx / BM; }
+      else { kl = idx % BK; il = idx / BK; }
+      const int64_t i = m0 + il, kk = k0 + kl;
+      const bool ok = i < g.m && kk < g.k;
+      const double* src = ok ? (TA == 0 ? A + i + kk * g.lda : A + kk + i * g.lda) : A;
+      cp8(As + kl * LDA_S + il, src, ok);
+    }
+#pragma unroll
+    for (int r = 0; r < (BN * BK) / THREADS; ++r) {
+      const int idx = t + THREADS * r;
+      int jl, kl;
+      if (TB == 0) { kl = idx % BK; jl = idx / BK; }
+      else { jl = idx % BN; kl = idx / BN; }
+      const int64_t j = n0 + jl, kk = k0 + kl;
+      const bool ok = j < g.n && kk < g.k;
+      const double* src = ok ? (TB == 0 ? B + kk + j * g.ldb : B + j + kk * g.ldb) : B;
+      cp8(Bs + kl * LDB_S + jl, src, ok);
+    }
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load(s, s);
+    cp_commit();
+  }
+  for (int64_t kt = 0; kt < ktiles; ++kt) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    if (kt + STAGES - 1 < ktiles) load(kt + STAGES - 1, (int)((kt + STAGES - 1) % STAGES));
+    cp_commit();
+    const double* As = smem + (size_t)(kt % STAGES) * STAGE_DOUBLES;
+    const double* Bs = As + BK * LDA_S;
+#pragma unroll
+    for (int k4 = 0; k4 < BK / 4; ++k4) {
+      const int kr = k4 * 4 + (lane & 3);
+      double a[4], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) a[mi] = As[kr * LDA_S + wm * 32 + mi * 8 + (lane >> 2)];
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[kr * LDB_S + wn * 32 + ni * 8 + (lane >> 2)];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+    }
+  }
+  cp_wait<0>();
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t i = m0 + wm * 32 + mi * 8 + (lane >> 2);
+        const int64_t j = n0 + wn * 32 + ni * 8 + 2 * (lane & 3) + h;
+        if (i >= g.m || j >= g.n || (g.lower && i < j)) continue;
+        double* c = C + i + j * g.ldc;
+        const double v = g.alpha * acc[mi][ni][h];
+        *c = g.beta == 0.0 ? v : fma(g.beta, *c, v);
+      }
+}
+
+void launch(const GemmArgs& g, Op ta, Op tb, int64_t batch, cudaStream_t s) {
+  if (g.m <= 0 || g.n <= 0 || batch <= 0) return;
+  static bool init = false;
+  if (!init) {
+    HC_CUDA(cudaFuncSetAttribute(k_dgemm<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    HC_CUDA(cudaFuncSetAttribute(k_dgemm<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    HC_CUDA(cudaFuncSetAttribute(k_dgemm<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    HC_CUDA(cudaFuncSetAttribute(k_dgemm<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+    init = true;
+  }
+  const dim3 grid((unsigned)((g.m + BM - 1) / BM), (unsigned)((g.n + BN - 1) / BN), (unsigned)batch);
+  require(grid.y <= 65535 && grid.z <= 65535, "dblas::gemm: grid too large");
+  if (ta == N && tb == N) k_dgemm<0, 0><<<grid, THREADS, SMEM, s>>>(g);
+  else if (ta == N && tb == T) k_dgemm<0, 1><<<grid, THREADS, SMEM, s>>>(g);
+  else if (ta == T && tb == N) k_dgemm<1, 0><<<grid, THREADS, SMEM, s>>>(g);
+  else k_dgemm<1, 1><<<grid, THREADS, SMEM, s>>>(g);
+  HC_CHECK_LAUNCH();
+}
+
+// Inverse of the lower-triangular nb x nb blocks (nb <= 64) of a batch: one
+// CTA of 64 threads per block, column j of the inverse by thread j
+// (forward substitution on e_j), L staged in shared memory.
+__global__ void __launch_bounds__(64) k_trtri_leaf(int nb, const double* const* Lp, const double* L0, int64_t ldl,
+                                                   double* const* Lip, double* Li0, int64_t ldi, int64_t stride) {
+  extern __shared__ double leaf_smem[];
+  double(*Ls)[NB0 + 1] = reinterpret_cast<double(*)[NB0 + 1]>(leaf_smem);
+  double(*X)[NB0 + 1] = reinterpret_cast<double(*)[NB0 + 1]>(leaf_smem + NB0 * (NB0 + 1));
+  const int64_t bz = blockIdx.x;
+  const double* L = Lp ? Lp[bz] : L0 + bz * stride * (ldl + 1);
+  double* Li = Lip ? Lip[bz] : Li0 + bz * stride * (ldi + 1);
+  const int j = threadIdx.x;
+  for (int c = 0; c < nb; ++c)
+    if (j < nb) Ls[j][c] = j >= c ? L[j + (int64_t)c * ldl] : 0.0;
+  __syncthreads();
+  if (j < nb) {
+    for (int i = 0; i < nb; ++i) {
+      double v = i == j ? 1.0 : 0.0;
+      for (int p = j; p < i; ++p) v = fma(-Ls[i][p], X[p][j], v);
+      X[i][j] = i >= j ? v / Ls[i][i] : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int c = 0; c < nb; ++c)
+    if (j < nb) Li[j + (int64_t)c * ldi] = X[j][c];
+}
+
+// dst (rows x cols, ld ldd) = src (ld lds)
+__global__ void k_copy2d(int64_t rows, int64_t cols, const double* __restrict__ src, int64_t lds,
+                         double* __restrict__ dst, int64_t ldd) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows * cols; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % rows, c = t / rows;
+    dst[i + c * ldd] = src[i + c * lds];
+  }
+}
+
+void copy2d(int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return;
+  k_copy2d<<<grid_for(rows * cols, 256, kSMs * 16), 256, 0, s>>>(rows, cols, src, lds, dst, ldd);
+  HC_CHECK_LAUNCH();
+}
+
+constexpr size_t LEAF_SMEM = sizeof(double) * 2 * NB0 * (NB0 + 1);
+
+void leaf_init() {
+  static bool init = false;
+  if (!init) {
+    HC_CUDA(cudaFuncSetAttribute(k_trtri_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LEAF_SMEM));
+    init = true;
+  }
+}
+
+int64_t split_at(int64_t m) {  // first half, a multiple of the leaf size
+  const int64_t h = (m / 2 + NB0 - 1) / NB0 * NB0;
+  return std::min<int64_t>(std::max<int64_t>(h, NB0), m - 1);
+}
+
+}  // namespace
+
+void gemm(Op ta, Op tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda, const double* B,
+          int64_t ldb, double beta, double* C, int64_t ldc, cudaStream_t s, bool lower) {
+  GemmArgs g{m, n, k, lda, ldb, ldc, alpha, beta, A, B, C, nullptr, nullptr, nullptr, lower ? 1 : 0, 0};
+  launch(g, ta, tb, 1, s);
+  count_flops(2.0 * m * n * k * (lower ? 0.5 : 1.0));
+}
+
+void gemm_batched(Op ta, Op tb, int64_t m, int64_t n, int64_t k, double alpha, const double* const* A, int64_t lda,
+                  const double* const* B, int64_t ldb, double beta, double* const* C, int64_t ldc, int64_t batch,
+                  cudaStream_t s) {
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = std::min<int64_t>(65535, batch - b0);
+    GemmArgs g{m, n, k, lda, ldb, ldc, alpha, beta, nullptr, nullptr, nullptr, A + b0, B + b0, C + b0, 0, 0};
+    launch(g, ta, tb, nb, s);
+  }
+  count_flops(2.0 * m * n * k * batch);
+}
+
+void gemm_tri_lower_tn(int64_t n, const double* Y, int64_t ldy, double* C, int64_t ldc, cudaStream_t s) {
+  GemmArgs g{n, n, n, ldy, ldy, ldc, 1.0, 0.0, Y, Y, C, nullptr, nullptr, nullptr, 1, 1};
+  launch(g, T, N, 1, s);
+  count_flops(2.0 * n * n * n / 6.0);
+}
+
+void syrk_ln(int64_t n, int64_t k, double alpha, const double* A, int64_t lda, double beta, double* C, int64_t ldc,
+             cudaStream_t s) {
+  gemm(N, T, n, n, k, alpha, A, lda, A, lda, beta, C, ldc, s, true);
+}
+
+void trtri_lower(int64_t n, const double* L, int64_t ldl, double* Li, int64_t ldi, cudaStream_t s) {
+  if (n <= 0) return;
+  if (n <= NB0) {
+    leaf_init();
+    k_trtri_leaf<<<1, NB0, LEAF_SMEM, s>>>((int)n, nullptr, L, ldl, nullptr, Li, ldi, 0);
+    HC_CHECK_LAUNCH();
+    count_flops((double)n * n * n / 3.0);
+    return;
+  }
+  // [L11 0; L21 L22]^{-1} = [Li11 0; -Li22 L21 Li11  Li22]
+  const int64_t m1 = split_at(n), m2 = n - m1;
+  trtri_lower(m1, L, ldl, Li, ldi, s);
+  trtri_lower(m2, L + m1 + m1 * ldl, ldl, Li + m1 + m1 * ldi, ldi, s);
+  DBuf<double> Tm(m2 * m1, s);
+  gemm(N, N, m2, m1, m1, 1.0, L + m1, ldl, Li, ldi, 0.0, Tm.p, m2, s);                    // L21 Li11
+  gemm(N, N, m2, m1, m2, -1.0, Li + m1 + m1 * ldi, ldi, Tm.p, m2, 0.0, Li + m1, ldi, s);  // -Li22 (L21 Li11)
+  if (m1 > 0) HC_CUDA(cudaMemset2DAsync(Li + m1 * ldi, sizeof(double) * ldi, 0, sizeof(double) * m1, m2, s));
+}
+
+void trtri_lower_batched(int64_t nb, const double* const* L, int64_t ldl, double* const* Li, int64_t ldi, int64_t batch,
+                         cudaStream_t s) {
+  if (batch <= 0) return;
+  if (nb <= NB0) {
+    leaf_init();
+    k_trtri_leaf<<<(unsigned)batch, NB0, LEAF_SMEM, s>>>((int)nb, L, nullptr, ldl, Li, nullptr, ldi, 0);
+    HC_CHECK_LAUNCH();
+    count_flops((double)nb * nb * nb / 3.0 * batch);
+    return;
+  }
+  std::vector<const double*> hl((size_t)batch);
+  std::vector<double*> hi((size_t)batch);
+  HC_CUDA(cudaMemcpyAsync(hl.data(), L, sizeof(void*) * batch, cudaMemcpyDeviceToHost, s));
+  HC_CUDA(cudaMemcpyAsync(hi.data(), Li, sizeof(void*) * batch, cudaMemcpyDeviceToHost, s));
+  HC_CUDA(cudaStreamSynchronize(s));
+  for (int64_t b = 0; b < batch; ++b) trtri_lower(nb, hl[(size_t)b], ldl, hi[(size_t)b], ldi, s);
+}
+
+void trsm(Side side, Op op, int64_t m, int64_t n, const double* L, int64_t ldl, double* B, int64_t ldb,
+          cudaStream_t s) {
+  const int64_t d = side == Left ? m : n;  // dimension of L
+  if (m <= 0 || n <= 0) return;
+  if (d <= NB0) {
+    // leaf: X = op(Li) B (left) or B op(Li) (right) through a temporary
+    DBuf<double> Li(d * d, s), X(m * n, s);
+    trtri_lower(d, L, ldl, Li.p, d, s);
+    if (side == Left) gemm(op, N, m, n, d, 1.0, Li.p, d, B, ldb, 0.0, X.p, m, s);
+    else gemm(N, op, m, n, d, 1.0, B, ldb, Li.p, d, 0.0, X.p, m, s);
+    copy2d(m, n, X.p, m, B, ldb, s);
+    return;
+  }
+  const int64_t d1 = split_at(d), d2 = d - d1;
+  const double* L11 = L;
+  const double* L21 = L + d1;
+  const double* L22 = L + d1 + d1 * ldl;
+  if (side == Left && op == N) {        // L X = B
+    trsm(side, op, d1, n, L11, ldl, B, ldb, s);
+    gemm(N, N, d2, n, d1, -1.0, L21, ldl, B, ldb, 1.0, B + d1, ldb, s);
+    trsm(side, op, d2, n, L22, ldl, B + d1, ldb, s);
+  } else if (side == Left) {           // L^T X = B
+    trsm(side, op, d2, n, L22, ldl, B + d1, ldb, s);
+    gemm(T, N, d1, n, d2, -1.0, L21, ldl, B + d1, ldb, 1.0, B, ldb, s);
+    trsm(side, op, d1, n, L11, ldl, B, ldb, s);
+  } else if (op == T) {                // X L^T = B
+    trsm(side, op, m, d1, L11, ldl, B, ldb, s);
+    gemm(N, T, m, d2, d1, -1.0, B, ldb, L21, ldl, 1.0, B + d1 * ldb, ldb, s);
+    trsm(side, op, m, d2, L22, ldl, B + d1 * ldb, ldb, s);
+  } else {                             // X L = B
+    trsm(side, op, m, d2, L22, ldl, B + d1 * ldb, ldb, s);
+    gemm(N, N, m, d1, d2, -1.0, B + d1 * ldb, ldb, L21, ldl, 1.0, B, ldb, s);
+    trsm(side, op, m, d1, L11, ldl, B, ldb, s);
+  }
+}
+
+void trsm_rlt_batched(int64_t m, int64_t nb, const double* const* L, int64_t ldl, double* const* B, int64_t ldb,
+                      int64_t batch, cudaStream_t s) {
+  // X_i = B_i L_i^{-T}: the inverses (distinct tiles only), then one batched GEMM into temporaries
+  if (batch <= 0) return;
+  std::vector<const double*> hl((size_t)batch);
+  std::vector<double*> hb((size_t)batch);
+  HC_CUDA(cudaMemcpyAsync(hl.data(), L, sizeof(void*) * batch, cudaMemcpyDeviceToHost, s));
+  HC_CUDA(cudaMemcpyAsync(hb.data(), B, sizeof(void*) * batch, cudaMemcpyDeviceToHost, s));
+  HC_CUDA(cudaStreamSynchronize(s));
+  std::vector<const double*> uniq;
+  std::vector<int64_t> which((size_t)batch);
+  for (int64_t b = 0; b < batch; ++b) {
+    auto it = std::find(uniq.begin(), uniq.end(), hl[(size_t)b]);
+    which[(size_t)b] = it - uniq.begin();
+    if (it == uniq.end()) uniq.push_back(hl[(size_t)b]);
+  }
+  DBuf<double> Li((int64_t)uniq.size() * nb * nb, s), X(batch * m * nb, s);
+  for (size_t u = 0; u < uniq.size(); ++u) trtri_lower(nb, uniq[u], ldl, Li.p + u * nb * nb, nb, s);
+  std::vector<const double*> pa((size_t)batch), pb((size_t)batch);
+  std::vector<double*> pc((size_t)batch);
+  for (int64_t b = 0; b < batch; ++b) {
+    pa[(size_t)b] = hb[(size_t)b];
+    pb[(size_t)b] = Li.p + which[(size_t)b] * nb * nb;
+    pc[(size_t)b] = X.p + b * m * nb;
+  }
+  DBuf<const double*> da, db;
+  DBuf<double*> dc;
+  da.upload(pa.data(), batch, s);
+  db.upload(pb.data(), batch, s);
+  dc.upload(pc.data(), batch, s);
+  gemm_batched(N, T, m, nb, nb, 1.0, da.p, ldb, db.p, nb, 0.0, dc.p, m, batch, s);
+  for (int64_t b = 0; b < batch; ++b) copy2d(m, nb, X.p + b * m * nb, m, hb[(size_t)b], ldb, s);
+  HC_CUDA(cudaStreamSynchronize(s));  // host pointer vectors go out of scope
+}
+
+}  // namespace dblas
+}  // namespace hcamg

@@ -1,0 +1,50 @@
+// FP64 level-3 kernels of the dense setup work (sm_100a, DMMA m8n8k4 tensor-core
+// instructions): GEMM (also batched over pointer arrays and restricted to the
+// lower triangle for SYRK), triangular solves and the triangular inverse.
+// Column-major with cuBLAS's argument conventions, so each call site in
+// dense.cu / giant.cu reads like the BLAS call it replaces.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace hcamg {
+namespace dblas {
+
+enum Op : int { N = 0, T = 1 };
+enum Side : int { Left = 0, Right = 1 };
+
+// C = alpha op(A) op(B) + beta C   (m x n, inner k).  lower: only C's entries
+// with row >= col are computed / written (SYRK: op(B) = op(A)^T).
+void gemm(Op ta, Op tb, int64_t m, int64_t n, int64_t k, double alpha, const double* A, int64_t lda, const double* B,
+          int64_t ldb, double beta, double* C, int64_t ldc, cudaStream_t s, bool lower = false);
+// the same for `batch` independent products given by device pointer arrays
+void gemm_batched(Op ta, Op tb, int64_t m, int64_t n, int64_t k, double alpha, const double* const* A, int64_t lda,
+                  const double* const* B, int64_t ldb, double beta, double* const* C, int64_t ldc, int64_t batch,
+                  cudaStream_t s);
+// C (n x n, lower triangle) = alpha A A^T + beta C  (A n x k), cublasDsyrk(LOWER, N)
+void syrk_ln(int64_t n, int64_t k, double alpha, const double* A, int64_t lda, double beta, double* C, int64_t ldc,
+             cudaStream_t s);
+
+// lower(C) = Y^T Y for a lower-triangular n x n Y (the inner sum of entry
+// (i, j), i >= j, runs over k >= i only; n^3/3 flops)
+void gemm_tri_lower_tn(int64_t n, const double* Y, int64_t ldy, double* C, int64_t ldc, cudaStream_t s);
+
+// Triangular solves with a lower-triangular, non-unit L (cublasDtrsm with
+// FILL_MODE_LOWER, DIAG_NON_UNIT, alpha = 1):
+//   Left:  op(L) X = B  (B m x n, L m x m);   Right: X op(L) = B  (L n x n).
+// Recursive: halves of L down to 64 x 64 diagonal blocks applied as their
+// explicit inverses; everything else is GEMM.
+void trsm(Side side, Op op, int64_t m, int64_t n, const double* L, int64_t ldl, double* B, int64_t ldb,
+          cudaStream_t s);
+// Batched right-side solve X L^T = B for `batch` pairs of nb x nb tiles (m rows of B).
+void trsm_rlt_batched(int64_t m, int64_t nb, const double* const* L, int64_t ldl, double* const* B, int64_t ldb,
+                      int64_t batch, cudaStream_t s);
+// Li = L^{-1} for a lower-triangular n x n L (Li lower, ld ldi; the strict upper part is zeroed).
+void trtri_lower(int64_t n, const double* L, int64_t ldl, double* Li, int64_t ldi, cudaStream_t s);
+// Batched inverses of `batch` nb x nb lower-triangular tiles.
+void trtri_lower_batched(int64_t nb, const double* const* L, int64_t ldl, double* const* Li, int64_t ldi, int64_t batch,
+                         cudaStream_t s);
+
+}  // namespace dblas
+}  // namespace hcamg

@@ -2,6 +2,7 @@
 #include <cmath>
 #include <vector>
 
+#include "dblas.cuh"
 #include "dense.cuh"
 
 namespace hcamg {
@@ -132,10 +133,6 @@ __global__ void k_diag_absmax(const double* __restrict__ A, int64_t k, int64_t l
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
-void cublas_check(cublasStatus_t st, const char* what) {
-  if (st != CUBLAS_STATUS_SUCCESS) throw Error(ECUDA_, std::string("cuBLAS failure in ") + what);
-}
-
 }  // namespace
 
 void batched_small_spd_solve(const DenseJob* d_jobs, int64_t njobs, double* A, double* B, double* piv,
@@ -154,14 +151,12 @@ void batched_small_spd_inverse(const DenseJob* d_jobs, int64_t njobs, double* A,
   HC_CHECK_LAUNCH();
 }
 
-int64_t dense_cholesky_raw(cublasHandle_t h, double* A, int64_t k, int64_t ld, double* piv, cudaStream_t s) {
+int64_t dense_cholesky_raw(double* A, int64_t k, int64_t ld, double* piv, cudaStream_t s) {
   if (k == 0) return 0;
-  cublas_check(cublasSetStream(h, s), "setStream");
   DBuf<int> bad(1, s);
   bad.fill_bytes(0xff);
   const size_t smem = sizeof(double) * kTile * (kTile + 1);
   HC_CUDA(cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const double one = 1.0, mone = -1.0;
   for (int64_t kb = 0; kb < k; kb += kTile) {
     const int nb = (int)std::min<int64_t>(kTile, k - kb);
     double* Akk = A + kb + kb * ld;
@@ -174,11 +169,8 @@ int64_t dense_cholesky_raw(cublasHandle_t h, double* A, int64_t k, int64_t ld, d
     if (rest > 0) {
       double* A21 = Akk + nb;
       double* A22 = A21 + nb * ld;
-      cublas_check(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT,
-                               (int)rest, nb, &one, Akk, (int)ld, A21, (int)ld), "dtrsm");
-      count_flops((double)rest * nb * nb + (double)rest * rest * nb);
-      cublas_check(cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, (int)rest, nb, &mone, A21, (int)ld, &one,
-                               A22, (int)ld), "dsyrk");
+      dblas::trsm(dblas::Right, dblas::T, rest, nb, Akk, ld, A21, ld, s);  // A21 L11^{-T}
+      dblas::syrk_ln(rest, nb, -1.0, A21, ld, 1.0, A22, ld, s);           // A22 -= A21 A21^T
     }
   }
   return k;
@@ -198,14 +190,14 @@ int64_t pivot_verdict(const std::vector<double>& hp, int64_t k, int64_t j0, doub
   return hp[(size_t)am] <= floor_ ? am : -1;
 }
 
-int64_t dense_cholesky(cublasHandle_t h, double* A, int64_t k, int64_t ld, cudaStream_t s) {
+int64_t dense_cholesky(double* A, int64_t k, int64_t ld, cudaStream_t s) {
   if (k == 0) return -1;
   DBuf<unsigned long long> mx(1, s);
   mx.zero();
   k_diag_absmax<<<grid_for(k, 256), 256, 0, s>>>(A, k, ld, mx.p);
   HC_CHECK_LAUNCH();
   DBuf<double> piv(k, s);
-  const int64_t j0 = dense_cholesky_raw(h, A, k, ld, piv.p, s);
+  const int64_t j0 = dense_cholesky_raw(A, k, ld, piv.p, s);
   unsigned long long hm = read_scalar(mx.p, s);
   double scale;
   memcpy(&scale, &hm, 8);
@@ -221,64 +213,29 @@ __global__ void k_sym_from_lower(const double* __restrict__ Lw, int64_t n, doubl
     out[t] = i >= j ? Lw[i + j * n] : Lw[j + i * n];
   }
 }
-__global__ void k_eye_panel(double* __restrict__ X, int64_t n, int64_t j0, int64_t nb) {
-  // X = columns [j0, j0 + nb) of the identity, rows [j0, n) (column-major, ld n)
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (n - j0) * nb; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = j0 + t % (n - j0), c = j0 + t / (n - j0);
-    X[r + c * n] = r == c ? 1.0 : 0.0;
-  }
-}
 }  // namespace
 
 // A^{-1} from its Cholesky factor L (lower, column-major in Lbuf, ld = n),
-// exactly symmetric: Y = L^{-1} block column by block column (TRSM on the
-// trailing panel only, n^3/3 flops), then the lower triangle of Y^T Y block
-// column by block column with TRMM (Y[J:, J] is all of column block J, and
-// Y[J:, J:] is triangular: another n^3/3), written over Lbuf; the full
-// symmetric inverse goes to Ainv.  (Two full TRSMs against the identity
-// cost 2 n^3.)
-void dense_spd_inverse(cublasHandle_t h, double* Lbuf, int64_t n, double* Ainv, cudaStream_t s) {
+// exactly symmetric: Y = L^{-1} (recursive triangular inverse, n^3/3 flops),
+// then the lower triangle of Y^T Y by GEMM tiles that start their inner
+// dimension at their first row (Y is lower triangular: another n^3/3), written
+// over Lbuf; the full symmetric inverse goes to Ainv.
+void dense_spd_inverse(double* Lbuf, int64_t n, double* Ainv, cudaStream_t s) {
   if (n == 0) return;
-  cublas_check(cublasSetStream(h, s), "setStream");
-  constexpr int64_t NB = 1024;
-  const double one = 1.0;
-  // Y = L^{-1} into Ainv (zero above the diagonal blocks)
-  HC_CUDA(cudaMemsetAsync(Ainv, 0, sizeof(double) * (size_t)(n * n), s));
-  for (int64_t j0 = 0; j0 < n; j0 += NB) {
-    const int64_t nb = std::min(NB, n - j0), m = n - j0;
-    k_eye_panel<<<grid_for(m * nb, 256), 256, 0, s>>>(Ainv, n, j0, nb);
-    HC_CHECK_LAUNCH();
-    cublas_check(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m,
-                             (int)nb, &one, Lbuf + j0 + j0 * n, (int)n, Ainv + j0 + j0 * n, (int)n),
-                 "dtrsm L^-1 panel");
-    count_flops((double)m * m * nb);
-  }
+  dblas::trtri_lower(n, Lbuf, n, Ainv, n, s);
   StageTimer st(s);
   st.mark("    inverse: Y = L^-1");
-  // lower(Y^T Y) block column J: Y[J:, J:]^T Y[J:, J]  -> Lbuf[J:, J]
-  for (int64_t j0 = 0; j0 < n; j0 += NB) {
-    const int64_t nb = std::min(NB, n - j0), m = n - j0;
-    cublas_check(cublasDtrmm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)m,
-                             (int)nb, &one, Ainv + j0 + j0 * n, (int)n, Ainv + j0 + j0 * n, (int)n,
-                             Lbuf + j0 + j0 * n, (int)n),
-                 "dtrmm Y^T Y");
-    count_flops((double)m * m * nb);
-  }
+  dblas::gemm_tri_lower_tn(n, Ainv, n, Lbuf, n, s);
   st.mark("    inverse: lower(Y^T Y)");
   k_sym_from_lower<<<grid_for(n * n, 256, kSMs * 32), 256, 0, s>>>(Lbuf, n, Ainv);
   HC_CHECK_LAUNCH();
 }
 
-void dense_cholesky_solve(cublasHandle_t h, const double* L, int64_t k, int64_t ld, double* B, int64_t nrhs,
-                          int64_t ldb, cudaStream_t s) {
+void dense_cholesky_solve(const double* L, int64_t k, int64_t ld, double* B, int64_t nrhs, int64_t ldb,
+                          cudaStream_t s) {
   if (k == 0 || nrhs == 0) return;
-  cublas_check(cublasSetStream(h, s), "setStream");
-  const double one = 1.0;
-  cublas_check(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)k,
-                           (int)nrhs, &one, L, (int)ld, B, (int)ldb), "dtrsm L");
-  cublas_check(cublasDtrsm(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)k,
-                           (int)nrhs, &one, L, (int)ld, B, (int)ldb), "dtrsm L^T");
-  count_flops(2.0 * k * k * nrhs);
+  dblas::trsm(dblas::Left, dblas::N, k, nrhs, L, ld, B, ldb, s);
+  dblas::trsm(dblas::Left, dblas::T, k, nrhs, L, ld, B, ldb, s);
 }
 
 }  // namespace hcamg

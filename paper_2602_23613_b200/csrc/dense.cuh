@@ -5,7 +5,6 @@
 // pivot is <= 0 the first pivot under the floor is reported (the slow column
 // loop's answer), otherwise the smallest pivot if it is under the floor.
 #pragma once
-#include <cublas_v2.h>
 
 #include <vector>
 
@@ -33,19 +32,19 @@ void batched_small_spd_inverse(const DenseJob* d_jobs, int64_t njobs, double* A,
 
 // Large SPD factor in place (column-major, lower, leading dim ld).  Returns
 // -1 on success or the failing pivot index (reference semantics).
-int64_t dense_cholesky(cublasHandle_t h, double* A, int64_t k, int64_t ld, cudaStream_t s);
+int64_t dense_cholesky(double* A, int64_t k, int64_t ld, cudaStream_t s);
 
 // Factor in place and write the pivots; returns the index of the first
 // non-positive / non-finite pivot, or k.  No verdict.
-int64_t dense_cholesky_raw(cublasHandle_t h, double* A, int64_t k, int64_t ld, double* piv, cudaStream_t s);
+int64_t dense_cholesky_raw(double* A, int64_t k, int64_t ld, double* piv, cudaStream_t s);
 // Reference breakdown verdict from the pivots (-1: fine).
 int64_t pivot_verdict(const std::vector<double>& hp, int64_t k, int64_t j0, double scale);
 
 // B := A^{-1} B using the factor produced by dense_cholesky.
 // A^{-1} (exactly symmetric, n x n into Ainv) from the lower Cholesky factor in Lbuf (ld n;
 // overwritten).
-void dense_spd_inverse(cublasHandle_t h, double* Lbuf, int64_t n, double* Ainv, cudaStream_t s);
-void dense_cholesky_solve(cublasHandle_t h, const double* L, int64_t k, int64_t ld, double* B, int64_t nrhs,
-                          int64_t ldb, cudaStream_t s);
+void dense_spd_inverse(double* Lbuf, int64_t n, double* Ainv, cudaStream_t s);
+void dense_cholesky_solve(const double* L, int64_t k, int64_t ld, double* B, int64_t nrhs, int64_t ldb,
+                          cudaStream_t s);
 
 }  // namespace hcamg

@@ -26,6 +26,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "dblas.cuh"
 #include "dense.cuh"
 #include "giant.cuh"
 #include "dist.cuh"
@@ -37,9 +38,6 @@ namespace {
 
 constexpr int64_t kNB = 1024;
 
-void cb(cublasStatus_t st, const char* what) {
-  if (st != CUBLAS_STATUS_SUCCESS) throw Error(ECUDA_, std::string("cuBLAS failure in ") + what);
-}
 
 // Lower Cholesky factor in NB x NB column-major tiles, stored only inside the
 // block envelope: block row I keeps tiles J in [j0[I], I], where j0[I] is the
@@ -422,16 +420,6 @@ __global__ void __launch_bounds__(256) k_spmm_rows(const int64_t* __restrict__ a
   }
 }
 
-__global__ void k_to_f32(const double* __restrict__ in, int64_t n, float* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = (float)in[i];
-}
-
-__global__ void k_to_f64(const float* __restrict__ in, int64_t n, double* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = (double)in[i];
-}
-
 __global__ void k_add_csr_dense(const int64_t* __restrict__ wp, const int32_t* __restrict__ wi,
                                 const double* __restrict__ wv, int64_t n, int64_t nc, double* __restrict__ Y) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
@@ -617,7 +605,7 @@ void blocks_transpose(std::vector<const double*>& src, int64_t lds, std::vector<
 // tile are not part of L.  Linv_II = L_II^{-1} (TRSM on identity blocks), M_I = Linv_II
 // L_{I,I-1}, N_I = Linv_II^T L_{I+1,I}^T, forward folds L_{i,I-1} copied
 // row-major; the backward folds are columns of L, read in place.
-void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_t s) {
+void build_factor_ops(const Packed& L, FactorP& f, cudaStream_t s) {
   // SP sweep blocks per factor tile (SB <= NB) or Q factor tiles per sweep block (SB = Q NB)
   constexpr int64_t SP = kSB <= kNB ? kNB / kSB : 1, Q = kSB > kNB ? kSB / kNB : 1;
   static_assert(SP * kSB == kNB || Q * kNB == kSB, "sweep block and factor tile must nest");
@@ -706,25 +694,8 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
   DBuf<double> fpool((TS + nM + nF) * SS, s), bpool((TS + nN) * SS, s);
   auto fp = [&](int64_t slot) { return fpool.p + slot * SS; };
   auto bp = [&](int64_t slot) { return bpool.p + slot * SS; };
-  cb(cublasSetStream(h, s), "setStream");
-  const double one = 1.0, zero = 0.0;
   {
-    std::vector<double*> eye;
-    std::vector<const double*> lii;
-    for (int64_t I = 0; I < TS; ++I) {
-      eye.push_back(bp(I));
-      lii.push_back(sub(I, I));
-    }
-    DBuf<double*> de;
-    de.upload(eye.data(), TS, s);
-    k_blocks_eye<<<dim3(128, (unsigned)TS), 256, 0, s>>>(de.p);
-    HC_CHECK_LAUNCH();
-    DBuf<const double*> dl;
-    dl.upload(lii.data(), TS, s);
-    cb(cublasDtrsmBatched(h, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)kSB,
-                          (int)kSB, &one, dl.p, (int)LDS, de.p, (int)kSB, (int)TS),
-       "dtrsmBatched Linv");
-    count_flops((double)TS * kSB * kSB * kSB);
+    for (int64_t I = 0; I < TS; ++I) dblas::trtri_lower(kSB, sub(I, I), LDS, bp(I), kSB, s);  // Linv_II
     HC_CUDA(cudaStreamSynchronize(s));
     std::vector<const double*> src;
     std::vector<double*> dst;
@@ -734,18 +705,15 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
     }
     blocks_transpose(src, kSB, dst, s);
   }
-  auto batched_gemm = [&](cublasOperation_t ta, std::vector<const double*>& ha, std::vector<const double*>& hb,
-                          std::vector<double*>& hc, const char* what) {
+  auto batched_gemm = [&](dblas::Op ta, std::vector<const double*>& ha, std::vector<const double*>& hb,
+                          std::vector<double*>& hc) {
     if (ha.empty()) return;
     DBuf<const double*> da, db;
     DBuf<double*> dc;
     da.upload(ha.data(), (int64_t)ha.size(), s);
     db.upload(hb.data(), (int64_t)hb.size(), s);
     dc.upload(hc.data(), (int64_t)hc.size(), s);
-    cb(cublasDgemmBatched(h, ta, ta, (int)kSB, (int)kSB, (int)kSB, &one, da.p, (int)LDS, db.p, (int)kSB, &zero, dc.p,
-                          (int)kSB, (int)ha.size()),
-       what);
-    count_flops(2.0 * kSB * kSB * kSB * (double)ha.size());
+    dblas::gemm_batched(ta, ta, kSB, kSB, kSB, 1.0, da.p, LDS, db.p, kSB, 0.0, dc.p, kSB, (int64_t)ha.size(), s);
     HC_CUDA(cudaStreamSynchronize(s));
   };
   {  // row-major M_I = column-major (L_{I,I-1}^T Linv_II^T)
@@ -757,7 +725,7 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
         hb.push_back(bp(I));
         hc.push_back(fp(TS + mslot[(size_t)I]));
       }
-    batched_gemm(CUBLAS_OP_T, ha, hb, hc, "dgemmBatched M");
+    batched_gemm(dblas::T, ha, hb, hc);
   }
   {  // row-major N_I = column-major (L_{I+1,I} Linv_II)
     std::vector<const double*> ha, hb;
@@ -768,7 +736,7 @@ void build_factor_ops(cublasHandle_t h, const Packed& L, FactorP& f, cudaStream_
         hb.push_back(bp(I));
         hc.push_back(bp(TS + nslot[(size_t)I]));
       }
-    batched_gemm(CUBLAS_OP_N, ha, hb, hc, "dgemmBatched N");
+    batched_gemm(dblas::N, ha, hb, hc);
   }
   std::vector<TriSrcStep> fs, bs;
   {
@@ -919,8 +887,8 @@ __global__ void k_unperm_sym(int64_t m, const int32_t* __restrict__ colperm, con
 }
 }  // namespace
 
-void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m, cudaStream_t s, FactorP* fac,
-                        double* D, bool want_z) {
+void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, FactorP* fac, double* D,
+                        bool want_z) {
   const int64_t n = Agg.nrows;
   StageTimer st(s);
   // ordering: reverse Cuthill-McKee (default) or the natural component order
@@ -977,13 +945,11 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
   double scale;
   memcpy(&scale, &hm, 8);
   DBuf<double> piv(T * kNB, s);
-  cb(cublasSetStream(h, s), "setStream");
-  const double one = 1.0, mone = -1.0;
   DBuf<const double*> dA, dB;
   DBuf<const double*> dC;
   int64_t fail = -1;
   for (int64_t K = 0; K < T; ++K) {  // right-looking, inside the envelope
-    const int64_t j0 = dense_cholesky_raw(h, L.tile(K, K), kNB, kNB, piv.p + K * kNB, s);  // counts its own flops
+    const int64_t j0 = dense_cholesky_raw(L.tile(K, K), kNB, kNB, piv.p + K * kNB, s);
     if (j0 < kNB) {
       fail = K * kNB + j0;
       break;
@@ -997,10 +963,7 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
       for (int64_t I : below) hb.push_back(L.tile(I, K));
       const double** pa = upload_ptrs(ha, dA, s);
       const double** pb = upload_ptrs(hb, dB, s);
-      cb(cublasDtrsmBatched(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, (int)kNB,
-                            (int)kNB, &one, pa, (int)kNB, (double* const*)pb, (int)kNB, (int)below.size()),
-         "dtrsmBatched");
-      count_flops((double)kNB * kNB * kNB * (double)below.size());
+      dblas::trsm_rlt_batched(kNB, kNB, pa, kNB, (double* const*)pb, kNB, (int64_t)below.size(), s);
     }
     {
       std::vector<const double*> ha, hb, hc;
@@ -1013,10 +976,8 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
       const double** pa = upload_ptrs(ha, dA, s);
       const double** pb = upload_ptrs(hb, dB, s);
       const double** pc = upload_ptrs(hc, dC, s);
-      cb(cublasDgemmBatched(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)kNB, (int)kNB, (int)kNB, &mone, pa, (int)kNB, pb,
-                            (int)kNB, &one, (double* const*)pc, (int)kNB, (int)ha.size()),
-         "dgemmBatched");
-      count_flops(2.0 * kNB * kNB * kNB * (double)ha.size());
+      dblas::gemm_batched(dblas::N, dblas::T, kNB, kNB, kNB, -1.0, pa, kNB, pb, kNB, 1.0, (double* const*)pc, kNB,
+                          (int64_t)ha.size(), s);
       HC_CUDA(cudaStreamSynchronize(s));  // host pointer vectors go out of scope
     }
   }
@@ -1031,7 +992,7 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
   }
   st.mark("  giant: envelope Cholesky");
   if (fac) {
-    build_factor_ops(h, L, *fac, s);
+    build_factor_ops(L, *fac, s);
     fac->nG = n;
     fac->T = T;
     st.mark("  giant: sweep operators");
@@ -1069,16 +1030,10 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
   for (int64_t J = 0; J < T; ++J) {  // U^T = B^T L^{-T}; columns >= active[J] of blocks <= J are zero
     const int ma = (int)active[(size_t)J];
     if (ma == 0) continue;
-    cb(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, ma, (int)nbk(J),
-                   &one, L.tile(J, J), (int)kNB, blk(J), (int)m),
-       "dtrsm fwd");
-    count_flops((double)ma * nbk(J) * nbk(J));
+    dblas::trsm(dblas::Right, dblas::T, ma, nbk(J), L.tile(J, J), kNB, blk(J), m, s);
     for (int64_t I = J + 1; I < T; ++I)
       if (L.has(I, J)) {
-        cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, ma, (int)nbk(I), (int)nbk(J), &mone, blk(J), (int)m,
-                       L.tile(I, J), (int)kNB, &one, blk(I), (int)m),
-           "dgemm fwd");
-        count_flops(2.0 * ma * nbk(I) * nbk(J));
+        dblas::gemm(dblas::N, dblas::T, ma, nbk(I), nbk(J), -1.0, blk(J), m, L.tile(I, J), kNB, 1.0, blk(I), m, s);
       }
   }
   st.mark("  giant: forward solve");
@@ -1088,10 +1043,7 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
     for (int64_t J = 0; J < T; ++J) {
       const int ma = (int)active[(size_t)J];
       if (ma == 0) continue;
-      cb(cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, ma, (int)nbk(J), &one, blk(J), (int)m, &one, Dp.p,
-                     (int)m),
-         "dsyrk Y^T Y");
-      count_flops((double)ma * (ma + 1) * nbk(J));
+      dblas::syrk_ln(ma, nbk(J), 1.0, blk(J), m, 1.0, Dp.p, m, s);
     }
     k_unperm_sym<<<grid_for(m * m, 256, kSMs * 32), 256, 0, s>>>(m, dcol.p, Dp.p, D);
     HC_CHECK_LAUNCH();
@@ -1104,15 +1056,9 @@ void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B, int64_t m,
     return;
   }
   for (int64_t K = T - 1; K >= 0; --K) {  // Z^T = U^T L^{-1}
-    cb(cublasDtrsm(h, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, (int)m, (int)nbk(K),
-                   &one, L.tile(K, K), (int)kNB, blk(K), (int)m),
-       "dtrsm bwd");
-    count_flops((double)m * nbk(K) * nbk(K));
+    dblas::trsm(dblas::Right, dblas::N, m, nbk(K), L.tile(K, K), kNB, blk(K), m, s);
     for (int64_t I = L.j0[(size_t)K]; I < K; ++I) {
-      cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_N, (int)m, (int)kNB, (int)nbk(K), &mone, blk(K), (int)m, L.tile(K, I),
-                     (int)kNB, &one, blk(I), (int)m),
-         "dgemm bwd");
-      count_flops(2.0 * m * kNB * nbk(K));
+      dblas::gemm(dblas::N, dblas::N, m, kNB, nbk(K), -1.0, blk(K), m, L.tile(K, I), kNB, 1.0, blk(I), m, s);
     }
   }
   st.mark("  giant: triangular solves");
@@ -1209,14 +1155,14 @@ __global__ void k_rows_dense(const int64_t* __restrict__ wp, const int32_t* __re
 }
 }  // namespace
 
-void hybrid_ensure_z(cublasHandle_t h, HybridP& hp, cudaStream_t s) {
+void hybrid_ensure_z(HybridP& hp, cudaStream_t s) {
   if (!hp.on || hp.Z.p) return;
   require(hp.Agg.nrows == hp.nG && hp.Wg.nrows == hp.nG, "dense block data missing");
   hp.Z.alloc(hp.nG * hp.nc, s);
   hp.Z.zero();
   k_rows_dense<<<grid_for(hp.nG, 128), 128, 0, s>>>(hp.Wg.ptr.p, hp.Wg.idx.p, hp.Wg.val.p, hp.nG, hp.nc, hp.Z.p);
   HC_CHECK_LAUNCH();
-  giant_factor_solve(h, hp.Agg, hp.Z.p, hp.nc, s, nullptr, nullptr, true);
+  giant_factor_solve(hp.Agg, hp.Z.p, hp.nc, s, nullptr, nullptr, true);
   hybrid_prepare(hp, s);
 }
 
@@ -1276,8 +1222,7 @@ void dense_to_csr(int64_t nc, const DBuf<double>& Ad, DCsr& Ac, cudaStream_t s) 
 }
 }  // namespace
 
-void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr& Pst, const HybridP& hp, DCsr& Ac,
-                     cudaStream_t s) {
+void galerkin_hybrid(const DCsr& A, const DCsr& Ps, const DCsr& Pst, const HybridP& hp, DCsr& Ac, cudaStream_t s) {
   const int64_t nG = hp.nG, nc = hp.nc, n = A.nrows;
   // W' = A[G, :] P_s ; A_GG
   DBuf<int32_t> gmap(n, s);
@@ -1314,20 +1259,8 @@ void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr
   // 2.3e14 flops in well under a second instead of ~7 s of DGEMM.
   // HCAMG_GALERKIN_E=fp64 keeps the fp64 product (validation).
   DBuf<double> E(nc * nc, s);
-  cb(cublasSetStream(h, s), "setStream");
-  if (opts().galerkin_fp64) {
-    DBuf<double> rho(nG * nc, s);
-    k_spmm_rows<<<(unsigned)std::min<int64_t>(nG, kSMs * 16), 256, 0, s>>>(Agg.ptr.p, Agg.idx.p, Agg.val.p, nG, nc,
-                                                                           hp.Z.p, rho.p);
-    k_add_csr_dense<<<grid_for(nG, 256), 256, 0, s>>>(Wp.ptr.p, Wp.idx.p, Wp.val.p, nG, nc, rho.p);
-    HC_CHECK_LAUNCH();
-    const double one = 1.0, zero = 0.0;
-    cb(cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)nc, (int)nc, (int)nG, &one, hp.Z.p, (int)nc, rho.p, (int)nc,
-                   &zero, E.p, (int)nc),
-       "dgemm Z^T rho");
-  } else {
-    DBuf<float> Z32(nG * nc, s), rho32(nG * nc, s);
-    k_to_f32<<<grid_for(nG * nc, 256, kSMs * 16), 256, 0, s>>>(hp.Z.p, nG * nc, Z32.p);
+  {
+    // rho in row blocks of at most 512 MB, E += Z_blk^T rho_blk (own FP64 GEMM)
     const int64_t rb = std::max<int64_t>(1, std::min<int64_t>(nG, (int64_t)(512ll << 20) / (8 * std::max<int64_t>(nc, 1))));
     DBuf<double> blk(rb * nc, s);
     for (int64_t q0 = 0; q0 < nG; q0 += rb) {
@@ -1335,18 +1268,12 @@ void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr
       k_spmm_rows<<<(unsigned)std::min<int64_t>(nr, kSMs * 16), 256, 0, s>>>(Agg.ptr.p + q0, Agg.idx.p, Agg.val.p, nr,
                                                                              nc, hp.Z.p, blk.p);
       k_add_csr_dense<<<grid_for(nr, 256), 256, 0, s>>>(Wp.ptr.p + q0, Wp.idx.p, Wp.val.p, nr, nc, blk.p);
-      k_to_f32<<<grid_for(nr * nc, 256, kSMs * 16), 256, 0, s>>>(blk.p, nr * nc, rho32.p + q0 * nc);
       HC_CHECK_LAUNCH();
+      // column-major nc x nc: E = sum over rows q of Z[q, :]^T rho[q, :]; the row-major
+      // nr x nc blocks are column-major nc x nr views
+      dblas::gemm(dblas::N, dblas::T, nc, nc, nr, 1.0, hp.Z.p + q0 * nc, nc, blk.p, nc, q0 == 0 ? 0.0 : 1.0, E.p, nc,
+                  s);
     }
-    blk.release();
-    DBuf<float> E32(nc * nc, s);
-    const float one = 1.0f, zero = 0.0f;
-    cb(cublasGemmEx(h, CUBLAS_OP_N, CUBLAS_OP_T, (int)nc, (int)nc, (int)nG, &one, Z32.p, CUDA_R_32F, (int)nc, rho32.p,
-                    CUDA_R_32F, (int)nc, &zero, E32.p, CUDA_R_32F, (int)nc, CUBLAS_COMPUTE_32F_FAST_TF32,
-                    CUBLAS_GEMM_DEFAULT),
-       "gemmEx tf32 Z^T rho");
-    k_to_f64<<<grid_for(nc * nc, 256, kSMs * 16), 256, 0, s>>>(E32.p, nc * nc, E.p);
-    HC_CHECK_LAUNCH();
   }
   // D1 = Z^T W'
   DBuf<double> D1(nc * nc, s);

@@ -4,7 +4,6 @@
 // is applied in hybrid form (sparse part + dense block) and the Galerkin
 // product uses the Schur form with the solve residual (see giant.cu).
 #pragma once
-#include <cublas_v2.h>
 
 #include "common.cuh"
 #include "dist.cuh"
@@ -23,8 +22,8 @@ namespace hcamg {
 // Y = L^{-1} B (the forward half of the solve, staircase-restricted: column c
 // of Y is zero above the first row of its right-hand side), and, unless
 // want_z, the backward solve is skipped and B is left as it was.
-void giant_factor_solve(cublasHandle_t h, const DCsr& Agg, double* B_rowmajor, int64_t m, cudaStream_t s,
-                        FactorP* fac = nullptr, double* D = nullptr, bool want_z = true);
+void giant_factor_solve(const DCsr& Agg, double* B_rowmajor, int64_t m, cudaStream_t s, FactorP* fac = nullptr,
+                        double* D = nullptr, bool want_z = true);
 
 // Reverse Cuthill-McKee order of a symmetric CSR pattern (scipy's
 // csgraph.reverse_cuthill_mckee, which the reference's cholesky() applies,
@@ -51,7 +50,7 @@ struct HybridP {
 void hybrid_prepare(HybridP& hp, cudaStream_t s);
 // Form the explicit block Z = A_GG^{-1} W' if the setup did not keep it
 // (one more factorisation and a full two-sided solve, ~4 s on config 2).
-void hybrid_ensure_z(cublasHandle_t h, HybridP& hp, cudaStream_t s);
+void hybrid_ensure_z(HybridP& hp, cudaStream_t s);
 // The three products below take an optional distributed context `d` (rows
 // split across ranks, results exchanged through exchange site `off`, see
 // dist.cuh) and `part`: 0 = all, 1 = up to the exchange signal (producer),
@@ -71,10 +70,9 @@ void hybrid_restrict(const int* stop, HybridP& hp, const double* r, double* bc, 
 //   with hp.D (default): A_c = sym(P_s^T A P_s) - Y^T Y, Y = L^{-1} W' (L the
 //     envelope Cholesky factor of A_GG; W'^T A_GG^{-1} W' = Y^T Y exactly);
 //   with Z: A_c = sym(P_s^T A P_s) - sym(W'^T Z) - sym(Z^T rho), rho = W' - A_GG Z
-//     (the residual term in fp64, or TF32 with option galerkin_fp64 = 0).
+//     (the residual term Z^T rho in fp64).
 // Output canonical CSR (exact zeros dropped).
-void galerkin_hybrid(cublasHandle_t h, const DCsr& A, const DCsr& Ps, const DCsr& Pst, const HybridP& hp,
-                     DCsr& Ac, cudaStream_t s);
+void galerkin_hybrid(const DCsr& A, const DCsr& Ps, const DCsr& Pst, const HybridP& hp, DCsr& Ac, cudaStream_t s);
 
 // nnz of the materialised P (exact zeros of Z excluded)
 int64_t hybrid_nnz(const DCsr& Ps, const HybridP& hp, cudaStream_t s);

@@ -271,8 +271,7 @@ int64_t connected_components(const DCsr& M, DBuf<int32_t>& label, cudaStream_t s
   return nc;
 }
 
-void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode, cublasHandle_t h,
-                  InterpResult& out, cudaStream_t s) {
+void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode, InterpResult& out, cudaStream_t s) {
   const int64_t n = A.nrows, npair = sp.n_pairs(), ni = (int64_t)sp.interior.size();
   StageTimer st(s);
   DBuf<int64_t> pairs(7 * std::max<int64_t>(npair, 1), s), interior(std::max<int64_t>(ni, 1), s);
@@ -413,12 +412,12 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
     for (int64_t c : large_comp) {
       if (c > fail_comp) break;
       const int64_t k = hc[(size_t)c + 1] - hc[(size_t)c], nk = hk[(size_t)c + 1] - hk[(size_t)c];
-      int64_t bad = dense_cholesky(h, Ad.p + a_off[(size_t)c], k, k, s);
+      int64_t bad = dense_cholesky(Ad.p + a_off[(size_t)c], k, k, s);
       if (bad >= 0) {
         if (c < fail_comp) { fail_comp = c; fail_piv = bad; }
         break;
       }
-      dense_cholesky_solve(h, Ad.p + a_off[(size_t)c], k, k, Bd.p + b_off[(size_t)c], nk, k, s);
+      dense_cholesky_solve(Ad.p + a_off[(size_t)c], k, k, Bd.p + b_off[(size_t)c], nk, k, s);
     }
     if (giant >= 0 && giant < fail_comp) {
       // dense-regime component: packed tiled Cholesky, Z kept dense (row-major nG x n_c)
@@ -448,7 +447,7 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
         const bool fac = factorp_enabled();
         const bool want_z = !fac || opts().form_z;
         hp.D.alloc(npair * npair, s);
-        giant_factor_solve(h, hp.Agg, hp.Z.p, npair, s, fac ? &hp.fac : nullptr, hp.D.p, want_z);
+        giant_factor_solve(hp.Agg, hp.Z.p, npair, s, fac ? &hp.fac : nullptr, hp.D.p, want_z);
         if (!want_z) hp.Z.release();
         if (hp.fac.T) factorp_attach(hp.fac, W, mpos.p, hp.rows.p, s);
       } catch (const Error& e) {

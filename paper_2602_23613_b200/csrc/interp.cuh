@@ -1,6 +1,5 @@
 // Sparse approximate ideal interpolation and coarse gradient on the GPU.
 #pragma once
-#include <cublas_v2.h>
 
 #include "giant.cuh"
 #include "split.cuh"
@@ -21,8 +20,7 @@ struct InterpResult {
 
 // transfer.py:77-122 (+ coarse_gradient 55-74).  mode: 0 = refinement, 1 = algebraic.
 // Throws Error(ENOTSPD_, ..., pivot) on a breakdown in a component solve.
-void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode, cublasHandle_t h,
-                  InterpResult& out, cudaStream_t s);
+void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode, InterpResult& out, cudaStream_t s);
 
 // Connected components of the graph of M (square, symmetric pattern):
 // label[v] = component index, components numbered by their smallest vertex.

@@ -28,7 +28,6 @@ Options options_from_env() {
   o.giant_min = env_i("HCAMG_GIANT_MIN", o.giant_min);
   o.coarse_gemv_min = env_i("HCAMG_COARSE_GEMV_MIN", o.coarse_gemv_min);
   o.coarse_symv = (int)env_i("HCAMG_COARSE_SYMV", o.coarse_symv);
-  if (const char* e = getenv("HCAMG_GALERKIN_E")) o.galerkin_fp64 = std::string(e) == "fp64";
   if (const char* e = getenv("HCAMG_PAPPLY")) o.factor_apply = std::string(e) != "z";
   o.form_z = (int)env_i("HCAMG_FORM_Z", o.form_z);
   o.tri_calib = (int)env_i("HCAMG_TRI_CALIB", o.tri_calib);

@@ -25,12 +25,14 @@ pytestmark = pytest.mark.gpu
 
 DENSE = {"giant_min": 200, "coarse_gemv_min": 0, "coarse_symv": 1}
 VARIANTS = {
-    # dense regime as on c2: factor sweeps (TMA kernel), fp64 Galerkin, packed-triangle coarsest solve
-    "dense": dict(DENSE, galerkin_fp64=1),
-    # the same with the TF32 tensor-core Galerkin correction term
-    "dense_tf32": dict(DENSE, galerkin_fp64=0),
-    # dense regime with the explicit Z block (row GEMV / chunked column sums)
-    "dense_z": dict(DENSE, galerkin_fp64=1, factor_apply=0, coarse_symv=0),
+    # dense regime as on c2: factor sweeps (TMA kernel), Galerkin as sym(Ps^T A Ps) - Y^T Y,
+    # packed-triangle coarsest solve
+    "dense": dict(DENSE),
+    # the same with the explicit Z formed as well (the export / multi-GPU representation)
+    "dense_formz": dict(DENSE, form_z=1),
+    # dense regime with the explicit Z block applied (row GEMV / chunked column sums) and the
+    # Schur-form Galerkin with the fp64 Z^T rho term
+    "dense_z": dict(DENSE, factor_apply=0, coarse_symv=0),
 }
 SWEEPS = ["grid", "wave", "leg", "flow"]
 
