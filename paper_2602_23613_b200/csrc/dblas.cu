@@ -18,7 +18,14 @@ namespace dblas {
 
 namespace {
 
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 3, THREADS = 256;
+#ifndef DBLAS_BN
+#define DBLAS_BN 64
+#endif
+#ifndef DBLAS_STAGES
+#define DBLAS_STAGES 3
+#endif
+constexpr int BM = 128, BN = DBLAS_BN, BK = 16, STAGES = DBLAS_STAGES, THREADS = 256;
+constexpr int WNF = BN / 16;  // n fragments per warp (warps: 4 along m x 2 along n)
 constexpr int LDA_S = BM + 4, LDB_S = BN + 4;
 constexpr int STAGE_DOUBLES = BK * LDA_S + BK * LDB_S;
 constexpr size_t SMEM = sizeof(double) * STAGES * STAGE_DOUBLES;
@@ -94,11 +101,11 @@ __global__ void __launch_bounds__(THREADS) k_dgemm(GemmArgs g) {
     }
   };
 
-  double acc[4][4][2];
+  double acc[4][WNF][2];
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    for (int ni = 0; ni < WNF; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
@@ -115,26 +122,26 @@ __global__ void __launch_bounds__(THREADS) k_dgemm(GemmArgs g) {
 #pragma unroll
     for (int k4 = 0; k4 < BK / 4; ++k4) {
       const int kr = k4 * 4 + (lane & 3);
-      double a[4], b[4];
+      double a[4], b[WNF];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) a[mi] = As[kr * LDA_S + wm * 32 + mi * 8 + (lane >> 2)];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[kr * LDB_S + wn * 32 + ni * 8 + (lane >> 2)];
+      for (int ni = 0; ni < WNF; ++ni) b[ni] = Bs[kr * LDB_S + wn * (BN / 2) + ni * 8 + (lane >> 2)];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+        for (int ni = 0; ni < WNF; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
     }
   }
   cp_wait<0>();
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
+    for (int ni = 0; ni < WNF; ++ni)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int64_t i = m0 + wm * 32 + mi * 8 + (lane >> 2);
-        const int64_t j = n0 + wn * 32 + ni * 8 + 2 * (lane & 3) + h;
+        const int64_t j = n0 + wn * (BN / 2) + ni * 8 + 2 * (lane & 3) + h;
         if (i >= g.m || j >= g.n || (g.lower && i < j)) continue;
         double* c = C + i + j * g.ldc;
         const double v = g.alpha * acc[mi][ni][h];
@@ -322,15 +329,10 @@ void trsm(Side side, Op op, int64_t m, int64_t n, const double* L, int64_t ldl, 
   }
 }
 
-void trsm_rlt_batched(int64_t m, int64_t nb, const double* const* L, int64_t ldl, double* const* B, int64_t ldb,
-                      int64_t batch, cudaStream_t s) {
-  // X_i = B_i L_i^{-T}: the inverses (distinct tiles only), then one batched GEMM into temporaries
+void trsm_rlt_batched(int64_t m, int64_t nb, const std::vector<const double*>& hl, int64_t ldl,
+                      const std::vector<double*>& hb, int64_t ldb, cudaStream_t s) {
+  const int64_t batch = (int64_t)hb.size();
   if (batch <= 0) return;
-  std::vector<const double*> hl((size_t)batch);
-  std::vector<double*> hb((size_t)batch);
-  HC_CUDA(cudaMemcpyAsync(hl.data(), L, sizeof(void*) * batch, cudaMemcpyDeviceToHost, s));
-  HC_CUDA(cudaMemcpyAsync(hb.data(), B, sizeof(void*) * batch, cudaMemcpyDeviceToHost, s));
-  HC_CUDA(cudaStreamSynchronize(s));
   std::vector<const double*> uniq;
   std::vector<int64_t> which((size_t)batch);
   for (int64_t b = 0; b < batch; ++b) {
@@ -354,7 +356,6 @@ void trsm_rlt_batched(int64_t m, int64_t nb, const double* const* L, int64_t ldl
   dc.upload(pc.data(), batch, s);
   gemm_batched(N, T, m, nb, nb, 1.0, da.p, ldb, db.p, nb, 0.0, dc.p, m, batch, s);
   for (int64_t b = 0; b < batch; ++b) copy2d(m, nb, X.p + b * m * nb, m, hb[(size_t)b], ldb, s);
-  HC_CUDA(cudaStreamSynchronize(s));  // host pointer vectors go out of scope
 }
 
 }  // namespace dblas

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace hcamg {
 namespace dblas {
@@ -37,9 +38,11 @@ void gemm_tri_lower_tn(int64_t n, const double* Y, int64_t ldy, double* C, int64
 // explicit inverses; everything else is GEMM.
 void trsm(Side side, Op op, int64_t m, int64_t n, const double* L, int64_t ldl, double* B, int64_t ldb,
           cudaStream_t s);
-// Batched right-side solve X L^T = B for `batch` pairs of nb x nb tiles (m rows of B).
-void trsm_rlt_batched(int64_t m, int64_t nb, const double* const* L, int64_t ldl, double* const* B, int64_t ldb,
-                      int64_t batch, cudaStream_t s);
+// Batched right-side solve X L^T = B for pairs (L[i], B[i]) of nb x nb tiles
+// (m rows of B), host pointer lists: the distinct L are inverted once, then one
+// batched GEMM.
+void trsm_rlt_batched(int64_t m, int64_t nb, const std::vector<const double*>& L, int64_t ldl,
+                      const std::vector<double*>& B, int64_t ldb, cudaStream_t s);
 // Li = L^{-1} for a lower-triangular n x n L (Li lower, ld ldi; the strict upper part is zeroed).
 void trtri_lower(int64_t n, const double* L, int64_t ldl, double* Li, int64_t ldi, cudaStream_t s);
 // Batched inverses of `batch` nb x nb lower-triangular tiles.

@@ -89,10 +89,14 @@ constexpr int kTile = 96;
 constexpr int kTileThreads = 256;
 
 // Unblocked Cholesky of one nb x nb diagonal tile in shared memory.
+// `bad` holds the first failing pivot index (-1: none so far); a tile after a
+// failure returns at once, so a whole factorisation runs without host syncs.
 __global__ void __launch_bounds__(kTileThreads) k_potrf_tile(double* __restrict__ A, int64_t ld, int nb,
-                                                             double* __restrict__ piv, int* __restrict__ bad) {
+                                                             double* __restrict__ piv, long long* __restrict__ bad,
+                                                             long long base) {
   extern __shared__ double T[];  // nb x (nb+1), row-major T[i*(nb+1)+j]
   const int ldt = nb + 1;
+  if (*(volatile long long*)bad >= 0) return;
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
     int i = e % nb, j = e / nb;
     if (i >= j) T[i * ldt + j] = A[i + (int64_t)j * ld];
@@ -105,7 +109,7 @@ __global__ void __launch_bounds__(kTileThreads) k_potrf_tile(double* __restrict_
     double d = T[j * ldt + j];
     if (threadIdx.x == 0) {
       piv[j] = d;
-      if (!(d > 0.0) || !isfinite(d)) { stop = 1; *bad = j; }
+      if (!(d > 0.0) || !isfinite(d)) { stop = 1; *bad = base + j; }
     }
     __syncthreads();
     if (stop) return;
@@ -151,29 +155,46 @@ void batched_small_spd_inverse(const DenseJob* d_jobs, int64_t njobs, double* A,
   HC_CHECK_LAUNCH();
 }
 
+namespace {
+// Recursive right-looking Cholesky: L11 = chol(A11); A21 := A21 L11^{-T};
+// A22 -= A21 A21^T; L22 = chol(A22) -- leaves of <= kTile on one CTA, the
+// updates on the own FP64 kernels (the trailing matrix is touched O(log n)
+// times instead of once per 96-column panel)
+void chol_rec(double* A, int64_t k, int64_t ld, double* piv, long long* bad, int64_t base, cudaStream_t s) {
+  if (k <= kTile) {
+    const size_t smem = sizeof(double) * kTile * (kTile + 1);
+    static bool init = false;
+    if (!init) {
+      HC_CUDA(cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      init = true;
+    }
+    k_potrf_tile<<<1, kTileThreads, smem, s>>>(A, ld, (int)k, piv, bad, (long long)base);
+    HC_CHECK_LAUNCH();
+    count_flops((double)k * k * k / 3.0);
+    return;
+  }
+  const int64_t k1 = std::min<int64_t>(k - 1, std::max<int64_t>(kTile, (k / 2 + kTile - 1) / kTile * kTile)), k2 = k - k1;
+  double* A21 = A + k1;
+  double* A22 = A + k1 + k1 * ld;
+  chol_rec(A, k1, ld, piv, bad, base, s);
+  dblas::trsm(dblas::Right, dblas::T, k2, k1, A, ld, A21, ld, s);
+  dblas::syrk_ln(k2, k1, -1.0, A21, ld, 1.0, A22, ld, s);
+  chol_rec(A22, k2, ld, piv + k1, bad, base + k1, s);
+}
+}  // namespace
+
+void dense_cholesky_async(double* A, int64_t k, int64_t ld, double* piv, long long* bad, int64_t base,
+                          cudaStream_t s) {
+  if (k > 0) chol_rec(A, k, ld, piv, bad, base, s);
+}
+
 int64_t dense_cholesky_raw(double* A, int64_t k, int64_t ld, double* piv, cudaStream_t s) {
   if (k == 0) return 0;
-  DBuf<int> bad(1, s);
+  DBuf<long long> bad(1, s);
   bad.fill_bytes(0xff);
-  const size_t smem = sizeof(double) * kTile * (kTile + 1);
-  HC_CUDA(cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  for (int64_t kb = 0; kb < k; kb += kTile) {
-    const int nb = (int)std::min<int64_t>(kTile, k - kb);
-    double* Akk = A + kb + kb * ld;
-    k_potrf_tile<<<1, kTileThreads, smem, s>>>(Akk, ld, nb, piv + kb, bad.p);
-    count_flops((double)nb * nb * nb / 3.0);
-    HC_CHECK_LAUNCH();
-    int b = read_scalar(bad.p, s);
-    if (b >= 0) return kb + b;
-    const int64_t rest = k - kb - nb;
-    if (rest > 0) {
-      double* A21 = Akk + nb;
-      double* A22 = A21 + nb * ld;
-      dblas::trsm(dblas::Right, dblas::T, rest, nb, Akk, ld, A21, ld, s);  // A21 L11^{-T}
-      dblas::syrk_ln(rest, nb, -1.0, A21, ld, 1.0, A22, ld, s);           // A22 -= A21 A21^T
-    }
-  }
-  return k;
+  chol_rec(A, k, ld, piv, bad.p, 0, s);
+  const long long b = read_scalar(bad.p, s);
+  return b >= 0 ? (int64_t)b : k;
 }
 
 int64_t pivot_verdict(const std::vector<double>& hp, int64_t k, int64_t j0, double scale) {

@@ -35,8 +35,12 @@ void batched_small_spd_inverse(const DenseJob* d_jobs, int64_t njobs, double* A,
 int64_t dense_cholesky(double* A, int64_t k, int64_t ld, cudaStream_t s);
 
 // Factor in place and write the pivots; returns the index of the first
-// non-positive / non-finite pivot, or k.  No verdict.
+// non-positive / non-finite pivot, or k.  No verdict.  One host sync at the end.
 int64_t dense_cholesky_raw(double* A, int64_t k, int64_t ld, double* piv, cudaStream_t s);
+// The same without any host sync: *bad (device, -1 initially) receives base +
+// the first failing pivot; later calls sharing `bad` become no-ops.
+void dense_cholesky_async(double* A, int64_t k, int64_t ld, double* piv, long long* bad, int64_t base,
+                          cudaStream_t s);
 // Reference breakdown verdict from the pivots (-1: fine).
 int64_t pivot_verdict(const std::vector<double>& hp, int64_t k, int64_t j0, double scale);
 

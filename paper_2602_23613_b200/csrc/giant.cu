@@ -542,11 +542,6 @@ __global__ void __launch_bounds__(256) k_blocks_transpose(const double* const* _
   for (int j = threadIdx.y; j < 32; j += 8) D[(by + threadIdx.x) + (bx + j) * kSB] = sm[threadIdx.x][j];
 }
 
-__global__ void k_blocks_eye(double* const* __restrict__ dst) {
-  double* D = dst[blockIdx.y];
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < kSB * kSB; t += (int64_t)gridDim.x * blockDim.x)
-    D[t] = t % (kSB + 1) == 0 ? 1.0 : 0.0;
-}
 
 // Per row of each source block (SB rows of SB doubles at p + r ld): the
 // 64-column chunk range [j0, j1) holding its nonzeros (0, 0 when empty).
@@ -947,23 +942,19 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
   DBuf<double> piv(T * kNB, s);
   DBuf<const double*> dA, dB;
   DBuf<const double*> dC;
-  int64_t fail = -1;
-  for (int64_t K = 0; K < T; ++K) {  // right-looking, inside the envelope
-    const int64_t j0 = dense_cholesky_raw(L.tile(K, K), kNB, kNB, piv.p + K * kNB, s);
-    if (j0 < kNB) {
-      fail = K * kNB + j0;
-      break;
-    }
+  DBuf<long long> badf(1, s);
+  badf.fill_bytes(0xff);
+  for (int64_t K = 0; K < T; ++K) {  // right-looking, inside the envelope; no host sync until the end
+    dense_cholesky_async(L.tile(K, K), kNB, kNB, piv.p + K * kNB, badf.p, K * kNB, s);
     std::vector<int64_t> below;  // block rows I > K whose envelope reaches column K
     for (int64_t I = K + 1; I < T; ++I)
       if (L.has(I, K)) below.push_back(I);
     if (below.empty()) continue;
     {
-      std::vector<const double*> ha(below.size(), L.tile(K, K)), hb;
+      std::vector<const double*> ha(below.size(), L.tile(K, K));
+      std::vector<double*> hb;
       for (int64_t I : below) hb.push_back(L.tile(I, K));
-      const double** pa = upload_ptrs(ha, dA, s);
-      const double** pb = upload_ptrs(hb, dB, s);
-      dblas::trsm_rlt_batched(kNB, kNB, pa, kNB, (double* const*)pb, kNB, (int64_t)below.size(), s);
+      dblas::trsm_rlt_batched(kNB, kNB, ha, kNB, hb, kNB, s);
     }
     {
       std::vector<const double*> ha, hb, hc;
@@ -978,9 +969,11 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
       const double** pc = upload_ptrs(hc, dC, s);
       dblas::gemm_batched(dblas::N, dblas::T, kNB, kNB, kNB, -1.0, pa, kNB, pb, kNB, 1.0, (double* const*)pc, kNB,
                           (int64_t)ha.size(), s);
-      HC_CUDA(cudaStreamSynchronize(s));  // host pointer vectors go out of scope
+      // (pageable-host uploads are staged before cudaMemcpyAsync returns: no sync needed)
     }
   }
+  const long long badv = read_scalar(badf.p, s);
+  const int64_t fail = badv >= 0 ? (int64_t)badv : -1;
   {
     // pivot indices are reported in the factored (permuted) order, as the
     // reference's cholesky() does for its RCM-permuted matrix

@@ -80,6 +80,45 @@ int main() {
              2.0 * n * n * n / (ms2 * 1e-3) / 1e12);
     }
   }
+  // setup shapes: forward-solve GEMM (m x 1024 x 1024, NT) and the staircase SYRK (n x n, k 1024)
+  {
+    const int64_t m = 26236, kk = 1024;
+    DBuf<double> A(m * kk, s), B(kk * kk, s), C(m * m, s);
+    std::vector<double> h1(m * kk);
+    for (auto& v : h1) v = U(rng);
+    HC_CUDA(cudaMemcpy(A.p, h1.data(), 8 * m * kk, cudaMemcpyHostToDevice));
+    HC_CUDA(cudaMemcpy(B.p, h1.data(), 8 * kk * kk, cudaMemcpyHostToDevice));
+    const double one = 1.0, mone = -1.0;
+    float ms, ms2;
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0, s);
+      dblas::gemm(dblas::N, dblas::T, m, kk, kk, -1.0, A.p, m, B.p, kk, 1.0, C.p, m, s);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      cudaEventRecord(e0, s);
+      cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, m, kk, kk, &mone, A.p, m, B.p, kk, &one, C.p, m);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms2, e0, e1);
+    }
+    printf("gemm %lldx1024x1024 NT: own %.1f TF/s, cuBLAS %.1f TF/s\n", (long long)m, 2.0 * m * kk * kk / (ms * 1e-3) / 1e12,
+           2.0 * m * kk * kk / (ms2 * 1e-3) / 1e12);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(e0, s);
+      dblas::syrk_ln(m, kk, 1.0, A.p, m, 1.0, C.p, m, s);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      cudaEventRecord(e0, s);
+      cublasDsyrk(h, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, m, kk, &one, A.p, m, &one, C.p, m);
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms2, e0, e1);
+    }
+    printf("syrk %lld k 1024: own %.1f TF/s, cuBLAS %.1f TF/s\n", (long long)m, 1.0 * m * m * kk / (ms * 1e-3) / 1e12,
+           1.0 * m * m * kk / (ms2 * 1e-3) / 1e12);
+  }
   // TRSM variants vs cuBLAS (well-conditioned L)
   for (int side = 0; side < 2; ++side)
     for (int op = 0; op < 2; ++op) {
