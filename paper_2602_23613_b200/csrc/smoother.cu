@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <thread>
 
 #include "dense.cuh"
 #include "smoother.cuh"
@@ -507,10 +508,12 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
   }
   const std::vector<int64_t> boff = sm.binv_off.download();
   const std::vector<double> binv = sm.binv.download();
-  int64_t recmax = 0;
   std::vector<std::vector<unsigned char>> recs(2);
   std::vector<std::vector<int64_t>> offs(2);
-  for (int dir = 0; dir < 2; ++dir) {
+  int64_t rmax[2] = {0, 0};
+  bool okdir[2] = {true, true};
+  // the two directions are independent: built on two host threads
+  auto build_dir = [&](int dir) {
     // execution order: waves ascending (forward) / descending (backward), patches ascending within a wave
     std::vector<int64_t> order;
     order.reserve((size_t)m);
@@ -567,7 +570,10 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
               xp = (int32_t)(t - (size_t)tstart.back());
               break;
             }
-          if (xp > 31) return;  // beyond the unrolled term window of the kernel: flow leg not applicable
+          if (xp > 31) {  // beyond the unrolled term window of the kernel: flow leg not applicable
+            okdir[dir] = false;
+            return;
+          }
         }
         xpart.push_back(xp);
         tstart.push_back((int32_t)ts.size());
@@ -599,10 +605,15 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
         memcpy(r + o_slot, ts.data(), 4 * (size_t)nt);
         memcpy(r + o_val, tv.data(), 8 * (size_t)nt);
       }
-      recmax = std::max(recmax, bytes);
+      rmax[dir] = std::max(rmax[dir], bytes);
       off.push_back((int64_t)R.size());
     }
-  }
+  };
+  std::thread th(build_dir, 1);
+  build_dir(0);
+  th.join();
+  if (!okdir[0] || !okdir[1]) return;
+  const int64_t recmax = std::max(rmax[0], rmax[1]);
   if (flow_smem_bytes(recmax) > 200 * 1024) return;  // a patch record too large to double-buffer per warp
   for (int dir = 0; dir < 2; ++dir) {
     f.recs[dir].upload(recs[(size_t)dir].data(), (int64_t)recs[(size_t)dir].size(), s);
