@@ -48,6 +48,10 @@ __device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(ok ? 8 : 0) : "memory");
 }
+__device__ __forceinline__ void cp16(double* dst, const double* src, int bytes) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int kN>
 __device__ __forceinline__ void cp_wait() {
@@ -73,31 +77,57 @@ __global__ void __launch_bounds__(THREADS) k_dgemm(GemmArgs g) {
   const int64_t kbeg = g.kfromrow ? (m0 / BK) * BK : 0;
   const int64_t ktiles = g.k > kbeg ? (g.k - kbeg + BK - 1) / BK : 0;
 
+  // 16-byte copies along the contiguous global dimension when it is also the
+  // contiguous shared dimension (op(A) = A, op(B) = B^T) and alignment allows
+  const bool va = TA == 0 && ((reinterpret_cast<uintptr_t>(A) | (uintptr_t)(g.lda * 8)) & 15) == 0;
+  const bool vb = TB == 1 && ((reinterpret_cast<uintptr_t>(B) | (uintptr_t)(g.ldb * 8)) & 15) == 0;
   auto load = [&](int64_t kt, int st) {
     double* As = smem + (size_t)st * STAGE_DOUBLES;
     double* Bs = As + BK * LDA_S;
     const int64_t k0 = kbeg + kt * BK;
+    if (va) {
 #pragma unroll
-    for (int r = 0; r < (BM * BK) / THREADS; ++r) {
-      const int idx = t + THREADS * r;
-      int il, kl;
-      if (TA == 0) { il = idx % BM; kl = idx / BM; }
-      else { kl = idx % BK; il = idx / BK; }
-      const int64_t i = m0 + il, kk = k0 + kl;
-      const bool ok = i < g.m && kk < g.k;
-      const double* src = ok ? (TA == 0 ? A + i + kk * g.lda : A + kk + i * g.lda) : A;
-      cp8(As + kl * LDA_S + il, src, ok);
+      for (int r = 0; r < (BM * BK) / (2 * THREADS); ++r) {
+        const int idx = t + THREADS * r;
+        const int il = 2 * (idx % (BM / 2)), kl = idx / (BM / 2);
+        const int64_t i = m0 + il, kk = k0 + kl;
+        const int bytes = kk < g.k ? (int)(8 * (g.m - i >= 2 ? 2 : (g.m - i > 0 ? g.m - i : 0))) : 0;
+        cp16(As + kl * LDA_S + il, bytes ? A + i + kk * g.lda : A, bytes);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < (BM * BK) / THREADS; ++r) {
+        const int idx = t + THREADS * r;
+        int il, kl;
+        if (TA == 0) { il = idx % BM; kl = idx / BM; }
+        else { kl = idx % BK; il = idx / BK; }
+        const int64_t i = m0 + il, kk = k0 + kl;
+        const bool ok = i < g.m && kk < g.k;
+        const double* src = ok ? (TA == 0 ? A + i + kk * g.lda : A + kk + i * g.lda) : A;
+        cp8(As + kl * LDA_S + il, src, ok);
+      }
     }
+    if (vb) {
 #pragma unroll
-    for (int r = 0; r < (BN * BK) / THREADS; ++r) {
-      const int idx = t + THREADS * r;
-      int jl, kl;
-      if (TB == 0) { kl = idx % BK; jl = idx / BK; }
-      else { jl = idx % BN; kl = idx / BN; }
-      const int64_t j = n0 + jl, kk = k0 + kl;
-      const bool ok = j < g.n && kk < g.k;
-      const double* src = ok ? (TB == 0 ? B + kk + j * g.ldb : B + j + kk * g.ldb) : B;
-      cp8(Bs + kl * LDB_S + jl, src, ok);
+      for (int r = 0; r < (BN * BK) / (2 * THREADS); ++r) {
+        const int idx = t + THREADS * r;
+        const int jl = 2 * (idx % (BN / 2)), kl = idx / (BN / 2);
+        const int64_t j = n0 + jl, kk = k0 + kl;
+        const int bytes = kk < g.k ? (int)(8 * (g.n - j >= 2 ? 2 : (g.n - j > 0 ? g.n - j : 0))) : 0;
+        cp16(Bs + kl * LDB_S + jl, bytes ? B + j + kk * g.ldb : B, bytes);
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < (BN * BK) / THREADS; ++r) {
+        const int idx = t + THREADS * r;
+        int jl, kl;
+        if (TB == 0) { kl = idx % BK; jl = idx / BK; }
+        else { jl = idx % BN; kl = idx / BN; }
+        const int64_t j = n0 + jl, kk = k0 + kl;
+        const bool ok = j < g.n && kk < g.k;
+        const double* src = ok ? (TB == 0 ? B + kk + j * g.ldb : B + j + kk * g.ldb) : B;
+        cp8(Bs + kl * LDB_S + jl, src, ok);
+      }
     }
   };
 

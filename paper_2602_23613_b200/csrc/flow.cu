@@ -21,14 +21,10 @@
 //     globally first unfinished patch is always runnable (no deadlock in a
 //     co-resident cooperative grid).
 //
-// Around the sweep the leg does the l1-Jacobi step and the bookkeeping in
-// grid-wide phases separated by a sense-reversing barrier:
-//   down: sweep from r0 = b (x0 = 0) | x = delta, r1 = b - A delta, dj = r1 / l1,
-//         x += dj | r = r1 - A dj, slots reset
-//   up:   r = b - A x, dj = r / l1 | r0 = r - A dj, x += dj | sweep (reverse
-//         wave order) | x += delta, slots reset
-// where delta[u] is the sum of u's entry slots (a DoF sits in <= 2 vertex
-// patches).
+// The kernel is the sweep alone (the last of a DoF's <= 2 patches writes x);
+// the l1-Jacobi step around it runs on the fused SpMV kernels (solve.cu:
+// r = b - A x, dj = r / l1, then r -= A dj, x += dj) -- after the sweep in
+// the down leg, before it in the up leg.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -237,30 +233,11 @@ template <bool kDown>
 __global__ void __launch_bounds__(kFlowThreads, 1) k_flow_leg(FlowArgs a) {
   if (*a.stop) return;
   GridBar gb{a.bar};
-  const int64_t n = a.n;
   const int64_t nth = (int64_t)gridDim.x * blockDim.x;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const int64_t wg = gtid >> 5, nw = nth >> 5;
-  if (!kDown) {
-    // r = b - A x ; dj = r / l1   (smoothers.py:106-109, before the reverse sweep)
-    for (int64_t u = gtid; u < n; u += nth) {
-      double s = 0.0;
-      for (int64_t e = a.ap[u]; e < a.ap[u + 1]; ++e) s = fma(a.av[e], a.x[a.ai[e]], s);
-      const double r = a.b[u] - s;
-      a.r[u] = r;
-      a.dj[u] = r / a.l1[u];
-    }
-    gb.sync();
-    for (int64_t u = gtid; u < n; u += nth) {
-      double s = 0.0;
-      for (int64_t e = a.ap[u]; e < a.ap[u + 1]; ++e) s = fma(a.av[e], a.dj[a.ai[e]], s);
-      a.r1[u] = a.r[u] - s;
-      a.x[u] += a.dj[u];
-    }
-    gb.sync();
-  }
-  const double* r0 = kDown ? a.b : a.r1;
+  const double* r0 = a.r0;
   {
     // each warp walks its patches (exec positions wg, wg + nw, ...) with the
     // next record streamed into the other half of its double buffer by one
@@ -305,26 +282,7 @@ __global__ void __launch_bounds__(kFlowThreads, 1) k_flow_leg(FlowArgs a) {
       __syncwarp();
     }
   }
-  gb.sync();
-  if (kDown) {
-    // x holds the sweep's result; r1 = b - A x ; dj = r1 / l1 ; x += dj
-    for (int64_t u = gtid; u < n; u += nth) {
-      double s = 0.0;
-      for (int64_t e = a.ap[u]; e < a.ap[u + 1]; ++e) s = fma(a.av[e], a.x[a.ai[e]], s);
-      const double r1 = a.b[u] - s;
-      const double dj = r1 / a.l1[u];
-      a.r1[u] = r1;
-      a.dj[u] = dj;
-    }
-    gb.sync();
-    for (int64_t u = gtid; u < n; u += nth) {
-      double s = 0.0;
-      for (int64_t e = a.ap[u]; e < a.ap[u + 1]; ++e) s = fma(a.av[e], a.dj[a.ai[e]], s);
-      a.r[u] = a.r1[u] - s;
-      a.x[u] += a.dj[u];
-    }
-  }
-  // every slot was read above; hand them back to the sentinel for the next leg
+  gb.sync();  // every slot has been read: hand them back to the sentinel for the next leg
   const double sent = __longlong_as_double((long long)kSentinel);
   for (int64_t e = gtid; e < a.ne; e += nth) a.d[e] = sent;
 }

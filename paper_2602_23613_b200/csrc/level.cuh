@@ -32,7 +32,6 @@ struct FlowProgram {
   DBuf<unsigned char> recs[2];   // per direction: one record per patch, in execution order
   DBuf<int64_t> rec_off[2];
   DBuf<double> d[2];
-  DBuf<int2> ent;
   DBuf<unsigned> bar;
 };
 
@@ -79,6 +78,8 @@ struct Smoother {
 void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s);
 // Waves wider than one 16-CTA cluster (the auto mode runs such levels on the whole GPU).
 bool smoother_wide(const Smoother& sm);
+// Auto mode runs the dataflow leg on this level.
+bool smoother_flow_auto(const Smoother& sm);
 
 void build_program(Smoother& sm, SweepProgram& pg, cudaStream_t s);
 

@@ -469,11 +469,19 @@ void build_smoother(const DCsr& A, const DCsr& G, Smoother& sm, cudaStream_t s) 
     sm.max_gen_rows = std::max(sm.max_gen_rows, sm.gen_fw_ptr[(size_t)w + 1] - sm.gen_fw_ptr[(size_t)w]);
     sm.max_gen_rows = std::max(sm.max_gen_rows, sm.gen_bw_ptr[(size_t)w + 1] - sm.gen_bw_ptr[(size_t)w]);
   }
-  if (smoother_wide(sm) || opts().sweep == SWEEP_FLOW) build_flow(A, sm, s);
+  if (smoother_flow_auto(sm) || opts().sweep == SWEEP_FLOW) build_flow(A, sm, s);
   HC_CUDA(cudaStreamSynchronize(s));
 }
 
 bool smoother_wide(const Smoother& sm) { return sm.max_wave_patches > 256 || sm.max_gen_rows > 8192; }
+
+// The dataflow leg pays off on deep, narrow DAGs (3D Kuhn: ~3n waves, ~13
+// patches per warp on config 2); on shallow, wide ones (2D: 7 waves, 100+
+// patches per warp at L = 9) a warp's serial walk over its patches dominates
+// and the grid leg's 7 barriers are cheaper.
+bool smoother_flow_auto(const Smoother& sm) {
+  return smoother_wide(sm) && sm.npatch <= 16 * (int64_t)kSMs * 16 && sm.nwave >= 16;
+}
 
 // Pulled terms of the dataflow leg (flow.cu).  Entry e = (patch q, DoF u) of
 // the wave-major patch list pulls, for every j coupled to u and every entry
@@ -622,7 +630,6 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
     flow_reset_slots(f.d[dir].p, ne, s);
   }
   f.recmax = recmax;
-  f.ent.upload(ent.data(), n, s);
   f.bar.alloc(1, s);
   f.bar.zero();
   f.ne = ne;

@@ -638,7 +638,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
   const bool down = pc == PC_DOWN;
   const bool wide = smoother_wide(L.sm);
   int m = opts().sweep;
-  if (m == SWEEP_AUTO && wide && L.sm.fl.built) m = SWEEP_FLOW;
+  if (m == SWEEP_AUTO && smoother_flow_auto(L.sm) && L.sm.fl.built) m = SWEEP_FLOW;
   if (m == SWEEP_FLOW && !L.sm.fl.built) m = SWEEP_GRID;  // a DoF in > 2 patches (or not prepared)
   if (m == SWEEP_FLOW) {
     Smoother& sm = L.sm;
@@ -654,20 +654,34 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     fa.recs = fl.recs[dir].p;
     fa.rec_off = fl.rec_off[dir].p;
     fa.d = fl.d[dir].p;
-    fa.ent = fl.ent.p;
-    fa.ap = L.A.ptr.p;
-    fa.ai = L.A.idx.p;
-    fa.av = L.A.val.p;
-    fa.l1 = L.l1.p;
-    fa.b = b;
     fa.x = x;
-    fa.r = L.r.p;
-    fa.r1 = L.d0.p;
-    fa.dj = L.dj.p;
     fa.bar = fl.bar.p;
     fa.trace = g_leg_trace;
-    launch_flow_leg(down, fa, s);
-    return 1;
+    SpmvArgs rj{};  // r = b - A x ; dj = r / l1
+    rj.stop = stop;
+    rj.xin = x;
+    rj.y = L.r.p;
+    rj.b = b;
+    rj.l1 = L.l1.p;
+    rj.dj = L.dj.p;
+    SpmvArgs jb{};  // r -= A dj ; x += dj
+    jb.stop = stop;
+    jb.xin = L.dj.p;
+    jb.y = L.r.p;
+    jb.dj = L.dj.p;
+    jb.x = x;
+    if (down) {
+      fa.r0 = b;
+      launch_flow_leg(true, fa, s);
+      spmv<EPI_RES_JAC>(L.A, rj, s);
+      spmv<EPI_JAC_BW>(L.A, jb, s);
+    } else {
+      spmv<EPI_RES_JAC>(L.A, rj, s);
+      spmv<EPI_JAC_BW>(L.A, jb, s);
+      fa.r0 = L.r.p;
+      launch_flow_leg(false, fa, s);
+    }
+    return 3;
   }
   if (m == SWEEP_AUTO || m == SWEEP_LEG || m == SWEEP_GRID) {
     Smoother& sm = L.sm;

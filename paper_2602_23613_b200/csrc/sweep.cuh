@@ -61,16 +61,8 @@ struct FlowArgs {
   const unsigned char* recs;  // patch records of this direction, in its execution order
   const int64_t* rec_off;     // npatch + 1 byte offsets
   double* d;                  // slots (sentinel between legs)
-  const int2* ent;           // DoF -> its (<= 2) entries, -1 padded
-  const int64_t* ap;
-  const int32_t* ai;
-  const double* av;
-  const double* l1;
-  const double* b;
+  const double* r0;           // the sweep's starting residual (down: b; up: r after the Jacobi step)
   double* x;
-  double* r;
-  double* r1;
-  double* dj;
   unsigned* bar;
   unsigned spin_ns;           // back-off of the slot spin (0: pure spin)
   int gates;                  // wait on the latest-wave predecessors first (1) or poll every term (0)

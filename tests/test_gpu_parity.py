@@ -129,6 +129,12 @@ def test_solves(pair):
     if rg.iterations == ro.iterations:
         assert np.allclose(rg.residual_history, ro.residual_history, rtol=max(c.hist_tol, 10 * tol), atol=0)
     xa, ra = P.amg_solve(hg, c.z["amg_b"], x0=c.z["amg_x0"], tol=1e-8, maxit=200)
+    if c.meta["amg_iters"] >= 200:
+        # the reference's stand-alone AMG stagnates on the 1e6-contrast fields (no
+        # convergence in 200 cycles); whether and when its divergence guard fires
+        # is roundoff-driven there
+        assert not ra.converged
+        return
     assert abs(ra.iterations - c.meta["amg_iters"]) <= 1
     assert np.linalg.norm(xa - c.z["amg_x"]) <= tol * np.linalg.norm(c.z["amg_x"])
 
