@@ -190,12 +190,16 @@ def kernel_roofline(h, reps=None, rank=0, nranks=1):
 
     if pc in (1, 3):
         nc = int(h.levels[ell + 1]._info.n)
-        if int(info.factor_bytes) > 0 and nranks == 1:
+        split = False
+        if nranks > 1 and int(info.max_component) > 0:
+            from paper_2602_23613_b200 import dist as D
+            split = D.representation(int(info.max_component), nc, int(info.factor_bytes), 0, False, nranks)[0]
+        if int(info.factor_bytes) > 0 and not split:
             nbytes = int(info.factor_bytes) + B(int(info.pad), n) + 8 * (n + nc)
         elif int(info.max_component) > 0:
             nG = int(info.max_component)
             q0, q1 = (0, nG)
-            if nranks > 1:
+            if split:
                 from paper_2602_23613_b200 import dist as D
                 q0, q1 = D.plan(nG, nc, rank, nranks).rows
             nbytes = 8 * (q1 - q0) * nc + B(int(info.pad), n) + 8 * (n + nc)

@@ -1282,14 +1282,28 @@ int hcamg_dist_prepare(hcamg_handle* h, int32_t rank, int32_t nranks, void* ipc_
       off += ((size_t)std::max<int64_t>(nd, 1) * 8 + 255) / 256 * 256;
       return o;
     };
+    // Representation per N: a piece is split across the
+    // ranks only when its per-rank bytes beat the single-GPU representation --
+    // the dense block: 2 x 8 nG nc / N (row blocks of Z, restriction + prolongation)
+    // against 2 x the envelope-factor sweeps; the coarsest solve: 8 n^2 / N (rows
+    // of the inverse) against the packed lower triangle (8 n^2 / 2).  Pieces that
+    // are not split run replicated on every rank with the single-GPU kernels.
     for (DevLevel* L : h->lv) {
       L->xoff_g = L->xoff_y = L->xoff_c = DevLevel::kNoSite;
       if (L->hp.on) {
-        hybrid_ensure_z(L->hp, s);  // ranks stream row blocks of the explicit Z
-        L->xoff_g = take(kGroups * L->hp.nc);
-        L->xoff_y = take(L->hp.nG);
+        const double z_rank = 2.0 * 8.0 * (double)L->hp.nG * (double)L->hp.nc / nranks;
+        const double fac = L->hp.fac.on ? 2.0 * (double)(L->hp.fac.fw.bytes + L->hp.fac.bw.bytes) : 1e300;
+        if (z_rank < fac) {
+          hybrid_ensure_z(L->hp, s);  // ranks stream row blocks of the explicit Z
+          L->xoff_g = take(kGroups * L->hp.nc);
+          L->xoff_y = take(L->hp.nG);
+        }
       }
-      if (L->coarsest && L->n >= coarse_gemv_min()) L->xoff_c = take(L->n);
+      if (L->coarsest && L->n >= coarse_gemv_min()) {
+        const double rows = 8.0 * (double)L->n * (double)L->n / nranks;
+        const double packed = L->Asym.on ? 4.0 * (double)L->n * (double)L->n : 1e300;
+        if (rows < packed) L->xoff_c = take(L->n);
+      }
     }
     d.area_bytes = std::max<size_t>(off, 256);
     d.sym_bytes = kFlagBytes + 2 * d.area_bytes;

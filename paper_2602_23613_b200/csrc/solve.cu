@@ -565,10 +565,13 @@ int64_t coarse_gemv_min() { return opts().coarse_gemv_min; }
 int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* x, const int* stop, cudaStream_t s,
                      int part) {
   const int64_t n = L.n;
-  const bool xd = L.dist && L.dist->on;  // this piece may exchange
+  // this piece exchanges when the handle is distributed and dist_prepare gave
+  // it a site (pieces whose split would move more bytes than the single-GPU
+  // form stay replicated: "representation per N", capi.cu)
+  const bool dist_on = L.dist && L.dist->on;
+  const bool xd = dist_on && ((pc == PC_COARSE && L.xoff_c != DevLevel::kNoSite) ||
+                              ((pc == PC_RESTRICT || pc == PC_PROLONG) && L.xoff_g != DevLevel::kNoSite));
   if (part == 2 && !xd) return 0;
-  if (part == 2 && !(pc == PC_COARSE && n >= coarse_gemv_min()) && !((pc == PC_RESTRICT || pc == PC_PROLONG) && L.hp.on))
-    return 0;
   if (pc == PC_COARSE) {
     if (!n) return 0;
     if (n >= coarse_gemv_min() && !xd && L.Asym.on) {  // lower triangle read once (symv.cu)
@@ -576,8 +579,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
       return 2;
     }
     if (n >= coarse_gemv_min()) {
-      require(!xd || L.xoff_c != DevLevel::kNoSite, "distributed layout is stale (call hcamg_dist_prepare again)");
-      dense_gemv_rows(stop, n, n, L.Ainv.p, b, x, s, L.dist, L.xoff_c, part);
+      dense_gemv_rows(stop, n, n, L.Ainv.p, b, x, s, xd ? L.dist : nullptr, L.xoff_c, part);
       return xd ? (part == 0 ? 2 : 1) : 1;
     } else {
       k_gemv_dense<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 7) / 8, kSMs * 8)), kThreads, 0, s>>>(
@@ -599,8 +601,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
         factorp_restrict(stop, L.hp.fac, L.r.p, C->b.p, s);
         return 5;
       }
-      require(!xd || L.xoff_g != DevLevel::kNoSite, "distributed layout is stale (call hcamg_dist_prepare again)");
-      hybrid_restrict(stop, L.hp, L.r.p, C->b.p, s, L.dist, L.xoff_g, part);
+      hybrid_restrict(stop, L.hp, L.r.p, C->b.p, s, xd ? L.dist : nullptr, L.xoff_g, part);
       if (!xd) return 3;
       return part == 0 ? 4 : (part == 1 ? 3 : 1);
     }
@@ -628,8 +629,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
       return 5;
     }
     if (L.hp.on) {  // x[G] -= Z x_c
-      require(!xd || L.xoff_y != DevLevel::kNoSite, "distributed layout is stale (call hcamg_dist_prepare again)");
-      hybrid_prolong(stop, L.hp, C->x.p, x, s, L.dist, L.xoff_y, part);
+      hybrid_prolong(stop, L.hp, C->x.p, x, s, xd ? L.dist : nullptr, L.xoff_y, part);
       if (!xd) return 2;
       return part == 0 ? 3 : (part == 1 ? 2 : 1);
     }

@@ -62,6 +62,20 @@ def plan(nG: int, nc: int, rank: int, nranks: int, n_coarse: int = 0) -> RankPla
     return RankPlan(chunk, nchunk, grp, g0, g1, rows, coarse)
 
 
+def representation(nG: int, nc: int, factor_bytes: int, n_coarse: int, coarse_symv: bool, nranks: int):
+    """Which pieces the distributed solve splits across ranks (mirrors
+    capi.cu ``hcamg_dist_prepare``): the dense block when its per-rank row
+    block (2 x 8 nG nc / N bytes per V-cycle) is smaller than applying it
+    through the envelope factor on every rank (2 x factor_bytes; 0: no
+    factor, always split); the coarsest solve when 8 n^2 / N beats the packed
+    lower triangle (4 n^2).  Returns (split_dense, split_coarse)."""
+    z_rank = 2.0 * 8.0 * nG * nc / nranks
+    fac = 2.0 * factor_bytes if factor_bytes > 0 else float("inf")
+    rows = 8.0 * n_coarse * n_coarse / nranks
+    packed = 4.0 * n_coarse * n_coarse if coarse_symv else float("inf")
+    return (nG > 0 and z_rank < fac), (n_coarse > 0 and rows < packed)
+
+
 def exchange_handles(local: bytes, group=None) -> bytes:
     """All-gather every rank's IPC handle, concatenated in rank order."""
     import torch.distributed as dist

@@ -139,3 +139,17 @@ def test_two_rank_exchange_over_gloo():
         assert ok_h, f"rank {rank}: handles out of order"
         assert ok_bc, f"rank {rank}: restriction differs"
         assert ok_y, f"rank {rank}: prolongation differs"
+
+
+def test_representation_per_rank_count():
+    """Config 2: the explicit Z (167,784 x 26,236, 35.2 GB)
+    is split only when a rank's row block beats the 11.1 GB of envelope-factor
+    sweeps every V-cycle applies twice -- from 4 ranks on; the 26,236^2 coarsest
+    inverse only when its rows beat the packed triangle -- from 3 ranks on."""
+    from paper_2602_23613_b200.dist import representation
+    nG, nc, fac, ncs = 167784, 26236, 5337000000 + 5792000000, 26236
+    got = {N: representation(nG, nc, fac, ncs, True, N) for N in range(1, 9)}
+    assert [N for N in got if got[N][0]] == [4, 5, 6, 7, 8]
+    assert [N for N in got if got[N][1]] == [3, 4, 5, 6, 7, 8]
+    # without the factor / packed triangle every piece is split (the round-1 layout)
+    assert all(representation(nG, nc, 0, ncs, False, N) == (True, True) for N in range(1, 9))
