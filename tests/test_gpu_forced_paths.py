@@ -51,6 +51,18 @@ def same_pattern(a, b):
             and np.array_equal(a.indices, b.indices))
 
 
+def max_interior_component(level):
+    """Largest connected component of A_II (transfer.py:49-52): the dense
+    regime applies to components above the giant_min cutoff (interp.cu)."""
+    from scipy.sparse.csgraph import connected_components
+
+    I = np.asarray(level.splitting.interior_dofs)
+    if I.size == 0:
+        return 0
+    _, lab = connected_components(level.A.tocsr()[I][:, I], directed=False)
+    return int(np.bincount(lab).max())
+
+
 @pytest.fixture(scope="module", params=CASES)
 def oracle_case(request):
     c = load(request.param)
@@ -90,6 +102,7 @@ def test_dense_regime_forced(oracle_case, variant):
     hg = P.build_hierarchy(c.system, c.meta["method"], meshes=c.meshes, rmaps=c.rmaps, options=VARIANTS[variant])
     assert hg.depth == ho.depth and hg.stalled == ho.stalled and hg.notes == ho.notes
     dense_levels = 0
+    expect_dense = name.startswith("kuhn")
     for ell, (lg, lo) in enumerate(zip(hg.levels, ho.levels)):
         assert lg.n == lo.n
         assert same_pattern(lg.A, lo.A), f"A_{ell} pattern"
@@ -97,6 +110,7 @@ def test_dense_regime_forced(oracle_case, variant):
         if lo.P is None:
             continue
         dense_levels += int(lg._info.max_component) > 0
+        expect_dense |= max_interior_component(lo) > VARIANTS[variant].get("giant_min", 4096)
         so, sg = lo.splitting, lg.splitting
         assert [tuple(p) for p in sg.pairs] == [(p.dof1, p.dof2, p.sign1, p.sign2, p.tail, p.mid, p.head)
                                                for p in so.pairs]
@@ -106,7 +120,7 @@ def test_dense_regime_forced(oracle_case, variant):
         # A_{l+1} is the Galerkin product of the exported P (Schur form in the dense regime)
         M = lg.P.T @ (lg.A @ lg.P)
         assert rel(P.csr(0.5 * (M + M.T)).toarray(), hg.levels[ell + 1].A.toarray()) <= 1e-12
-    if name.startswith("kuhn") or variant == "multi_giant":
+    if expect_dense:
         assert dense_levels >= 1, "the dense-regime path was not taken"
     check_solves(c, ho, hg)
 
