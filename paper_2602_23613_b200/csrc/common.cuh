@@ -57,13 +57,14 @@ struct DBuf {
   T* p = nullptr;
   int64_t n = 0;
   cudaStream_t s = 0;
+  bool view = false;  // points into memory owned elsewhere (the row partition's symmetric buffer)
   DBuf() = default;
   DBuf(int64_t count, cudaStream_t st) { alloc(count, st); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n), s(o.s), view(o.view) { o.p = nullptr; o.n = 0; o.view = false; }
   DBuf& operator=(DBuf&& o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; view = o.view; o.p = nullptr; o.n = 0; o.view = false; }
     return *this;
   }
   ~DBuf() { release(); }
@@ -78,9 +79,17 @@ struct DBuf {
     }
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p && !view) cudaFreeAsync(p, s);
     p = nullptr;
     n = 0;
+    view = false;
+  }
+  void alias(T* ptr, int64_t count, cudaStream_t st) {
+    release();
+    p = ptr;
+    n = count;
+    s = st;
+    view = true;
   }
   void zero() { if (n) HC_CUDA(cudaMemsetAsync(p, 0, sizeof(T) * (size_t)n, s)); }
   void fill_bytes(int v) { if (n) HC_CUDA(cudaMemsetAsync(p, v, sizeof(T) * (size_t)n, s)); }

@@ -78,6 +78,8 @@ struct Smoother {
 void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s);
 // Waves wider than one 16-CTA cluster (the auto mode runs such levels on the whole GPU).
 bool smoother_wide(const Smoother& sm);
+// Auto mode runs this level one launch per wavefront (shallow, very wide schedules).
+bool smoother_wave_auto(const Smoother& sm);
 // Auto mode runs the dataflow leg on this level.
 bool smoother_flow_auto(const Smoother& sm);
 

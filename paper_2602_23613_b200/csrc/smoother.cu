@@ -479,6 +479,14 @@ bool smoother_wide(const Smoother& sm) { return sm.max_wave_patches > 256 || sm.
 // patches per warp on config 2); on shallow, wide ones (2D: 7 waves, 100+
 // patches per warp at L = 9) a warp's serial walk over its patches dominates
 // and the grid leg's 7 barriers are cheaper.
+// Shallow, very wide schedules (2D: 7-10 waves of up to tens of thousands of
+// patches): one full-GPU launch per wavefront, several patches per warp.  The
+// cooperative grid leg gives each warp one fast patch per wave and walks the
+// rest serially; it is the right shape only while a wave fits its warps.
+bool smoother_wave_auto(const Smoother& sm) {
+  return sm.nwave > 0 && sm.max_wave_patches > (int64_t)kSMs * 16 && sm.npatch / sm.nwave > (int64_t)kSMs * 8;
+}
+
 bool smoother_flow_auto(const Smoother& sm) {
   return smoother_wide(sm) && sm.npatch <= 16 * (int64_t)kSMs * 16 && sm.nwave >= 16;
 }

@@ -77,88 +77,100 @@ __device__ __forceinline__ void set_cond(unsigned long long cond, unsigned v) {
 struct WaveArgs {
   const int* stop;
   int64_t n;
-  // generic pulled rows
+  // generic pulled rows: (u, start, end) triples of the source wave, or -- row
+  // partition -- this rank's subset of them through `gen` (indices into the triples)
+  const int32_t* genrow;
   const int32_t* gen;
   int64_t ngen;
-  const int64_t* grow_ptr;
-  const int32_t* grow_u;
   const int32_t* gcol;
   const double* gval;
   const double* dsrc;
-  // patches of the destination wave
-  int64_t p0, p1;
+  // patches of the destination wave: [p0, p0 + np), or plist[0..np)
+  int64_t p0, np;
+  const int32_t* plist;
   const int64_t* patch_ptr;
   const int32_t* dofs;
   const int64_t* binv_off;
   const double* binv;
-  const int32_t* own;
+  const int32_t* ownr;        // per patch entry: (start, end) of the gather row pulled before the solve, or (-1, -1)
   double* r;
   double* x;
   double* ddst;
   const double* b;            // init step only
   const uint8_t* in_first;    // init step only
+  const int32_t* rows;        // init step only: the rows this rank initialises (null: all n)
+  int64_t nrows;
   int gen_blocks;
 };
 
-__device__ __forceinline__ double pull(int32_t rho, const int64_t* __restrict__ gp, const int32_t* __restrict__ gc,
+// sum_k gval[k] d[gcol[k]] over [s, e), sequential fma order
+__device__ __forceinline__ double pull(int32_t s, int32_t e, const int32_t* __restrict__ gc,
                                        const double* __restrict__ gv, const double* __restrict__ d) {
-  const int64_t s = gp[rho], e = gp[rho + 1];
   double acc = 0.0;
-  for (int64_t k0 = s; k0 < e; k0 += 8) {
-    int32_t c[8];
-    double v[8], dv[8];
+  for (int32_t k0 = s; k0 < e; k0 += 4) {
+    int32_t c[4];
+    double v[4], dv[4];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
+    for (int t = 0; t < 4; ++t) {
       const bool ok = k0 + t < e;
       c[t] = ok ? __ldg(gc + k0 + t) : 0;
       v[t] = ok ? __ldg(gv + k0 + t) : 0.0;
     }
 #pragma unroll
-    for (int t = 0; t < 8; ++t) dv[t] = k0 + t < e ? d[c[t]] : 0.0;
+    for (int t = 0; t < 4; ++t) dv[t] = k0 + t < e ? d[c[t]] : 0.0;
 #pragma unroll
-    for (int t = 0; t < 8; ++t) acc = fma(v[t], dv[t], acc);
+    for (int t = 0; t < 4; ++t)
+      if (k0 + t < e) acc = fma(v[t], dv[t], acc);
   }
   return acc;
 }
 
-template <bool kInit>
+// One wavefront of the multiplicative sweep.  KG lanes per patch (the level's
+// largest patch rounded up to 8 / 16 / 32), so a warp solves 32 / KG patches:
+// on the wide 2D waves (tens of thousands of 6-DoF patches) the kernel is
+// bound by loads in flight, not by lanes.
+template <int KG, bool kInit>
 __global__ void __launch_bounds__(kThreads) k_wave(WaveArgs a) {
   if (*a.stop) return;
   if ((int)blockIdx.x < a.gen_blocks) {
     const int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x;
     if (kInit) {
-      for (int64_t u = t; u < a.n; u += (int64_t)a.gen_blocks * kThreads) {
+      for (int64_t q = t; q < a.nrows; q += (int64_t)a.gen_blocks * kThreads) {
+        const int64_t u = a.rows ? a.rows[q] : q;
         a.r[u] = a.b[u];
         if (!a.in_first[u]) a.x[u] = 0.0;
       }
     } else if (t < a.ngen) {
-      const int32_t rho = a.gen[t];
-      const int32_t u = a.grow_u[rho];
-      a.r[u] -= pull(rho, a.grow_ptr, a.gcol, a.gval, a.dsrc);
+      const int32_t* g = a.genrow + 3 * (int64_t)(a.gen ? a.gen[t] : t);
+      const int32_t u = g[0];
+      a.r[u] -= pull(g[1], g[2], a.gcol, a.gval, a.dsrc);
     }
     return;
   }
-  const int lane = threadIdx.x & 31;
-  const int64_t p = a.p0 + ((int64_t)(blockIdx.x - a.gen_blocks) * kThreads + threadIdx.x) / 32;
-  if (p >= a.p1) return;
-  const int64_t e0 = a.patch_ptr[p];
-  const int k = (int)(a.patch_ptr[p + 1] - e0);
-  const double* Bi = a.binv + a.binv_off[p];
-  double bcol[16];
+  constexpr int kB = KG < 16 ? KG : 16;  // inverse columns held in registers
+  const int sub = threadIdx.x & (KG - 1);
+  const int64_t t = ((int64_t)(blockIdx.x - a.gen_blocks) * kThreads + threadIdx.x) / KG;
+  const bool have = t < a.np;
+  const int64_t p = have ? (a.plist ? (int64_t)a.plist[t] : a.p0 + t) : 0;
+  const int64_t e0 = have ? a.patch_ptr[p] : 0;
+  const int k = have ? (int)(a.patch_ptr[p + 1] - e0) : 0;
+  const bool act = sub < k;
+  const double* Bi = a.binv + (have ? a.binv_off[p] : 0);
+  double bcol[kB];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) bcol[c] = (c < k && lane < k) ? __ldg(Bi + (int64_t)c * k + lane) : 0.0;
+  for (int c = 0; c < kB; ++c) bcol[c] = (c < k && act) ? __ldg(Bi + (int64_t)c * k + sub) : 0.0;
   int32_t i = 0;
   double v = 0.0;
-  if (lane < k) {
-    i = a.dofs[e0 + lane];
+  if (act) {
+    i = a.dofs[e0 + sub];
     if (kInit) {
       v = a.b[i];
     } else {
       v = a.r[i];
-      if (a.own) {
-        const int32_t rho = a.own[e0 + lane];
-        if (rho >= 0) {
-          v -= pull(rho, a.grow_ptr, a.gcol, a.gval, a.dsrc);
+      if (a.ownr) {
+        const int32_t s = a.ownr[2 * (e0 + sub)], e = a.ownr[2 * (e0 + sub) + 1];
+        if (s >= 0) {
+          v -= pull(s, e, a.gcol, a.gval, a.dsrc);
           a.r[i] = v;
         }
       }
@@ -167,12 +179,16 @@ __global__ void __launch_bounds__(kThreads) k_wave(WaveArgs a) {
   // d = B_p^{-1} r[patch]  (column-major inverse: coalesced over the lanes)
   double d = 0.0;
 #pragma unroll
-  for (int c = 0; c < 16; ++c) d = fma(bcol[c], __shfl_sync(0xffffffffu, v, c), d);
-  for (int c = 16; c < k; ++c) {
-    const double vc = __shfl_sync(0xffffffffu, v, c);
-    if (lane < k) d = fma(Bi[(int64_t)c * k + lane], vc, d);
+  for (int c = 0; c < kB; ++c) d = fma(bcol[c], __shfl_sync(0xffffffffu, v, c, KG), d);
+  if (KG > kB) {
+    int kmax = k;
+    for (int o = 16; o; o >>= 1) kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    for (int c = kB; c < kmax; ++c) {
+      const double vc = __shfl_sync(0xffffffffu, v, c, KG);
+      if (act && c < k) d = fma(Bi[(int64_t)c * k + sub], vc, d);
+    }
   }
-  if (lane < k) {
+  if (act) {
     a.x[i] = kInit ? d : a.x[i] + d;
     a.ddst[i] = d;
   }
@@ -180,9 +196,9 @@ __global__ void __launch_bounds__(kThreads) k_wave(WaveArgs a) {
 
 struct FinalArgs {
   const int* stop;
-  int64_t n;
-  const int32_t* last_row;
-  const int64_t* grow_ptr;
+  int64_t n;                  // rows handled: all of the level, or rows[0..n)
+  const int32_t* rows;
+  const int32_t* lastr;       // per DoF: (start, end) of the last wave's gather row, or (-1, -1)
   const int32_t* gcol;
   const double* gval;
   const double* dsrc;
@@ -194,11 +210,12 @@ struct FinalArgs {
 
 __global__ void __launch_bounds__(kThreads) k_fw_final(FinalArgs a) {
   if (*a.stop) return;
-  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < a.n; u += (int64_t)gridDim.x * kThreads) {
+  for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < a.n; q += (int64_t)gridDim.x * kThreads) {
+    const int64_t u = a.rows ? a.rows[q] : q;
     double v = a.r[u];
-    if (a.last_row) {
-      const int32_t rho = a.last_row[u];
-      if (rho >= 0) v -= pull(rho, a.grow_ptr, a.gcol, a.gval, a.dsrc);
+    if (a.lastr) {
+      const int32_t s = a.lastr[2 * u], e = a.lastr[2 * u + 1];
+      if (s >= 0) v -= pull(s, e, a.gcol, a.gval, a.dsrc);
     }
     const double d = v / a.l1[u];
     a.x[u] += d;
@@ -208,9 +225,10 @@ __global__ void __launch_bounds__(kThreads) k_fw_final(FinalArgs a) {
 }
 
 __global__ void k_init_rb(const int* stop, int64_t n, const double* __restrict__ b, double* __restrict__ r,
-                          double* __restrict__ x) {
+                          double* __restrict__ x, const int32_t* __restrict__ rows) {
   if (*stop) return;
-  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t u = rows ? (int64_t)rows[q] : q;
     r[u] = b[u];
     x[u] = 0.0;
   }
@@ -248,7 +266,55 @@ struct SpmvArgs {
   double* part2;
   double* hist;
   unsigned long long cond;
+  const int32_t* rows;  // row partition: this rank's rows (nrows of them); null: rows [0, nrows)
+  double* red;          // row partition: the rank's partial sum(s) go here, k_finish completes the reduction
 };
+
+// ---- scalar logic behind the reductions (run by the last block of the
+// reducing kernel, or by k_finish after the cross-rank sum)
+
+__device__ __forceinline__ void fin_ap(Ctl* c, double S, unsigned long long cond) {
+  c->pAp = S;
+  if (!(S > 0.0)) { c->error = kErrPAp; c->stop = 1; set_cond(cond, 0); }
+  else c->alpha = c->rz / S;
+}
+
+__device__ __forceinline__ void fin_init(Ctl* c, double S, double S2, unsigned long long cond) {
+  c->bnorm = sqrt(S2);
+  c->it = 0;
+  c->error = kErrNone;
+  c->growth = 0;
+  c->converged = 0;
+  c->zero_b = 0;
+  c->stop = 0;
+  if (c->bnorm == 0.0) {
+    c->zero_b = 1; c->converged = 1; c->stop = 1;
+  } else {
+    c->rel = sqrt(S) / c->bnorm;
+    c->prev_rel = c->rel;
+    if (c->rel <= c->tol) { c->converged = 1; c->stop = 1; }
+    else if (c->maxit <= 0) c->stop = 1;
+  }
+  set_cond(cond, c->stop ? 0u : 1u);
+}
+
+__device__ __forceinline__ void fin_update(Ctl* c, double S, double* hist, unsigned long long cond) {
+  const double rel = sqrt(S) / c->bnorm;
+  c->rel = rel;
+  hist[c->it] = rel;
+  c->it += 1;
+  if (rel <= c->tol) { c->converged = 1; c->stop = 1; }
+  else if (c->it >= c->maxit) c->stop = 1;
+  set_cond(cond, c->stop ? 0u : 1u);
+}
+
+template <bool kFirst>
+__device__ __forceinline__ void fin_rz(Ctl* c, double S, unsigned long long cond) {
+  if (kFirst) { c->rz = S; return; }
+  if (!(S > 0.0)) { c->error = kErrRz; c->stop = 1; set_cond(cond, 0); return; }
+  c->beta = S / c->rz;
+  c->rz = S;
+}
 
 template <int G, int E>
 __global__ void __launch_bounds__(kThreads) k_spmv(SpmvArgs a) {
@@ -261,12 +327,14 @@ __global__ void __launch_bounds__(kThreads) k_spmv(SpmvArgs a) {
   const int64_t ngrp = (int64_t)gridDim.x * kThreads / G;
   double part = 0.0, part2 = 0.0;
   const int64_t rows_iter = ((a.nrows + ngrp - 1) / ngrp) * ngrp;
-  for (int64_t row = grp; row < rows_iter; row += ngrp) {
+  for (int64_t q = grp; q < rows_iter; q += ngrp) {
+    const bool live = q < a.nrows;
+    const int64_t row = live ? (a.rows ? (int64_t)a.rows[q] : q) : 0;
     double s = 0.0;
-    if (row < a.nrows)
+    if (live)
       for (int64_t e = a.ptr[row] + lg; e < a.ptr[row + 1]; e += G) s = fma(a.val[e], a.xin[a.idx[e]], s);
     for (int o = G / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
-    if (lg != 0 || row >= a.nrows) continue;
+    if (lg != 0 || !live) continue;
     if (E == EPI_SET) a.y[row] = s;
     else if (E == EPI_ADD) a.y[row] += s;
     else if (E == EPI_JAC_FW) a.y[row] -= s;
@@ -288,27 +356,15 @@ __global__ void __launch_bounds__(kThreads) k_spmv(SpmvArgs a) {
   const double S2 = two ? ordered_sum(a.part2, gridDim.x) : 0.0;
   if (threadIdx.x != 0) return;
   c->ticket[E - EPI_AP] = 0u;
+  if (a.red) {  // row partition: publish the rank's partials, k_finish sums over the ranks
+    a.red[0] = S;
+    a.red[1] = S2;
+    return;
+  }
   if (E == EPI_AP) {
-    c->pAp = S;
-    if (!(S > 0.0)) { c->error = kErrPAp; c->stop = 1; set_cond(a.cond, 0); }
-    else c->alpha = c->rz / S;
+    fin_ap(c, S, a.cond);
   } else if (E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN) {
-    c->bnorm = sqrt(S2);
-    c->it = 0;
-    c->error = kErrNone;
-    c->growth = 0;
-    c->converged = 0;
-    c->zero_b = 0;
-    c->stop = 0;
-    if (c->bnorm == 0.0) {
-      c->zero_b = 1; c->converged = 1; c->stop = 1;
-    } else {
-      c->rel = sqrt(S) / c->bnorm;
-      c->prev_rel = c->rel;
-      if (c->rel <= c->tol) { c->converged = 1; c->stop = 1; }
-      else if (c->maxit <= 0) c->stop = 1;
-    }
-    set_cond(a.cond, c->stop ? 0u : 1u);
+    fin_init(c, S, S2, a.cond);
   } else if (E == EPI_AMG_RES) {
     const double prev = c->rel;
     const double rel = sqrt(S) / c->bnorm;
@@ -330,11 +386,13 @@ __global__ void __launch_bounds__(kThreads) k_spmv(SpmvArgs a) {
 __global__ void __launch_bounds__(kThreads) k_pcg_update(const int* stop, int64_t n, double* __restrict__ x,
                                                          double* __restrict__ r, const double* __restrict__ p,
                                                          const double* __restrict__ Ap, Ctl* c, double* part,
-                                                         double* hist, unsigned long long cond) {
+                                                         double* hist, unsigned long long cond,
+                                                         const int32_t* __restrict__ rows, double* red) {
   if (*stop) return;
   const double alpha = c->alpha;
   double acc = 0.0;
-  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < n; u += (int64_t)gridDim.x * kThreads) {
+  for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < n; q += (int64_t)gridDim.x * kThreads) {
+    const int64_t u = rows ? (int64_t)rows[q] : q;
     x[u] = fma(alpha, p[u], x[u]);
     const double rv = fma(-alpha, Ap[u], r[u]);
     r[u] = rv;
@@ -344,22 +402,19 @@ __global__ void __launch_bounds__(kThreads) k_pcg_update(const int* stop, int64_
   const double S = ordered_sum(part, gridDim.x);
   if (threadIdx.x != 0) return;
   c->ticket[6] = 0u;
-  const double rel = sqrt(S) / c->bnorm;
-  c->rel = rel;
-  hist[c->it] = rel;
-  c->it += 1;
-  if (rel <= c->tol) { c->converged = 1; c->stop = 1; }
-  else if (c->it >= c->maxit) c->stop = 1;
-  set_cond(cond, c->stop ? 0u : 1u);
+  if (red) { red[0] = S; red[1] = 0.0; return; }
+  fin_update(c, S, hist, cond);
 }
 
 template <bool kFirst>
 __global__ void __launch_bounds__(kThreads) k_dot_rz(const int* stop, int64_t n, const double* __restrict__ r,
                                                      const double* __restrict__ z, double* __restrict__ p, Ctl* c,
-                                                     double* part, unsigned long long cond) {
+                                                     double* part, unsigned long long cond,
+                                                     const int32_t* __restrict__ rows, double* red) {
   if (*stop) return;
   double acc = 0.0;
-  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < n; u += (int64_t)gridDim.x * kThreads) {
+  for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < n; q += (int64_t)gridDim.x * kThreads) {
+    const int64_t u = rows ? (int64_t)rows[q] : q;
     const double zv = z[u];
     acc = fma(r[u], zv, acc);
     if (kFirst) p[u] = zv;
@@ -368,18 +423,41 @@ __global__ void __launch_bounds__(kThreads) k_dot_rz(const int* stop, int64_t n,
   const double S = ordered_sum(part, gridDim.x);
   if (threadIdx.x != 0) return;
   c->ticket[7] = 0u;
-  if (kFirst) { c->rz = S; return; }
-  if (!(S > 0.0)) { c->error = kErrRz; c->stop = 1; set_cond(cond, 0); return; }
-  c->beta = S / c->rz;
-  c->rz = S;
+  if (red) { red[0] = S; red[1] = 0.0; return; }
+  fin_rz<kFirst>(c, S, cond);
 }
 
 __global__ void __launch_bounds__(kThreads) k_p_update(const int* stop, int64_t n, const double* __restrict__ z,
-                                                       double* __restrict__ p, const Ctl* c) {
+                                                       double* __restrict__ p, const Ctl* c,
+                                                       const int32_t* __restrict__ rows) {
   if (*stop) return;
   const double beta = c->beta;
-  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < n; u += (int64_t)gridDim.x * kThreads)
+  for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < n; q += (int64_t)gridDim.x * kThreads) {
+    const int64_t u = rows ? (int64_t)rows[q] : q;
     p[u] = fma(beta, p[u], z[u]);
+  }
+}
+
+// Row partition: complete a reduction.  red holds (S, S2) per rank; every rank
+// sums them in rank order, so all ranks take identical decisions.
+// site: 0 PCG init, 1 pAp, 2 residual update, 3 r.z (first), 4 r.z
+__global__ void k_finish(const int* stop, int site, Ctl* c, const double* red, int nranks, double* hist,
+                         unsigned long long cond) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (site != 0 && *stop) {
+    if (site == 1) set_cond(cond, 0);
+    return;
+  }
+  double S = 0.0, S2 = 0.0;
+  for (int r = 0; r < nranks; ++r) {
+    S += red[2 * r];
+    S2 += red[2 * r + 1];
+  }
+  if (site == 0) fin_init(c, S, S2, cond);
+  else if (site == 1) fin_ap(c, S, cond);
+  else if (site == 2) fin_update(c, S, hist, cond);
+  else if (site == 3) fin_rz<true>(c, S, cond);
+  else fin_rz<false>(c, S, cond);
 }
 
 __global__ void k_loop_guard(const int* stop, unsigned long long cond) {
@@ -438,12 +516,12 @@ void launch_spmv_g(int G, unsigned grid, SpmvArgs& a, cudaStream_t s) {
 
 template <int E>
 unsigned spmv(const DCsr& M, SpmvArgs a, cudaStream_t s) {
-  a.nrows = M.nrows;
+  if (!a.rows) a.nrows = M.nrows;  // a row list carries its own count
   a.ptr = M.ptr.p;
   a.idx = M.idx.p;
   a.val = M.val.p;
   const int G = group_for(M);
-  const unsigned grid = spmv_grid(M.nrows, G);
+  const unsigned grid = spmv_grid(a.nrows, G);
   launch_spmv_g<E>(G, grid, a, s);
   return grid;
 }
@@ -472,62 +550,102 @@ void Workspace::ensure(int64_t n_, int64_t maxit, cudaStream_t s) {
 
 long long* g_leg_trace = nullptr;  // debug: set by hcamg_debug_trace
 
+// ---- one wavefront launch (shared by the per-wave leg and the row partition)
+
+// The ranges of a wave step this process computes: everything (single GPU,
+// agglomerated levels) or one rank's share of a row-partitioned level.
+struct WaveShare {
+  const int32_t* plist = nullptr;  // this rank's patches of the destination wave (null: the whole wave)
+  int64_t np = -1;
+  const int32_t* gen = nullptr;    // this rank's generic rows of the source wave (indices into the wave's triples)
+  int64_t ngen = -1;
+  const int32_t* rows = nullptr;   // init step: this rank's rows
+  int64_t nrows = -1;
+};
+
+template <bool kInit>
+static void launch_wave_kg(int kg, unsigned grid, const WaveArgs& a, cudaStream_t s) {
+  if (kg == 8) k_wave<8, kInit><<<grid, kThreads, 0, s>>>(a);
+  else if (kg == 16) k_wave<16, kInit><<<grid, kThreads, 0, s>>>(a);
+  else k_wave<32, kInit><<<grid, kThreads, 0, s>>>(a);
+  HC_CHECK_LAUNCH();
+}
+
+// destination wave `dst`, pulling the corrections of wave `src` (-1: none);
+// dir 0 forward / 1 backward; init: the first forward wave (r = b, x = 0)
+static void launch_wave(DevLevel& L, const double* b, double* x, const int* stop, bool init, int64_t dst, int64_t src,
+                        int dir, const WaveShare& sh, cudaStream_t s) {
+  Smoother& sm = L.sm;
+  const int64_t n = L.n;
+  double* dbuf[2] = {L.d0.p, L.d1.p};
+  WaveArgs a{};
+  a.stop = stop;
+  a.n = n;
+  a.gcol = sm.gcol.p;
+  a.gval = sm.gval.p;
+  a.p0 = sm.wave_ptr[(size_t)dst];
+  a.np = sh.np >= 0 ? sh.np : sm.wave_ptr[(size_t)dst + 1] - a.p0;
+  a.plist = sh.plist;
+  a.patch_ptr = sm.patch_ptr.p;
+  a.dofs = sm.patch_dofs.p;
+  a.binv_off = sm.binv_off.p;
+  a.binv = sm.binv.p;
+  a.r = L.r.p;
+  a.x = x;
+  a.ddst = dbuf[dst & 1];
+  if (init) {
+    a.b = b;
+    a.in_first = sm.in_first.p;
+    a.rows = sh.rows;
+    a.nrows = sh.nrows >= 0 ? sh.nrows : n;
+    a.gen_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((a.nrows + kThreads - 1) / kThreads, kSMs * 4));
+  } else if (src >= 0) {
+    const std::vector<int64_t>& gp = dir == 0 ? sm.gen_fw_ptr : sm.gen_bw_ptr;
+    const int64_t g0 = gp[(size_t)src], g1 = gp[(size_t)src + 1];
+    a.genrow = (dir == 0 ? sm.genrow_fw.p : sm.genrow_bw.p) + 3 * g0;
+    a.gen = sh.gen;
+    a.ngen = sh.ngen >= 0 ? sh.ngen : g1 - g0;
+    a.dsrc = dbuf[src & 1];
+    a.ownr = dir == 0 ? sm.ownr_fw.p : sm.ownr_bw.p;
+    a.gen_blocks = (int)((a.ngen + kThreads - 1) / kThreads);
+  }
+  const int kg = sm.kmax <= 8 ? 8 : sm.kmax <= 16 ? 16 : 32;
+  const int64_t per_block = kThreads / kg;
+  const int64_t pb = (a.np + per_block - 1) / per_block;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, a.gen_blocks + pb);
+  if (init) launch_wave_kg<true>(kg, grid, a, s);
+  else launch_wave_kg<false>(kg, grid, a, s);
+}
+
+static void launch_fw_final(DevLevel& L, double* x, const int* stop, const int32_t* rows, int64_t nrows,
+                            cudaStream_t s) {
+  Smoother& sm = L.sm;
+  const int64_t W = sm.nwave;
+  double* dbuf[2] = {L.d0.p, L.d1.p};
+  const int64_t cnt = rows ? nrows : L.n;
+  FinalArgs f{stop, cnt, rows, W > 0 ? sm.lastr.p : nullptr, sm.gcol.p, sm.gval.p,
+              W > 0 ? dbuf[(W - 1) & 1] : nullptr, L.l1.p, L.r.p, x, L.dj.p};
+  k_fw_final<<<vec_grid(std::max<int64_t>(cnt, 1)), kThreads, 0, s>>>(f);
+  HC_CHECK_LAUNCH();
+}
+
 // per-wave kernel sequence of one smoothing leg (one launch per wavefront)
 static int64_t record_leg_waves(DevLevel& L, const double* b, double* x, const int* stop, bool down, cudaStream_t s) {
   Smoother& sm = L.sm;
   const int64_t n = L.n, W = sm.nwave;
-  double* dbuf[2] = {L.d0.p, L.d1.p};
   int64_t launches = 0;
-  auto wave = [&](bool init, int64_t dst, int64_t src, int dir) {
-    WaveArgs a{};
-    a.stop = stop;
-    a.n = n;
-    a.grow_ptr = sm.grow_ptr.p;
-    a.grow_u = sm.grow_u.p;
-    a.gcol = sm.gcol.p;
-    a.gval = sm.gval.p;
-    a.p0 = sm.wave_ptr[(size_t)dst];
-    a.p1 = sm.wave_ptr[(size_t)dst + 1];
-    a.patch_ptr = sm.patch_ptr.p;
-    a.dofs = sm.patch_dofs.p;
-    a.binv_off = sm.binv_off.p;
-    a.binv = sm.binv.p;
-    a.r = L.r.p;
-    a.x = x;
-    a.ddst = dbuf[dst & 1];
-    if (init) {
-      a.b = b;
-      a.in_first = sm.in_first.p;
-      a.gen_blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + kThreads - 1) / kThreads, kSMs * 4));
-    } else if (src >= 0) {
-      const std::vector<int64_t>& gp = dir == 0 ? sm.gen_fw_ptr : sm.gen_bw_ptr;
-      const int64_t g0 = gp[(size_t)src], g1 = gp[(size_t)src + 1];
-      a.gen = (dir == 0 ? sm.gen_fw.p : sm.gen_bw.p) + g0;
-      a.ngen = g1 - g0;
-      a.dsrc = dbuf[src & 1];
-      a.own = dir == 0 ? sm.own_fw.p : sm.own_bw.p;
-      a.gen_blocks = (int)((a.ngen + kThreads - 1) / kThreads);
-    }
-    const int64_t pb = (a.p1 - a.p0 + kThreads / 32 - 1) / (kThreads / 32);
-    const unsigned grid = (unsigned)std::max<int64_t>(1, a.gen_blocks + pb);
-    if (init) k_wave<true><<<grid, kThreads, 0, s>>>(a);
-    else k_wave<false><<<grid, kThreads, 0, s>>>(a);
-    HC_CHECK_LAUNCH();
-    ++launches;
-  };
+  const WaveShare all{};
   if (down) {
     if (W > 0) {
-      wave(true, 0, -1, 0);
-      for (int64_t d = 1; d < W; ++d) wave(false, d, d - 1, 0);
+      launch_wave(L, b, x, stop, true, 0, -1, 0, all, s);
+      for (int64_t d = 1; d < W; ++d) launch_wave(L, b, x, stop, false, d, d - 1, 0, all, s);
+      launches += W;
     } else {
-      k_init_rb<<<vec_grid(n), kThreads, 0, s>>>(stop, n, b, L.r.p, x);
+      k_init_rb<<<vec_grid(n), kThreads, 0, s>>>(stop, n, b, L.r.p, x, nullptr);
       HC_CHECK_LAUNCH();
       ++launches;
     }
-    FinalArgs f{stop, n, W > 0 ? sm.last_row.p : nullptr, sm.grow_ptr.p, sm.gcol.p, sm.gval.p,
-                W > 0 ? dbuf[(W - 1) & 1] : nullptr, L.l1.p, L.r.p, x, L.dj.p};
-    k_fw_final<<<vec_grid(n), kThreads, 0, s>>>(f);
-    HC_CHECK_LAUNCH();
+    launch_fw_final(L, x, stop, nullptr, 0, s);
     SpmvArgs a{};
     a.stop = stop;
     a.xin = L.dj.p;
@@ -551,8 +669,8 @@ static int64_t record_leg_waves(DevLevel& L, const double* b, double* x, const i
   jb.x = x;
   spmv<EPI_JAC_BW>(L.A, jb, s);
   launches += 2;
-  for (int64_t d = W - 1; d >= 0; --d) wave(false, d, d == W - 1 ? -1 : d + 1, 1);
-  return launches;
+  for (int64_t d = W - 1; d >= 0; --d) launch_wave(L, b, x, stop, false, d, d == W - 1 ? -1 : d + 1, 1, all, s);
+  return launches + W;
 }
 
 // Coarsest levels of at least this size apply their inverse with the
@@ -638,6 +756,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
   const bool down = pc == PC_DOWN;
   const bool wide = smoother_wide(L.sm);
   int m = opts().sweep;
+  if (m == SWEEP_AUTO && smoother_wave_auto(L.sm)) m = SWEEP_WAVE;
   if (m == SWEEP_AUTO && smoother_flow_auto(L.sm) && L.sm.fl.built) m = SWEEP_FLOW;
   if (m == SWEEP_FLOW && !L.sm.fl.built) m = SWEEP_GRID;  // a DoF in > 2 patches (or not prepared)
   if (m == SWEEP_FLOW) {
@@ -776,7 +895,7 @@ int64_t record_pcg_init(DevLevel& L0, Workspace& w, const double* b, const doubl
 int64_t record_pcg_first(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s) {
   const int* stop = &w.ctl.p->stop;
   int64_t l = record_vcycle(lv, w.r.p, w.z.p, stop, s);
-  k_dot_rz<true><<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, 0);
+  k_dot_rz<true><<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, 0, nullptr, nullptr);
   HC_CHECK_LAUNCH();
   return l + 1;
 }
@@ -793,11 +912,11 @@ int64_t record_pcg_body(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s
   a.cond = cond;
   spmv<EPI_AP>(L0.A, a, s);
   k_pcg_update<<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.x.p, w.r.p, w.p.p, w.Ap.p, w.ctl.p, w.part.p,
-                                                  w.hist.p, cond);
+                                                  w.hist.p, cond, nullptr, nullptr);
   HC_CHECK_LAUNCH();
   int64_t l = 2 + record_vcycle(lv, w.r.p, w.z.p, stop, s);
-  k_dot_rz<false><<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, cond);
-  k_p_update<<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.z.p, w.p.p, w.ctl.p);
+  k_dot_rz<false><<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, cond, nullptr, nullptr);
+  k_p_update<<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.z.p, w.p.p, w.ctl.p, nullptr);
   HC_CHECK_LAUNCH();
   return l + 2;
 }
@@ -874,13 +993,13 @@ void generic_pap(const DCsr& A, Workspace& w, cudaStream_t s) {
 
 void generic_update(Workspace& w, cudaStream_t s) {
   k_pcg_update<<<vec_grid(w.n), kThreads, 0, s>>>(w.zero_flag.p, w.n, w.x.p, w.r.p, w.p.p, w.Ap.p, w.ctl.p,
-                                                  w.part.p, w.hist.p, 0);
+                                                  w.part.p, w.hist.p, 0, nullptr, nullptr);
   HC_CHECK_LAUNCH();
 }
 
 void generic_rz(Workspace& w, bool first, cudaStream_t s) {
-  if (first) k_dot_rz<true><<<vec_grid(w.n), kThreads, 0, s>>>(w.zero_flag.p, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, 0);
-  else k_dot_rz<false><<<vec_grid(w.n), kThreads, 0, s>>>(w.zero_flag.p, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, 0);
+  if (first) k_dot_rz<true><<<vec_grid(w.n), kThreads, 0, s>>>(w.zero_flag.p, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, 0, nullptr, nullptr);
+  else k_dot_rz<false><<<vec_grid(w.n), kThreads, 0, s>>>(w.zero_flag.p, w.n, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, 0, nullptr, nullptr);
   HC_CHECK_LAUNCH();
 }
 
@@ -936,7 +1055,7 @@ void vec_add(int64_t n, const double* a, const double* b, double* out, cudaStrea
 }
 
 void generic_p(Workspace& w, cudaStream_t s) {
-  k_p_update<<<vec_grid(w.n), kThreads, 0, s>>>(w.zero_flag.p, w.n, w.z.p, w.p.p, w.ctl.p);
+  k_p_update<<<vec_grid(w.n), kThreads, 0, s>>>(w.zero_flag.p, w.n, w.z.p, w.p.p, w.ctl.p, nullptr);
   HC_CHECK_LAUNCH();
 }
 
