@@ -248,6 +248,56 @@ int hcamg_dist_connect_ptrs(hcamg_handle* h, void* const* bufs);
 int hcamg_dist_disconnect(hcamg_handle* h);
 int hcamg_dist_info(hcamg_handle* h, int32_t* rank, int32_t* nranks, int32_t* connected, int64_t* buffer_bytes);
 
+/* ---- Subdomain row partition of the sparse regime (the north-star
+ * layout; csrc/rows.cuh).  Every level with at least `min_rows` rows is split by rows
+ * into one subdomain per rank (BFS slabs of A's graph on level 0, coarse rows follow
+ * the fine DoF carrying their largest |P| entry); each rank computes its rows of every
+ * SpMV (multilevel.py:177-184), its patches of every smoother wavefront
+ * (smoothers.py:98-109), its rows of P / P^T and its partial CG dot products
+ * (multilevel.py:238-281), and pushes the entries a neighbour reads next into that
+ * neighbour's vectors over NVLink peer memory; coarser levels are agglomerated (kept
+ * whole and solved redundantly on every rank).  The V-cycle is bit-identical to the
+ * single-GPU per-wavefront V-cycle; PCG differs by the grouping of its dot products.
+ * Protocol as hcamg_dist_*: prepare on every rank, all-gather the 64-byte IPC handles,
+ * connect; vcycle / pcg then are collective.  b, x0 are passed in full by every rank
+ * and x is returned in full to every rank. */
+int hcamg_rows_prepare(hcamg_handle* h, int32_t rank, int32_t nranks, int64_t min_rows, void* ipc_handle,
+                       void** dev_ptr);
+int hcamg_rows_connect(hcamg_handle* h, const void* ipc_handles);
+int hcamg_rows_connect_ptrs(hcamg_handle* h, void* const* bufs);
+int hcamg_rows_disconnect(hcamg_handle* h);
+/* out[0..cap): rank, nranks, connected, split levels, buffer bytes, owned rows and ghost
+ * columns of level 0, then per program segment (V-cycle, PCG init, first, body, gather):
+ * steps, barriers, entries this rank pushes, entries all ranks push. */
+int hcamg_rows_info(hcamg_handle* h, int64_t* out, int32_t cap);
+/* Lockstep emulation of an n-rank partitioned solve on ONE GPU (tests): hs = n handles
+ * of this process holding the same hierarchy, prepared as ranks 0..n-1 and connected with
+ * hcamg_rows_connect_ptrs.  kind 0: z = V(b); kind 1: PCG from x0 = 0.  x: n x n0 doubles,
+ * row r = the full result as rank r holds it.  poison != 0 fills the working vectors with
+ * NaN first (an entry neither computed nor received then shows). */
+int hcamg_rows_emulate(hcamg_handle* const* hs, int32_t n, int32_t kind, const double* b, double* x, double tol,
+                       int64_t maxit, int32_t poison, hcamg_report* report);
+
+/* The partition's planner, host only (no GPU needed; csrc/rows_plan.cu).  Ownership:
+ * owner[u] = rank of row u (BFS slabs of the graph, equal nonzero counts).  Planner: a
+ * symbolic walk over steps; each step lists, per rank, the (vector, entry) pairs it reads
+ * and writes; a read of an entry the rank does not hold becomes a push (producer ->
+ * reader) at the boundary in front of the step (= the step's index). */
+typedef struct hcamg_plan hcamg_plan;
+int hcamg_rows_owner(int64_t n, const int64_t* indptr, const int32_t* indices, int32_t nranks, int8_t* owner);
+int hcamg_plan_create(hcamg_plan** out, int32_t nranks, int32_t nvec, const int64_t* vec_len);
+int hcamg_plan_destroy(hcamg_plan* p);
+/* entries of `vec` are held by the ranks in `holder_mask`; owner != NULL: only by owner[i] */
+int hcamg_plan_set_vector(hcamg_plan* p, int32_t vec, int32_t holder_mask, const int8_t* owner);
+int hcamg_plan_invalidate(hcamg_plan* p, int32_t vec);
+/* nreads / nwrites: per rank counts; rvec / ridx, wvec / widx: the accesses, rank after rank */
+int hcamg_plan_step(hcamg_plan* p, const int64_t* nreads, const int32_t* rvec, const int32_t* ridx,
+                    const int64_t* nwrites, const int32_t* wvec, const int32_t* widx);
+/* counts[0] = push segments, counts[1] = push entries, counts[2] = reads of undefined entries */
+int hcamg_plan_counts(hcamg_plan* p, int64_t* counts);
+/* seg: 5 ints per segment (boundary, src, dst, vec, count); idx: the entries, segment after segment */
+int hcamg_plan_pushes(hcamg_plan* p, int32_t* seg, int32_t* idx);
+
 #ifdef __cplusplus
 }
 #endif

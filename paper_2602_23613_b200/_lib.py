@@ -29,6 +29,9 @@ EXPORTS = [
     "hcamg_dist_prepare", "hcamg_dist_connect", "hcamg_dist_connect_ptrs", "hcamg_dist_disconnect", "hcamg_dist_info",
     "hcamg_set_option", "hcamg_get_option", "hcamg_coarse_solve", "hcamg_solve_status", "hcamg_cholesky_factor",
     "hcamg_smoother_setup", "hcamg_smooth",
+    "hcamg_rows_prepare", "hcamg_rows_connect", "hcamg_rows_connect_ptrs", "hcamg_rows_disconnect", "hcamg_rows_info",
+    "hcamg_rows_emulate", "hcamg_rows_owner", "hcamg_plan_create", "hcamg_plan_destroy", "hcamg_plan_set_vector",
+    "hcamg_plan_invalidate", "hcamg_plan_step", "hcamg_plan_counts", "hcamg_plan_pushes",
 ]
 
 
@@ -124,6 +127,21 @@ def load(required=True):
         "hcamg_cholesky_factor": (C.c_int, [P, C.c_int32, P, P]),
         "hcamg_smoother_setup": (C.c_int, [P, C.POINTER(CSR), C.POINTER(CSR)]),
         "hcamg_smooth": (C.c_int, [P, C.c_int32, C.c_int32, P, P, P]),
+        "hcamg_rows_prepare": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int64, P, C.POINTER(C.c_void_p)]),
+        "hcamg_rows_connect": (C.c_int, [P, P]),
+        "hcamg_rows_connect_ptrs": (C.c_int, [P, P]),
+        "hcamg_rows_disconnect": (C.c_int, [P]),
+        "hcamg_rows_info": (C.c_int, [P, P, C.c_int32]),
+        "hcamg_rows_emulate": (C.c_int, [P, C.c_int32, C.c_int32, P, P, C.c_double, C.c_int64, C.c_int32,
+                                         C.POINTER(Report)]),
+        "hcamg_rows_owner": (C.c_int, [C.c_int64, P, P, C.c_int32, P]),
+        "hcamg_plan_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.c_int32, P]),
+        "hcamg_plan_destroy": (C.c_int, [P]),
+        "hcamg_plan_set_vector": (C.c_int, [P, C.c_int32, C.c_int32, P]),
+        "hcamg_plan_invalidate": (C.c_int, [P, C.c_int32]),
+        "hcamg_plan_step": (C.c_int, [P, P, P, P, P, P, P]),
+        "hcamg_plan_counts": (C.c_int, [P, P]),
+        "hcamg_plan_pushes": (C.c_int, [P, P, P]),
         # debug entry points (not in the public header)
         "hcamg_debug_dist_piece": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, P, P]),
         "hcamg_debug_apply_p": (C.c_int, [P, C.c_int32, C.c_int32, P, P]),

@@ -13,6 +13,7 @@
 #include "../../include/hcamg.h"
 #include "dense.cuh"
 #include "dist.cuh"
+#include "rows_dev.cuh"
 #include "giant.cuh"
 #include "kuhn.cuh"
 #include "interp.cuh"
@@ -63,6 +64,8 @@ struct hcamg_handle {
   SplitResult last_split;
   // row-partitioned solve across processes (dist.cuh)
   Dist dist;
+  // subdomain row partition of the sparse regime (rows.cuh)
+  std::unique_ptr<RowsCtx> rows;
   // last hcamg_kuhn_assemble result (kuhn.cuh)
   DCsr kuhn_A, kuhn_G;
   std::vector<int64_t> kuhn_fe, kuhn_fv;
@@ -86,8 +89,24 @@ void invalidate(hcamg_handle* h) {
   h->graph_maxit = -1;
 }
 
+bool rows_on(const hcamg_handle* h) { return h->rows && h->rows->on; }
+
+void drop_rows(hcamg_handle* h) {
+  if (!h->rows) return;
+  // the level / workspace vectors point into the partition's symmetric buffer
+  std::vector<DevLevel*> lv;
+  for (auto& l : h->levels) lv.push_back(l.get());
+  rows_detach(*h->rows, lv, h->ws, h->stream);
+  h->rows.reset();
+}
+
 void refresh_views(hcamg_handle* h) {
   h->dist.release();  // a new hierarchy needs a new exchange layout
+  if (h->rows) {      // the old levels are gone: nothing to re-point
+    for (DBuf<double>* v : {&h->ws.x, &h->ws.r, &h->ws.z, &h->ws.p, &h->ws.Ap, &h->ws.b})
+      if (v->view) { v->release(); h->ws.n = -1; }
+    h->rows.reset();
+  }
   h->lv.clear();
   for (auto& l : h->levels) h->lv.push_back(l.get());
 }
@@ -336,8 +355,10 @@ void build_loop_graph(hcamg_handle* h, Graph& G, bool pcg) {
                                         : cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault);
   if (ce == cudaSuccess) {
     HC_CUDA(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    int64_t lp = pcg ? record_pcg_init(*h->lv[0], w, b, nullptr, s, 0) + record_pcg_first(h->lv, w, s)
-                     : record_amg_init(*h->lv[0], w, b, nullptr, s, 0);
+    int64_t lp = rows_on(h) ? rows_record(*h->rows, SEG_INIT, h->lv, w, &w.ctl.p->stop, 0, s) +
+                                  rows_record(*h->rows, SEG_FIRST, h->lv, w, &w.ctl.p->stop, 0, s)
+                 : pcg ? record_pcg_init(*h->lv[0], w, b, nullptr, s, 0) + record_pcg_first(h->lv, w, s)
+                       : record_amg_init(*h->lv[0], w, b, nullptr, s, 0);
     cudaStreamCaptureStatus st;
     const cudaGraphNode_t* deps = nullptr;
     size_t nd = 0;
@@ -354,7 +375,8 @@ void build_loop_graph(hcamg_handle* h, Graph& G, bool pcg) {
     HC_CUDA(cudaStreamUpdateCaptureDependencies(s, &cn, 1, cudaStreamSetCaptureDependencies));
     HC_CUDA(cudaStreamBeginCaptureToGraph(s2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     const unsigned long long hc = (unsigned long long)cond;
-    int64_t lb = pcg ? record_pcg_body(h->lv, w, s2, hc) : record_amg_body(h->lv, w, s2, hc);
+    int64_t lb = rows_on(h) ? rows_record(*h->rows, SEG_BODY, h->lv, w, &w.ctl.p->stop, hc, s2)
+                 : pcg ? record_pcg_body(h->lv, w, s2, hc) : record_amg_body(h->lv, w, s2, hc);
     HC_CUDA(cudaStreamEndCapture(s2, &body));
     cudaGraph_t gout = nullptr;
     HC_CUDA(cudaStreamEndCapture(s, &gout));
@@ -375,11 +397,14 @@ void build_loop_graph(hcamg_handle* h, Graph& G, bool pcg) {
   // fallback: host-driven loop over a body graph
   cudaGraph_t gp = nullptr, gb = nullptr;
   HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  G.launches_pre = pcg ? record_pcg_init(*h->lv[0], w, b, nullptr, s, 0) + record_pcg_first(h->lv, w, s)
-                       : record_amg_init(*h->lv[0], w, b, nullptr, s, 0);
+  G.launches_pre = rows_on(h) ? rows_record(*h->rows, SEG_INIT, h->lv, w, &w.ctl.p->stop, 0, s) +
+                                    rows_record(*h->rows, SEG_FIRST, h->lv, w, &w.ctl.p->stop, 0, s)
+                   : pcg ? record_pcg_init(*h->lv[0], w, b, nullptr, s, 0) + record_pcg_first(h->lv, w, s)
+                         : record_amg_init(*h->lv[0], w, b, nullptr, s, 0);
   HC_CUDA(cudaStreamEndCapture(s, &gp));
   HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  G.launches_body = pcg ? record_pcg_body(h->lv, w, s, 0) : record_amg_body(h->lv, w, s, 0);
+  G.launches_body = rows_on(h) ? rows_record(*h->rows, SEG_BODY, h->lv, w, &w.ctl.p->stop, 0, s)
+                    : pcg ? record_pcg_body(h->lv, w, s, 0) : record_amg_body(h->lv, w, s, 0);
   HC_CUDA(cudaStreamEndCapture(s, &gb));
   HC_CUDA(cudaGraphInstantiate(&G.pre, gp, 0));
   HC_CUDA(cudaGraphInstantiate(&G.body, gb, 0));
@@ -456,6 +481,16 @@ int guarded(hcamg_handle* h, F&& f) {
 // Distributed solve: a consumer that waited ~60 s for a peer flags the
 // handle (the solve then finishes on stale data); report it as an error.
 void check_dist(hcamg_handle* h) {
+  if (rows_on(h)) {
+    int e = 0;
+    HC_CUDA(cudaMemcpyAsync(&e, h->rows->err.p, sizeof e, cudaMemcpyDeviceToHost, h->stream));
+    HC_CUDA(cudaStreamSynchronize(h->stream));
+    if (e) {
+      h->rows->err.zero();
+      throw Error(ECUDA_, e == 2 ? "row partition: a peer rank had not reached the boundary (lockstep emulation)"
+                                 : "row partition: timed out waiting for a peer rank at a boundary");
+    }
+  }
   if (!h->dist.on) return;
   int e = 0;
   HC_CUDA(cudaMemcpyAsync(&e, h->dist.err.p, sizeof e, cudaMemcpyDeviceToHost, h->stream));
@@ -532,6 +567,7 @@ void hcamg_destroy(hcamg_handle* h) {
   h->ws = Workspace();
   h->vc_b.release();
   h->vc_x.release();
+  if (h->rows) drop_rows(h);
   h->dist.release();
   h->dist.ep.release();
   h->dist.cta.release();
@@ -1012,7 +1048,8 @@ int hcamg_vcycle(hcamg_handle* h, const double* b, const double* x_or_null, doub
     if (!h->g_vc.exec) {
       cudaGraph_t g;
       HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-      h->g_vc.launches_pre = record_vcycle(h->lv, h->ws.r.p, h->ws.z.p, h->ws.zero_flag.p, s);
+      h->g_vc.launches_pre = rows_on(h) ? rows_record(*h->rows, SEG_VCYCLE, h->lv, h->ws, h->ws.zero_flag.p, 0, s)
+                                        : record_vcycle(h->lv, h->ws.r.p, h->ws.z.p, h->ws.zero_flag.p, s);
       HC_CUDA(cudaStreamEndCapture(s, &g));
       HC_CUDA(cudaGraphInstantiate(&h->g_vc.exec, g, 0));
       cudaGraphDestroy(g);
@@ -1048,6 +1085,7 @@ static int pcg_impl(hcamg_handle* h, const double* b, bool b_dev, const double* 
     set_ctl(h, tol, maxit);
     run_loop_graph(h, h->g_pcg);
     zero_x_if_zero_rhs(h->ws, s);
+    if (rows_on(h)) rows_record(*h->rows, SEG_GATHER, h->lv, h->ws, h->ws.zero_flag.p, 0, s);  // every rank gets all of x
     HC_CUDA(cudaMemcpyAsync(x, h->ws.x.p, 8 * n, x_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     if (!sync && !report && !history) return;  // errors deferred: hcamg_solve_status
     int error = 0;
@@ -1077,6 +1115,7 @@ int hcamg_amg_solve(hcamg_handle* h, const double* b, const double* x0, double t
   return guarded(h, [&] {
     require_hierarchy(h);
     require(tol > 0, "tolerance must be positive");
+    if (rows_on(h)) throw Error(EUNSUPPORTED_, "amg_solve is not partitioned by rows; use pcg / vcycle");
     cudaStream_t s = h->stream;
     const int64_t n = h->levels[0]->n;
     prepare_loop(h, h->g_amg, false, maxit);
@@ -1430,6 +1469,312 @@ int hcamg_debug_apply_p(hcamg_handle* h, int32_t level, int32_t kind, const doub
     }
     HC_CUDA(cudaStreamSynchronize(s));
   });
+}
+
+
+// ---- subdomain row partition (rows.cuh)
+
+int hcamg_rows_prepare(hcamg_handle* h, int32_t rank, int32_t nranks, int64_t min_rows, void* ipc_handle,
+                       void** dev_ptr) {
+  return guarded(h, [&] {
+    require_hierarchy(h);
+    cudaStream_t s = h->stream;
+    HC_CUDA(cudaStreamSynchronize(s));
+    if (h->rows) drop_rows(h);
+    h->dist.release();
+    for (DevLevel* L : h->lv) L->dist = nullptr;
+    ensure_ws(h, 1);
+    invalidate(h);
+    h->rows.reset(new RowsCtx());
+    try {
+      rows_prepare(*h->rows, h->lv, h->ws, rank, nranks, min_rows, s);
+    } catch (...) {
+      drop_rows(h);
+      throw;
+    }
+    if (ipc_handle) {
+      cudaIpcMemHandle_t mh;
+      HC_CUDA(cudaIpcGetMemHandle(&mh, h->rows->sym));
+      memcpy(ipc_handle, &mh, sizeof mh);
+    }
+    if (dev_ptr) *dev_ptr = h->rows->sym;
+  });
+}
+
+int hcamg_rows_connect(hcamg_handle* h, const void* ipc_handles) {
+  return guarded(h, [&] {
+    require(h->rows && h->rows->sym, "hcamg_rows_prepare must be called first");
+    require(ipc_handles != nullptr, "missing peer handles");
+    RowsCtx& rc = *h->rows;
+    for (int r = 0; r < rc.nranks; ++r) {
+      if (r == rc.rank) {
+        rc.base[r] = rc.sym;
+        continue;
+      }
+      cudaIpcMemHandle_t mh;
+      memcpy(&mh, static_cast<const char*>(ipc_handles) + (size_t)r * sizeof mh, sizeof mh);
+      void* p = nullptr;
+      HC_CUDA(cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess));
+      rc.base[r] = static_cast<char*>(p);
+      rc.opened[r] = true;
+    }
+    rc.on = true;
+    invalidate(h);
+  });
+}
+
+int hcamg_rows_connect_ptrs(hcamg_handle* h, void* const* bufs) {
+  return guarded(h, [&] {
+    require(h->rows && h->rows->sym, "hcamg_rows_prepare must be called first");
+    require(bufs != nullptr, "missing peer buffers");
+    RowsCtx& rc = *h->rows;
+    for (int r = 0; r < rc.nranks; ++r) {
+      require(bufs[r] != nullptr, "null peer buffer");
+      rc.base[r] = static_cast<char*>(bufs[r]);
+    }
+    require(rc.base[rc.rank] == rc.sym, "bufs[rank] must be this handle's own buffer");
+    rc.on = true;
+    invalidate(h);
+  });
+}
+
+int hcamg_rows_disconnect(hcamg_handle* h) {
+  return guarded(h, [&] {
+    HC_CUDA(cudaStreamSynchronize(h->stream));
+    if (h->rows) drop_rows(h);
+    invalidate(h);
+  });
+}
+
+// out[0..]: rank, nranks, connected, split levels, buffer bytes, owned rows of
+// level 0, ghost columns of level 0, then per segment (V-cycle, init, first,
+// body, gather): steps, barriers, entries this rank pushes, entries all ranks push
+int hcamg_rows_info(hcamg_handle* h, int64_t* out, int32_t cap) {
+  return guarded(h, [&] {
+    require(h->rows != nullptr, "no row partition on this handle");
+    const RowsCtx& rc = *h->rows;
+    std::vector<int64_t> v = {rc.rank, rc.nranks, rc.on ? 1 : 0, rc.stats.split_levels, (int64_t)rc.sym_bytes,
+                              rc.stats.own_rows0, rc.stats.ghost_rows0};
+    for (int g = 0; g < SEG_COUNT; ++g) {
+      v.push_back(rc.stats.boundaries[g]);
+      v.push_back(rc.stats.barriers[g]);
+      v.push_back(rc.stats.push_out[g]);
+      v.push_back(rc.stats.push_all[g]);
+    }
+    for (int32_t i = 0; i < cap && i < (int32_t)v.size(); ++i) out[i] = v[(size_t)i];
+  });
+}
+
+namespace {
+
+struct HandleScope {  // what guarded() installs, for a loop over several handles
+  OptionsScope os;
+  PoolScope ps;
+  explicit HandleScope(hcamg_handle* h) : os(&h->opts), ps(h->pool) {}
+};
+
+// every rank's boundary k (push + signal), then every rank's check + step k:
+// no kernel ever waits for a kernel that has not run
+void lockstep(hcamg_handle* const* hs, int n, int g, bool use_stop) {
+  const size_t steps = hs[0]->rows->seg[g].size();
+  for (size_t k = 0; k < steps; ++k) {
+    for (int r = 0; r < n; ++r) {
+      HandleScope sc(hs[r]);
+      const int* stop = use_stop ? &hs[r]->ws.ctl.p->stop : hs[r]->ws.zero_flag.p;
+      rows_boundary(*hs[r]->rows, g, k, stop, false, hs[r]->stream);
+    }
+    HC_CUDA(cudaDeviceSynchronize());
+    for (int r = 0; r < n; ++r) {
+      HandleScope sc(hs[r]);
+      const int* stop = use_stop ? &hs[r]->ws.ctl.p->stop : hs[r]->ws.zero_flag.p;
+      const int32_t b = hs[r]->rows->seg_boundary[g][k];
+      if (hs[r]->rows->barrier[(size_t)b]) rows_wait(*hs[r]->rows, stop, hs[r]->stream);
+      rows_launch_step(hs[r]->rows->seg[g][k], *hs[r]->rows, hs[r]->lv, hs[r]->ws, stop, 0, hs[r]->stream);
+    }
+    HC_CUDA(cudaDeviceSynchronize());
+  }
+}
+
+}  // namespace
+
+// Lockstep emulation of an n-rank partitioned solve on ONE GPU (tests): hs are
+// n handles of this process holding the same hierarchy, prepared as ranks
+// 0..n-1 and connected with each other's buffers (hcamg_rows_connect_ptrs).
+// kind 0: V-cycle z = V(b); kind 1: PCG from x0 = 0.  b: n0 doubles (host);
+// x: n x n0 doubles (host), row r = the full result as rank r holds it.
+// `poison` != 0 fills every working vector with NaN first, so an entry that
+// was neither computed nor received shows up in the result.
+int hcamg_rows_emulate(hcamg_handle* const* hs, int32_t n, int32_t kind, const double* b, double* x, double tol,
+                       int64_t maxit, int32_t poison, hcamg_report* report) {
+  if (!hs || n < 1 || !hs[0]) return HCAMG_EINVAL;
+  return guarded(hs[0], [&] {
+    for (int r = 0; r < n; ++r) {
+      require(hs[r] && rows_on(hs[r]), "every handle must hold a connected row partition");
+      require(hs[r]->rows->nranks == n && hs[r]->rows->rank == r, "handles must be ranks 0..n-1 of an n-rank partition");
+      require(hs[r]->device == hs[0]->device, "lockstep emulation runs on one GPU");
+    }
+    const int64_t n0 = hs[0]->levels[0]->n;
+    for (int r = 0; r < n; ++r) {
+      HandleScope sc(hs[r]);
+      hcamg_handle* h = hs[r];
+      ensure_ws(h, std::max<int64_t>(maxit, 1));
+      cudaStream_t s = h->stream;
+      if (poison) {
+        RowsCtx& rc = *h->rows;
+        HC_CUDA(cudaMemsetAsync(rc.sym + kRowsFlagBytes, 0xff, rc.sym_bytes - kRowsFlagBytes, s));
+      }
+      if (kind == 0) {
+        HC_CUDA(cudaMemcpyAsync(h->ws.r.p, b, 8 * n0, cudaMemcpyHostToDevice, s));
+      } else {
+        HC_CUDA(cudaMemcpyAsync(h->ws.b.p, b, 8 * n0, cudaMemcpyHostToDevice, s));
+        h->ws.x.zero();
+        set_ctl(h, tol, maxit);
+      }
+    }
+    HC_CUDA(cudaDeviceSynchronize());
+    if (kind == 0) {
+      lockstep(hs, n, SEG_VCYCLE, false);
+      for (int r = 0; r < n; ++r)
+        HC_CUDA(cudaMemcpy(x + (size_t)r * n0, hs[r]->ws.z.p, 8 * n0, cudaMemcpyDeviceToHost));
+    } else {
+      lockstep(hs, n, SEG_INIT, true);
+      lockstep(hs, n, SEG_FIRST, true);
+      while (true) {
+        int stop0 = read_scalar(&hs[0]->ws.ctl.p->stop, hs[0]->stream);
+        for (int r = 1; r < n; ++r)
+          require(read_scalar(&hs[r]->ws.ctl.p->stop, hs[r]->stream) == stop0, "ranks disagree on convergence");
+        if (stop0) break;
+        lockstep(hs, n, SEG_BODY, true);
+      }
+      for (int r = 0; r < n; ++r) {
+        HandleScope sc(hs[r]);
+        zero_x_if_zero_rhs(hs[r]->ws, hs[r]->stream);
+      }
+      HC_CUDA(cudaDeviceSynchronize());
+      lockstep(hs, n, SEG_GATHER, false);
+      for (int r = 0; r < n; ++r)
+        HC_CUDA(cudaMemcpy(x + (size_t)r * n0, hs[r]->ws.x.p, 8 * n0, cudaMemcpyDeviceToHost));
+      int error = 0;
+      hcamg_report rep{};
+      read_report(hs[0], &rep, &error);
+      for (int r = 1; r < n; ++r) {
+        int e2 = 0;
+        hcamg_report r2{};
+        read_report(hs[r], &r2, &e2);
+        require(r2.iterations == rep.iterations && r2.final_relres == rep.final_relres,
+                "ranks disagree on the iteration count / residual");
+      }
+      pcg_breakdown(hs[0], error);
+      if (report) *report = rep;
+    }
+    for (int r = 0; r < n; ++r) check_dist(hs[r]);
+  });
+}
+
+
+// ---- the partition's planner as a host-only API (no device call below)
+
+struct hcamg_plan {
+  PlanState st;
+  PlanResult out;
+  int32_t steps = 0;
+};
+
+int hcamg_rows_owner(int64_t n, const int64_t* indptr, const int32_t* indices, int32_t nranks, int8_t* owner) {
+  if (n < 0 || !indptr || (!indices && n > 0 && indptr[n] > 0) || nranks < 1 || nranks > kRowsMaxRanks || !owner)
+    return HCAMG_EINVAL;
+  try {
+    std::vector<int8_t> o;
+    rows_bfs_owner(n, indptr, indices, nranks, o);
+    memcpy(owner, o.data(), (size_t)n);
+    return HCAMG_OK;
+  } catch (...) {
+    return HCAMG_ENOMEM;
+  }
+}
+
+int hcamg_plan_create(hcamg_plan** out, int32_t nranks, int32_t nvec, const int64_t* vec_len) {
+  if (!out || nranks < 1 || nranks > kRowsMaxRanks || nvec < 1 || !vec_len) return HCAMG_EINVAL;
+  try {
+    std::unique_ptr<hcamg_plan> p(new hcamg_plan());
+    p->st.init(nranks, std::vector<int64_t>(vec_len, vec_len + nvec));
+    *out = p.release();
+    return HCAMG_OK;
+  } catch (...) {
+    return HCAMG_ENOMEM;
+  }
+}
+
+int hcamg_plan_destroy(hcamg_plan* p) {
+  delete p;
+  return HCAMG_OK;
+}
+
+int hcamg_plan_set_vector(hcamg_plan* p, int32_t vec, int32_t holder_mask, const int8_t* owner) {
+  if (!p || vec < 0 || vec + 1 >= (int32_t)p->st.vec_off.size()) return HCAMG_EINVAL;
+  p->st.set_vector(vec, (uint8_t)holder_mask, owner);
+  return HCAMG_OK;
+}
+
+int hcamg_plan_invalidate(hcamg_plan* p, int32_t vec) {
+  if (!p || vec < 0 || vec + 1 >= (int32_t)p->st.vec_off.size()) return HCAMG_EINVAL;
+  p->st.invalidate_vector(vec);
+  return HCAMG_OK;
+}
+
+int hcamg_plan_step(hcamg_plan* p, const int64_t* nreads, const int32_t* rvec, const int32_t* ridx,
+                    const int64_t* nwrites, const int32_t* wvec, const int32_t* widx) {
+  if (!p || !nreads || !nwrites) return HCAMG_EINVAL;
+  try {
+    const int N = p->st.nranks;
+    const int nvec = (int)p->st.vec_off.size() - 1;
+    std::vector<PlanAccess> acc((size_t)N);
+    int64_t ro = 0, wo = 0;
+    for (int q = 0; q < N; ++q) {
+      PlanAccess& a = acc[(size_t)q];
+      for (int64_t k = 0; k < nreads[q]; ++k) {
+        const int32_t v = rvec[ro + k], i = ridx[ro + k];
+        if (v < 0 || v >= nvec || i < 0 || i >= p->st.vec_off[(size_t)v + 1] - p->st.vec_off[(size_t)v]) return HCAMG_EINVAL;
+        a.rvec.push_back(v);
+        a.ridx.push_back(i);
+      }
+      for (int64_t k = 0; k < nwrites[q]; ++k) {
+        const int32_t v = wvec[wo + k], i = widx[wo + k];
+        if (v < 0 || v >= nvec || i < 0 || i >= p->st.vec_off[(size_t)v + 1] - p->st.vec_off[(size_t)v]) return HCAMG_EINVAL;
+        a.wvec.push_back(v);
+        a.widx.push_back(i);
+      }
+      ro += nreads[q];
+      wo += nwrites[q];
+    }
+    plan_step(p->st, p->steps, p->steps, acc, p->out);
+    ++p->steps;
+    return HCAMG_OK;
+  } catch (...) {
+    return HCAMG_ENOMEM;
+  }
+}
+
+int hcamg_plan_counts(hcamg_plan* p, int64_t* counts) {
+  if (!p || !counts) return HCAMG_EINVAL;
+  counts[0] = (int64_t)p->out.segs.size();
+  counts[1] = (int64_t)p->out.idx.size();
+  counts[2] = p->out.unheld_reads;
+  return HCAMG_OK;
+}
+
+int hcamg_plan_pushes(hcamg_plan* p, int32_t* seg, int32_t* idx) {
+  if (!p || (!seg && !p->out.segs.empty()) || (!idx && !p->out.idx.empty())) return HCAMG_EINVAL;
+  for (size_t k = 0; k < p->out.segs.size(); ++k) {
+    const PushSeg& s = p->out.segs[k];
+    seg[5 * k] = s.boundary;
+    seg[5 * k + 1] = s.src;
+    seg[5 * k + 2] = s.dst;
+    seg[5 * k + 3] = s.vec;
+    seg[5 * k + 4] = (int32_t)(s.end - s.begin);
+  }
+  if (!p->out.idx.empty()) memcpy(idx, p->out.idx.data(), p->out.idx.size() * sizeof(int32_t));
+  return HCAMG_OK;
 }
 
 }  // extern "C"

@@ -144,10 +144,8 @@ void rows_bfs_owner(int64_t n, const int64_t* ptr, const int32_t* idx, int nrank
     bfs_levels(n, ptr, idx, start, lev, order);
     // deepest level of the start's own component: the last DoF reached before another seed was needed
     int32_t best = order[0];
-    for (int32_t u : order) {
+    for (int32_t u : order)
       if (lev[(size_t)u] >= lev[(size_t)best]) best = u;
-      else if (lev[(size_t)u] < lev[(size_t)best] - 0 && false) break;
-    }
     start = best;
   }
   bfs_levels(n, ptr, idx, start, lev, order);

@@ -18,6 +18,7 @@
 
 #include <algorithm>
 
+#include "rows_dev.cuh"
 #include "solve.cuh"
 #include "sweep.cuh"
 #include <cstdlib>
@@ -955,6 +956,167 @@ int64_t record_amg_body(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s
   a.cond = cond;
   spmv<EPI_AMG_RES>(lv[0]->A, a, s);
   return l + 2;
+}
+
+// ----------------------------------------------------------------------------- subdomain row partition (rows.cuh)
+
+static_assert(RE_SET == EPI_SET && RE_ADD == EPI_ADD && RE_JAC_FW == EPI_JAC_FW && RE_RES_JAC == EPI_RES_JAC &&
+                  RE_JAC_BW == EPI_JAC_BW && RE_AP == EPI_AP && RE_PCG_INIT == EPI_PCG_INIT,
+              "rows.cuh REpi mirrors Epi");
+
+// One step of the partitioned program on this rank: the single-GPU kernel on
+// the rank's row list / patch list (or on everything, for agglomerated levels).
+int64_t rows_launch_step(const RStep& st, RowsCtx& rc, std::vector<DevLevel*>& lv, Workspace& w, const int* stop,
+                         unsigned long long cond, cudaStream_t s) {
+  const int depth = rc.depth, N = rc.nranks;
+  double* red_base = rc.vec(rows_vec_red(depth));
+  auto red = [&](int site) { return red_base + (int64_t)site * 2 * N + 2 * rc.rank; };
+  const RowsLevelDev& D0 = rc.lev[0];
+  switch (st.kind) {
+    case RK_GATHER:
+      return 0;
+    case RK_FINISH:
+      k_finish<<<1, 32, 0, s>>>(stop, st.site, w.ctl.p, red_base + (int64_t)st.site * 2 * N, N, w.hist.p, cond);
+      HC_CHECK_LAUNCH();
+      return 1;
+    case RK_PCG_UPDATE: {
+      const int64_t cnt = D0.split ? D0.nrows : w.n;
+      k_pcg_update<<<vec_grid(cnt), kThreads, 0, s>>>(stop, cnt, w.x.p, w.r.p, w.p.p, w.Ap.p, w.ctl.p, w.part.p,
+                                                      w.hist.p, cond, D0.split ? D0.rows.p : nullptr, red(st.site));
+      HC_CHECK_LAUNCH();
+      return 1;
+    }
+    case RK_DOT_RZ: {
+      const int64_t cnt = D0.split ? D0.nrows : w.n;
+      const int32_t* rows = D0.split ? D0.rows.p : nullptr;
+      if (st.site == RS_RZ_FIRST)
+        k_dot_rz<true><<<vec_grid(cnt), kThreads, 0, s>>>(stop, cnt, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, cond,
+                                                          rows, red(st.site));
+      else
+        k_dot_rz<false><<<vec_grid(cnt), kThreads, 0, s>>>(stop, cnt, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, cond,
+                                                           rows, red(st.site));
+      HC_CHECK_LAUNCH();
+      return 1;
+    }
+    case RK_P_UPDATE: {
+      const int64_t cnt = D0.split ? D0.nrows : w.n;
+      k_p_update<<<vec_grid(cnt), kThreads, 0, s>>>(stop, cnt, w.z.p, w.p.p, w.ctl.p, D0.split ? D0.rows.p : nullptr);
+      HC_CHECK_LAUNCH();
+      return 1;
+    }
+    default:
+      break;
+  }
+  DevLevel& L = *lv[(size_t)st.level];
+  const RowsLevelDev& D = rc.lev[(size_t)st.level];
+  const double* b = st.level == 0 ? w.r.p : L.b.p;
+  double* x = st.level == 0 ? w.z.p : L.x.p;
+  switch (st.kind) {
+    case RK_COARSE:
+      return record_piece(PC_COARSE, L, nullptr, b, x, stop, s);
+    case RK_INIT_RB: {
+      const int64_t cnt = D.split ? D.nrows : L.n;
+      k_init_rb<<<vec_grid(cnt), kThreads, 0, s>>>(stop, cnt, b, L.r.p, x, D.split ? D.rows.p : nullptr);
+      HC_CHECK_LAUNCH();
+      return 1;
+    }
+    case RK_FW_FINAL:
+      launch_fw_final(L, x, stop, D.split ? D.rows.p : nullptr, D.nrows, s);
+      return 1;
+    case RK_WAVE: {
+      WaveShare sh{};
+      if (D.split) {
+        const int64_t p0 = D.poff[(size_t)st.dst], p1 = D.poff[(size_t)st.dst + 1];
+        sh.plist = D.plist.p + p0;
+        sh.np = p1 - p0;
+        if (st.init) {
+          sh.rows = D.rows.p;
+          sh.nrows = D.nrows;
+        } else if (st.src >= 0) {
+          const int64_t g0 = D.goff[st.dir][(size_t)st.src], g1 = D.goff[st.dir][(size_t)st.src + 1];
+          sh.gen = D.gen[st.dir].p + g0;
+          sh.ngen = g1 - g0;
+        }
+      }
+      launch_wave(L, b, x, stop, st.init, st.dst, st.src, st.dir, sh, s);
+      return 1;
+    }
+    case RK_SPMV: {
+      SpmvArgs a{};
+      a.stop = stop;
+      if (st.epi == RE_AP || st.epi == RE_PCG_INIT) {
+        DevLevel& L0 = *lv[0];
+        a.ctl = w.ctl.p;
+        a.part = w.part.p;
+        a.part2 = w.part2.p;
+        a.red = red(st.site);
+        if (D0.split) {
+          a.rows = D0.rows.p;
+          a.nrows = D0.nrows;
+        }
+        if (st.epi == RE_AP) {
+          a.xin = w.p.p;
+          a.y = w.Ap.p;
+          a.cond = cond;
+          spmv<EPI_AP>(L0.A, a, s);
+        } else {
+          a.xin = w.x.p;
+          a.y = w.r.p;
+          a.b = w.b.p;
+          spmv<EPI_PCG_INIT>(L0.A, a, s);
+        }
+        return 1;
+      }
+      if (st.mat == 2) {  // b_c = P^T r: rows of the coarser level
+        DevLevel& C = *lv[(size_t)st.level + 1];
+        const RowsLevelDev& DC = rc.lev[(size_t)st.level + 1];
+        if (D.split) {
+          a.rows = DC.rows.p;
+          a.nrows = DC.nrows;
+        }
+        a.xin = L.r.p;
+        a.y = C.b.p;
+        if (!D.split && L.pt_seg.nseg) {
+          launch_segmented(stop, L.Pt, L.pt_seg, L.r.p, C.b.p, s);
+          return 2;
+        }
+        spmv<EPI_SET>(L.Pt, a, s);
+        return 1;
+      }
+      if (D.split) {
+        a.rows = D.rows.p;
+        a.nrows = D.nrows;
+      }
+      if (st.mat == 1) {  // x += P x_c
+        DevLevel& C = *lv[(size_t)st.level + 1];
+        a.xin = C.x.p;
+        a.y = x;
+        spmv<EPI_ADD>(L.P, a, s);
+        return 1;
+      }
+      if (st.epi == RE_JAC_FW) {
+        a.xin = L.dj.p;
+        a.y = L.r.p;
+        spmv<EPI_JAC_FW>(L.A, a, s);
+      } else if (st.epi == RE_RES_JAC) {
+        a.xin = x;
+        a.y = L.r.p;
+        a.b = b;
+        a.l1 = L.l1.p;
+        a.dj = L.dj.p;
+        spmv<EPI_RES_JAC>(L.A, a, s);
+      } else {
+        a.xin = L.dj.p;
+        a.y = L.r.p;
+        a.dj = L.dj.p;
+        a.x = x;
+        spmv<EPI_JAC_BW>(L.A, a, s);
+      }
+      return 1;
+    }
+    default:
+      return 0;
+  }
 }
 
 // ----------------------------------------------------------------------------- generic PCG helpers

@@ -124,3 +124,173 @@ def info(h):
     r, n, c, b = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int64()
     dev.check(dev.lib.hcamg_dist_info(dev.h, C.byref(r), C.byref(n), C.byref(c), C.byref(b)))
     return r.value, n.value, bool(c.value), b.value
+
+
+# ----------------------------------------------------------------------------------------------
+# Subdomain row partition of the sparse regime (the north-star layout, csrc/rows.cuh)
+# ----------------------------------------------------------------------------------------------
+
+SEGMENTS = ("vcycle", "pcg_init", "pcg_first", "pcg_body", "gather")
+
+
+def distribute_rows(h, group=None, min_rows=16384):
+    """Partition the solve of ``h`` by rows over ``group`` (torch.distributed).
+
+    Every level with at least ``min_rows`` rows is split into one subdomain per
+    rank; coarser levels are agglomerated (every rank keeps them whole).  Every
+    rank must have built ``h`` from the same system; afterwards ``vcycle`` and
+    ``pcg`` on ``h`` are collective.  Each rank passes the full right-hand side
+    and receives the full solution."""
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = _device_for(h)
+    handle = (C.c_char * IPC_HANDLE_BYTES)()
+    dptr = C.c_void_p()
+    dev.check(dev.lib.hcamg_rows_prepare(dev.h, rank, world, int(min_rows), handle, C.byref(dptr)))
+    allh = exchange_handles(bytes(handle), group)
+    buf = C.create_string_buffer(allh, len(allh))
+    dev.check(dev.lib.hcamg_rows_connect(dev.h, buf))
+    h._dist = (rank, world)
+    return h
+
+
+def undistribute_rows(h):
+    dev = _device_for(h)
+    dev.check(dev.lib.hcamg_rows_disconnect(dev.h))
+    h._dist = None
+    return h
+
+
+def rows_info(h):
+    """Partition statistics of ``h``'s handle (hcamg_rows_info)."""
+    import numpy as np
+
+    dev = _device_for(h)
+    out = np.zeros(7 + 4 * len(SEGMENTS), dtype=np.int64)
+    dev.check(dev.lib.hcamg_rows_info(dev.h, out.ctypes.data, len(out)))
+    info = dict(rank=int(out[0]), nranks=int(out[1]), connected=bool(out[2]), split_levels=int(out[3]),
+                buffer_bytes=int(out[4]), own_rows0=int(out[5]), ghost_cols0=int(out[6]), segments={})
+    for g, name in enumerate(SEGMENTS):
+        s = out[7 + 4 * g: 11 + 4 * g]
+        info["segments"][name] = dict(steps=int(s[0]), barriers=int(s[1]), push_out=int(s[2]), push_all=int(s[3]))
+    return info
+
+
+def emulate_rows(hs, b, kind="vcycle", tol=1e-8, maxit=500, min_rows=64, poison=True):
+    """Lockstep emulation of a ``len(hs)``-rank partitioned solve on ONE GPU.
+
+    ``hs``: hierarchies built from the same system on the same device (one
+    handle each).  Prepares them as ranks 0..n-1, connects them through raw
+    device pointers and runs the step program rank after rank (every rank's
+    boundary push, then every rank's kernel), so no kernel waits for one that
+    has not run.  Returns (X, report): X[r] = the full result as rank r holds
+    it; report is None for a V-cycle."""
+    import numpy as np
+    from . import _lib
+
+    n = len(hs)
+    devs = [_device_for(h) for h in hs]
+    ptrs = []
+    for r, dev in enumerate(devs):
+        p = C.c_void_p()
+        dev.check(dev.lib.hcamg_rows_prepare(dev.h, r, n, int(min_rows), None, C.byref(p)))
+        ptrs.append(p.value)
+    arr = (C.c_void_p * n)(*ptrs)
+    for dev in devs:
+        dev.check(dev.lib.hcamg_rows_connect_ptrs(dev.h, arr))
+    handles = (C.c_void_p * n)(*[dev.h for dev in devs])
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    X = np.empty((n, b.shape[0]))
+    rep = _lib.Report()
+    devs[0].check(devs[0].lib.hcamg_rows_emulate(handles, n, 0 if kind == "vcycle" else 1, b.ctypes.data,
+                                                 X.ctypes.data, float(tol), int(maxit), 1 if poison else 0,
+                                                 C.byref(rep)))
+    return X, (None if kind == "vcycle" else rep)
+
+
+class Plan:
+    """The partition's dataflow planner (host only; csrc/rows_plan.cu)."""
+
+    def __init__(self, nranks, vec_len):
+        import numpy as np
+        from . import _lib
+
+        self.lib = _lib.load()
+        self.nranks = int(nranks)
+        lens = np.ascontiguousarray(vec_len, dtype=np.int64)
+        self.p = C.c_void_p()
+        rc = self.lib.hcamg_plan_create(C.byref(self.p), self.nranks, len(lens), lens.ctypes.data)
+        if rc != 0:
+            raise ValueError("hcamg_plan_create failed")
+
+    def close(self):
+        if self.p:
+            self.lib.hcamg_plan_destroy(self.p)
+            self.p = None
+
+    __del__ = close
+
+    def set_vector(self, vec, mask, owner=None):
+        import numpy as np
+
+        o = None if owner is None else np.ascontiguousarray(owner, dtype=np.int8)
+        if self.lib.hcamg_plan_set_vector(self.p, int(vec), int(mask), None if o is None else o.ctypes.data) != 0:
+            raise ValueError("hcamg_plan_set_vector failed")
+
+    def invalidate(self, vec):
+        if self.lib.hcamg_plan_invalidate(self.p, int(vec)) != 0:
+            raise ValueError("hcamg_plan_invalidate failed")
+
+    def step(self, reads, writes):
+        """reads / writes: per rank a list of (vec, index array) pairs."""
+        import numpy as np
+
+        def flat(acc):
+            cnt, vs, ix = [], [], []
+            for per_rank in acc:
+                c = 0
+                for vec, idx in per_rank:
+                    idx = np.asarray(idx, dtype=np.int32).ravel()
+                    vs.append(np.full(idx.shape, vec, dtype=np.int32))
+                    ix.append(idx)
+                    c += idx.size
+                cnt.append(c)
+            cat = lambda a: np.ascontiguousarray(np.concatenate(a) if a else np.zeros(0, np.int32), dtype=np.int32)
+            return np.asarray(cnt, dtype=np.int64), cat(vs), cat(ix)
+
+        nr, rv, ri = flat(reads)
+        nw, wv, wi = flat(writes)
+        if self.lib.hcamg_plan_step(self.p, nr.ctypes.data, rv.ctypes.data, ri.ctypes.data,
+                                    nw.ctypes.data, wv.ctypes.data, wi.ctypes.data) != 0:
+            raise ValueError("hcamg_plan_step failed")
+
+    def pushes(self):
+        """[(boundary, src, dst, vec, indices)], and the number of reads of undefined entries."""
+        import numpy as np
+
+        counts = np.zeros(3, dtype=np.int64)
+        self.lib.hcamg_plan_counts(self.p, counts.ctypes.data)
+        seg = np.zeros((int(counts[0]), 5), dtype=np.int32)
+        idx = np.zeros(int(counts[1]), dtype=np.int32)
+        self.lib.hcamg_plan_pushes(self.p, seg.ctypes.data, idx.ctypes.data)
+        out, o = [], 0
+        for b, s, d, v, c in seg:
+            out.append((int(b), int(s), int(d), int(v), idx[o:o + c].copy()))
+            o += c
+        return out, int(counts[2])
+
+
+def rows_owner(A, nranks):
+    """owner[u] = rank of row u: BFS slabs of A's graph with equal nonzero counts (hcamg_rows_owner)."""
+    import numpy as np
+    from . import _lib
+
+    lib = _lib.load()
+    A = A.tocsr()
+    ptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
+    idx = np.ascontiguousarray(A.indices, dtype=np.int32)
+    owner = np.zeros(A.shape[0], dtype=np.int8)
+    if lib.hcamg_rows_owner(A.shape[0], ptr.ctypes.data, idx.ctypes.data, int(nranks), owner.ctypes.data) != 0:
+        raise ValueError("hcamg_rows_owner failed")
+    return owner

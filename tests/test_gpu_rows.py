@@ -1,0 +1,153 @@
+"""Subdomain row partition of the sparse regime (csrc/rows.cuh), checked on one GPU.
+
+Ranks of a partitioned solve wait on each other at every boundary, so they
+cannot run as concurrent launches on one GPU.  The n-rank solve is emulated in
+lockstep (hcamg_rows_emulate): n handles of this process hold the same
+hierarchy as ranks 0..n-1 and map each other's symmetric buffers; for every
+step of the program every rank's boundary push runs first, then every rank's
+kernel -- the same kernels, push tables and epoch flags a multi-process run
+uses.  The working vectors are filled with NaN first, so an entry that a rank
+reads without having computed or received it shows up in the result.
+
+Checks: the V-cycle of every rank equals the single-GPU per-wavefront V-cycle
+bit for bit (every kernel does the same arithmetic on a subset of the rows);
+PCG agrees with the single-GPU solve and with the CPU oracle within the
+parity tolerance (the cross-rank dot products are grouped differently) and
+takes the same number of iterations.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import amg_oracle as O
+from tests.cases import load
+
+import paper_2602_23613_b200 as P
+from paper_2602_23613_b200 import dist, tri2d
+
+pytestmark = pytest.mark.gpu
+
+SPARSE_CASES = ["tri3s_alg", "tri5s_alg", "tri5s_ref", "quad3_alg"]
+
+
+def build(c, n):
+    return [P.build_hierarchy(c.system, c.meta["method"], meshes=c.meshes, rmaps=c.rmaps, options={"sweep": "wave"})
+            for _ in range(n)]
+
+
+@pytest.mark.parametrize("name", SPARSE_CASES)
+@pytest.mark.parametrize("nranks", [2, 3, 4])
+def test_emulated_vcycle_bit_identical(name, nranks):
+    c = load(name)
+    href = build(c, 1)[0]
+    b = c.z["pcg_b"]
+    zref = P.vcycle(href, b)
+    hs = build(c, nranks)
+    Z, _ = dist.emulate_rows(hs, b, kind="vcycle", min_rows=32)
+    info = dist.rows_info(hs[0])
+    assert info["nranks"] == nranks and info["connected"]
+    if href.levels[0].A.shape[0] >= 32 and href.depth > 1:
+        assert info["split_levels"] >= 1
+        assert info["segments"]["vcycle"]["push_all"] > 0
+    for r in range(nranks):
+        assert np.all(np.isfinite(Z[r])), f"rank {r} read an entry it never received"
+        assert np.array_equal(Z[r], zref), f"rank {r}: max diff {np.max(np.abs(Z[r] - zref))}"
+    # the handles go back to the single-GPU solve, bit-identical
+    for h in hs:
+        dist.undistribute_rows(h)
+    assert np.array_equal(P.vcycle(hs[-1], b), zref)
+
+
+@pytest.mark.parametrize("name", ["tri5s_alg", "tri5s_ref"])
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_emulated_pcg_matches_single_gpu_and_oracle(name, nranks):
+    c = load(name)
+    b = c.z["pcg_b"]
+    href = build(c, 1)[0]
+    xref, rref = P.pcg(c.system.A, b, precond=lambda r: P.vcycle(href, r), tol=1e-8)
+    hs = build(c, nranks)
+    X, rep = dist.emulate_rows(hs, b, kind="pcg", tol=1e-8, min_rows=32)
+    assert rep.converged and abs(rep.iterations - rref.iterations) <= 1
+    ho = O.hierarchy(c.system, c.meta["method"], meshes=c.meshes, rmaps=c.rmaps)
+    xo, ro = O.pcg(c.system.A, b, precond=lambda r: O.vcycle(ho, r), tol=1e-8)
+    assert abs(rep.iterations - ro.iterations) <= 1
+    for r in range(nranks):
+        assert np.array_equal(X[r], X[0]), "ranks hold different solutions"
+    assert np.linalg.norm(X[0] - xref) / np.linalg.norm(xref) <= 1e-10
+    # against the oracle: no further than the single-GPU solve is (its distance is the
+    # measured conditioning floor of the case, tests/test_gpu_parity.py)
+    single = np.linalg.norm(xref - xo) / np.linalg.norm(xo)
+    assert np.linalg.norm(X[0] - xo) / np.linalg.norm(xo) <= max(1e-10, 2.0 * single)
+
+
+def test_emulated_zero_rhs_and_immediate_convergence():
+    c = load("tri5s_alg")
+    hs = build(c, 2)
+    n = c.system.A.shape[0]
+    X, rep = dist.emulate_rows(hs, np.zeros(n), kind="pcg", min_rows=32)
+    assert rep.zero_rhs and rep.iterations == 0 and not X.any()
+
+
+def test_stripes_l7_four_ranks():
+    """48,896 DoFs, 5 levels; default agglomeration threshold scaled down so three levels split."""
+    system = tri2d.stripes_system(7)
+    b = np.random.default_rng(0).uniform(-1, 1, system.A.shape[0])
+    hs = [P.build_hierarchy(system, "alg", options={"sweep": "wave"}) for _ in range(5)]
+    href = hs.pop()
+    zref = P.vcycle(href, b)
+    Z, _ = dist.emulate_rows(hs, b, kind="vcycle", min_rows=1500)
+    for r in range(4):
+        assert np.array_equal(Z[r], zref)
+    info = [dist.rows_info(h) for h in hs]
+    assert info[0]["split_levels"] == 3
+    # BFS slabs: the ghost columns of a rank are a small fraction of its rows
+    for i in info:
+        assert i["ghost_cols0"] < 0.2 * i["own_rows0"], i
+    # what one PCG iteration (A p, V-cycle over three split levels with 7-10 wavefronts per
+    # leg, the agglomeration gather, three reductions) moves between the ranks: halo-sized,
+    # against n (N - 1) entries for ONE all-gather of a level-0 vector
+    n = system.A.shape[0]
+    body = info[0]["segments"]["pcg_body"]
+    assert body["push_all"] < 2 * n, body
+    assert body["barriers"] <= body["steps"]
+    # the stand-alone V-cycle additionally returns the whole of z to every rank
+    assert info[0]["segments"]["vcycle"]["push_all"] - 3 * n < 2 * n
+    xref, rref = P.pcg(system.A, b, precond=lambda r: P.vcycle(href, r), tol=1e-8)
+    X, rep = dist.emulate_rows(hs, b, kind="pcg", tol=1e-8, min_rows=1500)
+    assert rep.iterations == rref.iterations
+    assert np.linalg.norm(X[0] - xref) / np.linalg.norm(xref) <= 1e-10
+    assert np.array_equal(X[3], X[0])
+
+
+def test_one_rank_partition_runs_the_collective_graph():
+    """A one-rank partition exchanges with itself: the graph-captured PCG with the
+    boundary kernels (push, epoch flag, wait) inside the device WHILE loop."""
+    c = load("tri5s_alg")
+    b = c.z["pcg_b"]
+    href = build(c, 1)[0]
+    xref, rref = P.pcg(c.system.A, b, precond=lambda r: P.vcycle(href, r), tol=1e-8)
+    h = build(c, 1)[0]
+    dev = P.multilevel._device_for(h)
+    import ctypes as C
+
+    p = C.c_void_p()
+    dev.check(dev.lib.hcamg_rows_prepare(dev.h, 0, 1, 32, None, C.byref(p)))
+    arr = (C.c_void_p * 1)(p.value)
+    dev.check(dev.lib.hcamg_rows_connect_ptrs(dev.h, arr))
+    x, rep = P.pcg(c.system.A, b, precond=lambda r: P.vcycle(h, r), tol=1e-8)
+    assert rep.iterations == rref.iterations
+    assert np.linalg.norm(x - xref) / np.linalg.norm(xref) <= 1e-12
+    assert np.array_equal(P.vcycle(h, b), P.vcycle(href, b))
+
+
+def test_dense_regime_is_refused():
+    from paper_2602_23613_b200 import kuhn
+
+    system = kuhn.config_system("c1", 8)
+    h = P.build_hierarchy(system, "alg", options={"giant_min": 200})
+    dev = P.multilevel._device_for(h)
+    import ctypes as C
+
+    p = C.c_void_p()
+    with pytest.raises((NotImplementedError, ValueError)):
+        dev.check(dev.lib.hcamg_rows_prepare(dev.h, 0, 2, 32, None, C.byref(p)))
