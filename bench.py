@@ -443,7 +443,12 @@ def run_ours(args, world, rank, local, dist):
         # one system solved by all ranks: rows of the dense blocks split, results
         # exchanged through NVLink peer memory (paper_2602_23613_b200/dist.py)
         from paper_2602_23613_b200 import dist as D
-        D.distribute(h)
+        if args.config.startswith("2d"):
+            # sparse regime: every level split into one subdomain per rank (csrc/rows.cuh)
+            D.distribute_rows(h, min_rows=args.rows_min)
+            log(f"row partition: {D.rows_info(h)}")
+        else:
+            D.distribute(h)
     dev = h._dev
     lib = dev.lib
     stream = torch.cuda.ExternalStream(int(lib.hcamg_stream(dev.h)), device=f"cuda:{local}")
@@ -555,8 +560,11 @@ def run_ours(args, world, rank, local, dist):
             "operator_complexity": P.operator_complexity(h),
             "final_relres": float(rep.final_relres), "true_relres": true_rel,
             "l2_flush": "256 MiB write before every timed step",
-            "parallelism": (f"row-partitioned x{world} (dense blocks and coarsest inverse split by rows, "
-                            "NVLink peer-memory exchange; smoother replicated)") if partitioned
+            "parallelism": (f"subdomain row partition x{world} (every level >= {args.rows_min} rows split by rows: "
+                            "SpMV / smoother wavefront / P, P^T halos and CG reductions pushed over NVLink peer "
+                            "memory, coarser levels agglomerated)") if partitioned and args.config.startswith("2d")
+                           else (f"row-partitioned x{world} (dense blocks and coarsest inverse split by rows, "
+                                 "NVLink peer-memory exchange; smoother replicated)") if partitioned
                            else (f"replicas x{world}" if world > 1 else "single GPU"),
         },
         "roofline": {"bound": "hbm", "achieved": kr["gbs"], "peak": peak, "unit": "GB/s", "frac": kr["gbs"] / peak,
@@ -611,6 +619,8 @@ def main():
                                                   "2d-L<L>: the supplementary 2D stripes family (e.g. 2d-L9)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rows-min", type=int, default=16384,
+                    help="2D configs, N>1: levels with at least this many rows are split across the ranks")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas (weak scaling) instead of one row-partitioned solve")
     args = ap.parse_args()
