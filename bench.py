@@ -449,6 +449,16 @@ def run_ours(args, world, rank, local, dist):
             log(f"row partition: {D.rows_info(h)}")
         else:
             D.distribute(h)
+    if args.rows_self and world == 1:
+        # a one-rank row partition exchanges with itself: the partitioned step program (row lists,
+        # boundary kernels with epoch flags, split reductions) on one GPU -- measures what the
+        # partition costs before any NVLink latency
+        import ctypes as C_
+        from paper_2602_23613_b200 import dist as D
+        p_ = C_.c_void_p()
+        h._dev.check(h._dev.lib.hcamg_rows_prepare(h._dev.h, 0, 1, args.rows_min, None, C_.byref(p_)))
+        h._dev.check(h._dev.lib.hcamg_rows_connect_ptrs(h._dev.h, (C_.c_void_p * 1)(p_.value)))
+        log(f"one-rank row partition: {D.rows_info(h)}")
     dev = h._dev
     lib = dev.lib
     stream = torch.cuda.ExternalStream(int(lib.hcamg_stream(dev.h)), device=f"cuda:{local}")
@@ -621,6 +631,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rows-min", type=int, default=16384,
                     help="2D configs, N>1: levels with at least this many rows are split across the ranks")
+    ap.add_argument("--rows-self", action="store_true",
+                    help="N=1, 2D configs: run the solve as a one-rank row partition (overhead measurement)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replicas (weak scaling) instead of one row-partitioned solve")
     args = ap.parse_args()

@@ -327,27 +327,61 @@ __global__ void __launch_bounds__(kThreads) k_spmv(SpmvArgs a) {
   const int64_t grp = ((int64_t)blockIdx.x * kThreads + threadIdx.x) / G;
   const int64_t ngrp = (int64_t)gridDim.x * kThreads / G;
   double part = 0.0, part2 = 0.0;
-  const int64_t rows_iter = ((a.nrows + ngrp - 1) / ngrp) * ngrp;
-  for (int64_t q = grp; q < rows_iter; q += ngrp) {
-    const bool live = q < a.nrows;
-    const int64_t row = live ? (a.rows ? (int64_t)a.rows[q] : q) : 0;
-    double s = 0.0;
-    if (live)
-      for (int64_t e = a.ptr[row] + lg; e < a.ptr[row + 1]; e += G) s = fma(a.val[e], a.xin[a.idx[e]], s);
-    for (int o = G / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
-    if (lg != 0 || !live) continue;
-    if (E == EPI_SET) a.y[row] = s;
-    else if (E == EPI_ADD) a.y[row] += s;
-    else if (E == EPI_JAC_FW) a.y[row] -= s;
-    else if (E == EPI_RES_JAC) { const double r = a.b[row] - s; a.y[row] = r; a.dj[row] = r / a.l1[row]; }
-    else if (E == EPI_JAC_BW) { a.y[row] -= s; a.x[row] += a.dj[row]; }
-    else if (E == EPI_AP) { a.y[row] = s; part = fma(a.xin[row], s, part); }
-    else if (E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN) {
-      const double bb = a.b[row], r = bb - s;
-      a.y[row] = r;
-      part = fma(r, r, part);
-      part2 = fma(bb, bb, part2);
-    } else if (E == EPI_AMG_RES) { const double r = a.b[row] - s; a.y[row] = r; part = fma(r, r, part); }
+  // kU rows per thread group and pass, their loads issued together: the rows
+  // of the sparse-regime operators hold 3-6 entries, so a pass is one
+  // dependent chain (row pointers -> entries -> x) and the kernel is bound by
+  // chains in flight, not by lanes
+  constexpr int kU = 4;
+  const int64_t span = ngrp * kU;
+  const int64_t rows_iter = ((a.nrows + span - 1) / span) * span;
+  for (int64_t q0 = grp; q0 < rows_iter; q0 += span) {
+    int64_t row[kU], e0[kU], e1[kU];
+    bool live[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t q = q0 + u * ngrp;
+      live[u] = q < a.nrows;
+      row[u] = live[u] ? (a.rows ? (int64_t)a.rows[q] : q) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      e0[u] = live[u] ? a.ptr[row[u]] + lg : 0;
+      e1[u] = live[u] ? a.ptr[row[u] + 1] : 0;
+    }
+    double v[kU], xv[kU], sum[kU];
+    int32_t c[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const bool ok = e0[u] < e1[u];
+      v[u] = ok ? a.val[e0[u]] : 0.0;
+      c[u] = ok ? a.idx[e0[u]] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) xv[u] = c[u] >= 0 ? a.xin[c[u]] : 0.0;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      sum[u] = c[u] >= 0 ? fma(v[u], xv[u], 0.0) : 0.0;
+      for (int64_t e = e0[u] + G; e < e1[u]; e += G) sum[u] = fma(a.val[e], a.xin[a.idx[e]], sum[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      double s = sum[u];
+      for (int o = G / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
+      if (lg != 0 || !live[u]) continue;
+      const int64_t r_ = row[u];
+      if (E == EPI_SET) a.y[r_] = s;
+      else if (E == EPI_ADD) a.y[r_] += s;
+      else if (E == EPI_JAC_FW) a.y[r_] -= s;
+      else if (E == EPI_RES_JAC) { const double r = a.b[r_] - s; a.y[r_] = r; a.dj[r_] = r / a.l1[r_]; }
+      else if (E == EPI_JAC_BW) { a.y[r_] -= s; a.x[r_] += a.dj[r_]; }
+      else if (E == EPI_AP) { a.y[r_] = s; part = fma(a.xin[r_], s, part); }
+      else if (E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN) {
+        const double bb = a.b[r_], r = bb - s;
+        a.y[r_] = r;
+        part = fma(r, r, part);
+        part2 = fma(bb, bb, part2);
+      } else if (E == EPI_AMG_RES) { const double r = a.b[r_] - s; a.y[r_] = r; part = fma(r, r, part); }
+    }
   }
   if (E < EPI_AP) return;
   const bool two = E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN;
