@@ -615,7 +615,7 @@ int hcamg_set_option(hcamg_handle* h, const char* key, double value) {
     if (k->i) {
       require(value == (double)(int)value, std::string("option ") + key + " takes an integer");
       if (k->i == &Options::sweep) {
-        require(value >= SWEEP_AUTO && value <= SWEEP_FLOW, "sweep mode out of range");
+        require(value >= SWEEP_AUTO && value <= SWEEP_FWAVE, "sweep mode out of range");
         if (value == SWEEP_FLOW)  // the dataflow terms are built on first request
           for (auto& l : h->levels)
             if (!l->coarsest && l->l1.p) build_flow(l->A, l->sm, h->stream);

@@ -167,6 +167,7 @@ enum SweepMode : int {
   SWEEP_GRID = 2,     // cooperative grid leg
   SWEEP_WAVE = 3,     // one launch per wavefront
   SWEEP_FLOW = 4,     // dataflow leg: per-patch ready counters, no wave barriers
+  SWEEP_FWAVE = 5,    // one launch per wavefront over the dataflow records (wide 2D schedules)
 };
 struct Options {
   int sweep = SWEEP_AUTO;

@@ -287,6 +287,85 @@ __global__ void __launch_bounds__(kFlowThreads, 1) k_flow_leg(FlowArgs a) {
   for (int64_t e = gtid; e < a.ne; e += nth) a.d[e] = sent;
 }
 
+// ---- wave-parallel sweep over the same records (mode "fwave": the default for
+// shallow, very wide schedules -- 2D: 7-10 waves of tens of thousands of 6-DoF
+// patches).  One launch per wavefront, so no slot is ever pending and there are
+// no gates or sentinels; what the records buy here is traffic: a patch needs
+// its record (streamed once, contiguous per wave), r0 at its DoFs and the slots
+// of its terms -- no read-modify-write of a full-length residual and of two
+// full-length correction vectors per wave, which on these schedules touch one
+// DoF in seven per wave and so move every 32-byte sector of r, x, d0, d1 seven
+// times per leg (measured: 314 MB per level-0 wave at 3.1 M DoFs, 2x the
+// algorithmic bytes).  A CTA copies the records of its kPer consecutive patches
+// into shared memory with 16-byte loads (a contiguous range: full-rate,
+// independent loads), then kG lanes per patch parse them there; the only
+// dependent global loads are r0[u] and the term slots.
+constexpr int kFwThreads = 256;
+
+template <int kG, bool kDown>
+__global__ void __launch_bounds__(kFwThreads) k_flow_wave(FlowArgs a, int64_t i0, int64_t cnt) {
+  if (*a.stop) return;
+  extern __shared__ __align__(16) unsigned char fw_smem[];
+  constexpr int kPer = kFwThreads / kG;
+  __shared__ int64_t off_sh[kPer + 1];
+  const int64_t tb = (int64_t)blockIdx.x * kPer;
+  const int np = (int)(cnt - tb < (int64_t)kPer ? cnt - tb : (int64_t)kPer);
+  for (int j = threadIdx.x; j <= np; j += kFwThreads) off_sh[j] = a.rec_off[i0 + tb + j];
+  __syncthreads();
+  const int64_t base = off_sh[0];
+  const int bytes = (int)(off_sh[np] - base);
+  {
+    const int4* src = reinterpret_cast<const int4*>(a.recs + base);
+    int4* dst = reinterpret_cast<int4*>(fw_smem);
+    for (int q = threadIdx.x; q < bytes / 16; q += kFwThreads) dst[q] = __ldg(src + q);
+  }
+  __syncthreads();
+  const int sub = threadIdx.x & (kG - 1), pl = threadIdx.x / kG;
+  const bool have = pl < np;
+  const unsigned char* rec = fw_smem + (have ? (off_sh[pl] - base) : 0);
+  const int4 hd = have ? *reinterpret_cast<const int4*>(rec) : make_int4(0, 0, 0, 0);
+  const int k = hd.x, e0 = hd.y, nt = hd.z;
+  int o_dof, o_ts, o_binv, o_slot, o_val;
+  rec_layout(k, nt, o_dof, o_ts, o_binv, o_slot, o_val);
+  const int32_t* dof = reinterpret_cast<const int32_t*>(rec + o_dof);
+  const int32_t* ts = reinterpret_cast<const int32_t*>(rec + o_ts);
+  const int32_t* xpart = reinterpret_cast<const int32_t*>(rec + o_ts + 4 * ((k + 1 + 3) & ~3));
+  const double* binv = reinterpret_cast<const double*>(rec + o_binv);
+  const int32_t* tslot = reinterpret_cast<const int32_t*>(rec + o_slot);
+  const double* tval = reinterpret_cast<const double*>(rec + o_val);
+  const bool act = have && sub < k;
+  const int32_t u = act ? dof[sub] : 0;
+  const int32_t xp = act ? xpart[sub] : -1;
+  const double rv = act ? a.r0[u] : 0.0;
+  const double xv = (!kDown && act && xp != -1) ? a.x[u] : 0.0;
+  const int t0 = act ? ts[sub] : 0, t1 = act ? ts[sub + 1] : 0;
+  double acc = 0.0, dpart = 0.0;
+  for (int tt = t0; tt < t1; tt += 4) {
+    double xs[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xs[j] = tt + j < t1 ? __ldcg(a.d + tslot[tt + j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (tt + j < t1) {
+        acc = fma(tval[tt + j], xs[j], acc);
+        if (tt + j - t0 == xp) dpart = xs[j];
+      }
+  }
+  const double v = act ? rv - acc : 0.0;
+  double d = 0.0;
+#pragma unroll
+  for (int c = 0; c < kG; ++c) {
+    const double vc = __shfl_sync(0xffffffffu, v, c, kG);
+    if (act && c < k) d = fma(binv[sub * k + c], vc, d);
+  }
+  if (act) {
+    a.d[e0 + sub] = d;
+    // the last of the DoF's (<= 2) patches writes x: (x0 + d_earlier) + d (smoothers.py:102)
+    if (xp >= 0) a.x[u] = kDown ? dpart + d : (xv + dpart) + d;
+    else if (xp == -2) a.x[u] = kDown ? d : xv + d;
+  }
+}
+
 __global__ void k_fill_sentinel(double* d, int64_t n) {
   const double sent = __longlong_as_double((long long)kSentinel);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
@@ -301,6 +380,25 @@ void flow_reset_slots(double* d, int64_t ne, cudaStream_t s) {
 }
 
 int64_t flow_smem_bytes(int64_t recmax) { return (kFlowThreads / 32) * 2 * recmax; }
+
+bool flow_wave_ok(int64_t kmax, int64_t recmax) { return kmax <= 8 && (kFwThreads / 8) * recmax <= 96 * 1024; }
+
+// patches [i0, i0 + cnt) of the direction's execution order: one wavefront
+void launch_flow_wave(bool down, const FlowArgs& args, int64_t i0, int64_t cnt, cudaStream_t s) {
+  if (cnt <= 0) return;
+  constexpr int kG = 8, kPer = kFwThreads / kG;
+  const size_t smem = (size_t)kPer * (size_t)args.recmax;
+  static size_t attr = 0;
+  if (smem > attr) {
+    HC_CUDA(cudaFuncSetAttribute(k_flow_wave<kG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HC_CUDA(cudaFuncSetAttribute(k_flow_wave<kG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const unsigned grid = (unsigned)((cnt + kPer - 1) / kPer);
+  if (down) k_flow_wave<kG, true><<<grid, kFwThreads, smem, s>>>(args, i0, cnt);
+  else k_flow_wave<kG, false><<<grid, kFwThreads, smem, s>>>(args, i0, cnt);
+  HC_CHECK_LAUNCH();
+}
 
 void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s) {
   const size_t smem = (size_t)flow_smem_bytes(args.recmax);

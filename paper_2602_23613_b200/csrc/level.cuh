@@ -32,6 +32,7 @@ struct FlowProgram {
   DBuf<unsigned char> recs[2];   // per direction: one record per patch, in execution order
   DBuf<int64_t> rec_off[2];
   DBuf<double> d[2];
+  DBuf<double> dw;               // slots of the wave-parallel variant (no sentinel protocol)
   DBuf<unsigned> bar;
 };
 

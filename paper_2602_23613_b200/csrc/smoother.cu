@@ -469,7 +469,8 @@ void build_smoother(const DCsr& A, const DCsr& G, Smoother& sm, cudaStream_t s) 
     sm.max_gen_rows = std::max(sm.max_gen_rows, sm.gen_fw_ptr[(size_t)w + 1] - sm.gen_fw_ptr[(size_t)w]);
     sm.max_gen_rows = std::max(sm.max_gen_rows, sm.gen_bw_ptr[(size_t)w + 1] - sm.gen_bw_ptr[(size_t)w]);
   }
-  if (smoother_flow_auto(sm) || opts().sweep == SWEEP_FLOW) build_flow(A, sm, s);
+  if (smoother_flow_auto(sm) || smoother_wave_auto(sm) || opts().sweep == SWEEP_FLOW || opts().sweep == SWEEP_FWAVE)
+    build_flow(A, sm, s);
   HC_CUDA(cudaStreamSynchronize(s));
 }
 

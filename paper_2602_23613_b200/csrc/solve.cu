@@ -791,7 +791,60 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
   const bool down = pc == PC_DOWN;
   const bool wide = smoother_wide(L.sm);
   int m = opts().sweep;
-  if (m == SWEEP_AUTO && smoother_wave_auto(L.sm)) m = SWEEP_WAVE;
+  if (m == SWEEP_AUTO && smoother_wave_auto(L.sm)) m = SWEEP_FWAVE;
+  if (m == SWEEP_FWAVE && !(L.sm.fl.built && flow_wave_ok(L.sm.kmax, L.sm.fl.recmax))) m = SWEEP_WAVE;
+  if (m == SWEEP_FWAVE) {
+    Smoother& sm = L.sm;
+    FlowProgram& fl = sm.fl;
+    if (!fl.dw.p) {
+      fl.dw.alloc(std::max<int64_t>(fl.ne, 1), s);
+      fl.dw.zero();
+    }
+    const int dir = down ? 0 : 1;
+    FlowArgs fa{};
+    fa.stop = stop;
+    fa.n = n;
+    fa.nwave = sm.nwave;
+    fa.ne = fl.ne;
+    fa.npatch = sm.npatch;
+    fa.recmax = fl.recmax;
+    fa.recs = fl.recs[dir].p;
+    fa.rec_off = fl.rec_off[dir].p;
+    fa.d = fl.dw.p;
+    fa.x = x;
+    SpmvArgs rj{};  // r = b - A x ; dj = r / l1
+    rj.stop = stop;
+    rj.xin = x;
+    rj.y = L.r.p;
+    rj.b = b;
+    rj.l1 = L.l1.p;
+    rj.dj = L.dj.p;
+    SpmvArgs jb{};  // r -= A dj ; x += dj
+    jb.stop = stop;
+    jb.xin = L.dj.p;
+    jb.y = L.r.p;
+    jb.dj = L.dj.p;
+    jb.x = x;
+    const int64_t W = sm.nwave;
+    if (down) {
+      fa.r0 = b;
+      for (int64_t w = 0; w < W; ++w)
+        launch_flow_wave(true, fa, sm.wave_ptr[(size_t)w], sm.wave_ptr[(size_t)w + 1] - sm.wave_ptr[(size_t)w], s);
+      spmv<EPI_RES_JAC>(L.A, rj, s);
+      spmv<EPI_JAC_BW>(L.A, jb, s);
+    } else {
+      spmv<EPI_RES_JAC>(L.A, rj, s);
+      spmv<EPI_JAC_BW>(L.A, jb, s);
+      fa.r0 = L.r.p;
+      int64_t pos = 0;  // the backward records run the waves in descending order
+      for (int64_t w = W - 1; w >= 0; --w) {
+        const int64_t c = sm.wave_ptr[(size_t)w + 1] - sm.wave_ptr[(size_t)w];
+        launch_flow_wave(false, fa, pos, c, s);
+        pos += c;
+      }
+    }
+    return W + 2;
+  }
   if (m == SWEEP_AUTO && smoother_flow_auto(L.sm) && L.sm.fl.built) m = SWEEP_FLOW;
   if (m == SWEEP_FLOW && !L.sm.fl.built) m = SWEEP_GRID;  // a DoF in > 2 patches (or not prepared)
   if (m == SWEEP_FLOW) {

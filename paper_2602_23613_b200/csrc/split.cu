@@ -175,75 +175,151 @@ __global__ void k_set_state(const int64_t* __restrict__ ids, int64_t cnt, int8_t
   for (; t < cnt; t += st) state[ids[t]] = v;
 }
 
+// Unassigned nodes by measure: one hierarchical bitmap per measure value
+// (level 0: a bit per node, level l + 1: a bit per level-l word), so the
+// reference's pick -- np.argmax over the masked measure, lowest index on ties
+// (splitting.py:197-208) -- is "first set bit of the highest non-empty
+// bucket": a handful of dependent loads per pick instead of a scan over all
+// nodes (the scan made the setup quadratic: 500 s at 12.6 M DoFs).
+constexpr int kBkLevels = 4;
+struct Buckets {
+  unsigned long long* w;
+  int64_t off[kBkLevels], nw[kBkLevels], stride;
+  int nb;
+};
+
+// set-only phase (any number of threads; readers come after a barrier)
+__device__ __forceinline__ void bk_set(const Buckets& b, int m, int64_t i) {
+  unsigned long long* base = b.w + (int64_t)m * b.stride;
+  int64_t idx = i;
+  for (int l = 0; l < kBkLevels; ++l) {
+    const unsigned long long bit = 1ull << (idx & 63);
+    const unsigned long long old = atomicOr(base + b.off[l] + (idx >> 6), bit);
+    if (old != 0ull) break;  // the word was non-empty: its summaries are (being) set
+    idx >>= 6;
+  }
+}
+
+// clear-only phase: the thread that empties a word clears its summary bit
+__device__ __forceinline__ void bk_clear(const Buckets& b, int m, int64_t i) {
+  unsigned long long* base = b.w + (int64_t)m * b.stride;
+  int64_t idx = i;
+  for (int l = 0; l < kBkLevels; ++l) {
+    const unsigned long long bit = 1ull << (idx & 63);
+    const unsigned long long old = atomicAnd(base + b.off[l] + (idx >> 6), ~bit);
+    if (!(old & bit) || (old & ~bit) != 0ull) break;
+    idx >>= 6;
+  }
+}
+
+// first node of bucket m, or -1 (one thread)
+__device__ __forceinline__ int64_t bk_first(const Buckets& b, int m) {
+  const unsigned long long* base = b.w + (int64_t)m * b.stride;
+  int64_t idx = -1;
+  for (int64_t t = 0; t < b.nw[kBkLevels - 1]; ++t) {
+    const unsigned long long v = ((volatile const unsigned long long*)base)[b.off[kBkLevels - 1] + t];
+    if (v) {
+      idx = t * 64 + (__ffsll((long long)v) - 1);
+      break;
+    }
+  }
+  if (idx < 0) return -1;
+  for (int l = kBkLevels - 2; l >= 0; --l) {
+    const unsigned long long v = ((volatile const unsigned long long*)base)[b.off[l] + idx];
+    idx = idx * 64 + (__ffsll((long long)v) - 1);
+  }
+  return idx;
+}
+
 __global__ void k_cf_measure(const int64_t* __restrict__ sp_, const int32_t* __restrict__ si,
                              const int8_t* __restrict__ state, int64_t n,
-                             int32_t* __restrict__ measure, unsigned long long* __restrict__ key) {
+                             int32_t* __restrict__ measure, Buckets bk) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t st = (int64_t)gridDim.x * blockDim.x;
   for (; r < n; r += st) {
     int32_t m = 0;
     for (int64_t e = sp_[r]; e < sp_[r + 1]; ++e) m += state[si[e]] == kF;
     measure[r] = m;
-    key[r] = state[r] == kU ? ((unsigned long long)(uint32_t)m << 32) | (0xffffffffull - (unsigned long long)r) : 0ull;
+    if (state[r] == kU) bk_set(bk, m, r);
   }
 }
 
-// One CTA runs the whole pick loop (splitting.py:197-208).  key[i] encodes
-// (measure, lowest index wins) for unassigned nodes and 0 otherwise, so the
-// block-wide max is exactly np.argmax over the masked measure.
+// One CTA runs the whole pick loop (splitting.py:197-208).
 constexpr int kCfThreads = 1024;
 
 __global__ void __launch_bounds__(kCfThreads) k_cf_greedy(
     int64_t n, const int64_t* __restrict__ np_, const int32_t* __restrict__ ni,
     const int64_t* __restrict__ tp, const int32_t* __restrict__ ti, int8_t* state, int32_t* measure,
-    unsigned long long* key, int32_t* scratch /* n */) {
-  __shared__ unsigned long long red[kCfThreads / 32];
-  __shared__ unsigned long long best;
-  __shared__ int nnew;
+    Buckets bk, int32_t* scratch /* n */) {
+  __shared__ int64_t pick;
+  __shared__ int nnew, top;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) top = bk.nb - 1;
+  __syncthreads();
   while (true) {
-    unsigned long long m = 0;
-    for (int64_t i = tid; i < n; i += kCfThreads) m = max(m, key[i]);
-    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) red[wid] = m;
-    __syncthreads();
-    if (wid == 0) {
-      m = red[lane];
-      for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) { best = m; nnew = 0; }
+    if (tid == 0) {
+      int64_t i = -1;
+      int t = top;
+      while (t >= 0 && (i = bk_first(bk, t)) < 0) --t;
+      top = t < 0 ? 0 : t;
+      pick = i;
+      nnew = 0;
+      if (i >= 0) {
+        state[i] = kC;
+        bk_clear(bk, measure[i], i);
+      }
     }
     __syncthreads();
-    if (best == 0ull) break;
-    const int64_t i = (int64_t)(0xffffffffull - (best & 0xffffffffull));
-    if (tid == 0) { state[i] = kC; key[i] = 0ull; }
-    __syncthreads();
+    const int64_t i = pick;
+    if (i < 0) break;
     // all unassigned graph neighbours of i become fine
     for (int64_t e = np_[i] + tid; e < np_[i + 1]; e += kCfThreads) {
       int32_t j = ni[e];
       if (state[j] == kU) {
         state[j] = kF;
-        key[j] = 0ull;
         scratch[atomicAdd(&nnew, 1)] = j;
       }
     }
     __syncthreads();
     const int cnt = nnew;
+    // clear phase: the new fine nodes and every unassigned node whose measure is about to change
+    for (int t = tid; t < cnt; t += kCfThreads) bk_clear(bk, measure[scratch[t]], scratch[t]);
+    for (int t = wid; t < cnt; t += kCfThreads / 32) {
+      int32_t j = scratch[t];
+      for (int64_t e = tp[j] + lane; e < tp[j + 1]; e += 32) {
+        int32_t k = ti[e];
+        if (state[k] == kU) bk_clear(bk, measure[k], k);
+      }
+    }
+    __syncthreads();
     // measure[k] += 1 for k in strong_to[j] (one warp per new fine node)
     for (int t = wid; t < cnt; t += kCfThreads / 32) {
       int32_t j = scratch[t];
       for (int64_t e = tp[j] + lane; e < tp[j + 1]; e += 32) atomicAdd(&measure[ti[e]], 1);
     }
     __syncthreads();
+    // set phase: back into the bucket of the new measure
     for (int t = wid; t < cnt; t += kCfThreads / 32) {
       int32_t j = scratch[t];
       for (int64_t e = tp[j] + lane; e < tp[j + 1]; e += 32) {
         int32_t k = ti[e];
-        if (state[k] == kU)
-          key[k] = ((unsigned long long)(uint32_t)measure[k] << 32) | (0xffffffffull - (unsigned long long)k);
+        if (state[k] == kU) {
+          const int m = measure[k];
+          bk_set(bk, m, k);
+          if (m > top) atomicMax(&top, m);
+        }
       }
     }
     __syncthreads();
   }
+}
+
+__global__ void k_row_len_max(const int64_t* __restrict__ ptr, int64_t n, int* __restrict__ out) {
+  int m = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, (int)(ptr[r + 1] - ptr[r]));
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 
 __global__ void k_flag_state(const int8_t* __restrict__ state, int8_t v, int64_t n, int64_t* __restrict__ f) {
@@ -285,12 +361,32 @@ void nodal_cf(const DCsr& An, const DBuf<int64_t>& bcols, double theta, DCsr& nb
     HC_CHECK_LAUNCH();
   }
   DBuf<int32_t> measure(n, s), scratch(n + 1, s);
-  DBuf<unsigned long long> key(n, s);
   if (n) {
-    k_cf_measure<<<grid_for(n, 256), 256, 0, s>>>(strong.ptr.p, strong.idx.p, state.p, n, measure.p, key.p);
-    k_cf_greedy<<<1, kCfThreads, 0, s>>>(n, nbr.ptr.p, nbr.idx.p, strongT.ptr.p, strongT.idx.p, state.p,
-                                         measure.p, key.p, scratch.p);
+    // a node's measure never exceeds the length of its strong row (each strong
+    // neighbour counts once: fine from the start, or one increment when it turns fine)
+    DBuf<int> mx(1, s);
+    mx.zero();
+    k_row_len_max<<<grid_for(n, 256), 256, 0, s>>>(strong.ptr.p, n, mx.p);
     HC_CHECK_LAUNCH();
+    Buckets bk{};
+    bk.nb = read_scalar(mx.p, s) + 1;
+    int64_t words = 0, cnt = n;
+    for (int l = 0; l < kBkLevels; ++l) {
+      cnt = (cnt + 63) / 64;
+      bk.off[l] = words;
+      bk.nw[l] = cnt;
+      words += cnt;
+    }
+    require(bk.nw[kBkLevels - 1] <= 64, "nodal graph too large for the C/F bucket index");
+    bk.stride = words;
+    DBuf<unsigned long long> bits(words * bk.nb, s);
+    bits.zero();
+    bk.w = bits.p;
+    k_cf_measure<<<grid_for(n, 256), 256, 0, s>>>(strong.ptr.p, strong.idx.p, state.p, n, measure.p, bk);
+    k_cf_greedy<<<1, kCfThreads, 0, s>>>(n, nbr.ptr.p, nbr.idx.p, strongT.ptr.p, strongT.idx.p, state.p,
+                                         measure.p, bk, scratch.p);
+    HC_CHECK_LAUNCH();
+    HC_CUDA(cudaStreamSynchronize(s));  // bits is released below
   }
 }
 

@@ -69,6 +69,9 @@ struct FlowArgs {
   long long* trace;           // debug: per execution position {record ready, pulls done, stored, warp} (globaltimer)
 };
 void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s);
+// wave-parallel sweep over the same records (mode "fwave"): one launch per wavefront
+void launch_flow_wave(bool down, const FlowArgs& args, int64_t i0, int64_t cnt, cudaStream_t s);
+bool flow_wave_ok(int64_t kmax, int64_t recmax);
 int64_t flow_smem_bytes(int64_t recmax);
 void flow_reset_slots(double* d, int64_t ne, cudaStream_t s);
 
