@@ -796,10 +796,6 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
   if (m == SWEEP_FWAVE) {
     Smoother& sm = L.sm;
     FlowProgram& fl = sm.fl;
-    if (!fl.dw.p) {
-      fl.dw.alloc(std::max<int64_t>(fl.ne, 1), s);
-      fl.dw.zero();
-    }
     const int dir = down ? 0 : 1;
     FlowArgs fa{};
     fa.stop = stop;
@@ -1047,8 +1043,9 @@ int64_t record_amg_body(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s
 
 // ----------------------------------------------------------------------------- subdomain row partition (rows.cuh)
 
-static_assert(RE_SET == EPI_SET && RE_ADD == EPI_ADD && RE_JAC_FW == EPI_JAC_FW && RE_RES_JAC == EPI_RES_JAC &&
-                  RE_JAC_BW == EPI_JAC_BW && RE_AP == EPI_AP && RE_PCG_INIT == EPI_PCG_INIT,
+static_assert((int)RE_SET == (int)EPI_SET && (int)RE_ADD == (int)EPI_ADD && (int)RE_JAC_FW == (int)EPI_JAC_FW &&
+                  (int)RE_RES_JAC == (int)EPI_RES_JAC && (int)RE_JAC_BW == (int)EPI_JAC_BW &&
+                  (int)RE_AP == (int)EPI_AP && (int)RE_PCG_INIT == (int)EPI_PCG_INIT,
               "rows.cuh REpi mirrors Epi");
 
 // One step of the partitioned program on this rank: the single-GPU kernel on

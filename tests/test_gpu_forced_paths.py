@@ -38,7 +38,7 @@ VARIANTS = {
     # (transfer.py:100-116; round 1 raised NotImplementedError)
     "multi_giant": {"giant_min": 4, "coarse_gemv_min": 0},
 }
-SWEEPS = ["grid", "wave", "leg", "flow"]
+SWEEPS = ["grid", "wave", "leg", "flow", "fwave"]
 
 
 def rel(a, b):
@@ -128,7 +128,8 @@ def test_dense_regime_forced(oracle_case, variant):
 @pytest.mark.parametrize("sweep", SWEEPS)
 def test_smoothing_legs_forced(oracle_case, sweep):
     """Every smoothing-leg kernel (cluster leg, grid leg, per-wave launches,
-    dataflow leg) against the oracle's sequential OSS-l1 sweep."""
+    dataflow leg, wave-parallel sweep over the dataflow records) against the
+    oracle's sequential OSS-l1 sweep."""
     name, c, ho = oracle_case
     hg = P.build_hierarchy(c.system, c.meta["method"], meshes=c.meshes, rmaps=c.rmaps)
     set_options(hg, sweep=sweep)
