@@ -197,6 +197,9 @@ void finish_level(hcamg_handle* h, DevLevel& L) {
   if (L.has_P) {
     build_l1(L.A, L.l1, s);
     build_smoother(L.A, L.G, L.sm, s);
+    build_sell(L.A, s);
+    build_sell(L.P, s);
+    build_sell(L.Pt, s);
     // restriction with long P^T rows (dense interior blocks): segmented plan
     std::vector<int64_t> tp = L.Pt.ptr.download();
     L.pt_maxrow = 0;

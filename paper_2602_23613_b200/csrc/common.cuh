@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <memory>
 #include <stdexcept>
 #include <chrono>
 #include <cstdio>
@@ -117,12 +118,23 @@ inline T read_scalar(const T* dev, cudaStream_t s) {
   return h;
 }
 
+// Sliced-ELLPACK copy of a short-row CSR (solve.cu build_sell): 32 rows per
+// slice, entries of a slice column-major (entry j of the slice's row l at
+// soff[slice] + 32 j + l), padded to the slice's longest row with column -1.
+struct DSell {
+  int64_t nslice = 0, padded = 0;
+  DBuf<int64_t> soff;
+  DBuf<int32_t> idx;
+  DBuf<double> val;
+};
+
 // Device CSR: int64 row pointers, int32 column indices, fp64 values.
 struct DCsr {
   int64_t nrows = 0, ncols = 0, nnz = 0;
   DBuf<int64_t> ptr;
   DBuf<int32_t> idx;
   DBuf<double> val;
+  std::unique_ptr<DSell> sell;  // optional SpMV layout of the solve phase
   void alloc(int64_t r, int64_t c, int64_t z, cudaStream_t s) {
     nrows = r; ncols = c; nnz = z;
     ptr.alloc(r + 1, s);

@@ -317,6 +317,110 @@ __device__ __forceinline__ void fin_rz(Ctl* c, double S, unsigned long long cond
   c->rz = S;
 }
 
+// what a row does with its product s = (M xin)[row]
+template <int E>
+__device__ __forceinline__ void spmv_epi(const SpmvArgs& a, int64_t r_, double s, double& part, double& part2) {
+  if (E == EPI_SET) a.y[r_] = s;
+  else if (E == EPI_ADD) a.y[r_] += s;
+  else if (E == EPI_JAC_FW) a.y[r_] -= s;
+  else if (E == EPI_RES_JAC) { const double r = a.b[r_] - s; a.y[r_] = r; a.dj[r_] = r / a.l1[r_]; }
+  else if (E == EPI_JAC_BW) { a.y[r_] -= s; a.x[r_] += a.dj[r_]; }
+  else if (E == EPI_AP) { a.y[r_] = s; part = fma(a.xin[r_], s, part); }
+  else if (E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN) {
+    const double bb = a.b[r_], r = bb - s;
+    a.y[r_] = r;
+    part = fma(r, r, part);
+    part2 = fma(bb, bb, part2);
+  } else if (E == EPI_AMG_RES) { const double r = a.b[r_] - s; a.y[r_] = r; part = fma(r, r, part); }
+}
+
+// the reduction tail of the reducing epilogues (every thread of every block calls it)
+template <int E>
+__device__ __forceinline__ void spmv_reduce(const SpmvArgs& a, double part, double part2) {
+  const bool two = E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN;
+  Ctl* c = a.ctl;
+  if (!publish(part, part2, a.part, two ? a.part2 : nullptr, &c->ticket[E - EPI_AP])) return;
+  const double S = ordered_sum(a.part, gridDim.x);
+  const double S2 = two ? ordered_sum(a.part2, gridDim.x) : 0.0;
+  if (threadIdx.x != 0) return;
+  c->ticket[E - EPI_AP] = 0u;
+  if (a.red) {  // row partition: publish the rank's partials, k_finish sums over the ranks
+    a.red[0] = S;
+    a.red[1] = S2;
+    return;
+  }
+  if (E == EPI_AP) {
+    fin_ap(c, S, a.cond);
+  } else if (E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN) {
+    fin_init(c, S, S2, a.cond);
+  } else if (E == EPI_AMG_RES) {
+    const double prev = c->rel;
+    const double rel = sqrt(S) / c->bnorm;
+    c->rel = rel;
+    a.hist[c->it] = rel;
+    c->it += 1;
+    if (rel <= c->tol) { c->converged = 1; c->stop = 1; }
+    else {
+      c->growth = rel > prev ? c->growth + 1 : 0;
+      if (c->growth >= 5) { c->error = 3; c->stop = 1; }
+      else if (c->it >= c->maxit) c->stop = 1;
+    }
+    set_cond(a.cond, c->stop ? 0u : 1u);
+  }
+}
+
+// Thread per row over the sliced-ELLPACK copy: every load of a warp is one
+// coalesced 128 / 256-byte line, a row's entries are independent loads (no row
+// pointers, no shuffles), and the row sum reproduces the CSR kernel's order --
+// entry j into partial j mod G, partials folded as the xor butterfly does -- so
+// the two kernels are bit-identical and interchangeable (the row partition
+// runs the CSR kernel on row lists).
+template <int G, int E>
+__global__ void __launch_bounds__(kThreads) k_spmv_sell(SpmvArgs a, const int64_t* __restrict__ soff,
+                                                        const int32_t* __restrict__ sidx,
+                                                        const double* __restrict__ sval) {
+  if (E != EPI_PCG_INIT && E != EPI_AMG_INIT && E != EPI_RES_PLAIN && *a.stop) {
+    if (E == EPI_AP && blockIdx.x == 0 && threadIdx.x == 0) set_cond(a.cond, 0);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t nsl = (a.nrows + 31) >> 5;
+  double part = 0.0, part2 = 0.0;
+  for (int64_t sl = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5; sl < nsl;
+       sl += ((int64_t)gridDim.x * kThreads) >> 5) {
+    const int64_t base = soff[sl];
+    const int width = (int)((soff[sl + 1] - base) >> 5);
+    const int64_t row = sl * 32 + lane;
+    const int32_t* ip = sidx + base + lane;
+    const double* vp = sval + base + lane;
+    double acc[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) acc[g] = 0.0;
+    for (int j0 = 0; j0 < width; j0 += G) {
+      int32_t c[G];
+      double v[G], xv[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const bool ok = j0 + g < width;
+        c[g] = ok ? __ldg(ip + (int64_t)(j0 + g) * 32) : -1;
+        v[g] = ok ? __ldg(vp + (int64_t)(j0 + g) * 32) : 0.0;
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) xv[g] = c[g] >= 0 ? a.xin[c[g]] : 0.0;
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if (c[g] >= 0) acc[g] = fma(v[g], xv[g], acc[g]);
+    }
+#pragma unroll
+    for (int o = G / 2; o; o >>= 1)
+#pragma unroll
+      for (int g = 0; g < o; ++g) acc[g] += acc[g + o];
+    if (row < a.nrows) spmv_epi<E>(a, row, acc[0], part, part2);
+  }
+  if (E < EPI_AP) return;
+  spmv_reduce<E>(a, part, part2);
+}
+
 template <int G, int E>
 __global__ void __launch_bounds__(kThreads) k_spmv(SpmvArgs a) {
   if (E != EPI_PCG_INIT && E != EPI_AMG_INIT && E != EPI_RES_PLAIN && *a.stop) {
@@ -368,52 +472,11 @@ __global__ void __launch_bounds__(kThreads) k_spmv(SpmvArgs a) {
       double s = sum[u];
       for (int o = G / 2; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o, G);
       if (lg != 0 || !live[u]) continue;
-      const int64_t r_ = row[u];
-      if (E == EPI_SET) a.y[r_] = s;
-      else if (E == EPI_ADD) a.y[r_] += s;
-      else if (E == EPI_JAC_FW) a.y[r_] -= s;
-      else if (E == EPI_RES_JAC) { const double r = a.b[r_] - s; a.y[r_] = r; a.dj[r_] = r / a.l1[r_]; }
-      else if (E == EPI_JAC_BW) { a.y[r_] -= s; a.x[r_] += a.dj[r_]; }
-      else if (E == EPI_AP) { a.y[r_] = s; part = fma(a.xin[r_], s, part); }
-      else if (E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN) {
-        const double bb = a.b[r_], r = bb - s;
-        a.y[r_] = r;
-        part = fma(r, r, part);
-        part2 = fma(bb, bb, part2);
-      } else if (E == EPI_AMG_RES) { const double r = a.b[r_] - s; a.y[r_] = r; part = fma(r, r, part); }
+      spmv_epi<E>(a, row[u], s, part, part2);
     }
   }
   if (E < EPI_AP) return;
-  const bool two = E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN;
-  Ctl* c = a.ctl;
-  if (!publish(part, part2, a.part, two ? a.part2 : nullptr, &c->ticket[E - EPI_AP])) return;
-  const double S = ordered_sum(a.part, gridDim.x);
-  const double S2 = two ? ordered_sum(a.part2, gridDim.x) : 0.0;
-  if (threadIdx.x != 0) return;
-  c->ticket[E - EPI_AP] = 0u;
-  if (a.red) {  // row partition: publish the rank's partials, k_finish sums over the ranks
-    a.red[0] = S;
-    a.red[1] = S2;
-    return;
-  }
-  if (E == EPI_AP) {
-    fin_ap(c, S, a.cond);
-  } else if (E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN) {
-    fin_init(c, S, S2, a.cond);
-  } else if (E == EPI_AMG_RES) {
-    const double prev = c->rel;
-    const double rel = sqrt(S) / c->bnorm;
-    c->rel = rel;
-    a.hist[c->it] = rel;
-    c->it += 1;
-    if (rel <= c->tol) { c->converged = 1; c->stop = 1; }
-    else {
-      c->growth = rel > prev ? c->growth + 1 : 0;
-      if (c->growth >= 5) { c->error = 3; c->stop = 1; }
-      else if (c->it >= c->maxit) c->stop = 1;
-    }
-    set_cond(a.cond, c->stop ? 0u : 1u);
-  }
+  spmv_reduce<E>(a, part, part2);
 }
 
 // ----------------------------------------------------------------------------- PCG vector kernels
@@ -556,6 +619,14 @@ unsigned spmv(const DCsr& M, SpmvArgs a, cudaStream_t s) {
   a.idx = M.idx.p;
   a.val = M.val.p;
   const int G = group_for(M);
+  if (M.sell && !a.rows && (G == 4 || G == 8)) {
+    const DSell& S = *M.sell;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((S.nslice + 7) / 8, kSMs * 8));
+    if (G == 4) k_spmv_sell<4, E><<<grid, kThreads, 0, s>>>(a, S.soff.p, S.idx.p, S.val.p);
+    else k_spmv_sell<8, E><<<grid, kThreads, 0, s>>>(a, S.soff.p, S.idx.p, S.val.p);
+    HC_CHECK_LAUNCH();
+    return grid;
+  }
   const unsigned grid = spmv_grid(a.nrows, G);
   launch_spmv_g<E>(G, grid, a, s);
   return grid;
@@ -564,6 +635,53 @@ unsigned spmv(const DCsr& M, SpmvArgs a, cudaStream_t s) {
 unsigned vec_grid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + kThreads - 1) / kThreads, kSMs * 4)); }
 
 }  // namespace
+
+namespace {
+__global__ void k_sell_width(const int64_t* __restrict__ ptr, int64_t nrows, int64_t nsl, int64_t* __restrict__ w) {
+  for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < nsl; sl += (int64_t)gridDim.x * blockDim.x) {
+    int64_t m = 0;
+    for (int64_t r = sl * 32; r < min(nrows, sl * 32 + 32); ++r) m = max(m, ptr[r + 1] - ptr[r]);
+    w[sl] = 32 * m;
+  }
+}
+__global__ void k_sell_fill(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
+                            const double* __restrict__ val, int64_t nrows, int64_t nsl,
+                            const int64_t* __restrict__ soff, int32_t* __restrict__ sidx, double* __restrict__ sval) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nsl * 32; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sl = t >> 5, base = soff[sl];
+    const int lane = (int)(t & 31), width = (int)((soff[sl + 1] - base) >> 5);
+    const int64_t e0 = t < nrows ? ptr[t] : 0, e1 = t < nrows ? ptr[t + 1] : 0;
+    for (int j = 0; j < width; ++j) {
+      const bool ok = e0 + j < e1;
+      sidx[base + (int64_t)j * 32 + lane] = ok ? idx[e0 + j] : -1;
+      sval[base + (int64_t)j * 32 + lane] = ok ? val[e0 + j] : 0.0;
+    }
+  }
+}
+}  // namespace
+
+// Give M the sliced-ELLPACK copy its SpMVs run on, when its rows are short
+// (the 4- and 8-lane classes of group_for) and the padding stays below 50 %.
+void build_sell(DCsr& M, cudaStream_t s) {
+  M.sell.reset();
+  const int G = group_for(M);
+  if (M.nrows < 4096 || (G != 4 && G != 8)) return;
+  const int64_t nsl = (M.nrows + 31) / 32;
+  DBuf<int64_t> w(nsl, s);
+  k_sell_width<<<grid_for(nsl, 256), 256, 0, s>>>(M.ptr.p, M.nrows, nsl, w.p);
+  HC_CHECK_LAUNCH();
+  std::unique_ptr<DSell> S(new DSell());
+  S->nslice = nsl;
+  S->soff.alloc(nsl + 1, s);
+  S->padded = exclusive_scan(w.p, S->soff.p, nsl, s);
+  if (S->padded > M.nnz + M.nnz / 2) return;
+  S->idx.alloc(std::max<int64_t>(S->padded, 1), s);
+  S->val.alloc(std::max<int64_t>(S->padded, 1), s);
+  k_sell_fill<<<grid_for(nsl * 32, 256), 256, 0, s>>>(M.ptr.p, M.idx.p, M.val.p, M.nrows, nsl, S->soff.p, S->idx.p,
+                                                      S->val.p);
+  HC_CHECK_LAUNCH();
+  M.sell = std::move(S);
+}
 
 void Workspace::ensure(int64_t n_, int64_t maxit, cudaStream_t s) {
   if (!ctl.p) {

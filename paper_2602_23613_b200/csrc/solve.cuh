@@ -60,6 +60,9 @@ int64_t record_amg_init(DevLevel& L0, Workspace& w, const double* b, const doubl
                         unsigned long long cond);
 int64_t record_amg_body(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s, unsigned long long cond);
 
+// Sliced-ELLPACK SpMV layout for short-row operators (no-op otherwise).
+void build_sell(DCsr& M, cudaStream_t s);
+
 // y = A x (device), for the generic PCG path.
 void apply_operator(const DCsr& A, const double* x, double* y, cudaStream_t s);
 
