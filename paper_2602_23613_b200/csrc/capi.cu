@@ -615,6 +615,7 @@ int hcamg_set_option(hcamg_handle* h, const char* key, double value) {
   return guarded(h, [&] {
     const OptKey* k = find_opt(key);
     require(k != nullptr, std::string("unknown option ") + (key ? key : "(null)"));
+    require(!h->rows, "options cannot change while a row partition is attached (hcamg_rows_disconnect first)");
     if (k->i) {
       require(value == (double)(int)value, std::string("option ") + key + " takes an integer");
       if (k->i == &Options::sweep) {

@@ -118,6 +118,13 @@ void host_image(std::vector<DevLevel*>& lv, std::vector<RowsHostLevel>& out, cud
       fetch(sm.lastr, 2 * L.n, H.lastr, s);
       fetch(sm.gcol, sm.gcol.n, H.gcol, s);
       fetch(sm.in_first, L.n, H.in_first, s);
+      H.fw = leg_mode(L) == SWEEP_FWAVE;
+      H.ne = sm.fl.built ? sm.fl.ne : 0;
+      if (H.fw)
+        for (int d = 0; d < 2; ++d) {
+          fetch(sm.fl.rec_off[d], sm.npatch + 1, H.rec_off[d], s);
+          fetch(sm.fl.recs[d], sm.fl.recs[d].n, H.recs[d], s);
+        }
     }
     HC_CUDA(cudaStreamSynchronize(s));
   }
@@ -191,7 +198,25 @@ void rows_prepare(RowsCtx& rc, std::vector<DevLevel*>& lv, Workspace& w, int ran
     D.nrows = (int64_t)S.rows.size();
     D.rows.s = s;
     D.rows.upload(S.rows.data(), (int64_t)S.rows.size());
-    if (D.split) {
+    D.fw = D.split && H[(size_t)l].fw;
+    if (D.fw) {
+      const RowsHostLevel& HL = H[(size_t)l];
+      for (int d = 0; d < 2; ++d) {
+        std::vector<unsigned char> loc;
+        std::vector<int64_t> off(1, 0);
+        for (int64_t pos : S.fpos[d]) {
+          const int64_t b0 = HL.rec_off[d][(size_t)pos], b1 = HL.rec_off[d][(size_t)pos + 1];
+          loc.insert(loc.end(), HL.recs[d].begin() + b0, HL.recs[d].begin() + b1);
+          off.push_back((int64_t)loc.size());
+        }
+        if (loc.empty()) loc.assign(16, 0);
+        D.frecs[d].s = s;
+        D.frecs[d].upload(loc.data(), (int64_t)loc.size());
+        D.frec_off[d].s = s;
+        D.frec_off[d].upload(off.data(), (int64_t)off.size());
+        D.foff[d] = S.foff[d];
+      }
+    } else if (D.split) {
       D.plist.s = s;
       D.plist.upload(S.plist.data(), (int64_t)S.plist.size());
       D.poff = S.poff;
@@ -201,6 +226,13 @@ void rows_prepare(RowsCtx& rc, std::vector<DevLevel*>& lv, Workspace& w, int ran
         D.goff[d] = S.goff[d];
       }
     }
+    if (D.split) {  // this rank's rows of the level's operators in the SpMV layout
+      DevLevel& L = *lv[(size_t)l];
+      D.sA = build_sell_rows(L.A, D.rows.p, D.nrows, s);
+      if (L.has_P) D.sP = build_sell_rows(L.P, D.rows.p, D.nrows, s);
+    }
+    if (l > 0 && H[(size_t)l - 1].split)  // rows of P^T of the finer level
+      rc.lev[(size_t)l - 1].sPt = build_sell_rows(lv[(size_t)l - 1]->Pt, D.rows.p, D.nrows, s);
   }
   // ---- push tables of this rank as the source
   const int32_t nb = plan.nboundary;
@@ -283,7 +315,8 @@ void rows_prepare(RowsCtx& rc, std::vector<DevLevel*>& lv, Workspace& w, int ran
     off += ((size_t)std::max<int64_t>(len, 1) * 8 + 255) / 256 * 256;
   };
   for (int l = 0; l < depth; ++l)
-    for (int k = 0; k < LV_COUNT; ++k) take(rows_vec_level(l, k), lv[(size_t)l]->n);
+    for (int k = 0; k < LV_COUNT; ++k)
+      take(rows_vec_level(l, k), k == LV_DW ? std::max<int64_t>(H[(size_t)l].ne, 1) : lv[(size_t)l]->n);
   for (int k = 0; k < WS_COUNT; ++k) take(rows_vec_ws(depth, k), lv[0]->n);
   take(rows_vec_red(depth), (int64_t)RS_COUNT * 2 * nranks);
   rc.sym_bytes = off;
@@ -302,8 +335,9 @@ void rows_prepare(RowsCtx& rc, std::vector<DevLevel*>& lv, Workspace& w, int ran
   // ---- re-point the working vectors into the symmetric buffer
   for (int l = 0; l < depth; ++l) {
     DevLevel& L = *lv[(size_t)l];
-    DBuf<double>* v[LV_COUNT] = {&L.b, &L.x, &L.r, &L.d0, &L.d1, &L.dj};
-    for (int k = 0; k < LV_COUNT; ++k) v[k]->alias(rc.vec(rows_vec_level(l, k)), std::max<int64_t>(L.n, 1), s);
+    DBuf<double>* v[6] = {&L.b, &L.x, &L.r, &L.d0, &L.d1, &L.dj};
+    for (int k = 0; k < 6; ++k) v[k]->alias(rc.vec(rows_vec_level(l, k)), std::max<int64_t>(L.n, 1), s);
+    if (L.sm.fl.built) L.sm.fl.dw.alias(rc.vec(rows_vec_level(l, LV_DW)), std::max<int64_t>(L.sm.fl.ne, 1), s);
   }
   {
     DBuf<double>* v[WS_COUNT] = {&w.x, &w.r, &w.z, &w.p, &w.Ap, &w.b};
@@ -318,6 +352,10 @@ void rows_detach(RowsCtx& rc, std::vector<DevLevel*>& lv, Workspace& w, cudaStre
       if (!v->view) continue;
       v->alloc(std::max<int64_t>(L->n, 1), s);
       v->zero();
+    }
+    if (L->sm.fl.dw.view) {
+      L->sm.fl.dw.alloc(std::max<int64_t>(L->sm.fl.ne, 1), s);
+      L->sm.fl.dw.zero();
     }
   }
   for (DBuf<double>* v : {&w.x, &w.r, &w.z, &w.p, &w.Ap, &w.b}) {

@@ -88,6 +88,8 @@ enum RKind : int {
   RK_P_UPDATE,     // p = z + beta p
   RK_FINISH,       // sum a reduction over the ranks, scalar logic
   RK_GATHER,       // no kernel: every rank reads the whole vector (all-gather through the push lists)
+  RK_FWAVE,        // one wavefront of the sweep over the dataflow records (flow.cu k_flow_wave)
+  RK_LEG,          // a whole smoothing leg of an agglomerated level, as the single-GPU solve runs it
 };
 
 // SpMV epilogues a step can ask for (numerically equal to solve.cu's Epi)
@@ -101,15 +103,16 @@ enum RSite : int { RS_INIT = 0, RS_AP = 1, RS_UPD = 2, RS_RZ_FIRST = 3, RS_RZ = 
 enum RSeg : int { SEG_VCYCLE = 0, SEG_INIT = 1, SEG_FIRST = 2, SEG_BODY = 3, SEG_GATHER = 4, SEG_COUNT = 5 };
 
 // vectors of a level / of the PCG workspace, as the planner numbers them
-enum RVec : int { LV_B = 0, LV_X, LV_R, LV_D0, LV_D1, LV_DJ, LV_COUNT };
+enum RVec : int { LV_B = 0, LV_X, LV_R, LV_D0, LV_D1, LV_DJ, LV_DW, LV_COUNT };  // LV_DW: correction slots, one per patch entry
 enum RWs : int { WS_X = 0, WS_R, WS_Z, WS_P, WS_AP, WS_B, WS_COUNT };
 
 struct RStep {
   int kind = 0, level = 0;
   int mat = 0, epi = 0;       // RK_SPMV
-  int dir = 0;                // RK_WAVE
+  int dir = 0;                // RK_WAVE / RK_FWAVE (RK_FWAVE: dst = position of the wave in the direction's order)
   int64_t dst = 0, src = -1;
   bool init = false;
+  bool down = false;          // RK_LEG
   int site = 0;               // reductions
   int vec = -1;               // RK_GATHER: vector id
 };
@@ -127,7 +130,20 @@ struct RowsHostLevel {
   std::vector<int32_t> patch_dofs, ownr[2], genrow[2], lastr, gcol;
   std::vector<uint8_t> in_first;
   std::vector<int8_t> owner;  // row -> rank
+  // dataflow records (levels swept by k_flow_wave): per direction the byte
+  // offsets of the patch records in execution order, and the records
+  bool fw = false;
+  int64_t ne = 0;
+  std::vector<int64_t> rec_off[2];
+  std::vector<unsigned char> recs[2];
 };
+
+// one patch record as the host sees it (layout: flow.cu rec_layout)
+struct FlowRecView {
+  int32_t k, e0, nt;
+  const int32_t *dof, *ts, *xpart, *tslot;
+};
+FlowRecView flow_rec_view(const unsigned char* rec);
 
 // One rank's share of a level
 struct RowsShare {
@@ -136,6 +152,8 @@ struct RowsShare {
   std::vector<int64_t> poff;                 // nwave + 1 offsets into plist
   std::vector<int32_t> gen[2];               // its generic rows per direction (indices relative to the wave's first triple)
   std::vector<int64_t> goff[2];              // nwave + 1 offsets into gen[dir]
+  std::vector<int64_t> fpos[2];              // fw levels: its record positions per direction, in execution order
+  std::vector<int64_t> foff[2];              // nwave + 1 offsets into fpos[dir] (by position of the wave in the order)
 };
 
 // slab ownership of a graph (BFS level sets from a pseudo-peripheral node,

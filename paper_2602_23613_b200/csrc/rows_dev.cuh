@@ -19,6 +19,14 @@ struct RowsLevelDev {
   std::vector<int64_t> poff;
   DBuf<int32_t> gen[2];
   std::vector<int64_t> goff[2];
+  // levels swept over the dataflow records: this rank's records, compacted in
+  // execution order, and their per-wave offsets
+  bool fw = false;
+  DBuf<unsigned char> frecs[2];
+  DBuf<int64_t> frec_off[2];
+  std::vector<int64_t> foff[2];
+  // sliced-ELLPACK copies of this rank's rows of A, P (rows of the level) and P^T (rows of the next level)
+  std::unique_ptr<DSell> sA, sP, sPt;
 };
 
 // what the boundary kernel needs, by value
@@ -80,6 +88,11 @@ struct RowsCtx {
 // solve.cu: launch one step's kernel for this rank (no-op for RK_GATHER); returns launches
 int64_t rows_launch_step(const RStep& st, RowsCtx& rc, std::vector<DevLevel*>& lv, Workspace& w, const int* stop,
                          unsigned long long cond, cudaStream_t s);
+
+// solve.cu: the leg kernels record_piece would run on this level with the handle's options
+int leg_mode(const DevLevel& L);
+// solve.cu: sliced-ELLPACK copy of the listed rows of M (null when the rows are not short)
+std::unique_ptr<DSell> build_sell_rows(const DCsr& M, const int32_t* rows, int64_t nrows, cudaStream_t s);
 
 // rows.cu
 // Build the context of `rank` for the resident hierarchy: ownership, lists,

@@ -178,11 +178,43 @@ void rows_coarse_owner(int64_t nc, const int64_t* pt_ptr, const int32_t* pt_idx,
   }
 }
 
+FlowRecView flow_rec_view(const unsigned char* rec) {
+  FlowRecView v{};
+  const int32_t* hd = reinterpret_cast<const int32_t*>(rec);
+  v.k = hd[0];
+  v.e0 = hd[1];
+  v.nt = hd[2];
+  const int k4 = (v.k + 3) & ~3, kp4 = (v.k + 1 + 3) & ~3;
+  const int o_dof = 16 + 4 * 8, o_ts = o_dof + 4 * k4, o_xp = o_ts + 4 * kp4, o_binv = o_xp + 4 * k4,
+            o_slot = o_binv + 8 * v.k * v.k;
+  v.dof = reinterpret_cast<const int32_t*>(rec + o_dof);
+  v.ts = reinterpret_cast<const int32_t*>(rec + o_ts);
+  v.xpart = reinterpret_cast<const int32_t*>(rec + o_xp);
+  v.tslot = reinterpret_cast<const int32_t*>(rec + o_slot);
+  return v;
+}
+
 void rows_shares(const RowsHostLevel& L, int nranks, std::vector<RowsShare>& out) {
   out.assign((size_t)nranks, RowsShare{});
   for (int64_t u = 0; u < L.n; ++u) out[(size_t)L.owner[(size_t)u]].rows.push_back((int32_t)u);
   if (!L.split) return;
   const int64_t W = L.nwave;
+  if (L.fw) {
+    // execution order of direction d: waves ascending (0) / descending (1), patches ascending inside
+    for (int d = 0; d < 2; ++d) {
+      for (int r = 0; r < nranks; ++r) out[(size_t)r].foff[d].assign((size_t)W + 1, 0);
+      int64_t pos = 0;
+      for (int64_t s0 = 0; s0 < W; ++s0) {
+        const int64_t w = d == 0 ? s0 : W - 1 - s0;
+        for (int64_t t = L.wave_ptr[(size_t)w]; t < L.wave_ptr[(size_t)w + 1]; ++t, ++pos) {
+          const int32_t first = L.patch_dofs[(size_t)L.patch_ptr[(size_t)t]];
+          out[(size_t)L.owner[(size_t)first]].fpos[d].push_back(pos);
+        }
+        for (int r = 0; r < nranks; ++r) out[(size_t)r].foff[d][(size_t)s0 + 1] = (int64_t)out[(size_t)r].fpos[d].size();
+      }
+    }
+    return;
+  }
   for (int r = 0; r < nranks; ++r) {
     out[(size_t)r].poff.assign((size_t)W + 1, 0);
     for (int d = 0; d < 2; ++d) out[(size_t)r].goff[d].assign((size_t)W + 1, 0);
@@ -228,6 +260,14 @@ void level_steps(const std::vector<RowsHostLevel>& lv, size_t ell, std::vector<R
     w.dir = dir;
     out.push_back(w);
   };
+  auto fwave = [&](int dir, int64_t s0) {
+    RStep w{};
+    w.kind = RK_FWAVE;
+    w.level = (int)ell;
+    w.dir = dir;
+    w.dst = s0;
+    out.push_back(w);
+  };
   auto spmv = [&](int mat, int epi) {
     RStep m{};
     m.kind = RK_SPMV;
@@ -236,22 +276,44 @@ void level_steps(const std::vector<RowsHostLevel>& lv, size_t ell, std::vector<R
     m.epi = epi;
     out.push_back(m);
   };
-  if (W > 0) {
-    wave(true, 0, -1, 0);
-    for (int64_t d = 1; d < W; ++d) wave(false, d, d - 1, 0);
+  auto leg = [&](bool down) {
+    RStep g{};
+    g.kind = RK_LEG;
+    g.level = (int)ell;
+    g.down = down;
+    out.push_back(g);
+  };
+  // down leg
+  if (!L.split) {
+    leg(true);  // agglomerated: one step, whatever kernels the single-GPU solve picks
+  } else if (L.fw) {
+    for (int64_t s0 = 0; s0 < W; ++s0) fwave(0, s0);
+    spmv(0, RE_RES_JAC);
+    spmv(0, RE_JAC_BW);
   } else {
-    st.kind = RK_INIT_RB;
+    if (W > 0) {
+      wave(true, 0, -1, 0);
+      for (int64_t d = 1; d < W; ++d) wave(false, d, d - 1, 0);
+    } else {
+      st.kind = RK_INIT_RB;
+      out.push_back(st);
+    }
+    st.kind = RK_FW_FINAL;
     out.push_back(st);
+    spmv(0, RE_JAC_FW);
   }
-  st.kind = RK_FW_FINAL;
-  out.push_back(st);
-  spmv(0, RE_JAC_FW);
   spmv(2, RE_SET);
   level_steps(lv, ell + 1, out);
   spmv(1, RE_ADD);
-  spmv(0, RE_RES_JAC);
-  spmv(0, RE_JAC_BW);
-  for (int64_t d = W - 1; d >= 0; --d) wave(false, d, d == W - 1 ? -1 : d + 1, 1);
+  // up leg
+  if (!L.split) {
+    leg(false);
+  } else {
+    spmv(0, RE_RES_JAC);
+    spmv(0, RE_JAC_BW);
+    if (L.fw) for (int64_t s0 = 0; s0 < W; ++s0) fwave(1, s0);
+    else for (int64_t d = W - 1; d >= 0; --d) wave(false, d, d == W - 1 ? -1 : d + 1, 1);
+  }
 }
 
 RStep simple(int kind, int site = 0, int vec = -1, int epi = 0) {
@@ -304,6 +366,7 @@ void rows_access(const RStep& st, const std::vector<RowsHostLevel>& lv, const st
   const int vX = ell == 0 ? rows_vec_ws(depth, WS_Z) : rows_vec_level(ell, LV_X);
   const int vR = rows_vec_level(ell, LV_R), vDJ = rows_vec_level(ell, LV_DJ);
   const int vD[2] = {rows_vec_level(ell, LV_D0), rows_vec_level(ell, LV_D1)};
+  const int vDW = rows_vec_level(ell, LV_DW);
   const int vRed = rows_vec_red(depth);
   for (int q = 0; q < nranks; ++q) {
     PlanAccess& a = acc[(size_t)q];
@@ -410,6 +473,39 @@ void rows_access(const RStep& st, const std::vector<RowsHostLevel>& lv, const st
         }
         break;
       }
+      case RK_FWAVE: {
+        const int d = st.dir;
+        const int r0 = d == 0 ? vB : vR;
+        const RowsShare& sq = sh[(size_t)ell][(size_t)q];
+        for (int64_t t = sq.foff[d][(size_t)st.dst]; t < sq.foff[d][(size_t)st.dst + 1]; ++t) {
+          const FlowRecView v = flow_rec_view(L.recs[d].data() + L.rec_off[d][(size_t)sq.fpos[d][(size_t)t]]);
+          for (int a = 0; a < v.k; ++a) {
+            const int32_t u = v.dof[a], xp = v.xpart[a];
+            R(r0, u);
+            if (d == 1 && xp != -1) R(vX, u);
+            for (int32_t tt = v.ts[a]; tt < v.ts[a + 1]; ++tt) R(vDW, v.tslot[tt]);
+            Wr(vDW, v.e0 + a);
+            if (xp >= 0 || xp == -2) Wr(vX, u);
+          }
+        }
+        break;
+      }
+      case RK_LEG: {
+        // a whole leg of an agglomerated level on every rank: reads the level's right-hand side
+        // (and iterate, going up), defines every working vector of the level
+        for (int64_t u = 0; u < L.n; ++u) {
+          R(vB, u);
+          if (!st.down) R(vX, u);
+        }
+        for (int64_t u = 0; u < L.n; ++u) {
+          Wr(vX, u);
+          Wr(vR, u);
+          Wr(vDJ, u);
+          Wr(vD[0], u);
+          Wr(vD[1], u);
+        }
+        break;
+      }
       case RK_FW_FINAL: {
         const int64_t W = L.nwave;
         const int dsrc = W > 0 ? vD[(W - 1) & 1] : -1;
@@ -488,6 +584,8 @@ bool step_partitioned(const RStep& st, const std::vector<RowsHostLevel>& lv) {
       if (st.epi == RE_AP || st.epi == RE_PCG_INIT) return lv[0].split;
       return lv[(size_t)st.level].split;
     case RK_WAVE:
+    case RK_FWAVE:
+    case RK_LEG:
     case RK_FW_FINAL:
     case RK_INIT_RB: return lv[(size_t)st.level].split;
     default: return lv[0].split;
@@ -501,7 +599,8 @@ void rows_plan_all(const std::vector<RowsHostLevel>& lv, const std::vector<std::
   const int depth = (int)lv.size();
   std::vector<int64_t> len((size_t)rows_vec_count(depth), 0);
   for (int l = 0; l < depth; ++l)
-    for (int k = 0; k < LV_COUNT; ++k) len[(size_t)rows_vec_level(l, k)] = lv[(size_t)l].n;
+    for (int k = 0; k < LV_COUNT; ++k)
+      len[(size_t)rows_vec_level(l, k)] = k == LV_DW ? std::max<int64_t>(lv[(size_t)l].ne, 1) : lv[(size_t)l].n;
   for (int k = 0; k < WS_COUNT; ++k) len[(size_t)rows_vec_ws(depth, k)] = lv[0].n;
   len[(size_t)rows_vec_red(depth)] = (int64_t)RS_COUNT * 2 * nranks;
   PlanState st;

@@ -267,6 +267,7 @@ struct SpmvArgs {
   double* part2;
   double* hist;
   unsigned long long cond;
+  const DSell* sell;    // row partition: sliced-ELLPACK copy of exactly the listed rows (host-side pointer)
   const int32_t* rows;  // row partition: this rank's rows (nrows of them); null: rows [0, nrows)
   double* red;          // row partition: the rank's partial sum(s) go here, k_finish completes the reduction
 };
@@ -390,7 +391,8 @@ __global__ void __launch_bounds__(kThreads) k_spmv_sell(SpmvArgs a, const int64_
        sl += ((int64_t)gridDim.x * kThreads) >> 5) {
     const int64_t base = soff[sl];
     const int width = (int)((soff[sl + 1] - base) >> 5);
-    const int64_t row = sl * 32 + lane;
+    const int64_t q = sl * 32 + lane;
+    const int64_t row = a.rows ? (q < a.nrows ? (int64_t)a.rows[q] : 0) : q;
     const int32_t* ip = sidx + base + lane;
     const double* vp = sval + base + lane;
     double acc[G];
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(kThreads) k_spmv_sell(SpmvArgs a, const int64_
     for (int o = G / 2; o; o >>= 1)
 #pragma unroll
       for (int g = 0; g < o; ++g) acc[g] += acc[g + o];
-    if (row < a.nrows) spmv_epi<E>(a, row, acc[0], part, part2);
+    if (q < a.nrows) spmv_epi<E>(a, row, acc[0], part, part2);
   }
   if (E < EPI_AP) return;
   spmv_reduce<E>(a, part, part2);
@@ -619,8 +621,9 @@ unsigned spmv(const DCsr& M, SpmvArgs a, cudaStream_t s) {
   a.idx = M.idx.p;
   a.val = M.val.p;
   const int G = group_for(M);
-  if (M.sell && !a.rows && (G == 4 || G == 8)) {
-    const DSell& S = *M.sell;
+  const DSell* sell = a.rows ? a.sell : M.sell.get();
+  if (sell && (G == 4 || G == 8)) {
+    const DSell& S = *sell;
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((S.nslice + 7) / 8, kSMs * 8));
     if (G == 4) k_spmv_sell<4, E><<<grid, kThreads, 0, s>>>(a, S.soff.p, S.idx.p, S.val.p);
     else k_spmv_sell<8, E><<<grid, kThreads, 0, s>>>(a, S.soff.p, S.idx.p, S.val.p);
@@ -637,20 +640,26 @@ unsigned vec_grid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<in
 }  // namespace
 
 namespace {
-__global__ void k_sell_width(const int64_t* __restrict__ ptr, int64_t nrows, int64_t nsl, int64_t* __restrict__ w) {
+__global__ void k_sell_width(const int64_t* __restrict__ ptr, const int32_t* __restrict__ rows, int64_t nrows,
+                             int64_t nsl, int64_t* __restrict__ w) {
   for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < nsl; sl += (int64_t)gridDim.x * blockDim.x) {
     int64_t m = 0;
-    for (int64_t r = sl * 32; r < min(nrows, sl * 32 + 32); ++r) m = max(m, ptr[r + 1] - ptr[r]);
+    for (int64_t q = sl * 32; q < min(nrows, sl * 32 + 32); ++q) {
+      const int64_t r = rows ? (int64_t)rows[q] : q;
+      m = max(m, ptr[r + 1] - ptr[r]);
+    }
     w[sl] = 32 * m;
   }
 }
 __global__ void k_sell_fill(const int64_t* __restrict__ ptr, const int32_t* __restrict__ idx,
-                            const double* __restrict__ val, int64_t nrows, int64_t nsl,
+                            const double* __restrict__ val, const int32_t* __restrict__ rows, int64_t nrows,
+                            int64_t nsl,
                             const int64_t* __restrict__ soff, int32_t* __restrict__ sidx, double* __restrict__ sval) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nsl * 32; t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t sl = t >> 5, base = soff[sl];
     const int lane = (int)(t & 31), width = (int)((soff[sl + 1] - base) >> 5);
-    const int64_t e0 = t < nrows ? ptr[t] : 0, e1 = t < nrows ? ptr[t + 1] : 0;
+    const int64_t r = t < nrows ? (rows ? (int64_t)rows[t] : t) : 0;
+    const int64_t e0 = t < nrows ? ptr[r] : 0, e1 = t < nrows ? ptr[r + 1] : 0;
     for (int j = 0; j < width; ++j) {
       const bool ok = e0 + j < e1;
       sidx[base + (int64_t)j * 32 + lane] = ok ? idx[e0 + j] : -1;
@@ -660,27 +669,34 @@ __global__ void k_sell_fill(const int64_t* __restrict__ ptr, const int32_t* __re
 }
 }  // namespace
 
-// Give M the sliced-ELLPACK copy its SpMVs run on, when its rows are short
-// (the 4- and 8-lane classes of group_for) and the padding stays below 50 %.
-void build_sell(DCsr& M, cudaStream_t s) {
-  M.sell.reset();
+// Sliced-ELLPACK copy of M's rows (all of them, or the listed ones in list
+// order), when they are short (the 4- and 8-lane classes of group_for) and
+// the padding stays below 50 %.
+std::unique_ptr<DSell> build_sell_rows(const DCsr& M, const int32_t* rows, int64_t nrows, cudaStream_t s) {
   const int G = group_for(M);
-  if (M.nrows < 4096 || (G != 4 && G != 8)) return;
-  const int64_t nsl = (M.nrows + 31) / 32;
+  if (nrows < 1 || (G != 4 && G != 8)) return nullptr;
+  const int64_t nsl = (nrows + 31) / 32;
   DBuf<int64_t> w(nsl, s);
-  k_sell_width<<<grid_for(nsl, 256), 256, 0, s>>>(M.ptr.p, M.nrows, nsl, w.p);
+  k_sell_width<<<grid_for(nsl, 256), 256, 0, s>>>(M.ptr.p, rows, nrows, nsl, w.p);
   HC_CHECK_LAUNCH();
   std::unique_ptr<DSell> S(new DSell());
   S->nslice = nsl;
   S->soff.alloc(nsl + 1, s);
   S->padded = exclusive_scan(w.p, S->soff.p, nsl, s);
-  if (S->padded > M.nnz + M.nnz / 2) return;
+  const int64_t share = rows ? (int64_t)((double)M.nnz * (double)nrows / (double)std::max<int64_t>(M.nrows, 1)) : M.nnz;
+  if (S->padded > 2 * share + 32 * 16) return nullptr;
   S->idx.alloc(std::max<int64_t>(S->padded, 1), s);
   S->val.alloc(std::max<int64_t>(S->padded, 1), s);
-  k_sell_fill<<<grid_for(nsl * 32, 256), 256, 0, s>>>(M.ptr.p, M.idx.p, M.val.p, M.nrows, nsl, S->soff.p, S->idx.p,
-                                                      S->val.p);
+  k_sell_fill<<<grid_for(nsl * 32, 256), 256, 0, s>>>(M.ptr.p, M.idx.p, M.val.p, rows, nrows, nsl, S->soff.p,
+                                                      S->idx.p, S->val.p);
   HC_CHECK_LAUNCH();
-  M.sell = std::move(S);
+  return S;
+}
+
+void build_sell(DCsr& M, cudaStream_t s) {
+  M.sell.reset();
+  if (M.nrows < 4096) return;
+  M.sell = build_sell_rows(M, nullptr, M.nrows, s);
 }
 
 void Workspace::ensure(int64_t n_, int64_t maxit, cudaStream_t s) {
@@ -832,6 +848,18 @@ static int64_t record_leg_waves(DevLevel& L, const double* b, double* x, const i
 // (tests lower it to exercise the streaming paths on small cases).
 int64_t coarse_gemv_min() { return opts().coarse_gemv_min; }
 
+// Which leg kernels run on a level under the handle's options: the record-
+// streaming wavefront launches on very wide schedules, the dataflow leg on
+// deep narrow ones, else AUTO (cluster / grid leg by width) or the forced mode.
+int leg_mode(const DevLevel& L) {
+  int m = opts().sweep;
+  if (m == SWEEP_AUTO && smoother_wave_auto(L.sm)) m = SWEEP_FWAVE;
+  if (m == SWEEP_FWAVE && !(L.sm.fl.built && flow_wave_ok(L.sm.kmax, L.sm.fl.recmax))) m = SWEEP_WAVE;
+  if (m == SWEEP_AUTO && smoother_flow_auto(L.sm) && L.sm.fl.built) m = SWEEP_FLOW;
+  if (m == SWEEP_FLOW && !L.sm.fl.built) m = SWEEP_GRID;  // a DoF in > 2 patches (or not prepared)
+  return m;
+}
+
 // One piece of a level's V-cycle work (separately launchable for profiling).
 int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* x, const int* stop, cudaStream_t s,
                      int part) {
@@ -908,9 +936,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
   }
   const bool down = pc == PC_DOWN;
   const bool wide = smoother_wide(L.sm);
-  int m = opts().sweep;
-  if (m == SWEEP_AUTO && smoother_wave_auto(L.sm)) m = SWEEP_FWAVE;
-  if (m == SWEEP_FWAVE && !(L.sm.fl.built && flow_wave_ok(L.sm.kmax, L.sm.fl.recmax))) m = SWEEP_WAVE;
+  int m = leg_mode(L);
   if (m == SWEEP_FWAVE) {
     Smoother& sm = L.sm;
     FlowProgram& fl = sm.fl;
@@ -959,8 +985,6 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     }
     return W + 2;
   }
-  if (m == SWEEP_AUTO && smoother_flow_auto(L.sm) && L.sm.fl.built) m = SWEEP_FLOW;
-  if (m == SWEEP_FLOW && !L.sm.fl.built) m = SWEEP_GRID;  // a DoF in > 2 patches (or not prepared)
   if (m == SWEEP_FLOW) {
     Smoother& sm = L.sm;
     FlowProgram& fl = sm.fl;
@@ -1216,6 +1240,26 @@ int64_t rows_launch_step(const RStep& st, RowsCtx& rc, std::vector<DevLevel*>& l
   switch (st.kind) {
     case RK_COARSE:
       return record_piece(PC_COARSE, L, nullptr, b, x, stop, s);
+    case RK_LEG:
+      return record_piece(st.down ? PC_DOWN : PC_UP, L, nullptr, b, x, stop, s);
+    case RK_FWAVE: {
+      Smoother& sm = L.sm;
+      FlowArgs fa{};
+      fa.stop = stop;
+      fa.n = L.n;
+      fa.nwave = sm.nwave;
+      fa.ne = sm.fl.ne;
+      fa.npatch = sm.npatch;
+      fa.recmax = sm.fl.recmax;
+      fa.recs = D.frecs[st.dir].p;          // this rank's records, compacted
+      fa.rec_off = D.frec_off[st.dir].p;
+      fa.d = sm.fl.dw.p;
+      fa.x = x;
+      fa.r0 = st.dir == 0 ? b : L.r.p;
+      const int64_t i0 = D.foff[st.dir][(size_t)st.dst], i1 = D.foff[st.dir][(size_t)st.dst + 1];
+      launch_flow_wave(st.dir == 0, fa, i0, i1 - i0, s);
+      return i1 > i0 ? 1 : 0;
+    }
     case RK_INIT_RB: {
       const int64_t cnt = D.split ? D.nrows : L.n;
       k_init_rb<<<vec_grid(cnt), kThreads, 0, s>>>(stop, cnt, b, L.r.p, x, D.split ? D.rows.p : nullptr);
@@ -1255,6 +1299,7 @@ int64_t rows_launch_step(const RStep& st, RowsCtx& rc, std::vector<DevLevel*>& l
         if (D0.split) {
           a.rows = D0.rows.p;
           a.nrows = D0.nrows;
+          a.sell = D0.sA.get();
         }
         if (st.epi == RE_AP) {
           a.xin = w.p.p;
@@ -1275,6 +1320,7 @@ int64_t rows_launch_step(const RStep& st, RowsCtx& rc, std::vector<DevLevel*>& l
         if (D.split) {
           a.rows = DC.rows.p;
           a.nrows = DC.nrows;
+          a.sell = D.sPt.get();
         }
         a.xin = L.r.p;
         a.y = C.b.p;
@@ -1288,6 +1334,7 @@ int64_t rows_launch_step(const RStep& st, RowsCtx& rc, std::vector<DevLevel*>& l
       if (D.split) {
         a.rows = D.rows.p;
         a.nrows = D.nrows;
+        a.sell = st.mat == 1 ? D.sP.get() : D.sA.get();
       }
       if (st.mat == 1) {  // x += P x_c
         DevLevel& C = *lv[(size_t)st.level + 1];
