@@ -90,8 +90,7 @@ int hcamg_version(void);
  * Select code paths per handle (they seed from the HCAMG_* environment at
  * hcamg_create).  Keys: "sweep" (smoothing leg: 0 auto, 1 cluster leg, 2 grid
  * leg, 3 one launch per wavefront, 4 dataflow leg, 5 one launch per wavefront
- * over the dataflow records, 6 single-CTA leg with the vectors in shared memory),
- * "giant_min" (dense-regime
+ * over the dataflow records), "giant_min" (dense-regime
  * cutoff, reference transfer.py:35 _DENSE_COMPONENT_CUTOFF = 4096),
  * "coarse_gemv_min" (coarsest solve streams its inverse from this size on),
  * "coarse_symv" (packed-triangle coarsest solve), "factor_apply" (apply the dense

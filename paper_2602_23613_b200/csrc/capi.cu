@@ -619,7 +619,7 @@ int hcamg_set_option(hcamg_handle* h, const char* key, double value) {
     if (k->i) {
       require(value == (double)(int)value, std::string("option ") + key + " takes an integer");
       if (k->i == &Options::sweep) {
-        require(value >= SWEEP_AUTO && value <= SWEEP_SOLO, "sweep mode out of range");
+        require(value >= SWEEP_AUTO && value <= SWEEP_FWAVE, "sweep mode out of range");
         if (value == SWEEP_FLOW || value == SWEEP_FWAVE)  // the dataflow terms are built on first request
           for (auto& l : h->levels)
             if (!l->coarsest && l->l1.p) build_flow(l->A, l->sm, h->stream);

@@ -180,7 +180,6 @@ enum SweepMode : int {
   SWEEP_WAVE = 3,     // one launch per wavefront
   SWEEP_FLOW = 4,     // dataflow leg: per-patch ready counters, no wave barriers
   SWEEP_FWAVE = 5,    // one launch per wavefront over the dataflow records (wide 2D schedules)
-  SWEEP_SOLO = 6,     // one CTA, the level's vectors in shared memory (levels of a few thousand DoFs)
 };
 struct Options {
   int sweep = SWEEP_AUTO;

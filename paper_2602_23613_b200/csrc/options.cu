@@ -23,7 +23,7 @@ Options options_from_env() {
   if (const char* e = getenv("HCAMG_SWEEP")) {
     const std::string m(e);
     o.sweep = m == "leg" || m == "cluster" ? SWEEP_LEG : m == "grid" ? SWEEP_GRID : m == "wave" ? SWEEP_WAVE
-              : m == "flow" ? SWEEP_FLOW : m == "fwave" ? SWEEP_FWAVE : m == "solo" ? SWEEP_SOLO : SWEEP_AUTO;
+              : m == "flow" ? SWEEP_FLOW : m == "fwave" ? SWEEP_FWAVE : SWEEP_AUTO;
   }
   o.giant_min = env_i("HCAMG_GIANT_MIN", o.giant_min);
   o.coarse_gemv_min = env_i("HCAMG_COARSE_GEMV_MIN", o.coarse_gemv_min);

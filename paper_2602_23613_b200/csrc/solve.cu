@@ -857,10 +857,6 @@ int leg_mode(const DevLevel& L) {
   if (m == SWEEP_FWAVE && !(L.sm.fl.built && flow_wave_ok(L.sm.kmax, L.sm.fl.recmax))) m = SWEEP_WAVE;
   if (m == SWEEP_AUTO && smoother_flow_auto(L.sm) && L.sm.fl.built) m = SWEEP_FLOW;
   if (m == SWEEP_FLOW && !L.sm.fl.built) m = SWEEP_GRID;  // a DoF in > 2 patches (or not prepared)
-  // small levels: one CTA with the vectors in shared memory (a forced "solo" falls back to the
-  // cluster leg where the level does not fit)
-  if (m == SWEEP_AUTO && !smoother_wide(L.sm) && leg_solo_ok(L.n, L.sm.nwave)) m = SWEEP_SOLO;
-  if (m == SWEEP_SOLO && !leg_solo_ok(L.n, L.sm.nwave)) m = SWEEP_LEG;
   return m;
 }
 
@@ -1032,7 +1028,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     }
     return 3;
   }
-  if (m == SWEEP_AUTO || m == SWEEP_LEG || m == SWEEP_GRID || m == SWEEP_SOLO) {
+  if (m == SWEEP_AUTO || m == SWEEP_LEG || m == SWEEP_GRID) {
     Smoother& sm = L.sm;
     SweepProgram& pg = sm.pg;
     LegArgs la{};
@@ -1080,8 +1076,7 @@ int64_t record_piece(int pc, DevLevel& L, DevLevel* C, const double* b, double* 
     la.dj = L.dj.p;
     la.trace = g_leg_trace;
     la.gbar = pg.gbar.p;
-    if (m == SWEEP_SOLO) launch_leg_solo(down, la, s);
-    else if ((m == SWEEP_AUTO && wide) || m == SWEEP_GRID) launch_leg_grid(down, la, s);
+    if ((m == SWEEP_AUTO && wide) || m == SWEEP_GRID) launch_leg_grid(down, la, s);
     else launch_leg(down, la, s);
     return 1;
   }

@@ -68,9 +68,6 @@ struct FlowArgs {
   int gates;                  // wait on the latest-wave predecessors first (1) or poll every term (0)
   long long* trace;           // debug: per execution position {record ready, pulls done, stored, warp} (globaltimer)
 };
-// single-CTA leg with the level's vectors in shared memory (small levels)
-bool leg_solo_ok(int64_t n, int64_t nwave);
-void launch_leg_solo(bool down, const LegArgs& args, cudaStream_t s);
 void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s);
 // wave-parallel sweep over the same records (mode "fwave"): one launch per wavefront
 void launch_flow_wave(bool down, const FlowArgs& args, int64_t i0, int64_t cnt, cudaStream_t s);

@@ -237,18 +237,11 @@ __device__ void solve_patch_slow(const LegArgs& a, int dir, int64_t p, int lane,
   }
 }
 
-// kMode = 2 ("solo"): one CTA, the vectors on the sweep's dependency chain (the
-// residual and both correction buffers) in shared memory for the whole leg: on
-// levels of a few thousand DoFs a wavefront then costs a __syncthreads and
-// shared-memory latency instead of a cluster barrier and an L2 round trip
-// (config 1's level 0: 22 waves at 2.8 us each in the cluster leg).  x and the
-// Jacobi step stay in global memory: they are accumulated, never waited for.
 // kGrid = false: one 16-CTA cluster (split barrier.cluster); kGrid = true: the
 // whole GPU as one cooperative grid (grid.sync), for levels whose waves are
 // wider than a cluster.
-template <bool kDown, int kMode = 0>
+template <bool kDown, bool kGrid = false>
 __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
-  constexpr bool kGrid = kMode == 1, kSolo = kMode == 2;
   if (*a.stop) return;
   // Grid barrier in two halves (arrive / wait) so the next phase's index
   // prefetch overlaps the barrier latency, as the cluster barrier does.  The
@@ -260,7 +253,6 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
     unsigned* bar;
     unsigned old;
     __device__ void arrive() {
-      if (kSolo) return;
       if (kGrid) {
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -272,10 +264,6 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
       }
     }
     __device__ void wait() {
-      if (kSolo) {
-        __syncthreads();
-        return;
-      }
       if (kGrid) {
         if (threadIdx.x == 0) {
           unsigned cur;
@@ -292,21 +280,14 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
       arrive();
       wait();
     }
-    __device__ unsigned rank() const { return kSolo ? 0u : kGrid ? blockIdx.x : cl.block_rank(); }
-    __device__ unsigned blocks() const { return kSolo ? 1u : kGrid ? gridDim.x : cl.num_blocks(); }
+    __device__ unsigned rank() const { return kGrid ? blockIdx.x : cl.block_rank(); }
+    __device__ unsigned blocks() const { return kGrid ? gridDim.x : cl.num_blocks(); }
   } cl{cg::this_cluster(), a.gbar, 0u};
   extern __shared__ int64_t sh_ptrs[];  // wave_ptr (W+1) then gen_ptr (W+1)
   const int64_t W = a.nwave, n = a.n;
   int64_t* wp = sh_ptrs;
   int64_t* gp = sh_ptrs + W + 1;
   const int dir = kDown ? 0 : 1;
-  double* const gr = a.r;
-  if (kSolo) {  // r, d0, d1 live in shared memory; r (going down) goes out at the end
-    double* sv = reinterpret_cast<double*>(sh_ptrs + 2 * (W + 1));
-    a.r = sv;
-    a.d0 = sv + n;
-    a.d1 = sv + 2 * n;
-  }
   for (int64_t t = threadIdx.x; t <= W; t += blockDim.x) {
     wp[t] = a.wave_ptr[t];
     gp[t] = kDown ? a.gen_fw_ptr[t] : a.gen_bw_ptr[t];
@@ -451,7 +432,6 @@ __global__ void __launch_bounds__(kLegThreads, 1) k_leg(LegArgs a) {
     double s = 0.0;
     for (int64_t e = a.ap[u]; e < a.ap[u + 1]; ++e) s = fma(a.av[e], a.dj[a.ai[e]], s);
     a.r[u] -= s;
-    if (kSolo) gr[u] = a.r[u];
   }
 }
 
@@ -494,8 +474,8 @@ void launch_leg_grid(bool down, const LegArgs& args, cudaStream_t s) {
   static int per_sm = 0;
   if (!per_sm) {
     int a = 0, b = 0;
-    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_leg<true, 1>, kLegThreads, 16 * 1024));
-    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_leg<false, 1>, kLegThreads, 16 * 1024));
+    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_leg<true, true>, kLegThreads, 16 * 1024));
+    HC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_leg<false, true>, kLegThreads, 16 * 1024));
     per_sm = std::max(1, std::min(a, b));
   }
   require(smem <= 16 * 1024, "too many wavefronts for the grid leg");
@@ -518,8 +498,8 @@ void launch_leg_grid(bool down, const LegArgs& args, cudaStream_t s) {
   static const int l2pf = getenv("HCAMG_LEG_L2PF") ? std::max(0, atoi(getenv("HCAMG_LEG_L2PF"))) : 1;
   LegArgs ga = args;
   ga.l2pf = l2pf;
-  if (down) HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<true, 1>, ga));
-  else HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<false, 1>, ga));
+  if (down) HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<true, true>, ga));
+  else HC_CUDA(cudaLaunchKernelEx(&cfg, k_leg<false, true>, ga));
 }
 
 // Largest cluster the leg can use on this device: 16 (non-portable) when
@@ -546,24 +526,6 @@ int sweep_cluster_size() {
   cudaGetLastError();
   c = best;
   return c;
-}
-
-// levels the single-CTA leg takes: three vectors and the wave pointers within a CTA's shared memory
-bool leg_solo_ok(int64_t n, int64_t nwave) {
-  return n > 0 && (size_t)n * 24 + sizeof(int64_t) * 2 * (size_t)(nwave + 1) <= 200 * 1024;
-}
-
-void launch_leg_solo(bool down, const LegArgs& args, cudaStream_t s) {
-  const size_t smem = sizeof(int64_t) * 2 * (size_t)(args.nwave + 1) + (size_t)args.n * 24;
-  static size_t attr = 0;
-  if (smem > attr) {
-    HC_CUDA(cudaFuncSetAttribute(k_leg<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    HC_CUDA(cudaFuncSetAttribute(k_leg<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
-  if (down) k_leg<true, 2><<<1, kLegThreads, smem, s>>>(args);
-  else k_leg<false, 2><<<1, kLegThreads, smem, s>>>(args);
-  HC_CHECK_LAUNCH();
 }
 
 void launch_leg(bool down, const LegArgs& args, cudaStream_t s) {

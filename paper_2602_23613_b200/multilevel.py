@@ -251,7 +251,7 @@ class _Device:
         raise AttributeError(name)
 
 
-SWEEP_MODES = {"auto": 0, "leg": 1, "grid": 2, "wave": 3, "flow": 4, "fwave": 5, "solo": 6}
+SWEEP_MODES = {"auto": 0, "leg": 1, "grid": 2, "wave": 3, "flow": 4, "fwave": 5}
 
 
 def _level_matrix(dev, idx):

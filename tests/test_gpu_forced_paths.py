@@ -38,7 +38,7 @@ VARIANTS = {
     # (transfer.py:100-116; round 1 raised NotImplementedError)
     "multi_giant": {"giant_min": 4, "coarse_gemv_min": 0},
 }
-SWEEPS = ["grid", "wave", "leg", "flow", "fwave", "solo"]
+SWEEPS = ["grid", "wave", "leg", "flow", "fwave"]
 
 
 def rel(a, b):

@@ -140,7 +140,7 @@ def test_smooth_matches_oracle_all_legs():
     l1o = O.l1_diag(s.A)
     rng = np.random.default_rng(4)
     x0, b = rng.standard_normal((2, s.n))
-    for sweep in ("auto", "leg", "grid", "wave", "flow", "fwave", "solo"):
+    for sweep in ("auto", "leg", "grid", "wave", "flow", "fwave"):
         ps._dev.set_option("sweep", P.multilevel.SWEEP_MODES[sweep])
         for d in ("forward", "backward", "symmetric"):
             xg = smooth(s.A, ps, None, x0, b, d)
