@@ -173,8 +173,9 @@ void rows_prepare(RowsCtx& rc, std::vector<DevLevel*>& lv, Workspace& w, int ran
   bool finer = true;
   rc.stats = RowsStats{};
   for (int l = 0; l < depth; ++l) {
-    H[(size_t)l].split = finer && !H[(size_t)l].coarsest && H[(size_t)l].n >= std::max<int64_t>(min_rows, 1) &&
-                         lv[(size_t)l]->pt_seg.nseg == 0;
+    // (a level whose P^T has long rows -- 3D levels below the dense-regime cutoff -- is split too:
+    // its restriction runs the row-list SpMV instead of the segmented single-GPU plan)
+    H[(size_t)l].split = finer && !H[(size_t)l].coarsest && H[(size_t)l].n >= std::max<int64_t>(min_rows, 1);
     finer = H[(size_t)l].split;
     rc.stats.split_levels += H[(size_t)l].split ? 1 : 0;
   }

@@ -27,7 +27,9 @@ from paper_2602_23613_b200 import dist, tri2d
 
 pytestmark = pytest.mark.gpu
 
-SPARSE_CASES = ["tri3s_alg", "tri5s_alg", "tri5s_ref", "quad3_alg"]
+# 2D hierarchies (6-DoF vertex patches, sparse P) and 3D Kuhn ones below the dense-regime cutoff
+# (patches of up to 14 DoFs: the 16-lane wave kernels; CSR interpolation with long rows)
+SPARSE_CASES = ["tri3s_alg", "tri5s_alg", "tri5s_ref", "quad3_alg", "kuhn4_c1", "kuhn8_c1"]
 
 
 def build(c, n, sweep="wave"):
@@ -55,7 +57,13 @@ def test_emulated_vcycle_bit_identical(name, nranks, sweep):
         assert info["segments"]["vcycle"]["push_all"] > 0
     for r in range(nranks):
         assert np.all(np.isfinite(Z[r])), f"rank {r} read an entry it never received"
-        assert np.array_equal(Z[r], zref), f"rank {r}: max diff {np.max(np.abs(Z[r] - zref))}"
+        if name.startswith("kuhn8"):
+            # P^T has rows of thousands of entries here: the single GPU restricts through its
+            # segmented plan (256-entry partial sums), the partition through the row-list SpMV
+            assert np.array_equal(Z[r], Z[0])
+            assert np.max(np.abs(Z[r] - zref)) <= 1e-10 * np.max(np.abs(zref))
+        else:
+            assert np.array_equal(Z[r], zref), f"rank {r}: max diff {np.max(np.abs(Z[r] - zref))}"
     # the handles go back to the single-GPU solve, bit-identical
     for h in hs:
         dist.undistribute_rows(h)
