@@ -273,7 +273,8 @@ int hcamg_rows_disconnect(hcamg_handle* h);
 int hcamg_rows_info(hcamg_handle* h, int64_t* out, int32_t cap);
 /* Lockstep emulation of an n-rank partitioned solve on ONE GPU (tests): hs = n handles
  * of this process holding the same hierarchy, prepared as ranks 0..n-1 and connected with
- * hcamg_rows_connect_ptrs.  kind 0: z = V(b); kind 1: PCG from x0 = 0.  x: n x n0 doubles,
+ * hcamg_rows_connect_ptrs.  kind 0: z = V(b); kind 1: PCG from x0 = 0; kind 2: the
+ * stand-alone AMG iteration from x0 = 0.  x: n x n0 doubles,
  * row r = the full result as rank r holds it.  poison != 0 fills the working vectors with
  * NaN first (an entry neither computed nor received then shows). */
 int hcamg_rows_emulate(hcamg_handle* const* hs, int32_t n, int32_t kind, const double* b, double* x, double tol,

@@ -358,7 +358,8 @@ void build_loop_graph(hcamg_handle* h, Graph& G, bool pcg) {
                                         : cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault);
   if (ce == cudaSuccess) {
     HC_CUDA(cudaStreamBeginCaptureToGraph(s, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    int64_t lp = rows_on(h) ? rows_record(*h->rows, SEG_INIT, h->lv, w, &w.ctl.p->stop, 0, s) +
+    int64_t lp = rows_on(h) && !pcg ? rows_record(*h->rows, SEG_AMG_INIT, h->lv, w, &w.ctl.p->stop, 0, s)
+                 : rows_on(h) ? rows_record(*h->rows, SEG_INIT, h->lv, w, &w.ctl.p->stop, 0, s) +
                                   rows_record(*h->rows, SEG_FIRST, h->lv, w, &w.ctl.p->stop, 0, s)
                  : pcg ? record_pcg_init(*h->lv[0], w, b, nullptr, s, 0) + record_pcg_first(h->lv, w, s)
                        : record_amg_init(*h->lv[0], w, b, nullptr, s, 0);
@@ -378,7 +379,7 @@ void build_loop_graph(hcamg_handle* h, Graph& G, bool pcg) {
     HC_CUDA(cudaStreamUpdateCaptureDependencies(s, &cn, 1, cudaStreamSetCaptureDependencies));
     HC_CUDA(cudaStreamBeginCaptureToGraph(s2, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     const unsigned long long hc = (unsigned long long)cond;
-    int64_t lb = rows_on(h) ? rows_record(*h->rows, SEG_BODY, h->lv, w, &w.ctl.p->stop, hc, s2)
+    int64_t lb = rows_on(h) ? rows_record(*h->rows, pcg ? SEG_BODY : SEG_AMG_BODY, h->lv, w, &w.ctl.p->stop, hc, s2)
                  : pcg ? record_pcg_body(h->lv, w, s2, hc) : record_amg_body(h->lv, w, s2, hc);
     HC_CUDA(cudaStreamEndCapture(s2, &body));
     cudaGraph_t gout = nullptr;
@@ -400,13 +401,14 @@ void build_loop_graph(hcamg_handle* h, Graph& G, bool pcg) {
   // fallback: host-driven loop over a body graph
   cudaGraph_t gp = nullptr, gb = nullptr;
   HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  G.launches_pre = rows_on(h) ? rows_record(*h->rows, SEG_INIT, h->lv, w, &w.ctl.p->stop, 0, s) +
+  G.launches_pre = rows_on(h) && !pcg ? rows_record(*h->rows, SEG_AMG_INIT, h->lv, w, &w.ctl.p->stop, 0, s)
+                   : rows_on(h) ? rows_record(*h->rows, SEG_INIT, h->lv, w, &w.ctl.p->stop, 0, s) +
                                     rows_record(*h->rows, SEG_FIRST, h->lv, w, &w.ctl.p->stop, 0, s)
                    : pcg ? record_pcg_init(*h->lv[0], w, b, nullptr, s, 0) + record_pcg_first(h->lv, w, s)
                          : record_amg_init(*h->lv[0], w, b, nullptr, s, 0);
   HC_CUDA(cudaStreamEndCapture(s, &gp));
   HC_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  G.launches_body = rows_on(h) ? rows_record(*h->rows, SEG_BODY, h->lv, w, &w.ctl.p->stop, 0, s)
+  G.launches_body = rows_on(h) ? rows_record(*h->rows, pcg ? SEG_BODY : SEG_AMG_BODY, h->lv, w, &w.ctl.p->stop, 0, s)
                     : pcg ? record_pcg_body(h->lv, w, s, 0) : record_amg_body(h->lv, w, s, 0);
   HC_CUDA(cudaStreamEndCapture(s, &gb));
   HC_CUDA(cudaGraphInstantiate(&G.pre, gp, 0));
@@ -1119,7 +1121,6 @@ int hcamg_amg_solve(hcamg_handle* h, const double* b, const double* x0, double t
   return guarded(h, [&] {
     require_hierarchy(h);
     require(tol > 0, "tolerance must be positive");
-    if (rows_on(h)) throw Error(EUNSUPPORTED_, "amg_solve is not partitioned by rows; use pcg / vcycle");
     cudaStream_t s = h->stream;
     const int64_t n = h->levels[0]->n;
     prepare_loop(h, h->g_amg, false, maxit);
@@ -1129,6 +1130,7 @@ int hcamg_amg_solve(hcamg_handle* h, const double* b, const double* x0, double t
     set_ctl(h, tol, maxit);
     run_loop_graph(h, h->g_amg);
     zero_x_if_zero_rhs(h->ws, s);
+    if (rows_on(h)) rows_record(*h->rows, SEG_GATHER, h->lv, h->ws, h->ws.zero_flag.p, 0, s);
     HC_CUDA(cudaMemcpyAsync(x, h->ws.x.p, 8 * n, cudaMemcpyDeviceToHost, s));
     int error = 0;
     hcamg_report rep{};
@@ -1627,6 +1629,7 @@ int hcamg_rows_emulate(hcamg_handle* const* hs, int32_t n, int32_t kind, const d
         RowsCtx& rc = *h->rows;
         HC_CUDA(cudaMemsetAsync(rc.sym + kRowsFlagBytes, 0xff, rc.sym_bytes - kRowsFlagBytes, s));
       }
+      require(kind >= 0 && kind <= 2, "kind: 0 V-cycle, 1 PCG, 2 stand-alone AMG iteration");
       if (kind == 0) {
         HC_CUDA(cudaMemcpyAsync(h->ws.r.p, b, 8 * n0, cudaMemcpyHostToDevice, s));
       } else {
@@ -1641,14 +1644,18 @@ int hcamg_rows_emulate(hcamg_handle* const* hs, int32_t n, int32_t kind, const d
       for (int r = 0; r < n; ++r)
         HC_CUDA(cudaMemcpy(x + (size_t)r * n0, hs[r]->ws.z.p, 8 * n0, cudaMemcpyDeviceToHost));
     } else {
-      lockstep(hs, n, SEG_INIT, true);
-      lockstep(hs, n, SEG_FIRST, true);
+      if (kind == 1) {
+        lockstep(hs, n, SEG_INIT, true);
+        lockstep(hs, n, SEG_FIRST, true);
+      } else {
+        lockstep(hs, n, SEG_AMG_INIT, true);
+      }
       while (true) {
         int stop0 = read_scalar(&hs[0]->ws.ctl.p->stop, hs[0]->stream);
         for (int r = 1; r < n; ++r)
           require(read_scalar(&hs[r]->ws.ctl.p->stop, hs[r]->stream) == stop0, "ranks disagree on convergence");
         if (stop0) break;
-        lockstep(hs, n, SEG_BODY, true);
+        lockstep(hs, n, kind == 1 ? SEG_BODY : SEG_AMG_BODY, true);
       }
       for (int r = 0; r < n; ++r) {
         HandleScope sc(hs[r]);

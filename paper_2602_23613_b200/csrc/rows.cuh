@@ -90,17 +90,21 @@ enum RKind : int {
   RK_GATHER,       // no kernel: every rank reads the whole vector (all-gather through the push lists)
   RK_FWAVE,        // one wavefront of the sweep over the dataflow records (flow.cu k_flow_wave)
   RK_LEG,          // a whole smoothing leg of an agglomerated level, as the single-GPU solve runs it
+  RK_AXPY1,        // stand-alone AMG iteration: x += z
+  RK_GUARD,        // stand-alone AMG iteration: leave the device loop when the solve has stopped
 };
 
 // SpMV epilogues a step can ask for (numerically equal to solve.cu's Epi)
-enum REpi : int { RE_SET = 0, RE_ADD = 1, RE_JAC_FW = 2, RE_RES_JAC = 3, RE_JAC_BW = 4, RE_AP = 5, RE_PCG_INIT = 6 };
+enum REpi : int { RE_SET = 0, RE_ADD = 1, RE_JAC_FW = 2, RE_RES_JAC = 3, RE_JAC_BW = 4, RE_AP = 5, RE_PCG_INIT = 6,
+                  RE_AMG_INIT = 7, RE_AMG_RES = 8 };
 
 // reduction sites: (S, S2) per rank each
-enum RSite : int { RS_INIT = 0, RS_AP = 1, RS_UPD = 2, RS_RZ_FIRST = 3, RS_RZ = 4, RS_COUNT = 5 };
+enum RSite : int { RS_INIT = 0, RS_AP = 1, RS_UPD = 2, RS_RZ_FIRST = 3, RS_RZ = 4, RS_AMG = 5, RS_COUNT = 6 };
 
 // program segments; the planner canonicalises the state between them so the
 // body's push lists hold for every iteration of the PCG loop
-enum RSeg : int { SEG_VCYCLE = 0, SEG_INIT = 1, SEG_FIRST = 2, SEG_BODY = 3, SEG_GATHER = 4, SEG_COUNT = 5 };
+enum RSeg : int { SEG_VCYCLE = 0, SEG_INIT = 1, SEG_FIRST = 2, SEG_BODY = 3, SEG_GATHER = 4, SEG_AMG_INIT = 5,
+                  SEG_AMG_BODY = 6, SEG_COUNT = 7 };
 
 // vectors of a level / of the PCG workspace, as the planner numbers them
 enum RVec : int { LV_B = 0, LV_X, LV_R, LV_D0, LV_D1, LV_DJ, LV_DW, LV_COUNT };  // LV_DW: correction slots, one per patch entry

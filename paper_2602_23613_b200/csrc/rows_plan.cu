@@ -346,6 +346,14 @@ void rows_program(const std::vector<RowsHostLevel>& lv, std::vector<RStep> seg[S
   seg[SEG_BODY].push_back(simple(RK_FINISH, RS_RZ));
   seg[SEG_BODY].push_back(simple(RK_P_UPDATE));
   seg[SEG_GATHER].push_back(simple(RK_GATHER, 0, rows_vec_ws(depth, WS_X)));
+  // stand-alone AMG iteration (multilevel.py:204-235): r = b - A x; loop { x += V(r); r = b - A x }
+  seg[SEG_AMG_INIT].push_back(simple(RK_SPMV, RS_INIT, -1, RE_AMG_INIT));
+  seg[SEG_AMG_INIT].push_back(simple(RK_FINISH, RS_INIT));
+  seg[SEG_AMG_BODY].push_back(simple(RK_GUARD));
+  level_steps(lv, 0, seg[SEG_AMG_BODY]);
+  seg[SEG_AMG_BODY].push_back(simple(RK_AXPY1));
+  seg[SEG_AMG_BODY].push_back(simple(RK_SPMV, RS_AMG, -1, RE_AMG_RES));
+  seg[SEG_AMG_BODY].push_back(simple(RK_FINISH, RS_AMG));
 }
 
 // ----------------------------------------------------------------------------- accesses
@@ -383,7 +391,7 @@ void rows_access(const RStep& st, const std::vector<RowsHostLevel>& lv, const st
     };
     switch (st.kind) {
       case RK_SPMV: {
-        if (st.epi == RE_AP || st.epi == RE_PCG_INIT) {
+        if (st.epi == RE_AP || st.epi == RE_PCG_INIT || st.epi == RE_AMG_INIT || st.epi == RE_AMG_RES) {
           const RowsHostLevel& L0 = lv[0];
           const int xin = rows_vec_ws(depth, st.epi == RE_AP ? WS_P : WS_X);
           const int y = rows_vec_ws(depth, st.epi == RE_AP ? WS_AP : WS_R);
@@ -549,6 +557,13 @@ void rows_access(const RStep& st, const std::vector<RowsHostLevel>& lv, const st
         });
         red(st.site);
         break;
+      case RK_AXPY1:
+        for_rows(0, lv[0].split, [&](int64_t u) {
+          R(rows_vec_ws(depth, WS_Z), u);
+          R(rows_vec_ws(depth, WS_X), u);
+          Wr(rows_vec_ws(depth, WS_X), u);
+        });
+        break;
       case RK_P_UPDATE:
         for_rows(0, lv[0].split, [&](int64_t u) {
           R(rows_vec_ws(depth, WS_Z), u);
@@ -581,7 +596,7 @@ bool step_partitioned(const RStep& st, const std::vector<RowsHostLevel>& lv) {
   switch (st.kind) {
     case RK_COARSE: return false;
     case RK_SPMV:
-      if (st.epi == RE_AP || st.epi == RE_PCG_INIT) return lv[0].split;
+      if (st.epi == RE_AP || st.epi == RE_PCG_INIT || st.epi == RE_AMG_INIT || st.epi == RE_AMG_RES) return lv[0].split;
       return lv[(size_t)st.level].split;
     case RK_WAVE:
     case RK_FWAVE:
@@ -621,6 +636,8 @@ void rows_plan_all(const std::vector<RowsHostLevel>& lv, const std::vector<std::
     else if (g == SEG_INIT) { everywhere(WS_B); everywhere(WS_X); }
     else if (g == SEG_FIRST) { owned(WS_X); owned(WS_R); }
     else if (g == SEG_BODY) { owned(WS_X); owned(WS_R); owned(WS_P); }
+    else if (g == SEG_AMG_INIT) { everywhere(WS_B); everywhere(WS_X); }
+    else if (g == SEG_AMG_BODY) { everywhere(WS_B); owned(WS_X); owned(WS_R); }
     else owned(WS_X);
     plan.seg_boundary[g].clear();
     for (size_t k = 0; k < seg[g].size(); ++k) {

@@ -310,6 +310,21 @@ __device__ __forceinline__ void fin_update(Ctl* c, double S, double* hist, unsig
   set_cond(cond, c->stop ? 0u : 1u);
 }
 
+__device__ __forceinline__ void fin_amg_res(Ctl* c, double S, double* hist, unsigned long long cond) {
+  const double prev = c->rel;
+  const double rel = sqrt(S) / c->bnorm;
+  c->rel = rel;
+  hist[c->it] = rel;
+  c->it += 1;
+  if (rel <= c->tol) { c->converged = 1; c->stop = 1; }
+  else {
+    c->growth = rel > prev ? c->growth + 1 : 0;
+    if (c->growth >= 5) { c->error = 3; c->stop = 1; }
+    else if (c->it >= c->maxit) c->stop = 1;
+  }
+  set_cond(cond, c->stop ? 0u : 1u);
+}
+
 template <bool kFirst>
 __device__ __forceinline__ void fin_rz(Ctl* c, double S, unsigned long long cond) {
   if (kFirst) { c->rz = S; return; }
@@ -355,18 +370,7 @@ __device__ __forceinline__ void spmv_reduce(const SpmvArgs& a, double part, doub
   } else if (E == EPI_PCG_INIT || E == EPI_AMG_INIT || E == EPI_RES_PLAIN) {
     fin_init(c, S, S2, a.cond);
   } else if (E == EPI_AMG_RES) {
-    const double prev = c->rel;
-    const double rel = sqrt(S) / c->bnorm;
-    c->rel = rel;
-    a.hist[c->it] = rel;
-    c->it += 1;
-    if (rel <= c->tol) { c->converged = 1; c->stop = 1; }
-    else {
-      c->growth = rel > prev ? c->growth + 1 : 0;
-      if (c->growth >= 5) { c->error = 3; c->stop = 1; }
-      else if (c->it >= c->maxit) c->stop = 1;
-    }
-    set_cond(a.cond, c->stop ? 0u : 1u);
+    fin_amg_res(c, S, a.hist, a.cond);
   }
 }
 
@@ -540,7 +544,7 @@ __global__ void __launch_bounds__(kThreads) k_p_update(const int* stop, int64_t 
 
 // Row partition: complete a reduction.  red holds (S, S2) per rank; every rank
 // sums them in rank order, so all ranks take identical decisions.
-// site: 0 PCG init, 1 pAp, 2 residual update, 3 r.z (first), 4 r.z
+// site: 0 PCG / AMG init, 1 pAp, 2 residual update, 3 r.z (first), 4 r.z, 5 AMG residual
 __global__ void k_finish(const int* stop, int site, Ctl* c, const double* red, int nranks, double* hist,
                          unsigned long long cond) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
@@ -557,7 +561,8 @@ __global__ void k_finish(const int* stop, int site, Ctl* c, const double* red, i
   else if (site == 1) fin_ap(c, S, cond);
   else if (site == 2) fin_update(c, S, hist, cond);
   else if (site == 3) fin_rz<true>(c, S, cond);
-  else fin_rz<false>(c, S, cond);
+  else if (site == 4) fin_rz<false>(c, S, cond);
+  else fin_amg_res(c, S, hist, cond);
 }
 
 __global__ void k_loop_guard(const int* stop, unsigned long long cond) {
@@ -565,10 +570,12 @@ __global__ void k_loop_guard(const int* stop, unsigned long long cond) {
 }
 
 __global__ void __launch_bounds__(kThreads) k_axpy1(const int* stop, int64_t n, const double* __restrict__ e,
-                                                    double* __restrict__ x) {
+                                                    double* __restrict__ x, const int32_t* __restrict__ rows) {
   if (*stop) return;
-  for (int64_t u = (int64_t)blockIdx.x * kThreads + threadIdx.x; u < n; u += (int64_t)gridDim.x * kThreads)
+  for (int64_t q = (int64_t)blockIdx.x * kThreads + threadIdx.x; q < n; q += (int64_t)gridDim.x * kThreads) {
+    const int64_t u = rows ? (int64_t)rows[q] : q;
     x[u] += e[u];
+  }
 }
 
 // coarsest: x = Ainv b (row-major, one warp per row)
@@ -1168,7 +1175,7 @@ int64_t record_amg_body(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s
   k_loop_guard<<<1, 32, 0, s>>>(stop, cond);
   HC_CHECK_LAUNCH();
   int64_t l = 1 + record_vcycle(lv, w.r.p, w.z.p, stop, s);
-  k_axpy1<<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.z.p, w.x.p);
+  k_axpy1<<<vec_grid(w.n), kThreads, 0, s>>>(stop, w.n, w.z.p, w.x.p, nullptr);
   HC_CHECK_LAUNCH();
   SpmvArgs a{};
   a.stop = stop;
@@ -1187,7 +1194,8 @@ int64_t record_amg_body(std::vector<DevLevel*>& lv, Workspace& w, cudaStream_t s
 
 static_assert((int)RE_SET == (int)EPI_SET && (int)RE_ADD == (int)EPI_ADD && (int)RE_JAC_FW == (int)EPI_JAC_FW &&
                   (int)RE_RES_JAC == (int)EPI_RES_JAC && (int)RE_JAC_BW == (int)EPI_JAC_BW &&
-                  (int)RE_AP == (int)EPI_AP && (int)RE_PCG_INIT == (int)EPI_PCG_INIT,
+                  (int)RE_AP == (int)EPI_AP && (int)RE_PCG_INIT == (int)EPI_PCG_INIT &&
+                  (int)RE_AMG_INIT == (int)EPI_AMG_INIT && (int)RE_AMG_RES == (int)EPI_AMG_RES,
               "rows.cuh REpi mirrors Epi");
 
 // One step of the partitioned program on this rank: the single-GPU kernel on
@@ -1221,6 +1229,16 @@ int64_t rows_launch_step(const RStep& st, RowsCtx& rc, std::vector<DevLevel*>& l
       else
         k_dot_rz<false><<<vec_grid(cnt), kThreads, 0, s>>>(stop, cnt, w.r.p, w.z.p, w.p.p, w.ctl.p, w.part.p, cond,
                                                            rows, red(st.site));
+      HC_CHECK_LAUNCH();
+      return 1;
+    }
+    case RK_GUARD:
+      k_loop_guard<<<1, 32, 0, s>>>(stop, cond);
+      HC_CHECK_LAUNCH();
+      return 1;
+    case RK_AXPY1: {
+      const int64_t cnt = D0.split ? D0.nrows : w.n;
+      k_axpy1<<<vec_grid(cnt), kThreads, 0, s>>>(stop, cnt, w.z.p, w.x.p, D0.split ? D0.rows.p : nullptr);
       HC_CHECK_LAUNCH();
       return 1;
     }
@@ -1290,7 +1308,7 @@ int64_t rows_launch_step(const RStep& st, RowsCtx& rc, std::vector<DevLevel*>& l
     case RK_SPMV: {
       SpmvArgs a{};
       a.stop = stop;
-      if (st.epi == RE_AP || st.epi == RE_PCG_INIT) {
+      if (st.epi == RE_AP || st.epi == RE_PCG_INIT || st.epi == RE_AMG_INIT || st.epi == RE_AMG_RES) {
         DevLevel& L0 = *lv[0];
         a.ctl = w.ctl.p;
         a.part = w.part.p;
@@ -1310,7 +1328,11 @@ int64_t rows_launch_step(const RStep& st, RowsCtx& rc, std::vector<DevLevel*>& l
           a.xin = w.x.p;
           a.y = w.r.p;
           a.b = w.b.p;
-          spmv<EPI_PCG_INIT>(L0.A, a, s);
+          a.hist = w.hist.p;
+          a.cond = cond;
+          if (st.epi == RE_PCG_INIT) spmv<EPI_PCG_INIT>(L0.A, a, s);
+          else if (st.epi == RE_AMG_INIT) spmv<EPI_AMG_INIT>(L0.A, a, s);
+          else spmv<EPI_AMG_RES>(L0.A, a, s);
         }
         return 1;
       }

@@ -130,7 +130,7 @@ def info(h):
 # Subdomain row partition of the sparse regime (the north-star layout, csrc/rows.cuh)
 # ----------------------------------------------------------------------------------------------
 
-SEGMENTS = ("vcycle", "pcg_init", "pcg_first", "pcg_body", "gather")
+SEGMENTS = ("vcycle", "pcg_init", "pcg_first", "pcg_body", "gather", "amg_init", "amg_body")
 
 
 def distribute_rows(h, group=None, min_rows=16384):
@@ -203,7 +203,7 @@ def emulate_rows(hs, b, kind="vcycle", tol=1e-8, maxit=500, min_rows=64, poison=
     b = np.ascontiguousarray(b, dtype=np.float64)
     X = np.empty((n, b.shape[0]))
     rep = _lib.Report()
-    devs[0].check(devs[0].lib.hcamg_rows_emulate(handles, n, 0 if kind == "vcycle" else 1, b.ctypes.data,
+    devs[0].check(devs[0].lib.hcamg_rows_emulate(handles, n, {"vcycle": 0, "pcg": 1, "amg": 2}[kind], b.ctypes.data,
                                                  X.ctypes.data, float(tol), int(maxit), 1 if poison else 0,
                                                  C.byref(rep)))
     return X, (None if kind == "vcycle" else rep)

@@ -168,3 +168,29 @@ def test_dense_regime_is_refused():
     p = C.c_void_p()
     with pytest.raises((NotImplementedError, ValueError)):
         dev.check(dev.lib.hcamg_rows_prepare(dev.h, 0, 2, 32, None, C.byref(p)))
+
+
+@pytest.mark.parametrize("sweep", ["wave", "fwave"])
+def test_emulated_amg_solve(sweep):
+    """The stand-alone AMG iteration (multilevel.py:204-235) on the partition: same iteration
+    count and residual history length as the single GPU, x within the dot-product grouping."""
+    c = load("tri5s_alg")
+    b = c.z["pcg_b"]
+    href = build(c, 1, sweep)[0]
+    xref, rref = P.amg_solve(href, b, tol=1e-8, maxit=200)
+    hs = build(c, 3, sweep)
+    X, rep = dist.emulate_rows(hs, b, kind="amg", tol=1e-8, maxit=200, min_rows=32)
+    assert rep.converged and rep.iterations == rref.iterations
+    assert np.array_equal(X[1], X[0]) and np.array_equal(X[2], X[0])
+    assert np.linalg.norm(X[0] - xref) / np.linalg.norm(xref) <= 1e-10
+    # graph-captured, one rank exchanging with itself
+    h = build(c, 1, sweep)[0]
+    dev = P.multilevel._device_for(h)
+    import ctypes as C
+
+    p = C.c_void_p()
+    dev.check(dev.lib.hcamg_rows_prepare(dev.h, 0, 1, 32, None, C.byref(p)))
+    dev.check(dev.lib.hcamg_rows_connect_ptrs(dev.h, (C.c_void_p * 1)(p.value)))
+    x1, r1 = P.amg_solve(h, b, tol=1e-8, maxit=200)
+    assert r1.iterations == rref.iterations
+    assert np.linalg.norm(x1 - xref) / np.linalg.norm(xref) <= 1e-10
