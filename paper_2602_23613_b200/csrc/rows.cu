@@ -247,7 +247,6 @@ void rows_prepare(RowsCtx& rc, std::vector<DevLevel*>& lv, Workspace& w, int ran
     for (int32_t b = 0; b < nb; ++b) {
       rc.bfirst[(size_t)b] = (int64_t)hdst.size();
       int64_t cum = 0;
-      size_t first_cum = hcum.size();
       for (; k < segs.size() && segs[k].boundary == b; ++k) {
         const PushSeg& sg = segs[k];
         require(plan.barrier[(size_t)b] != 0, "row partition: push at a boundary without a barrier");
@@ -260,7 +259,6 @@ void rows_prepare(RowsCtx& rc, std::vector<DevLevel*>& lv, Workspace& w, int ran
         cum += sg.end - sg.begin;
       }
       hcum.push_back(cum);  // closing entry (each boundary owns nseg + 1 cum entries)
-      (void)first_cum;
       rc.bcount[(size_t)b] = cum;
       require((int64_t)hdst.size() - rc.bfirst[(size_t)b] < 63, "row partition: too many push segments at one boundary");
     }
