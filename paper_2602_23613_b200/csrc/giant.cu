@@ -944,8 +944,19 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
   DBuf<const double*> dC;
   DBuf<long long> badf(1, s);
   badf.fill_bytes(0xff);
+  // HCAMG_SETUP_TIMING: per-phase totals of the factorisation loop (synchronises after every phase)
+  double tphase[3] = {0, 0, 0};
+  auto phase = [&](int which, std::chrono::steady_clock::time_point& t0) {
+    if (!st.on) return;
+    cudaStreamSynchronize(s);
+    const auto t1 = std::chrono::steady_clock::now();
+    tphase[which] += std::chrono::duration<double>(t1 - t0).count();
+    t0 = t1;
+  };
   for (int64_t K = 0; K < T; ++K) {  // right-looking, inside the envelope; no host sync until the end
+    auto t0 = std::chrono::steady_clock::now();
     dense_cholesky_async(L.tile(K, K), kNB, kNB, piv.p + K * kNB, badf.p, K * kNB, s);
+    phase(0, t0);
     std::vector<int64_t> below;  // block rows I > K whose envelope reaches column K
     for (int64_t I = K + 1; I < T; ++I)
       if (L.has(I, K)) below.push_back(I);
@@ -956,6 +967,7 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
       for (int64_t I : below) hb.push_back(L.tile(I, K));
       dblas::trsm_rlt_batched(kNB, kNB, ha, kNB, hb, kNB, s);
     }
+    phase(1, t0);
     {
       std::vector<const double*> ha, hb, hc;
       for (size_t a = 0; a < below.size(); ++a)
@@ -971,7 +983,11 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
                           (int64_t)ha.size(), s);
       // (pageable-host uploads are staged before cudaMemcpyAsync returns: no sync needed)
     }
+    phase(2, t0);
   }
+  if (st.on)
+    fprintf(stderr, "[hcamg setup]   envelope Cholesky phases: potrf %.3f s, trsm %.3f s, gemm %.3f s (%lld block columns)\n",
+            tphase[0], tphase[1], tphase[2], (long long)T);
   const long long badv = read_scalar(badf.p, s);
   const int64_t fail = badv >= 0 ? (int64_t)badv : -1;
   {
