@@ -359,6 +359,31 @@ void trsm(Side side, Op op, int64_t m, int64_t n, const double* L, int64_t ldl, 
   }
 }
 
+void copy_block(int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd, cudaStream_t s) {
+  copy2d(rows, cols, src, lds, dst, ldd, s);
+}
+
+// B_b := B_b Li^T for every tile of the batch, Li = L^{-1} (nb x nb, ld nb) given
+void apply_rinv_t_batched(int64_t m, int64_t nb, const double* Li, const std::vector<double*>& hb, int64_t ldb,
+                          cudaStream_t s) {
+  const int64_t batch = (int64_t)hb.size();
+  if (batch <= 0) return;
+  DBuf<double> X(batch * m * nb, s);
+  std::vector<const double*> pa((size_t)batch), pb((size_t)batch, Li);
+  std::vector<double*> pc((size_t)batch);
+  for (int64_t b = 0; b < batch; ++b) {
+    pa[(size_t)b] = hb[(size_t)b];
+    pc[(size_t)b] = X.p + b * m * nb;
+  }
+  DBuf<const double*> da, db;
+  DBuf<double*> dc;
+  da.upload(pa.data(), batch, s);
+  db.upload(pb.data(), batch, s);
+  dc.upload(pc.data(), batch, s);
+  gemm_batched(N, T, m, nb, nb, 1.0, da.p, ldb, db.p, nb, 0.0, dc.p, m, batch, s);
+  for (int64_t b = 0; b < batch; ++b) copy2d(m, nb, X.p + b * m * nb, m, hb[(size_t)b], ldb, s);
+}
+
 void trsm_rlt_batched(int64_t m, int64_t nb, const std::vector<const double*>& hl, int64_t ldl,
                       const std::vector<double*>& hb, int64_t ldb, cudaStream_t s) {
   const int64_t batch = (int64_t)hb.size();

@@ -46,6 +46,10 @@ void trsm_rlt_batched(int64_t m, int64_t nb, const std::vector<const double*>& L
 // Li = L^{-1} for a lower-triangular n x n L (Li lower, ld ldi; the strict upper part is zeroed).
 void trtri_lower(int64_t n, const double* L, int64_t ldl, double* Li, int64_t ldi, cudaStream_t s);
 // Batched inverses of `batch` nb x nb lower-triangular tiles.
+void copy_block(int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd, cudaStream_t s);
+// B_b := B_b Li^T for every tile of the batch (host pointer list), Li = L^{-1} given (nb x nb, ld nb)
+void apply_rinv_t_batched(int64_t m, int64_t nb, const double* Li, const std::vector<double*>& hb, int64_t ldb,
+                          cudaStream_t s);
 void trtri_lower_batched(int64_t nb, const double* const* L, int64_t ldl, double* const* Li, int64_t ldi, int64_t batch,
                          cudaStream_t s);
 

@@ -98,7 +98,7 @@ constexpr int kTileThreads = 512;
 // order with the same expression, so the factor is bit-identical.
 __global__ void __launch_bounds__(kTileThreads) k_potrf_tile(double* __restrict__ A, int64_t ld, int nb,
                                                              double* __restrict__ piv, long long* __restrict__ bad,
-                                                             long long base) {
+                                                             long long base, double* __restrict__ Li, int64_t ldi) {
   extern __shared__ double T[];  // nb x (nb+1), row-major T[i*(nb+1)+j]
   const int ldt = nb + 1;
   if (*(volatile long long*)bad >= 0) return;
@@ -122,16 +122,37 @@ __global__ void __launch_bounds__(kTileThreads) k_potrf_tile(double* __restrict_
     for (int i = j + 1 + threadIdx.x; i < nb; i += blockDim.x) T[i * ldt + j] /= ljj;
     __syncthreads();
     if (threadIdx.x == 0) T[j * ldt + j] = ljj;
-    const int m = nb - j - 1;
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      const int i = j + 1 + e / m, l = j + 1 + e % m;
-      if (l <= i) T[i * ldt + l] -= T[i * ldt + j] * T[l * ldt + j];
+    for (int i = j + 1 + (int)(threadIdx.x >> 5); i < nb; i += kTileThreads / 32) {  // a warp per row, lanes along it
+      const double lij = T[i * ldt + j];
+      for (int l = j + 1 + (int)(threadIdx.x & 31); l <= i; l += 32) T[i * ldt + l] -= lij * T[l * ldt + j];
     }
     __syncthreads();
   }
   for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
     int i = e % nb, j = e / nb;
     if (i >= j) A[i + (int64_t)j * ld] = T[i * ldt + j];
+  }
+  if (!Li) return;
+  // X = L^{-1} in place (L X = I, rows final from the top): at step p row p is
+  // scaled by 1 / L[p][p], then every row below takes -L[i][p] X[p][.]; column
+  // p of L is staged first because its positions receive X[.][p]
+  __shared__ double col[kTile];
+  for (int p = 0; p < nb; ++p) {
+    const double lpp = T[p * ldt + p];
+    __syncthreads();
+    for (int i = p + 1 + threadIdx.x; i < nb; i += blockDim.x) col[i] = T[i * ldt + p];
+    for (int j = threadIdx.x; j <= p; j += blockDim.x) T[p * ldt + j] = (j == p ? 1.0 : T[p * ldt + j]) / lpp;
+    __syncthreads();
+    for (int i = p + 1 + (int)(threadIdx.x >> 5); i < nb; i += kTileThreads / 32) {
+      const double ci = col[i];
+      for (int j = (int)(threadIdx.x & 31); j <= p; j += 32)
+        T[i * ldt + j] = (j == p ? 0.0 : T[i * ldt + j]) - ci * T[p * ldt + j];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nb * nb; e += blockDim.x) {
+    int i = e % nb, j = e / nb;
+    Li[i + (int64_t)j * ldi] = i >= j ? T[i * ldt + j] : 0.0;
   }
 }
 
@@ -166,7 +187,8 @@ namespace {
 // A22 -= A21 A21^T; L22 = chol(A22) -- leaves of <= kTile on one CTA, the
 // updates on the own FP64 kernels (the trailing matrix is touched O(log n)
 // times instead of once per 96-column panel)
-void chol_rec(double* A, int64_t k, int64_t ld, double* piv, long long* bad, int64_t base, cudaStream_t s) {
+void chol_rec(double* A, int64_t k, int64_t ld, double* piv, long long* bad, int64_t base, cudaStream_t s,
+              double* Li = nullptr, int64_t ldi = 0) {
   if (k <= kTile) {
     const size_t smem = sizeof(double) * kTile * (kTile + 1);
     static bool init = false;
@@ -174,20 +196,42 @@ void chol_rec(double* A, int64_t k, int64_t ld, double* piv, long long* bad, int
       HC_CUDA(cudaFuncSetAttribute(k_potrf_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       init = true;
     }
-    k_potrf_tile<<<1, kTileThreads, smem, s>>>(A, ld, (int)k, piv, bad, (long long)base);
+    k_potrf_tile<<<1, kTileThreads, smem, s>>>(A, ld, (int)k, piv, bad, (long long)base, Li, ldi);
     HC_CHECK_LAUNCH();
-    count_flops((double)k * k * k / 3.0);
+    count_flops((double)k * k * k / 3.0 * (Li ? 2.0 : 1.0));
     return;
   }
   const int64_t k1 = std::min<int64_t>(k - 1, std::max<int64_t>(kTile, (k / 2 + kTile - 1) / kTile * kTile)), k2 = k - k1;
   double* A21 = A + k1;
   double* A22 = A + k1 + k1 * ld;
-  chol_rec(A, k1, ld, piv, bad, base, s);
-  dblas::trsm(dblas::Right, dblas::T, k2, k1, A, ld, A21, ld, s);
+  if (!Li) {
+    chol_rec(A, k1, ld, piv, bad, base, s);
+    dblas::trsm(dblas::Right, dblas::T, k2, k1, A, ld, A21, ld, s);
+    dblas::syrk_ln(k2, k1, -1.0, A21, ld, 1.0, A22, ld, s);
+    chol_rec(A22, k2, ld, piv + k1, bad, base + k1, s);
+    return;
+  }
+  // with the inverse of the factor alongside: the panel solve is a product with
+  // L11^{-T} (no latency-bound triangular leaves), and L^{-1} is assembled as
+  // [Li11 0; -Li22 L21 Li11, Li22]
+  double* Li21 = Li + k1;
+  double* Li22 = Li + k1 + k1 * ldi;
+  chol_rec(A, k1, ld, piv, bad, base, s, Li, ldi);
+  dblas::gemm(dblas::N, dblas::T, k2, k1, k1, 1.0, A21, ld, Li, ldi, 0.0, Li21, ldi, s);  // A21 L11^{-T} (Li21 as scratch)
+  dblas::copy_block(k2, k1, Li21, ldi, A21, ld, s);
   dblas::syrk_ln(k2, k1, -1.0, A21, ld, 1.0, A22, ld, s);
-  chol_rec(A22, k2, ld, piv + k1, bad, base + k1, s);
+  chol_rec(A22, k2, ld, piv + k1, bad, base + k1, s, Li22, ldi);
+  DBuf<double> Tm(k2 * k1, s);
+  dblas::gemm(dblas::N, dblas::N, k2, k1, k1, 1.0, A21, ld, Li, ldi, 0.0, Tm.p, k2, s);       // L21 Li11
+  dblas::gemm(dblas::N, dblas::N, k2, k1, k2, -1.0, Li22, ldi, Tm.p, k2, 0.0, Li21, ldi, s);  // -Li22 (L21 Li11)
+  HC_CUDA(cudaMemset2DAsync(Li + k1 * ldi, sizeof(double) * ldi, 0, sizeof(double) * k1, k2, s));
 }
 }  // namespace
+
+void dense_cholesky_inv_async(double* A, int64_t k, int64_t ld, double* Li, int64_t ldi, double* piv, long long* bad,
+                              int64_t base, cudaStream_t s) {
+  if (k > 0) chol_rec(A, k, ld, piv, bad, base, s, Li, ldi);
+}
 
 void dense_cholesky_async(double* A, int64_t k, int64_t ld, double* piv, long long* bad, int64_t base,
                           cudaStream_t s) {

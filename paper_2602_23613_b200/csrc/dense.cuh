@@ -41,6 +41,11 @@ int64_t dense_cholesky_raw(double* A, int64_t k, int64_t ld, double* piv, cudaSt
 // the first failing pivot; later calls sharing `bad` become no-ops.
 void dense_cholesky_async(double* A, int64_t k, int64_t ld, double* piv, long long* bad, int64_t base,
                           cudaStream_t s);
+// The same, and Li (k x k, ld ldi) receives L^{-1} (lower triangular, zeros above): the panel
+// solves of the recursion become products with the inverse, so there are no latency-bound
+// triangular leaves, and a caller that needs L^{-1} anyway (block-column panel solves) has it.
+void dense_cholesky_inv_async(double* A, int64_t k, int64_t ld, double* Li, int64_t ldi, double* piv, long long* bad,
+                              int64_t base, cudaStream_t s);
 // Reference breakdown verdict from the pivots (-1: fine).
 int64_t pivot_verdict(const std::vector<double>& hp, int64_t k, int64_t j0, double scale);
 

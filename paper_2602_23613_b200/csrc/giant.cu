@@ -944,6 +944,8 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
   DBuf<const double*> dC;
   DBuf<long long> badf(1, s);
   badf.fill_bytes(0xff);
+  DBuf<double> LinvKK(kNB * kNB, s);
+  LinvKK.zero();
   // HCAMG_SETUP_TIMING: per-phase totals of the factorisation loop (synchronises after every phase)
   double tphase[3] = {0, 0, 0};
   auto phase = [&](int which, std::chrono::steady_clock::time_point& t0) {
@@ -955,17 +957,16 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
   };
   for (int64_t K = 0; K < T; ++K) {  // right-looking, inside the envelope; no host sync until the end
     auto t0 = std::chrono::steady_clock::now();
-    dense_cholesky_async(L.tile(K, K), kNB, kNB, piv.p + K * kNB, badf.p, K * kNB, s);
+    dense_cholesky_inv_async(L.tile(K, K), kNB, kNB, LinvKK.p, kNB, piv.p + K * kNB, badf.p, K * kNB, s);
     phase(0, t0);
     std::vector<int64_t> below;  // block rows I > K whose envelope reaches column K
     for (int64_t I = K + 1; I < T; ++I)
       if (L.has(I, K)) below.push_back(I);
     if (below.empty()) continue;
-    {
-      std::vector<const double*> ha(below.size(), L.tile(K, K));
+    {  // L_IK = A_IK L_KK^{-T} with the inverse the diagonal factorisation produced
       std::vector<double*> hb;
       for (int64_t I : below) hb.push_back(L.tile(I, K));
-      dblas::trsm_rlt_batched(kNB, kNB, ha, kNB, hb, kNB, s);
+      dblas::apply_rinv_t_batched(kNB, kNB, LinvKK.p, hb, kNB, s);
     }
     phase(1, t0);
     {
