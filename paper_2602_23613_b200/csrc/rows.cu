@@ -32,9 +32,11 @@ __global__ void __launch_bounds__(kPushThreads) k_xpush(const int* stop, XPush x
   __syncthreads();
   if (threadIdx.x != 0) return;
   __threadfence_system();
-  if (atomicAdd(x.cta, 1u) != gridDim.x - 1) return;
-  __threadfence_system();
-  *x.cta = 0u;
+  if (gridDim.x > 1) {  // the last block to finish signals (most boundaries are one block: no ticket)
+    if (atomicAdd(x.cta, 1u) != gridDim.x - 1) return;
+    __threadfence_system();
+    *x.cta = 0u;
+  }
   const unsigned long long e = *x.ep + 1;
   *x.ep = e;
   for (int r = 0; r < x.nranks; ++r) {
