@@ -323,6 +323,89 @@ void trtri_lower_batched(int64_t nb, const double* const* L, int64_t ldl, double
   for (int64_t b = 0; b < batch; ++b) trtri_lower(nb, hl[(size_t)b], ldl, hi[(size_t)b], ldi, s);
 }
 
+namespace {
+__global__ void k_zero_upper(double* const* P, int64_t n, int64_t ld) {
+  double* A = P[blockIdx.y];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t % n, j = t / n;
+    if (i < j) A[i + j * ld] = 0.0;
+  }
+}
+}  // namespace
+
+// Inverses of many lower-triangular n x n matrices at once (host pointer
+// lists).  For n = NB0 * 2^k the recursion of trtri_lower is run level by
+// level over ALL matrices: one launch inverts every 64 x 64 diagonal block of
+// every matrix, then each doubling of the block size is two batched GEMMs
+// (L21 Li11, then -Li22 (L21 Li11)) over every node of every matrix -- 2 k + 2
+// launches in all, where the per-matrix recursion issues ~100 small ones each.
+// Same arithmetic per matrix as trtri_lower.
+void trtri_lower_many(int64_t n, const std::vector<const double*>& L, int64_t ldl, const std::vector<double*>& Li,
+                      int64_t ldi, cudaStream_t s) {
+  const int64_t batch = (int64_t)L.size();
+  if (batch == 0 || n <= 0) return;
+  bool pow2 = n % NB0 == 0;
+  for (int64_t q = n / NB0; pow2 && q > 1; q /= 2) pow2 = q % 2 == 0;
+  if (!pow2 || batch == 1) {
+    for (int64_t b = 0; b < batch; ++b) trtri_lower(n, L[(size_t)b], ldl, Li[(size_t)b], ldi, s);
+    return;
+  }
+  auto up = [&](const std::vector<const double*>& h, DBuf<const double*>& d) {
+    d.upload(h.data(), (int64_t)h.size(), s);
+    return d.p;
+  };
+  {
+    DBuf<double*> dli;
+    dli.upload(Li.data(), batch, s);
+    k_zero_upper<<<dim3(kSMs / 2, (unsigned)batch), 256, 0, s>>>(dli.p, n, ldi);
+    HC_CHECK_LAUNCH();
+    const int64_t nl = n / NB0;
+    std::vector<const double*> hl;
+    std::vector<double*> hi;
+    for (int64_t b = 0; b < batch; ++b)
+      for (int64_t t = 0; t < nl; ++t) {
+        hl.push_back(L[(size_t)b] + t * NB0 * (ldl + 1));
+        hi.push_back(Li[(size_t)b] + t * NB0 * (ldi + 1));
+      }
+    DBuf<const double*> dl;
+    DBuf<double*> di;
+    dl.upload(hl.data(), (int64_t)hl.size(), s);
+    di.upload(hi.data(), (int64_t)hi.size(), s);
+    leaf_init();
+    for (int64_t b0 = 0; b0 < (int64_t)hl.size(); b0 += 65535) {
+      const int64_t nb = std::min<int64_t>(65535, (int64_t)hl.size() - b0);
+      k_trtri_leaf<<<(unsigned)nb, NB0, LEAF_SMEM, s>>>((int)NB0, dl.p + b0, nullptr, ldl, di.p + b0, nullptr, ldi, 0);
+      HC_CHECK_LAUNCH();
+    }
+    count_flops((double)NB0 * NB0 * NB0 / 3.0 * (double)hl.size());
+    HC_CUDA(cudaStreamSynchronize(s));  // the host pointer lists above are staged
+  }
+  for (int64_t h = NB0; h < n; h *= 2) {
+    const int64_t nodes = n / (2 * h);
+    DBuf<double> Tm(batch * nodes * h * h, s);
+    std::vector<const double*> a1, b1, a2, b2;
+    std::vector<double*> c1, c2;
+    for (int64_t b = 0; b < batch; ++b)
+      for (int64_t q = 0; q < nodes; ++q) {
+        const int64_t o = q * 2 * h;
+        double* tm = Tm.p + (b * nodes + q) * h * h;
+        a1.push_back(L[(size_t)b] + (o + h) + o * ldl);          // L21
+        b1.push_back(Li[(size_t)b] + o * (ldi + 1));            // Li11
+        c1.push_back(tm);
+        a2.push_back(Li[(size_t)b] + (o + h) * (ldi + 1));      // Li22
+        b2.push_back(tm);
+        c2.push_back(Li[(size_t)b] + (o + h) + o * ldi);        // Li21
+      }
+    DBuf<const double*> da1, db1, da2, db2;
+    DBuf<double*> dc1, dc2;
+    dc1.upload(c1.data(), (int64_t)c1.size(), s);
+    dc2.upload(c2.data(), (int64_t)c2.size(), s);
+    gemm_batched(N, N, h, h, h, 1.0, up(a1, da1), ldl, up(b1, db1), ldi, 0.0, dc1.p, h, (int64_t)a1.size(), s);
+    gemm_batched(N, N, h, h, h, -1.0, up(a2, da2), ldi, up(b2, db2), h, 0.0, dc2.p, ldi, (int64_t)a2.size(), s);
+    HC_CUDA(cudaStreamSynchronize(s));  // Tm and the pointer lists go out of scope
+  }
+}
+
 void trsm(Side side, Op op, int64_t m, int64_t n, const double* L, int64_t ldl, double* B, int64_t ldb,
           cudaStream_t s) {
   const int64_t d = side == Left ? m : n;  // dimension of L

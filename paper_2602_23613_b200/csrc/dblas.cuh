@@ -50,6 +50,9 @@ void copy_block(int64_t rows, int64_t cols, const double* src, int64_t lds, doub
 // B_b := B_b Li^T for every tile of the batch (host pointer list), Li = L^{-1} given (nb x nb, ld nb)
 void apply_rinv_t_batched(int64_t m, int64_t nb, const double* Li, const std::vector<double*>& hb, int64_t ldb,
                           cudaStream_t s);
+// inverses of many n x n lower-triangular matrices (host pointer lists), level-synchronous
+void trtri_lower_many(int64_t n, const std::vector<const double*>& L, int64_t ldl, const std::vector<double*>& Li,
+                      int64_t ldi, cudaStream_t s);
 void trtri_lower_batched(int64_t nb, const double* const* L, int64_t ldl, double* const* Li, int64_t ldi, int64_t batch,
                          cudaStream_t s);
 

@@ -601,6 +601,7 @@ void blocks_transpose(std::vector<const double*>& src, int64_t lds, std::vector<
 // L_{I,I-1}, N_I = Linv_II^T L_{I+1,I}^T, forward folds L_{i,I-1} copied
 // row-major; the backward folds are columns of L, read in place.
 void build_factor_ops(const Packed& L, FactorP& f, cudaStream_t s) {
+  StageTimer stf(s);
   // SP sweep blocks per factor tile (SB <= NB) or Q factor tiles per sweep block (SB = Q NB)
   constexpr int64_t SP = kSB <= kNB ? kNB / kSB : 1, Q = kSB > kNB ? kSB / kNB : 1;
   static_assert(SP * kSB == kNB || Q * kNB == kSB, "sweep block and factor tile must nest");
@@ -665,6 +666,7 @@ void build_factor_ops(const Packed& L, FactorP& f, cudaStream_t s) {
       HC_CUDA(cudaStreamSynchronize(s));
     }
   }
+  stf.mark("    ops: blocks of L");
   const int64_t LDS = Q > 1 ? kSB : kNB;  // leading dimension of the blocks of L
   auto sub = [&](int64_t I, int64_t J) -> double* {  // column-major, ld LDS
     if (Q > 1) return Lsb.p + lslot[(size_t)(I * TS + J)] * SS;
@@ -690,7 +692,15 @@ void build_factor_ops(const Packed& L, FactorP& f, cudaStream_t s) {
   auto fp = [&](int64_t slot) { return fpool.p + slot * SS; };
   auto bp = [&](int64_t slot) { return bpool.p + slot * SS; };
   {
-    for (int64_t I = 0; I < TS; ++I) dblas::trtri_lower(kSB, sub(I, I), LDS, bp(I), kSB, s);  // Linv_II
+    {  // Linv_II of every block in one level-synchronous batch
+      std::vector<const double*> hl;
+      std::vector<double*> hi;
+      for (int64_t I = 0; I < TS; ++I) {
+        hl.push_back(sub(I, I));
+        hi.push_back(bp(I));
+      }
+      dblas::trtri_lower_many(kSB, hl, LDS, hi, kSB, s);
+    }
     HC_CUDA(cudaStreamSynchronize(s));
     std::vector<const double*> src;
     std::vector<double*> dst;
@@ -700,6 +710,7 @@ void build_factor_ops(const Packed& L, FactorP& f, cudaStream_t s) {
     }
     blocks_transpose(src, kSB, dst, s);
   }
+  stf.mark("    ops: Linv_II");
   auto batched_gemm = [&](dblas::Op ta, std::vector<const double*>& ha, std::vector<const double*>& hb,
                           std::vector<double*>& hc) {
     if (ha.empty()) return;
@@ -803,8 +814,10 @@ void build_factor_ops(const Packed& L, FactorP& f, cudaStream_t s) {
   }
   const std::vector<uint8_t> hr = rng.download();
   auto ranges = [&](const double* p) -> const uint8_t* { return hr.data() + index.at(p) * kSB * 2; };
+  stf.mark("    ops: M, N, folds, ranges");
   tri_compact(fs, ranges, f.fw, s, 0);
   tri_compact(bs, ranges, f.bw, s, 1);
+  stf.mark("    ops: compact + partition");
   if (getenv("HCAMG_SETUP_TIMING"))
     fprintf(stderr, "[hcamg setup]   sweeps: %lld blocks of %lld rows, fwd %.3f GB, bwd %.3f GB\n", (long long)TS,
             (long long)kSB, f.fw.bytes / 1e9, f.bw.bytes / 1e9);
