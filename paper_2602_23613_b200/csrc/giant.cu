@@ -132,6 +132,23 @@ __global__ void k_first_row(int64_t n, int64_t m, const double* __restrict__ B, 
       if (B[r * m + c] != 0.0) atomicMin(first + c, rank[r]);
 }
 
+// the same from a CSR right-hand side (explicit zeros skipped, as the dense test does)
+__global__ void k_first_row_csr(int64_t n, const int64_t* __restrict__ bp, const int32_t* __restrict__ bi,
+                                const double* __restrict__ bv, const int32_t* __restrict__ rank,
+                                int* __restrict__ first) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = bp[r]; e < bp[r + 1]; ++e)
+      if (bv[e] != 0.0) atomicMin(first + bi[e], rank[r]);
+}
+
+// out[rank[r], colinv[c]] = B[r, c] for the entries of a CSR B (out zeroed before; row-major n x m)
+__global__ void k_scatter_rc_csr(int64_t n, int64_t m, const int64_t* __restrict__ bp, const int32_t* __restrict__ bi,
+                                 const double* __restrict__ bv, const int32_t* __restrict__ rank,
+                                 const int32_t* __restrict__ colinv, double* __restrict__ out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
+    for (int64_t e = bp[r]; e < bp[r + 1]; ++e) out[(int64_t)rank[r] * m + colinv[bi[e]]] = bv[e];
+}
+
 __global__ void k_csr_diag_absmax(const int64_t* __restrict__ ap, const int32_t* __restrict__ ai,
                                   const double* __restrict__ av, int64_t n, unsigned long long* out) {
   double m = 0.0;
@@ -896,8 +913,11 @@ __global__ void k_unperm_sym(int64_t m, const int32_t* __restrict__ colperm, con
 }  // namespace
 
 void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, FactorP* fac, double* D,
-                        bool want_z) {
+                        bool want_z, const DCsr* Bs) {
   const int64_t n = Agg.nrows;
+  const bool sparse_rhs = Bs != nullptr && !want_z;
+  require(sparse_rhs || B != nullptr, "giant_factor_solve: no right-hand side");
+  if (sparse_rhs) require(Bs->nrows == n && Bs->ncols == m, "giant_factor_solve: sparse right-hand side shape");
   StageTimer st(s);
   // ordering: reverse Cuthill-McKee (default) or the natural component order
   std::vector<int64_t> hptr = Agg.ptr.download();
@@ -1030,7 +1050,10 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
   {
     DBuf<int> first(m, s);
     HC_CUDA(cudaMemsetAsync(first.p, 0x7f, sizeof(int) * (size_t)m, s));
-    k_first_row<<<(unsigned)std::min<int64_t>(n, kSMs * 16), 256, 0, s>>>(n, m, B, dinv.p, first.p);
+    if (sparse_rhs)
+      k_first_row_csr<<<grid_for(n, 256), 256, 0, s>>>(n, Bs->ptr.p, Bs->idx.p, Bs->val.p, dinv.p, first.p);
+    else
+      k_first_row<<<(unsigned)std::min<int64_t>(n, kSMs * 16), 256, 0, s>>>(n, m, B, dinv.p, first.p);
     HC_CHECK_LAUNCH();
     st.mark("  giant: column order");
     std::vector<int> hf = first.download();
@@ -1045,7 +1068,18 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
   DBuf<int32_t> dcol;
   dcol.upload(colperm.data(), m);
   DBuf<double> Bp(n * m, s);
-  permute_rc<false>(n, m, dperm.p, dcol.p, B, Bp.p, s);
+  if (sparse_rhs) {
+    std::vector<int32_t> colinv((size_t)m);
+    for (int64_t k = 0; k < m; ++k) colinv[(size_t)colperm[(size_t)k]] = (int32_t)k;
+    DBuf<int32_t> dcinv;
+    dcinv.upload(colinv.data(), m, s);
+    Bp.zero();
+    k_scatter_rc_csr<<<grid_for(n, 256), 256, 0, s>>>(n, m, Bs->ptr.p, Bs->idx.p, Bs->val.p, dinv.p, dcinv.p, Bp.p);
+    HC_CHECK_LAUNCH();
+    HC_CUDA(cudaStreamSynchronize(s));  // dcinv is a host-ordered upload: keep it alive until the kernel has run
+  } else {
+    permute_rc<false>(n, m, dperm.p, dcol.p, B, Bp.p, s);
+  }
   st.mark("  giant: permute in");
   // Solve (A Z = B with B row-major n x m)  <=>  Z^T L L^T = B^T on the column-major m x n view.
   auto nbk = [&](int64_t K) { return std::min(kNB, n - K * kNB); };

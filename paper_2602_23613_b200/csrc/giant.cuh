@@ -22,8 +22,12 @@ namespace hcamg {
 // Y = L^{-1} B (the forward half of the solve, staircase-restricted: column c
 // of Y is zero above the first row of its right-hand side), and, unless
 // want_z, the backward solve is skipped and B is left as it was.
+// With `Bs` (the right-hand side as CSR, n x m) and !want_z, B_rowmajor may be
+// null: the permuted dense right-hand side is scattered straight from Bs, so
+// the unpermuted dense copy (config 2: 35 GB, its allocation, fill and the
+// 70 GB permutation pass) never exists.
 void giant_factor_solve(const DCsr& Agg, double* B_rowmajor, int64_t m, cudaStream_t s, FactorP* fac = nullptr,
-                        double* D = nullptr, bool want_z = true);
+                        double* D = nullptr, bool want_z = true, const DCsr* Bs = nullptr);
 
 // Reverse Cuthill-McKee order of a symmetric CSR pattern (scipy's
 // csgraph.reverse_cuthill_mckee, which the reference's cholesky() applies,

@@ -435,20 +435,23 @@ void build_interp(const DCsr& A, const DCsr& G, const SplitResult& sp, int mode,
       csr_extract(Aii, mpos.p, nG, gmap.p, nG, hp.Agg, s);
       csr_extract(W, mpos.p, nG, nullptr, npair, hp.Wg, s);
       st.mark("  interp: components, small solves");
-      hp.Z.alloc(nG * npair, s);
-      hp.Z.zero();
-      k_giant_rhs<<<grid_for(nG, 128), 128, 0, s>>>(mpos.p, nG, W.ptr.p, W.idx.p, W.val.p, npair, hp.Z.p);
-      HC_CHECK_LAUNCH();
+      // single-GPU default: the V-cycle applies A_GG^{-1} through the factor
+      // and the Galerkin product needs only Y^T Y (Y = L^{-1} W'), so the
+      // 35 GB explicit block Z is not formed (hybrid_ensure_z forms it
+      // on demand) -- nor is its dense right-hand side: the solve scatters
+      // the rows of W' straight into factored order; explicit-Z apply
+      // (factor_apply = 0) or form_z keep it
+      const bool fac = factorp_enabled();
+      const bool want_z = !fac || opts().form_z;
+      if (want_z) {
+        hp.Z.alloc(nG * npair, s);
+        hp.Z.zero();
+        k_giant_rhs<<<grid_for(nG, 128), 128, 0, s>>>(mpos.p, nG, W.ptr.p, W.idx.p, W.val.p, npair, hp.Z.p);
+        HC_CHECK_LAUNCH();
+      }
       try {
-        // single-GPU default: the V-cycle applies A_GG^{-1} through the factor
-        // and the Galerkin product needs only Y^T Y (Y = L^{-1} W'), so the
-        // 35 GB explicit block Z is not formed (hybrid_ensure_z forms it
-        // on demand); explicit-Z apply (factor_apply = 0) or form_z keep it
-        const bool fac = factorp_enabled();
-        const bool want_z = !fac || opts().form_z;
         hp.D.alloc(npair * npair, s);
-        giant_factor_solve(hp.Agg, hp.Z.p, npair, s, fac ? &hp.fac : nullptr, hp.D.p, want_z);
-        if (!want_z) hp.Z.release();
+        giant_factor_solve(hp.Agg, hp.Z.p, npair, s, fac ? &hp.fac : nullptr, hp.D.p, want_z, &hp.Wg);
         if (hp.fac.T) factorp_attach(hp.fac, W, mpos.p, hp.rows.p, s);
       } catch (const Error& e) {
         if (e.code == ENOTSPD_ && giant < fail_comp) { fail_comp = giant; fail_piv = e.index; }

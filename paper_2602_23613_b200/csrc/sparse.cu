@@ -225,8 +225,78 @@ static void segmented_sort(DCsr& C, cudaStream_t s) {
   C.val = std::move(vo);
 }
 
+// ---- left factor stored as a fully dense canonical CSR (the dense-regime
+// coarse operator, config 2: 26,236^2 entries): the row kernels above walk
+// the 26 k entries of a row one after the other, two lanes busy on a
+// gradient's two entries (0.32 s for A_1 G~).  With every A[i, k] stored, the
+// pattern of C is the same for every row (the non-empty columns of B) and
+// C[i, v] = sum over the rows k of B's column v, ascending, of A[i, k] B[k, v]
+// -- scipy's csr_matmat order (k ascending, product rounded, then added), one
+// thread per output entry.
+namespace {
+__global__ void k_dense_canonical(const int64_t* __restrict__ ap, const int32_t* __restrict__ ai, int64_t nrows,
+                                  int64_t ncols, int* __restrict__ bad) {
+  const int64_t total = nrows * ncols;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x)
+    if (ai[e] != (int32_t)(e % ncols) || (e % ncols == 0 && ap[e / ncols] != e)) *bad = 1;
+}
+__global__ void k_col_nonempty(const int64_t* __restrict__ tp, int64_t m, int64_t* __restrict__ f) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < m; v += (int64_t)gridDim.x * blockDim.x)
+    f[v] = tp[v + 1] > tp[v];
+}
+__global__ void k_dense_left_fill(const double* __restrict__ av, int64_t nrows, int64_t ka,
+                                  const int64_t* __restrict__ tp, const int32_t* __restrict__ ti,
+                                  const double* __restrict__ tv, int64_t m, const int64_t* __restrict__ cpos,
+                                  int64_t nc, int64_t* __restrict__ cp, int32_t* __restrict__ ci,
+                                  double* __restrict__ cv) {
+  const int64_t i = blockIdx.y + (int64_t)gridDim.y * blockIdx.z;
+  if (i >= nrows) return;
+  const double* arow = av + i * ka;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < m; v += (int64_t)gridDim.x * blockDim.x) {
+    if (tp[v + 1] == tp[v]) continue;
+    double acc = 0.0;
+    for (int64_t t = tp[v]; t < tp[v + 1]; ++t) acc = __dadd_rn(acc, __dmul_rn(arow[ti[t]], tv[t]));
+    ci[i * nc + cpos[v]] = (int32_t)v;
+    cv[i * nc + cpos[v]] = acc;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    cp[i] = i * nc;
+    if (i == nrows - 1) cp[nrows] = nrows * nc;
+  }
+}
+}  // namespace
+
+static bool spgemm_dense_left(const DCsr& A, const DCsr& B, DCsr& C, cudaStream_t s) {
+  const int64_t nrows = A.nrows, ka = A.ncols, m = B.ncols;
+  if (nrows < 32 || ka < 32 || A.nnz != nrows * ka || nrows >= 65535LL * 65535LL) return false;
+  DBuf<int> bad(1, s);
+  bad.zero();
+  k_dense_canonical<<<kSMs * 8, 256, 0, s>>>(A.ptr.p, A.idx.p, nrows, ka, bad.p);
+  HC_CHECK_LAUNCH();
+  if (read_scalar(bad.p, s)) return false;
+  DCsr Bt;
+  csr_transpose(B, Bt, s);
+  DBuf<int64_t> f(m, s), cpos(m + 1, s);  // the scan writes m + 1 offsets
+  k_col_nonempty<<<grid_for(m, 256), 256, 0, s>>>(Bt.ptr.p, m, f.p);
+  HC_CHECK_LAUNCH();
+  const int64_t nc = exclusive_scan(f.p, cpos.p, m, s);
+  C.nrows = nrows;
+  C.ncols = m;
+  C.nnz = nrows * nc;
+  C.ptr.alloc(nrows + 1, s);
+  C.idx.alloc(C.nnz, s);
+  C.val.alloc(C.nnz, s);
+  const unsigned gy = (unsigned)std::min<int64_t>(nrows, 65535), gz = (unsigned)((nrows + gy - 1) / gy);
+  const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 64));
+  k_dense_left_fill<<<dim3(gx, gy, gz), 256, 0, s>>>(A.val.p, nrows, ka, Bt.ptr.p, Bt.idx.p, Bt.val.p, m, cpos.p, nc,
+                                                    C.ptr.p, C.idx.p, C.val.p);
+  HC_CHECK_LAUNCH();
+  return true;
+}
+
 void spgemm(const DCsr& A, const DCsr& B, DCsr& C, cudaStream_t s) {
   require(A.ncols == B.nrows, "spgemm: dimension mismatch");
+  if (spgemm_dense_left(A, B, C, s)) return;
   const int64_t nrows = A.nrows, ncols = B.ncols;
   C.nrows = nrows;
   C.ncols = ncols;
