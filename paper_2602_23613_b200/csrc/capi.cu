@@ -147,6 +147,31 @@ __global__ void k_asym(const int64_t* __restrict__ p, const int32_t* __restrict_
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
 }
 
+// the same for a fully dense canonical CSR (val[i n + j] = M[i, j]): 32 x 32 tiles
+// against their mirror tiles through shared memory (config 2's 26,236^2 coarse
+// operator: the row-walk with a binary search per entry took 144 ms)
+__global__ void k_asym_dense(const double* __restrict__ v, int64_t n, unsigned long long* out) {
+  __shared__ double t[32][33];
+  const int64_t nt = (n + 31) / 32;
+  double m = 0.0;
+  for (int64_t b = blockIdx.x; b < nt * nt; b += gridDim.x) {
+    const int64_t bi = b / nt, bj = b % nt;
+    if (bj > bi) continue;
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const int64_t i = bj * 32 + r, j = bi * 32 + threadIdx.x;  // the mirror tile, read by rows
+      t[r][threadIdx.x] = (i < n && j < n) ? v[i * n + j] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const int64_t i = bi * 32 + r, j = bj * 32 + threadIdx.x;
+      if (i < n && j < n) m = fmax(m, fabs(v[i * n + j] - t[threadIdx.x][r]));
+    }
+  }
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (threadIdx.x == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
 __global__ void k_densify(const int64_t* __restrict__ p, const int32_t* __restrict__ ix, const double* __restrict__ v,
                           int64_t n, double* __restrict__ D) {
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x)
@@ -162,7 +187,8 @@ void factor_coarsest(hcamg_handle* h, DevLevel& L, const DCsr& M) {
   {
     DBuf<unsigned long long> a(1, s);
     a.zero();
-    if (n) k_asym<<<grid_for(n, 128), 128, 0, s>>>(M.ptr.p, M.idx.p, M.val.p, n, a.p);
+    if (n >= 64 && csr_is_dense_canonical(M, s)) k_asym_dense<<<kSMs * 8, dim3(32, 8), 0, s>>>(M.val.p, n, a.p);
+    else if (n) k_asym<<<grid_for(n, 128), 128, 0, s>>>(M.ptr.p, M.idx.p, M.val.p, n, a.p);
     HC_CHECK_LAUNCH();
     unsigned long long ha = read_scalar(a.p, s);
     double asym;

@@ -149,13 +149,20 @@ struct StageTimer {
   cudaStream_t s;
   bool on;
   std::chrono::steady_clock::time_point t;
-  explicit StageTimer(cudaStream_t st) : s(st), on(getenv("HCAMG_SETUP_TIMING") != nullptr), t(std::chrono::steady_clock::now()) {}
+  double f0 = 0.0;  // dense FP64 flops counted when the stage began (count_flops)
+  explicit StageTimer(cudaStream_t st) : s(st), on(getenv("HCAMG_SETUP_TIMING") != nullptr), t(std::chrono::steady_clock::now()) {
+    if (on) f0 = peek_flops();
+  }
+  static double peek_flops();
   void mark(const char* what) {
     if (!on) return;
     cudaStreamSynchronize(s);
     const auto now = std::chrono::steady_clock::now();
-    fprintf(stderr, "[hcamg setup] %-28s %9.3f s\n", what, std::chrono::duration<double>(now - t).count());
+    const double dt = std::chrono::duration<double>(now - t).count(), f = peek_flops();
+    if (f - f0 > 1e9) fprintf(stderr, "[hcamg setup] %-28s %9.3f s  %6.1f TF/s\n", what, dt, (f - f0) / dt / 1e12);
+    else fprintf(stderr, "[hcamg setup] %-28s %9.3f s\n", what, dt);
     t = now;
+    f0 = f;
   }
 };
 

@@ -189,7 +189,8 @@ namespace {
 // times instead of once per 96-column panel)
 void chol_rec(double* A, int64_t k, int64_t ld, double* piv, long long* bad, int64_t base, cudaStream_t s,
               double* Li = nullptr, int64_t ldi = 0) {
-  if (k <= kTile) {
+  static const int leaf = getenv("HCAMG_POTRF_TILE") ? std::max(32, std::min(kTile, atoi(getenv("HCAMG_POTRF_TILE")))) : 64;
+  if (k <= leaf) {
     const size_t smem = sizeof(double) * kTile * (kTile + 1);
     static bool init = false;
     if (!init) {
@@ -201,7 +202,7 @@ void chol_rec(double* A, int64_t k, int64_t ld, double* piv, long long* bad, int
     count_flops((double)k * k * k / 3.0 * (Li ? 2.0 : 1.0));
     return;
   }
-  const int64_t k1 = std::min<int64_t>(k - 1, std::max<int64_t>(kTile, (k / 2 + kTile - 1) / kTile * kTile)), k2 = k - k1;
+  const int64_t k1 = std::min<int64_t>(k - 1, std::max<int64_t>(leaf, (k / 2 + leaf - 1) / leaf * leaf)), k2 = k - k1;
   double* A21 = A + k1;
   double* A22 = A + k1 + k1 * ld;
   if (!Li) {

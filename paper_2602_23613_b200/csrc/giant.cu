@@ -977,8 +977,12 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
   DBuf<const double*> dC;
   DBuf<long long> badf(1, s);
   badf.fill_bytes(0xff);
-  DBuf<double> LinvKK(kNB * kNB, s);
-  LinvKK.zero();
+  // the inverse of every diagonal tile is kept: the forward solve of the
+  // right-hand sides below applies it as one product per block column (the
+  // recursive triangular solve inverted its 64 x 64 leaves again for each,
+  // 2,600 single-CTA launches of 77 us)
+  DBuf<double> LinvAll(T * kNB * kNB, s);
+  LinvAll.zero();
   // HCAMG_SETUP_TIMING: per-phase totals of the factorisation loop (synchronises after every phase)
   double tphase[3] = {0, 0, 0};
   auto phase = [&](int which, std::chrono::steady_clock::time_point& t0) {
@@ -990,7 +994,8 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
   };
   for (int64_t K = 0; K < T; ++K) {  // right-looking, inside the envelope; no host sync until the end
     auto t0 = std::chrono::steady_clock::now();
-    dense_cholesky_inv_async(L.tile(K, K), kNB, kNB, LinvKK.p, kNB, piv.p + K * kNB, badf.p, K * kNB, s);
+    double* LinvKK = LinvAll.p + K * kNB * kNB;
+    dense_cholesky_inv_async(L.tile(K, K), kNB, kNB, LinvKK, kNB, piv.p + K * kNB, badf.p, K * kNB, s);
     phase(0, t0);
     std::vector<int64_t> below;  // block rows I > K whose envelope reaches column K
     for (int64_t I = K + 1; I < T; ++I)
@@ -999,7 +1004,7 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
     {  // L_IK = A_IK L_KK^{-T} with the inverse the diagonal factorisation produced
       std::vector<double*> hb;
       for (int64_t I : below) hb.push_back(L.tile(I, K));
-      dblas::apply_rinv_t_batched(kNB, kNB, LinvKK.p, hb, kNB, s);
+      dblas::apply_rinv_t_batched(kNB, kNB, LinvKK, hb, kNB, s);
     }
     phase(1, t0);
     {
@@ -1084,10 +1089,14 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
   // Solve (A Z = B with B row-major n x m)  <=>  Z^T L L^T = B^T on the column-major m x n view.
   auto nbk = [&](int64_t K) { return std::min(kNB, n - K * kNB); };
   auto blk = [&](int64_t K) { return Bp.p + K * kNB * m; };
+  DBuf<double> Xs(m * kNB, s);
   for (int64_t J = 0; J < T; ++J) {  // U^T = B^T L^{-T}; columns >= active[J] of blocks <= J are zero
     const int ma = (int)active[(size_t)J];
     if (ma == 0) continue;
-    dblas::trsm(dblas::Right, dblas::T, ma, nbk(J), L.tile(J, J), kNB, blk(J), m, s);
+    {  // blk(J) := blk(J) L_JJ^{-T} with the stored inverse (its leading nbk(J) block for a partial last tile)
+      dblas::gemm(dblas::N, dblas::T, ma, nbk(J), nbk(J), 1.0, blk(J), m, LinvAll.p + J * kNB * kNB, kNB, 0.0, Xs.p, ma, s);
+      dblas::copy_block(ma, nbk(J), Xs.p, ma, blk(J), m, s);
+    }
     for (int64_t I = J + 1; I < T; ++I)
       if (L.has(I, J)) {
         dblas::gemm(dblas::N, dblas::T, ma, nbk(I), nbk(J), -1.0, blk(J), m, L.tile(I, J), kNB, 1.0, blk(I), m, s);

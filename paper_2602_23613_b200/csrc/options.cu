@@ -46,6 +46,7 @@ namespace {
 thread_local double t_flops = 0.0;
 }
 void count_flops(double f) { t_flops += f; }
+double StageTimer::peek_flops() { return t_flops; }
 double take_flops() {
   const double f = t_flops;
   t_flops = 0.0;

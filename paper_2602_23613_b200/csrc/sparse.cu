@@ -266,14 +266,18 @@ __global__ void k_dense_left_fill(const double* __restrict__ av, int64_t nrows, 
 }
 }  // namespace
 
-static bool spgemm_dense_left(const DCsr& A, const DCsr& B, DCsr& C, cudaStream_t s) {
-  const int64_t nrows = A.nrows, ka = A.ncols, m = B.ncols;
-  if (nrows < 32 || ka < 32 || A.nnz != nrows * ka || nrows >= 65535LL * 65535LL) return false;
+bool csr_is_dense_canonical(const DCsr& A, cudaStream_t s) {
+  if (A.nrows <= 0 || A.ncols <= 0 || A.nnz != A.nrows * A.ncols) return false;
   DBuf<int> bad(1, s);
   bad.zero();
-  k_dense_canonical<<<kSMs * 8, 256, 0, s>>>(A.ptr.p, A.idx.p, nrows, ka, bad.p);
+  k_dense_canonical<<<kSMs * 8, 256, 0, s>>>(A.ptr.p, A.idx.p, A.nrows, A.ncols, bad.p);
   HC_CHECK_LAUNCH();
-  if (read_scalar(bad.p, s)) return false;
+  return read_scalar(bad.p, s) == 0;
+}
+
+static bool spgemm_dense_left(const DCsr& A, const DCsr& B, DCsr& C, cudaStream_t s) {
+  const int64_t nrows = A.nrows, ka = A.ncols, m = B.ncols;
+  if (nrows < 32 || ka < 32 || nrows >= 65535LL * 65535LL || !csr_is_dense_canonical(A, s)) return false;
   DCsr Bt;
   csr_transpose(B, Bt, s);
   DBuf<int64_t> f(m, s), cpos(m + 1, s);  // the scan writes m + 1 offsets

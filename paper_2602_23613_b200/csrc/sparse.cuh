@@ -18,6 +18,9 @@ void csr_transpose(const DCsr& A, DCsr& At, cudaStream_t s);
 // C = A * B in scipy's order; structural zeros kept (dropped by the callers'
 // canonicalisation, which never changes values).  Output columns sorted.
 void spgemm(const DCsr& A, const DCsr& B, DCsr& C, cudaStream_t s);
+// Every entry stored and in canonical order (val[i * ncols + j] = A[i, j]): the
+// dense-regime coarse operator kept as CSR.
+bool csr_is_dense_canonical(const DCsr& A, cudaStream_t s);
 
 // S = canon(0.5 (M + M^T)) for square, sorted M (sparse.py:122, splitting.py:133).
 void symmetrize(const DCsr& M, DCsr& S, cudaStream_t s);

@@ -5,8 +5,12 @@ sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 import paper_2602_23613_b200 as P
 from paper_2602_23613_b200 import kuhn
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-s = kuhn.config_system(cfg)
+if cfg.startswith("2d-L"):
+    from paper_2602_23613_b200 import tri2d
+    s = tri2d.stripes_system(int(cfg[4:]))
+else:
+    s = kuhn.config_system(cfg)
 h = None
-for rep in range(3):
+for rep in range(int(os.environ.get("HCAMG_BUILDS", "3"))):
     h = None
     t = time.perf_counter(); h = P.build_hierarchy(s, "alg"); print(f"== build {rep}: {time.perf_counter() - t:.3f} s", file=sys.stderr)
