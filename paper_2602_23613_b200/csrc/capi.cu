@@ -1268,6 +1268,31 @@ int hcamg_spmv(hcamg_handle* h, const hcamg_csr* A, const double* x, double* y) 
   });
 }
 
+// Debug (not in the public header): C = A B with the library's SpGEMM (scipy
+// csr_matmat order, canonical output).  *nnz receives nnz(C); when indptr is
+// non-null and cap >= nnz(C) the product is copied out.  Tests use it to hold
+// every SpGEMM path (row kernels, dense-left) against scipy bit for bit.
+int hcamg_debug_spgemm(hcamg_handle* h, const hcamg_csr* A, const hcamg_csr* B, int64_t* nnz, int64_t* indptr,
+                       int32_t* indices, double* data, int64_t cap) {
+  return guarded(h, [&] {
+    cudaStream_t s = h->stream;
+    DCsr Ma, Mb, Mc;
+    upload_csr(A, Ma, s);
+    upload_csr(B, Mb, s);
+    spgemm(Ma, Mb, Mc, s);
+    require(nnz != nullptr, "nnz output missing");
+    *nnz = Mc.nnz;
+    if (indptr && cap >= Mc.nnz) {
+      HC_CUDA(cudaMemcpyAsync(indptr, Mc.ptr.p, 8 * (Mc.nrows + 1), cudaMemcpyDeviceToHost, s));
+      if (Mc.nnz) {
+        HC_CUDA(cudaMemcpyAsync(indices, Mc.idx.p, 4 * Mc.nnz, cudaMemcpyDeviceToHost, s));
+        HC_CUDA(cudaMemcpyAsync(data, Mc.val.p, 8 * Mc.nnz, cudaMemcpyDeviceToHost, s));
+      }
+    }
+    HC_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
 int hcamg_pcg_generic(hcamg_handle* h, const hcamg_csr* A, const double* b, const double* x0, double tol,
                       int64_t maxit, hcamg_precond_fn precond, void* ctx, double* x, double* history,
                       hcamg_report* report) {
