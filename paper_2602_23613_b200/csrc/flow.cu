@@ -159,18 +159,32 @@ __device__ __forceinline__ void flow_patch(const FlowArgs& a, const unsigned cha
   }
   // every pulled slot of the entry loaded at once (one L2 round trip); slots
   // of earlier-wave predecessors that are still pending are polled again
+  // Branch- and predicate-free: a lane's unused positions load the spare slot
+  // d[ne] (always 0.0), so all 32 loads are issued before the first result is
+  // tested.  With a load-and-test per term under `i < cnt` the compiler runs
+  // out of predicate registers and waits for the loads in groups of 2-5
+  // (SASS: ISETP on the first result between the LDGs): 3-4 L2 round trips
+  // per patch instead of one.
   const int t0 = act ? ts[lane] : 0, t1 = act ? ts[lane + 1] : 0;
   const int cnt = min(32, t1 - t0);
+  const int tl = max(nt - 1, 0);
+  const int32_t spare = (int32_t)a.ne;
   double x[32];
   unsigned pend = 0;
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    x[i] = 0.0;
-    if (i < cnt) {
-      x[i] = ld_slot(a.d + tslot[t0 + i]);
-      if (is_sentinel(x[i])) pend |= 1u << i;
-    }
+    const int32_t sl = tslot[min(t0 + i, tl)];
+    x[i] = ld_slot(a.d + (i < cnt ? sl : spare));
   }
+  // (scheduling fence: every load above is issued before any result below is tested)
+  asm volatile("" : "+d"(x[0]), "+d"(x[1]), "+d"(x[2]), "+d"(x[3]), "+d"(x[4]), "+d"(x[5]), "+d"(x[6]), "+d"(x[7]),
+                    "+d"(x[8]), "+d"(x[9]), "+d"(x[10]), "+d"(x[11]), "+d"(x[12]), "+d"(x[13]), "+d"(x[14]), "+d"(x[15]));
+  asm volatile("" : "+d"(x[16]), "+d"(x[17]), "+d"(x[18]), "+d"(x[19]), "+d"(x[20]), "+d"(x[21]), "+d"(x[22]),
+                    "+d"(x[23]), "+d"(x[24]), "+d"(x[25]), "+d"(x[26]), "+d"(x[27]), "+d"(x[28]), "+d"(x[29]),
+                    "+d"(x[30]), "+d"(x[31]));
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (is_sentinel(x[i])) pend |= 1u << i;  // (the spare slot never holds the sentinel)
   while (__any_sync(0xffffffffu, pend != 0)) {
 #pragma unroll
     for (int i = 0; i < 32; ++i)
@@ -266,25 +280,56 @@ __global__ void __launch_bounds__(kFlowThreads, 1) k_flow_leg(FlowArgs a) {
                    : "memory");
     };
     const int64_t m = a.npatch;
-    if (lane == 0 && wg < m) issue(wg, 0);
-    int64_t j = 0;
-    for (int64_t i = wg; i < m; i += nw, ++j) {
-      const int b = (int)(j & 1);
-      if (lane == 0 && i + nw < m) issue(i + nw, b ^ 1);
-      __syncwarp();
-      mbar_wait(b ? bar1 : bar0, (uint32_t)((j >> 1) & 1));
-      long long* tr = a.trace ? a.trace + 6 * i : nullptr;
-      if (tr && lane == 0) {
-        tr[0] = gclock();
-        tr[3] = wg;
+    if (a.dynamic) {
+      // Patches claimed in execution order from a ticket (a.bar[1]) when the
+      // warp has finished its previous one.  With the static round-robin a warp
+      // whose patch i is late (its predecessors straggle) cannot attend patch
+      // i + nw, seven waves on, although that patch's own predecessors are
+      // done: head-of-line blocking put 5-15 us links on the critical chain
+      // (tools/trace_flow.py: median link 1.5 us, mean 3).  A claimed patch
+      // always has its own waiting warp; the claim frontier runs nw patches
+      // ahead of the completion frontier, so the claim (ticket, offsets,
+      // record copy: ~2.5 us) is off the critical path.  The first unfinished
+      // patch is always held by a running warp: no deadlock.
+      unsigned* ticket = a.bar + 1;
+      int64_t i = wg;
+      for (uint32_t j = 0; i < m; ++j) {
+        if (lane == 0) issue(i, 0);
+        __syncwarp();
+        mbar_wait(bar0, j & 1u);
+        long long* tr = a.trace ? a.trace + 6 * i : nullptr;
+        if (tr && lane == 0) {
+          tr[0] = gclock();
+          tr[3] = wg;
+        }
+        flow_patch(a, buf0, lane, r0, kDown ? nullptr : a.x, tr);
+        __syncwarp();
+        unsigned t = 0;
+        if (lane == 0) t = atomicAdd(ticket, 1u);
+        i = nw + (int64_t)__shfl_sync(0xffffffffu, t, 0);
       }
-      flow_patch(a, buf0 + (size_t)b * a.recmax, lane, r0, kDown ? nullptr : a.x, tr);
-      __syncwarp();
+    } else {
+      if (lane == 0 && wg < m) issue(wg, 0);
+      int64_t j = 0;
+      for (int64_t i = wg; i < m; i += nw, ++j) {
+        const int b = (int)(j & 1);
+        if (lane == 0 && i + nw < m) issue(i + nw, b ^ 1);
+        __syncwarp();
+        mbar_wait(b ? bar1 : bar0, (uint32_t)((j >> 1) & 1));
+        long long* tr = a.trace ? a.trace + 6 * i : nullptr;
+        if (tr && lane == 0) {
+          tr[0] = gclock();
+          tr[3] = wg;
+        }
+        flow_patch(a, buf0 + (size_t)b * a.recmax, lane, r0, kDown ? nullptr : a.x, tr);
+        __syncwarp();
+      }
     }
   }
   gb.sync();  // every slot has been read: hand them back to the sentinel for the next leg
   const double sent = __longlong_as_double((long long)kSentinel);
   for (int64_t e = gtid; e < a.ne; e += nth) a.d[e] = sent;
+  if (gtid == 0) a.bar[1] = 0u;  // the ticket of the next leg
 }
 
 // ---- wave-parallel sweep over the same records (mode "fwave": the default for
@@ -420,6 +465,7 @@ void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s) {
   FlowArgs fa = args;
   fa.spin_ns = getenv("HCAMG_FLOW_NS") ? (unsigned)atoi(getenv("HCAMG_FLOW_NS")) : 0u;  // measurement knobs
   fa.gates = getenv("HCAMG_FLOW_GATE") ? atoi(getenv("HCAMG_FLOW_GATE")) : 1;
+  fa.dynamic = getenv("HCAMG_FLOW_DYN") ? atoi(getenv("HCAMG_FLOW_DYN")) : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)blocks);
   cfg.blockDim = dim3(kFlowThreads);

@@ -672,13 +672,14 @@ void build_flow(const DCsr& A, Smoother& sm, cudaStream_t s) {
   for (int dir = 0; dir < 2; ++dir) {
     f.recs[dir].upload(recs[(size_t)dir].data(), (int64_t)recs[(size_t)dir].size(), s);
     f.rec_off[dir].upload(offs[(size_t)dir].data(), (int64_t)offs[(size_t)dir].size(), s);
-    f.d[dir].alloc(ne, s);
+    f.d[dir].alloc(ne + 1, s);  // slot ne: a spare that always holds 0.0 (the target of unused term positions)
     flow_reset_slots(f.d[dir].p, ne, s);
+    HC_CUDA(cudaMemsetAsync(f.d[dir].p + ne, 0, sizeof(double), s));
   }
   f.dw.alloc(std::max<int64_t>(ne, 1), s);
   f.dw.zero();
   f.recmax = recmax;
-  f.bar.alloc(1, s);
+  f.bar.alloc(2, s);  // grid-barrier word, patch ticket
   f.bar.zero();
   f.ne = ne;
   HC_CUDA(cudaStreamSynchronize(s));

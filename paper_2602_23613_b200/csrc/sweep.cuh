@@ -63,9 +63,10 @@ struct FlowArgs {
   double* d;                  // slots (sentinel between legs)
   const double* r0;           // the sweep's starting residual (down: b; up: r after the Jacobi step)
   double* x;
-  unsigned* bar;
+  unsigned* bar;              // [0] grid-barrier word, [1] patch ticket (both 0 between legs)
   unsigned spin_ns;           // back-off of the slot spin (0: pure spin)
   int gates;                  // wait on the latest-wave predecessors first (1) or poll every term (0)
+  int dynamic;                // patches claimed from a ticket in execution order (1) or dealt round-robin (0)
   long long* trace;           // debug: per execution position {record ready, pulls done, stored, warp} (globaltimer)
 };
 void launch_flow_leg(bool down, const FlowArgs& args, cudaStream_t s);
