@@ -346,6 +346,9 @@ __global__ void __launch_bounds__(kFlowThreads, 1) k_flow_leg(FlowArgs a) {
 // independent loads), then kG lanes per patch parse them there; the only
 // dependent global loads are r0[u] and the term slots.
 constexpr int kFwThreads = 256;
+#ifndef FW_TERM_BATCH
+#define FW_TERM_BATCH 8
+#endif
 
 template <int kG, bool kDown>
 __global__ void __launch_bounds__(kFwThreads) k_flow_wave(FlowArgs a, int64_t i0, int64_t cnt) {
@@ -385,12 +388,13 @@ __global__ void __launch_bounds__(kFwThreads) k_flow_wave(FlowArgs a, int64_t i0
   const double xv = (!kDown && act && xp != -1) ? a.x[u] : 0.0;
   const int t0 = act ? ts[sub] : 0, t1 = act ? ts[sub + 1] : 0;
   double acc = 0.0, dpart = 0.0;
-  for (int tt = t0; tt < t1; tt += 4) {
-    double xs[4];
+  constexpr int kTB = FW_TERM_BATCH;  // term loads in flight per lane
+  for (int tt = t0; tt < t1; tt += kTB) {
+    double xs[kTB];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) xs[j] = tt + j < t1 ? __ldcg(a.d + tslot[tt + j]) : 0.0;
+    for (int j = 0; j < kTB; ++j) xs[j] = tt + j < t1 ? __ldcg(a.d + tslot[tt + j]) : 0.0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < kTB; ++j)
       if (tt + j < t1) {
         acc = fma(tval[tt + j], xs[j], acc);
         if (tt + j - t0 == xp) dpart = xs[j];
