@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "../../include/hcamg.h"
+#include "dblas.cuh"
 #include "dense.cuh"
 #include "dist.cuh"
 #include "rows_dev.cuh"
@@ -207,6 +208,7 @@ void factor_coarsest(hcamg_handle* h, DevLevel& L, const DCsr& M) {
   k_densify<<<grid_for(n, 128), 128, 0, s>>>(M.ptr.p, M.idx.p, M.val.p, n, D.p);
   HC_CHECK_LAUNCH();
   StageTimer st(s);
+  dblas::LeafCacheScope leaves;  // the factor's 64 x 64 diagonal leaves are inverted once for both steps
   int64_t bad = dense_cholesky(D.p, n, n, s);
   st.mark("  coarsest: cholesky");
   if (bad >= 0) throw Error(ENOTSPD_, "matrix is not positive definite (pivot " + std::to_string(bad) + ")", bad);

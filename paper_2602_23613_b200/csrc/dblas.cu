@@ -8,6 +8,7 @@
 // Triangular solves and inverses are recursive: halves down to 64 x 64
 // diagonal blocks, inverted explicitly by one CTA each; everything else is GEMM.
 #include <algorithm>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -286,9 +287,49 @@ void syrk_ln(int64_t n, int64_t k, double alpha, const double* A, int64_t lda, d
   gemm(N, T, n, n, k, alpha, A, lda, A, lda, beta, C, ldc, s, true);
 }
 
+namespace {
+struct LeafCache {
+  std::unordered_map<const double*, const double*> map;
+  std::vector<DBuf<double>> store;
+};
+thread_local LeafCache* t_leaf = nullptr;
+}  // namespace
+LeafCacheScope::LeafCacheScope() : prev(t_leaf) { t_leaf = new LeafCache; }
+LeafCacheScope::~LeafCacheScope() {
+  delete t_leaf;
+  t_leaf = static_cast<LeafCache*>(prev);
+}
+bool LeafCacheScope::active() { return t_leaf != nullptr; }
+
+// the d x d inverse (ld d) of the diagonal leaf at L: cached per address inside a LeafCacheScope
+static const double* leaf_inverse(int64_t d, const double* L, int64_t ldl, DBuf<double>& tmp, cudaStream_t s) {
+  if (t_leaf && d == NB0) {
+    auto it = t_leaf->map.find(L);
+    if (it != t_leaf->map.end()) return it->second;
+    t_leaf->store.emplace_back(d * d, s);
+    double* p = t_leaf->store.back().p;
+    leaf_init();
+    k_trtri_leaf<<<1, NB0, LEAF_SMEM, s>>>((int)d, nullptr, L, ldl, nullptr, p, d, 0);
+    HC_CHECK_LAUNCH();
+    count_flops((double)d * d * d / 3.0);
+    t_leaf->map[L] = p;
+    return p;
+  }
+  tmp.alloc(d * d, s);
+  trtri_lower(d, L, ldl, tmp.p, d, s);
+  return tmp.p;
+}
+
 void trtri_lower(int64_t n, const double* L, int64_t ldl, double* Li, int64_t ldi, cudaStream_t s) {
   if (n <= 0) return;
   if (n <= NB0) {
+    if (t_leaf && n == NB0) {
+      auto it = t_leaf->map.find(L);
+      if (it != t_leaf->map.end()) {
+        copy2d(n, n, it->second, n, Li, ldi, s);
+        return;
+      }
+    }
     leaf_init();
     k_trtri_leaf<<<1, NB0, LEAF_SMEM, s>>>((int)n, nullptr, L, ldl, nullptr, Li, ldi, 0);
     HC_CHECK_LAUNCH();
@@ -412,10 +453,10 @@ void trsm(Side side, Op op, int64_t m, int64_t n, const double* L, int64_t ldl, 
   if (m <= 0 || n <= 0) return;
   if (d <= NB0) {
     // leaf: X = op(Li) B (left) or B op(Li) (right) through a temporary
-    DBuf<double> Li(d * d, s), X(m * n, s);
-    trtri_lower(d, L, ldl, Li.p, d, s);
-    if (side == Left) gemm(op, N, m, n, d, 1.0, Li.p, d, B, ldb, 0.0, X.p, m, s);
-    else gemm(N, op, m, n, d, 1.0, B, ldb, Li.p, d, 0.0, X.p, m, s);
+    DBuf<double> Lt, X(m * n, s);
+    const double* Li = leaf_inverse(d, L, ldl, Lt, s);
+    if (side == Left) gemm(op, N, m, n, d, 1.0, Li, d, B, ldb, 0.0, X.p, m, s);
+    else gemm(N, op, m, n, d, 1.0, B, ldb, Li, d, 0.0, X.p, m, s);
     copy2d(m, n, X.p, m, B, ldb, s);
     return;
   }

@@ -45,6 +45,19 @@ void trsm_rlt_batched(int64_t m, int64_t nb, const std::vector<const double*>& L
                       const std::vector<double*>& B, int64_t ldb, cudaStream_t s);
 // Li = L^{-1} for a lower-triangular n x n L (Li lower, ld ldi; the strict upper part is zeroed).
 void trtri_lower(int64_t n, const double* L, int64_t ldl, double* Li, int64_t ldi, cudaStream_t s);
+// While a scope is alive (per thread), the inverse of a full 64 x 64 diagonal
+// leaf is computed once per leaf address: the recursive triangular solves of a
+// Cholesky factorisation revisit the same (final) leaves of L at every level of
+// the recursion, and the triangular inverse after it visits them once more
+// (config 2's coarsest operator: ~1,900 single-CTA leaf inversions of 77 us
+// become 410).  Only for factors that are not modified inside the scope.
+struct LeafCacheScope {
+  LeafCacheScope();
+  ~LeafCacheScope();
+  LeafCacheScope(const LeafCacheScope&) = delete;
+  void* prev;
+  static bool active();
+};
 // Batched inverses of `batch` nb x nb lower-triangular tiles.
 void copy_block(int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd, cudaStream_t s);
 // B_b := B_b Li^T for every tile of the batch (host pointer list), Li = L^{-1} given (nb x nb, ld nb)

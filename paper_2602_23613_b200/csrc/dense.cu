@@ -3,6 +3,8 @@
 #include <vector>
 
 #include "dblas.cuh"
+#include <memory>
+
 #include "dense.cuh"
 
 namespace hcamg {
@@ -241,6 +243,9 @@ void dense_cholesky_async(double* A, int64_t k, int64_t ld, double* piv, long lo
 
 int64_t dense_cholesky_raw(double* A, int64_t k, int64_t ld, double* piv, cudaStream_t s) {
   if (k == 0) return 0;
+  // leaf inverses of the panel solves cached for this factorisation (unless the caller's scope also spans its next step)
+  std::unique_ptr<dblas::LeafCacheScope> leaves;
+  if (!dblas::LeafCacheScope::active()) leaves.reset(new dblas::LeafCacheScope);
   DBuf<long long> bad(1, s);
   bad.fill_bytes(0xff);
   chol_rec(A, k, ld, piv, bad.p, 0, s);
