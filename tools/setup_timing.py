@@ -1,6 +1,7 @@
 """Setup stage times (HCAMG_SETUP_TIMING=1) for one configuration; three builds."""
 import os, sys, time
-os.environ["HCAMG_SETUP_TIMING"] = "1"
+if not os.environ.get("HCAMG_NO_STAGES"):
+    os.environ["HCAMG_SETUP_TIMING"] = "1"  # HCAMG_NO_STAGES=1: wall time per build only (stage marks synchronise)
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 import paper_2602_23613_b200 as P
 from paper_2602_23613_b200 import kuhn
