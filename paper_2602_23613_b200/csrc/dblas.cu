@@ -43,6 +43,8 @@ struct GemmArgs {
   double* const* Cb;
   int lower;     // only C entries with row >= col
   int kfromrow;  // op(A) is upper triangular in (row, k): k starts at the tile's first row
+  int kfromcol;  // op(B) is lower triangular in (k, col): k starts at the tile's first column
+  int ktorow;    // op(A) is lower triangular in (row, k): k ends with the tile's last row
 };
 
 __device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
@@ -75,8 +77,10 @@ __global__ void __launch_bounds__(THREADS) k_dgemm(GemmArgs g) {
   if (g.lower && m0 + BM <= n0) return;  // tile strictly above the diagonal
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const int wm = w & 3, wn = w >> 2;
-  const int64_t kbeg = g.kfromrow ? (m0 / BK) * BK : 0;
-  const int64_t ktiles = g.k > kbeg ? (g.k - kbeg + BK - 1) / BK : 0;
+  // (the skipped products are exact zeros of a triangular factor: the sums are unchanged bit for bit)
+  const int64_t kbeg = g.kfromrow ? (m0 / BK) * BK : g.kfromcol ? (n0 / BK) * BK : 0;
+  const int64_t kend = g.ktorow ? (g.k < m0 + BM ? g.k : m0 + BM) : g.k;
+  const int64_t ktiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
 
   // 16-byte copies along the contiguous global dimension when it is also the
   // contiguous shared dimension (op(A) = A, op(B) = B^T) and alignment allows
@@ -276,6 +280,20 @@ void gemm_batched(Op ta, Op tb, int64_t m, int64_t n, int64_t k, double alpha, c
   count_flops(2.0 * m * n * k * batch);
 }
 
+// batched product with a triangular factor: tri = 1: op(B) lower triangular (L21 Li11), tri = 2: op(A) lower
+// triangular (Li22 X); the inner range of every tile is cut to the factor's nonzeros
+static void gemm_batched_tri(int tri, int64_t m, int64_t n, int64_t k, double alpha, const double* const* A, int64_t lda,
+                             const double* const* B, int64_t ldb, double* const* C, int64_t ldc, int64_t batch,
+                             cudaStream_t s) {
+  for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+    const int64_t nb = std::min<int64_t>(65535, batch - b0);
+    GemmArgs g{m, n, k, lda, ldb, ldc, alpha, 0.0, nullptr, nullptr, nullptr, A + b0, B + b0, C + b0, 0, 0,
+               tri == 1 ? 1 : 0, tri == 2 ? 1 : 0};
+    launch(g, N, N, nb, s);
+  }
+  count_flops(1.0 * m * n * k * batch);
+}
+
 void gemm_tri_lower_tn(int64_t n, const double* Y, int64_t ldy, double* C, int64_t ldc, cudaStream_t s) {
   GemmArgs g{n, n, n, ldy, ldy, ldc, 1.0, 0.0, Y, Y, C, nullptr, nullptr, nullptr, 1, 1};
   launch(g, T, N, 1, s);
@@ -320,8 +338,116 @@ static const double* leaf_inverse(int64_t d, const double* L, int64_t ldl, DBuf<
   return tmp.p;
 }
 
+namespace {
+__global__ void k_zero_upper(double* const* P, int64_t n, int64_t ld);  // (below)
+
+// The recursion of trtri_lower on ONE large matrix of any size, level by level:
+// every diagonal leaf in one launch per leaf size, then the nodes of each depth,
+// deepest first, as two batched products per (m1, m2) shape.  Same tree
+// (split_at), same products per node: the same inverse, bit for bit, in ~40
+// launches instead of the ~2,500 dependent ones of the recursion (n = 26,236).
+struct TriNode {
+  int64_t off, m1, m2;
+};
+void tri_tree(int64_t off, int64_t n, int depth, std::vector<std::vector<TriNode>>& nodes,
+              std::vector<std::pair<int64_t, int64_t>>& leaves) {
+  if (n <= NB0) {
+    leaves.emplace_back(off, n);
+    return;
+  }
+  const int64_t m1 = split_at(n);
+  if ((int)nodes.size() <= depth) nodes.resize((size_t)depth + 1);
+  nodes[(size_t)depth].push_back(TriNode{off, m1, n - m1});
+  tri_tree(off, m1, depth + 1, nodes, leaves);
+  tri_tree(off + m1, n - m1, depth + 1, nodes, leaves);
+}
+}  // namespace
+
+static void trtri_lower_levels(int64_t n, const double* L, int64_t ldl, double* Li, int64_t ldi, cudaStream_t s) {
+  std::vector<std::vector<TriNode>> nodes;
+  std::vector<std::pair<int64_t, int64_t>> leaves;
+  tri_tree(0, n, 0, nodes, leaves);
+  {
+    DBuf<double*> one;
+    one.upload(&Li, 1, s);
+    k_zero_upper<<<dim3(kSMs * 4, 1), 256, 0, s>>>(one.p, n, ldi);
+    HC_CHECK_LAUNCH();
+    HC_CUDA(cudaStreamSynchronize(s));
+  }
+  // leaves, grouped by size
+  std::sort(leaves.begin(), leaves.end(), [](auto& a, auto& b) { return a.second != b.second ? a.second > b.second : a.first < b.first; });
+  leaf_init();
+  for (size_t i = 0; i < leaves.size();) {
+    size_t j = i;
+    while (j < leaves.size() && leaves[j].second == leaves[i].second) ++j;
+    std::vector<const double*> hl;
+    std::vector<double*> hi;
+    for (size_t t = i; t < j; ++t) {
+      hl.push_back(L + leaves[t].first * (ldl + 1));
+      hi.push_back(Li + leaves[t].first * (ldi + 1));
+    }
+    DBuf<const double*> dl;
+    DBuf<double*> di;
+    dl.upload(hl.data(), (int64_t)hl.size(), s);
+    di.upload(hi.data(), (int64_t)hi.size(), s);
+    const int64_t nb = leaves[i].second;
+    for (int64_t b0 = 0; b0 < (int64_t)hl.size(); b0 += 65535) {
+      const int64_t cnt = std::min<int64_t>(65535, (int64_t)hl.size() - b0);
+      k_trtri_leaf<<<(unsigned)cnt, NB0, LEAF_SMEM, s>>>((int)nb, dl.p + b0, nullptr, ldl, di.p + b0, nullptr, ldi, 0);
+      HC_CHECK_LAUNCH();
+    }
+    count_flops((double)nb * nb * nb / 3.0 * (double)hl.size());
+    HC_CUDA(cudaStreamSynchronize(s));  // the host pointer lists are staged
+    i = j;
+  }
+  for (int d = (int)nodes.size() - 1; d >= 0; --d) {
+    std::vector<TriNode>& nd = nodes[(size_t)d];
+    std::sort(nd.begin(), nd.end(), [](const TriNode& a, const TriNode& b) {
+      return a.m1 != b.m1 ? a.m1 > b.m1 : a.m2 != b.m2 ? a.m2 > b.m2 : a.off < b.off;
+    });
+    int64_t scratch = 0;
+    for (const TriNode& q : nd) scratch += q.m1 * q.m2;
+    DBuf<double> Tm(scratch, s);
+    int64_t used = 0;
+    for (size_t i = 0; i < nd.size();) {
+      size_t j = i;
+      while (j < nd.size() && nd[j].m1 == nd[i].m1 && nd[j].m2 == nd[i].m2) ++j;
+      const int64_t m1 = nd[i].m1, m2 = nd[i].m2;
+      std::vector<const double*> a1, b1, a2, b2;
+      std::vector<double*> c1, c2;
+      for (size_t t = i; t < j; ++t) {
+        const int64_t o = nd[t].off;
+        double* tm = Tm.p + used;
+        used += m1 * m2;
+        a1.push_back(L + (o + m1) + o * ldl);           // L21
+        b1.push_back(Li + o * (ldi + 1));               // Li11
+        c1.push_back(tm);
+        a2.push_back(Li + (o + m1) * (ldi + 1));        // Li22
+        b2.push_back(tm);
+        c2.push_back(Li + (o + m1) + o * ldi);          // Li21
+      }
+      DBuf<const double*> da1, db1, da2, db2;
+      DBuf<double*> dc1, dc2;
+      da1.upload(a1.data(), (int64_t)a1.size(), s);
+      db1.upload(b1.data(), (int64_t)b1.size(), s);
+      dc1.upload(c1.data(), (int64_t)c1.size(), s);
+      da2.upload(a2.data(), (int64_t)a2.size(), s);
+      db2.upload(b2.data(), (int64_t)b2.size(), s);
+      dc2.upload(c2.data(), (int64_t)c2.size(), s);
+      gemm_batched_tri(1, m2, m1, m1, 1.0, da1.p, ldl, db1.p, ldi, dc1.p, m2, (int64_t)a1.size(), s);   // L21 Li11
+      gemm_batched_tri(2, m2, m1, m2, -1.0, da2.p, ldi, db2.p, m2, dc2.p, ldi, (int64_t)a2.size(), s);  // -Li22 (..)
+      HC_CUDA(cudaStreamSynchronize(s));  // the pointer lists go out of scope
+      i = j;
+    }
+  }
+}
+
 void trtri_lower(int64_t n, const double* L, int64_t ldl, double* Li, int64_t ldi, cudaStream_t s) {
   if (n <= 0) return;
+  if (n >= 16 * NB0 && !getenv("HCAMG_TRTRI_RECURSIVE")) {
+    trtri_lower_levels(n, L, ldl, Li, ldi, s);
+    return;
+  }
   if (n <= NB0) {
     if (t_leaf && n == NB0) {
       auto it = t_leaf->map.find(L);
@@ -441,8 +567,8 @@ void trtri_lower_many(int64_t n, const std::vector<const double*>& L, int64_t ld
     DBuf<double*> dc1, dc2;
     dc1.upload(c1.data(), (int64_t)c1.size(), s);
     dc2.upload(c2.data(), (int64_t)c2.size(), s);
-    gemm_batched(N, N, h, h, h, 1.0, up(a1, da1), ldl, up(b1, db1), ldi, 0.0, dc1.p, h, (int64_t)a1.size(), s);
-    gemm_batched(N, N, h, h, h, -1.0, up(a2, da2), ldi, up(b2, db2), h, 0.0, dc2.p, ldi, (int64_t)a2.size(), s);
+    gemm_batched_tri(1, h, h, h, 1.0, up(a1, da1), ldl, up(b1, db1), ldi, dc1.p, h, (int64_t)a1.size(), s);
+    gemm_batched_tri(2, h, h, h, -1.0, up(a2, da2), ldi, up(b2, db2), h, dc2.p, ldi, (int64_t)a2.size(), s);
     HC_CUDA(cudaStreamSynchronize(s));  // Tm and the pointer lists go out of scope
   }
 }

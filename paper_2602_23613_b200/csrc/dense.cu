@@ -299,8 +299,8 @@ __global__ void k_sym_from_lower(const double* __restrict__ Lw, int64_t n, doubl
 // over Lbuf; the full symmetric inverse goes to Ainv.
 void dense_spd_inverse(double* Lbuf, int64_t n, double* Ainv, cudaStream_t s) {
   if (n == 0) return;
-  dblas::trtri_lower(n, Lbuf, n, Ainv, n, s);
   StageTimer st(s);
+  dblas::trtri_lower(n, Lbuf, n, Ainv, n, s);
   st.mark("    inverse: Y = L^-1");
   dblas::gemm_tri_lower_tn(n, Ainv, n, Lbuf, n, s);
   st.mark("    inverse: lower(Y^T Y)");
