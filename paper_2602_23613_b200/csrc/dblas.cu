@@ -45,6 +45,7 @@ struct GemmArgs {
   int kfromrow;  // op(A) is upper triangular in (row, k): k starts at the tile's first row
   int kfromcol;  // op(B) is lower triangular in (k, col): k starts at the tile's first column
   int ktorow;    // op(A) is lower triangular in (row, k): k ends with the tile's last row
+  int ktocol;    // op(B) is upper triangular in (k, col) (B = Li^T, Li lower): k ends with the tile's last column
 };
 
 __device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(THREADS) k_dgemm(GemmArgs g) {
   const int wm = w & 3, wn = w >> 2;
   // (the skipped products are exact zeros of a triangular factor: the sums are unchanged bit for bit)
   const int64_t kbeg = g.kfromrow ? (m0 / BK) * BK : g.kfromcol ? (n0 / BK) * BK : 0;
-  const int64_t kend = g.ktorow ? (g.k < m0 + BM ? g.k : m0 + BM) : g.k;
+  const int64_t kend = g.ktorow ? (g.k < m0 + BM ? g.k : m0 + BM) : g.ktocol ? (g.k < n0 + BN ? g.k : n0 + BN) : g.k;
   const int64_t ktiles = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
 
   // 16-byte copies along the contiguous global dimension when it is also the
@@ -292,6 +293,14 @@ static void gemm_batched_tri(int tri, int64_t m, int64_t n, int64_t k, double al
     launch(g, N, N, nb, s);
   }
   count_flops(1.0 * m * n * k * batch);
+}
+
+// C = X Li^T for a lower-triangular Li (n x n): the inner range of a tile ends with its last column
+void gemm_rinv_t(int64_t m, int64_t n, const double* X, int64_t ldx, const double* Li, int64_t ldi, double* C,
+                 int64_t ldc, cudaStream_t s) {
+  GemmArgs g{m, n, n, ldx, ldi, ldc, 1.0, 0.0, X, Li, C, nullptr, nullptr, nullptr, 0, 0, 0, 0, 1};
+  launch(g, N, T, 1, s);
+  count_flops(1.0 * m * n * n);
 }
 
 void gemm_tri_lower_tn(int64_t n, const double* Y, int64_t ldy, double* C, int64_t ldc, cudaStream_t s) {
@@ -630,7 +639,11 @@ void apply_rinv_t_batched(int64_t m, int64_t nb, const double* Li, const std::ve
   da.upload(pa.data(), batch, s);
   db.upload(pb.data(), batch, s);
   dc.upload(pc.data(), batch, s);
-  gemm_batched(N, T, m, nb, nb, 1.0, da.p, ldb, db.p, nb, 0.0, dc.p, m, batch, s);
+  {
+    GemmArgs g{m, nb, nb, ldb, nb, m, 1.0, 0.0, nullptr, nullptr, nullptr, da.p, db.p, dc.p, 0, 0, 0, 0, 1};
+    launch(g, N, T, batch, s);  // (batch <= the tiles of one block column)
+    count_flops(1.0 * m * nb * nb * batch);
+  }
   for (int64_t b = 0; b < batch; ++b) copy2d(m, nb, X.p + b * m * nb, m, hb[(size_t)b], ldb, s);
 }
 

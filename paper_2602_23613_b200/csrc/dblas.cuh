@@ -61,6 +61,9 @@ struct LeafCacheScope {
 // Batched inverses of `batch` nb x nb lower-triangular tiles.
 void copy_block(int64_t rows, int64_t cols, const double* src, int64_t lds, double* dst, int64_t ldd, cudaStream_t s);
 // B_b := B_b Li^T for every tile of the batch (host pointer list), Li = L^{-1} given (nb x nb, ld nb)
+// C = X Li^T with Li lower triangular (n x n, given explicitly): a product whose inner range per tile is cut to Li's nonzeros
+void gemm_rinv_t(int64_t m, int64_t n, const double* X, int64_t ldx, const double* Li, int64_t ldi, double* C,
+                 int64_t ldc, cudaStream_t s);
 void apply_rinv_t_batched(int64_t m, int64_t nb, const double* Li, const std::vector<double*>& hb, int64_t ldb,
                           cudaStream_t s);
 // inverses of many n x n lower-triangular matrices (host pointer lists), level-synchronous

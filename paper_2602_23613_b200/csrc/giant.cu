@@ -1094,7 +1094,7 @@ void giant_factor_solve(const DCsr& Agg, double* B, int64_t m, cudaStream_t s, F
     const int ma = (int)active[(size_t)J];
     if (ma == 0) continue;
     {  // blk(J) := blk(J) L_JJ^{-T} with the stored inverse (its leading nbk(J) block for a partial last tile)
-      dblas::gemm(dblas::N, dblas::T, ma, nbk(J), nbk(J), 1.0, blk(J), m, LinvAll.p + J * kNB * kNB, kNB, 0.0, Xs.p, ma, s);
+      dblas::gemm_rinv_t(ma, nbk(J), blk(J), m, LinvAll.p + J * kNB * kNB, kNB, Xs.p, ma, s);
       dblas::copy_block(ma, nbk(J), Xs.p, ma, blk(J), m, s);
     }
     for (int64_t I = J + 1; I < T; ++I)
